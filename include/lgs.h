@@ -1,0 +1,224 @@
+/*
+ * lgs.h -- C ABI of the B200-native LEGO-SLAM splat rasterizer (liblgs.so).
+ *
+ * Drop-in boundary for the reference renderer, proj/include/legoslam/renderer.hpp:
+ *
+ *   lego::project_gaussian   renderer.hpp:49-53  -> lgs_debug_projected
+ *   lego::render             renderer.hpp:55-56  -> lgs_render_forward
+ *   lego::render_backward    renderer.hpp:72-74  -> lgs_render_backward
+ *   lego::RenderConfig       renderer.hpp:15-22  -> lgs_render_config
+ *   lego::RenderOutput       renderer.hpp:33-45  -> lgs_images (images) + lgs_saved (backward tape)
+ *   lego::MapGradients       renderer.hpp:59-68  -> lgs_map_grads
+ *   lego::GaussianMap (SoA)  gaussian_map.hpp:57-93 -> lgs_gaussians (reference layouts) / lgs_map (device)
+ *   lego::Pose + CameraIntrinsics geometry.hpp:18-29, 43-52 -> lgs_camera
+ *
+ * The reference ships no C API (proj/src/capi.cpp is a one-line placeholder), so this
+ * header is the first C binding of these entry points; INTEGRATION.md shows the C++
+ * shim with the exact lego:: signatures and the ctypes binding.
+ *
+ * Conventions (all mirror the reference):
+ *  - Buffers are plain pointers; `memory` says whether they are host or device memory.
+ *  - Map layouts: positions [N][3]; rotations [N][4] in Eigen storage order (x,y,z,w);
+ *    log_scales [N][3]; opacity_logits [N]; sh [N][K][3] with K = (sh_degree+1)^2, K = 1 being
+ *    the reference `colors`; features [d][N] (the column-major N x d Eigen matrix).
+ *  - Images are row-major, channel-interleaved HWC (image.hpp:22-34).
+ *  - Gradients are dense over the map, zero for culled Gaussians (renderer.cpp:185-186);
+ *    rotation gradients are ordered (w,x,y,z) (renderer.hpp:61); feature gradients [d][N].
+ *  - A NULL cotangent is the reference's empty image (= zero, renderer.hpp:70-71).
+ *  - No exceptions cross the ABI: every call returns an lgs_status.  The reference's only
+ *    thrown error, std::invalid_argument on a cotangent shape mismatch (renderer.cpp:176-178),
+ *    is LGS_EINVAL.
+ *  - All work is enqueued on the context's stream; calls are asynchronous with respect to the
+ *    host unless a host buffer is involved (then the call synchronizes before returning).
+ *  - Thread safety: one lgs_ctx per host thread / GPU.  Renders are pure w.r.t. the map, so
+ *    several contexts may render the same lgs_map concurrently.
+ */
+#ifndef LGS_H_
+#define LGS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(_WIN32)
+#define LGS_API __declspec(dllexport)
+#else
+#define LGS_API __attribute__((visibility("default")))
+#endif
+
+typedef enum {
+  LGS_OK = 0,
+  LGS_EINVAL = 1, /* bad argument / shape mismatch (reference: std::invalid_argument) */
+  LGS_ECUDA = 2,  /* CUDA runtime error; see lgs_last_error() */
+  LGS_ENOMEM = 3, /* device or host allocation failed */
+  LGS_ENODEV = 4  /* no usable sm_100 device */
+} lgs_status;
+
+enum { LGS_MEM_HOST = 0, LGS_MEM_DEVICE = 1 };
+
+enum { LGS_TILE = 16, LGS_MAX_FEATURE_DIM = 32, LGS_MAX_SH_DEGREE = 3 };
+
+typedef struct lgs_ctx lgs_ctx;
+typedef struct lgs_map lgs_map;
+typedef struct lgs_saved lgs_saved;
+
+/* renderer.hpp:15-22; defaults from lgs_render_config_default(). */
+typedef struct {
+  double near_plane;        /* 0.01; must be >= 0 */
+  double dilation;          /* 0.3 px^2 */
+  double alpha_clamp;       /* 0.99 */
+  double alpha_skip;        /* 1/255 */
+  double transmittance_min; /* 1e-4 */
+  double radius_sigma;      /* 3.0 */
+} lgs_render_config;
+
+/* cam_pose is world<-camera (gaussian_map.hpp:30): q = (w,x,y,z), normalized by the callee
+ * like Pose(q, t) (geometry.hpp:23). */
+typedef struct {
+  double q[4];
+  double t[3];
+  double fx, fy, cx, cy;
+  int32_t width, height;
+} lgs_camera;
+
+/* The map in the reference's logical layouts. */
+typedef struct {
+  int64_t n;
+  int32_t feature_dim; /* d, 0..LGS_MAX_FEATURE_DIM */
+  int32_t sh_degree;   /* 0..3 */
+  const float* positions;      /* [N][3] */
+  const float* rotations;      /* [N][4] x,y,z,w */
+  const float* log_scales;     /* [N][3] */
+  const float* opacity_logits; /* [N] */
+  const float* sh;             /* [N][K][3] */
+  const float* features;       /* [d][N] */
+  int32_t memory;              /* LGS_MEM_HOST / LGS_MEM_DEVICE */
+} lgs_gaussians;
+
+/* Caller-owned output images, HWC.  Any pointer may be NULL (not written). */
+typedef struct {
+  float* rgb;   /* [H][W][3] */
+  float* depth; /* [H][W], alpha-normalized (renderer.cpp:163-165) */
+  float* feat;  /* [H][W][d] */
+  float* acc;   /* [H][W] */
+  int32_t memory;
+} lgs_images;
+
+/* Dense gradients (MapGradients, renderer.hpp:59-68).  NULL members are skipped. */
+typedef struct {
+  float* position;      /* [N][3] */
+  float* rotation;      /* [N][4] w,x,y,z */
+  float* log_scale;     /* [N][3] */
+  float* opacity_logit; /* [N] */
+  float* sh;            /* [N][K][3]; K = 1: the reference colour gradient */
+  float* feature;       /* [d][N] */
+  int32_t memory;
+  int32_t accumulate; /* 0: overwrite (reference semantics); 1: add into (multi-view batches) */
+} lgs_map_grads;
+
+/* Optional fused L1 loss: targets HWC; when given to lgs_render_forward the
+ * forward also writes the cotangents of L = mean|rgb-T| + mean|depth-T| + mean|feat-T|
+ * (sign(0) = 0) into the tape, and lgs_render_backward_l1 consumes them. */
+typedef struct {
+  const float* rgb;   /* [H][W][3] */
+  const float* depth; /* [H][W] */
+  const float* feat;  /* [H][W][d] */
+  int32_t memory;
+} lgs_l1_targets;
+
+/* Per-render counters (parity / roofline bookkeeping). */
+typedef struct {
+  int64_t visible;        /* V: Gaussians that survived culling */
+  int64_t pairs;          /* P: (tile, Gaussian) pairs */
+  int64_t tiles;          /* number of 16x16 tiles */
+  int64_t max_tile_list;  /* longest per-tile list */
+} lgs_render_stats;
+
+/* ---- library / context ---------------------------------------------------------------- */
+LGS_API const char* lgs_version(void);
+LGS_API const char* lgs_last_error(void); /* thread-local message of the last failure */
+LGS_API lgs_render_config lgs_render_config_default(void);
+
+/* One CUDA stream + device arena per context.  `stream` may be NULL (the context creates its
+ * own non-blocking stream) or an existing cudaStream_t to enqueue on (e.g. torch's). */
+LGS_API lgs_status lgs_ctx_create(int32_t device, void* stream, lgs_ctx** out);
+LGS_API lgs_status lgs_ctx_destroy(lgs_ctx* ctx);
+LGS_API lgs_status lgs_ctx_set_stream(lgs_ctx* ctx, void* stream);
+LGS_API lgs_status lgs_ctx_synchronize(lgs_ctx* ctx);
+
+/* ---- device-resident map (K9 pack: reference layouts -> device SoA) ------------------- */
+LGS_API lgs_status lgs_map_create(lgs_ctx* ctx, const lgs_gaussians* src, lgs_map** out);
+/* Re-upload attribute values (same n, d, sh_degree). */
+LGS_API lgs_status lgs_map_update(lgs_ctx* ctx, lgs_map* map, const lgs_gaussians* src);
+LGS_API lgs_status lgs_map_destroy(lgs_map* map);
+LGS_API int64_t lgs_map_size(const lgs_map* map);
+
+/* ---- forward (lego::render) ------------------------------------------------------------
+ * Renders `map` from `cam`.  `targets` may be NULL.  On success *tape receives a new
+ * lgs_saved (free with lgs_saved_destroy) unless tape == NULL. */
+LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lgs_camera* cam,
+                                      const lgs_render_config* cfg, const lgs_l1_targets* targets,
+                                      lgs_images* out, lgs_saved** tape);
+
+/* Convenience drop-in for lego::render(const GaussianMap&, ...): uploads `src` (reference
+ * layouts, host or device) into a map owned by the returned tape. */
+LGS_API lgs_status lgs_render(lgs_ctx* ctx, const lgs_gaussians* src, const lgs_camera* cam,
+                              const lgs_render_config* cfg, lgs_images* out, lgs_saved** tape);
+
+/* ---- backward (lego::render_backward) --------------------------------------------------
+ * Cotangents are HWC with the reference's shapes; `cot_memory` says where they live.  Shape
+ * checking is by construction (H, W, d come from the tape); pass cot_height/width/channels of
+ * the caller's images to reproduce the reference's std::invalid_argument (LGS_EINVAL).
+ * `pose_grad` (6 floats, host; NULL = skip) receives dL/dxi at xi = 0 for
+ * cam_pose <- compose(se3_exp(xi), cam_pose), xi = (omega, nu). */
+typedef struct {
+  const float* rgb;   /* [H][W][3] or NULL */
+  const float* depth; /* [H][W] or NULL */
+  const float* feat;  /* [H][W][d] or NULL */
+  int32_t memory;
+  int32_t rgb_shape[3];   /* H, W, C of the caller's image (0,0,0 = trust) */
+  int32_t depth_shape[3];
+  int32_t feat_shape[3];
+} lgs_cotangents;
+
+LGS_API lgs_status lgs_render_backward(lgs_ctx* ctx, const lgs_saved* tape, const lgs_cotangents* cot,
+                                       lgs_map_grads* grads, float* pose_grad);
+/* Backward of the fused L1 loss recorded by lgs_render_forward(targets != NULL). */
+LGS_API lgs_status lgs_render_backward_l1(lgs_ctx* ctx, const lgs_saved* tape, lgs_map_grads* grads,
+                                          float* pose_grad);
+/* L1 loss value of the last forward with targets (host float; synchronizes). */
+LGS_API lgs_status lgs_saved_l1_loss(lgs_ctx* ctx, const lgs_saved* tape, double* loss);
+LGS_API lgs_status lgs_saved_stats(const lgs_saved* tape, lgs_render_stats* stats);
+LGS_API lgs_status lgs_saved_destroy(lgs_saved* tape);
+
+/* ---- parity / debug exports (used by the bit-exact tests) ------------------------------ */
+/* Per map index: visible flag, u, v, depth, conic (A, B, C with q = A dx^2 + 2B dx dy + C dy^2),
+ * radius, pixel rect (x0, x1, y0, y1), opacity, colour.  Host buffers, each length N (x3/x4). */
+LGS_API lgs_status lgs_debug_projected(lgs_ctx* ctx, const lgs_saved* tape, uint8_t* visible, float* u,
+                                       float* v, float* depth, float* conic, float* radius, int32_t* bbox,
+                                       float* opacity, float* color);
+/* Sorted tile key list: keys = (tile << 32) | f32bits(depth), vals = map index, ranges
+ * [tiles][2] = [begin, end).  Host buffers; keys/vals of length lgs_render_stats.pairs. */
+LGS_API lgs_status lgs_debug_tile_keys(lgs_ctx* ctx, const lgs_saved* tape, uint64_t* keys, uint32_t* vals,
+                                       uint32_t* ranges);
+/* Per pixel: final transmittance and contributor-list end (index into the tile list,
+ * relative to the tile's begin). Host buffers of H*W. */
+LGS_API lgs_status lgs_debug_pixel_state(lgs_ctx* ctx, const lgs_saved* tape, float* final_t,
+                                         uint32_t* n_contrib);
+
+/* ---- multi-view helpers ------------------------------------------------------------------
+ * Size (floats) of one flat fp32 gradient buffer holding a whole MapGradients back to back in the
+ * order position | rotation | log_scale | opacity_logit | sh | feature.  Point an lgs_map_grads
+ * into it (accumulate = 1 across the rank's views) and all-reduce it once (NCCL, sum). */
+LGS_API int64_t lgs_grads_flat_size(int64_t n, int32_t feature_dim, int32_t sh_degree);
+
+/* Kernel launches issued by this context since creation (for bench bookkeeping). */
+LGS_API int64_t lgs_ctx_launch_count(const lgs_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LGS_H_ */

@@ -1,0 +1,125 @@
+"""ctypes binding of liblgs.so (include/lgs.h).
+
+This is the Python side of the C ABI: plain structs and pointers, no torch types.  It fails
+loudly when the library is missing -- there is no CPU fallback anywhere in the product path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "liblgs.so")
+
+LGS_OK, LGS_EINVAL, LGS_ECUDA, LGS_ENOMEM, LGS_ENODEV = range(5)
+LGS_MEM_HOST, LGS_MEM_DEVICE = 0, 1
+
+_fp = C.POINTER(C.c_float)
+
+
+class LgsRenderConfig(C.Structure):
+    _fields_ = [(n, C.c_double) for n in (
+        "near_plane", "dilation", "alpha_clamp", "alpha_skip", "transmittance_min", "radius_sigma")]
+
+
+class LgsCamera(C.Structure):
+    _fields_ = [("q", C.c_double * 4), ("t", C.c_double * 3), ("fx", C.c_double), ("fy", C.c_double),
+                ("cx", C.c_double), ("cy", C.c_double), ("width", C.c_int32), ("height", C.c_int32)]
+
+
+class LgsGaussians(C.Structure):
+    _fields_ = [("n", C.c_int64), ("feature_dim", C.c_int32), ("sh_degree", C.c_int32),
+                ("positions", C.c_void_p), ("rotations", C.c_void_p), ("log_scales", C.c_void_p),
+                ("opacity_logits", C.c_void_p), ("sh", C.c_void_p), ("features", C.c_void_p),
+                ("memory", C.c_int32)]
+
+
+class LgsImages(C.Structure):
+    _fields_ = [("rgb", C.c_void_p), ("depth", C.c_void_p), ("feat", C.c_void_p), ("acc", C.c_void_p),
+                ("memory", C.c_int32)]
+
+
+class LgsMapGrads(C.Structure):
+    _fields_ = [("position", C.c_void_p), ("rotation", C.c_void_p), ("log_scale", C.c_void_p),
+                ("opacity_logit", C.c_void_p), ("sh", C.c_void_p), ("feature", C.c_void_p),
+                ("memory", C.c_int32), ("accumulate", C.c_int32)]
+
+
+class LgsL1Targets(C.Structure):
+    _fields_ = [("rgb", C.c_void_p), ("depth", C.c_void_p), ("feat", C.c_void_p), ("memory", C.c_int32)]
+
+
+class LgsCotangents(C.Structure):
+    _fields_ = [("rgb", C.c_void_p), ("depth", C.c_void_p), ("feat", C.c_void_p), ("memory", C.c_int32),
+                ("rgb_shape", C.c_int32 * 3), ("depth_shape", C.c_int32 * 3), ("feat_shape", C.c_int32 * 3)]
+
+
+class LgsRenderStats(C.Structure):
+    _fields_ = [("visible", C.c_int64), ("pairs", C.c_int64), ("tiles", C.c_int64), ("max_tile_list", C.c_int64)]
+
+
+# (name, restype, argtypes) for every symbol declared in include/lgs.h
+SIGNATURES = [
+    ("lgs_version", C.c_char_p, []),
+    ("lgs_last_error", C.c_char_p, []),
+    ("lgs_render_config_default", LgsRenderConfig, []),
+    ("lgs_ctx_create", C.c_int, [C.c_int32, C.c_void_p, C.POINTER(C.c_void_p)]),
+    ("lgs_ctx_destroy", C.c_int, [C.c_void_p]),
+    ("lgs_ctx_set_stream", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("lgs_ctx_synchronize", C.c_int, [C.c_void_p]),
+    ("lgs_ctx_launch_count", C.c_int64, [C.c_void_p]),
+    ("lgs_map_create", C.c_int, [C.c_void_p, C.POINTER(LgsGaussians), C.POINTER(C.c_void_p)]),
+    ("lgs_map_update", C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(LgsGaussians)]),
+    ("lgs_map_destroy", C.c_int, [C.c_void_p]),
+    ("lgs_map_size", C.c_int64, [C.c_void_p]),
+    ("lgs_render_forward", C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(LgsCamera), C.POINTER(LgsRenderConfig),
+                                     C.POINTER(LgsL1Targets), C.POINTER(LgsImages), C.POINTER(C.c_void_p)]),
+    ("lgs_render", C.c_int, [C.c_void_p, C.POINTER(LgsGaussians), C.POINTER(LgsCamera), C.POINTER(LgsRenderConfig),
+                             C.POINTER(LgsImages), C.POINTER(C.c_void_p)]),
+    ("lgs_render_backward", C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(LgsCotangents), C.POINTER(LgsMapGrads), _fp]),
+    ("lgs_render_backward_l1", C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(LgsMapGrads), _fp]),
+    ("lgs_saved_l1_loss", C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_double)]),
+    ("lgs_saved_stats", C.c_int, [C.c_void_p, C.POINTER(LgsRenderStats)]),
+    ("lgs_saved_destroy", C.c_int, [C.c_void_p]),
+    ("lgs_debug_projected", C.c_int, [C.c_void_p, C.c_void_p] + [C.c_void_p] * 9),
+    ("lgs_debug_tile_keys", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("lgs_debug_pixel_state", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("lgs_grads_flat_size", C.c_int64, [C.c_int64, C.c_int32, C.c_int32]),
+]
+
+_lib = None
+
+
+class LgsError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"lgs status {status}: {msg}")
+        self.status = status
+
+
+class LgsInvalidArgument(LgsError, ValueError):
+    """LGS_EINVAL -- the reference's std::invalid_argument (renderer.cpp:176-178)."""
+
+
+def load(path: str | None = None):
+    """Load liblgs.so (raises if it is missing: the CUDA path has no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    p = path or LIB_PATH
+    if not os.path.exists(p):
+        raise RuntimeError(f"{p} is missing: build it with __graft_entry__.build() (nvcc, sm_100a)")
+    L = C.CDLL(p)
+    for name, res, args in SIGNATURES:
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = L
+    return L
+
+
+def check(status):
+    if status != LGS_OK:
+        msg = load().lgs_last_error().decode(errors="replace")
+        if status == LGS_EINVAL:
+            raise LgsInvalidArgument(status, msg)
+        raise LgsError(status, msg)

@@ -1,0 +1,108 @@
+// binning.cu -- K2 (scan + key duplication), K3 (radix sorts) and K4 (tile ranges).
+//
+// The reference sorts all projected Gaussians once by (depth, map index)
+// (proj/src/renderer.cpp:114-117) and composites each Gaussian over its pixel rect.  The tile
+// rasterizer needs, per 16x16 tile, the list of Gaussians whose pixel rect overlaps it, in that
+// same (depth, index) order.  It is built in two sorts instead of one 64-bit (tile|depth) sort:
+//   1. a stable radix sort of the N 32-bit depth keys (f32 bits; culled = 0xffffffff), values =
+//      map index in ascending order, so ties keep index order (renderer.cpp:116);
+//   2. a scan of tiles-touched in that order and the duplication of one (tile id, index) pair per
+//      overlapped tile, emitted in depth order;
+//   3. a stable radix sort of the pairs on the ceil(log2(tiles)) tile bits only.
+// The result is exactly the stable sort of the (tile << 32 | f32bits(depth)) keys (the debug
+// export rebuilds those 64-bit keys for the bit-exact test) but moves 6 B per pair per pass over
+// 1-2 passes instead of 12 B over 5-6.
+// Roofline: HBM-bound.  Bytes per pair: 6 (emit) + 2 x 12 (sort passes) + 2 (ranges).
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include "lgs_internal.cuh"
+#include "lgs_kernels.h"
+
+namespace lgs {
+
+size_t binning_temp_bytes(int64_t n, int64_t pairs_cap, int tile_bits) {
+  size_t a = 0, b = 0, c = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, a, (uint32_t*)nullptr, (uint32_t*)nullptr, (uint32_t*)nullptr,
+                                  (uint32_t*)nullptr, (int)n, 0, 32);
+  cub::DeviceScan::InclusiveSum(nullptr, b, (uint32_t*)nullptr, (uint32_t*)nullptr, (int)n);
+  cub::DeviceRadixSort::SortPairs(nullptr, c, (uint16_t*)nullptr, (uint16_t*)nullptr, (uint32_t*)nullptr,
+                                  (uint32_t*)nullptr, (int)pairs_cap, 0, tile_bits > 0 ? tile_bits : 1);
+  size_t m = a > b ? a : b;
+  return m > c ? m : c;
+}
+
+void launch_depth_sort(const ViewBufs& v, int64_t n, uint32_t* dkey_sorted, uint32_t* idx_sorted, void* temp,
+                       size_t temp_bytes, cudaStream_t s) {
+  if (n == 0) return;
+  cub::DeviceRadixSort::SortPairs(temp, temp_bytes, v.dkey, dkey_sorted, v.iota, idx_sorted, (int)n, 0, 32, s);
+}
+
+__global__ void gather_tiles_kernel(const uint32_t* __restrict__ tiles, const uint32_t* __restrict__ idx_sorted,
+                                    int64_t n, uint32_t* __restrict__ out) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < n) out[s] = tiles[idx_sorted[s]];
+}
+
+// incl[s] = sum_{s' <= s} tiles[idx_sorted[s']]; `scratch` (n u32) receives the gathered counts.
+void launch_scan_tiles(const uint32_t* tiles, const uint32_t* idx_sorted, int64_t n, uint32_t* scratch,
+                       uint32_t* incl, void* temp, size_t temp_bytes, cudaStream_t s) {
+  if (n == 0) return;
+  gather_tiles_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(tiles, idx_sorted, n, scratch);
+  cub::DeviceScan::InclusiveSum(temp, temp_bytes, scratch, incl, (int)n, s);
+}
+
+// One thread per depth-sorted Gaussian; its pairs are written contiguously at its scan offset,
+// tile ids row-major over the Gaussian's tile rect.
+__global__ void duplicate_kernel(const uint2* __restrict__ rect, const uint32_t* __restrict__ tiles,
+                                 const uint32_t* __restrict__ idx_sorted, const uint32_t* __restrict__ incl,
+                                 int64_t n, int tiles_x, uint16_t* __restrict__ key_out,
+                                 uint32_t* __restrict__ val_out) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  const uint32_t g = idx_sorted[s];
+  const uint32_t cnt = tiles[g];
+  if (cnt == 0) return;
+  uint32_t o = incl[s] - cnt;
+  const uint2 r = rect[g];
+  const int tx0 = (int)(r.x & 0xffffu) / kTile, tx1 = (int)(r.x >> 16) / kTile;
+  const int ty0 = (int)(r.y & 0xffffu) / kTile, ty1 = (int)(r.y >> 16) / kTile;
+  for (int ty = ty0; ty <= ty1; ++ty)
+    for (int tx = tx0; tx <= tx1; ++tx) {
+      key_out[o] = (uint16_t)(ty * tiles_x + tx);
+      val_out[o] = g;
+      ++o;
+    }
+}
+
+void launch_duplicate(const ViewBufs& v, const uint32_t* idx_sorted, const uint32_t* incl, int64_t n,
+                      int tiles_x, uint16_t* key_out, uint32_t* val_out, cudaStream_t s) {
+  if (n == 0) return;
+  const int threads = 256;
+  duplicate_kernel<<<(unsigned)((n + threads - 1) / threads), threads, 0, s>>>(v.rect, v.tiles, idx_sorted, incl,
+                                                                                n, tiles_x, key_out, val_out);
+}
+
+void launch_tile_sort(uint16_t* keys_in, uint16_t* keys_out, uint32_t* vals_in, uint32_t* vals_out, int64_t pairs,
+                      int tile_bits, void* temp, size_t temp_bytes, cudaStream_t s) {
+  if (pairs == 0) return;
+  cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys_in, keys_out, vals_in, vals_out, (int)pairs, 0,
+                                  tile_bits > 0 ? tile_bits : 1, s);
+}
+
+__global__ void ranges_kernel(const uint16_t* __restrict__ keys, int64_t pairs, uint2* __restrict__ ranges) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= pairs) return;
+  const uint32_t t = keys[i];
+  if (i == 0 || keys[i - 1] != t) ranges[t].x = (uint32_t)i;
+  if (i == pairs - 1 || keys[i + 1] != t) ranges[t].y = (uint32_t)(i + 1);
+}
+
+void launch_ranges(const uint16_t* keys, int64_t pairs, int ntiles, uint2* ranges, cudaStream_t s) {
+  cudaMemsetAsync(ranges, 0, sizeof(uint2) * (size_t)ntiles, s);
+  if (pairs == 0) return;
+  const int threads = 256;
+  ranges_kernel<<<(unsigned)((pairs + threads - 1) / threads), threads, 0, s>>>(keys, pairs, ranges);
+}
+
+}  // namespace lgs

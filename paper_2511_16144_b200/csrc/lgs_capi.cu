@@ -1,0 +1,816 @@
+// lgs_capi.cu -- host side of the C ABI declared in include/lgs.h.
+//
+// Orchestrates one render (K1 preprocess -> depth sort -> scan -> K2 duplicate -> tile sort ->
+// K4 ranges -> K5 blend) and one backward (K6 blend bwd -> K7 preprocess bwd) on the context's
+// stream.  Device memory comes from the stream-ordered pool (cudaMallocAsync, release threshold
+// raised so steady-state iterations reuse blocks without cudaMalloc).  No C++ exception crosses the
+// ABI; failures return lgs_status with a thread-local message (lgs_last_error).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/lgs.h"
+#include "lgs_internal.cuh"
+#include "lgs_kernels.h"
+
+using namespace lgs;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+lgs_status fail(lgs_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return st;
+}
+
+#define LGS_CUDA(call)                                                                              \
+  do {                                                                                              \
+    cudaError_t e_ = (call);                                                                        \
+    if (e_ != cudaSuccess) {                                                                        \
+      return fail(e_ == cudaErrorMemoryAllocation ? LGS_ENOMEM : LGS_ECUDA, "%s: %s (%s:%d)", #call, \
+                  cudaGetErrorString(e_), __FILE__, __LINE__);                                      \
+    }                                                                                               \
+  } while (0)
+
+#define LGS_TRY(expr)               \
+  do {                              \
+    lgs_status s_ = (expr);         \
+    if (s_ != LGS_OK) return s_;    \
+  } while (0)
+
+int pad_dim(int d) {
+  if (d == 0) return 0;
+  if (d <= 4) return 4;
+  if (d <= 8) return 8;
+  if (d <= 16) return 16;
+  return 32;
+}
+
+int bits_for(int ntiles) {
+  int b = 0;
+  while ((1 << b) < ntiles) ++b;
+  return b;
+}
+
+}  // namespace
+
+struct lgs_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  std::atomic<int> refs{1};
+  std::atomic<int64_t> launches{0};
+  uint32_t* host_u32 = nullptr;  // pinned scalar readback
+};
+
+struct lgs_map {
+  lgs_ctx* ctx = nullptr;
+  DevMap dm{};
+  float4* pos_opa = nullptr;
+  float4* rot = nullptr;
+  float4* scale = nullptr;
+  float* sh = nullptr;
+  float* feat = nullptr;
+};
+
+struct lgs_saved {
+  lgs_ctx* ctx = nullptr;
+  lgs_map* owned_map = nullptr;  // lgs_render convenience path
+  DevMap dm{};
+  DevCam cam{};
+  ViewBufs vb{};
+  uint16_t* keys = nullptr;  // sorted tile ids
+  uint32_t* vals = nullptr;  // sorted map indices
+  uint2* ranges = nullptr;
+  PixelState ps{};
+  float* cot = nullptr;     // fused L1 cotangents [H][W][4 + DP]
+  double* loss = nullptr;
+  int64_t pairs = 0;
+  int ntiles = 0;
+};
+
+namespace {
+
+void ctx_release(lgs_ctx* ctx) {
+  if (ctx->refs.fetch_sub(1) == 1) {
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    if (ctx->host_u32) cudaFreeHost(ctx->host_u32);
+    delete ctx;
+  }
+}
+
+template <typename T>
+lgs_status dalloc(lgs_ctx* ctx, T** p, size_t count) {
+  *p = nullptr;
+  if (count == 0) count = 1;
+  LGS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(p), sizeof(T) * count, ctx->stream));
+  return LGS_OK;
+}
+
+template <typename T>
+void dfree(lgs_ctx* ctx, T*& p) {
+  if (p) cudaFreeAsync(p, ctx->stream);
+  p = nullptr;
+}
+
+// Camera setup: same double formula as oracle/lgs_oracle.c camera_setup (geometry.hpp:23 Pose
+// normalizes q; geometry.cpp:15-20 inverse), then rounded to float.
+void quat_to_rot(double w, double x, double y, double z, double r[9]) {
+  const double tx = 2 * x, ty = 2 * y, tz = 2 * z;
+  const double twx = tx * w, twy = ty * w, twz = tz * w;
+  const double txx = tx * x, txy = ty * x, txz = tz * x;
+  const double tyy = ty * y, tyz = tz * y, tzz = tz * z;
+  r[0] = 1 - (tyy + tzz); r[1] = txy - twz;       r[2] = txz + twy;
+  r[3] = txy + twz;       r[4] = 1 - (txx + tzz); r[5] = tyz - twx;
+  r[6] = txz - twy;       r[7] = tyz + twx;       r[8] = 1 - (txx + tyy);
+}
+
+lgs_status make_devcam(const lgs_camera* cam, const lgs_render_config* cfg, DevCam* out) {
+  if (!cam) return fail(LGS_EINVAL, "camera is NULL");
+  if (cam->width <= 0 || cam->height <= 0 || cam->width > 65535 || cam->height > 65535)
+    return fail(LGS_EINVAL, "image size %dx%d out of range [1, 65535]", cam->width, cam->height);
+  if (!(cam->fx > 0.0) || !(cam->fy > 0.0)) return fail(LGS_EINVAL, "focal lengths must be positive");
+  if (!(cfg->near_plane >= 0.0)) return fail(LGS_EINVAL, "near_plane must be >= 0 (depth keys are f32 bits)");
+  double w = cam->q[0], x = cam->q[1], y = cam->q[2], z = cam->q[3];
+  const double nrm = std::sqrt(w * w + x * x + y * y + z * z);
+  if (!(nrm > 0.0)) return fail(LGS_EINVAL, "camera quaternion has zero norm");
+  w /= nrm; x /= nrm; y /= nrm; z /= nrm;
+  double rcw[9];
+  quat_to_rot(w, -x, -y, -z, rcw);
+  for (int i = 0; i < 9; ++i) out->rcw[i] = (float)rcw[i];
+  for (int i = 0; i < 3; ++i) {
+    const double tcw = -(rcw[i * 3 + 0] * cam->t[0] + rcw[i * 3 + 1] * cam->t[1] + rcw[i * 3 + 2] * cam->t[2]);
+    out->tcw[i] = (float)tcw;
+    out->cc[i] = (float)cam->t[i];
+  }
+  out->fx = (float)cam->fx; out->fy = (float)cam->fy;
+  out->cx = (float)cam->cx; out->cy = (float)cam->cy;
+  out->W = cam->width; out->H = cam->height;
+  out->tiles_x = (cam->width + kTile - 1) / kTile;
+  out->tiles_y = (cam->height + kTile - 1) / kTile;
+  if (out->tiles_x * out->tiles_y > 65536) return fail(LGS_EINVAL, "more than 65536 tiles");
+  out->near_plane = (float)cfg->near_plane;
+  out->dilation = (float)cfg->dilation;
+  out->radius_sigma = (float)cfg->radius_sigma;
+  out->alpha_clamp = (float)cfg->alpha_clamp;
+  out->alpha_skip = (float)cfg->alpha_skip;
+  out->t_min = (float)cfg->transmittance_min;
+  return LGS_OK;
+}
+
+lgs_status copy_in(lgs_ctx* ctx, void* dst, const void* src, size_t bytes, int memory) {
+  if (bytes == 0) return LGS_OK;
+  LGS_CUDA(cudaMemcpyAsync(dst, src, bytes, memory == LGS_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
+                           ctx->stream));
+  return LGS_OK;
+}
+
+lgs_status map_upload(lgs_ctx* ctx, lgs_map* m, const lgs_gaussians* src) {
+  const int64_t n = m->dm.n;
+  const int d = m->dm.d, K = m->dm.K;
+  // the SH block has the same layout on both sides
+  LGS_TRY(copy_in(ctx, m->sh, src->sh, sizeof(float) * (size_t)n * K * 3, src->memory));
+  const float *pos = src->positions, *rot = src->rotations, *ls = src->log_scales, *op = src->opacity_logits,
+              *ft = src->features;
+  float* stage = nullptr;
+  if (src->memory == LGS_MEM_HOST) {
+    const size_t tot = (size_t)n * (3 + 4 + 3 + 1 + d);
+    LGS_TRY(dalloc(ctx, &stage, tot));
+    float* p = stage;
+    LGS_TRY(copy_in(ctx, p, src->positions, sizeof(float) * n * 3, LGS_MEM_HOST)); pos = p; p += n * 3;
+    LGS_TRY(copy_in(ctx, p, src->rotations, sizeof(float) * n * 4, LGS_MEM_HOST)); rot = p; p += n * 4;
+    LGS_TRY(copy_in(ctx, p, src->log_scales, sizeof(float) * n * 3, LGS_MEM_HOST)); ls = p; p += n * 3;
+    LGS_TRY(copy_in(ctx, p, src->opacity_logits, sizeof(float) * n, LGS_MEM_HOST)); op = p; p += n;
+    if (d > 0) { LGS_TRY(copy_in(ctx, p, src->features, sizeof(float) * n * d, LGS_MEM_HOST)); ft = p; }
+  }
+  launch_pack_map(pos, rot, ls, op, ft, n, d, m->dm.dp, m->pos_opa, m->rot, m->scale, m->feat, ctx->stream);
+  ctx->launches++;
+  if (stage) dfree(ctx, stage);
+  LGS_CUDA(cudaGetLastError());
+  return LGS_OK;
+}
+
+lgs_status check_gaussians(const lgs_gaussians* src) {
+  if (!src) return fail(LGS_EINVAL, "gaussians is NULL");
+  if (src->n < 0 || src->n > 0x7fffffffLL) return fail(LGS_EINVAL, "n out of range");
+  if (src->feature_dim < 0 || src->feature_dim > LGS_MAX_FEATURE_DIM)
+    return fail(LGS_EINVAL, "feature_dim %d out of range [0, %d]", src->feature_dim, LGS_MAX_FEATURE_DIM);
+  if (src->sh_degree < 0 || src->sh_degree > LGS_MAX_SH_DEGREE)
+    return fail(LGS_EINVAL, "sh_degree %d out of range [0, 3]", src->sh_degree);
+  if (src->n > 0 && (!src->positions || !src->rotations || !src->log_scales || !src->opacity_logits || !src->sh ||
+                     (src->feature_dim > 0 && !src->features)))
+    return fail(LGS_EINVAL, "a map attribute pointer is NULL");
+  if (src->memory != LGS_MEM_HOST && src->memory != LGS_MEM_DEVICE) return fail(LGS_EINVAL, "bad memory kind");
+  return LGS_OK;
+}
+
+void free_map(lgs_map* m) {
+  lgs_ctx* ctx = m->ctx;
+  cudaSetDevice(ctx->device);
+  dfree(ctx, m->pos_opa);
+  dfree(ctx, m->rot);
+  dfree(ctx, m->scale);
+  dfree(ctx, m->sh);
+  dfree(ctx, m->feat);
+  delete m;
+  ctx_release(ctx);
+}
+
+void free_saved(lgs_saved* t) {
+  lgs_ctx* ctx = t->ctx;
+  cudaSetDevice(ctx->device);
+  dfree(ctx, t->vb.rec0);
+  dfree(ctx, t->vb.rec1);
+  dfree(ctx, t->vb.rect);
+  dfree(ctx, t->vb.color);
+  dfree(ctx, t->vb.tiles);
+  dfree(ctx, t->vb.dkey);
+  dfree(ctx, t->vb.iota);
+  dfree(ctx, t->keys);
+  dfree(ctx, t->vals);
+  dfree(ctx, t->ranges);
+  dfree(ctx, t->ps.final_t);
+  dfree(ctx, t->ps.n_contrib);
+  dfree(ctx, t->ps.depth);
+  dfree(ctx, t->ps.acc);
+  dfree(ctx, t->cot);
+  dfree(ctx, t->loss);
+  if (t->owned_map) free_map(t->owned_map);
+  delete t;
+  ctx_release(ctx);
+}
+
+struct DeviceImages {  // device views of caller images (staged when they are host memory)
+  float *rgb = nullptr, *depth = nullptr, *feat = nullptr, *acc = nullptr;
+  bool staged = false;
+};
+
+}  // namespace
+
+// ===========================================================================================
+extern "C" {
+
+LGS_API const char* lgs_version(void) { return "lgs 0.1.0 (sm_100a)"; }
+
+LGS_API const char* lgs_last_error(void) { return g_last_error.c_str(); }
+
+LGS_API lgs_render_config lgs_render_config_default(void) {
+  lgs_render_config c;
+  c.near_plane = 0.01;
+  c.dilation = 0.3;
+  c.alpha_clamp = 0.99;
+  c.alpha_skip = 1.0 / 255.0;
+  c.transmittance_min = 1e-4;
+  c.radius_sigma = 3.0;
+  return c;
+}
+
+LGS_API lgs_status lgs_ctx_create(int32_t device, void* stream, lgs_ctx** out) {
+  if (!out) return fail(LGS_EINVAL, "out is NULL");
+  *out = nullptr;
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) return fail(LGS_ENODEV, "no CUDA device");
+  if (device < 0 || device >= count) return fail(LGS_EINVAL, "device %d out of range", device);
+  cudaDeviceProp prop;
+  LGS_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10) return fail(LGS_ENODEV, "device %d is sm_%d%d; this build targets sm_100a", device, prop.major,
+                                    prop.minor);
+  LGS_CUDA(cudaSetDevice(device));
+  lgs_ctx* ctx = new lgs_ctx();
+  ctx->device = device;
+  if (stream) {
+    ctx->stream = (cudaStream_t)stream;
+  } else {
+    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+      delete ctx;
+      return fail(LGS_ECUDA, "cudaStreamCreate failed");
+    }
+    ctx->own_stream = true;
+  }
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  if (cudaMallocHost(&ctx->host_u32, 64) != cudaSuccess) {
+    delete ctx;
+    return fail(LGS_ENOMEM, "cudaMallocHost failed");
+  }
+  *out = ctx;
+  return LGS_OK;
+}
+
+LGS_API lgs_status lgs_ctx_destroy(lgs_ctx* ctx) {
+  if (!ctx) return LGS_OK;
+  ctx_release(ctx);
+  return LGS_OK;
+}
+
+LGS_API lgs_status lgs_ctx_set_stream(lgs_ctx* ctx, void* stream) {
+  if (!ctx) return fail(LGS_EINVAL, "ctx is NULL");
+  cudaSetDevice(ctx->device);
+  if (ctx->own_stream) {
+    cudaStreamSynchronize(ctx->stream);
+    cudaStreamDestroy(ctx->stream);
+    ctx->own_stream = false;
+  }
+  ctx->stream = (cudaStream_t)stream;
+  return LGS_OK;
+}
+
+LGS_API lgs_status lgs_ctx_synchronize(lgs_ctx* ctx) {
+  if (!ctx) return fail(LGS_EINVAL, "ctx is NULL");
+  LGS_CUDA(cudaSetDevice(ctx->device));
+  LGS_CUDA(cudaStreamSynchronize(ctx->stream));
+  return LGS_OK;
+}
+
+LGS_API int64_t lgs_ctx_launch_count(const lgs_ctx* ctx) { return ctx ? ctx->launches.load() : 0; }
+
+LGS_API lgs_status lgs_map_create(lgs_ctx* ctx, const lgs_gaussians* src, lgs_map** out) {
+  if (!ctx || !out) return fail(LGS_EINVAL, "ctx/out is NULL");
+  *out = nullptr;
+  LGS_TRY(check_gaussians(src));
+  LGS_CUDA(cudaSetDevice(ctx->device));
+  lgs_map* m = new lgs_map();
+  m->ctx = ctx;
+  ctx->refs++;
+  m->dm.n = src->n;
+  m->dm.d = src->feature_dim;
+  m->dm.dp = pad_dim(src->feature_dim);
+  m->dm.deg = src->sh_degree;
+  m->dm.K = (src->sh_degree + 1) * (src->sh_degree + 1);
+  const size_t n = (size_t)src->n;
+  lgs_status st = LGS_OK;
+  if ((st = dalloc(ctx, &m->pos_opa, n)) != LGS_OK || (st = dalloc(ctx, &m->rot, n)) != LGS_OK ||
+      (st = dalloc(ctx, &m->scale, n)) != LGS_OK || (st = dalloc(ctx, &m->sh, n * m->dm.K * 3)) != LGS_OK ||
+      (st = dalloc(ctx, &m->feat, n * (m->dm.dp > 0 ? m->dm.dp : 1))) != LGS_OK ||
+      (st = map_upload(ctx, m, src)) != LGS_OK) {
+    free_map(m);
+    return st;
+  }
+  m->dm.pos_opa = m->pos_opa;
+  m->dm.rot = m->rot;
+  m->dm.scale = m->scale;
+  m->dm.sh = m->sh;
+  m->dm.feat = m->feat;
+  if (src->memory == LGS_MEM_HOST) LGS_CUDA(cudaStreamSynchronize(ctx->stream));
+  *out = m;
+  return LGS_OK;
+}
+
+LGS_API lgs_status lgs_map_update(lgs_ctx* ctx, lgs_map* map, const lgs_gaussians* src) {
+  if (!ctx || !map) return fail(LGS_EINVAL, "ctx/map is NULL");
+  LGS_TRY(check_gaussians(src));
+  if (src->n != map->dm.n || src->feature_dim != map->dm.d || src->sh_degree != map->dm.deg)
+    return fail(LGS_EINVAL, "lgs_map_update: shape differs from the map");
+  LGS_CUDA(cudaSetDevice(ctx->device));
+  LGS_TRY(map_upload(ctx, map, src));
+  if (src->memory == LGS_MEM_HOST) LGS_CUDA(cudaStreamSynchronize(ctx->stream));
+  return LGS_OK;
+}
+
+LGS_API lgs_status lgs_map_destroy(lgs_map* map) {
+  if (map) free_map(map);
+  return LGS_OK;
+}
+
+LGS_API int64_t lgs_map_size(const lgs_map* map) { return map ? map->dm.n : -1; }
+
+LGS_API int64_t lgs_grads_flat_size(int64_t n, int32_t feature_dim, int32_t sh_degree) {
+  const int64_t K = (int64_t)(sh_degree + 1) * (sh_degree + 1);
+  return n * (3 + 4 + 3 + 1 + 3 * K + feature_dim);
+}
+
+// -------------------------------------------------------------------------------------------
+// forward
+// -------------------------------------------------------------------------------------------
+LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lgs_camera* cam,
+                                      const lgs_render_config* cfg_in, const lgs_l1_targets* targets,
+                                      lgs_images* out, lgs_saved** tape) {
+  if (!ctx || !map) return fail(LGS_EINVAL, "ctx/map is NULL");
+  if (tape) *tape = nullptr;
+  const lgs_render_config cfg = cfg_in ? *cfg_in : lgs_render_config_default();
+  DevCam dc;
+  LGS_TRY(make_devcam(cam, &cfg, &dc));
+  if (targets && (!targets->rgb || !targets->depth || (map->dm.d > 0 && !targets->feat)))
+    return fail(LGS_EINVAL, "L1 targets: rgb/depth/feat must all be given");
+  LGS_CUDA(cudaSetDevice(ctx->device));
+  cudaStream_t s = ctx->stream;
+  const int64_t n = map->dm.n;
+  const size_t npix = (size_t)dc.W * dc.H;
+  const int ntiles = dc.tiles_x * dc.tiles_y;
+  const int dp = map->dm.dp, d = map->dm.d;
+
+  lgs_saved* t = new lgs_saved();
+  t->ctx = ctx;
+  ctx->refs++;
+  t->dm = map->dm;
+  t->cam = dc;
+  t->ntiles = ntiles;
+  auto bail = [&](lgs_status st) {
+    free_saved(t);
+    return st;
+  };
+#define TRYB(expr)                      \
+  do {                                  \
+    lgs_status s2_ = (expr);            \
+    if (s2_ != LGS_OK) return bail(s2_); \
+  } while (0)
+#define CUDAB(call)                                                                                   \
+  do {                                                                                                \
+    cudaError_t e_ = (call);                                                                          \
+    if (e_ != cudaSuccess)                                                                            \
+      return bail(fail(e_ == cudaErrorMemoryAllocation ? LGS_ENOMEM : LGS_ECUDA, "%s: %s (%s:%d)", #call, \
+                       cudaGetErrorString(e_), __FILE__, __LINE__));                                  \
+  } while (0)
+
+  TRYB(dalloc(ctx, &t->vb.rec0, n));
+  TRYB(dalloc(ctx, &t->vb.rec1, n));
+  TRYB(dalloc(ctx, &t->vb.rect, n));
+  TRYB(dalloc(ctx, &t->vb.color, n));
+  TRYB(dalloc(ctx, &t->vb.tiles, n));
+  TRYB(dalloc(ctx, &t->vb.dkey, n));
+  TRYB(dalloc(ctx, &t->vb.iota, n));
+  TRYB(dalloc(ctx, &t->ranges, ntiles));
+  TRYB(dalloc(ctx, &t->ps.final_t, npix));
+  TRYB(dalloc(ctx, &t->ps.n_contrib, npix));
+  TRYB(dalloc(ctx, &t->ps.depth, npix));
+  TRYB(dalloc(ctx, &t->ps.acc, npix));
+
+  // K1
+  launch_preprocess(map->dm, dc, t->vb, s);
+  ctx->launches++;
+
+  // depth sort + scan
+  uint32_t *dkey_sorted = nullptr, *idx_sorted = nullptr, *incl = nullptr;
+  void* temp = nullptr;
+  const int tile_bits = bits_for(ntiles);
+  size_t temp_bytes = binning_temp_bytes(n, 0, tile_bits);
+  TRYB(dalloc(ctx, &dkey_sorted, n));
+  TRYB(dalloc(ctx, &idx_sorted, n));
+  TRYB(dalloc(ctx, &incl, n));
+  TRYB(dalloc(ctx, reinterpret_cast<uint8_t**>(&temp), temp_bytes));
+  launch_depth_sort(t->vb, n, dkey_sorted, idx_sorted, temp, temp_bytes, s);
+  launch_scan_tiles(t->vb.tiles, idx_sorted, n, dkey_sorted, incl, temp, temp_bytes, s);
+  ctx->launches += n > 0 ? 6 : 0;
+  int64_t P = 0;
+  if (n > 0) {
+    CUDAB(cudaMemcpyAsync(ctx->host_u32, incl + (n - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    CUDAB(cudaStreamSynchronize(s));
+    P = ctx->host_u32[0];
+  }
+  t->pairs = P;
+  uint16_t* keys_in = nullptr;
+  uint32_t* vals_in = nullptr;
+  TRYB(dalloc(ctx, &keys_in, P));
+  TRYB(dalloc(ctx, &vals_in, P));
+  TRYB(dalloc(ctx, &t->keys, P));
+  TRYB(dalloc(ctx, &t->vals, P));
+  launch_duplicate(t->vb, idx_sorted, incl, n, dc.tiles_x, keys_in, vals_in, s);
+  const size_t sort_bytes = binning_temp_bytes(0, P, tile_bits);
+  if (sort_bytes > temp_bytes) {
+    dfree(ctx, temp);
+    temp_bytes = sort_bytes;
+    TRYB(dalloc(ctx, reinterpret_cast<uint8_t**>(&temp), temp_bytes));
+  }
+  launch_tile_sort(keys_in, t->keys, vals_in, t->vals, P, tile_bits, temp, temp_bytes, s);
+  launch_ranges(t->keys, P, ntiles, t->ranges, s);
+  ctx->launches += (n > 0 ? 1 : 0) + (P > 0 ? 5 : 0);
+  dfree(ctx, keys_in);
+  dfree(ctx, vals_in);
+  dfree(ctx, temp);
+  dfree(ctx, dkey_sorted);
+  dfree(ctx, idx_sorted);
+  dfree(ctx, incl);
+
+  // K5 (+ fused L1)
+  FwdOut fo{};
+  DeviceImages di;
+  const bool host_out = out && out->memory == LGS_MEM_HOST;
+  if (out) {
+    if (host_out) {
+      if (out->rgb) TRYB(dalloc(ctx, &di.rgb, npix * 3));
+      if (out->depth) TRYB(dalloc(ctx, &di.depth, npix));
+      if (out->feat && d > 0) TRYB(dalloc(ctx, &di.feat, npix * d));
+      if (out->acc) TRYB(dalloc(ctx, &di.acc, npix));
+      di.staged = true;
+    } else {
+      di.rgb = out->rgb; di.depth = out->depth; di.feat = d > 0 ? out->feat : nullptr; di.acc = out->acc;
+    }
+  }
+  fo.rgb = di.rgb; fo.depth = di.depth; fo.feat = di.feat; fo.acc = di.acc;
+  float* tstage = nullptr;
+  if (targets) {
+    TRYB(dalloc(ctx, &t->cot, npix * (4 + dp)));
+    TRYB(dalloc(ctx, &t->loss, 1));
+    CUDAB(cudaMemsetAsync(t->loss, 0, sizeof(double), s));
+    fo.t_rgb = targets->rgb; fo.t_depth = targets->depth; fo.t_feat = targets->feat;
+    if (targets->memory == LGS_MEM_HOST) {
+      TRYB(dalloc(ctx, &tstage, npix * (4 + d)));
+      CUDAB(cudaMemcpyAsync(tstage, targets->rgb, sizeof(float) * npix * 3, cudaMemcpyHostToDevice, s));
+      CUDAB(cudaMemcpyAsync(tstage + npix * 3, targets->depth, sizeof(float) * npix, cudaMemcpyHostToDevice, s));
+      if (d > 0)
+        CUDAB(cudaMemcpyAsync(tstage + npix * 4, targets->feat, sizeof(float) * npix * d, cudaMemcpyHostToDevice, s));
+      fo.t_rgb = tstage; fo.t_depth = tstage + npix * 3; fo.t_feat = tstage + npix * 4;
+    }
+    fo.cot = t->cot;
+    fo.loss = t->loss;
+  }
+  launch_blend_fwd(map->dm, dc, t->vb, TileLists{t->vals, t->ranges}, t->ps, fo, s);
+  ctx->launches++;
+  CUDAB(cudaGetLastError());
+  if (tstage) dfree(ctx, tstage);
+  if (di.staged) {
+    if (di.rgb) CUDAB(cudaMemcpyAsync(out->rgb, di.rgb, sizeof(float) * npix * 3, cudaMemcpyDeviceToHost, s));
+    if (di.depth) CUDAB(cudaMemcpyAsync(out->depth, di.depth, sizeof(float) * npix, cudaMemcpyDeviceToHost, s));
+    if (di.feat) CUDAB(cudaMemcpyAsync(out->feat, di.feat, sizeof(float) * npix * d, cudaMemcpyDeviceToHost, s));
+    if (di.acc) CUDAB(cudaMemcpyAsync(out->acc, di.acc, sizeof(float) * npix, cudaMemcpyDeviceToHost, s));
+    dfree(ctx, di.rgb); dfree(ctx, di.depth); dfree(ctx, di.feat); dfree(ctx, di.acc);
+    CUDAB(cudaStreamSynchronize(s));
+  }
+  // the tape no longer needs the sort keys of the depth pass
+  dfree(ctx, t->vb.dkey);
+  dfree(ctx, t->vb.iota);
+  if (tape) *tape = t;
+  else free_saved(t);
+  return LGS_OK;
+#undef TRYB
+#undef CUDAB
+}
+
+LGS_API lgs_status lgs_render(lgs_ctx* ctx, const lgs_gaussians* src, const lgs_camera* cam,
+                              const lgs_render_config* cfg, lgs_images* out, lgs_saved** tape) {
+  lgs_map* m = nullptr;
+  LGS_TRY(lgs_map_create(ctx, src, &m));
+  lgs_saved* t = nullptr;
+  lgs_status st = lgs_render_forward(ctx, m, cam, cfg, nullptr, out, &t);
+  if (st != LGS_OK) {
+    free_map(m);
+    return st;
+  }
+  t->owned_map = m;
+  if (tape) *tape = t;
+  else free_saved(t);
+  return LGS_OK;
+}
+
+// -------------------------------------------------------------------------------------------
+// backward
+// -------------------------------------------------------------------------------------------
+namespace {
+
+lgs_status run_backward(lgs_ctx* ctx, const lgs_saved* t, const BwdIn& in_dev, lgs_map_grads* grads, float* pose_grad) {
+  cudaStream_t s = ctx->stream;
+  const int64_t n = t->dm.n;
+  const int d = t->dm.d, K = t->dm.K;
+  const int slots = slots_for(t->dm.dp);
+  float* gacc = nullptr;
+  LGS_TRY(dalloc(ctx, &gacc, (size_t)n * slots));
+  LGS_CUDA(cudaMemsetAsync(gacc, 0, sizeof(float) * (size_t)n * slots, s));
+  launch_blend_bwd(t->dm, t->cam, t->vb, TileLists{t->vals, t->ranges}, t->ps, in_dev, gacc, slots, s);
+  ctx->launches += 2;
+
+  GradOut go{};
+  go.accumulate = grads ? grads->accumulate : 0;
+  float* gstage = nullptr;
+  const size_t sz_pos = (size_t)n * 3, sz_rot = (size_t)n * 4, sz_ls = (size_t)n * 3, sz_op = (size_t)n,
+               sz_sh = (size_t)n * K * 3, sz_ft = (size_t)n * d;
+  const bool host = grads && grads->memory == LGS_MEM_HOST;
+  if (grads) {
+    if (host) {
+      LGS_TRY(dalloc(ctx, &gstage, sz_pos + sz_rot + sz_ls + sz_op + sz_sh + sz_ft));
+      float* p = gstage;
+      float* dst[6] = {grads->position, grads->rotation, grads->log_scale, grads->opacity_logit, grads->sh,
+                       grads->feature};
+      const size_t szs[6] = {sz_pos, sz_rot, sz_ls, sz_op, sz_sh, sz_ft};
+      float** outs[6] = {&go.position, &go.rotation, &go.log_scale, &go.opacity_logit, &go.sh, &go.feature};
+      for (int k = 0; k < 6; ++k) {
+        if (dst[k] && szs[k]) {
+          *outs[k] = p;
+          if (go.accumulate) LGS_CUDA(cudaMemcpyAsync(p, dst[k], sizeof(float) * szs[k], cudaMemcpyHostToDevice, s));
+        }
+        p += szs[k];
+      }
+    } else {
+      go.position = grads->position; go.rotation = grads->rotation; go.log_scale = grads->log_scale;
+      go.opacity_logit = grads->opacity_logit; go.sh = grads->sh; go.feature = d > 0 ? grads->feature : nullptr;
+    }
+  }
+  double* dpose = nullptr;
+  if (pose_grad) {
+    LGS_TRY(dalloc(ctx, &dpose, 6));
+    LGS_CUDA(cudaMemsetAsync(dpose, 0, sizeof(double) * 6, s));
+    go.pose = dpose;
+  }
+  launch_preprocess_bwd(t->dm, t->cam, t->vb, gacc, slots, go, s);
+  ctx->launches++;
+  LGS_CUDA(cudaGetLastError());
+  if (host) {
+    float* dst[6] = {grads->position, grads->rotation, grads->log_scale, grads->opacity_logit, grads->sh,
+                     grads->feature};
+    float* src[6] = {go.position, go.rotation, go.log_scale, go.opacity_logit, go.sh, go.feature};
+    const size_t szs[6] = {sz_pos, sz_rot, sz_ls, sz_op, sz_sh, sz_ft};
+    for (int k = 0; k < 6; ++k)
+      if (dst[k] && src[k] && szs[k])
+        LGS_CUDA(cudaMemcpyAsync(dst[k], src[k], sizeof(float) * szs[k], cudaMemcpyDeviceToHost, s));
+  }
+  double hpose[6];
+  if (pose_grad) LGS_CUDA(cudaMemcpyAsync(hpose, dpose, sizeof hpose, cudaMemcpyDeviceToHost, s));
+  dfree(ctx, gacc);
+  dfree(ctx, gstage);
+  dfree(ctx, dpose);
+  if (host || pose_grad) LGS_CUDA(cudaStreamSynchronize(s));
+  if (pose_grad)
+    for (int a = 0; a < 6; ++a) pose_grad[a] = (float)hpose[a];
+  return LGS_OK;
+}
+
+lgs_status check_shape(const int32_t shape[3], int H, int W, int C, const char* name) {
+  if (shape[0] == 0 && shape[1] == 0 && shape[2] == 0) return LGS_OK;
+  if (shape[0] != H || shape[1] != W || shape[2] != C)  // renderer.cpp:174-180
+    return fail(LGS_EINVAL, "render_backward: bad shape for %s", name);
+  return LGS_OK;
+}
+
+}  // namespace
+
+LGS_API lgs_status lgs_render_backward(lgs_ctx* ctx, const lgs_saved* tape, const lgs_cotangents* cot,
+                                       lgs_map_grads* grads, float* pose_grad) {
+  if (!ctx || !tape) return fail(LGS_EINVAL, "ctx/tape is NULL");
+  const int H = tape->cam.H, W = tape->cam.W, d = tape->dm.d;
+  const size_t npix = (size_t)W * H;
+  BwdIn in{};
+  float* stage = nullptr;
+  if (cot) {
+    if (cot->rgb) LGS_TRY(check_shape(cot->rgb_shape, H, W, 3, "grad_rgb"));
+    if (cot->depth) LGS_TRY(check_shape(cot->depth_shape, H, W, 1, "grad_depth"));
+    if (cot->feat) LGS_TRY(check_shape(cot->feat_shape, H, W, d, "grad_feat"));
+  }
+  LGS_CUDA(cudaSetDevice(ctx->device));
+  cudaStream_t s = ctx->stream;
+  if (cot) {
+    in.g_rgb = cot->rgb;
+    in.g_depth = cot->depth;
+    in.g_feat = d > 0 ? cot->feat : nullptr;
+    if (cot->memory == LGS_MEM_HOST) {
+      LGS_TRY(dalloc(ctx, &stage, npix * (4 + d)));
+      if (cot->rgb) {
+        LGS_CUDA(cudaMemcpyAsync(stage, cot->rgb, sizeof(float) * npix * 3, cudaMemcpyHostToDevice, s));
+        in.g_rgb = stage;
+      }
+      if (cot->depth) {
+        LGS_CUDA(cudaMemcpyAsync(stage + npix * 3, cot->depth, sizeof(float) * npix, cudaMemcpyHostToDevice, s));
+        in.g_depth = stage + npix * 3;
+      }
+      if (cot->feat && d > 0) {
+        LGS_CUDA(cudaMemcpyAsync(stage + npix * 4, cot->feat, sizeof(float) * npix * d, cudaMemcpyHostToDevice, s));
+        in.g_feat = stage + npix * 4;
+      }
+    }
+  }
+  lgs_status st = run_backward(ctx, tape, in, grads, pose_grad);
+  if (stage) dfree(ctx, stage);
+  return st;
+}
+
+LGS_API lgs_status lgs_render_backward_l1(lgs_ctx* ctx, const lgs_saved* tape, lgs_map_grads* grads,
+                                          float* pose_grad) {
+  if (!ctx || !tape) return fail(LGS_EINVAL, "ctx/tape is NULL");
+  if (!tape->cot) return fail(LGS_EINVAL, "tape has no fused L1 cotangents (forward without targets)");
+  LGS_CUDA(cudaSetDevice(ctx->device));
+  BwdIn in{};
+  in.g_rgb = tape->cot;
+  in.cot_stride = 4 + tape->dm.dp;
+  return run_backward(ctx, tape, in, grads, pose_grad);
+}
+
+LGS_API lgs_status lgs_saved_l1_loss(lgs_ctx* ctx, const lgs_saved* tape, double* loss) {
+  if (!ctx || !tape || !loss) return fail(LGS_EINVAL, "NULL argument");
+  if (!tape->loss) return fail(LGS_EINVAL, "tape has no fused L1 loss");
+  LGS_CUDA(cudaSetDevice(ctx->device));
+  LGS_CUDA(cudaMemcpyAsync(loss, tape->loss, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  LGS_CUDA(cudaStreamSynchronize(ctx->stream));
+  return LGS_OK;
+}
+
+LGS_API lgs_status lgs_saved_stats(const lgs_saved* tape, lgs_render_stats* st) {
+  if (!tape || !st) return fail(LGS_EINVAL, "NULL argument");
+  lgs_ctx* ctx = tape->ctx;
+  LGS_CUDA(cudaSetDevice(ctx->device));
+  std::vector<uint32_t> tiles((size_t)tape->dm.n);
+  std::vector<uint2> ranges((size_t)tape->ntiles);
+  if (tape->dm.n)
+    LGS_CUDA(cudaMemcpyAsync(tiles.data(), tape->vb.tiles, sizeof(uint32_t) * tiles.size(), cudaMemcpyDeviceToHost,
+                             ctx->stream));
+  LGS_CUDA(cudaMemcpyAsync(ranges.data(), tape->ranges, sizeof(uint2) * ranges.size(), cudaMemcpyDeviceToHost,
+                           ctx->stream));
+  LGS_CUDA(cudaStreamSynchronize(ctx->stream));
+  int64_t vis = 0, mx = 0;
+  for (uint32_t v : tiles) vis += v != 0;
+  for (const uint2& r : ranges) mx = std::max<int64_t>(mx, (int64_t)r.y - (int64_t)r.x);
+  st->visible = vis;
+  st->pairs = tape->pairs;
+  st->tiles = tape->ntiles;
+  st->max_tile_list = mx;
+  return LGS_OK;
+}
+
+LGS_API lgs_status lgs_saved_destroy(lgs_saved* tape) {
+  if (tape) free_saved(tape);
+  return LGS_OK;
+}
+
+// -------------------------------------------------------------------------------------------
+// debug / parity exports
+// -------------------------------------------------------------------------------------------
+LGS_API lgs_status lgs_debug_projected(lgs_ctx* ctx, const lgs_saved* t, uint8_t* visible, float* u, float* v,
+                                       float* depth, float* conic, float* radius, int32_t* bbox, float* opacity,
+                                       float* color) {
+  if (!ctx || !t) return fail(LGS_EINVAL, "NULL argument");
+  LGS_CUDA(cudaSetDevice(ctx->device));
+  const size_t n = (size_t)t->dm.n;
+  std::vector<float4> r0(n), r1(n), col(n);
+  std::vector<uint2> rect(n);
+  std::vector<uint32_t> tiles(n);
+  cudaStream_t s = ctx->stream;
+  if (n) {
+    LGS_CUDA(cudaMemcpyAsync(r0.data(), t->vb.rec0, sizeof(float4) * n, cudaMemcpyDeviceToHost, s));
+    LGS_CUDA(cudaMemcpyAsync(r1.data(), t->vb.rec1, sizeof(float4) * n, cudaMemcpyDeviceToHost, s));
+    LGS_CUDA(cudaMemcpyAsync(col.data(), t->vb.color, sizeof(float4) * n, cudaMemcpyDeviceToHost, s));
+    LGS_CUDA(cudaMemcpyAsync(rect.data(), t->vb.rect, sizeof(uint2) * n, cudaMemcpyDeviceToHost, s));
+    LGS_CUDA(cudaMemcpyAsync(tiles.data(), t->vb.tiles, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost, s));
+  }
+  LGS_CUDA(cudaStreamSynchronize(s));
+  for (size_t i = 0; i < n; ++i) {
+    if (visible) visible[i] = tiles[i] != 0;
+    if (u) u[i] = r0[i].x;
+    if (v) v[i] = r0[i].y;
+    if (depth) depth[i] = r0[i].z;
+    if (opacity) opacity[i] = r0[i].w;
+    if (conic) { conic[i * 3] = r1[i].x; conic[i * 3 + 1] = r1[i].y; conic[i * 3 + 2] = r1[i].z; }
+    if (radius) radius[i] = r1[i].w;
+    if (bbox) {
+      bbox[i * 4 + 0] = (int32_t)(rect[i].x & 0xffffu);
+      bbox[i * 4 + 1] = (int32_t)(rect[i].x >> 16);
+      bbox[i * 4 + 2] = (int32_t)(rect[i].y & 0xffffu);
+      bbox[i * 4 + 3] = (int32_t)(rect[i].y >> 16);
+    }
+    if (color) { color[i * 3] = col[i].x; color[i * 3 + 1] = col[i].y; color[i * 3 + 2] = col[i].z; }
+  }
+  return LGS_OK;
+}
+
+LGS_API lgs_status lgs_debug_tile_keys(lgs_ctx* ctx, const lgs_saved* t, uint64_t* keys, uint32_t* vals,
+                                       uint32_t* ranges) {
+  if (!ctx || !t) return fail(LGS_EINVAL, "NULL argument");
+  LGS_CUDA(cudaSetDevice(ctx->device));
+  cudaStream_t s = ctx->stream;
+  const size_t P = (size_t)t->pairs, n = (size_t)t->dm.n;
+  std::vector<uint16_t> k16(P);
+  std::vector<uint32_t> v32(P);
+  std::vector<float4> r0(n);
+  if (P) {
+    LGS_CUDA(cudaMemcpyAsync(k16.data(), t->keys, sizeof(uint16_t) * P, cudaMemcpyDeviceToHost, s));
+    LGS_CUDA(cudaMemcpyAsync(v32.data(), t->vals, sizeof(uint32_t) * P, cudaMemcpyDeviceToHost, s));
+  }
+  if (n) LGS_CUDA(cudaMemcpyAsync(r0.data(), t->vb.rec0, sizeof(float4) * n, cudaMemcpyDeviceToHost, s));
+  if (ranges) LGS_CUDA(cudaMemcpyAsync(ranges, t->ranges, sizeof(uint2) * t->ntiles, cudaMemcpyDeviceToHost, s));
+  LGS_CUDA(cudaStreamSynchronize(s));
+  for (size_t i = 0; i < P; ++i) {
+    uint32_t db;
+    std::memcpy(&db, &r0[v32[i]].z, 4);
+    if (keys) keys[i] = ((uint64_t)k16[i] << 32) | db;
+    if (vals) vals[i] = v32[i];
+  }
+  return LGS_OK;
+}
+
+LGS_API lgs_status lgs_debug_pixel_state(lgs_ctx* ctx, const lgs_saved* t, float* final_t, uint32_t* n_contrib) {
+  if (!ctx || !t) return fail(LGS_EINVAL, "NULL argument");
+  LGS_CUDA(cudaSetDevice(ctx->device));
+  const size_t npix = (size_t)t->cam.W * t->cam.H;
+  if (final_t)
+    LGS_CUDA(cudaMemcpyAsync(final_t, t->ps.final_t, sizeof(float) * npix, cudaMemcpyDeviceToHost, ctx->stream));
+  if (n_contrib)
+    LGS_CUDA(cudaMemcpyAsync(n_contrib, t->ps.n_contrib, sizeof(uint32_t) * npix, cudaMemcpyDeviceToHost, ctx->stream));
+  LGS_CUDA(cudaStreamSynchronize(ctx->stream));
+  return LGS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,156 @@
+// lgs_internal.cuh -- device-side types and math shared by the rasterizer kernels.
+//
+// Data layout in HBM:
+//   map (resident, lgs_map)       pos_opa float4[N] (x,y,z,opacity_logit)  rot float4[N] (x,y,z,w raw)
+//                                 scale float4[N] (log_s xyz, 0)            sh float[N][K][3]
+//                                 feat float[N][DP] (DP = d padded to 4/8/16/32, zero tail)
+//   per view (lgs_saved)          rec0 float4[N] (u, v, depth, opacity)     rec1 float4[N] (A, B, C, radius)
+//                                 rect uint2[N] (x0 | x1<<16, y0 | y1<<16)  color float4[N]
+//                                 tile list vals u32[P], ranges uint2[tiles], per-pixel T / n_contrib
+//   backward accumulator          gacc float[N][SLOTS] (one 128 B line per Gaussian for SLOTS = 32)
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace lgs {
+
+constexpr int kTile = 16;
+constexpr int kBlock = kTile * kTile;
+
+// Backward accumulator slots (per Gaussian).  Slot order is shared by blend_bwd.cu and
+// preprocess_bwd.cu.
+enum : int {
+  kSlotMuX = 0,
+  kSlotMuY = 1,
+  kSlotConA = 2,  // dL/dconic(0,0)
+  kSlotConB = 3,  // dL/dconic(0,1) == dL/dconic(1,0) (renderer.cpp:286-287)
+  kSlotConC = 4,  // dL/dconic(1,1)
+  kSlotOpac = 5,  // dL/d opacity_logit
+  kSlotZ = 6,     // dL/d depth via the depth image (renderer.cpp:265)
+  kSlotColor = 8, // 3 slots
+  kSlotFeat = 12  // DP slots
+};
+
+__host__ __device__ constexpr int slots_for(int dp) { return (kSlotFeat + dp) <= 32 ? 32 : 64; }
+
+struct DevCam {
+  float rcw[9];  // world -> camera rotation (row-major)
+  float tcw[3];
+  float cc[3];   // camera centre in world (cam_pose translation)
+  float fx, fy, cx, cy;
+  int W, H, tiles_x, tiles_y;
+  float near_plane, dilation, radius_sigma, alpha_clamp, alpha_skip, t_min;
+};
+
+struct DevMap {
+  int64_t n;
+  int d, dp, deg, K;
+  const float4* pos_opa;
+  const float4* rot;
+  const float4* scale;
+  const float* sh;
+  const float* feat;
+};
+
+// ------------------------------------------------------------------------------------------
+// Deterministic fp32 exp: range reduction + degree-7 Taylor, explicit fma, exact scaling.
+// Identical code in oracle/lgs_oracle.c (orc_expf) so preprocess is bit-exact CPU vs GPU.
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ float lgs_expf(float x) {
+  if (x != x) return x;
+  if (x > 88.72f) return __int_as_float(0x7f800000);
+  if (x < -103.97f) return 0.0f;
+  const float k = rintf(x * 1.44269504088896341f);
+  float r = fmaf(k, -0.693145751953125f, x);
+  r = fmaf(k, -1.428606765330187045e-06f, r);
+  float p = 1.98412698412698413e-04f;
+  p = fmaf(p, r, 1.38888888888888889e-03f);
+  p = fmaf(p, r, 8.33333333333333333e-03f);
+  p = fmaf(p, r, 4.16666666666666667e-02f);
+  p = fmaf(p, r, 1.66666666666666667e-01f);
+  p = fmaf(p, r, 0.5f);
+  p = fmaf(p, r, 1.0f);
+  p = fmaf(p, r, 1.0f);
+  const int ki = (int)k;
+  const int k1 = ki / 2, k2 = ki - k1;
+  const float s1 = __int_as_float((k1 + 127) << 23);
+  const float s2 = __int_as_float((k2 + 127) << 23);
+  return (p * s1) * s2;
+}
+
+// Real SH basis up to degree 3 (standard constants).  Colour convention: DC is used directly
+// (no C0, no +0.5, no clamp), so SH degree 0 is exactly the reference colour (renderer.cpp:128).
+constexpr float kShC1 = 0.4886025119029199f;
+__device__ __constant__ static const float kShC2[5] = {1.0925484305920792f, -1.0925484305920792f,
+                                                       0.31539156525252005f, -1.0925484305920792f,
+                                                       0.5462742152960396f};
+__device__ __constant__ static const float kShC3[7] = {-0.5900435899266435f, 2.890611442640554f,
+                                                       -0.4570457994644658f, 0.3731763325901154f,
+                                                       -0.4570457994644658f, 1.445305721320277f,
+                                                       -0.5900435899266435f};
+
+// basis values b[0..K) for a unit direction; same op order as oracle orc32_sh_color
+__device__ __forceinline__ void sh_basis_f32(int deg, float x, float y, float z, float b[16]) {
+  b[0] = 1.0f;
+  if (deg >= 1) {
+    b[1] = -kShC1 * y;
+    b[2] = kShC1 * z;
+    b[3] = -kShC1 * x;
+  }
+  if (deg >= 2) {
+    const float xx = x * x, yy = y * y, zz = z * z;
+    b[4] = kShC2[0] * (x * y);
+    b[5] = kShC2[1] * (y * z);
+    b[6] = kShC2[2] * ((zz + zz) - xx - yy);
+    b[7] = kShC2[3] * (x * z);
+    b[8] = kShC2[4] * (xx - yy);
+    if (deg >= 3) {
+      b[9] = kShC3[0] * y * (3.0f * xx - yy);
+      b[10] = kShC3[1] * (x * y) * z;
+      b[11] = kShC3[2] * y * (4.0f * zz - xx - yy);
+      b[12] = kShC3[3] * z * (2.0f * zz - 3.0f * xx - 3.0f * yy);
+      b[13] = kShC3[4] * x * (4.0f * zz - xx - yy);
+      b[14] = kShC3[5] * z * (xx - yy);
+      b[15] = kShC3[6] * x * (xx - 3.0f * yy);
+    }
+  }
+}
+
+// d b_k / d(x, y, z) (unnormalized direction components treated as independent)
+__device__ __forceinline__ void sh_basis_grad_f32(int deg, float x, float y, float z, float db[16][3]) {
+#pragma unroll
+  for (int k = 0; k < 16; ++k) db[k][0] = db[k][1] = db[k][2] = 0.0f;
+  if (deg < 1) return;
+  db[1][1] = -kShC1;
+  db[2][2] = kShC1;
+  db[3][0] = -kShC1;
+  if (deg < 2) return;
+  const float xx = x * x, yy = y * y, zz = z * z;
+  db[4][0] = kShC2[0] * y; db[4][1] = kShC2[0] * x;
+  db[5][1] = kShC2[1] * z; db[5][2] = kShC2[1] * y;
+  db[6][0] = -2.0f * kShC2[2] * x; db[6][1] = -2.0f * kShC2[2] * y; db[6][2] = 4.0f * kShC2[2] * z;
+  db[7][0] = kShC2[3] * z; db[7][2] = kShC2[3] * x;
+  db[8][0] = 2.0f * kShC2[4] * x; db[8][1] = -2.0f * kShC2[4] * y;
+  if (deg < 3) return;
+  db[9][0] = kShC3[0] * 6.0f * x * y; db[9][1] = kShC3[0] * (3.0f * xx - 3.0f * yy);
+  db[10][0] = kShC3[1] * y * z; db[10][1] = kShC3[1] * x * z; db[10][2] = kShC3[1] * x * y;
+  db[11][0] = kShC3[2] * (-2.0f * x * y); db[11][1] = kShC3[2] * (4.0f * zz - xx - 3.0f * yy);
+  db[11][2] = kShC3[2] * 8.0f * y * z;
+  db[12][0] = kShC3[3] * (-6.0f * x * z); db[12][1] = kShC3[3] * (-6.0f * y * z);
+  db[12][2] = kShC3[3] * (6.0f * zz - 3.0f * xx - 3.0f * yy);
+  db[13][0] = kShC3[4] * (4.0f * zz - 3.0f * xx - yy); db[13][1] = kShC3[4] * (-2.0f * x * y);
+  db[13][2] = kShC3[4] * 8.0f * x * z;
+  db[14][0] = kShC3[5] * 2.0f * x * z; db[14][1] = kShC3[5] * (-2.0f * y * z); db[14][2] = kShC3[5] * (xx - yy);
+  db[15][0] = kShC3[6] * (3.0f * xx - 3.0f * yy); db[15][1] = kShC3[6] * (-6.0f * x * y);
+}
+
+__device__ __forceinline__ float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+constexpr float kNegHalfLog2e = -0.72134752044448170368f;  // -0.5 * log2(e)
+
+}  // namespace lgs

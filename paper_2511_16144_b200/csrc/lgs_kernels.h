@@ -1,0 +1,95 @@
+// lgs_kernels.h -- launch entry points of the sm_100a kernels (host-callable).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace lgs {
+
+struct DevCam;
+struct DevMap;
+
+// Per-view projected records, indexed by map index (written by K1).
+struct ViewBufs {
+  float4* rec0;     // u, v, depth, opacity
+  float4* rec1;     // conic A, B, C (q = A dx^2 + 2B dx dy + C dy^2), radius
+  uint2* rect;      // x0 | x1 << 16, y0 | y1 << 16 (inclusive pixel rect, renderer.cpp:131-134)
+  float4* color;    // r, g, b, 0
+  uint32_t* tiles;  // tiles touched (0 = culled)
+  uint32_t* dkey;   // f32 bits of depth (0xffffffff = culled) -> depth sort key
+  uint32_t* iota;   // map index
+};
+
+// Tile lists for the blend kernels.
+struct TileLists {
+  const uint32_t* vals;  // map index per list entry, sorted by (tile, depth, index)
+  const uint2* ranges;   // [tiles] begin, end
+};
+
+// Per-pixel forward state kept for the backward pass.
+struct PixelState {
+  float* final_t;      // transmittance after the last evaluated Gaussian
+  uint32_t* n_contrib; // list position (relative to the tile begin) after the last contributor
+  float* depth;        // normalized depth (renderer.cpp:163-165), read by the backward
+  float* acc;          // accumulated alpha
+};
+
+struct FwdOut {
+  float* rgb;    // [H][W][3] or null
+  float* depth;  // [H][W] or null
+  float* feat;   // [H][W][d] or null
+  float* acc;    // [H][W] or null
+  // fused L1 (optional)
+  const float* t_rgb;
+  const float* t_depth;
+  const float* t_feat;
+  float* cot;        // [H][W][4 + d]: g_rgb(3), g_depth, g_feat(d)
+  double* loss;      // 1 double (atomic sum)
+};
+
+struct BwdIn {
+  const float* g_rgb;    // [H][W][3] or null
+  const float* g_depth;  // [H][W] or null
+  const float* g_feat;   // [H][W][d] or null
+  int cot_stride;        // 0: separate images; else interleaved [H][W][cot_stride] (fused L1 layout)
+};
+
+void launch_pack_map(const float* pos, const float* rot, const float* log_s, const float* opac,
+                     const float* feat_dn, int64_t n, int d, int dp, float4* pos_opa, float4* rot4,
+                     float4* scale4, float* feat_nd, cudaStream_t s);
+
+void launch_preprocess(const DevMap& m, const DevCam& c, const ViewBufs& v, cudaStream_t s);
+
+// Binning (binning.cu).  The pair count is read back once per view (host sync) to size the
+// pair arrays and the sort.
+size_t binning_temp_bytes(int64_t n, int64_t pairs_cap, int tile_bits);
+void launch_depth_sort(const ViewBufs& v, int64_t n, uint32_t* dkey_sorted, uint32_t* idx_sorted,
+                       void* temp, size_t temp_bytes, cudaStream_t s);
+void launch_scan_tiles(const uint32_t* tiles, const uint32_t* idx_sorted, int64_t n, uint32_t* scratch,
+                       uint32_t* incl, void* temp, size_t temp_bytes, cudaStream_t s);
+void launch_duplicate(const ViewBufs& v, const uint32_t* idx_sorted, const uint32_t* incl, int64_t n,
+                      int tiles_x, uint16_t* key_out, uint32_t* val_out, cudaStream_t s);
+void launch_tile_sort(uint16_t* keys_in, uint16_t* keys_out, uint32_t* vals_in, uint32_t* vals_out,
+                      int64_t pairs, int tile_bits, void* temp, size_t temp_bytes, cudaStream_t s);
+void launch_ranges(const uint16_t* keys, int64_t pairs, int ntiles, uint2* ranges, cudaStream_t s);
+
+void launch_blend_fwd(const DevMap& m, const DevCam& c, const ViewBufs& v, const TileLists& tl,
+                      const PixelState& ps, const FwdOut& o, cudaStream_t s);
+void launch_blend_bwd(const DevMap& m, const DevCam& c, const ViewBufs& v, const TileLists& tl,
+                      const PixelState& ps, const BwdIn& in, float* gacc, int slots, cudaStream_t s);
+
+struct GradOut {
+  float* position;      // [N][3]
+  float* rotation;      // [N][4] w,x,y,z
+  float* log_scale;     // [N][3]
+  float* opacity_logit; // [N]
+  float* sh;            // [N][K][3]
+  float* feature;       // [d][N]
+  int accumulate;
+  double* pose;         // 6 doubles (device, atomically accumulated) or null
+};
+void launch_preprocess_bwd(const DevMap& m, const DevCam& c, const ViewBufs& v, const float* gacc, int slots,
+                           const GradOut& g, cudaStream_t s);
+
+}  // namespace lgs

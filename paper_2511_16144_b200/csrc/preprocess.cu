@@ -1,0 +1,165 @@
+// preprocess.cu -- K9 map pack and K1 preprocess (EWA projection, SH colour, tile rect).
+//
+// Compiled with -fmad=false: the only fused multiply-adds are the explicit fmaf() calls, so
+// the result is bit-identical to the fp32 twin in oracle/lgs_oracle.c (orc32_project), which
+// the key-list / sort-order / range parity tests rely on.
+//
+// K1 restates project_gaussian (proj/src/renderer.cpp:53-92) in fp32:
+//   t = w2c(p) (:59), near cull (:60), Sigma3 = R diag(e^{2s}) R^T (:63-65),
+//   Sigma_c = R_cw Sigma3 R_cw^T (:66), cov2d = J Sigma_c J^T + dilation I (:68-71),
+//   lambda_max (:74-76), u, v, depth (:79-81), radius (:83), bbox cull (:86-89),
+//   conic (:90), pixel rect (:131-134), opacity sigmoid (:127), colour (:128, + SH).
+// Sigma_c is formed as M M^T with M = R_cw R diag(s) (same matrix, fewer flops).
+// Roofline: HBM-bound, 64 B map read + 92 B record write per Gaussian (+SH: 4*3*K B).
+#include "lgs_internal.cuh"
+#include "lgs_kernels.h"
+
+namespace lgs {
+
+__global__ void pack_map_kernel(const float* __restrict__ pos, const float* __restrict__ rot,
+                                const float* __restrict__ log_s, const float* __restrict__ opac,
+                                const float* __restrict__ feat_dn, int64_t n, int d, int dp,
+                                float4* __restrict__ pos_opa, float4* __restrict__ rot4,
+                                float4* __restrict__ scale4, float* __restrict__ feat_nd) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  pos_opa[i] = make_float4(pos[i * 3 + 0], pos[i * 3 + 1], pos[i * 3 + 2], opac[i]);
+  rot4[i] = make_float4(rot[i * 4 + 0], rot[i * 4 + 1], rot[i * 4 + 2], rot[i * 4 + 3]);
+  scale4[i] = make_float4(log_s[i * 3 + 0], log_s[i * 3 + 1], log_s[i * 3 + 2], 0.0f);
+  float4* fo = reinterpret_cast<float4*>(feat_nd + i * dp);
+  for (int c4 = 0; c4 < dp / 4; ++c4) {
+    float v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int c = c4 * 4 + k;
+      v[k] = c < d ? feat_dn[(int64_t)c * n + i] : 0.0f;
+    }
+    fo[c4] = make_float4(v[0], v[1], v[2], v[3]);
+  }
+}
+
+void launch_pack_map(const float* pos, const float* rot, const float* log_s, const float* opac,
+                     const float* feat_dn, int64_t n, int d, int dp, float4* pos_opa, float4* rot4,
+                     float4* scale4, float* feat_nd, cudaStream_t s) {
+  if (n == 0) return;
+  const int threads = 256;
+  const unsigned blocks = (unsigned)((n + threads - 1) / threads);
+  pack_map_kernel<<<blocks, threads, 0, s>>>(pos, rot, log_s, opac, feat_dn, n, d, dp, pos_opa, rot4, scale4,
+                                             feat_nd);
+}
+
+// ------------------------------------------------------------------------------------------
+// K1
+// ------------------------------------------------------------------------------------------
+template <int DEG>
+__global__ void __launch_bounds__(256) preprocess_kernel(DevMap m, DevCam c, ViewBufs v) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m.n) return;
+  v.iota[i] = (uint32_t)i;
+  const float4 po = m.pos_opa[i];
+  const float P0 = po.x, P1 = po.y, P2 = po.z;
+  const float* R = c.rcw;
+  const float t0 = fmaf(R[0], P0, fmaf(R[1], P1, fmaf(R[2], P2, c.tcw[0])));
+  const float t1 = fmaf(R[3], P0, fmaf(R[4], P1, fmaf(R[5], P2, c.tcw[1])));
+  const float t2 = fmaf(R[6], P0, fmaf(R[7], P1, fmaf(R[8], P2, c.tcw[2])));
+  bool ok = t2 > c.near_plane;  // renderer.cpp:60 (NaN -> culled)
+
+  const float4 q = m.rot[i];  // x, y, z, w
+  const float n2 = fmaf(q.w, q.w, fmaf(q.x, q.x, fmaf(q.y, q.y, q.z * q.z)));
+  const float nrm = sqrtf(n2);
+  const float qw = q.w / nrm, qx = q.x / nrm, qy = q.y / nrm, qz = q.z / nrm;
+  const float tx = 2.0f * qx, ty = 2.0f * qy, tz = 2.0f * qz;
+  const float twx = tx * qw, twy = ty * qw, twz = tz * qw;
+  const float txx = tx * qx, txy = ty * qx, txz = tz * qx;
+  const float tyy = ty * qy, tyz = tz * qy, tzz = tz * qz;
+  const float G[9] = {1.0f - (tyy + tzz), txy - twz,          txz + twy,
+                      txy + twz,          1.0f - (txx + tzz), tyz - twx,
+                      txz - twy,          tyz + twx,          1.0f - (txx + tyy)};
+  const float4 ls = m.scale[i];
+  const float s[3] = {lgs_expf(ls.x), lgs_expf(ls.y), lgs_expf(ls.z)};
+  float M[9];
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+      M[r * 3 + k] =
+          fmaf(R[r * 3 + 0], G[0 * 3 + k], fmaf(R[r * 3 + 1], G[1 * 3 + k], R[r * 3 + 2] * G[2 * 3 + k])) * s[k];
+  const float iz = 1.0f / t2;
+  const float xz = t0 * iz, yz = t1 * iz;
+  const float jx = c.fx * iz, jy = c.fy * iz;
+  float T0[3], T1[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    T0[k] = jx * fmaf(-xz, M[6 + k], M[0 + k]);
+    T1[k] = jy * fmaf(-yz, M[6 + k], M[3 + k]);
+  }
+  const float ca = fmaf(T0[0], T0[0], fmaf(T0[1], T0[1], T0[2] * T0[2])) + c.dilation;
+  const float cb = fmaf(T0[0], T1[0], fmaf(T0[1], T1[1], T0[2] * T1[2]));
+  const float cc = fmaf(T1[0], T1[0], fmaf(T1[1], T1[1], T1[2] * T1[2])) + c.dilation;
+  const float det = fmaf(ca, cc, -(cb * cb));
+  const float mid = 0.5f * (ca + cc);
+  const float disc = fmaxf(fmaf(mid, mid, -det), 0.0f);
+  const float lam = mid + sqrtf(disc);
+  const float radius = c.radius_sigma * sqrtf(lam);
+  const float u = fmaf(c.fx, xz, c.cx);
+  const float vv = fmaf(c.fy, yz, c.cy);
+  const float Wf = (float)c.W, Hf = (float)c.H;
+  ok = ok && (u + radius >= -0.5f && u - radius <= Wf - 0.5f && vv + radius >= -0.5f && vv - radius <= Hf - 0.5f);
+  ok = ok && det > 0.0f;
+  if (!ok) {
+    v.tiles[i] = 0;
+    v.dkey[i] = 0xffffffffu;
+    v.rec0[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    v.rec1[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    v.rect[i] = make_uint2(0u, 0u);
+    v.color[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    return;
+  }
+  const int x0 = (int)fmaxf(0.0f, floorf(u - radius));
+  const int x1 = (int)fminf(Wf - 1.0f, ceilf(u + radius));
+  const int y0 = (int)fmaxf(0.0f, floorf(vv - radius));
+  const int y1 = (int)fminf(Hf - 1.0f, ceilf(vv + radius));
+  const float opacity = 1.0f / (1.0f + lgs_expf(-po.w));
+  v.rec0[i] = make_float4(u, vv, t2, opacity);
+  v.rec1[i] = make_float4(cc / det, -cb / det, ca / det, radius);
+  v.rect[i] = make_uint2((uint32_t)x0 | ((uint32_t)x1 << 16), (uint32_t)y0 | ((uint32_t)y1 << 16));
+  v.tiles[i] = (uint32_t)((x1 / kTile - x0 / kTile + 1) * (y1 / kTile - y0 / kTile + 1));
+  v.dkey[i] = __float_as_uint(t2);
+
+  // colour (renderer.cpp:128; SH extension)
+  constexpr int K = (DEG + 1) * (DEG + 1);
+  const float* sh = m.sh + i * (K * 3);
+  float col[3];
+  if (DEG == 0) {
+    col[0] = sh[0]; col[1] = sh[1]; col[2] = sh[2];
+  } else {
+    float dx = P0 - c.cc[0], dy = P1 - c.cc[1], dz = P2 - c.cc[2];
+    const float dn = sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
+    const float idn = 1.0f / dn;
+    dx *= idn; dy *= idn; dz *= idn;
+    float b[16];
+    sh_basis_f32(DEG, dx, dy, dz, b);
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+      float acc = __ldg(sh + ch);
+#pragma unroll
+      for (int k = 1; k < K; ++k) acc = fmaf(b[k], __ldg(sh + k * 3 + ch), acc);
+      col[ch] = acc;
+    }
+  }
+  v.color[i] = make_float4(col[0], col[1], col[2], 0.0f);
+}
+
+void launch_preprocess(const DevMap& m, const DevCam& c, const ViewBufs& v, cudaStream_t s) {
+  if (m.n == 0) return;
+  const int threads = 256;
+  const unsigned blocks = (unsigned)((m.n + threads - 1) / threads);
+  switch (m.deg) {
+    case 0: preprocess_kernel<0><<<blocks, threads, 0, s>>>(m, c, v); break;
+    case 1: preprocess_kernel<1><<<blocks, threads, 0, s>>>(m, c, v); break;
+    case 2: preprocess_kernel<2><<<blocks, threads, 0, s>>>(m, c, v); break;
+    default: preprocess_kernel<3><<<blocks, threads, 0, s>>>(m, c, v); break;
+  }
+}
+
+}  // namespace lgs

@@ -1,0 +1,338 @@
+// preprocess_bwd.cu -- K7: chain per-Gaussian screen-space gradients to the map attributes.
+//
+// Restates proj/src/renderer.cpp:293-354 (+ rotation_derivatives :28-40) per Gaussian, in fp32:
+//   g_Sigma2 = -C gC C (:315); g_Sigma_c = J^T g_Sigma2 J (:316); g_J = (g_Sigma2 + g_Sigma2^T)
+//   J Sigma_c (:317-318); g_t incl. dJ/dt and the depth term (:320-327); g_p = R_cw^T g_t (:329);
+//   g_Sigma3 = R_cw^T g_Sigma_c R_cw (:331); log-scale (:335-338); rotation -> unit quaternion
+//   (:340-345) -> raw quaternion through the normalization (:347-353).
+// Extensions (parity unpinned by the reference; pinned by finite differences in tests/):
+//   - SH degree 1..3: colour -> SH coefficients and the view-direction term of the position grad;
+//   - the 6-DoF pose gradient dL/dxi for cam_pose <- compose(se3_exp(xi), cam_pose).
+// Outputs are written densely in the reference layouts (zeros for culled Gaussians unless
+// accumulating).  One thread per Gaussian; HBM-bound (gacc line + map read + grads write).
+#include "lgs_internal.cuh"
+#include "lgs_kernels.h"
+
+namespace lgs {
+
+template <int DEG, int DP, int SLOTS>
+__global__ void __launch_bounds__(256) preprocess_bwd_kernel(DevMap m, DevCam c, ViewBufs v,
+                                                               const float* __restrict__ gacc, GradOut g) {
+  constexpr int K = (DEG + 1) * (DEG + 1);
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n = m.n;
+  float pose[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  if (i < n) {
+    float o_pos[3] = {0.f, 0.f, 0.f}, o_rot[4] = {0.f, 0.f, 0.f, 0.f}, o_ls[3] = {0.f, 0.f, 0.f};
+    float o_op = 0.f;
+    float o_sh[K * 3];
+#pragma unroll
+    for (int k = 0; k < K * 3; ++k) o_sh[k] = 0.f;
+    float o_feat[DP > 0 ? DP : 1];
+#pragma unroll
+    for (int k = 0; k < (DP > 0 ? DP : 1); ++k) o_feat[k] = 0.f;
+
+    if (v.tiles[i] != 0) {
+      const float* ga = gacc + (size_t)i * SLOTS;
+      const float4 a0 = *reinterpret_cast<const float4*>(ga + 0);  // muX muY conA conB
+      const float4 a1 = *reinterpret_cast<const float4*>(ga + 4);  // conC opac z -
+      const float4 a2 = *reinterpret_cast<const float4*>(ga + 8);  // r g b -
+#pragma unroll
+      for (int q = 0; q < DP / 4; ++q) {
+        const float4 fv = *reinterpret_cast<const float4*>(ga + kSlotFeat + q * 4);
+        o_feat[q * 4 + 0] = fv.x; o_feat[q * 4 + 1] = fv.y; o_feat[q * 4 + 2] = fv.z; o_feat[q * 4 + 3] = fv.w;
+      }
+      o_op = a1.y;
+      const float4 po = m.pos_opa[i];
+      const float P[3] = {po.x, po.y, po.z};
+      float gpos[3] = {0.f, 0.f, 0.f};
+
+      // ---- colour -> SH (renderer.cpp:259-261 for K = 1) ------------------------------------
+      const float gc[3] = {a2.x, a2.y, a2.z};
+      if (DEG == 0) {
+        o_sh[0] = gc[0]; o_sh[1] = gc[1]; o_sh[2] = gc[2];
+      } else if (gc[0] != 0.f || gc[1] != 0.f || gc[2] != 0.f) {
+        const float dr[3] = {P[0] - c.cc[0], P[1] - c.cc[1], P[2] - c.cc[2]};
+        const float nr = sqrtf(dr[0] * dr[0] + dr[1] * dr[1] + dr[2] * dr[2]);
+        const float inr = 1.0f / nr;
+        const float dn[3] = {dr[0] * inr, dr[1] * inr, dr[2] * inr};
+        float b[16];
+        float db[16][3];
+        sh_basis_f32(DEG, dn[0], dn[1], dn[2], b);
+        sh_basis_grad_f32(DEG, dn[0], dn[1], dn[2], db);
+        const float* coef = m.sh + (size_t)i * K * 3;
+        float gdn[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          float s = 0.f;
+#pragma unroll
+          for (int ch = 0; ch < 3; ++ch) {
+            o_sh[k * 3 + ch] = b[k] * gc[ch];
+            s = fmaf(__ldg(coef + k * 3 + ch), gc[ch], s);
+          }
+          gdn[0] = fmaf(db[k][0], s, gdn[0]);
+          gdn[1] = fmaf(db[k][1], s, gdn[1]);
+          gdn[2] = fmaf(db[k][2], s, gdn[2]);
+        }
+        const float dd = dn[0] * gdn[0] + dn[1] * gdn[1] + dn[2] * gdn[2];
+        float gdir[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          gdir[a] = (gdn[a] - dn[a] * dd) * inr;
+          gpos[a] += gdir[a];
+        }
+        if (g.pose) {  // dir = p - c with c' = c + omega x c + nu
+          pose[0] += gdir[1] * c.cc[2] - gdir[2] * c.cc[1];
+          pose[1] += gdir[2] * c.cc[0] - gdir[0] * c.cc[2];
+          pose[2] += gdir[0] * c.cc[1] - gdir[1] * c.cc[0];
+          pose[3] -= gdir[0];
+          pose[4] -= gdir[1];
+          pose[5] -= gdir[2];
+        }
+      }
+
+      // ---- screen-space -> 3D (renderer.cpp:297-354) ----------------------------------------
+      const float gmu0 = a0.x, gmu1 = a0.y, gA = a0.z, gB = a0.w, gC = a1.x, gz = a1.z;
+      if (gmu0 != 0.f || gmu1 != 0.f || gA != 0.f || gB != 0.f || gC != 0.f || gz != 0.f) {
+        const float* R = c.rcw;
+        float t[3];
+#pragma unroll
+        for (int r = 0; r < 3; ++r) t[r] = R[r * 3 + 0] * P[0] + R[r * 3 + 1] * P[1] + R[r * 3 + 2] * P[2] + c.tcw[r];
+        const float z = t[2];
+        const float4 qr = m.rot[i];  // x,y,z,w
+        const float qv[4] = {qr.w, qr.x, qr.y, qr.z};
+        const float norm = sqrtf(qv[0] * qv[0] + qv[1] * qv[1] + qv[2] * qv[2] + qv[3] * qv[3]);
+        const float inorm = 1.0f / norm;
+        const float qh[4] = {qv[0] * inorm, qv[1] * inorm, qv[2] * inorm, qv[3] * inorm};
+        const float w = qh[0], x = qh[1], y = qh[2], zq = qh[3];
+        float W[9];  // R_g (rotation of the Gaussian)
+        {
+          const float tx = 2 * x, ty = 2 * y, tz = 2 * zq;
+          const float twx = tx * w, twy = ty * w, twz = tz * w, txx = tx * x, txy = ty * x, txz = tz * x;
+          const float tyy = ty * y, tyz = tz * y, tzz = tz * zq;
+          W[0] = 1 - (tyy + tzz); W[1] = txy - twz;       W[2] = txz + twy;
+          W[3] = txy + twz;       W[4] = 1 - (txx + tzz); W[5] = tyz - twx;
+          W[6] = txz - twy;       W[7] = tyz + twx;       W[8] = 1 - (txx + tyy);
+        }
+        const float4 ls = m.scale[i];
+        const float s2[3] = {__expf(2.f * ls.x), __expf(2.f * ls.y), __expf(2.f * ls.z)};
+        // Sigma3 = W S^2 W^T, Sigma_c = R Sigma3 R^T
+        float S3[9], RS[9], Sc[9];
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+#pragma unroll
+          for (int cc = 0; cc < 3; ++cc)
+            S3[r * 3 + cc] = W[r * 3 + 0] * s2[0] * W[cc * 3 + 0] + W[r * 3 + 1] * s2[1] * W[cc * 3 + 1] +
+                             W[r * 3 + 2] * s2[2] * W[cc * 3 + 2];
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+#pragma unroll
+          for (int cc = 0; cc < 3; ++cc)
+            RS[r * 3 + cc] = R[r * 3 + 0] * S3[0 * 3 + cc] + R[r * 3 + 1] * S3[1 * 3 + cc] + R[r * 3 + 2] * S3[2 * 3 + cc];
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+#pragma unroll
+          for (int cc = 0; cc < 3; ++cc)
+            Sc[r * 3 + cc] = RS[r * 3 + 0] * R[cc * 3 + 0] + RS[r * 3 + 1] * R[cc * 3 + 1] + RS[r * 3 + 2] * R[cc * 3 + 2];
+        const float iz = 1.0f / z;
+        const float J[6] = {c.fx * iz, 0.f, -c.fx * t[0] * iz * iz, 0.f, c.fy * iz, -c.fy * t[1] * iz * iz};
+
+        // g_Sigma2 = -C gC C, C = conic (symmetric), gC = [[gA, gB], [gB, gC]]
+        const float4 r1 = v.rec1[i];
+        const float C0 = r1.x, C1 = r1.y, C3 = r1.z;
+        const float cg00 = C0 * gA + C1 * gB, cg01 = C0 * gB + C1 * gC;
+        const float cg10 = C1 * gA + C3 * gB, cg11 = C1 * gB + C3 * gC;
+        const float gs[4] = {-(cg00 * C0 + cg01 * C1), -(cg00 * C1 + cg01 * C3), -(cg10 * C0 + cg11 * C1),
+                             -(cg10 * C1 + cg11 * C3)};
+        // g_Sigma_c = J^T gs J
+        float gSc[9];
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+#pragma unroll
+          for (int cc = 0; cc < 3; ++cc)
+            gSc[r * 3 + cc] = J[0 * 3 + r] * (gs[0] * J[0 * 3 + cc] + gs[1] * J[1 * 3 + cc]) +
+                              J[1 * 3 + r] * (gs[2] * J[0 * 3 + cc] + gs[3] * J[1 * 3 + cc]);
+        // g_J = (gs + gs^T) J Sigma_c
+        const float sy[4] = {2.f * gs[0], gs[1] + gs[2], gs[2] + gs[1], 2.f * gs[3]};
+        float JS[6], gJ[6];
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+          for (int cc = 0; cc < 3; ++cc)
+            JS[r * 3 + cc] = J[r * 3 + 0] * Sc[0 * 3 + cc] + J[r * 3 + 1] * Sc[1 * 3 + cc] + J[r * 3 + 2] * Sc[2 * 3 + cc];
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+          for (int cc = 0; cc < 3; ++cc) gJ[r * 3 + cc] = sy[r * 2 + 0] * JS[0 * 3 + cc] + sy[r * 2 + 1] * JS[1 * 3 + cc];
+        // g_t (renderer.cpp:320-327)
+        float gt[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) gt[a] = J[0 * 3 + a] * gmu0 + J[1 * 3 + a] * gmu1;
+        const float iz2 = iz * iz, iz3 = iz2 * iz;
+        gt[0] += gJ[2] * (-c.fx * iz2);
+        gt[1] += gJ[5] * (-c.fy * iz2);
+        gt[2] += gJ[0] * (-c.fx * iz2) + gJ[2] * (2.f * c.fx * t[0] * iz3) + gJ[4] * (-c.fy * iz2) +
+                 gJ[5] * (2.f * c.fy * t[1] * iz3);
+        gt[2] += gz;
+        // g_p = R^T g_t (renderer.cpp:329)
+        float gw[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          gw[a] = R[0 * 3 + a] * gt[0] + R[1 * 3 + a] * gt[1] + R[2 * 3 + a] * gt[2];
+          gpos[a] += gw[a];
+        }
+        // G3 = R^T gSc R (symmetric)
+        float tmp[9], G3[9];
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+#pragma unroll
+          for (int cc = 0; cc < 3; ++cc)
+            tmp[r * 3 + cc] = R[0 * 3 + r] * gSc[0 * 3 + cc] + R[1 * 3 + r] * gSc[1 * 3 + cc] + R[2 * 3 + r] * gSc[2 * 3 + cc];
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+#pragma unroll
+          for (int cc = 0; cc < 3; ++cc)
+            G3[r * 3 + cc] = tmp[r * 3 + 0] * R[0 * 3 + cc] + tmp[r * 3 + 1] * R[1 * 3 + cc] + tmp[r * 3 + 2] * R[2 * 3 + cc];
+        // Y = G3 W; g_logs_a = (W^T G3 W)_aa 2 s2_a; g_rot = (G3 + G3^T) W S^2
+        float Y[9];
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+#pragma unroll
+          for (int cc = 0; cc < 3; ++cc)
+            Y[r * 3 + cc] = G3[r * 3 + 0] * W[0 * 3 + cc] + G3[r * 3 + 1] * W[1 * 3 + cc] + G3[r * 3 + 2] * W[2 * 3 + cc];
+        float grot[9];
+        // (G3 + G3^T) = 2 G3 only if symmetric; use the explicit sum for fidelity
+        float Yt[9];
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+#pragma unroll
+          for (int cc = 0; cc < 3; ++cc)
+            Yt[r * 3 + cc] = G3[0 * 3 + r] * W[0 * 3 + cc] + G3[1 * 3 + r] * W[1 * 3 + cc] + G3[2 * 3 + r] * W[2 * 3 + cc];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          o_ls[a] = (W[0 * 3 + a] * Y[0 * 3 + a] + W[1 * 3 + a] * Y[1 * 3 + a] + W[2 * 3 + a] * Y[2 * 3 + a]) * 2.f * s2[a];
+#pragma unroll
+          for (int r = 0; r < 3; ++r) grot[r * 3 + a] = (Y[r * 3 + a] + Yt[r * 3 + a]) * s2[a];
+        }
+        // rotation_derivatives (renderer.cpp:28-40), all scaled by 2
+        const float dw[9] = {0, -zq, y, zq, 0, -x, -y, x, 0};
+        const float dxm[9] = {0, y, zq, y, -2 * x, -w, zq, w, -2 * x};
+        const float dym[9] = {-2 * y, x, w, x, 0, zq, -w, zq, -2 * y};
+        const float dzm[9] = {-2 * zq, -w, x, w, -2 * zq, y, x, y, 0};
+        float gq[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int e = 0; e < 9; ++e) {
+          gq[0] = fmaf(grot[e], dw[e], gq[0]);
+          gq[1] = fmaf(grot[e], dxm[e], gq[1]);
+          gq[2] = fmaf(grot[e], dym[e], gq[2]);
+          gq[3] = fmaf(grot[e], dzm[e], gq[3]);
+        }
+#pragma unroll
+        for (int a = 0; a < 4; ++a) gq[a] *= 2.f;
+        const float dot = qh[0] * gq[0] + qh[1] * gq[1] + qh[2] * gq[2] + qh[3] * gq[3];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) o_rot[a] = (gq[a] - qh[a] * dot) * inorm;
+
+        if (g.pose) {
+          // t' = R_cw (p - omega x p - nu) + t_cw: g_omega += g_w x p, g_nu -= g_w
+          pose[0] += gw[1] * P[2] - gw[2] * P[1];
+          pose[1] += gw[2] * P[0] - gw[0] * P[2];
+          pose[2] += gw[0] * P[1] - gw[1] * P[0];
+          pose[3] -= gw[0];
+          pose[4] -= gw[1];
+          pose[5] -= gw[2];
+          // Sigma3' = (I - [omega]x) Sigma3 (I + [omega]x): A = Sigma3 G3 - G3 Sigma3, vee(A - A^T)
+          float A1[9], A2[9];
+#pragma unroll
+          for (int r = 0; r < 3; ++r)
+#pragma unroll
+            for (int cc = 0; cc < 3; ++cc) {
+              A1[r * 3 + cc] = S3[r * 3 + 0] * G3[0 * 3 + cc] + S3[r * 3 + 1] * G3[1 * 3 + cc] + S3[r * 3 + 2] * G3[2 * 3 + cc];
+              A2[r * 3 + cc] = G3[r * 3 + 0] * S3[0 * 3 + cc] + G3[r * 3 + 1] * S3[1 * 3 + cc] + G3[r * 3 + 2] * S3[2 * 3 + cc];
+            }
+          pose[0] += (A1[7] - A2[7]) - (A1[5] - A2[5]);
+          pose[1] += (A1[2] - A2[2]) - (A1[6] - A2[6]);
+          pose[2] += (A1[3] - A2[3]) - (A1[1] - A2[1]);
+        }
+      }
+#pragma unroll
+      for (int a = 0; a < 3; ++a) o_pos[a] = gpos[a];
+    }
+
+    // ---- dense writes in the reference layouts ------------------------------------------------
+    const bool accum = g.accumulate != 0;
+#define LGS_STORE(ptr, idx, val) \
+  do {                           \
+    if (accum) (ptr)[idx] += (val); else (ptr)[idx] = (val); \
+  } while (0)
+    if (g.position)
+#pragma unroll
+      for (int a = 0; a < 3; ++a) LGS_STORE(g.position, i * 3 + a, o_pos[a]);
+    if (g.rotation)
+#pragma unroll
+      for (int a = 0; a < 4; ++a) LGS_STORE(g.rotation, i * 4 + a, o_rot[a]);
+    if (g.log_scale)
+#pragma unroll
+      for (int a = 0; a < 3; ++a) LGS_STORE(g.log_scale, i * 3 + a, o_ls[a]);
+    if (g.opacity_logit) LGS_STORE(g.opacity_logit, i, o_op);
+    if (g.sh)
+#pragma unroll
+      for (int k = 0; k < K * 3; ++k) LGS_STORE(g.sh, i * (K * 3) + k, o_sh[k]);
+    if (DP > 0 && g.feature)
+#pragma unroll
+      for (int k = 0; k < DP; ++k)
+        if (k < m.d) LGS_STORE(g.feature, (int64_t)k * n + i, o_feat[k]);
+#undef LGS_STORE
+  }
+
+  if (g.pose) {  // block reduction of the pose gradient, one double atomic per value per block
+    __shared__ float s_pose[8][6];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int a = 0; a < 6; ++a) {
+      float p = pose[a];
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) p += __shfl_xor_sync(0xffffffffu, p, off);
+      if (lane == 0) s_pose[wid][a] = p;
+    }
+    __syncthreads();
+    if (threadIdx.x < 6) {
+      double s = 0.0;
+      for (int w2 = 0; w2 < (int)(blockDim.x >> 5); ++w2) s += (double)s_pose[w2][threadIdx.x];
+      if (s != 0.0) atomicAdd(g.pose + threadIdx.x, s);
+    }
+  }
+}
+
+template <int DEG, int DP>
+static void launch_pb(const DevMap& m, const DevCam& c, const ViewBufs& v, const float* gacc, const GradOut& g,
+                      cudaStream_t s) {
+  const unsigned blocks = (unsigned)((m.n + 255) / 256);
+  preprocess_bwd_kernel<DEG, DP, slots_for(DP)><<<blocks, 256, 0, s>>>(m, c, v, gacc, g);
+}
+
+template <int DEG>
+static void launch_pb_deg(const DevMap& m, const DevCam& c, const ViewBufs& v, const float* gacc, const GradOut& g,
+                          cudaStream_t s) {
+  switch (m.dp) {
+    case 0: launch_pb<DEG, 0>(m, c, v, gacc, g, s); break;
+    case 4: launch_pb<DEG, 4>(m, c, v, gacc, g, s); break;
+    case 8: launch_pb<DEG, 8>(m, c, v, gacc, g, s); break;
+    case 16: launch_pb<DEG, 16>(m, c, v, gacc, g, s); break;
+    default: launch_pb<DEG, 32>(m, c, v, gacc, g, s); break;
+  }
+}
+
+void launch_preprocess_bwd(const DevMap& m, const DevCam& c, const ViewBufs& v, const float* gacc, int slots,
+                           const GradOut& g, cudaStream_t s) {
+  (void)slots;
+  if (m.n == 0) return;
+  switch (m.deg) {
+    case 0: launch_pb_deg<0>(m, c, v, gacc, g, s); break;
+    case 1: launch_pb_deg<1>(m, c, v, gacc, g, s); break;
+    case 2: launch_pb_deg<2>(m, c, v, gacc, g, s); break;
+    default: launch_pb_deg<3>(m, c, v, gacc, g, s); break;
+  }
+}
+
+}  // namespace lgs

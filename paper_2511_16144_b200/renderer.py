@@ -1,0 +1,327 @@
+"""Host-side mirror of the reference renderer interface over the C ABI.
+
+Reference (proj/include/legoslam/renderer.hpp):
+    RenderConfig                                   -> RenderConfig
+    RenderOutput render(map, cam_pose, K, cfg)     -> render(map, camera, cfg) -> RenderOutput
+    MapGradients render_backward(map, out, grad_rgb, grad_depth, grad_feat)
+                                                   -> render_backward(map, out, grad_rgb, grad_depth, grad_feat)
+    project_gaussian(map, i, cam_pose, K, cfg)     -> RenderOutput.projected() (all i at once)
+
+Same argument meaning and error behaviour: an empty / None cotangent is zero, a cotangent of the
+wrong shape raises ValueError (the reference's std::invalid_argument, renderer.cpp:176-178),
+gradients are dense over the map (zeros for culled Gaussians) with rotations ordered (w,x,y,z)
+and features [d][N].  Every call goes through liblgs.so on the GPU; there is no CPU fallback.
+
+Maps are scene dicts in the reference layouts (see scenes.py) holding either numpy arrays (host
+memory: copied in/out by the library, like the reference API) or CUDA torch tensors (device
+memory, zero-copy), or a DeviceMap already resident in HBM.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from ._lib import LGS_MEM_DEVICE, LGS_MEM_HOST, check
+
+try:
+    import torch
+except ImportError:  # pragma: no cover - torch is part of the image
+    torch = None
+
+
+@dataclass
+class RenderConfig:
+    """renderer.hpp:15-22."""
+    near_plane: float = 0.01
+    dilation: float = 0.3
+    alpha_clamp: float = 0.99
+    alpha_skip: float = 1.0 / 255.0
+    transmittance_min: float = 1e-4
+    radius_sigma: float = 3.0
+
+    def c(self):
+        return _lib.LgsRenderConfig(self.near_plane, self.dilation, self.alpha_clamp, self.alpha_skip,
+                                    self.transmittance_min, self.radius_sigma)
+
+
+def _is_torch(x):
+    return torch is not None and isinstance(x, torch.Tensor)
+
+
+def _ptr(x):
+    if x is None:
+        return None
+    if _is_torch(x):
+        assert x.is_contiguous()
+        return x.data_ptr()
+    assert isinstance(x, np.ndarray) and x.flags.c_contiguous and x.dtype == np.float32, (type(x), getattr(x, "dtype", None))
+    return x.ctypes.data
+
+
+def _mem(x):
+    if _is_torch(x):
+        return LGS_MEM_DEVICE if x.is_cuda else LGS_MEM_HOST
+    return LGS_MEM_HOST
+
+
+def _f32(x):
+    if _is_torch(x):
+        return x.contiguous().float() if x.dtype != torch.float32 or not x.is_contiguous() else x
+    return np.ascontiguousarray(x, dtype=np.float32)
+
+
+def make_camera(cam) -> _lib.LgsCamera:
+    c = _lib.LgsCamera()
+    for i in range(4):
+        c.q[i] = float(cam["q"][i])
+    for i in range(3):
+        c.t[i] = float(cam["t"][i])
+    c.fx, c.fy, c.cx, c.cy = (float(cam[k]) for k in ("fx", "fy", "cx", "cy"))
+    c.width, c.height = int(cam["width"]), int(cam["height"])
+    return c
+
+
+class Context:
+    """One CUDA stream + stream-ordered memory pool (lgs_ctx).  By default the library enqueues on
+    torch's current stream so torch tensors and library calls stay ordered."""
+
+    def __init__(self, device: int = 0, stream=None):
+        L = _lib.load()
+        if stream is None and torch is not None and torch.cuda.is_available():
+            with torch.cuda.device(device):
+                stream = torch.cuda.current_stream(device).cuda_stream
+        h = C.c_void_p()
+        check(L.lgs_ctx_create(device, C.c_void_p(stream) if stream else None, C.byref(h)))
+        self.h = h
+        self.device = device
+
+    def synchronize(self):
+        check(_lib.load().lgs_ctx_synchronize(self.h))
+
+    @property
+    def launches(self) -> int:
+        return int(_lib.load().lgs_ctx_launch_count(self.h))
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib._lib is not None:
+            _lib._lib.lgs_ctx_destroy(self.h)
+            self.h = None
+
+
+_default_ctx: dict[int, Context] = {}
+
+
+def default_context(device: int = 0) -> Context:
+    if device not in _default_ctx:
+        _default_ctx[device] = Context(device)
+    return _default_ctx[device]
+
+
+def _gaussians_struct(scene):
+    arrs = {k: _f32(scene[k]) for k in ("pos", "rot", "log_s", "opac", "sh", "feat")}
+    n = int(arrs["pos"].shape[0])
+    d = int(arrs["feat"].shape[0]) if arrs["feat"].ndim == 2 else 0
+    K = int(arrs["sh"].shape[1])
+    deg = {1: 0, 4: 1, 9: 2, 16: 3}[K]
+    mem = _mem(arrs["pos"])
+    g = _lib.LgsGaussians(n, d, deg, _ptr(arrs["pos"]), _ptr(arrs["rot"]), _ptr(arrs["log_s"]), _ptr(arrs["opac"]),
+                          _ptr(arrs["sh"]), _ptr(arrs["feat"]) if d else None, mem)
+    return g, arrs
+
+
+class DeviceMap:
+    """A Gaussian map resident in HBM in the kernels' packed layout (lgs_map)."""
+
+    def __init__(self, scene, ctx: Context | None = None):
+        self.ctx = ctx or default_context()
+        g, self._arrs = _gaussians_struct(scene)
+        self.n, self.d, self.sh_degree = g.n, g.feature_dim, g.sh_degree
+        self.K = (self.sh_degree + 1) ** 2
+        h = C.c_void_p()
+        check(_lib.load().lgs_map_create(self.ctx.h, C.byref(g), C.byref(h)))
+        self.h = h
+        self._arrs = None  # the library copied (host) or packed (device) the attributes
+
+    def update(self, scene):
+        g, keep = _gaussians_struct(scene)
+        check(_lib.load().lgs_map_update(self.ctx.h, self.h, C.byref(g)))
+        del keep
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib._lib is not None:
+            _lib._lib.lgs_map_destroy(self.h)
+            self.h = None
+
+
+class RenderOutput:
+    """renderer.hpp:33-45: images + the backward tape (lgs_saved)."""
+
+    def __init__(self, ctx, tape, rgb, depth, feat, acc, n, d, K, cam, dmap):
+        self.ctx, self.tape = ctx, tape
+        self.rgb, self.depth, self.feat, self.acc = rgb, depth, feat, acc
+        self.n, self.d, self.K = n, d, K
+        self.camera = cam
+        self._map = dmap  # keeps the device map alive for the backward
+
+    def stats(self):
+        s = _lib.LgsRenderStats()
+        check(_lib.load().lgs_saved_stats(self.tape, C.byref(s)))
+        return dict(visible=s.visible, pairs=s.pairs, tiles=s.tiles, max_tile_list=s.max_tile_list)
+
+    def l1_loss(self) -> float:
+        v = C.c_double()
+        check(_lib.load().lgs_saved_l1_loss(self.ctx.h, self.tape, C.byref(v)))
+        return v.value
+
+    def projected(self):
+        """Per map index fp32 projected records (the batched project_gaussian, renderer.cpp:53-92)."""
+        n = self.n
+        r = dict(visible=np.zeros(n, np.uint8), u=np.zeros(n, np.float32), v=np.zeros(n, np.float32),
+                 depth=np.zeros(n, np.float32), conic=np.zeros((n, 3), np.float32), radius=np.zeros(n, np.float32),
+                 bbox=np.zeros((n, 4), np.int32), opacity=np.zeros(n, np.float32), color=np.zeros((n, 3), np.float32))
+        check(_lib.load().lgs_debug_projected(self.ctx.h, self.tape, *(r[k].ctypes.data for k in (
+            "visible", "u", "v", "depth", "conic", "radius", "bbox", "opacity", "color"))))
+        return r
+
+    def tile_keys(self):
+        """(keys u64 = tile << 32 | f32bits(depth), vals u32 map index, ranges [tiles, 2])."""
+        st = self.stats()
+        keys = np.zeros(max(st["pairs"], 1), np.uint64)
+        vals = np.zeros(max(st["pairs"], 1), np.uint32)
+        ranges = np.zeros((st["tiles"], 2), np.uint32)
+        check(_lib.load().lgs_debug_tile_keys(self.ctx.h, self.tape, keys.ctypes.data, vals.ctypes.data,
+                                              ranges.ctypes.data))
+        return keys[:st["pairs"]], vals[:st["pairs"]], ranges
+
+    def pixel_state(self):
+        H, W = self.camera.height, self.camera.width
+        ft = np.zeros((H, W), np.float32)
+        nc = np.zeros((H, W), np.uint32)
+        check(_lib.load().lgs_debug_pixel_state(self.ctx.h, self.tape, ft.ctypes.data, nc.ctypes.data))
+        return ft, nc
+
+    def __del__(self):
+        if getattr(self, "tape", None) and _lib._lib is not None:
+            _lib._lib.lgs_saved_destroy(self.tape)
+            self.tape = None
+
+
+def _alloc_like(device_side, shape, device):
+    if device_side:
+        return torch.empty(shape, dtype=torch.float32, device=f"cuda:{device}")
+    return np.empty(shape, np.float32)
+
+
+def render(map_, camera, cfg: RenderConfig | None = None, targets=None, ctx: Context | None = None,
+           out: dict | None = None) -> RenderOutput:
+    """lego::render (renderer.hpp:55-56).  ``map_``: DeviceMap or scene dict (numpy / CUDA tensors).
+
+    ``targets`` (optional dict rgb/depth/feat) fuses the L1 loss of SURVEY.md §8d into the forward.
+    Output images are CUDA tensors when the map is device-resident, numpy otherwise (or ``out``).
+    """
+    ctx = ctx or (map_.ctx if isinstance(map_, DeviceMap) else default_context())
+    dmap = map_ if isinstance(map_, DeviceMap) else None
+    host_scene = False
+    if dmap is None:
+        host_scene = _mem(map_["pos"]) == LGS_MEM_HOST
+        dmap = DeviceMap(map_, ctx)
+    cam = make_camera(camera)
+    H, W, d = cam.height, cam.width, dmap.d
+    if out is None:
+        dev = not host_scene
+        out = dict(rgb=_alloc_like(dev, (H, W, 3), ctx.device), depth=_alloc_like(dev, (H, W), ctx.device),
+                   feat=_alloc_like(dev, (H, W, d), ctx.device), acc=_alloc_like(dev, (H, W), ctx.device))
+    imgs = _lib.LgsImages(_ptr(out["rgb"]), _ptr(out["depth"]), _ptr(out["feat"]) if d else None, _ptr(out["acc"]),
+                          _mem(out["rgb"]))
+    tg = None
+    keep = None
+    if targets is not None:
+        keep = {k: _f32(targets[k]) for k in ("rgb", "depth", "feat")}
+        tg = _lib.LgsL1Targets(_ptr(keep["rgb"]), _ptr(keep["depth"]), _ptr(keep["feat"]) if d else None,
+                               _mem(keep["rgb"]))
+    c = (cfg or RenderConfig()).c()
+    tape = C.c_void_p()
+    check(_lib.load().lgs_render_forward(ctx.h, dmap.h, C.byref(cam), C.byref(c), C.byref(tg) if tg else None,
+                                         C.byref(imgs), C.byref(tape)))
+    del keep
+    return RenderOutput(ctx, tape, out["rgb"], out["depth"], out["feat"], out["acc"], dmap.n, d, dmap.K, cam, dmap)
+
+
+def alloc_grads(n, d, K, device=None, flat=None):
+    """MapGradients (renderer.hpp:59-68) as views into one flat fp32 buffer (NCCL-friendly):
+    position [N,3] | rotation [N,4] (w,x,y,z) | log_scale [N,3] | opacity_logit [N] | sh [N,K,3] | feature [d,N]."""
+    sizes = [("position", (n, 3)), ("rotation", (n, 4)), ("log_scale", (n, 3)), ("opacity_logit", (n,)),
+             ("sh", (n, K, 3)), ("feature", (d, n))]
+    total = sum(int(np.prod(s)) for _, s in sizes)
+    if flat is None:
+        flat = (torch.zeros(total, dtype=torch.float32, device=f"cuda:{device}") if device is not None
+                else np.zeros(total, np.float32))
+    out, o = {"flat": flat}, 0
+    for name, s in sizes:
+        k = int(np.prod(s))
+        out[name] = flat[o:o + k].reshape(s)
+        o += k
+    return out
+
+
+def _size(x):
+    return x.numel() if _is_torch(x) else x.size
+
+
+def _grads_struct(g, accumulate):
+    ptrs = [_ptr(g[k]) if _size(g[k]) else None
+            for k in ("position", "rotation", "log_scale", "opacity_logit", "sh", "feature")]
+    return _lib.LgsMapGrads(*ptrs, _mem(g["position"]), 1 if accumulate else 0)
+
+
+def _check_cot(x, shape, name):
+    if x is None:
+        return None
+    if (x.numel() if _is_torch(x) else x.size) == 0:
+        return None  # empty image = zero cotangent (renderer.hpp:70-71)
+    s = tuple(x.shape)
+    if len(s) == 2:
+        s = s + (1,)
+    if s != shape:
+        raise ValueError(f"render_backward: bad shape for {name}")  # renderer.cpp:176-178
+    return _f32(x)
+
+
+def render_backward(map_, out: RenderOutput, grad_rgb=None, grad_depth=None, grad_feat=None, pose: bool = False,
+                    into: dict | None = None, accumulate: bool = False):
+    """lego::render_backward (renderer.hpp:72-74).  ``map_`` is accepted for signature parity (the
+    tape references the map it was rendered from, which must be unchanged -- SPEC.md:278).
+
+    Returns the MapGradients dict (+ ``pose`` [6] = dL/d(omega, nu) when ``pose``)."""
+    H, W, d = out.camera.height, out.camera.width, out.d
+    cr = _check_cot(grad_rgb, (H, W, 3), "grad_rgb")
+    cd = _check_cot(grad_depth, (H, W, 1), "grad_depth")
+    cf = _check_cot(grad_feat, (H, W, d), "grad_feat") if d else None
+    mems = {_mem(x) for x in (cr, cd, cf) if x is not None}
+    if len(mems) > 1:
+        raise ValueError("cotangents must all be host or all be device memory")
+    cot = _lib.LgsCotangents(_ptr(cr), _ptr(cd), _ptr(cf), mems.pop() if mems else LGS_MEM_DEVICE)
+    dev = _is_torch(out.rgb) and out.rgb.is_cuda
+    g = into or alloc_grads(out.n, d, out.K, device=out.ctx.device if dev else None)
+    gs = _grads_struct(g, accumulate)
+    pg = (C.c_float * 6)() if pose else None
+    check(_lib.load().lgs_render_backward(out.ctx.h, out.tape, C.byref(cot), C.byref(gs), pg))
+    del cr, cd, cf
+    if pose:
+        g["pose"] = np.array(list(pg), dtype=np.float64)
+    return g
+
+
+def render_backward_l1(out: RenderOutput, pose: bool = False, into: dict | None = None, accumulate: bool = False):
+    """Backward of the L1 loss fused into ``render(..., targets=...)``."""
+    dev = _is_torch(out.rgb) and out.rgb.is_cuda
+    g = into or alloc_grads(out.n, out.d, out.K, device=out.ctx.device if dev else None)
+    gs = _grads_struct(g, accumulate)
+    pg = (C.c_float * 6)() if pose else None
+    check(_lib.load().lgs_render_backward_l1(out.ctx.h, out.tape, C.byref(gs), pg))
+    if pose:
+        g["pose"] = np.array(list(pg), dtype=np.float64)
+    return g

@@ -1,0 +1,190 @@
+"""Seeded synthetic scenes for the BASELINE.json configs (numpy PCG64, fp32-rounded).
+
+No public dataset ships with the reference or this container: the paper's
+Replica / TUM-RGBD / ScanNet scenes are replaced by seeded
+synthetic Gaussian maps with the shapes and value distributions BASELINE.json
+states.  Every value is drawn in float64 then rounded to float32 (the
+"draw through float" trick of proj/tests/test_map.cpp:17-18), so the fp64 CPU
+oracle and the fp32 GPU path see bit-identical inputs.
+
+Layouts are the reference's (proj/include/legoslam/gaussian_map.hpp:57-93):
+pos [N,3], rot [N,4] in Eigen storage order (x,y,z,w), log_s [N,3],
+opac [N] (logits), sh [N,K,3] (K=1 is the reference ``colors``), feat [d,N]
+(the column-major N x d Eigen matrix).
+
+Choices BASELINE.json leaves open are pinned here and
+recorded in DESIGN.md: config-1 pose = identity; config-2 camera on the room
+wall looking along +z; config-3 circle plane; config-4 arc and the remaining
+30% of Gaussians; L1 target ranges; seeds = 1000 + config id.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+CONFIG_NAMES = ("c0", "c1", "c1_500k", "c2", "c3", "c4")
+
+
+def _f32(a):
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float64).astype(np.float32))
+
+
+def camera(width, height, fx, fy, cx, cy, q=(1.0, 0.0, 0.0, 0.0), t=(0.0, 0.0, 0.0)):
+    """cam_pose is world<-camera (gaussian_map.hpp:30), q = (w,x,y,z); +z forward, +y down."""
+    return dict(q=np.array(q, np.float64), t=np.array(t, np.float64), fx=float(fx), fy=float(fy),
+                cx=float(cx), cy=float(cy), width=int(width), height=int(height))
+
+
+def _rot_to_quat(m):
+    tr = m[0, 0] + m[1, 1] + m[2, 2]
+    if tr > 0:
+        s = math.sqrt(tr + 1.0) * 2
+        w, x, y, z = 0.25 * s, (m[2, 1] - m[1, 2]) / s, (m[0, 2] - m[2, 0]) / s, (m[1, 0] - m[0, 1]) / s
+    elif m[0, 0] > m[1, 1] and m[0, 0] > m[2, 2]:
+        s = math.sqrt(1.0 + m[0, 0] - m[1, 1] - m[2, 2]) * 2
+        w, x, y, z = (m[2, 1] - m[1, 2]) / s, 0.25 * s, (m[0, 1] + m[1, 0]) / s, (m[0, 2] + m[2, 0]) / s
+    elif m[1, 1] > m[2, 2]:
+        s = math.sqrt(1.0 + m[1, 1] - m[0, 0] - m[2, 2]) * 2
+        w, x, y, z = (m[0, 2] - m[2, 0]) / s, (m[0, 1] + m[1, 0]) / s, 0.25 * s, (m[1, 2] + m[2, 1]) / s
+    else:
+        s = math.sqrt(1.0 + m[2, 2] - m[0, 0] - m[1, 1]) * 2
+        w, x, y, z = (m[1, 0] - m[0, 1]) / s, (m[0, 2] + m[2, 0]) / s, (m[1, 2] + m[2, 1]) / s, 0.25 * s
+    q = np.array([w, x, y, z])
+    return q / np.linalg.norm(q)
+
+
+def look_at(center, target):
+    """world<-camera pose at ``center`` with +z towards ``target`` and +y along world +y (down)."""
+    c = np.asarray(center, np.float64)
+    z = np.asarray(target, np.float64) - c
+    z /= np.linalg.norm(z)
+    x = np.cross(np.array([0.0, 1.0, 0.0]), z)
+    x /= np.linalg.norm(x)
+    y = np.cross(z, x)
+    return _rot_to_quat(np.stack([x, y, z], axis=1)), c
+
+
+def _unit_quats(rng, n):
+    q = rng.standard_normal((n, 4))
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    return q  # drawn as (w,x,y,z)
+
+
+def _pack(pos, q_wxyz, log_s, opac, sh, feat_nd):
+    rot = np.concatenate([q_wxyz[:, 1:4], q_wxyz[:, 0:1]], axis=1)  # -> Eigen storage x,y,z,w
+    return dict(pos=_f32(pos), rot=_f32(rot), log_s=_f32(log_s), opac=_f32(opac), sh=_f32(sh),
+                feat=_f32(np.ascontiguousarray(feat_nd.T)))
+
+
+def _features(rng, n, d):
+    f = rng.standard_normal((n, d))
+    f /= np.linalg.norm(f, axis=1, keepdims=True)
+    return f
+
+
+def _sh(rng, n, deg, dc=None):
+    K = (deg + 1) ** 2
+    sh = np.zeros((n, K, 3))
+    sh[:, 0, :] = rng.uniform(0.0, 1.0, (n, 3)) if dc is None else dc
+    if K > 1:
+        sh[:, 1:, :] = rng.normal(0.0, 0.05, (n, K - 1, 3))
+    return sh
+
+
+def make_config(name: str, n: int | None = None, d: int = 16):
+    """Returns (scene, [cameras], info) for a BASELINE.json config.
+
+    c0      : configs[0]  160x120, 10k, SH0, identity pose.
+    c1      : configs[1]  640x480, 200k, SH3, identity pose (+ pose gradient).
+    c1_500k : the BASELINE metric workload: configs[1] distributions at 500k.
+    c2      : configs[2]  1200x680, 1M, 200 blobs, SH3.
+    c3      : configs[3]  500k (config-1 distributions), 8 views on a 1 m circle.
+    c4      : configs[4]  3M, 70% in a 0.5 m sphere, 16 views on a 2 m arc.
+    """
+    cid = {"c0": 0, "c1": 1, "c1_500k": 1, "c2": 2, "c3": 3, "c4": 4}[name]
+    rng = np.random.Generator(np.random.PCG64(1000 + cid))
+    info = dict(config=name, seed=1000 + cid)
+    if name == "c0":
+        n = n or 10_000
+        pos = np.stack([rng.uniform(-1, 1, n), rng.uniform(-1, 1, n), rng.uniform(2, 5, n)], 1)
+        scene = _pack(pos, _unit_quats(rng, n), rng.normal(-3, 0.5, (n, 3)), rng.normal(0, 1, n), _sh(rng, n, 0),
+                      _features(rng, n, d))
+        cams = [camera(160, 120, 140, 140, 80, 60)]
+        info.update(depth_range=(2.0, 5.0))
+    elif name in ("c1", "c1_500k", "c3"):
+        n = n or (200_000 if name == "c1" else 500_000)
+        pos = np.stack([rng.uniform(-2, 2, n), rng.uniform(-2, 2, n), rng.uniform(0.5, 6, n)], 1)
+        scene = _pack(pos, _unit_quats(rng, n), rng.normal(-3, 0.5, (n, 3)), rng.normal(0, 1, n), _sh(rng, n, 3),
+                      _features(rng, n, d))
+        K = dict(width=640, height=480, fx=577.6, fy=577.6, cx=319.5, cy=239.5)
+        if name == "c3":
+            # pinned: 8 cameras on a 1 m circle in the z = 0 plane around the optical axis of
+            # config 1, each looking at the cloud centre (0, 0, 3.25)
+            cams = []
+            for i in range(8):
+                th = 2 * math.pi * i / 8
+                q, t = look_at([math.cos(th), math.sin(th), 0.0], [0.0, 0.0, 3.25])
+                cams.append(camera(q=q, t=t, **K))
+        else:
+            cams = [camera(**K)]
+        info.update(depth_range=(0.5, 6.0))
+    elif name == "c2":
+        n = n or 1_000_000
+        nb = 200
+        centres = np.stack([rng.uniform(-3, 3, nb), rng.uniform(-1.5, 1.5, nb), rng.uniform(-3, 3, nb)], 1)
+        blob_feat = rng.standard_normal((nb, d))
+        which = rng.integers(0, nb, n)
+        pos = centres[which] + rng.normal(0, 0.3, (n, 3))
+        f = blob_feat[which] + rng.normal(0, 0.1, (n, d))
+        f /= np.linalg.norm(f, axis=1, keepdims=True)
+        scene = _pack(pos, _unit_quats(rng, n), rng.normal(-4, 0.7, (n, 3)), rng.normal(0, 1, n), _sh(rng, n, 3), f)
+        # pinned: camera on the room wall z = -3.2, looking along +z through the room centre
+        cams = [camera(1200, 680, 600, 600, 599.5, 339.5, t=(0.0, 0.0, -3.2))]
+        info.update(depth_range=(0.5, 6.5))
+    elif name == "c4":
+        n = n or 3_000_000
+        n_in = int(round(0.7 * n))
+        n_out = n - n_in
+        # 70%: uniform in a 0.5 m ball at (0, 0, 1.5), anisotropic scales
+        v = rng.standard_normal((n_in, 3))
+        v /= np.linalg.norm(v, axis=1, keepdims=True)
+        r = 0.5 * rng.uniform(0, 1, n_in) ** (1.0 / 3.0)
+        p_in = v * r[:, None] + np.array([0.0, 0.0, 1.5])
+        ls_in = np.stack([rng.normal(-1, 0.3, n_in), rng.normal(-5, 0.3, n_in), rng.normal(-5, 0.3, n_in)], 1)
+        ol_in = rng.normal(1, 1, n_in)
+        # pinned: remaining 30% follow the config-1 distributions
+        p_out = np.stack([rng.uniform(-2, 2, n_out), rng.uniform(-2, 2, n_out), rng.uniform(0.5, 6, n_out)], 1)
+        ls_out = rng.normal(-3, 0.5, (n_out, 3))
+        ol_out = rng.normal(0, 1, n_out)
+        pos = np.concatenate([p_in, p_out])
+        scene = _pack(pos, _unit_quats(rng, n), np.concatenate([ls_in, ls_out]), np.concatenate([ol_in, ol_out]),
+                      _sh(rng, n, 3), _features(rng, n, d))
+        # pinned: 16 cameras on a 2 m long arc of radius 1.5 m around the sphere centre (x-z plane)
+        cams = []
+        span = 2.0 / 1.5
+        for i in range(16):
+            th = (i / 15.0 - 0.5) * span
+            q, t = look_at([1.5 * math.sin(th), 0.0, 1.5 - 1.5 * math.cos(th)], [0.0, 0.0, 1.5])
+            cams.append(camera(1200, 680, 600, 600, 599.5, 339.5, q=q, t=t))
+        info.update(depth_range=(0.5, 6.0))
+    else:
+        raise ValueError(name)
+    info["n"] = n
+    return scene, cams, info
+
+
+def make_targets(cam, d, depth_range, seed):
+    """Seeded L1 targets (pinned): rgb U[0,1], depth U[depth_range], feature U[-1,1]; HWC fp32."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    H, W = cam["height"], cam["width"]
+    return dict(rgb=_f32(rng.uniform(0, 1, (H, W, 3))), depth=_f32(rng.uniform(*depth_range, (H, W))),
+                feat=_f32(rng.uniform(-1, 1, (H, W, d))))
+
+
+def l1_cotangents(rgb, depth, feat, targets):
+    """dL/d(image) of L = mean|rgb-T| + mean|depth-T| + mean|feat-T| (sign(0) = 0)."""
+    g_rgb = np.sign(rgb - targets["rgb"]) / rgb.size
+    g_depth = np.sign(depth - targets["depth"]) / depth.size
+    g_feat = np.sign(feat - targets["feat"]) / max(feat.size, 1)
+    return g_rgb, g_depth, g_feat

@@ -1,0 +1,370 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against the CPU oracle on identical inputs.
+
+* preprocess records, tile key lists, sorted order and per-tile ranges: bit-exact vs oracle B;
+* images: within 1e-4 rel / 1e-5 abs of the reference compositor (oracle A) run on the same
+  fp32 projected records (tests/parity.py documents the threshold-flip allowance);
+* gradients: within 1e-3 relative (with the gradcheck-style floor) of oracle A's backward;
+* the reference renderer test suite (proj/tests/test_renderer.cpp) re-run through the GPU.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from tests.parity import GROUPS, grad_mismatch, image_mismatch, to_np
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2511_16144_b200 import renderer as R  # noqa: E402
+from paper_2511_16144_b200 import scenes  # noqa: E402
+from tests.ref_scenes import MapBuilder, logit, make_grad_scene, small_camera, splat_at  # noqa: E402
+
+
+def dev_scene(scene):
+    return {k: torch.from_numpy(np.ascontiguousarray(v, dtype=np.float32)).cuda() for k, v in scene.items()}
+
+
+def f32_scene(scene):
+    return {k: np.ascontiguousarray(v, dtype=np.float32) for k, v in scene.items()}
+
+
+@pytest.fixture(scope="module")
+def c0():
+    scene, cams, info = scenes.make_config("c0")
+    return scene, cams[0], info
+
+
+def _projected_equal(gp, op):
+    vis = op["visible"].astype(bool)
+    assert np.array_equal(gp["visible"].astype(bool), vis), "visible sets differ"
+    for k in ("u", "v", "depth", "conic", "radius", "opacity", "color"):
+        a = gp[k][vis].view(np.uint32)
+        b = op[k][vis].view(np.uint32)
+        nd = int((a != b).sum())
+        assert nd == 0, f"{k}: {nd} values differ bitwise"
+    assert np.array_equal(gp["bbox"][vis], op["bbox"][vis])
+
+
+@pytest.mark.parametrize("name,n", [("c0", None), ("c1", 50_000), ("c2", 50_000), ("c4", 60_000)])
+def test_preprocess_and_keys_bit_exact(oracle, name, n):
+    scene, cams, info = scenes.make_config(name, n=n)
+    for cam in cams[:3]:
+        out = R.render(dev_scene(scene), cam)
+        torch.cuda.synchronize()
+        gp = out.projected()
+        op = oracle.preprocess_f32(scene, cam)
+        _projected_equal(gp, op)
+        keys, vals, ranges = out.tile_keys()
+        okeys, ovals, oranges = oracle.bin_f32(op, cam["width"], cam["height"])
+        assert keys.shape == okeys.shape
+        assert np.array_equal(keys, okeys), "tile key lists differ"
+        assert np.array_equal(vals, ovals), "sorted order differs"
+        assert np.array_equal(ranges, oranges), "tile ranges differ"
+
+
+def _oracle_fwd_bwd(oracle, scene, cam, cfg=None, inject=True, cot=None, pose=True):
+    pre = oracle.preprocess_f32(scene, cam, cfg) if inject else None
+    ref = oracle.render(scene, cam, cfg, inject=pre)
+    g = None
+    if cot is not None:
+        g = oracle.render_backward(ref, *cot, pose=pose)
+    return ref, g
+
+
+@pytest.mark.parametrize("name,n", [("c0", None), ("c1", 30_000)])
+def test_images_and_grads_match_oracle(oracle, name, n):
+    scene, cams, info = scenes.make_config(name, n=n)
+    cam = cams[0]
+    d = scene["feat"].shape[0]
+    tg = scenes.make_targets(cam, d, info["depth_range"], 11)
+    out = R.render(dev_scene(scene), cam)
+    ref, _ = _oracle_fwd_bwd(oracle, scene, cam)
+    for img, r in ((out.rgb, ref.rgb), (out.depth, ref.depth), (out.feat, ref.feat), (out.acc, ref.acc)):
+        frac, mx = image_mismatch(img, r)
+        assert frac < 2e-4, (frac, mx)
+    # identical cotangents on both sides (computed once from the oracle render)
+    cot = scenes.l1_cotangents(ref.rgb, ref.depth, ref.feat, tg)
+    gref = oracle.render_backward(ref, *cot, pose=True)
+    gg = R.render_backward(None, out, *(torch.from_numpy(c.astype(np.float32)).cuda() for c in cot), pose=True)
+    for k in GROUPS:
+        frac, worst = grad_mismatch(gg[k], gref[k])
+        assert frac < 1e-3, (k, frac, worst)
+    frac, worst = grad_mismatch(gg["pose"], gref["pose"], floor=0.0)
+    assert frac == 0.0, (gg["pose"], gref["pose"])
+
+
+def test_gradcheck_scene_vs_oracle(oracle):
+    """The reference's FD gradcheck scene (gradcheck.hpp:31-78, seed 101) through the GPU."""
+    scene, cam, cfg, w_rgb, w_depth, w_feat = make_grad_scene(oracle, 12, 16, 8, 101)
+    s32 = f32_scene(scene)
+    rc = R.RenderConfig(**{k: v for k, v in cfg.items()})
+    out = R.render(dev_scene(s32), cam, rc)
+    ref = oracle.render(s32, cam, cfg)
+    for img, r in ((out.rgb, ref.rgb), (out.depth, ref.depth), (out.feat, ref.feat)):
+        frac, mx = image_mismatch(img, r)
+        assert frac == 0.0, (frac, mx)
+    gref = oracle.render_backward(ref, w_rgb, w_depth, w_feat, pose=True)
+    gg = R.render_backward(None, out, *(torch.from_numpy(c.astype(np.float32)).cuda() for c in (w_rgb, w_depth, w_feat)),
+                           pose=True)
+    for k in GROUPS:
+        frac, worst = grad_mismatch(gg[k], gref[k])
+        assert frac == 0.0, (k, worst)
+
+
+@pytest.mark.parametrize("deg", [1, 2, 3])
+def test_sh_and_pose_grads(oracle, deg):
+    scene, cam, cfg, w_rgb, w_depth, w_feat = make_grad_scene(oracle, 12, 16, 8, 101, sh_degree=deg)
+    cam = oracle.perturb_pose(cam, np.array([0.05, -0.03, 0.02, 0.02, 0.01, -0.05]))
+    s32 = f32_scene(scene)
+    out = R.render(dev_scene(s32), cam, R.RenderConfig(**cfg))
+    ref = oracle.render(s32, cam, cfg)
+    frac, mx = image_mismatch(out.rgb, ref.rgb)
+    assert frac == 0.0, mx
+    gref = oracle.render_backward(ref, w_rgb, w_depth, w_feat, pose=True)
+    gg = R.render_backward(None, out, *(torch.from_numpy(c.astype(np.float32)).cuda() for c in (w_rgb, w_depth, w_feat)),
+                           pose=True)
+    for k in GROUPS:
+        frac, worst = grad_mismatch(gg[k], gref[k])
+        assert frac == 0.0, (k, worst)
+    frac, worst = grad_mismatch(gg["pose"], gref["pose"], floor=0.0)
+    assert frac == 0.0, (gg["pose"], gref["pose"])
+
+
+# ---- the reference renderer tests (proj/tests/test_renderer.cpp) through the GPU ------------------
+
+def _map1(p, scale, ol, color, d=4):
+    mb = MapBuilder(d)
+    splat_at(mb, p, scale, ol, color)
+    return f32_scene(mb.scene())
+
+
+def test_ref_on_axis_projection():
+    """test_renderer.cpp:38-49 (fp32: cov2d is not exported, check the conic = cov2d^-1)."""
+    out = R.render(dev_scene(_map1([0, 0, 1], 0.1, 0.0, [1, 0, 0])), small_camera())
+    p = out.projected()
+    assert p["visible"][0]
+    assert p["conic"][0, 0] == pytest.approx(1 / 100.3, rel=1e-6)
+    assert p["conic"][0, 2] == pytest.approx(1 / 100.3, rel=1e-6)
+    assert abs(p["conic"][0, 1]) < 1e-9
+    assert p["depth"][0] == pytest.approx(1.0)
+
+
+def test_ref_behind_camera_culled():
+    """test_renderer.cpp:51-57."""
+    out = R.render(dev_scene(_map1([0, 0, -1], 0.1, 0.0, [1, 0, 0])), small_camera())
+    assert not out.projected()["visible"][0]
+    assert float(out.acc.abs().max()) == 0.0
+
+
+def test_ref_doubling_fx():
+    """test_renderer.cpp:59-71 (fp32 tolerance)."""
+    s = _map1([0.2, 0.1, 1.5], 0.05, 0.0, [1, 0, 0])
+    k = small_camera()
+    p1 = R.render(dev_scene(s), k).projected()
+    k2 = dict(k, fx=200.0, fy=200.0)
+    p2 = R.render(dev_scene(s), k2).projected()
+    assert (p2["u"][0] - 31.5) == pytest.approx(2 * (p1["u"][0] - 31.5), rel=1e-6)
+    assert (p2["v"][0] - 31.5) == pytest.approx(2 * (p1["v"][0] - 31.5), rel=1e-6)
+
+
+def test_ref_empty_map():
+    """test_renderer.cpp:73-80."""
+    out = R.render(dev_scene(f32_scene(MapBuilder(4).scene())), small_camera())
+    for img in (out.rgb, out.acc, out.depth, out.feat):
+        assert float(img.abs().max()) == 0.0 if img.numel() else True
+    g = R.render_backward(None, out, torch.ones(64, 64, 3, device="cuda"))
+    assert g["position"].numel() == 0
+
+
+def test_ref_single_opaque_splat():
+    """test_renderer.cpp:82-93."""
+    out = R.render(dev_scene(_map1([0, 0, 1.0], 0.2, logit(0.99), [1, 0, 0])), small_camera())
+    rgb, depth, acc = to_np(out.rgb), to_np(out.depth), to_np(out.acc)
+    assert rgb[31, 31, 0] == pytest.approx(0.99, rel=1e-3)
+    assert rgb[31, 31, 1] == 0.0
+    assert depth[31, 31] == pytest.approx(1.0, rel=1e-6)
+    assert acc[31, 31] == pytest.approx(0.99, rel=1e-3)
+
+
+def test_ref_two_coincident_splats():
+    """test_renderer.cpp:95-106."""
+    mb = MapBuilder(4)
+    splat_at(mb, [0, 0, 1.0], 0.5, logit(0.5), [1, 0, 0])
+    splat_at(mb, [0, 0, 1.0001], 0.5, logit(0.5), [0, 1, 0])
+    rgb = to_np(R.render(dev_scene(f32_scene(mb.scene())), small_camera()).rgb)
+    assert rgb[31, 31, 0] == pytest.approx(0.5, rel=1e-3)
+    assert rgb[31, 31, 1] == pytest.approx(0.25, rel=1e-3)
+
+
+def test_ref_insertion_order_invariance(oracle):
+    """test_renderer.cpp:108-131 (bit-identical on the GPU: same sorted order either way)."""
+    rng = oracle.Rng(31)
+    gs = []
+    for _ in range(12):
+        p = [rng.uniform(-0.3, 0.3), rng.uniform(-0.3, 0.3), rng.uniform(0.8, 2.0)]
+        gs.append((p, rng.uniform(0.03, 0.08), rng.uniform(-1, 2), [rng.uniform(0, 1) for _ in range(3)],
+                   [rng.normal() for _ in range(8)]))
+    fwd, rev = MapBuilder(8), MapBuilder(8)
+    for g in gs:
+        splat_at(fwd, *g)
+    for g in reversed(gs):
+        splat_at(rev, *g)
+    a = to_np(R.render(dev_scene(f32_scene(fwd.scene())), small_camera()).rgb)
+    b = to_np(R.render(dev_scene(f32_scene(rev.scene())), small_camera()).rgb)
+    assert np.max(np.abs(a - b)) < 1e-6
+
+
+def test_ref_bounded_outputs(oracle):
+    """test_renderer.cpp:133-161."""
+    rng = oracle.Rng(32)
+    mb = MapBuilder(8)
+    mx = 0.0
+    for _ in range(30):
+        p = [rng.uniform(-0.4, 0.4), rng.uniform(-0.4, 0.4), rng.uniform(0.6, 2.5)]
+        sc, ol = rng.uniform(0.02, 0.1), rng.uniform(-1, 3)
+        col = [rng.uniform(0, 1) for _ in range(3)]
+        f = [rng.normal() for _ in range(8)]
+        mx = max(mx, float(np.linalg.norm(f)))
+        splat_at(mb, p, sc, ol, col, f)
+    out = R.render(dev_scene(f32_scene(mb.scene())), small_camera())
+    acc, rgb, feat = to_np(out.acc), to_np(out.rgb), to_np(out.feat)
+    assert acc.min() >= 0.0 and acc.max() <= 1.0 + 1e-6
+    assert rgb.max() <= 1.01 and rgb.min() >= 0.0
+    assert np.linalg.norm(feat, axis=2).max() <= mx + 1e-5
+
+
+def test_ref_zero_cotangent():
+    """test_renderer.cpp:163-173."""
+    out = R.render(dev_scene(_map1([0, 0, 1], 0.1, 0.5, [0.5, 0.5, 0.5])), small_camera())
+    g = R.render_backward(None, out, None, None, torch.zeros(64, 64, 4, device="cuda"))
+    assert float(g["feature"].abs().max()) == 0.0
+    assert float(g["position"][0].norm()) == 0.0
+
+
+def test_ref_color_grad_equals_weight():
+    """test_renderer.cpp:175-187."""
+    out = R.render(dev_scene(_map1([0, 0, 1], 0.2, logit(0.8), [0.3, 0.3, 0.3])), small_camera())
+    gr = torch.zeros(64, 64, 3, device="cuda")
+    gr[31, 31, 0] = 1.0
+    g = R.render_backward(None, out, gr)
+    assert float(g["sh"][0, 0, 0]) == pytest.approx(float(out.acc[31, 31]), rel=1e-6)
+    assert float(g["sh"][0, 0, 1]) == 0.0
+
+
+def test_ref_mismatched_cotangent_raises():
+    """test_renderer.cpp:189-196."""
+    out = R.render(dev_scene(_map1([0, 0, 1], 0.1, 0.0, [1, 1, 1])), small_camera())
+    with pytest.raises(ValueError):
+        R.render_backward(None, out, torch.zeros(8, 8, 3, device="cuda"))
+
+
+# ---- boundary behaviour -------------------------------------------------------------------------
+
+def test_host_and_device_paths_agree(c0):
+    scene, cam, info = c0
+    tg = scenes.make_targets(cam, 16, info["depth_range"], 3)
+    out_d = R.render(dev_scene(scene), cam)
+    out_h = R.render(f32_scene(scene), cam)  # numpy = host memory, copies inside the library
+    assert isinstance(out_h.rgb, np.ndarray)
+    for a, b in ((out_d.rgb, out_h.rgb), (out_d.feat, out_h.feat), (out_d.depth, out_h.depth)):
+        assert np.array_equal(to_np(a), b)
+    cot = scenes.l1_cotangents(out_h.rgb, out_h.depth, out_h.feat, tg)
+    gd = R.render_backward(None, out_d, *(torch.from_numpy(c.astype(np.float32)).cuda() for c in cot))
+    gh = R.render_backward(None, out_h, *(c.astype(np.float32) for c in cot))
+    for k in GROUPS:
+        frac, worst = grad_mismatch(gd[k], gh[k], rtol=1e-5)
+        assert frac == 0.0, (k, worst)
+
+
+def test_fused_l1_matches_explicit_cotangents(c0):
+    scene, cam, info = c0
+    tg = scenes.make_targets(cam, 16, info["depth_range"], 5)
+    dtg = {k: torch.from_numpy(v).cuda() for k, v in tg.items()}
+    out = R.render(dev_scene(scene), cam, targets=dtg)
+    g1 = R.render_backward_l1(out, pose=True)
+    rgb, depth, feat = to_np(out.rgb), to_np(out.depth), to_np(out.feat)
+    cot = scenes.l1_cotangents(rgb, depth, feat, tg)
+    loss = np.abs(rgb - tg["rgb"]).mean() + np.abs(depth - tg["depth"]).mean() + np.abs(feat - tg["feat"]).mean()
+    assert out.l1_loss() == pytest.approx(loss, rel=1e-5)
+    g2 = R.render_backward(None, out, *(torch.from_numpy(c.astype(np.float32)).cuda() for c in cot), pose=True)
+    for k in GROUPS:
+        frac, worst = grad_mismatch(g1[k], g2[k], rtol=1e-5)
+        assert frac == 0.0, (k, worst)
+
+
+def test_accumulate_sums_views(c0):
+    scene, cam, info = c0
+    ds = dev_scene(scene)
+    cams = [cam, dict(cam, t=np.array([0.05, 0.0, 0.0]))]
+    tg = scenes.make_targets(cam, 16, info["depth_range"], 9)
+    dtg = {k: torch.from_numpy(v).cuda() for k, v in tg.items()}
+    dm = R.DeviceMap(ds)
+    acc = R.alloc_grads(dm.n, dm.d, dm.K, device=0)
+    singles = []
+    for c in cams:
+        out = R.render(dm, c, targets=dtg)
+        R.render_backward_l1(out, into=acc, accumulate=True)
+        singles.append(R.render_backward_l1(R.render(dm, c, targets=dtg)))
+    for k in GROUPS:
+        frac, worst = grad_mismatch(acc[k], singles[0][k] + singles[1][k], rtol=1e-4)
+        assert frac == 0.0, (k, worst)
+
+
+@pytest.mark.parametrize("d", [0, 4, 8, 32])
+def test_feature_dims(oracle, d):
+    scene, cams, info = scenes.make_config("c0", n=3000, d=max(d, 1))
+    if d == 0:
+        scene["feat"] = np.zeros((0, scene["pos"].shape[0]), np.float32)
+    cam = cams[0]
+    out = R.render(dev_scene(scene), cam)
+    ref, _ = _oracle_fwd_bwd(oracle, scene, cam)
+    frac, mx = image_mismatch(out.rgb, ref.rgb)
+    assert frac < 1e-3, mx
+    if d:
+        frac, mx = image_mismatch(out.feat, ref.feat)
+        assert frac < 1e-3, mx
+    rng = np.random.default_rng(0)
+    cot = (rng.uniform(-1, 1, (120, 160, 3)), rng.uniform(-1, 1, (120, 160)), rng.uniform(-1, 1, (120, 160, d)))
+    gref = oracle.render_backward(ref, *cot)
+    gg = R.render_backward(None, out, *(torch.from_numpy(c.astype(np.float32)).cuda() for c in cot))
+    for k in GROUPS:
+        frac, worst = grad_mismatch(gg[k], gref[k])
+        assert frac < 1e-3, (k, frac, worst)
+
+
+@pytest.mark.parametrize("W,H", [(1, 1), (17, 33), (100, 7)])
+def test_ragged_image_sizes(oracle, W, H):
+    scene, cams, info = scenes.make_config("c0", n=2000)
+    cam = dict(cams[0], width=W, height=H, cx=W / 2, cy=H / 2)
+    out = R.render(dev_scene(scene), cam)
+    ref, _ = _oracle_fwd_bwd(oracle, scene, cam)
+    frac, mx = image_mismatch(out.rgb, ref.rgb)
+    assert frac < 1e-3, mx
+    keys, vals, ranges = out.tile_keys()
+    okeys, ovals, oranges = oracle.bin_f32(oracle.preprocess_f32(scene, cam), W, H)
+    assert np.array_equal(keys, okeys) and np.array_equal(ranges, oranges)
+
+
+def test_near_plane_giant_splats(oracle):
+    """Gaussians just past the near plane cover the whole image (radius >> image): rects clamp."""
+    mb = MapBuilder(4)
+    for i in range(20):
+        splat_at(mb, [0.001 * i, -0.001 * i, 0.011 + 0.001 * i], 0.05, 0.5, [0.1 * (i % 10), 0.5, 0.2],
+                 [0.1, 0.2, -0.3, 0.4])
+    s = f32_scene(mb.scene())
+    out = R.render(dev_scene(s), small_camera())
+    ref, _ = _oracle_fwd_bwd(oracle, s, small_camera())
+    frac, mx = image_mismatch(out.rgb, ref.rgb)
+    assert frac < 1e-3, mx
+
+
+def test_deterministic_images(c0):
+    scene, cam, _ = c0
+    ds = dev_scene(scene)
+    a = R.render(ds, cam)
+    b = R.render(ds, cam)
+    assert torch.equal(a.rgb, b.rgb) and torch.equal(a.feat, b.feat)
