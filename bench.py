@@ -1,0 +1,403 @@
+#!/usr/bin/env python
+"""Benchmark: fwd+bwd render iterations/s, 640x480 RGB + depth + 16-D feature, 500k Gaussians.
+
+BASELINE.json metric, configs[1] distributions at the metric's 500k Gaussians (SH degree 3,
+16-D normalized features, identity pose), seeded synthetic inputs (no dataset ships with the
+reference).  One step = one view: preprocess -> binning -> blend forward with the
+fused L1 loss -> blend backward -> preprocess backward (all map gradients + the 6-DoF pose
+gradient, read back to the host).  With N > 1 (torchrun) every rank renders its own view of the
+replicated map and the flat fp32 gradient (500k x 75 floats) is all-reduced over NCCL (weak
+scaling: one view per GPU per step).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Timing: W >= 3 untimed warm-up steps; K timed steps, each bracketed by CUDA events on the
+library's stream, with a 512 MiB L2 flush (not timed) before every step; barrier + synchronize
+on both sides; max over ranks.  SM clocks are sampled with nvidia-smi during the timed region.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fwd+bwd render iters/s, 640x480 RGB+depth+16-D feat, 500k Gaussians"
+UNIT = "it/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--config", default="c1_500k")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--e2e-steps", type=int, default=5)
+    return p.parse_args()
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, smax, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+def rank_camera(base_cam, rank, world):
+    """Rank r renders the headline view translated by 2 cm per rank (same work, distinct views)."""
+    import numpy as np
+    cam = dict(base_cam)
+    if world > 1:
+        cam["t"] = np.array([0.02 * rank, 0.0, 0.0])
+    return cam
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2511_16144_b200 import _lib
+    from paper_2511_16144_b200 import renderer as R
+    from paper_2511_16144_b200 import scenes
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    _lib.load()  # fails loudly without the CUDA library: there is no fallback
+
+    scene, cams, info = scenes.make_config(args.config)
+    cam = rank_camera(cams[0], rank, world)
+    d = scene["feat"].shape[0]
+    K = scene["sh"].shape[1]
+    n = scene["pos"].shape[0]
+    tg = scenes.make_targets(cam, d, info["depth_range"], 7 + rank)
+
+    stream = torch.cuda.Stream(device=local)
+    ctx = R.Context(local, stream=stream.cuda_stream)
+    with torch.cuda.stream(stream):
+        dscene = {k: torch.from_numpy(v).cuda(local) for k, v in scene.items()}
+        dtg = {k: torch.from_numpy(v).cuda(local) for k, v in tg.items()}
+        dmap = R.DeviceMap(dscene, ctx)
+        grads = R.alloc_grads(n, d, K, device=local)
+        flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
+    del dscene
+
+    def step():
+        out = R.render(dmap, cam, targets=dtg, ctx=ctx)
+        g = R.render_backward_l1(out, pose=True, into=grads)  # pose grad read back to the host
+        if world > 1:
+            with torch.cuda.stream(stream):
+                dist.all_reduce(grads["flat"])
+        return out, g
+
+    with torch.cuda.stream(stream):
+        for _ in range(max(args.warmup, 3)):
+            step()
+    torch.cuda.synchronize()
+
+    # ---- timed region --------------------------------------------------------------------------
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = ctx.launches
+    with ClockSampler(local) as clk, torch.cuda.stream(stream):
+        for k in range(args.steps):
+            flush.fill_(float(k))
+            evs[k][0].record(stream)
+            out, g = step()
+            evs[k][1].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = ctx.launches - launches0
+    per_step = [a.elapsed_time(b) for a, b in evs]
+    ms = sum(per_step) / len(per_step)
+    t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = world * 1000.0 / ms_max
+
+    # ---- phase profile (separate, untimed pass) -----------------------------------------------
+    ctx.profile(True)
+    n_prof = 5
+    with torch.cuda.stream(stream):
+        for k in range(n_prof):
+            flush.fill_(float(k))
+            out, g = step()
+    torch.cuda.synchronize()
+    phases = {k: (v[0] / n_prof, v[1] // n_prof) for k, v in ctx.phase_times().items() if v[1]}
+    ctx.profile(False)
+    st = out.stats()
+    evaluated, contributed = out.work()
+    peak = {}
+    try:
+        peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except (OSError, ValueError):
+        pass
+    hbm_peak = float(peak.get("hbm_gbs", 6650.0))
+    hbm_src = "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peak else "B200_PROFILING.md fallback"
+    import ctypes as C
+    v = C.c_double()
+    _lib.check(_lib.load().lgs_measure_fp32_peak(local, C.byref(v)))
+    fp32 = v.value
+
+    # algorithmic work per launch
+    npix = cam["width"] * cam["height"]
+    V, P = st["visible"], st["pairs"]
+    F_EVAL, F_FWD, F_BWD = 13.0, 45.0, 100.0
+    work = {
+        "preprocess": ("hbm", n * (16 * 3 + 12 * K) + n * (16 * 3 + 8 + 12)),
+        "depth_sort_scan": ("hbm", n * 8 * 2 * 4 + n * 4 * 3),
+        "duplicate_keys": ("hbm", V * 16 + P * 6),
+        "tile_sort_ranges": ("hbm", P * 6 * 2 * 2 + P * 2),
+        "blend_fwd": ("fp32", F_EVAL * evaluated + F_FWD * contributed),
+        "blend_bwd": ("fp32", F_EVAL * evaluated + F_BWD * contributed),
+        "preprocess_bwd": ("hbm", n * (16 * 3 + 12 * K + 16 + 128 + 4) + n * 4 * (11 + 3 * K + d)),
+    }
+    phase_rows = {}
+    for name, (pms, cnt) in phases.items():
+        if name not in work:
+            continue
+        bound, amount = work[name]
+        if bound == "hbm":
+            ach = amount / (pms * 1e-3) / 1e9
+            frac = ach / hbm_peak
+            phase_rows[name] = {"ms": round(pms, 4), "bound": "hbm", "achieved": round(ach, 1), "unit": "GB/s",
+                                "frac": round(frac, 4), "algorithmic_bytes": int(amount)}
+        else:
+            ach = amount / (pms * 1e-3) / 1e12
+            phase_rows[name] = {"ms": round(pms, 4), "bound": "fp32", "achieved": round(ach, 3), "unit": "TFLOP/s",
+                                "frac": round(ach / fp32, 4), "algorithmic_flops": int(amount)}
+    dom = max(phase_rows, key=lambda k: phase_rows[k]["ms"])
+    dr = phase_rows[dom]
+    t_roof = 0.0
+    for name, row in phase_rows.items():
+        if row["bound"] == "hbm":
+            t_roof += row["algorithmic_bytes"] / (hbm_peak * 1e9)
+        else:
+            t_roof += row["algorithmic_flops"] / (fp32 * 1e12)
+    roofline = {
+        "kernel": dom,
+        "bound": dr["bound"],
+        "achieved": dr["achieved"],
+        "peak": round(hbm_peak if dr["bound"] == "hbm" else fp32, 2),
+        "peak_source": hbm_src if dr["bound"] == "hbm" else "lgs_measure_fp32_peak (FFMA microbenchmark, this box)",
+        "unit": dr["unit"],
+        "frac": dr["frac"],
+        "traffic": None,
+        "step_t_roof_ms": round(t_roof * 1e3, 4),
+        "step_frac": round(t_roof * 1e3 / ms_max, 4),
+        "phases": phase_rows,
+    }
+
+    result = {
+        "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": round(ms_max, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded; BASELINE configs[1] distributions at 500k; no dataset ships with the reference)",
+        "config": {"workload": args.config, "image": f"{cam['width']}x{cam['height']}", "gaussians": n,
+                   "sh_degree": int(math.isqrt(K) - 1), "feature_dim": d, "views_per_gpu_per_step": 1,
+                   "loss": "L1 rgb+depth+feat (fused)", "pose_grad": True,
+                   "parallelism": f"views over {world} GPU(s), NCCL all-reduce of fp32 grads" if world > 1 else "1 GPU",
+                   "l2": "512 MiB L2 flush before every timed step"},
+        "clocks": clk.summary(),
+        "gpu_launches": int(launches),
+        "roofline": roofline,
+        "work": {"visible": V, "pairs": P, "evaluated": evaluated, "contributed": contributed,
+                 "max_tile_list": st["max_tile_list"]},
+        "per_step_ms": [round(x, 4) for x in per_step],
+    }
+
+    # ---- end to end through the public API with host buffers -----------------------------------
+    if not args.no_e2e:
+        result["e2e"] = run_e2e(args, scene, cam, tg, R, local)
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        result["cpu_baseline"] = cpu_baseline(scene, cam, tg, args)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+
+
+def pinned_like(a):
+    import torch
+    t = torch.empty(a.shape, dtype=torch.float32, pin_memory=True)
+    t.numpy()[...] = a
+    return t.numpy()
+
+
+def run_e2e(args, scene, cam, tg, R, device):
+    """Same step through the reference-facing API with HOST buffers: every step uploads the map
+    and targets (H2D), renders, reads back the images, the gradients and the loss (D2H)."""
+    import numpy as np
+    import torch
+
+    hscene = {k: pinned_like(v) for k, v in scene.items()}
+    htg = {k: pinned_like(v) for k, v in tg.items()}
+    H, W = cam["height"], cam["width"]
+    d = scene["feat"].shape[0]
+    n = scene["pos"].shape[0]
+    K = scene["sh"].shape[1]
+    himg = {"rgb": pinned_like(np.zeros((H, W, 3), np.float32)), "depth": pinned_like(np.zeros((H, W), np.float32)),
+            "feat": pinned_like(np.zeros((H, W, d), np.float32)), "acc": pinned_like(np.zeros((H, W), np.float32))}
+    total = n * (11 + 3 * K + d)
+    hflat = pinned_like(np.zeros(total, np.float32))
+    hgrads = R.alloc_grads(n, d, K, flat=hflat)
+    ctx = R.Context(device)
+
+    def step():
+        out = R.render(hscene, cam, targets=htg, ctx=ctx, out=himg)
+        g = R.render_backward_l1(out, pose=True, into=hgrads)
+        return out.l1_loss(), g
+
+    for _ in range(2):
+        step()
+    torch.cuda.synchronize()
+    times = []
+    for _ in range(args.e2e_steps):
+        t0 = time.perf_counter()
+        step()
+        times.append(time.perf_counter() - t0)
+    ms = 1e3 * sum(times) / len(times)
+    h2d = sum(v.nbytes for v in hscene.values()) + sum(v.nbytes for v in htg.values())
+    d2h = sum(v.nbytes for v in himg.values()) + hflat.nbytes + 6 * 4 + 8
+    return {"value": round(1000.0 / ms, 3), "unit": UNIT, "ms_per_step": round(ms, 3), "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "api": "renderer.render(host numpy map) + render_backward_l1(host grads)"}
+
+
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def reference_step(scene, cam, tg, threads):
+    """One full fwd+bwd of the reference algorithm (oracle A: fp64, global sort, per-pixel
+    contributor lists -- renderer.cpp:94-356) with the L1 cotangents, on `threads` row bands."""
+    from oracle import oracle as orc
+    t0 = time.perf_counter()
+    out = orc.fwd_bwd_bands(scene, cam, None, None, None, threads=threads, targets=tg)
+    return time.perf_counter() - t0, out
+
+
+def cpu_baseline(scene, cam, tg, args):
+    threads = cpu_threads()
+    secs, _ = reference_step(scene, cam, tg, threads)
+    return {"value": round(1.0 / secs, 4), "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"1 full fwd+bwd step of the headline workload (oracle A, fp64 reference algorithm) on "
+                      f"{threads} row bands, {secs:.2f} s"}
+
+
+def run_reference(args):
+    """--impl reference: the reference's CPU algorithm (oracle A port; the reference itself cannot
+    be built here) on all host cores, same metric / config."""
+    rank, world, local = dist_env()
+    if rank != 0:
+        return
+    from paper_2511_16144_b200 import scenes
+    scene, cams, info = scenes.make_config(args.config)
+    cam = cams[0]
+    d = scene["feat"].shape[0]
+    tg = scenes.make_targets(cam, d, info["depth_range"], 7)
+    threads = cpu_threads()
+    warm = 1  # one untimed step (page-in, allocator); each CPU step is seconds long
+    for _ in range(warm):
+        reference_step(scene, cam, tg, threads)
+    steps = max(1, min(args.steps, 5))
+    times = [reference_step(scene, cam, tg, threads)[0] for _ in range(steps)]
+    ms = 1e3 * sum(times) / len(times)
+    v = 1000.0 / ms
+    res = {"metric": METRIC, "value": round(v, 4), "unit": UNIT, "n_gpus": world, "steps": steps, "warmup": warm,
+           "ms_per_step": round(ms, 2), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "dtype": "f64", "data": "synthetic (seeded, same as --impl ours)", "impl": "reference",
+           "config": {"workload": args.config, "image": f"{cam['width']}x{cam['height']}",
+                      "gaussians": int(scene['pos'].shape[0])},
+           "cpu_baseline": {"value": round(v, 4), "unit": UNIT, "cores": threads, "kind": "port",
+                            "sample": f"{steps} full fwd+bwd steps (after {warm} warm-up) of oracle A on {threads} "
+                                      f"row bands; requested --steps {args.steps} capped at 5 to bound CPU time"},
+           "e2e": {"value": round(v, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(res), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -218,6 +218,24 @@ LGS_API int64_t lgs_grads_flat_size(int64_t n, int32_t feature_dim, int32_t sh_d
 /* Kernel launches issued by this context since creation (for bench bookkeeping). */
 LGS_API int64_t lgs_ctx_launch_count(const lgs_ctx* ctx);
 
+/* ---- phase profiling (CUDA events recorded on the context stream around each phase) -------
+ * Phases: 0 preprocess, 1 depth sort + scan, 2 key duplication, 3 tile sort + ranges,
+ * 4 blend forward, 5 blend backward, 6 preprocess backward, 7 map upload (pack). */
+enum { LGS_PHASE_COUNT = 8 };
+LGS_API const char* lgs_phase_name(int32_t phase);
+LGS_API lgs_status lgs_ctx_profile(lgs_ctx* ctx, int32_t enable);
+/* Accumulated device milliseconds and launch counts per phase since the last reset
+ * (synchronizes on the recorded events). */
+LGS_API lgs_status lgs_ctx_phase_times(lgs_ctx* ctx, double* ms, int64_t* counts, int32_t reset);
+
+/* Work counters of a forward: (pixel, Gaussian) pairs that reached the alpha test and pairs
+ * that contributed (the reference's pixel_contribs entries, renderer.cpp:157).  Synchronizes. */
+LGS_API lgs_status lgs_saved_work(const lgs_saved* tape, int64_t* evaluated, int64_t* contributed);
+
+/* Measured FP32 FFMA throughput of `device` (TFLOP/s): the roofline denominator of the blend
+ * kernels.  Runs a ~10 ms microbenchmark on the legacy stream; call outside timed regions. */
+LGS_API lgs_status lgs_measure_fp32_peak(int32_t device, double* tflops);
+
 #ifdef __cplusplus
 }
 #endif

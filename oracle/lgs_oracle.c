@@ -812,15 +812,52 @@ typedef struct {
   int32_t win[4];
   double *rgb, *depth, *feat, *acc;
   const double *g_rgb, *g_depth, *g_feat;
+  const double *t_rgb, *t_depth, *t_feat; /* EXT: L1 targets (cotangents computed per band) */
   double *o_pos, *o_rot, *o_logs, *o_opac, *o_sh, *o_feat, pose[6];
+  double loss;
 } band_job;
 
 static void* band_worker(void* arg) {
   band_job* j = (band_job*)arg;
   orc_render* R = orc_render_forward(j->m, j->cam, j->cfg, NULL, j->win, j->rgb, j->depth, j->feat, j->acc);
-  orc_render_backward(R, j->g_rgb, j->g_depth, j->g_feat, j->o_pos, j->o_rot, j->o_logs, j->o_opac, j->o_sh,
-                      j->o_feat, j->pose);
+  const double *g_rgb = j->g_rgb, *g_depth = j->g_depth, *g_feat = j->g_feat;
+  double* cot = NULL;
+  if (j->t_rgb) {
+    /* EXT (SURVEY.md §8d loss): L = mean|rgb-T| + mean|depth-T| + mean|feat-T|, cotangent
+     * sign(diff)/count, computed per pixel of this band from its own forward output. */
+    const int W = j->cam->width, H = j->cam->height, d = j->m->d;
+    const size_t npix = (size_t)W * H;
+    cot = (double*)calloc(npix * (size_t)(4 + d), sizeof(double));
+    double* cr = cot;
+    double* cd = cot + npix * 3;
+    double* cf = cot + npix * 4;
+    const double nr = 3.0 * (double)npix, nd = (double)npix, nf = (double)d * (double)npix;
+    double loss = 0.0;
+    for (int y = j->win[1]; y < j->win[3]; ++y)
+      for (int x = j->win[0]; x < j->win[2]; ++x) {
+        const size_t p = (size_t)y * W + x;
+        for (int c = 0; c < 3; ++c) {
+          const double df = j->rgb[p * 3 + c] - j->t_rgb[p * 3 + c];
+          cr[p * 3 + c] = df > 0 ? 1.0 / nr : (df < 0 ? -1.0 / nr : 0.0);
+          loss += fabs(df) / nr;
+        }
+        const double dd = j->depth[p] - j->t_depth[p];
+        cd[p] = dd > 0 ? 1.0 / nd : (dd < 0 ? -1.0 / nd : 0.0);
+        loss += fabs(dd) / nd;
+        for (int c = 0; c < d; ++c) {
+          const double df = j->feat[p * d + c] - j->t_feat[p * d + c];
+          cf[p * d + c] = df > 0 ? 1.0 / nf : (df < 0 ? -1.0 / nf : 0.0);
+          loss += fabs(df) / nf;
+        }
+      }
+    (void)H;
+    j->loss = loss;
+    g_rgb = cr; g_depth = cd; g_feat = d > 0 ? cf : NULL;
+  }
+  orc_render_backward(R, g_rgb, g_depth, g_feat, j->o_pos, j->o_rot, j->o_logs, j->o_opac, j->o_sh, j->o_feat,
+                      j->pose);
   orc_render_free(R);
+  free(cot);
   return NULL;
 }
 
@@ -830,7 +867,8 @@ ORC_API int orc_fwd_bwd_bands(const orc_map* m, const orc_camera* cam, const orc
                               int32_t row_hi, int32_t threads, const double* g_rgb, const double* g_depth,
                               const double* g_feat, double* rgb, double* depth, double* feat, double* acc,
                               double* o_pos, double* o_rot, double* o_logs, double* o_opac, double* o_sh,
-                              double* o_feat, double* pose6) {
+                              double* o_feat, double* pose6, const double* t_rgb, const double* t_depth,
+                              const double* t_feat, double* loss) {
   if (threads < 1) threads = 1;
   const int W = cam->width, H = cam->height, d = m->d;
   const int K = sh_coeffs(m->sh_degree);
@@ -850,6 +888,7 @@ ORC_API int orc_fwd_bwd_bands(const orc_map* m, const orc_camera* cam, const orc
     j->feat = (double*)malloc(sizeof(double) * npix * (size_t)(d > 0 ? d : 1));
     j->acc = (double*)malloc(sizeof(double) * npix);
     j->g_rgb = g_rgb; j->g_depth = g_depth; j->g_feat = g_feat;
+    j->t_rgb = t_rgb; j->t_depth = t_depth; j->t_feat = t_feat;
     j->o_pos = (double*)malloc(sizeof(double) * (size_t)n * 3);
     j->o_rot = (double*)malloc(sizeof(double) * (size_t)n * 4);
     j->o_logs = (double*)malloc(sizeof(double) * (size_t)n * 3);
@@ -865,6 +904,7 @@ ORC_API int orc_fwd_bwd_bands(const orc_map* m, const orc_camera* cam, const orc
   memset(o_sh, 0, sizeof(double) * (size_t)n * K * 3);
   if (d > 0) memset(o_feat, 0, sizeof(double) * (size_t)n * d);
   if (pose6) memset(pose6, 0, sizeof(double) * 6);
+  if (loss) *loss = 0.0;
   for (int t = 0; t < threads; ++t) {
     pthread_join(th[t], NULL);
     band_job* j = &jobs[t];
@@ -880,6 +920,7 @@ ORC_API int orc_fwd_bwd_bands(const orc_map* m, const orc_camera* cam, const orc
     for (int64_t i = 0; i < n * d; ++i) o_feat[i] += j->o_feat[i];
     if (pose6)
       for (int a = 0; a < 6; ++a) pose6[a] += j->pose[a];
+    if (loss) *loss += j->loss;
     free(j->rgb); free(j->depth); free(j->feat); free(j->acc);
     free(j->o_pos); free(j->o_rot); free(j->o_logs); free(j->o_opac); free(j->o_sh); free(j->o_feat);
   }

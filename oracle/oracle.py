@@ -92,7 +92,7 @@ def lib():
         L.orc_fwd_bwd_bands.restype = C.c_int
         L.orc_fwd_bwd_bands.argtypes = [C.POINTER(OrcMap), C.POINTER(OrcCamera), C.POINTER(OrcConfig), C.c_int32,
                                         C.c_int32, C.c_int32, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp,
-                                        _dp, _dp, _dp, _dp]
+                                        _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp]
         L.orc_expf_export.restype = C.c_float
         L.orc_expf_export.argtypes = [C.c_float]
         L.orc32_camera_setup.argtypes = [C.POINTER(OrcCamera), C.POINTER(OrcConfig), C.POINTER(Orc32Cam)]
@@ -299,8 +299,11 @@ def perturb_pose(cam, xi):
     return c2
 
 
-def fwd_bwd_bands(scene, cam, g_rgb, g_depth, g_feat, threads, rows=None, cfg=None):
-    """All-cores reference fwd+bwd over image rows [lo, hi) (EXT, see lgs_oracle.c)."""
+def fwd_bwd_bands(scene, cam, g_rgb, g_depth, g_feat, threads, rows=None, cfg=None, targets=None):
+    """All-cores reference fwd+bwd over image rows [lo, hi) (EXT, see lgs_oracle.c).
+
+    With ``targets`` (dict rgb/depth/feat) the cotangents are the L1-loss ones computed per band
+    from the band's own forward output (g_* are then ignored) and ``loss`` is returned."""
     L = lib()
     m, s = _scene64(scene)
     c = make_camera(cam)
@@ -313,9 +316,15 @@ def fwd_bwd_bands(scene, cam, g_rgb, g_depth, g_feat, threads, rows=None, cfg=No
                log_scale=np.zeros((n, 3)), opacity_logit=np.zeros(n), sh=np.zeros((n, K, 3)),
                feature=np.zeros((max(d, 1), n)), pose=np.zeros(6))
     g = [None if x is None else np.ascontiguousarray(x, dtype=np.float64) for x in (g_rgb, g_depth, g_feat)]
+    t = [None, None, None]
+    if targets is not None:
+        t = [np.ascontiguousarray(targets[k], dtype=np.float64) for k in ("rgb", "depth", "feat")]
+    loss = np.zeros(1)
     L.orc_fwd_bwd_bands(C.byref(m), C.byref(c), C.byref(cfg), lo, hi, threads, *(_ptr(x, _dp) for x in g),
                         *(_ptr(out[k], _dp) for k in ("rgb", "depth", "feat", "acc", "position", "rotation",
-                                                       "log_scale", "opacity_logit", "sh", "feature", "pose")))
+                                                       "log_scale", "opacity_logit", "sh", "feature", "pose")),
+                        *(_ptr(x, _dp) for x in t), _ptr(loss, _dp))
+    out["loss"] = float(loss[0])
     return out
 
 

@@ -85,7 +85,14 @@ SIGNATURES = [
     ("lgs_debug_tile_keys", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     ("lgs_debug_pixel_state", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     ("lgs_grads_flat_size", C.c_int64, [C.c_int64, C.c_int32, C.c_int32]),
+    ("lgs_phase_name", C.c_char_p, [C.c_int32]),
+    ("lgs_ctx_profile", C.c_int, [C.c_void_p, C.c_int32]),
+    ("lgs_ctx_phase_times", C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int64), C.c_int32]),
+    ("lgs_saved_work", C.c_int, [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    ("lgs_measure_fp32_peak", C.c_int, [C.c_int32, C.POINTER(C.c_double)]),
 ]
+
+LGS_PHASE_COUNT = 8
 
 _lib = None
 

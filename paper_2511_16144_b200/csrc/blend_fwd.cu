@@ -47,6 +47,7 @@ __global__ void __launch_bounds__(kBlock) blend_fwd_kernel(DevMap m, DevCam c, V
 #pragma unroll
   for (int k = 0; k < (DP > 0 ? DP : 1); ++k) f[k] = 0.f;
   uint32_t last = 0;
+  uint32_t n_eval = 0, n_contrib = 0;
   bool done = !inside || !(1.0f >= c.t_min);
 
   for (uint32_t base = range.x; base < range.y; base += kBlock) {
@@ -72,7 +73,9 @@ __global__ void __launch_bounds__(kBlock) blend_fwd_kernel(DevMap m, DevCam c, V
       const float4 r1 = sm.r1[k];
       float dx, dy, G;
       float alpha = splat_alpha(r0.x, r0.y, r1.x, r1.y, r1.z, r0.w, fpx, fpy, dx, dy, G);
+      ++n_eval;
       if (!(alpha >= c.alpha_skip)) continue;
+      ++n_contrib;
       alpha = fminf(alpha, c.alpha_clamp);
       const float w = __fmul_rn(alpha, T);
       const float4 col = sm.col[k];
@@ -105,6 +108,7 @@ __global__ void __launch_bounds__(kBlock) blend_fwd_kernel(DevMap m, DevCam c, V
     ps.n_contrib[pix] = last;
     ps.depth[pix] = dnorm;
     ps.acc[pix] = acc;
+    ps.work[pix] = make_uint2(n_eval, n_contrib);
     if (o.rgb) {
       o.rgb[pix * 3 + 0] = cr;
       o.rgb[pix * 3 + 1] = cg;

@@ -67,6 +67,11 @@ int bits_for(int ntiles) {
 
 }  // namespace
 
+struct PhaseMark {
+  int phase;
+  cudaEvent_t a, b;
+};
+
 struct lgs_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -74,7 +79,49 @@ struct lgs_ctx {
   std::atomic<int> refs{1};
   std::atomic<int64_t> launches{0};
   uint32_t* host_u32 = nullptr;  // pinned scalar readback
+  // phase profiling
+  bool profiling = false;
+  std::vector<PhaseMark> marks;
+  std::vector<cudaEvent_t> event_pool;
+  double phase_ms[LGS_PHASE_COUNT] = {};
+  int64_t phase_n[LGS_PHASE_COUNT] = {};
 };
+
+namespace {
+
+// RAII phase marker: records an event pair around a phase when profiling is on.
+struct PhaseScope {
+  lgs_ctx* ctx;
+  PhaseMark m{};
+  bool on;
+  cudaEvent_t take() {
+    if (!ctx->event_pool.empty()) {
+      cudaEvent_t e = ctx->event_pool.back();
+      ctx->event_pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+  PhaseScope(lgs_ctx* c, int phase) : ctx(c), on(c->profiling) {
+    if (!on) return;
+    m.phase = phase;
+    m.a = take();
+    m.b = take();
+    cudaEventRecord(m.a, ctx->stream);
+  }
+  ~PhaseScope() {
+    if (!on) return;
+    cudaEventRecord(m.b, ctx->stream);
+    ctx->marks.push_back(m);
+  }
+};
+
+enum { PH_PREPROCESS = 0, PH_DEPTH_SORT, PH_DUPLICATE, PH_TILE_SORT, PH_BLEND_FWD, PH_BLEND_BWD, PH_PREPROCESS_BWD,
+       PH_UPLOAD };
+
+}  // namespace
 
 struct lgs_map {
   lgs_ctx* ctx = nullptr;
@@ -110,6 +157,11 @@ void ctx_release(lgs_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     if (ctx->host_u32) cudaFreeHost(ctx->host_u32);
+    for (auto& m : ctx->marks) {
+      cudaEventDestroy(m.a);
+      cudaEventDestroy(m.b);
+    }
+    for (auto e : ctx->event_pool) cudaEventDestroy(e);
     delete ctx;
   }
 }
@@ -198,7 +250,10 @@ lgs_status map_upload(lgs_ctx* ctx, lgs_map* m, const lgs_gaussians* src) {
     LGS_TRY(copy_in(ctx, p, src->opacity_logits, sizeof(float) * n, LGS_MEM_HOST)); op = p; p += n;
     if (d > 0) { LGS_TRY(copy_in(ctx, p, src->features, sizeof(float) * n * d, LGS_MEM_HOST)); ft = p; }
   }
-  launch_pack_map(pos, rot, ls, op, ft, n, d, m->dm.dp, m->pos_opa, m->rot, m->scale, m->feat, ctx->stream);
+  {
+    PhaseScope ph(ctx, PH_UPLOAD);
+    launch_pack_map(pos, rot, ls, op, ft, n, d, m->dm.dp, m->pos_opa, m->rot, m->scale, m->feat, ctx->stream);
+  }
   ctx->launches++;
   if (stage) dfree(ctx, stage);
   LGS_CUDA(cudaGetLastError());
@@ -248,6 +303,7 @@ void free_saved(lgs_saved* t) {
   dfree(ctx, t->ps.n_contrib);
   dfree(ctx, t->ps.depth);
   dfree(ctx, t->ps.acc);
+  dfree(ctx, t->ps.work);
   dfree(ctx, t->cot);
   dfree(ctx, t->loss);
   if (t->owned_map) free_map(t->owned_map);
@@ -452,9 +508,13 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
   TRYB(dalloc(ctx, &t->ps.n_contrib, npix));
   TRYB(dalloc(ctx, &t->ps.depth, npix));
   TRYB(dalloc(ctx, &t->ps.acc, npix));
+  TRYB(dalloc(ctx, &t->ps.work, npix));
 
   // K1
-  launch_preprocess(map->dm, dc, t->vb, s);
+  {
+    PhaseScope ph(ctx, PH_PREPROCESS);
+    launch_preprocess(map->dm, dc, t->vb, s);
+  }
   ctx->launches++;
 
   // depth sort + scan
@@ -466,8 +526,11 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
   TRYB(dalloc(ctx, &idx_sorted, n));
   TRYB(dalloc(ctx, &incl, n));
   TRYB(dalloc(ctx, reinterpret_cast<uint8_t**>(&temp), temp_bytes));
-  launch_depth_sort(t->vb, n, dkey_sorted, idx_sorted, temp, temp_bytes, s);
-  launch_scan_tiles(t->vb.tiles, idx_sorted, n, dkey_sorted, incl, temp, temp_bytes, s);
+  {
+    PhaseScope ph(ctx, PH_DEPTH_SORT);
+    launch_depth_sort(t->vb, n, dkey_sorted, idx_sorted, temp, temp_bytes, s);
+    launch_scan_tiles(t->vb.tiles, idx_sorted, n, dkey_sorted, incl, temp, temp_bytes, s);
+  }
   ctx->launches += n > 0 ? 6 : 0;
   int64_t P = 0;
   if (n > 0) {
@@ -482,15 +545,21 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
   TRYB(dalloc(ctx, &vals_in, P));
   TRYB(dalloc(ctx, &t->keys, P));
   TRYB(dalloc(ctx, &t->vals, P));
-  launch_duplicate(t->vb, idx_sorted, incl, n, dc.tiles_x, keys_in, vals_in, s);
+  {
+    PhaseScope ph(ctx, PH_DUPLICATE);
+    launch_duplicate(t->vb, idx_sorted, incl, n, dc.tiles_x, keys_in, vals_in, s);
+  }
   const size_t sort_bytes = binning_temp_bytes(0, P, tile_bits);
   if (sort_bytes > temp_bytes) {
     dfree(ctx, temp);
     temp_bytes = sort_bytes;
     TRYB(dalloc(ctx, reinterpret_cast<uint8_t**>(&temp), temp_bytes));
   }
-  launch_tile_sort(keys_in, t->keys, vals_in, t->vals, P, tile_bits, temp, temp_bytes, s);
-  launch_ranges(t->keys, P, ntiles, t->ranges, s);
+  {
+    PhaseScope ph(ctx, PH_TILE_SORT);
+    launch_tile_sort(keys_in, t->keys, vals_in, t->vals, P, tile_bits, temp, temp_bytes, s);
+    launch_ranges(t->keys, P, ntiles, t->ranges, s);
+  }
   ctx->launches += (n > 0 ? 1 : 0) + (P > 0 ? 5 : 0);
   dfree(ctx, keys_in);
   dfree(ctx, vals_in);
@@ -532,7 +601,10 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
     fo.cot = t->cot;
     fo.loss = t->loss;
   }
-  launch_blend_fwd(map->dm, dc, t->vb, TileLists{t->vals, t->ranges}, t->ps, fo, s);
+  {
+    PhaseScope ph(ctx, PH_BLEND_FWD);
+    launch_blend_fwd(map->dm, dc, t->vb, TileLists{t->vals, t->ranges}, t->ps, fo, s);
+  }
   ctx->launches++;
   CUDAB(cudaGetLastError());
   if (tstage) dfree(ctx, tstage);
@@ -583,7 +655,10 @@ lgs_status run_backward(lgs_ctx* ctx, const lgs_saved* t, const BwdIn& in_dev, l
   float* gacc = nullptr;
   LGS_TRY(dalloc(ctx, &gacc, (size_t)n * slots));
   LGS_CUDA(cudaMemsetAsync(gacc, 0, sizeof(float) * (size_t)n * slots, s));
-  launch_blend_bwd(t->dm, t->cam, t->vb, TileLists{t->vals, t->ranges}, t->ps, in_dev, gacc, slots, s);
+  {
+    PhaseScope ph(ctx, PH_BLEND_BWD);
+    launch_blend_bwd(t->dm, t->cam, t->vb, TileLists{t->vals, t->ranges}, t->ps, in_dev, gacc, slots, s);
+  }
   ctx->launches += 2;
 
   GradOut go{};
@@ -618,7 +693,10 @@ lgs_status run_backward(lgs_ctx* ctx, const lgs_saved* t, const BwdIn& in_dev, l
     LGS_CUDA(cudaMemsetAsync(dpose, 0, sizeof(double) * 6, s));
     go.pose = dpose;
   }
-  launch_preprocess_bwd(t->dm, t->cam, t->vb, gacc, slots, go, s);
+  {
+    PhaseScope ph(ctx, PH_PREPROCESS_BWD);
+    launch_preprocess_bwd(t->dm, t->cam, t->vb, gacc, slots, go, s);
+  }
   ctx->launches++;
   LGS_CUDA(cudaGetLastError());
   if (host) {
@@ -728,6 +806,59 @@ LGS_API lgs_status lgs_saved_stats(const lgs_saved* tape, lgs_render_stats* st) 
   st->pairs = tape->pairs;
   st->tiles = tape->ntiles;
   st->max_tile_list = mx;
+  return LGS_OK;
+}
+
+LGS_API lgs_status lgs_saved_work(const lgs_saved* tape, int64_t* evaluated, int64_t* contributed) {
+  if (!tape) return fail(LGS_EINVAL, "NULL argument");
+  lgs_ctx* ctx = tape->ctx;
+  LGS_CUDA(cudaSetDevice(ctx->device));
+  std::vector<uint2> w((size_t)tape->cam.W * tape->cam.H);
+  LGS_CUDA(cudaMemcpyAsync(w.data(), tape->ps.work, sizeof(uint2) * w.size(), cudaMemcpyDeviceToHost, ctx->stream));
+  LGS_CUDA(cudaStreamSynchronize(ctx->stream));
+  int64_t e = 0, c = 0;
+  for (const uint2& x : w) {
+    e += x.x;
+    c += x.y;
+  }
+  if (evaluated) *evaluated = e;
+  if (contributed) *contributed = c;
+  return LGS_OK;
+}
+
+LGS_API const char* lgs_phase_name(int32_t phase) {
+  static const char* names[LGS_PHASE_COUNT] = {"preprocess", "depth_sort_scan", "duplicate_keys", "tile_sort_ranges",
+                                               "blend_fwd", "blend_bwd", "preprocess_bwd", "map_upload"};
+  return (phase >= 0 && phase < LGS_PHASE_COUNT) ? names[phase] : "?";
+}
+
+LGS_API lgs_status lgs_ctx_profile(lgs_ctx* ctx, int32_t enable) {
+  if (!ctx) return fail(LGS_EINVAL, "ctx is NULL");
+  ctx->profiling = enable != 0;
+  return LGS_OK;
+}
+
+LGS_API lgs_status lgs_ctx_phase_times(lgs_ctx* ctx, double* ms, int64_t* counts, int32_t reset) {
+  if (!ctx) return fail(LGS_EINVAL, "ctx is NULL");
+  LGS_CUDA(cudaSetDevice(ctx->device));
+  for (auto& m : ctx->marks) {
+    LGS_CUDA(cudaEventSynchronize(m.b));
+    float t = 0.f;
+    LGS_CUDA(cudaEventElapsedTime(&t, m.a, m.b));
+    ctx->phase_ms[m.phase] += t;
+    ctx->phase_n[m.phase] += 1;
+    ctx->event_pool.push_back(m.a);
+    ctx->event_pool.push_back(m.b);
+  }
+  ctx->marks.clear();
+  for (int i = 0; i < LGS_PHASE_COUNT; ++i) {
+    if (ms) ms[i] = ctx->phase_ms[i];
+    if (counts) counts[i] = ctx->phase_n[i];
+    if (reset) {
+      ctx->phase_ms[i] = 0.0;
+      ctx->phase_n[i] = 0;
+    }
+  }
   return LGS_OK;
 }
 

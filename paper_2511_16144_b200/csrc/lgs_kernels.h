@@ -33,6 +33,7 @@ struct PixelState {
   uint32_t* n_contrib; // list position (relative to the tile begin) after the last contributor
   float* depth;        // normalized depth (renderer.cpp:163-165), read by the backward
   float* acc;          // accumulated alpha
+  uint2* work;         // per pixel: (evaluated pairs, contributing pairs)
 };
 
 struct FwdOut {

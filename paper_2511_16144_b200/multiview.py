@@ -1,0 +1,76 @@
+"""Multi-keyframe mapping batches sharded one view per GPU (BASELINE configs 3-4).
+
+The Gaussian map is replicated on every rank; each rank renders its views forward + backward and
+accumulates the per-Gaussian fp32 gradients of all of its views into ONE flat buffer
+(lgs_map_grads with accumulate = 1); a single all-reduce (sum) over NCCL / NVLink then produces
+the batch gradient on every rank.  The gradient is a sum over pixels of all views, so any
+partition of the views is valid and the same all-reduce sums it.
+
+The reference has no multi-view or distributed path at all (it is single-threaded CPU code,
+SURVEY.md §2 "Parallelism strategies"); this module is the B200-side extension named in
+BASELINE.json configs 3-4.
+"""
+from __future__ import annotations
+
+from typing import Callable, Sequence
+
+
+def assign_views(n_views: int, world: int, rank: int, costs: Sequence[float] | None = None) -> list[int]:
+    """Views owned by ``rank``.  Without costs: round-robin.  With per-view cost estimates (e.g. the
+    pair counts P of a previous step): deterministic longest-processing-time-first greedy, which
+    bounds the slowest rank at 4/3 of optimal -- the imbalance, not the all-reduce, is what limits
+    8-GPU efficiency on the multi-view configs (SURVEY.md §7 hard part 7)."""
+    if world < 1 or not (0 <= rank < world):
+        raise ValueError("bad rank/world")
+    if costs is None:
+        return [v for v in range(n_views) if v % world == rank]
+    if len(costs) != n_views:
+        raise ValueError("one cost per view")
+    order = sorted(range(n_views), key=lambda v: (-float(costs[v]), v))
+    load = [0.0] * world
+    owner = [0] * n_views
+    for v in order:
+        r = min(range(world), key=lambda q: (load[q], q))
+        owner[v] = r
+        load[r] += float(costs[v])
+    return [v for v in range(n_views) if owner[v] == rank]
+
+
+class MultiViewStep:
+    """One data-parallel mapping step: local views fwd+bwd into a flat gradient, then all-reduce.
+
+    ``view_grads(view, grads, accumulate)`` renders one view and adds its gradients into ``grads``
+    (the rasterizer path below, or any callable with that contract -- the CPU gloo tests plug in
+    the oracle to exercise the sharding / reduction logic without a GPU).
+    """
+
+    def __init__(self, views: Sequence[int], view_grads: Callable, grads: dict, group=None):
+        self.views = list(views)
+        self.view_grads = view_grads
+        self.grads = grads
+        self.group = group
+
+    def step(self):
+        import torch.distributed as dist
+
+        flat = self.grads["flat"]
+        flat.zero_()
+        for v in self.views:
+            self.view_grads(v, self.grads, True)
+        if dist.is_available() and dist.is_initialized() and dist.get_world_size(self.group) > 1:
+            dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=self.group)
+        return self.grads
+
+
+def rasterizer_view_grads(dmap, cams, targets, ctx=None, pose_out: dict | None = None):
+    """view_grads callable backed by the sm_100a rasterizer (fused L1 loss per view)."""
+    from . import renderer as R
+
+    def fn(v, grads, accumulate):
+        out = R.render(dmap, cams[v], targets=targets[v], ctx=ctx)
+        g = R.render_backward_l1(out, pose=pose_out is not None, into=grads, accumulate=accumulate)
+        if pose_out is not None:
+            pose_out[v] = g.pop("pose")
+        return out
+
+    return fn

@@ -84,6 +84,9 @@ def make_camera(cam) -> _lib.LgsCamera:
     return c
 
 
+CUDA_STREAM_LEGACY = 0x1  # cudaStreamLegacy
+
+
 class Context:
     """One CUDA stream + stream-ordered memory pool (lgs_ctx).  By default the library enqueues on
     torch's current stream so torch tensors and library calls stay ordered."""
@@ -93,6 +96,8 @@ class Context:
         if stream is None and torch is not None and torch.cuda.is_available():
             with torch.cuda.device(device):
                 stream = torch.cuda.current_stream(device).cuda_stream
+            if stream == 0:
+                stream = CUDA_STREAM_LEGACY  # torch's default stream is the legacy NULL stream
         h = C.c_void_p()
         check(L.lgs_ctx_create(device, C.c_void_p(stream) if stream else None, C.byref(h)))
         self.h = h
@@ -104,6 +109,17 @@ class Context:
     @property
     def launches(self) -> int:
         return int(_lib.load().lgs_ctx_launch_count(self.h))
+
+    def profile(self, enable: bool = True):
+        check(_lib.load().lgs_ctx_profile(self.h, 1 if enable else 0))
+
+    def phase_times(self, reset: bool = True) -> dict:
+        """{phase name: (device ms accumulated, launches)} from the CUDA events around each phase."""
+        L = _lib.load()
+        ms = (C.c_double * _lib.LGS_PHASE_COUNT)()
+        cnt = (C.c_int64 * _lib.LGS_PHASE_COUNT)()
+        check(L.lgs_ctx_phase_times(self.h, ms, cnt, 1 if reset else 0))
+        return {L.lgs_phase_name(i).decode(): (ms[i], cnt[i]) for i in range(_lib.LGS_PHASE_COUNT)}
 
     def __del__(self):
         if getattr(self, "h", None) and _lib._lib is not None:
@@ -170,6 +186,12 @@ class RenderOutput:
         s = _lib.LgsRenderStats()
         check(_lib.load().lgs_saved_stats(self.tape, C.byref(s)))
         return dict(visible=s.visible, pairs=s.pairs, tiles=s.tiles, max_tile_list=s.max_tile_list)
+
+    def work(self):
+        """(evaluated (pixel, Gaussian) pairs, contributing pairs) of this forward."""
+        e, c = C.c_int64(), C.c_int64()
+        check(_lib.load().lgs_saved_work(self.tape, C.byref(e), C.byref(c)))
+        return e.value, c.value
 
     def l1_loss(self) -> float:
         v = C.c_double()

@@ -33,7 +33,7 @@ def to_np(x):
 def image_mismatch(gpu, ref, rtol=IMG_RTOL, atol=IMG_ATOL):
     """Fraction of pixels (any channel) outside tolerance, and the max abs error."""
     g = to_np(gpu).astype(np.float64)
-    r = np.asarray(ref, dtype=np.float64)
+    r = to_np(ref).astype(np.float64)
     bad = np.abs(g - r) > atol + rtol * np.abs(r)
     if bad.ndim == 3:
         bad = bad.any(axis=2)
@@ -43,7 +43,7 @@ def image_mismatch(gpu, ref, rtol=IMG_RTOL, atol=IMG_ATOL):
 def grad_mismatch(gpu, ref, rtol=GRAD_RTOL, floor=GRAD_FLOOR):
     """Fraction of components outside tolerance and the worst normalized error."""
     g = to_np(gpu).astype(np.float64).ravel()
-    r = np.asarray(ref, dtype=np.float64).ravel()
+    r = to_np(ref).astype(np.float64).ravel()
     if r.size == 0:
         return 0.0, 0.0
     rms = float(np.sqrt(np.mean(r * r)))
