@@ -52,35 +52,66 @@ void launch_scan_tiles(const uint32_t* tiles, const uint32_t* idx_sorted, int64_
   cub::DeviceScan::InclusiveSum(temp, temp_bytes, scratch, incl, (int)n, s);
 }
 
-// One thread per depth-sorted Gaussian; its pairs are written contiguously at its scan offset,
-// tile ids row-major over the Gaussian's tile rect.
-__global__ void duplicate_kernel(const uint2* __restrict__ rect, const uint32_t* __restrict__ tiles,
-                                 const uint32_t* __restrict__ idx_sorted, const uint32_t* __restrict__ incl,
-                                 int64_t n, int tiles_x, uint16_t* __restrict__ key_out,
-                                 uint32_t* __restrict__ val_out) {
-  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= n) return;
-  const uint32_t g = idx_sorted[s];
-  const uint32_t cnt = tiles[g];
-  if (cnt == 0) return;
-  uint32_t o = incl[s] - cnt;
-  const uint2 r = rect[g];
-  const int tx0 = (int)(r.x & 0xffffu) / kTile, tx1 = (int)(r.x >> 16) / kTile;
-  const int ty0 = (int)(r.y & 0xffffu) / kTile, ty1 = (int)(r.y >> 16) / kTile;
-  for (int ty = ty0; ty <= ty1; ++ty)
-    for (int tx = tx0; tx <= tx1; ++tx) {
-      key_out[o] = (uint16_t)(ty * tiles_x + tx);
-      val_out[o] = g;
-      ++o;
+// Each CTA owns 256 consecutive depth-sorted Gaussians and writes their pairs cooperatively:
+// thread t handles output slots chunk_begin + t, + 256, ... and finds the owning Gaussian by a
+// binary search over the chunk's inclusive offsets in shared memory, so the key/value stores of a
+// warp are consecutive (coalesced) however unevenly the Gaussians' tile counts are spread.  Tile
+// ids run row-major over each Gaussian's tile rect, in depth order.
+constexpr int kDupChunk = 256;
+
+__global__ void __launch_bounds__(kDupChunk) duplicate_kernel(const uint2* __restrict__ rect,
+                                                              const uint32_t* __restrict__ tiles,
+                                                              const uint32_t* __restrict__ idx_sorted,
+                                                              const uint32_t* __restrict__ incl, int64_t n,
+                                                              int tiles_x, uint16_t* __restrict__ key_out,
+                                                              uint32_t* __restrict__ val_out) {
+  __shared__ uint32_t s_end[kDupChunk];
+  __shared__ uint32_t s_g[kDupChunk];
+  __shared__ uint32_t s_rect[kDupChunk];  // tx0 | ty0 << 16
+  __shared__ uint32_t s_w[kDupChunk];     // tile-rect width
+  const int64_t s0 = (int64_t)blockIdx.x * kDupChunk;
+  const int tid = threadIdx.x;
+  __shared__ uint32_t s_begin;
+  const int cnt_items = (int)min((int64_t)kDupChunk, n - s0);
+  if (tid < cnt_items) {
+    const uint32_t g = idx_sorted[s0 + tid];
+    const uint32_t c = tiles[g];
+    const uint2 r = rect[g];
+    const uint32_t tx0 = (r.x & 0xffffu) / kTile, tx1 = (r.x >> 16) / kTile;
+    const uint32_t ty0 = (r.y & 0xffffu) / kTile;
+    s_end[tid] = incl[s0 + tid];
+    s_g[tid] = g;
+    s_rect[tid] = tx0 | (ty0 << 16);
+    s_w[tid] = c ? tx1 - tx0 + 1 : 1;
+  }
+  if (tid == 0) s_begin = incl[s0] - tiles[idx_sorted[s0]];
+  __syncthreads();
+  const uint32_t begin = s_begin;
+  const uint32_t end = s_end[cnt_items - 1];
+  for (uint32_t o = begin + tid; o < end; o += kDupChunk) {
+    // first j with s_end[j] > o
+    int lo = 0, hi = cnt_items - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (s_end[mid] > o) hi = mid;
+      else lo = mid + 1;
     }
+    const uint32_t w = s_w[lo];
+    const uint32_t cnt = (lo == 0 ? s_end[0] - begin : s_end[lo] - s_end[lo - 1]);
+    const uint32_t local = o - (s_end[lo] - cnt);
+    const uint32_t tx = (s_rect[lo] & 0xffffu) + local % w;
+    const uint32_t ty = (s_rect[lo] >> 16) + local / w;
+    key_out[o] = (uint16_t)(ty * (uint32_t)tiles_x + tx);
+    val_out[o] = s_g[lo];
+  }
 }
 
 void launch_duplicate(const ViewBufs& v, const uint32_t* idx_sorted, const uint32_t* incl, int64_t n,
                       int tiles_x, uint16_t* key_out, uint32_t* val_out, cudaStream_t s) {
   if (n == 0) return;
-  const int threads = 256;
-  duplicate_kernel<<<(unsigned)((n + threads - 1) / threads), threads, 0, s>>>(v.rect, v.tiles, idx_sorted, incl,
-                                                                                n, tiles_x, key_out, val_out);
+  duplicate_kernel<<<(unsigned)((n + kDupChunk - 1) / kDupChunk), kDupChunk, 0, s>>>(v.rect, v.tiles, idx_sorted,
+                                                                                      incl, n, tiles_x, key_out,
+                                                                                      val_out);
 }
 
 void launch_tile_sort(uint16_t* keys_in, uint16_t* keys_out, uint32_t* vals_in, uint32_t* vals_out, int64_t pairs,

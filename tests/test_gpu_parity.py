@@ -276,7 +276,7 @@ def test_host_and_device_paths_agree(c0):
     gd = R.render_backward(None, out_d, *(torch.from_numpy(c.astype(np.float32)).cuda() for c in cot))
     gh = R.render_backward(None, out_h, *(c.astype(np.float32) for c in cot))
     for k in GROUPS:
-        frac, worst = grad_mismatch(gd[k], gh[k], rtol=1e-5)
+        frac, worst = grad_mismatch(gd[k], gh[k])  # atomics: summation order differs run to run
         assert frac == 0.0, (k, worst)
 
 
@@ -292,7 +292,7 @@ def test_fused_l1_matches_explicit_cotangents(c0):
     assert out.l1_loss() == pytest.approx(loss, rel=1e-5)
     g2 = R.render_backward(None, out, *(torch.from_numpy(c.astype(np.float32)).cuda() for c in cot), pose=True)
     for k in GROUPS:
-        frac, worst = grad_mismatch(g1[k], g2[k], rtol=1e-5)
+        frac, worst = grad_mismatch(g1[k], g2[k])  # atomics: summation order differs run to run
         assert frac == 0.0, (k, worst)
 
 
@@ -310,7 +310,7 @@ def test_accumulate_sums_views(c0):
         R.render_backward_l1(out, into=acc, accumulate=True)
         singles.append(R.render_backward_l1(R.render(dm, c, targets=dtg)))
     for k in GROUPS:
-        frac, worst = grad_mismatch(acc[k], singles[0][k] + singles[1][k], rtol=1e-4)
+        frac, worst = grad_mismatch(acc[k], singles[0][k] + singles[1][k])
         assert frac == 0.0, (k, worst)
 
 
