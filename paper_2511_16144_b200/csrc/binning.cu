@@ -58,6 +58,7 @@ void launch_scan_tiles(const uint32_t* tiles, const uint32_t* idx_sorted, int64_
 // warp are consecutive (coalesced) however unevenly the Gaussians' tile counts are spread.  Tile
 // ids run row-major over each Gaussian's tile rect, in depth order.
 constexpr int kDupChunk = 256;
+constexpr int kDupRun = 8;
 
 __global__ void __launch_bounds__(kDupChunk) duplicate_kernel(const uint2* __restrict__ rect,
                                                               const uint32_t* __restrict__ tiles,
@@ -88,21 +89,36 @@ __global__ void __launch_bounds__(kDupChunk) duplicate_kernel(const uint2* __res
   __syncthreads();
   const uint32_t begin = s_begin;
   const uint32_t end = s_end[cnt_items - 1];
-  for (uint32_t o = begin + tid; o < end; o += kDupChunk) {
-    // first j with s_end[j] > o
-    int lo = 0, hi = cnt_items - 1;
+  // each thread emits kDupRun consecutive slots: one binary search per run, then an incremental
+  // walk over the (row-major) tile rects -- no per-slot search or integer division
+  for (uint32_t o0 = begin + (uint32_t)tid * kDupRun; o0 < end; o0 += kDupChunk * kDupRun) {
+    int lo = 0, hi = cnt_items - 1;  // first j with s_end[j] > o0
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
-      if (s_end[mid] > o) hi = mid;
+      if (s_end[mid] > o0) hi = mid;
       else lo = mid + 1;
     }
-    const uint32_t w = s_w[lo];
-    const uint32_t cnt = (lo == 0 ? s_end[0] - begin : s_end[lo] - s_end[lo - 1]);
-    const uint32_t local = o - (s_end[lo] - cnt);
-    const uint32_t tx = (s_rect[lo] & 0xffffu) + local % w;
-    const uint32_t ty = (s_rect[lo] >> 16) + local / w;
-    key_out[o] = (uint16_t)(ty * (uint32_t)tiles_x + tx);
-    val_out[o] = s_g[lo];
+    uint32_t w = s_w[lo];
+    uint32_t gstart = lo == 0 ? begin : s_end[lo - 1];
+    uint32_t local = o0 - gstart;
+    uint32_t ly = local / w, lxx = local - ly * w;
+    const uint32_t o1 = min(o0 + kDupRun, end);
+    for (uint32_t o = o0; o < o1; ++o) {
+      if (o == s_end[lo]) {  // next Gaussian (culled ones have no slots and are skipped)
+        do { ++lo; } while (s_end[lo] == o);
+        w = s_w[lo];
+        ly = 0;
+        lxx = 0;
+      }
+      const uint32_t tx = (s_rect[lo] & 0xffffu) + lxx;
+      const uint32_t ty = (s_rect[lo] >> 16) + ly;
+      key_out[o] = (uint16_t)(ty * (uint32_t)tiles_x + tx);
+      val_out[o] = s_g[lo];
+      if (++lxx == w) {
+        lxx = 0;
+        ++ly;
+      }
+    }
   }
 }
 

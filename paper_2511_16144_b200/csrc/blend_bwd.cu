@@ -10,11 +10,17 @@
 //   - dL/dalpha_r = T_r dL/dw_r - (sum_{i>r} dL/dw_i w_i) / (1 - alpha_r) (:256-257);
 //   - colour / feature / depth grads for every contributor (:259-265); opacity, mean and conic
 //     grads only when opacity * G <= clamp (:274-288), both conic off-diagonals (:285-288).
-// Per-Gaussian reduction: the up to 32 gradient values of one Gaussian are reduced across the warp
-// by a transposed butterfly (31 SHFL instead of 5 per value) after which lane l holds slot l; one
-// warp-wide RED then adds the warp's partial sums into that Gaussian's 128-byte accumulator line.
-// Warps where no lane contributed skip both (__any_sync).
-// Roofline: FP32/SFU + L2-atomic bound (~110 FLOP per contribution; 1 RED line per warp-Gaussian).
+//
+// Work decomposition (B200): one CTA per 16x16 tile, each thread owns PPT vertically adjacent
+// pixels of one column (they share dx and the column rect test).  A thread first sums the up to
+// 28 gradient values of one Gaussian over its PPT pixels in registers; the warp then reduces them
+// with a transposed butterfly (31 SHFL for 32 values instead of 5 per value) after which lane l
+// holds slot l, and one warp-wide RED adds the partial sums into that Gaussian's 128-byte
+// accumulator line.  With PPT = 4 a tile has 2 warps, i.e. 2 reductions + 2 REDs per
+// (tile, Gaussian) instead of 8 with one pixel per thread -- the reduction, not the arithmetic,
+// is what bounds this kernel (ncu: issue-bound, ALU/SHFL).  Warps where no lane contributed skip
+// both (__any_sync).  The per-pixel feature cotangents live in shared memory ([DP/4][256] float4,
+// conflict-free), the other per-pixel state in registers.
 #include "blend_common.cuh"
 #include "lgs_kernels.h"
 
@@ -36,152 +42,182 @@ __device__ __forceinline__ void warp_transpose_reduce(float (&v)[SLOTS], int lan
   }
 }
 
+// list entries staged per shared-memory batch (static shared memory stays under 48 KB)
+template <int DP>
+constexpr int bwd_batch() { return DP > 16 ? 64 : 128; }
+
 template <int DP>
 struct BwdSmem {
-  float4 r0[kBlock];  // u, v, depth, opacity
-  float4 r1[kBlock];  // A, B, C, -
-  uint2 rect[kBlock];
-  float4 col[kBlock];
-  uint32_t gid[kBlock];
-  float4 feat[kBlock][DP > 0 ? DP / 4 : 1];
+  float4 r0[bwd_batch<DP>()];  // u, v, depth, opacity
+  float4 r1[bwd_batch<DP>()];  // A, B, C, -
+  uint2 rect[bwd_batch<DP>()];
+  float4 col[bwd_batch<DP>()];
+  uint32_t gid[bwd_batch<DP>()];
+  float4 feat[bwd_batch<DP>()][DP > 0 ? DP / 4 : 1];
+  float4 gfeat[DP > 0 ? DP / 4 : 1][kBlock];  // per-pixel feature cotangents
 };
 
-template <int DP, int SLOTS>
-__global__ void __launch_bounds__(kBlock) blend_bwd_kernel(DevMap m, DevCam c, ViewBufs v, TileLists tl,
-                                                             PixelState ps, BwdIn in, float* __restrict__ gacc) {
+template <int DP, int SLOTS, int PPT>
+__global__ void __launch_bounds__(kBlock / PPT) blend_bwd_kernel(DevMap m, DevCam c, ViewBufs v, TileLists tl,
+                                                                   PixelState ps, BwdIn in, float* __restrict__ gacc) {
+  constexpr int NT = kBlock / PPT;
+  constexpr int DQ = DP > 0 ? DP / 4 : 1;
   __shared__ BwdSmem<DP> sm;
   __shared__ uint32_t s_max;
   const int tile = blockIdx.x;
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int tx = tile % c.tiles_x, ty = tile / c.tiles_x;
-  const int px = tx * kTile + (tid & (kTile - 1));
-  const int py = ty * kTile + (tid >> 4);
-  const bool inside = px < c.W && py < c.H;
-  const float fpx = (float)px, fpy = (float)py;
+  const int lx = tid & (kTile - 1);
+  const int ly0 = (tid >> 4) * PPT;  // first tile row of this thread's strip
+  const int px = tx * kTile + lx;
+  const int py0 = ty * kTile + ly0;
+  const float fpx = (float)px;
   const uint2 range = tl.ranges[tile];
 
-  float T = 1.f;
-  uint32_t last = 0;
-  float g_rgb[3] = {0.f, 0.f, 0.f};
-  float g_f[DP > 0 ? DP : 1];
+  float T[PPT], accum[PPT], g_rgb[PPT][3], g_draw[PPT], g_acc[PPT];
+  uint32_t last[PPT];
+  uint32_t my_max = 0;
 #pragma unroll
-  for (int k = 0; k < (DP > 0 ? DP : 1); ++k) g_f[k] = 0.f;
-  float g_draw = 0.f, g_acc = 0.f;
-  if (inside) {
-    const size_t pix = (size_t)py * c.W + px;
-    T = ps.final_t[pix];
-    last = ps.n_contrib[pix];
-    float g_d = 0.f;
-    if (in.cot_stride) {
-      const float4* cp = reinterpret_cast<const float4*>(in.g_rgb + pix * in.cot_stride);
-      const float4 c0 = cp[0];
-      g_rgb[0] = c0.x; g_rgb[1] = c0.y; g_rgb[2] = c0.z; g_d = c0.w;
+  for (int k = 0; k < PPT; ++k) {
+    const int py = py0 + k;
+    const int lp = (ly0 + k) * kTile + lx;  // pixel index within the tile
+    T[k] = 1.f; accum[k] = 0.f; last[k] = 0; g_draw[k] = 0.f; g_acc[k] = 0.f;
+    g_rgb[k][0] = g_rgb[k][1] = g_rgb[k][2] = 0.f;
+    float gf[DP > 0 ? DP : 1];
 #pragma unroll
-      for (int q = 0; q < DP / 4; ++q) {
-        const float4 fv = cp[1 + q];
-        g_f[q * 4 + 0] = fv.x; g_f[q * 4 + 1] = fv.y; g_f[q * 4 + 2] = fv.z; g_f[q * 4 + 3] = fv.w;
-      }
-    } else {
-      if (in.g_rgb) {
-        g_rgb[0] = in.g_rgb[pix * 3 + 0];
-        g_rgb[1] = in.g_rgb[pix * 3 + 1];
-        g_rgb[2] = in.g_rgb[pix * 3 + 2];
-      }
-      if (in.g_depth) g_d = in.g_depth[pix];
-      if (DP > 0 && in.g_feat) {
+    for (int q = 0; q < (DP > 0 ? DP : 1); ++q) gf[q] = 0.f;
+    if (px < c.W && py < c.H) {
+      const size_t pix = (size_t)py * c.W + px;
+      T[k] = ps.final_t[pix];
+      last[k] = ps.n_contrib[pix];
+      float g_d = 0.f;
+      if (in.cot_stride) {
+        const float4* cp = reinterpret_cast<const float4*>(in.g_rgb + pix * in.cot_stride);
+        const float4 c0 = cp[0];
+        g_rgb[k][0] = c0.x; g_rgb[k][1] = c0.y; g_rgb[k][2] = c0.z; g_d = c0.w;
 #pragma unroll
-        for (int k = 0; k < DP; ++k) g_f[k] = k < m.d ? in.g_feat[pix * m.d + k] : 0.f;
+        for (int q = 0; q < DP / 4; ++q) {
+          const float4 fv = cp[1 + q];
+          gf[q * 4 + 0] = fv.x; gf[q * 4 + 1] = fv.y; gf[q * 4 + 2] = fv.z; gf[q * 4 + 3] = fv.w;
+        }
+      } else {
+        if (in.g_rgb) {
+          g_rgb[k][0] = in.g_rgb[pix * 3 + 0];
+          g_rgb[k][1] = in.g_rgb[pix * 3 + 1];
+          g_rgb[k][2] = in.g_rgb[pix * 3 + 2];
+        }
+        if (in.g_depth) g_d = in.g_depth[pix];
+        if (DP > 0 && in.g_feat) {
+#pragma unroll
+          for (int q = 0; q < DP; ++q) gf[q] = q < m.d ? in.g_feat[pix * m.d + q] : 0.f;
+        }
       }
+      const float acc = ps.acc[pix];
+      const float mm = fmaxf(acc, 1e-6f);
+      g_draw[k] = g_d / mm;
+      g_acc[k] = acc > 1e-6f ? -g_d * ps.depth[pix] / mm : 0.f;
     }
-    const float acc = ps.acc[pix];
-    const float mm = fmaxf(acc, 1e-6f);
-    g_draw = g_d / mm;
-    g_acc = acc > 1e-6f ? -g_d * ps.depth[pix] / mm : 0.f;
+    if (DP > 0) {
+#pragma unroll
+      for (int q = 0; q < DP / 4; ++q) sm.gfeat[q][lp] = make_float4(gf[q * 4], gf[q * 4 + 1], gf[q * 4 + 2], gf[q * 4 + 3]);
+    }
+    my_max = max(my_max, last[k]);
   }
   if (tid == 0) s_max = 0;
   __syncthreads();
-  if (last) atomicMax(&s_max, last);
+  if (my_max) atomicMax(&s_max, my_max);
   __syncthreads();
   const uint32_t end = range.x + s_max;
 
-  float accum = 0.f;
-  for (int64_t bend = end; bend > (int64_t)range.x; bend -= kBlock) {
-    const uint32_t bstart = (uint32_t)max((int64_t)range.x, bend - kBlock);
+  for (int64_t bend = end; bend > (int64_t)range.x; bend -= bwd_batch<DP>()) {
+    const uint32_t bstart = (uint32_t)max((int64_t)range.x, bend - bwd_batch<DP>());
     const int cnt = (int)(bend - bstart);
     __syncthreads();
-    if (tid < cnt) {
-      const uint32_t g = __ldg(tl.vals + bstart + tid);
-      sm.gid[tid] = g;
-      sm.r0[tid] = __ldg(v.rec0 + g);
-      sm.r1[tid] = __ldg(v.rec1 + g);
-      sm.rect[tid] = __ldg(v.rect + g);
-      sm.col[tid] = __ldg(v.color + g);
+    for (int e = tid; e < cnt; e += NT) {
+      const uint32_t g = __ldg(tl.vals + bstart + e);
+      sm.gid[e] = g;
+      sm.r0[e] = __ldg(v.rec0 + g);
+      sm.r1[e] = __ldg(v.rec1 + g);
+      sm.rect[e] = __ldg(v.rect + g);
+      sm.col[e] = __ldg(v.color + g);
       if (DP > 0) {
-        const float4* fg = reinterpret_cast<const float4*>(m.feat) + (size_t)g * (DP / 4);
+        const float4* fg = reinterpret_cast<const float4*>(m.feat) + (size_t)g * DQ;
 #pragma unroll
-        for (int k = 0; k < DP / 4; ++k) sm.feat[tid][k] = __ldg(fg + k);
+        for (int q = 0; q < DQ; ++q) sm.feat[e][q] = __ldg(fg + q);
       }
     }
     __syncthreads();
-    for (int k = cnt - 1; k >= 0; --k) {
-      const uint32_t jrel = bstart + (uint32_t)k - range.x;
-      bool contrib = inside && jrel < last && in_rect(sm.rect[k], px, py);
+    for (int e = cnt - 1; e >= 0; --e) {
+      const uint32_t jrel = bstart + (uint32_t)e - range.x;
+      const uint2 rc = sm.rect[e];
+      const int ry0 = (int)(rc.y & 0xffffu), ry1 = (int)(rc.y >> 16);
+      const bool col_in = px >= (int)(rc.x & 0xffffu) && px <= (int)(rc.x >> 16) && py0 <= ry1 && py0 + PPT - 1 >= ry0;
+      if (!__any_sync(0xffffffffu, col_in)) continue;  // no pixel of this warp inside the Gaussian's rect
       float vals[SLOTS];
 #pragma unroll
       for (int q = 0; q < SLOTS; ++q) vals[q] = 0.f;
-      if (contrib) {
-        const float4 r0 = sm.r0[k];
-        const float4 r1 = sm.r1[k];
-        float dx, dy, G;
-        const float alpha = splat_alpha(r0.x, r0.y, r1.x, r1.y, r1.z, r0.w, fpx, fpy, dx, dy, G);
-        contrib = alpha >= c.alpha_skip;
-        if (contrib) {
+      bool any = false;
+      if (col_in) {
+        const float4 r0 = sm.r0[e];
+        const float4 r1 = sm.r1[e];
+        const float4 col = sm.col[e];
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) {
+          const int py = py0 + k;
+          if (!(jrel < last[k] && py >= ry0 && py <= ry1)) continue;
+          float dx, dy, G;
+          const float alpha = splat_alpha(r0.x, r0.y, r1.x, r1.y, r1.z, r0.w, fpx, (float)py, dx, dy, G);
+          if (!(alpha >= c.alpha_skip)) continue;
+          any = true;
           const float a = fminf(alpha, c.alpha_clamp);
           const float inv1ma = 1.0f / (1.0f - a);
-          T = T * inv1ma;  // transmittance before this contributor
-          const float w = a * T;
-          const float4 col = sm.col[k];
-          float dldw = fmaf(g_draw, r0.z, g_acc);
-          dldw = fmaf(g_rgb[0], col.x, dldw);
-          dldw = fmaf(g_rgb[1], col.y, dldw);
-          dldw = fmaf(g_rgb[2], col.z, dldw);
+          T[k] = T[k] * inv1ma;  // transmittance before this contributor
+          const float w = a * T[k];
+          float dldw = fmaf(g_draw[k], r0.z, g_acc[k]);
+          dldw = fmaf(g_rgb[k][0], col.x, dldw);
+          dldw = fmaf(g_rgb[k][1], col.y, dldw);
+          dldw = fmaf(g_rgb[k][2], col.z, dldw);
           if (DP > 0) {
+            const int lp = (ly0 + k) * kTile + lx;
 #pragma unroll
-            for (int q = 0; q < DP / 4; ++q) {
-              const float4 fv = sm.feat[k][q];
-              dldw = fmaf(g_f[q * 4 + 0], fv.x, dldw);
-              dldw = fmaf(g_f[q * 4 + 1], fv.y, dldw);
-              dldw = fmaf(g_f[q * 4 + 2], fv.z, dldw);
-              dldw = fmaf(g_f[q * 4 + 3], fv.w, dldw);
+            for (int q = 0; q < DQ; ++q) {
+              const float4 fv = sm.feat[e][q];
+              const float4 gv = sm.gfeat[q][lp];
+              dldw = fmaf(gv.x, fv.x, dldw);
+              dldw = fmaf(gv.y, fv.y, dldw);
+              dldw = fmaf(gv.z, fv.z, dldw);
+              dldw = fmaf(gv.w, fv.w, dldw);
+              vals[kSlotFeat + q * 4 + 0] = fmaf(gv.x, w, vals[kSlotFeat + q * 4 + 0]);
+              vals[kSlotFeat + q * 4 + 1] = fmaf(gv.y, w, vals[kSlotFeat + q * 4 + 1]);
+              vals[kSlotFeat + q * 4 + 2] = fmaf(gv.z, w, vals[kSlotFeat + q * 4 + 2]);
+              vals[kSlotFeat + q * 4 + 3] = fmaf(gv.w, w, vals[kSlotFeat + q * 4 + 3]);
             }
           }
-          const float dl_da = T * dldw - accum * inv1ma;
-          accum = fmaf(dldw, w, accum);
-          vals[kSlotColor + 0] = g_rgb[0] * w;
-          vals[kSlotColor + 1] = g_rgb[1] * w;
-          vals[kSlotColor + 2] = g_rgb[2] * w;
-#pragma unroll
-          for (int q = 0; q < DP; ++q) vals[kSlotFeat + q] = g_f[q] * w;
-          vals[kSlotZ] = g_draw * w;
+          const float dl_da = T[k] * dldw - accum[k] * inv1ma;
+          accum[k] = fmaf(dldw, w, accum[k]);
+          vals[kSlotColor + 0] = fmaf(g_rgb[k][0], w, vals[kSlotColor + 0]);
+          vals[kSlotColor + 1] = fmaf(g_rgb[k][1], w, vals[kSlotColor + 1]);
+          vals[kSlotColor + 2] = fmaf(g_rgb[k][2], w, vals[kSlotColor + 2]);
+          vals[kSlotZ] = fmaf(g_draw[k], w, vals[kSlotZ]);
           if (!(alpha > c.alpha_clamp)) {
             const float o = r0.w;
-            vals[kSlotOpac] = dl_da * G * o * (1.0f - o);
+            vals[kSlotOpac] = fmaf(dl_da * G, o * (1.0f - o), vals[kSlotOpac]);
             const float cf = dl_da * o * (-0.5f * G);  // dl_dg * dg_dq
             const float twoB = 2.0f * r1.y;
             const float dq_ddx = 2.0f * r1.x * dx + twoB * dy;
             const float dq_ddy = 2.0f * r1.z * dy + twoB * dx;
-            vals[kSlotMuX] = -cf * dq_ddx;
-            vals[kSlotMuY] = -cf * dq_ddy;
-            vals[kSlotConA] = cf * dx * dx;
-            vals[kSlotConB] = cf * dx * dy;
-            vals[kSlotConC] = cf * dy * dy;
+            vals[kSlotMuX] = fmaf(-cf, dq_ddx, vals[kSlotMuX]);
+            vals[kSlotMuY] = fmaf(-cf, dq_ddy, vals[kSlotMuY]);
+            vals[kSlotConA] = fmaf(cf * dx, dx, vals[kSlotConA]);
+            vals[kSlotConB] = fmaf(cf * dx, dy, vals[kSlotConB]);
+            vals[kSlotConC] = fmaf(cf * dy, dy, vals[kSlotConC]);
           }
         }
       }
-      if (__any_sync(0xffffffffu, contrib)) {
+      if (__any_sync(0xffffffffu, any)) {
         warp_transpose_reduce<SLOTS>(vals, lane);
-        float* dst = gacc + (size_t)sm.gid[k] * SLOTS + lane * (SLOTS / 32);
+        float* dst = gacc + (size_t)sm.gid[e] * SLOTS + lane * (SLOTS / 32);
 #pragma unroll
         for (int q = 0; q < SLOTS / 32; ++q)
           if (vals[q] != 0.f) atomicAdd(dst + q, vals[q]);
@@ -195,7 +231,8 @@ static void launch_bwd_dp(const DevMap& m, const DevCam& c, const ViewBufs& v, c
                           const PixelState& ps, const BwdIn& in, float* gacc, cudaStream_t s) {
   const unsigned tiles = (unsigned)(c.tiles_x * c.tiles_y);
   constexpr int SLOTS = slots_for(DP);
-  blend_bwd_kernel<DP, SLOTS><<<tiles, kBlock, 0, s>>>(m, c, v, tl, ps, in, gacc);
+  constexpr int PPT = 4;
+  blend_bwd_kernel<DP, SLOTS, PPT><<<tiles, kBlock / PPT, 0, s>>>(m, c, v, tl, ps, in, gacc);
 }
 
 void launch_blend_bwd(const DevMap& m, const DevCam& c, const ViewBufs& v, const TileLists& tl,

@@ -25,22 +25,34 @@ __global__ void __launch_bounds__(256) preprocess_bwd_kernel(DevMap m, DevCam c,
   if (i < n) {
     float o_pos[3] = {0.f, 0.f, 0.f}, o_rot[4] = {0.f, 0.f, 0.f, 0.f}, o_ls[3] = {0.f, 0.f, 0.f};
     float o_op = 0.f;
-    float o_sh[K * 3];
-#pragma unroll
-    for (int k = 0; k < K * 3; ++k) o_sh[k] = 0.f;
-    float o_feat[DP > 0 ? DP : 1];
-#pragma unroll
-    for (int k = 0; k < (DP > 0 ? DP : 1); ++k) o_feat[k] = 0.f;
+    const bool accum = g.accumulate != 0;
+    // results are streamed out as soon as they are final (keeps the register footprint small)
+    auto store = [accum](float* p, int64_t idx, float val) {
+      if (accum) p[idx] += val;
+      else p[idx] = val;
+    };
+    const bool visible = v.tiles[i] != 0;
+    if (!visible && !accum) {
+      if (g.sh)
+        for (int k = 0; k < K * 3; ++k) g.sh[i * (K * 3) + k] = 0.f;
+      if (DP > 0 && g.feature)
+        for (int k = 0; k < m.d; ++k) g.feature[(int64_t)k * n + i] = 0.f;
+    }
 
-    if (v.tiles[i] != 0) {
+    if (visible) {
       const float* ga = gacc + (size_t)i * SLOTS;
       const float4 a0 = *reinterpret_cast<const float4*>(ga + 0);  // muX muY conA conB
       const float4 a1 = *reinterpret_cast<const float4*>(ga + 4);  // conC opac z -
       const float4 a2 = *reinterpret_cast<const float4*>(ga + 8);  // r g b -
+      if (DP > 0 && g.feature) {  // renderer.cpp:262-264, written as [d][N]
 #pragma unroll
-      for (int q = 0; q < DP / 4; ++q) {
-        const float4 fv = *reinterpret_cast<const float4*>(ga + kSlotFeat + q * 4);
-        o_feat[q * 4 + 0] = fv.x; o_feat[q * 4 + 1] = fv.y; o_feat[q * 4 + 2] = fv.z; o_feat[q * 4 + 3] = fv.w;
+        for (int q = 0; q < DP / 4; ++q) {
+          const float4 fv = *reinterpret_cast<const float4*>(ga + kSlotFeat + q * 4);
+          const float f4[4] = {fv.x, fv.y, fv.z, fv.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if (q * 4 + e < m.d) store(g.feature, (int64_t)(q * 4 + e) * n + i, f4[e]);
+        }
       }
       o_op = a1.y;
       const float4 po = m.pos_opa[i];
@@ -49,9 +61,15 @@ __global__ void __launch_bounds__(256) preprocess_bwd_kernel(DevMap m, DevCam c,
 
       // ---- colour -> SH (renderer.cpp:259-261 for K = 1) ------------------------------------
       const float gc[3] = {a2.x, a2.y, a2.z};
-      if (DEG == 0) {
-        o_sh[0] = gc[0]; o_sh[1] = gc[1]; o_sh[2] = gc[2];
-      } else if (gc[0] != 0.f || gc[1] != 0.f || gc[2] != 0.f) {
+      if (DEG == 0 || (gc[0] == 0.f && gc[1] == 0.f && gc[2] == 0.f)) {
+        if (g.sh) {
+          store(g.sh, i * (K * 3) + 0, gc[0]);
+          store(g.sh, i * (K * 3) + 1, gc[1]);
+          store(g.sh, i * (K * 3) + 2, gc[2]);
+          if (!accum)
+            for (int k = 3; k < K * 3; ++k) g.sh[i * (K * 3) + k] = 0.f;
+        }
+      } else {
         const float dr[3] = {P[0] - c.cc[0], P[1] - c.cc[1], P[2] - c.cc[2]};
         const float nr = sqrtf(dr[0] * dr[0] + dr[1] * dr[1] + dr[2] * dr[2]);
         const float inr = 1.0f / nr;
@@ -67,7 +85,7 @@ __global__ void __launch_bounds__(256) preprocess_bwd_kernel(DevMap m, DevCam c,
           float s = 0.f;
 #pragma unroll
           for (int ch = 0; ch < 3; ++ch) {
-            o_sh[k * 3 + ch] = b[k] * gc[ch];
+            if (g.sh) store(g.sh, i * (K * 3) + k * 3 + ch, b[k] * gc[ch]);
             s = fmaf(__ldg(coef + k * 3 + ch), gc[ch], s);
           }
           gdn[0] = fmaf(db[k][0], s, gdn[0]);
@@ -259,30 +277,17 @@ __global__ void __launch_bounds__(256) preprocess_bwd_kernel(DevMap m, DevCam c,
       for (int a = 0; a < 3; ++a) o_pos[a] = gpos[a];
     }
 
-    // ---- dense writes in the reference layouts ------------------------------------------------
-    const bool accum = g.accumulate != 0;
-#define LGS_STORE(ptr, idx, val) \
-  do {                           \
-    if (accum) (ptr)[idx] += (val); else (ptr)[idx] = (val); \
-  } while (0)
+    // ---- dense writes in the reference layouts (zeros for culled Gaussians) -------------------
     if (g.position)
 #pragma unroll
-      for (int a = 0; a < 3; ++a) LGS_STORE(g.position, i * 3 + a, o_pos[a]);
+      for (int a = 0; a < 3; ++a) store(g.position, i * 3 + a, o_pos[a]);
     if (g.rotation)
 #pragma unroll
-      for (int a = 0; a < 4; ++a) LGS_STORE(g.rotation, i * 4 + a, o_rot[a]);
+      for (int a = 0; a < 4; ++a) store(g.rotation, i * 4 + a, o_rot[a]);
     if (g.log_scale)
 #pragma unroll
-      for (int a = 0; a < 3; ++a) LGS_STORE(g.log_scale, i * 3 + a, o_ls[a]);
-    if (g.opacity_logit) LGS_STORE(g.opacity_logit, i, o_op);
-    if (g.sh)
-#pragma unroll
-      for (int k = 0; k < K * 3; ++k) LGS_STORE(g.sh, i * (K * 3) + k, o_sh[k]);
-    if (DP > 0 && g.feature)
-#pragma unroll
-      for (int k = 0; k < DP; ++k)
-        if (k < m.d) LGS_STORE(g.feature, (int64_t)k * n + i, o_feat[k]);
-#undef LGS_STORE
+      for (int a = 0; a < 3; ++a) store(g.log_scale, i * 3 + a, o_ls[a]);
+    if (g.opacity_logit) store(g.opacity_logit, i, o_op);
   }
 
   if (g.pose) {  // block reduction of the pose gradient, one double atomic per value per block
