@@ -21,6 +21,8 @@
 // is what bounds this kernel (ncu: issue-bound, ALU/SHFL).  Warps where no lane contributed skip
 // both (__any_sync).  The per-pixel feature cotangents live in shared memory ([DP/4][256] float4,
 // conflict-free), the other per-pixel state in registers.
+#include <cstdlib>
+
 #include "blend_common.cuh"
 #include "lgs_kernels.h"
 
@@ -231,8 +233,14 @@ static void launch_bwd_dp(const DevMap& m, const DevCam& c, const ViewBufs& v, c
                           const PixelState& ps, const BwdIn& in, float* gacc, cudaStream_t s) {
   const unsigned tiles = (unsigned)(c.tiles_x * c.tiles_y);
   constexpr int SLOTS = slots_for(DP);
-  constexpr int PPT = 4;
-  blend_bwd_kernel<DP, SLOTS, PPT><<<tiles, kBlock / PPT, 0, s>>>(m, c, v, tl, ps, in, gacc);
+  static const int ppt = [] {
+    const char* e = getenv("LGS_BWD_PPT");  // tuning knob (1, 2 or 4 pixels per thread)
+    const int v = e ? atoi(e) : 2;
+    return (v == 1 || v == 2 || v == 4) ? v : 2;
+  }();
+  if (ppt == 1) blend_bwd_kernel<DP, SLOTS, 1><<<tiles, kBlock, 0, s>>>(m, c, v, tl, ps, in, gacc);
+  else if (ppt == 4) blend_bwd_kernel<DP, SLOTS, 4><<<tiles, kBlock / 4, 0, s>>>(m, c, v, tl, ps, in, gacc);
+  else blend_bwd_kernel<DP, SLOTS, 2><<<tiles, kBlock / 2, 0, s>>>(m, c, v, tl, ps, in, gacc);
 }
 
 void launch_blend_bwd(const DevMap& m, const DevCam& c, const ViewBufs& v, const TileLists& tl,

@@ -539,30 +539,42 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
     P = ctx->host_u32[0];
   }
   t->pairs = P;
-  uint16_t* keys_in = nullptr;
-  uint32_t* vals_in = nullptr;
-  TRYB(dalloc(ctx, &keys_in, P));
-  TRYB(dalloc(ctx, &vals_in, P));
-  TRYB(dalloc(ctx, &t->keys, P));
   TRYB(dalloc(ctx, &t->vals, P));
-  {
-    PhaseScope ph(ctx, PH_DUPLICATE);
-    launch_duplicate(t->vb, idx_sorted, incl, n, dc.tiles_x, keys_in, vals_in, s);
+  if (fast_binning_supported(ntiles)) {
+    // stable counting sort by tile straight into the final lists (binning.cu fast path)
+    uint32_t* scratch = nullptr;
+    TRYB(dalloc(ctx, reinterpret_cast<uint8_t**>(&scratch), fast_binning_scratch_bytes(n, ntiles)));
+    {
+      PhaseScope ph(ctx, PH_TILE_SORT);
+      launch_fast_binning(t->vb, idx_sorted, n, ntiles, dc.tiles_x, scratch, t->vals, t->ranges, s);
+    }
+    ctx->launches += n > 0 ? 5 : 0;
+    dfree(ctx, scratch);
+  } else {
+    uint16_t* keys_in = nullptr;
+    uint32_t* vals_in = nullptr;
+    TRYB(dalloc(ctx, &keys_in, P));
+    TRYB(dalloc(ctx, &vals_in, P));
+    TRYB(dalloc(ctx, &t->keys, P));
+    {
+      PhaseScope ph(ctx, PH_DUPLICATE);
+      launch_duplicate(t->vb, idx_sorted, incl, n, dc.tiles_x, keys_in, vals_in, s);
+    }
+    const size_t sort_bytes = binning_temp_bytes(0, P, tile_bits);
+    if (sort_bytes > temp_bytes) {
+      dfree(ctx, temp);
+      temp_bytes = sort_bytes;
+      TRYB(dalloc(ctx, reinterpret_cast<uint8_t**>(&temp), temp_bytes));
+    }
+    {
+      PhaseScope ph(ctx, PH_TILE_SORT);
+      launch_tile_sort(keys_in, t->keys, vals_in, t->vals, P, tile_bits, temp, temp_bytes, s);
+      launch_ranges(t->keys, P, ntiles, t->ranges, s);
+    }
+    ctx->launches += (n > 0 ? 1 : 0) + (P > 0 ? 5 : 0);
+    dfree(ctx, keys_in);
+    dfree(ctx, vals_in);
   }
-  const size_t sort_bytes = binning_temp_bytes(0, P, tile_bits);
-  if (sort_bytes > temp_bytes) {
-    dfree(ctx, temp);
-    temp_bytes = sort_bytes;
-    TRYB(dalloc(ctx, reinterpret_cast<uint8_t**>(&temp), temp_bytes));
-  }
-  {
-    PhaseScope ph(ctx, PH_TILE_SORT);
-    launch_tile_sort(keys_in, t->keys, vals_in, t->vals, P, tile_bits, temp, temp_bytes, s);
-    launch_ranges(t->keys, P, ntiles, t->ranges, s);
-  }
-  ctx->launches += (n > 0 ? 1 : 0) + (P > 0 ? 5 : 0);
-  dfree(ctx, keys_in);
-  dfree(ctx, vals_in);
   dfree(ctx, temp);
   dfree(ctx, dkey_sorted);
   dfree(ctx, idx_sorted);
@@ -916,13 +928,18 @@ LGS_API lgs_status lgs_debug_tile_keys(lgs_ctx* ctx, const lgs_saved* t, uint64_
   std::vector<uint16_t> k16(P);
   std::vector<uint32_t> v32(P);
   std::vector<float4> r0(n);
+  std::vector<uint2> rg((size_t)t->ntiles);
   if (P) {
-    LGS_CUDA(cudaMemcpyAsync(k16.data(), t->keys, sizeof(uint16_t) * P, cudaMemcpyDeviceToHost, s));
+    if (t->keys) LGS_CUDA(cudaMemcpyAsync(k16.data(), t->keys, sizeof(uint16_t) * P, cudaMemcpyDeviceToHost, s));
     LGS_CUDA(cudaMemcpyAsync(v32.data(), t->vals, sizeof(uint32_t) * P, cudaMemcpyDeviceToHost, s));
   }
   if (n) LGS_CUDA(cudaMemcpyAsync(r0.data(), t->vb.rec0, sizeof(float4) * n, cudaMemcpyDeviceToHost, s));
-  if (ranges) LGS_CUDA(cudaMemcpyAsync(ranges, t->ranges, sizeof(uint2) * t->ntiles, cudaMemcpyDeviceToHost, s));
+  LGS_CUDA(cudaMemcpyAsync(rg.data(), t->ranges, sizeof(uint2) * t->ntiles, cudaMemcpyDeviceToHost, s));
   LGS_CUDA(cudaStreamSynchronize(s));
+  if (ranges) std::memcpy(ranges, rg.data(), sizeof(uint2) * rg.size());
+  if (!t->keys)  // fast binning keeps no per-pair tile ids: they are implied by the ranges
+    for (size_t tt = 0; tt < rg.size(); ++tt)
+      for (uint32_t i = rg[tt].x; i < rg[tt].y; ++i) k16[i] = (uint16_t)tt;
   for (size_t i = 0; i < P; ++i) {
     uint32_t db;
     std::memcpy(&db, &r0[v32[i]].z, 4);
