@@ -138,233 +138,6 @@ void launch_tile_sort(uint16_t* keys_in, uint16_t* keys_out, uint32_t* vals_in, 
 }
 
 // ------------------------------------------------------------------------------------------
-// Fast path (tiles <= kMaxFastTiles): stable counting sort by tile, no pair sort at all.
-//
-// The depth-sorted Gaussians are cut into chunks of kChunk (one CTA each, kChunkWarps warps of
-// kWarpRun consecutive Gaussians).  (1) count: per chunk, a shared-memory histogram of the tiles
-// its Gaussians touch -> counts[chunk][tile].  (2) scan: column-wise exclusive scan over chunks and
-// an exclusive scan over tiles give each (chunk, tile) its first output slot; the per-tile ranges
-// fall out of the same scan (no ranges kernel).  (3) scatter: each warp walks its Gaussians in
-// depth order, one Gaussian at a time (lanes = the Gaussian's tiles), bumping a warp-private
-// shared-memory offset table -- so every tile list is written in exact (depth, index) order, the
-// order the reference's global sort gives (renderer.cpp:114-117), with one 4-byte store per pair.
-// ------------------------------------------------------------------------------------------
-constexpr int kWarpRun = 128;
-constexpr int kChunkWarps = 4;
-constexpr int kChunk = kWarpRun * kChunkWarps;
-constexpr int kMaxFastTiles = 12288;  // 4 warp tables x 12288 x 4 B = 192 KB of shared memory
-
-__device__ __forceinline__ void rect_tiles(uint2 r, uint32_t& tx0, uint32_t& ty0, uint32_t& tw, uint32_t& th) {
-  tx0 = (r.x & 0xffffu) / kTile;
-  ty0 = (r.y & 0xffffu) / kTile;
-  tw = (r.x >> 16) / kTile - tx0 + 1;
-  th = (r.y >> 16) / kTile - ty0 + 1;
-}
-
-__global__ void __launch_bounds__(kChunkWarps * 32) tile_count_kernel(const uint2* __restrict__ rect,
-                                                                       const uint32_t* __restrict__ tiles,
-                                                                       const uint32_t* __restrict__ idx_sorted,
-                                                                       int64_t n, int ntiles, int tiles_x,
-                                                                       uint32_t* __restrict__ counts) {
-  extern __shared__ uint32_t s_hist[];
-  for (int t = threadIdx.x; t < ntiles; t += blockDim.x) s_hist[t] = 0;
-  __syncthreads();
-  const int64_t s0 = (int64_t)blockIdx.x * kChunk;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int j = 0; j < kWarpRun; ++j) {
-    const int64_t s = s0 + (int64_t)warp * kWarpRun + j;
-    if (s >= n) break;
-    const uint32_t g = idx_sorted[s];
-    const uint32_t cnt = tiles[g];
-    if (cnt == 0) break;  // culled Gaussians sort last
-    uint32_t tx0, ty0, tw, th;
-    rect_tiles(rect[g], tx0, ty0, tw, th);
-    for (uint32_t i = lane; i < cnt; i += 32) {
-      const uint32_t ry = i / tw;
-      atomicAdd(&s_hist[(ty0 + ry) * tiles_x + tx0 + (i - ry * tw)], 1u);
-    }
-  }
-  __syncthreads();
-  uint32_t* out = counts + (size_t)blockIdx.x * ntiles;
-  for (int t = threadIdx.x; t < ntiles; t += blockDim.x) out[t] = s_hist[t];
-}
-
-// (2a) per (chunk block of 32 rows, tile): partial column sums
-constexpr int kScanRows = 32;
-__global__ void tile_scan_partial_kernel(const uint32_t* __restrict__ counts, int nchunks, int ntiles,
-                                         uint32_t* __restrict__ block_sums) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  const int cb = blockIdx.y;
-  if (t >= ntiles) return;
-  uint32_t s = 0;
-  const int c1 = min(nchunks, (cb + 1) * kScanRows);
-  for (int c = cb * kScanRows; c < c1; ++c) s += counts[(size_t)c * ntiles + t];
-  block_sums[(size_t)cb * ntiles + t] = s;
-}
-
-// (2b) one CTA: scan block sums per tile, tile totals, exclusive scan over tiles -> ranges and
-// the start offset of every (chunk block, tile)
-__global__ void __launch_bounds__(1024) tile_scan_tiles_kernel(uint32_t* __restrict__ block_sums, int nblocks,
-                                                               int ntiles, uint2* __restrict__ ranges) {
-  __shared__ uint32_t s_warp[32];
-  __shared__ uint32_t s_carry;
-  if (threadIdx.x == 0) s_carry = 0;
-  __syncthreads();
-  for (int base = 0; base < ntiles; base += blockDim.x) {
-    const int t = base + threadIdx.x;
-    uint32_t total = 0;
-    if (t < ntiles)
-      for (int b = 0; b < nblocks; ++b) {
-        const uint32_t v = block_sums[(size_t)b * ntiles + t];
-        block_sums[(size_t)b * ntiles + t] = total;  // exclusive within the tile's column
-        total += v;
-      }
-    // block-wide exclusive scan of `total`
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t x = total;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, x, off);
-      if (lane >= off) x += y;
-    }
-    if (lane == 31) s_warp[warp] = x;
-    __syncthreads();
-    if (warp == 0) {
-      uint32_t w = lane < (int)(blockDim.x >> 5) ? s_warp[lane] : 0;
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, w, off);
-        if (lane >= off) w += y;
-      }
-      s_warp[lane] = w;  // inclusive warp prefix
-    }
-    __syncthreads();
-    const uint32_t start = s_carry + (warp ? s_warp[warp - 1] : 0) + x - total;
-    if (t < ntiles) {
-      ranges[t] = make_uint2(start, start + total);
-      for (int b = 0; b < nblocks; ++b) block_sums[(size_t)b * ntiles + t] += start;
-    }
-    __syncthreads();
-    if (threadIdx.x == blockDim.x - 1) s_carry = start + total;
-    __syncthreads();
-  }
-}
-
-// (2c) counts[c][t] <- first output slot of chunk c in tile t
-__global__ void tile_scan_apply_kernel(uint32_t* __restrict__ counts, const uint32_t* __restrict__ block_sums,
-                                       int nchunks, int ntiles) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  const int cb = blockIdx.y;
-  if (t >= ntiles) return;
-  uint32_t run = block_sums[(size_t)cb * ntiles + t];
-  const int c1 = min(nchunks, (cb + 1) * kScanRows);
-  for (int c = cb * kScanRows; c < c1; ++c) {
-    const uint32_t v = counts[(size_t)c * ntiles + t];
-    counts[(size_t)c * ntiles + t] = run;
-    run += v;
-  }
-}
-
-// (3) stable scatter.  Shared memory: kChunkWarps warp-private tables of ntiles u32.
-__global__ void __launch_bounds__(kChunkWarps * 32) tile_scatter_kernel(const uint2* __restrict__ rect,
-                                                                         const uint32_t* __restrict__ tiles,
-                                                                         const uint32_t* __restrict__ idx_sorted,
-                                                                         int64_t n, int ntiles, int tiles_x,
-                                                                         const uint32_t* __restrict__ chunk_off,
-                                                                         uint32_t* __restrict__ vals) {
-  extern __shared__ uint32_t s_tab[];  // [kChunkWarps][ntiles]
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t* my = s_tab + (size_t)warp * ntiles;
-  for (int t = lane; t < ntiles; t += 32) my[t] = 0;
-  __syncwarp();
-  const int64_t s0 = (int64_t)blockIdx.x * kChunk + (int64_t)warp * kWarpRun;
-  // pass 1: this warp's per-tile counts
-  for (int j = 0; j < kWarpRun; ++j) {
-    const int64_t s = s0 + j;
-    if (s >= n) break;
-    const uint32_t g = idx_sorted[s];
-    const uint32_t cnt = tiles[g];
-    if (cnt == 0) break;
-    uint32_t tx0, ty0, tw, th;
-    rect_tiles(rect[g], tx0, ty0, tw, th);
-    for (uint32_t i = lane; i < cnt; i += 32) {
-      const uint32_t ry = i / tw;
-      my[(ty0 + ry) * tiles_x + tx0 + (i - ry * tw)] += 1;  // distinct tiles per Gaussian
-    }
-    __syncwarp();
-  }
-  __syncthreads();
-  // exclusive scan across warps per tile, seeded with the chunk's global offsets
-  const uint32_t* coff = chunk_off + (size_t)blockIdx.x * ntiles;
-  for (int t = threadIdx.x; t < ntiles; t += blockDim.x) {
-    uint32_t run = coff[t];
-#pragma unroll
-    for (int w = 0; w < kChunkWarps; ++w) {
-      const uint32_t v = s_tab[(size_t)w * ntiles + t];
-      s_tab[(size_t)w * ntiles + t] = run;
-      run += v;
-    }
-  }
-  __syncthreads();
-  // pass 2: write in depth order
-  for (int j = 0; j < kWarpRun; ++j) {
-    const int64_t s = s0 + j;
-    if (s >= n) break;
-    const uint32_t g = idx_sorted[s];
-    const uint32_t cnt = tiles[g];
-    if (cnt == 0) break;
-    uint32_t tx0, ty0, tw, th;
-    rect_tiles(rect[g], tx0, ty0, tw, th);
-    for (uint32_t i = lane; i < cnt; i += 32) {
-      const uint32_t ry = i / tw;
-      const uint32_t t = (ty0 + ry) * tiles_x + tx0 + (i - ry * tw);
-      const uint32_t pos = my[t];
-      my[t] = pos + 1;
-      vals[pos] = g;
-    }
-    __syncwarp();
-  }
-}
-
-size_t fast_binning_scratch_bytes(int64_t n, int ntiles) {
-  const int64_t nchunks = (n + kChunk - 1) / kChunk;
-  const int64_t nblocks = (nchunks + kScanRows - 1) / kScanRows;
-  return sizeof(uint32_t) * (size_t)(nchunks + nblocks) * (size_t)ntiles;
-}
-
-bool fast_binning_supported(int ntiles) { return ntiles <= kMaxFastTiles; }
-
-void launch_fast_binning(const ViewBufs& v, const uint32_t* idx_sorted, int64_t n, int ntiles, int tiles_x,
-                         uint32_t* scratch, uint32_t* vals, uint2* ranges, cudaStream_t s) {
-  if (n == 0) {
-    cudaMemsetAsync(ranges, 0, sizeof(uint2) * (size_t)ntiles, s);
-    return;
-  }
-  const int nchunks = (int)((n + kChunk - 1) / kChunk);
-  const int nblocks = (nchunks + kScanRows - 1) / kScanRows;
-  uint32_t* counts = scratch;
-  uint32_t* block_sums = scratch + (size_t)nchunks * ntiles;
-  const size_t smem_count = sizeof(uint32_t) * (size_t)ntiles;
-  const size_t smem_scatter = sizeof(uint32_t) * (size_t)ntiles * kChunkWarps;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(tile_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(sizeof(uint32_t) * kMaxFastTiles));
-    cudaFuncSetAttribute(tile_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(sizeof(uint32_t) * kMaxFastTiles * kChunkWarps));
-    attr_set = true;
-  }
-  tile_count_kernel<<<nchunks, kChunkWarps * 32, smem_count, s>>>(v.rect, v.tiles, idx_sorted, n, ntiles, tiles_x,
-                                                                  counts);
-  const dim3 sg((ntiles + 127) / 128, nblocks);
-  tile_scan_partial_kernel<<<sg, 128, 0, s>>>(counts, nchunks, ntiles, block_sums);
-  tile_scan_tiles_kernel<<<1, 1024, 0, s>>>(block_sums, nblocks, ntiles, ranges);
-  tile_scan_apply_kernel<<<sg, 128, 0, s>>>(counts, block_sums, nchunks, ntiles);
-  tile_scatter_kernel<<<nchunks, kChunkWarps * 32, smem_scatter, s>>>(v.rect, v.tiles, idx_sorted, n, ntiles,
-                                                                      tiles_x, counts, vals);
-}
-
-// ------------------------------------------------------------------------------------------
 // Fallback (more tiles than the shared-memory tables hold): duplicate + radix sort + ranges.
 // ------------------------------------------------------------------------------------------
 __global__ void ranges_kernel(const uint16_t* __restrict__ keys, int64_t pairs, uint2* __restrict__ ranges) {

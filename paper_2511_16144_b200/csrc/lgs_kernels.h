@@ -80,7 +80,7 @@ void launch_ranges(const uint16_t* keys, int64_t pairs, int ntiles, uint2* range
 bool fast_binning_supported(int ntiles);
 size_t fast_binning_scratch_bytes(int64_t n, int ntiles);
 void launch_fast_binning(const ViewBufs& v, const uint32_t* idx_sorted, int64_t n, int ntiles, int tiles_x,
-                         uint32_t* scratch, uint32_t* vals, uint2* ranges, cudaStream_t s);
+                         uint32_t* scratch, uint32_t* vals, uint2* ranges, uint32_t pairs, cudaStream_t s);
 
 void launch_blend_fwd(const DevMap& m, const DevCam& c, const ViewBufs& v, const TileLists& tl,
                       const PixelState& ps, const FwdOut& o, cudaStream_t s);
