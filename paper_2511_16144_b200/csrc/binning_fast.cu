@@ -3,20 +3,25 @@
 // The reference composites Gaussians in one global (depth, map index) order
 // (proj/src/renderer.cpp:114-117).  After the depth sort (binning.cu), every tile's list must hold
 // the Gaussians whose pixel rect overlaps the tile in exactly that order.  Instead of emitting
-// (tile, index) pairs and radix-sorting them, the pairs are written straight into place:
-//   1. count   : the depth-sorted Gaussians are cut into chunks of kChunk (one CTA); a shared-memory
-//                histogram of the tiles each chunk touches is written tile-major, counts[t][c];
-//   2. scan    : one exclusive scan over counts (tile-major) gives, for every (tile, chunk), the
-//                global slot of that chunk's first pair in that tile -- lists are ordered by tile,
-//                then chunk (= depth order); the per-tile ranges are read off the same scan;
-//   3. scatter : each warp owns kWarpRun consecutive Gaussians; it counts its own pairs per tile
-//                (warp-private table), the CTA turns the warp tables into starting slots, then
-//                each warp walks its Gaussians in depth order (lanes = the Gaussian's tiles) and
-//                writes each map index once, bumping its table.
-// The per-warp Gaussian records are loaded once, coalesced, and broadcast with shuffles, so the
-// sequential walks never wait on dependent global loads.  Bytes per pair: one 4 B store (plus
-// the per-chunk tables, ~ntiles x V / kChunk x 12 B).  Debug exports rebuild the 64-bit
-// (tile << 32 | f32bits(depth)) keys from the ranges, bit-identical to the oracle's stable sort.
+// (tile, index) pairs and radix-sorting them, the pairs are written straight into place.
+//
+// Conceptually the depth-sorted Gaussians emit a stream of P pairs (each Gaussian its tiles,
+// row-major); excl[s] is where Gaussian s starts in that stream.  The stream is cut into chunks
+// of kPairsPerChunk pairs (a Gaussian belongs to the chunk its first pair falls in), and each
+// chunk into kWarps equal warp slices -- balanced by pairs, not by Gaussians, because the depth
+// order puts the large near-camera splats (hundreds of tiles each) first.
+//   1. count   : per chunk, a shared-memory histogram of its tiles -> counts[tile][chunk];
+//   2. scan    : one exclusive scan over counts (tile-major) gives every (tile, chunk) its first
+//                output slot -- lists are ordered by tile, then chunk (= depth order); the tile
+//                ranges are read off the same scan;
+//   3. scatter : each warp counts its slice per tile (warp-private u16 table), the CTA turns the
+//                tables into per-warp starting offsets, then each warp walks its Gaussians in
+//                depth order (lanes = the Gaussian's tiles) writing each map index once.
+// Warps read their Gaussians' records with coalesced loads, 32 at a time, and broadcast them by
+// shuffle, so the sequential walk never waits on dependent global loads.
+// Bytes per pair: one 4 B store; plus ~12 B per (tile, chunk) cell for the tables and the scan.
+// The debug export rebuilds the 64-bit (tile << 32 | f32bits(depth)) keys from the ranges,
+// bit-identical to the oracle's stable sort of those keys.
 #include <cub/device/device_scan.cuh>
 
 #include "lgs_internal.cuh"
@@ -24,75 +29,99 @@
 
 namespace lgs {
 
-constexpr int kWarpRun = 128;                      // Gaussians per warp
-constexpr int kChunkWarps = 4;                     // warps per CTA
-constexpr int kChunk = kWarpRun * kChunkWarps;     // Gaussians per CTA chunk
-constexpr int kMaxFastTiles = 12288;               // 4 warp tables x 12288 x 4 B = 192 KB shared memory
-constexpr int kRegs = kWarpRun / 32;               // preloaded Gaussians per lane
+constexpr int kWarps = 8;
+constexpr int kPairsPerWarp = 1024;
+constexpr int kPairsPerChunk = kWarps * kPairsPerWarp;
+constexpr int kMaxFastTiles = 8192;  // warp tables: 8 x 8192 x u16 = 128 KB shared memory
 
-struct WarpGaussians {  // lane l holds Gaussians l, l + 32, l + 64, l + 96 of the warp's run
-  uint32_t g[kRegs];
-  uint32_t cnt[kRegs];
-  uint32_t origin[kRegs];  // tx0 | ty0 << 16
-  uint32_t tw[kRegs];
-};
-
-__device__ __forceinline__ void load_warp_gaussians(WarpGaussians& w, const uint2* __restrict__ rect,
-                                                    const uint32_t* __restrict__ tiles,
-                                                    const uint32_t* __restrict__ idx_sorted, int64_t s0, int64_t n,
-                                                    int lane) {
-#pragma unroll
-  for (int r = 0; r < kRegs; ++r) {
-    const int64_t s = s0 + r * 32 + lane;
-    w.g[r] = 0; w.cnt[r] = 0; w.origin[r] = 0; w.tw[r] = 1;
-    if (s < n) {
-      const uint32_t g = __ldg(idx_sorted + s);
-      const uint32_t c = __ldg(tiles + g);
-      w.g[r] = g;
-      w.cnt[r] = c;
-      if (c) {
-        const uint2 rc = __ldg(rect + g);
-        const uint32_t tx0 = (rc.x & 0xffffu) / kTile, ty0 = (rc.y & 0xffffu) / kTile;
-        w.origin[r] = tx0 | (ty0 << 16);
-        w.tw[r] = (rc.x >> 16) / kTile - tx0 + 1;
-      }
-    }
+// excl[s] (in place over the gathered counts) and chunk_first[c] = first sorted Gaussian whose
+// stream offset is >= c * kPairsPerChunk (c in [0, nchunks]); culled Gaussians (count 0, sorted
+// last) map past the last chunk.
+__global__ void chunk_bounds_kernel(uint32_t* __restrict__ cnt_to_excl, const uint32_t* __restrict__ incl, int64_t n,
+                                    int nchunks, uint32_t* __restrict__ chunk_first) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  const uint32_t cnt = cnt_to_excl[s];
+  const uint32_t excl = incl[s] - cnt;
+  const int c = cnt ? (int)(excl / kPairsPerChunk) : nchunks;
+  int cp = -1;
+  if (s > 0) {
+    const uint32_t cntp = incl[s - 1] - (s > 1 ? incl[s - 2] : 0u);
+    cp = cntp ? (int)((incl[s - 1] - cntp) / kPairsPerChunk) : nchunks;
   }
+  for (int cc = cp + 1; cc <= c; ++cc) chunk_first[cc] = (uint32_t)s;
+  if (s == n - 1)
+    for (int cc = c + 1; cc <= nchunks; ++cc) chunk_first[cc] = (uint32_t)n;
+  cnt_to_excl[s] = excl;
 }
 
-// Visit every (Gaussian, tile) pair of the warp's run in depth order; f(g, tile) is called by the
-// lanes of one Gaussian at a time (distinct tiles), with a __syncwarp between Gaussians.
+// first s in [lo, hi) with excl[s] >= key (excl is non-decreasing over visible Gaussians)
+__device__ __forceinline__ uint32_t lower_bound_excl(const uint32_t* __restrict__ excl, uint32_t lo, uint32_t hi,
+                                                     uint32_t key) {
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (__ldg(excl + mid) < key) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// Sorted-Gaussian range [s0, s1) of warp `warp` of chunk `c`.
+__device__ __forceinline__ void warp_slice(const uint32_t* __restrict__ excl, const uint32_t* __restrict__ chunk_first,
+                                           int c, int warp, uint32_t& s0, uint32_t& s1) {
+  const uint32_t lo = __ldg(chunk_first + c), hi = __ldg(chunk_first + c + 1);
+  const uint32_t base = (uint32_t)c * kPairsPerChunk;
+  s0 = warp == 0 ? lo : lower_bound_excl(excl, lo, hi, base + (uint32_t)warp * kPairsPerWarp);
+  s1 = warp == kWarps - 1 ? hi : lower_bound_excl(excl, lo, hi, base + (uint32_t)(warp + 1) * kPairsPerWarp);
+}
+
+// Visit the (Gaussian, tile) pairs of sorted Gaussians [s0, s1) in depth order; f(g, tile) is
+// called by the lanes of one Gaussian at a time (distinct tiles), __syncwarp between Gaussians.
 template <typename F>
-__device__ __forceinline__ void for_each_pair(const WarpGaussians& w, int lane, int tiles_x, F&& f) {
-#pragma unroll
-  for (int r = 0; r < kRegs; ++r) {
-    for (int j = 0; j < 32; ++j) {
-      const uint32_t cnt = __shfl_sync(0xffffffffu, w.cnt[r], j);
-      if (cnt == 0) return;  // culled Gaussians sort last (depth key 0xffffffff)
-      const uint32_t g = __shfl_sync(0xffffffffu, w.g[r], j);
-      const uint32_t org = __shfl_sync(0xffffffffu, w.origin[r], j);
-      const uint32_t tw = __shfl_sync(0xffffffffu, w.tw[r], j);
-      for (uint32_t i = lane; i < cnt; i += 32) {
-        const uint32_t ry = i / tw;
-        f(g, ((org >> 16) + ry) * (uint32_t)tiles_x + (org & 0xffffu) + (i - ry * tw));
+__device__ __forceinline__ void for_each_pair(const uint2* __restrict__ rect, const uint32_t* __restrict__ tiles,
+                                              const uint32_t* __restrict__ idx_sorted, uint32_t s0, uint32_t s1,
+                                              int lane, int tiles_x, F&& f) {
+  for (uint32_t b = s0; b < s1; b += 32) {
+    const uint32_t s = b + lane;
+    uint32_t g = 0, cnt = 0, org = 0, tw = 1;
+    if (s < s1) {
+      g = __ldg(idx_sorted + s);
+      cnt = __ldg(tiles + g);
+      const uint2 rc = __ldg(rect + g);
+      const uint32_t tx0 = (rc.x & 0xffffu) / kTile, ty0 = (rc.y & 0xffffu) / kTile;
+      org = tx0 | (ty0 << 16);
+      tw = (rc.x >> 16) / kTile - tx0 + 1;
+    }
+    const int nb = (int)min(32u, s1 - b);
+    for (int j = 0; j < nb; ++j) {
+      const uint32_t cj = __shfl_sync(0xffffffffu, cnt, j);
+      const uint32_t gj = __shfl_sync(0xffffffffu, g, j);
+      const uint32_t oj = __shfl_sync(0xffffffffu, org, j);
+      const uint32_t wj = __shfl_sync(0xffffffffu, tw, j);
+      for (uint32_t i = lane; i < cj; i += 32) {
+        const uint32_t ry = i / wj;
+        f(gj, ((oj >> 16) + ry) * (uint32_t)tiles_x + (oj & 0xffffu) + (i - ry * wj));
       }
       __syncwarp();
     }
   }
 }
 
-__global__ void __launch_bounds__(kChunkWarps * 32) tile_count_kernel(const uint2* __restrict__ rect,
-                                                                       const uint32_t* __restrict__ tiles,
-                                                                       const uint32_t* __restrict__ idx_sorted,
-                                                                       int64_t n, int ntiles, int tiles_x, int nchunks,
-                                                                       uint32_t* __restrict__ counts) {
+__global__ void __launch_bounds__(kWarps * 32) tile_count_kernel(const uint2* __restrict__ rect,
+                                                                  const uint32_t* __restrict__ tiles,
+                                                                  const uint32_t* __restrict__ idx_sorted,
+                                                                  const uint32_t* __restrict__ excl,
+                                                                  const uint32_t* __restrict__ chunk_first, int ntiles,
+                                                                  int tiles_x, int nchunks,
+                                                                  uint32_t* __restrict__ counts) {
   extern __shared__ uint32_t s_hist[];
   for (int t = threadIdx.x; t < ntiles; t += blockDim.x) s_hist[t] = 0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  WarpGaussians w;
-  load_warp_gaussians(w, rect, tiles, idx_sorted, (int64_t)blockIdx.x * kChunk + (int64_t)warp * kWarpRun, n, lane);
+  uint32_t s0, s1;
+  warp_slice(excl, chunk_first, blockIdx.x, warp, s0, s1);
   __syncthreads();
-  for_each_pair(w, lane, tiles_x, [&](uint32_t, uint32_t t) { atomicAdd(&s_hist[t], 1u); });
+  for_each_pair(rect, tiles, idx_sorted, s0, s1, lane, tiles_x,
+                [&](uint32_t, uint32_t t) { atomicAdd(&s_hist[t], 1u); });
   __syncthreads();
   for (int t = threadIdx.x; t < ntiles; t += blockDim.x) counts[(size_t)t * nchunks + blockIdx.x] = s_hist[t];
 }
@@ -106,63 +135,71 @@ __global__ void tile_ranges_kernel(const uint32_t* __restrict__ offs, int nchunk
   ranges[t] = make_uint2(b, e);
 }
 
-__global__ void __launch_bounds__(kChunkWarps * 32) tile_scatter_kernel(const uint2* __restrict__ rect,
-                                                                         const uint32_t* __restrict__ tiles,
-                                                                         const uint32_t* __restrict__ idx_sorted,
-                                                                         int64_t n, int ntiles, int tiles_x, int nchunks,
-                                                                         const uint32_t* __restrict__ offs,
-                                                                         uint32_t* __restrict__ vals) {
-  extern __shared__ uint32_t s_tab[];  // [kChunkWarps][ntiles]
+__global__ void __launch_bounds__(kWarps * 32) tile_scatter_kernel(const uint2* __restrict__ rect,
+                                                                    const uint32_t* __restrict__ tiles,
+                                                                    const uint32_t* __restrict__ idx_sorted,
+                                                                    const uint32_t* __restrict__ excl,
+                                                                    const uint32_t* __restrict__ chunk_first,
+                                                                    int ntiles, int tiles_x, int nchunks,
+                                                                    const uint32_t* __restrict__ offs,
+                                                                    uint32_t* __restrict__ vals) {
+  extern __shared__ uint32_t s_dyn[];
+  uint32_t* s_coff = s_dyn;                                       // [ntiles] chunk start slot per tile
+  uint16_t* s_tab = reinterpret_cast<uint16_t*>(s_dyn + ntiles);  // [kWarps][ntiles] offsets within chunk
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t* my = s_tab + (size_t)warp * ntiles;
+  uint16_t* my = s_tab + (size_t)warp * ntiles;
   for (int t = lane; t < ntiles; t += 32) my[t] = 0;
-  WarpGaussians w;
-  load_warp_gaussians(w, rect, tiles, idx_sorted, (int64_t)blockIdx.x * kChunk + (int64_t)warp * kWarpRun, n, lane);
+  for (int t = threadIdx.x; t < ntiles; t += blockDim.x) s_coff[t] = offs[(size_t)t * nchunks + blockIdx.x];
+  uint32_t s0, s1;
+  warp_slice(excl, chunk_first, blockIdx.x, warp, s0, s1);
   __syncwarp();
-  // pass 1: this warp's per-tile pair counts (distinct tiles per Gaussian -> no atomics)
-  for_each_pair(w, lane, tiles_x, [&](uint32_t, uint32_t t) { my[t] += 1; });
+  // pass 1: this warp's per-tile pair counts (distinct tiles per Gaussian: no atomics)
+  for_each_pair(rect, tiles, idx_sorted, s0, s1, lane, tiles_x,
+                [&](uint32_t, uint32_t t) { my[t] = (uint16_t)(my[t] + 1); });
   __syncthreads();
-  // per tile: starting slot of each warp = chunk start + counts of the earlier warps
+  // per tile: offset of each warp within the chunk = counts of the earlier warps
   for (int t = threadIdx.x; t < ntiles; t += blockDim.x) {
-    uint32_t run = offs[(size_t)t * nchunks + blockIdx.x];
+    uint32_t run = 0;
 #pragma unroll
-    for (int q = 0; q < kChunkWarps; ++q) {
+    for (int q = 0; q < kWarps; ++q) {
       const uint32_t c = s_tab[(size_t)q * ntiles + t];
-      s_tab[(size_t)q * ntiles + t] = run;
+      s_tab[(size_t)q * ntiles + t] = (uint16_t)run;
       run += c;
     }
   }
   __syncthreads();
   // pass 2: depth-ordered writes
-  for_each_pair(w, lane, tiles_x, [&](uint32_t g, uint32_t t) {
-    const uint32_t pos = my[t];
-    my[t] = pos + 1;
-    vals[pos] = g;
+  for_each_pair(rect, tiles, idx_sorted, s0, s1, lane, tiles_x, [&](uint32_t g, uint32_t t) {
+    const uint32_t r = my[t];
+    my[t] = (uint16_t)(r + 1);
+    vals[s_coff[t] + r] = g;
   });
 }
 
 bool fast_binning_supported(int ntiles) { return ntiles <= kMaxFastTiles; }
 
-static int nchunks_for(int64_t n) { return (int)((n + kChunk - 1) / kChunk); }
+static int nchunks_for(int64_t pairs) { return (int)((pairs + kPairsPerChunk - 1) / kPairsPerChunk); }
 
-size_t fast_binning_scratch_bytes(int64_t n, int ntiles) {
-  const size_t cells = (size_t)nchunks_for(n) * (size_t)ntiles;
+size_t fast_binning_scratch_bytes(int64_t pairs, int ntiles) {
+  const size_t cells = (size_t)nchunks_for(pairs) * (size_t)ntiles;
   size_t scan = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, scan, (uint32_t*)nullptr, (uint32_t*)nullptr, (int)cells);
-  return sizeof(uint32_t) * cells * 2 + scan + 256;
+  return sizeof(uint32_t) * (cells * 2 + (size_t)nchunks_for(pairs) + 1) + scan + 256;
 }
 
-void launch_fast_binning(const ViewBufs& v, const uint32_t* idx_sorted, int64_t n, int ntiles, int tiles_x,
-                         uint32_t* scratch, uint32_t* vals, uint2* ranges, uint32_t pairs, cudaStream_t s) {
+void launch_fast_binning(const ViewBufs& v, const uint32_t* idx_sorted, uint32_t* cnt_sorted, const uint32_t* incl,
+                         int64_t n, int ntiles, int tiles_x, uint32_t* scratch, uint32_t* vals, uint2* ranges,
+                         uint32_t pairs, cudaStream_t s) {
   if (n == 0 || pairs == 0) {
     cudaMemsetAsync(ranges, 0, sizeof(uint2) * (size_t)ntiles, s);
     return;
   }
-  const int nchunks = nchunks_for(n);
+  const int nchunks = nchunks_for(pairs);
   const size_t cells = (size_t)nchunks * (size_t)ntiles;
   uint32_t* counts = scratch;
-  uint32_t* offs = scratch + cells;
-  void* temp = scratch + 2 * cells;
+  uint32_t* offs = counts + cells;
+  uint32_t* chunk_first = offs + cells;
+  void* temp = chunk_first + nchunks + 1;
   size_t temp_bytes = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, temp_bytes, counts, offs, (int)cells);
   static bool attr_set = false;
@@ -170,16 +207,18 @@ void launch_fast_binning(const ViewBufs& v, const uint32_t* idx_sorted, int64_t 
     cudaFuncSetAttribute(tile_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)(sizeof(uint32_t) * kMaxFastTiles));
     cudaFuncSetAttribute(tile_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(sizeof(uint32_t) * kMaxFastTiles * kChunkWarps));
+                         (int)(sizeof(uint32_t) * kMaxFastTiles + sizeof(uint16_t) * kMaxFastTiles * kWarps));
     attr_set = true;
   }
-  const int threads = kChunkWarps * 32;
-  tile_count_kernel<<<nchunks, threads, sizeof(uint32_t) * ntiles, s>>>(v.rect, v.tiles, idx_sorted, n, ntiles,
-                                                                        tiles_x, nchunks, counts);
+  const uint32_t* excl = cnt_sorted;  // rewritten in place by chunk_bounds_kernel
+  chunk_bounds_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(cnt_sorted, incl, n, nchunks, chunk_first);
+  const int threads = kWarps * 32;
+  tile_count_kernel<<<nchunks, threads, sizeof(uint32_t) * ntiles, s>>>(v.rect, v.tiles, idx_sorted, excl, chunk_first,
+                                                                        ntiles, tiles_x, nchunks, counts);
   cub::DeviceScan::ExclusiveSum(temp, temp_bytes, counts, offs, (int)cells, s);
   tile_ranges_kernel<<<(ntiles + 255) / 256, 256, 0, s>>>(offs, nchunks, ntiles, pairs, ranges);
-  tile_scatter_kernel<<<nchunks, threads, sizeof(uint32_t) * ntiles * kChunkWarps, s>>>(
-      v.rect, v.tiles, idx_sorted, n, ntiles, tiles_x, nchunks, offs, vals);
+  tile_scatter_kernel<<<nchunks, threads, sizeof(uint32_t) * ntiles + sizeof(uint16_t) * ntiles * kWarps, s>>>(
+      v.rect, v.tiles, idx_sorted, excl, chunk_first, ntiles, tiles_x, nchunks, offs, vals);
 }
 
 }  // namespace lgs

@@ -543,12 +543,13 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
   if (fast_binning_supported(ntiles)) {
     // stable counting sort by tile straight into the final lists (binning.cu fast path)
     uint32_t* scratch = nullptr;
-    TRYB(dalloc(ctx, reinterpret_cast<uint8_t**>(&scratch), fast_binning_scratch_bytes(n, ntiles)));
+    TRYB(dalloc(ctx, reinterpret_cast<uint8_t**>(&scratch), fast_binning_scratch_bytes(P, ntiles)));
     {
       PhaseScope ph(ctx, PH_TILE_SORT);
-      launch_fast_binning(t->vb, idx_sorted, n, ntiles, dc.tiles_x, scratch, t->vals, t->ranges, (uint32_t)P, s);
+      launch_fast_binning(t->vb, idx_sorted, dkey_sorted, incl, n, ntiles, dc.tiles_x, scratch, t->vals, t->ranges,
+                          (uint32_t)P, s);
     }
-    ctx->launches += P > 0 ? 5 : 0;
+    ctx->launches += P > 0 ? 6 : 0;
     dfree(ctx, scratch);
   } else {
     uint16_t* keys_in = nullptr;
