@@ -961,11 +961,34 @@ static float orc_expf(float x) {
 
 ORC_API float orc_expf_export(float x) { return orc_expf(x); }
 
+/* Deterministic logf for x >= 1: identical code in csrc/lgs_internal.cuh (lgs_logf). */
+static float orc_logf(float x) {
+  union { float f; uint32_t u; } b, mb;
+  b.f = x;
+  int e = (int)((b.u >> 23) & 0xffu) - 127;
+  mb.u = (b.u & 0x7fffffu) | 0x3f800000u;
+  float m = mb.f;
+  if (m > 1.41421356f) {
+    m = m * 0.5f;
+    e = e + 1;
+  }
+  const float s = (m - 1.0f) / (m + 1.0f);
+  const float s2 = s * s;
+  float p = fmaf(s2, 0.0909090909f, 0.111111111f);
+  p = fmaf(s2, p, 0.142857143f);
+  p = fmaf(s2, p, 0.2f);
+  p = fmaf(s2, p, 0.333333333f);
+  p = fmaf(s2, p, 1.0f);
+  return fmaf((float)e, 0.693147181f, (2.0f * s) * p);
+}
+
+ORC_API float orc_logf_export(float x) { return orc_logf(x); }
+
 typedef struct {
   float rcw[9], tcw[3], cc[3];
   float fx, fy, cx, cy;
   int32_t width, height;
-  float near_plane, dilation, radius_sigma;
+  float near_plane, dilation, radius_sigma, alpha_skip;
 } orc32_cam;
 
 /* Host camera setup: double math of camera_setup, then rounded to float. */
@@ -980,6 +1003,7 @@ ORC_API void orc32_camera_setup(const orc_camera* cam, const orc_config* cfg, or
   out->near_plane = (float)cfg->near_plane;
   out->dilation = (float)cfg->dilation;
   out->radius_sigma = (float)cfg->radius_sigma;
+  out->alpha_skip = (float)cfg->alpha_skip;
 }
 
 static const float SHF_C1 = 0.4886025119029199f;
@@ -1071,15 +1095,27 @@ static int orc32_project(const float* P, const float* Q, const float* LS, float 
   if (!(u + radius >= -0.5f && u - radius <= Wf - 0.5f && v + radius >= -0.5f && v - radius <= Hf - 0.5f))
     return 0;
   if (!(det > 0.0f)) return 0;
-  bbox_o[0] = (int32_t)fmaxf(0.0f, floorf(u - radius));
-  bbox_o[1] = (int32_t)fminf(Wf - 1.0f, ceilf(u + radius));
-  bbox_o[2] = (int32_t)fmaxf(0.0f, floorf(v - radius));
-  bbox_o[3] = (int32_t)fminf(Hf - 1.0f, ceilf(v + radius));
+  /* Pixel rect of renderer.cpp:131-134 intersected with the bounding box of the alpha >= skip
+   * ellipse q <= 2 ln(o / skip) (plus margin): pixels outside never pass renderer.cpp:147. */
+  const float opacity = 1.0f / (1.0f + orc_expf(-ol));
+  if (c->alpha_skip > 0.0f && !(opacity >= c->alpha_skip)) return 0;
+  float ex = 3.0e38f, ey = 3.0e38f;
+  if (c->alpha_skip > 0.0f) {
+    const float Q = 2.0f * orc_logf(opacity / c->alpha_skip);
+    const float Qm = fmaf(Q, 1.001f, 0.01f);
+    ex = sqrtf(Qm * ca) + 0.01f;
+    ey = sqrtf(Qm * cc) + 0.01f;
+  }
+  bbox_o[0] = (int32_t)fmaxf(fmaxf(0.0f, floorf(u - radius)), floorf(u - ex));
+  bbox_o[1] = (int32_t)fminf(fminf(Wf - 1.0f, ceilf(u + radius)), ceilf(u + ex));
+  bbox_o[2] = (int32_t)fmaxf(fmaxf(0.0f, floorf(v - radius)), floorf(v - ey));
+  bbox_o[3] = (int32_t)fminf(fminf(Hf - 1.0f, ceilf(v + radius)), ceilf(v + ey));
+  if (bbox_o[0] > bbox_o[1] || bbox_o[2] > bbox_o[3]) return 0;
   conic_o[0] = cc / det;
   conic_o[1] = -cb / det;
   conic_o[2] = ca / det;
   *u_o = u; *v_o = v; *depth_o = t2; *radius_o = radius;
-  *opac_o = 1.0f / (1.0f + orc_expf(-ol));
+  *opac_o = opacity;
   if (deg == 0) {
     color_o[0] = sh[0]; color_o[1] = sh[1]; color_o[2] = sh[2];
   } else {

@@ -56,7 +56,7 @@ class Orc32Cam(C.Structure):
     _fields_ = [("rcw", C.c_float * 9), ("tcw", C.c_float * 3), ("cc", C.c_float * 3), ("fx", C.c_float),
                 ("fy", C.c_float), ("cx", C.c_float), ("cy", C.c_float), ("width", C.c_int32),
                 ("height", C.c_int32), ("near_plane", C.c_float), ("dilation", C.c_float),
-                ("radius_sigma", C.c_float)]
+                ("radius_sigma", C.c_float), ("alpha_skip", C.c_float)]
 
 
 def build():
@@ -95,6 +95,8 @@ def lib():
                                         _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp]
         L.orc_expf_export.restype = C.c_float
         L.orc_expf_export.argtypes = [C.c_float]
+        L.orc_logf_export.restype = C.c_float
+        L.orc_logf_export.argtypes = [C.c_float]
         L.orc32_camera_setup.argtypes = [C.POINTER(OrcCamera), C.POINTER(OrcConfig), C.POINTER(Orc32Cam)]
         L.orc32_preprocess.restype = C.c_int64
         L.orc32_preprocess.argtypes = [C.c_int64, C.c_int32, _fp, _fp, _fp, _fp, _fp, C.POINTER(Orc32Cam), _u8p,

@@ -156,22 +156,33 @@ __global__ void __launch_bounds__(kBlock / PPT) blend_bwd_kernel(DevMap m, DevCa
       const int ry0 = (int)(rc.y & 0xffffu), ry1 = (int)(rc.y >> 16);
       const bool col_in = px >= (int)(rc.x & 0xffffu) && px <= (int)(rc.x >> 16) && py0 <= ry1 && py0 + PPT - 1 >= ry0;
       if (!__any_sync(0xffffffffu, col_in)) continue;  // no pixel of this warp inside the Gaussian's rect
+      // phase 1: alphas of this thread's pixels (cheap); most rect hits fail the alpha test
+      const float4 r0 = sm.r0[e];
+      const float4 r1 = sm.r1[e];
+      float alphas[PPT], Gs[PPT], dxs[PPT], dys[PPT];
+      bool any = false;
+#pragma unroll
+      for (int k = 0; k < PPT; ++k) {
+        const int py = py0 + k;
+        alphas[k] = 0.f;
+        if (col_in && jrel < last[k] && py >= ry0 && py <= ry1) {
+          alphas[k] = splat_alpha(r0.x, r0.y, r1.x, r1.y, r1.z, r0.w, fpx, (float)py, dxs[k], dys[k], Gs[k]);
+          if (!(alphas[k] >= c.alpha_skip)) alphas[k] = 0.f;
+          else any = true;
+        }
+      }
+      if (!__any_sync(0xffffffffu, any)) continue;
+      // phase 2: contributions, summed over this thread's pixels, then one warp reduction
       float vals[SLOTS];
 #pragma unroll
       for (int q = 0; q < SLOTS; ++q) vals[q] = 0.f;
-      bool any = false;
-      if (col_in) {
-        const float4 r0 = sm.r0[e];
-        const float4 r1 = sm.r1[e];
+      {
         const float4 col = sm.col[e];
 #pragma unroll
         for (int k = 0; k < PPT; ++k) {
-          const int py = py0 + k;
-          if (!(jrel < last[k] && py >= ry0 && py <= ry1)) continue;
-          float dx, dy, G;
-          const float alpha = splat_alpha(r0.x, r0.y, r1.x, r1.y, r1.z, r0.w, fpx, (float)py, dx, dy, G);
-          if (!(alpha >= c.alpha_skip)) continue;
-          any = true;
+          const float alpha = alphas[k];
+          if (alpha == 0.f) continue;
+          const float dx = dxs[k], dy = dys[k], G = Gs[k];
           const float a = fminf(alpha, c.alpha_clamp);
           const float inv1ma = 1.0f / (1.0f - a);
           T[k] = T[k] * inv1ma;  // transmittance before this contributor
@@ -217,13 +228,11 @@ __global__ void __launch_bounds__(kBlock / PPT) blend_bwd_kernel(DevMap m, DevCa
           }
         }
       }
-      if (__any_sync(0xffffffffu, any)) {
-        warp_transpose_reduce<SLOTS>(vals, lane);
-        float* dst = gacc + (size_t)sm.gid[e] * SLOTS + lane * (SLOTS / 32);
+      warp_transpose_reduce<SLOTS>(vals, lane);
+      float* dst = gacc + (size_t)sm.gid[e] * SLOTS + lane * (SLOTS / 32);
 #pragma unroll
-        for (int q = 0; q < SLOTS / 32; ++q)
-          if (vals[q] != 0.f) atomicAdd(dst + q, vals[q]);
-      }
+      for (int q = 0; q < SLOTS / 32; ++q)
+        if (vals[q] != 0.f) atomicAdd(dst + q, vals[q]);
     }
   }
 }

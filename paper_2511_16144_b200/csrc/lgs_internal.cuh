@@ -79,6 +79,26 @@ __device__ __forceinline__ float lgs_expf(float x) {
   return (p * s1) * s2;
 }
 
+// Deterministic fp32 natural log for x >= 1 (finite): x = m 2^e with m in [sqrt(1/2), sqrt(2)),
+// log m = 2 atanh((m-1)/(m+1)) by its odd series.  Identical code in oracle/lgs_oracle.c (orc_logf).
+__device__ __forceinline__ float lgs_logf(float x) {
+  const uint32_t bits = __float_as_uint(x);
+  int e = (int)((bits >> 23) & 0xffu) - 127;
+  float m = __uint_as_float((bits & 0x7fffffu) | 0x3f800000u);
+  if (m > 1.41421356f) {
+    m = m * 0.5f;
+    e = e + 1;
+  }
+  const float s = (m - 1.0f) / (m + 1.0f);
+  const float s2 = s * s;
+  float p = fmaf(s2, 0.0909090909f, 0.111111111f);
+  p = fmaf(s2, p, 0.142857143f);
+  p = fmaf(s2, p, 0.2f);
+  p = fmaf(s2, p, 0.333333333f);
+  p = fmaf(s2, p, 1.0f);
+  return fmaf((float)e, 0.693147181f, (2.0f * s) * p);
+}
+
 // Real SH basis up to degree 3 (standard constants).  Colour convention: DC is used directly
 // (no C0, no +0.5, no clamp), so SH degree 0 is exactly the reference colour (renderer.cpp:128).
 constexpr float kShC1 = 0.4886025119029199f;

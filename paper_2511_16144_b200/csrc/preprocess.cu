@@ -106,6 +106,28 @@ __global__ void __launch_bounds__(256) preprocess_kernel(DevMap m, DevCam c, Vie
   const float Wf = (float)c.W, Hf = (float)c.H;
   ok = ok && (u + radius >= -0.5f && u - radius <= Wf - 0.5f && vv + radius >= -0.5f && vv - radius <= Hf - 0.5f);
   ok = ok && det > 0.0f;
+  const float opacity = 1.0f / (1.0f + lgs_expf(-po.w));
+  // A pixel can only contribute if alpha = o exp(-q/2) >= alpha_skip, i.e. q <= Q = 2 ln(o / skip)
+  // (renderer.cpp:146-147).  The ellipse q <= Q lies inside |dx| <= sqrt(Q cov_xx),
+  // |dy| <= sqrt(Q cov_yy); with a safety margin for fp32 rounding this box is intersected with
+  // the reference pixel rect.  Pixels cut away have alpha < skip in exact arithmetic and in both
+  // implementations, so tile lists shrink and images / gradients are unchanged.
+  ok = ok && !(c.alpha_skip > 0.0f && !(opacity >= c.alpha_skip));
+  float ex = 3.0e38f, ey = 3.0e38f;
+  if (c.alpha_skip > 0.0f) {
+    const float Q = 2.0f * lgs_logf(opacity / c.alpha_skip);
+    const float Qm = fmaf(Q, 1.001f, 0.01f);
+    ex = sqrtf(Qm * ca) + 0.01f;
+    ey = sqrtf(Qm * cc) + 0.01f;
+  }
+  int x0 = 0, x1 = 0, y0 = 0, y1 = 0;
+  if (ok) {
+    x0 = (int)fmaxf(fmaxf(0.0f, floorf(u - radius)), floorf(u - ex));
+    x1 = (int)fminf(fminf(Wf - 1.0f, ceilf(u + radius)), ceilf(u + ex));
+    y0 = (int)fmaxf(fmaxf(0.0f, floorf(vv - radius)), floorf(vv - ey));
+    y1 = (int)fminf(fminf(Hf - 1.0f, ceilf(vv + radius)), ceilf(vv + ey));
+    ok = x0 <= x1 && y0 <= y1;
+  }
   if (!ok) {
     v.tiles[i] = 0;
     v.dkey[i] = 0xffffffffu;
@@ -115,11 +137,6 @@ __global__ void __launch_bounds__(256) preprocess_kernel(DevMap m, DevCam c, Vie
     v.color[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     return;
   }
-  const int x0 = (int)fmaxf(0.0f, floorf(u - radius));
-  const int x1 = (int)fminf(Wf - 1.0f, ceilf(u + radius));
-  const int y0 = (int)fmaxf(0.0f, floorf(vv - radius));
-  const int y1 = (int)fminf(Hf - 1.0f, ceilf(vv + radius));
-  const float opacity = 1.0f / (1.0f + lgs_expf(-po.w));
   v.rec0[i] = make_float4(u, vv, t2, opacity);
   v.rec1[i] = make_float4(cc / det, -cb / det, ca / det, radius);
   v.rect[i] = make_uint2((uint32_t)x0 | ((uint32_t)x1 << 16), (uint32_t)y0 | ((uint32_t)y1 << 16));
