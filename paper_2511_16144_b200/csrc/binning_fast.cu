@@ -176,6 +176,40 @@ __global__ void __launch_bounds__(kWarps * 32) tile_scatter_kernel(const uint2* 
   });
 }
 
+// One CTA: order tiles by decreasing list length, bucketed by floor(log2(length)) (approximate
+// longest-processing-time-first order for the blend kernels' persistent scheduler; the order
+// inside a bucket is arbitrary and does not affect any result).
+__global__ void __launch_bounds__(1024) tile_order_kernel(const uint2* __restrict__ ranges, int ntiles,
+                                                          uint32_t* __restrict__ order) {
+  __shared__ uint32_t s_cnt[33];
+  __shared__ uint32_t s_pos[33];
+  if (threadIdx.x < 33) s_cnt[threadIdx.x] = 0;
+  __syncthreads();
+  for (int t = threadIdx.x; t < ntiles; t += blockDim.x) {
+    const uint2 r = ranges[t];
+    const uint32_t len = r.y - r.x;
+    atomicAdd(&s_cnt[len ? 32 - __clz(len) : 0], 1u);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t run = 0;
+    for (int b = 32; b >= 0; --b) {  // longest bucket first
+      s_pos[b] = run;
+      run += s_cnt[b];
+    }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < ntiles; t += blockDim.x) {
+    const uint2 r = ranges[t];
+    const uint32_t len = r.y - r.x;
+    order[atomicAdd(&s_pos[len ? 32 - __clz(len) : 0], 1u)] = (uint32_t)t;
+  }
+}
+
+void launch_tile_order(const uint2* ranges, int ntiles, uint32_t* order, cudaStream_t s) {
+  tile_order_kernel<<<1, 1024, 0, s>>>(ranges, ntiles, order);
+}
+
 bool fast_binning_supported(int ntiles) { return ntiles <= kMaxFastTiles; }
 
 static int nchunks_for(int64_t pairs) { return (int)((pairs + kPairsPerChunk - 1) / kPairsPerChunk); }

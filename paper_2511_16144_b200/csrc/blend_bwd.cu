@@ -11,20 +11,18 @@
 //   - colour / feature / depth grads for every contributor (:259-265); opacity, mean and conic
 //     grads only when opacity * G <= clamp (:274-288), both conic off-diagonals (:285-288).
 //
-// Work decomposition (B200): one CTA per 16x16 tile, each thread owns PPT vertically adjacent
-// pixels of one column (they share dx and the column rect test).  A thread first sums the up to
-// 28 gradient values of one Gaussian over its PPT pixels in registers; the warp then reduces them
-// with a transposed butterfly (31 SHFL for 32 values instead of 5 per value) after which lane l
-// holds slot l, and one warp-wide RED adds the partial sums into that Gaussian's 128-byte
-// accumulator line.  With PPT = 4 a tile has 2 warps, i.e. 2 reductions + 2 REDs per
-// (tile, Gaussian) instead of 8 with one pixel per thread -- the reduction, not the arithmetic,
-// is what bounds this kernel (ncu: issue-bound, ALU/SHFL).  Warps where no lane contributed skip
-// both (__any_sync).  The per-pixel feature cotangents live in shared memory ([DP/4][256] float4,
-// conflict-free), the other per-pixel state in registers.
+// B200 structure: persistent CTAs pull tiles longest-first (blend_common.cuh).  Each thread owns
+// PPT vertically adjacent pixels of one column.  Per staged Gaussian a warp first evaluates its
+// pixels' alphas (cheap) and skips the Gaussian unless some pixel contributes; then each thread
+// sums the up to 28 gradient values over its PPT pixels in registers, the warp reduces them with a
+// transposed butterfly (31 SHFL for 32 values instead of 5 per value) after which lane l holds
+// slot l, and one warp-wide RED adds the partial sums into that Gaussian's 128-byte accumulator
+// line.  The per-pixel feature cotangents live in shared memory ([DP/4][256] float4, conflict-free),
+// the other per-pixel state in registers.
+// Roofline: FP32/SHFL; ~13 FLOP per evaluated (pixel, Gaussian) + ~100 per contribution.
 #include <cstdlib>
 
 #include "blend_common.cuh"
-#include "lgs_kernels.h"
 
 namespace lgs {
 
@@ -52,6 +50,7 @@ template <int DP>
 struct BwdSmem {
   float4 r0[bwd_batch<DP>()];  // u, v, depth, opacity
   float4 r1[bwd_batch<DP>()];  // A, B, C, -
+  float4 sc[bwd_batch<DP>()];  // scaled conic a, b2, c, -
   uint2 rect[bwd_batch<DP>()];
   float4 col[bwd_batch<DP>()];
   uint32_t gid[bwd_batch<DP>()];
@@ -64,119 +63,129 @@ __global__ void __launch_bounds__(kBlock / PPT) blend_bwd_kernel(DevMap m, DevCa
                                                                    PixelState ps, BwdIn in, float* __restrict__ gacc) {
   constexpr int NT = kBlock / PPT;
   constexpr int DQ = DP > 0 ? DP / 4 : 1;
+  constexpr int NB = bwd_batch<DP>();
   __shared__ BwdSmem<DP> sm;
   __shared__ uint32_t s_max;
-  const int tile = blockIdx.x;
+  __shared__ int s_slot;
   const int tid = threadIdx.x;
   const int lane = tid & 31;
-  const int tx = tile % c.tiles_x, ty = tile / c.tiles_x;
   const int lx = tid & (kTile - 1);
   const int ly0 = (tid >> 4) * PPT;  // first tile row of this thread's strip
-  const int px = tx * kTile + lx;
-  const int py0 = ty * kTile + ly0;
-  const float fpx = (float)px;
-  const uint2 range = tl.ranges[tile];
+  const int ntiles = c.tiles_x * c.tiles_y;
 
-  float T[PPT], accum[PPT], g_rgb[PPT][3], g_draw[PPT], g_acc[PPT];
-  uint32_t last[PPT];
-  uint32_t my_max = 0;
+  for (int tile = next_tile(tl, ntiles, &s_slot); tile >= 0; tile = next_tile(tl, ntiles, &s_slot)) {
+    const int tx = tile % c.tiles_x, ty = tile / c.tiles_x;
+    const int px = tx * kTile + lx;
+    const int py0 = ty * kTile + ly0;
+    const float fpx = (float)px;
+    const uint2 range = tl.ranges[tile];
+
+    float T[PPT], accum[PPT], g_rgb[PPT][3], g_draw[PPT], g_acc[PPT];
+    uint32_t last[PPT];
+    uint32_t my_max = 0;
 #pragma unroll
-  for (int k = 0; k < PPT; ++k) {
-    const int py = py0 + k;
-    const int lp = (ly0 + k) * kTile + lx;  // pixel index within the tile
-    T[k] = 1.f; accum[k] = 0.f; last[k] = 0; g_draw[k] = 0.f; g_acc[k] = 0.f;
-    g_rgb[k][0] = g_rgb[k][1] = g_rgb[k][2] = 0.f;
-    float gf[DP > 0 ? DP : 1];
+    for (int k = 0; k < PPT; ++k) {
+      const int py = py0 + k;
+      const int lp = (ly0 + k) * kTile + lx;  // pixel index within the tile
+      T[k] = 1.f; accum[k] = 0.f; last[k] = 0; g_draw[k] = 0.f; g_acc[k] = 0.f;
+      g_rgb[k][0] = g_rgb[k][1] = g_rgb[k][2] = 0.f;
+      float gf[DP > 0 ? DP : 1];
 #pragma unroll
-    for (int q = 0; q < (DP > 0 ? DP : 1); ++q) gf[q] = 0.f;
-    if (px < c.W && py < c.H) {
-      const size_t pix = (size_t)py * c.W + px;
-      T[k] = ps.final_t[pix];
-      last[k] = ps.n_contrib[pix];
-      float g_d = 0.f;
-      if (in.cot_stride) {
-        const float4* cp = reinterpret_cast<const float4*>(in.g_rgb + pix * in.cot_stride);
-        const float4 c0 = cp[0];
-        g_rgb[k][0] = c0.x; g_rgb[k][1] = c0.y; g_rgb[k][2] = c0.z; g_d = c0.w;
+      for (int q = 0; q < (DP > 0 ? DP : 1); ++q) gf[q] = 0.f;
+      if (px < c.W && py < c.H) {
+        const size_t pix = (size_t)py * c.W + px;
+        T[k] = ps.final_t[pix];
+        last[k] = ps.n_contrib[pix];
+        float g_d = 0.f;
+        if (in.cot_stride) {
+          const float4* cp = reinterpret_cast<const float4*>(in.g_rgb + pix * in.cot_stride);
+          const float4 c0 = cp[0];
+          g_rgb[k][0] = c0.x; g_rgb[k][1] = c0.y; g_rgb[k][2] = c0.z; g_d = c0.w;
 #pragma unroll
-        for (int q = 0; q < DP / 4; ++q) {
-          const float4 fv = cp[1 + q];
-          gf[q * 4 + 0] = fv.x; gf[q * 4 + 1] = fv.y; gf[q * 4 + 2] = fv.z; gf[q * 4 + 3] = fv.w;
+          for (int q = 0; q < DP / 4; ++q) {
+            const float4 fv = cp[1 + q];
+            gf[q * 4 + 0] = fv.x; gf[q * 4 + 1] = fv.y; gf[q * 4 + 2] = fv.z; gf[q * 4 + 3] = fv.w;
+          }
+        } else {
+          if (in.g_rgb) {
+            g_rgb[k][0] = in.g_rgb[pix * 3 + 0];
+            g_rgb[k][1] = in.g_rgb[pix * 3 + 1];
+            g_rgb[k][2] = in.g_rgb[pix * 3 + 2];
+          }
+          if (in.g_depth) g_d = in.g_depth[pix];
+          if (DP > 0 && in.g_feat) {
+#pragma unroll
+            for (int q = 0; q < DP; ++q) gf[q] = q < m.d ? in.g_feat[pix * m.d + q] : 0.f;
+          }
         }
-      } else {
-        if (in.g_rgb) {
-          g_rgb[k][0] = in.g_rgb[pix * 3 + 0];
-          g_rgb[k][1] = in.g_rgb[pix * 3 + 1];
-          g_rgb[k][2] = in.g_rgb[pix * 3 + 2];
-        }
-        if (in.g_depth) g_d = in.g_depth[pix];
-        if (DP > 0 && in.g_feat) {
-#pragma unroll
-          for (int q = 0; q < DP; ++q) gf[q] = q < m.d ? in.g_feat[pix * m.d + q] : 0.f;
-        }
+        const float acc = ps.acc[pix];
+        const float mm = fmaxf(acc, 1e-6f);
+        g_draw[k] = g_d / mm;
+        g_acc[k] = acc > 1e-6f ? -g_d * ps.depth[pix] / mm : 0.f;
       }
-      const float acc = ps.acc[pix];
-      const float mm = fmaxf(acc, 1e-6f);
-      g_draw[k] = g_d / mm;
-      g_acc[k] = acc > 1e-6f ? -g_d * ps.depth[pix] / mm : 0.f;
-    }
-    if (DP > 0) {
-#pragma unroll
-      for (int q = 0; q < DP / 4; ++q) sm.gfeat[q][lp] = make_float4(gf[q * 4], gf[q * 4 + 1], gf[q * 4 + 2], gf[q * 4 + 3]);
-    }
-    my_max = max(my_max, last[k]);
-  }
-  if (tid == 0) s_max = 0;
-  __syncthreads();
-  if (my_max) atomicMax(&s_max, my_max);
-  __syncthreads();
-  const uint32_t end = range.x + s_max;
-
-  for (int64_t bend = end; bend > (int64_t)range.x; bend -= bwd_batch<DP>()) {
-    const uint32_t bstart = (uint32_t)max((int64_t)range.x, bend - bwd_batch<DP>());
-    const int cnt = (int)(bend - bstart);
-    __syncthreads();
-    for (int e = tid; e < cnt; e += NT) {
-      const uint32_t g = __ldg(tl.vals + bstart + e);
-      sm.gid[e] = g;
-      sm.r0[e] = __ldg(v.rec0 + g);
-      sm.r1[e] = __ldg(v.rec1 + g);
-      sm.rect[e] = __ldg(v.rect + g);
-      sm.col[e] = __ldg(v.color + g);
       if (DP > 0) {
-        const float4* fg = reinterpret_cast<const float4*>(m.feat) + (size_t)g * DQ;
 #pragma unroll
-        for (int q = 0; q < DQ; ++q) sm.feat[e][q] = __ldg(fg + q);
+        for (int q = 0; q < DP / 4; ++q)
+          sm.gfeat[q][lp] = make_float4(gf[q * 4], gf[q * 4 + 1], gf[q * 4 + 2], gf[q * 4 + 3]);
       }
+      my_max = max(my_max, last[k]);
     }
+    if (tid == 0) s_max = 0;
     __syncthreads();
-    for (int e = cnt - 1; e >= 0; --e) {
-      const uint32_t jrel = bstart + (uint32_t)e - range.x;
-      const uint2 rc = sm.rect[e];
-      const int ry0 = (int)(rc.y & 0xffffu), ry1 = (int)(rc.y >> 16);
-      const bool col_in = px >= (int)(rc.x & 0xffffu) && px <= (int)(rc.x >> 16) && py0 <= ry1 && py0 + PPT - 1 >= ry0;
-      if (!__any_sync(0xffffffffu, col_in)) continue;  // no pixel of this warp inside the Gaussian's rect
-      // phase 1: alphas of this thread's pixels (cheap); most rect hits fail the alpha test
-      const float4 r0 = sm.r0[e];
-      const float4 r1 = sm.r1[e];
-      float alphas[PPT], Gs[PPT], dxs[PPT], dys[PPT];
-      bool any = false;
+    if (my_max) atomicMax(&s_max, my_max);
+    __syncthreads();
+    const uint32_t end = range.x + s_max;
+
+    for (int64_t bend = end; bend > (int64_t)range.x; bend -= NB) {
+      const uint32_t bstart = (uint32_t)max((int64_t)range.x, bend - NB);
+      const int cnt = (int)(bend - bstart);
+      __syncthreads();
+      for (int e = tid; e < cnt; e += NT) {
+        const uint32_t g = __ldg(tl.vals + bstart + e);
+        sm.gid[e] = g;
+        sm.r0[e] = __ldg(v.rec0 + g);
+        const float4 r1 = __ldg(v.rec1 + g);
+        sm.r1[e] = r1;
+        const ScaledConic s = scale_conic(r1.x, r1.y, r1.z);
+        sm.sc[e] = make_float4(s.a, s.b2, s.c, 0.f);
+        sm.rect[e] = __ldg(v.rect + g);
+        sm.col[e] = __ldg(v.color + g);
+        if (DP > 0) {
+          const float4* fg = reinterpret_cast<const float4*>(m.feat) + (size_t)g * DQ;
 #pragma unroll
-      for (int k = 0; k < PPT; ++k) {
-        const int py = py0 + k;
-        alphas[k] = 0.f;
-        if (col_in && jrel < last[k] && py >= ry0 && py <= ry1) {
-          alphas[k] = splat_alpha(r0.x, r0.y, r1.x, r1.y, r1.z, r0.w, fpx, (float)py, dxs[k], dys[k], Gs[k]);
-          if (!(alphas[k] >= c.alpha_skip)) alphas[k] = 0.f;
-          else any = true;
+          for (int q = 0; q < DQ; ++q) sm.feat[e][q] = __ldg(fg + q);
         }
       }
-      if (!__any_sync(0xffffffffu, any)) continue;
-      // phase 2: contributions, summed over this thread's pixels, then one warp reduction
-      float vals[SLOTS];
+      __syncthreads();
+      for (int e = cnt - 1; e >= 0; --e) {
+        const uint32_t jrel = bstart + (uint32_t)e - range.x;
+        const uint2 rc = sm.rect[e];
+        const int ry0 = (int)(rc.y & 0xffffu), ry1 = (int)(rc.y >> 16);
+        const bool col_in =
+            px >= (int)(rc.x & 0xffffu) && px <= (int)(rc.x >> 16) && py0 <= ry1 && py0 + PPT - 1 >= ry0;
+        if (!__any_sync(0xffffffffu, col_in)) continue;  // no pixel of this warp inside the Gaussian's rect
+        // phase 1: alphas of this thread's pixels (cheap); most rect hits fail the alpha test
+        const float4 r0 = sm.r0[e];
+        const float4 s4 = sm.sc[e];
+        const ScaledConic sc{s4.x, s4.y, s4.z};
+        float alphas[PPT], Gs[PPT], dxs[PPT], dys[PPT];
+        bool any = false;
 #pragma unroll
-      for (int q = 0; q < SLOTS; ++q) vals[q] = 0.f;
-      {
+        for (int k = 0; k < PPT; ++k) {
+          const int py = py0 + k;
+          alphas[k] = 0.f;
+          if (col_in && jrel < last[k] && py >= ry0 && py <= ry1) {
+            alphas[k] = splat_alpha(r0.x, r0.y, sc, r0.w, fpx, (float)py, dxs[k], dys[k], Gs[k]);
+            if (!(alphas[k] >= c.alpha_skip)) alphas[k] = 0.f;
+            else any = true;
+          }
+        }
+        if (!__any_sync(0xffffffffu, any)) continue;
+        // phase 2: contributions, summed over this thread's pixels, then one warp reduction
+        float vals[SLOTS];
+#pragma unroll
+        for (int q = 0; q < SLOTS; ++q) vals[q] = 0.f;
+        const float4 r1 = sm.r1[e];
         const float4 col = sm.col[e];
 #pragma unroll
         for (int k = 0; k < PPT; ++k) {
@@ -184,7 +193,7 @@ __global__ void __launch_bounds__(kBlock / PPT) blend_bwd_kernel(DevMap m, DevCa
           if (alpha == 0.f) continue;
           const float dx = dxs[k], dy = dys[k], G = Gs[k];
           const float a = fminf(alpha, c.alpha_clamp);
-          const float inv1ma = 1.0f / (1.0f - a);
+          const float inv1ma = __frcp_rn(1.0f - a);
           T[k] = T[k] * inv1ma;  // transmittance before this contributor
           const float w = a * T[k];
           float dldw = fmaf(g_draw[k], r0.z, g_acc[k]);
@@ -218,38 +227,55 @@ __global__ void __launch_bounds__(kBlock / PPT) blend_bwd_kernel(DevMap m, DevCa
             vals[kSlotOpac] = fmaf(dl_da * G, o * (1.0f - o), vals[kSlotOpac]);
             const float cf = dl_da * o * (-0.5f * G);  // dl_dg * dg_dq
             const float twoB = 2.0f * r1.y;
-            const float dq_ddx = 2.0f * r1.x * dx + twoB * dy;
-            const float dq_ddy = 2.0f * r1.z * dy + twoB * dx;
+            const float dq_ddx = fmaf(2.0f * r1.x, dx, twoB * dy);
+            const float dq_ddy = fmaf(2.0f * r1.z, dy, twoB * dx);
             vals[kSlotMuX] = fmaf(-cf, dq_ddx, vals[kSlotMuX]);
             vals[kSlotMuY] = fmaf(-cf, dq_ddy, vals[kSlotMuY]);
-            vals[kSlotConA] = fmaf(cf * dx, dx, vals[kSlotConA]);
-            vals[kSlotConB] = fmaf(cf * dx, dy, vals[kSlotConB]);
+            const float cdx = cf * dx;
+            vals[kSlotConA] = fmaf(cdx, dx, vals[kSlotConA]);
+            vals[kSlotConB] = fmaf(cdx, dy, vals[kSlotConB]);
             vals[kSlotConC] = fmaf(cf * dy, dy, vals[kSlotConC]);
           }
         }
-      }
-      warp_transpose_reduce<SLOTS>(vals, lane);
-      float* dst = gacc + (size_t)sm.gid[e] * SLOTS + lane * (SLOTS / 32);
+        warp_transpose_reduce<SLOTS>(vals, lane);
+        float* dst = gacc + (size_t)sm.gid[e] * SLOTS + lane * (SLOTS / 32);
 #pragma unroll
-      for (int q = 0; q < SLOTS / 32; ++q)
-        if (vals[q] != 0.f) atomicAdd(dst + q, vals[q]);
+        for (int q = 0; q < SLOTS / 32; ++q)
+          if (vals[q] != 0.f) atomicAdd(dst + q, vals[q]);
+      }
     }
   }
+}
+
+template <int DP, int SLOTS, int PPT>
+static void launch_bwd_cfg(const DevMap& m, const DevCam& c, const ViewBufs& v, const TileLists& tl,
+                           const PixelState& ps, const BwdIn& in, float* gacc, cudaStream_t s) {
+  static int ctas_per_sm = 0, sms = 0;
+  if (!ctas_per_sm) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, blend_bwd_kernel<DP, SLOTS, PPT>, kBlock / PPT, 0);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (ctas_per_sm < 1) ctas_per_sm = 1;
+  }
+  const int ntiles = c.tiles_x * c.tiles_y;
+  const int grid = min(ntiles, ctas_per_sm * sms);
+  cudaMemsetAsync(tl.counter, 0, sizeof(int), s);
+  blend_bwd_kernel<DP, SLOTS, PPT><<<grid, kBlock / PPT, 0, s>>>(m, c, v, tl, ps, in, gacc);
 }
 
 template <int DP>
 static void launch_bwd_dp(const DevMap& m, const DevCam& c, const ViewBufs& v, const TileLists& tl,
                           const PixelState& ps, const BwdIn& in, float* gacc, cudaStream_t s) {
-  const unsigned tiles = (unsigned)(c.tiles_x * c.tiles_y);
   constexpr int SLOTS = slots_for(DP);
   static const int ppt = [] {
     const char* e = getenv("LGS_BWD_PPT");  // tuning knob (1, 2 or 4 pixels per thread)
-    const int v = e ? atoi(e) : 2;
-    return (v == 1 || v == 2 || v == 4) ? v : 2;
+    const int val = e ? atoi(e) : 2;
+    return (val == 1 || val == 2 || val == 4) ? val : 2;
   }();
-  if (ppt == 1) blend_bwd_kernel<DP, SLOTS, 1><<<tiles, kBlock, 0, s>>>(m, c, v, tl, ps, in, gacc);
-  else if (ppt == 4) blend_bwd_kernel<DP, SLOTS, 4><<<tiles, kBlock / 4, 0, s>>>(m, c, v, tl, ps, in, gacc);
-  else blend_bwd_kernel<DP, SLOTS, 2><<<tiles, kBlock / 2, 0, s>>>(m, c, v, tl, ps, in, gacc);
+  if (ppt == 1) launch_bwd_cfg<DP, SLOTS, 1>(m, c, v, tl, ps, in, gacc, s);
+  else if (ppt == 4) launch_bwd_cfg<DP, SLOTS, 4>(m, c, v, tl, ps, in, gacc, s);
+  else launch_bwd_cfg<DP, SLOTS, 2>(m, c, v, tl, ps, in, gacc, s);
 }
 
 void launch_blend_bwd(const DevMap& m, const DevCam& c, const ViewBufs& v, const TileLists& tl,

@@ -1,8 +1,7 @@
 // blend_fwd.cu -- K5: per-tile front-to-back alpha blending (RGB + depth + d-dim feature + acc).
 //
-// Restates the compositing loop of proj/src/renderer.cpp:125-165 tile by tile: one 256-thread CTA
-// per 16x16 tile, one pixel per thread, Gaussians of the tile's (depth, index)-sorted list staged
-// 256 at a time in shared memory.  Reference semantics kept exactly:
+// Restates the compositing loop of proj/src/renderer.cpp:125-165 tile by tile.  Reference
+// semantics kept exactly:
 //   - pixel centres at integer coordinates (dx = x - u, :141-142);
 //   - a Gaussian only touches pixels inside its inclusive pixel rect (:131-136);
 //   - the transmittance test precedes evaluation, so the Gaussian that pushes T below T_min is
@@ -10,152 +9,193 @@
 //   - skip when !(alpha >= 1/255) (NaN-safe, :147), then clamp alpha to 0.99 (:148);
 //   - the same weight w = alpha T accumulates colour, feature, depth and acc (:150-156);
 //   - depth is normalized by max(acc, 1e-6) (:163-165).
-// The per-pixel feature accumulators (DP fp32) stay in registers.  A CTA leaves its list as soon as
-// every pixel of the tile is done (__syncthreads_count), the tile-level early exit.
-// Roofline: FP32/SFU-bound; ~30 FLOP + 1 EX2 per evaluated (pixel, Gaussian), +45 per contribution.
+//
+// B200 structure: persistent CTAs (a few per SM) pull 16x16 tiles longest-list-first from a
+// global counter, so the 1200-tile grid of the headline config does not end in a partial wave.
+// Each thread owns PPT vertically adjacent pixels of one column (shared dx, shared column rect
+// test, one shared-memory read of each staged Gaussian per PPT pixels).  Gaussians of the tile's
+// (depth, index)-sorted list are staged 256 at a time in shared memory (record + 16-D feature);
+// the per-pixel feature accumulators (DP fp32 each) stay in registers; the CTA leaves the list as
+// soon as every pixel is done (__syncthreads_count).  The optional fused L1 loss writes the
+// cotangents the backward reads and one loss partial per CTA.
+// Roofline: FP32/SFU; ~13 FLOP + 1 EX2 per evaluated (pixel, Gaussian), +45 per contribution.
 #include "blend_common.cuh"
-#include "lgs_kernels.h"
 
 namespace lgs {
 
 template <int DP>
 struct FwdSmem {
-  float4 r0[kBlock];    // u, v, depth, opacity
-  float4 r1[kBlock];    // A, B, C, -
+  float4 r0[kBlock];  // u, v, depth, opacity
+  float4 sc[kBlock];  // scaled conic a, b2, c, -
   uint2 rect[kBlock];
   float4 col[kBlock];
   float4 feat[kBlock][DP > 0 ? DP / 4 : 1];
 };
 
-template <int DP, bool L1>
-__global__ void __launch_bounds__(kBlock) blend_fwd_kernel(DevMap m, DevCam c, ViewBufs v, TileLists tl,
-                                                             PixelState ps, FwdOut o) {
+template <int DP, bool L1, int PPT>
+__global__ void __launch_bounds__(kBlock / PPT) blend_fwd_kernel(DevMap m, DevCam c, ViewBufs v, TileLists tl,
+                                                                   PixelState ps, FwdOut o) {
+  constexpr int NT = kBlock / PPT;
+  constexpr int DQ = DP > 0 ? DP / 4 : 1;
+  constexpr int FD = DP > 0 ? DP : 1;
   __shared__ FwdSmem<DP> sm;
-  __shared__ float s_loss[kBlock / 32];
-  const int tile = blockIdx.x;
+  __shared__ float s_loss[NT / 32];
+  __shared__ int s_slot;
   const int tid = threadIdx.x;
-  const int tx = tile % c.tiles_x, ty = tile / c.tiles_x;
-  const int px = tx * kTile + (tid & (kTile - 1));
-  const int py = ty * kTile + (tid >> 4);
-  const bool inside = px < c.W && py < c.H;
-  const float fpx = (float)px, fpy = (float)py;
-  const uint2 range = tl.ranges[tile];
-
-  float T = 1.0f;
-  float cr = 0.f, cg = 0.f, cb = 0.f, draw = 0.f, acc = 0.f;
-  float f[DP > 0 ? DP : 1];
-#pragma unroll
-  for (int k = 0; k < (DP > 0 ? DP : 1); ++k) f[k] = 0.f;
-  uint32_t last = 0;
-  uint32_t n_eval = 0, n_contrib = 0;
-  bool done = !inside || !(1.0f >= c.t_min);
-
-  for (uint32_t base = range.x; base < range.y; base += kBlock) {
-    if (__syncthreads_count(done) == kBlock) break;
-    const uint32_t j = base + tid;
-    if (j < range.y) {
-      const uint32_t g = __ldg(tl.vals + j);
-      sm.r0[tid] = __ldg(v.rec0 + g);
-      sm.r1[tid] = __ldg(v.rec1 + g);
-      sm.rect[tid] = __ldg(v.rect + g);
-      sm.col[tid] = __ldg(v.color + g);
-      if (DP > 0) {
-        const float4* fg = reinterpret_cast<const float4*>(m.feat) + (size_t)g * (DP / 4);
-#pragma unroll
-        for (int k = 0; k < DP / 4; ++k) sm.feat[tid][k] = __ldg(fg + k);
-      }
-    }
-    __syncthreads();
-    const int cnt = (int)min((uint32_t)kBlock, range.y - base);
-    for (int k = 0; k < cnt && !done; ++k) {
-      if (!in_rect(sm.rect[k], px, py)) continue;
-      const float4 r0 = sm.r0[k];
-      const float4 r1 = sm.r1[k];
-      float dx, dy, G;
-      float alpha = splat_alpha(r0.x, r0.y, r1.x, r1.y, r1.z, r0.w, fpx, fpy, dx, dy, G);
-      ++n_eval;
-      if (!(alpha >= c.alpha_skip)) continue;
-      ++n_contrib;
-      alpha = fminf(alpha, c.alpha_clamp);
-      const float w = __fmul_rn(alpha, T);
-      const float4 col = sm.col[k];
-      cr = fmaf(w, col.x, cr);
-      cg = fmaf(w, col.y, cg);
-      cb = fmaf(w, col.z, cb);
-      draw = fmaf(w, r0.z, draw);
-      acc += w;
-      if (DP > 0) {
-#pragma unroll
-        for (int q = 0; q < DP / 4; ++q) {
-          const float4 fv = sm.feat[k][q];
-          f[q * 4 + 0] = fmaf(w, fv.x, f[q * 4 + 0]);
-          f[q * 4 + 1] = fmaf(w, fv.y, f[q * 4 + 1]);
-          f[q * 4 + 2] = fmaf(w, fv.z, f[q * 4 + 2]);
-          f[q * 4 + 3] = fmaf(w, fv.w, f[q * 4 + 3]);
-        }
-      }
-      T = __fmul_rn(T, __fsub_rn(1.0f, alpha));
-      last = base + k + 1 - range.x;
-      if (T < c.t_min) done = true;
-    }
-  }
-
+  const int lx = tid & (kTile - 1);
+  const int ly0 = (tid >> 4) * PPT;
+  const int ntiles = c.tiles_x * c.tiles_y;
   float loss = 0.f;
-  if (inside) {
-    const size_t pix = (size_t)py * c.W + px;
-    const float dnorm = draw / fmaxf(acc, 1e-6f);
-    ps.final_t[pix] = T;
-    ps.n_contrib[pix] = last;
-    ps.depth[pix] = dnorm;
-    ps.acc[pix] = acc;
-    ps.work[pix] = make_uint2(n_eval, n_contrib);
-    if (o.rgb) {
-      o.rgb[pix * 3 + 0] = cr;
-      o.rgb[pix * 3 + 1] = cg;
-      o.rgb[pix * 3 + 2] = cb;
+
+  for (int tile = next_tile(tl, ntiles, &s_slot); tile >= 0; tile = next_tile(tl, ntiles, &s_slot)) {
+    const int tx = tile % c.tiles_x, ty = tile / c.tiles_x;
+    const int px = tx * kTile + lx;
+    const int py0 = ty * kTile + ly0;
+    const float fpx = (float)px;
+    const uint2 range = tl.ranges[tile];
+
+    float T[PPT], cr[PPT], cg[PPT], cb[PPT], draw[PPT], acc[PPT];
+    float f[PPT][FD];
+    uint32_t last[PPT], n_eval[PPT], n_contrib[PPT];
+    bool done[PPT];
+    bool all_done = true;
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) {
+      T[k] = 1.f; cr[k] = cg[k] = cb[k] = draw[k] = acc[k] = 0.f;
+#pragma unroll
+      for (int q = 0; q < FD; ++q) f[k][q] = 0.f;
+      last[k] = n_eval[k] = n_contrib[k] = 0;
+      done[k] = !(px < c.W && py0 + k < c.H) || !(1.0f >= c.t_min);
+      all_done = all_done && done[k];
     }
-    if (o.depth) o.depth[pix] = dnorm;
-    if (o.acc) o.acc[pix] = acc;
-    if (DP > 0 && o.feat) {
-      float* fo = o.feat + pix * m.d;
-      if (m.d == DP) {
+
+    for (uint32_t base = range.x; base < range.y; base += kBlock) {
+      if (__syncthreads_count(all_done) == NT) break;
+      for (int e = tid; e < kBlock; e += NT) {
+        const uint32_t j = base + e;
+        if (j < range.y) {
+          const uint32_t g = __ldg(tl.vals + j);
+          sm.r0[e] = __ldg(v.rec0 + g);
+          const float4 r1 = __ldg(v.rec1 + g);
+          const ScaledConic s = scale_conic(r1.x, r1.y, r1.z);
+          sm.sc[e] = make_float4(s.a, s.b2, s.c, 0.f);
+          sm.rect[e] = __ldg(v.rect + g);
+          sm.col[e] = __ldg(v.color + g);
+          if (DP > 0) {
+            const float4* fg = reinterpret_cast<const float4*>(m.feat) + (size_t)g * DQ;
 #pragma unroll
-        for (int q = 0; q < DP / 4; ++q)
-          reinterpret_cast<float4*>(fo)[q] = make_float4(f[q * 4], f[q * 4 + 1], f[q * 4 + 2], f[q * 4 + 3]);
-      } else {
-#pragma unroll
-        for (int k = 0; k < DP; ++k)
-          if (k < m.d) fo[k] = f[k];
-      }
-    }
-    if (L1) {
-      // L = mean|rgb - T| + mean|depth - T| + mean|feat - T|; cotangent sign(diff) / count
-      const float npx = (float)c.W * (float)c.H;
-      const float inv_rgb = 1.0f / (3.0f * npx), inv_d = 1.0f / npx, inv_f = m.d > 0 ? 1.0f / ((float)m.d * npx) : 0.f;
-      float* cot = o.cot + pix * (4 + DP);
-      const float vals[3] = {cr, cg, cb};
-      float lr = 0.f, lf = 0.f;
-#pragma unroll
-      for (int ch = 0; ch < 3; ++ch) {
-        const float df = vals[ch] - o.t_rgb[pix * 3 + ch];
-        cot[ch] = df > 0.f ? inv_rgb : (df < 0.f ? -inv_rgb : 0.f);
-        lr += fabsf(df);
-      }
-      const float dd = dnorm - o.t_depth[pix];
-      cot[3] = dd > 0.f ? inv_d : (dd < 0.f ? -inv_d : 0.f);
-#pragma unroll
-      for (int k = 0; k < DP; ++k) {
-        float gk = 0.f;
-        if (k < m.d) {
-          const float df = f[k] - o.t_feat[pix * m.d + k];
-          gk = df > 0.f ? inv_f : (df < 0.f ? -inv_f : 0.f);
-          lf += fabsf(df);
+            for (int q = 0; q < DQ; ++q) sm.feat[e][q] = __ldg(fg + q);
+          }
         }
-        cot[4 + k] = gk;
       }
-      loss = lr * inv_rgb + fabsf(dd) * inv_d + lf * inv_f;
+      __syncthreads();
+      const int cnt = (int)min((uint32_t)kBlock, range.y - base);
+      for (int e = 0; e < cnt && !all_done; ++e) {
+        const uint2 rc = sm.rect[e];
+        if (px < (int)(rc.x & 0xffffu) || px > (int)(rc.x >> 16)) continue;
+        const int ry0 = (int)(rc.y & 0xffffu), ry1 = (int)(rc.y >> 16);
+        if (py0 > ry1 || py0 + PPT - 1 < ry0) continue;
+        const float4 r0 = sm.r0[e];
+        const float4 s4 = sm.sc[e];
+        const ScaledConic sc{s4.x, s4.y, s4.z};
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) {
+          const int py = py0 + k;
+          if (done[k] || py < ry0 || py > ry1) continue;
+          float dx, dy, G;
+          float alpha = splat_alpha(r0.x, r0.y, sc, r0.w, fpx, (float)py, dx, dy, G);
+          ++n_eval[k];
+          if (!(alpha >= c.alpha_skip)) continue;
+          ++n_contrib[k];
+          alpha = fminf(alpha, c.alpha_clamp);
+          const float w = __fmul_rn(alpha, T[k]);
+          const float4 col = sm.col[e];
+          cr[k] = fmaf(w, col.x, cr[k]);
+          cg[k] = fmaf(w, col.y, cg[k]);
+          cb[k] = fmaf(w, col.z, cb[k]);
+          draw[k] = fmaf(w, r0.z, draw[k]);
+          acc[k] += w;
+          if (DP > 0) {
+#pragma unroll
+            for (int q = 0; q < DQ; ++q) {
+              const float4 fv = sm.feat[e][q];
+              f[k][q * 4 + 0] = fmaf(w, fv.x, f[k][q * 4 + 0]);
+              f[k][q * 4 + 1] = fmaf(w, fv.y, f[k][q * 4 + 1]);
+              f[k][q * 4 + 2] = fmaf(w, fv.z, f[k][q * 4 + 2]);
+              f[k][q * 4 + 3] = fmaf(w, fv.w, f[k][q * 4 + 3]);
+            }
+          }
+          T[k] = __fmul_rn(T[k], __fsub_rn(1.0f, alpha));
+          last[k] = base + e + 1 - range.x;
+          if (T[k] < c.t_min) done[k] = true;
+        }
+        all_done = true;
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) all_done = all_done && done[k];
+      }
+    }
+
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) {
+      const int py = py0 + k;
+      if (!(px < c.W && py < c.H)) continue;
+      const size_t pix = (size_t)py * c.W + px;
+      const float dnorm = draw[k] / fmaxf(acc[k], 1e-6f);
+      ps.final_t[pix] = T[k];
+      ps.n_contrib[pix] = last[k];
+      ps.depth[pix] = dnorm;
+      ps.acc[pix] = acc[k];
+      ps.work[pix] = make_uint2(n_eval[k], n_contrib[k]);
+      if (o.rgb) {
+        o.rgb[pix * 3 + 0] = cr[k];
+        o.rgb[pix * 3 + 1] = cg[k];
+        o.rgb[pix * 3 + 2] = cb[k];
+      }
+      if (o.depth) o.depth[pix] = dnorm;
+      if (o.acc) o.acc[pix] = acc[k];
+      if (DP > 0 && o.feat) {
+        float* fo = o.feat + pix * m.d;
+        if (m.d == DP) {
+#pragma unroll
+          for (int q = 0; q < DQ; ++q)
+            reinterpret_cast<float4*>(fo)[q] = make_float4(f[k][q * 4], f[k][q * 4 + 1], f[k][q * 4 + 2], f[k][q * 4 + 3]);
+        } else {
+#pragma unroll
+          for (int q = 0; q < FD; ++q)
+            if (q < m.d) fo[q] = f[k][q];
+        }
+      }
+      if (L1) {
+        // L = mean|rgb - T| + mean|depth - T| + mean|feat - T|; cotangent sign(diff) / count
+        const float npx = (float)c.W * (float)c.H;
+        const float inv_rgb = 1.0f / (3.0f * npx), inv_d = 1.0f / npx;
+        const float inv_f = m.d > 0 ? 1.0f / ((float)m.d * npx) : 0.f;
+        float* cot = o.cot + pix * (4 + DP);
+        const float vals[3] = {cr[k], cg[k], cb[k]};
+        float lr = 0.f, lf = 0.f;
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) {
+          const float df = vals[ch] - o.t_rgb[pix * 3 + ch];
+          cot[ch] = df > 0.f ? inv_rgb : (df < 0.f ? -inv_rgb : 0.f);
+          lr += fabsf(df);
+        }
+        const float dd = dnorm - o.t_depth[pix];
+        cot[3] = dd > 0.f ? inv_d : (dd < 0.f ? -inv_d : 0.f);
+#pragma unroll
+        for (int q = 0; q < DP; ++q) {
+          float gk = 0.f;
+          if (q < m.d) {
+            const float df = f[k][q] - o.t_feat[pix * m.d + q];
+            gk = df > 0.f ? inv_f : (df < 0.f ? -inv_f : 0.f);
+            lf += fabsf(df);
+          }
+          cot[4 + q] = gk;
+        }
+        loss += lr * inv_rgb + fabsf(dd) * inv_d + lf * inv_f;
+      }
     }
   }
+
   if (L1) {
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) loss += __shfl_xor_sync(0xffffffffu, loss, off);
@@ -163,18 +203,34 @@ __global__ void __launch_bounds__(kBlock) blend_fwd_kernel(DevMap m, DevCam c, V
     __syncthreads();
     if (tid == 0) {
       double s = 0.0;
-      for (int w = 0; w < kBlock / 32; ++w) s += s_loss[w];
+      for (int w = 0; w < NT / 32; ++w) s += s_loss[w];
       atomicAdd(o.loss, s);
     }
   }
 }
 
+template <int DP, bool L1, int PPT>
+static void launch_fwd_cfg(const DevMap& m, const DevCam& c, const ViewBufs& v, const TileLists& tl,
+                           const PixelState& ps, const FwdOut& o, cudaStream_t s) {
+  static int ctas_per_sm = 0, sms = 0;
+  if (!ctas_per_sm) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, blend_fwd_kernel<DP, L1, PPT>, kBlock / PPT, 0);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (ctas_per_sm < 1) ctas_per_sm = 1;
+  }
+  const int ntiles = c.tiles_x * c.tiles_y;
+  const int grid = min(ntiles, ctas_per_sm * sms);
+  cudaMemsetAsync(tl.counter, 0, sizeof(int), s);
+  blend_fwd_kernel<DP, L1, PPT><<<grid, kBlock / PPT, 0, s>>>(m, c, v, tl, ps, o);
+}
+
 template <int DP>
 static void launch_fwd_dp(const DevMap& m, const DevCam& c, const ViewBufs& v, const TileLists& tl,
                           const PixelState& ps, const FwdOut& o, cudaStream_t s) {
-  const unsigned tiles = (unsigned)(c.tiles_x * c.tiles_y);
-  if (o.cot) blend_fwd_kernel<DP, true><<<tiles, kBlock, 0, s>>>(m, c, v, tl, ps, o);
-  else blend_fwd_kernel<DP, false><<<tiles, kBlock, 0, s>>>(m, c, v, tl, ps, o);
+  if (o.cot) launch_fwd_cfg<DP, true, 2>(m, c, v, tl, ps, o, s);
+  else launch_fwd_cfg<DP, false, 2>(m, c, v, tl, ps, o, s);
 }
 
 void launch_blend_fwd(const DevMap& m, const DevCam& c, const ViewBufs& v, const TileLists& tl,

@@ -142,6 +142,8 @@ struct lgs_saved {
   uint16_t* keys = nullptr;  // sorted tile ids
   uint32_t* vals = nullptr;  // sorted map indices
   uint2* ranges = nullptr;
+  uint32_t* order = nullptr;  // tiles by decreasing list length
+  int* counter = nullptr;     // persistent-scheduler slot counter
   PixelState ps{};
   float* cot = nullptr;     // fused L1 cotangents [H][W][4 + DP]
   double* loss = nullptr;
@@ -299,6 +301,8 @@ void free_saved(lgs_saved* t) {
   dfree(ctx, t->keys);
   dfree(ctx, t->vals);
   dfree(ctx, t->ranges);
+  dfree(ctx, t->order);
+  dfree(ctx, t->counter);
   dfree(ctx, t->ps.final_t);
   dfree(ctx, t->ps.n_contrib);
   dfree(ctx, t->ps.depth);
@@ -504,6 +508,8 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
   TRYB(dalloc(ctx, &t->vb.dkey, n));
   TRYB(dalloc(ctx, &t->vb.iota, n));
   TRYB(dalloc(ctx, &t->ranges, ntiles));
+  TRYB(dalloc(ctx, &t->order, ntiles));
+  TRYB(dalloc(ctx, &t->counter, 1));
   TRYB(dalloc(ctx, &t->ps.final_t, npix));
   TRYB(dalloc(ctx, &t->ps.n_contrib, npix));
   TRYB(dalloc(ctx, &t->ps.depth, npix));
@@ -577,6 +583,11 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
     dfree(ctx, vals_in);
   }
   dfree(ctx, temp);
+  {
+    PhaseScope ph(ctx, PH_TILE_SORT);
+    launch_tile_order(t->ranges, ntiles, t->order, s);  // longest tile list first
+  }
+  ctx->launches++;
   dfree(ctx, dkey_sorted);
   dfree(ctx, idx_sorted);
   dfree(ctx, incl);
@@ -616,7 +627,7 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
   }
   {
     PhaseScope ph(ctx, PH_BLEND_FWD);
-    launch_blend_fwd(map->dm, dc, t->vb, TileLists{t->vals, t->ranges}, t->ps, fo, s);
+    launch_blend_fwd(map->dm, dc, t->vb, TileLists{t->vals, t->ranges, t->order, t->counter}, t->ps, fo, s);
   }
   ctx->launches++;
   CUDAB(cudaGetLastError());
@@ -670,7 +681,7 @@ lgs_status run_backward(lgs_ctx* ctx, const lgs_saved* t, const BwdIn& in_dev, l
   LGS_CUDA(cudaMemsetAsync(gacc, 0, sizeof(float) * (size_t)n * slots, s));
   {
     PhaseScope ph(ctx, PH_BLEND_BWD);
-    launch_blend_bwd(t->dm, t->cam, t->vb, TileLists{t->vals, t->ranges}, t->ps, in_dev, gacc, slots, s);
+    launch_blend_bwd(t->dm, t->cam, t->vb, TileLists{t->vals, t->ranges, t->order, t->counter}, t->ps, in_dev, gacc, slots, s);
   }
   ctx->launches += 2;
 

@@ -23,9 +23,14 @@ struct ViewBufs {
 
 // Tile lists for the blend kernels.
 struct TileLists {
-  const uint32_t* vals;  // map index per list entry, sorted by (tile, depth, index)
-  const uint2* ranges;   // [tiles] begin, end
+  const uint32_t* vals;    // map index per list entry, sorted by (tile, depth, index)
+  const uint2* ranges;     // [tiles] begin, end
+  const uint32_t* order;   // [tiles] tile ids, longest list first (persistent scheduler)
+  int* counter;            // scheduler slot counter (reset by the launcher)
 };
+
+// Longest-first tile order (binning_fast.cu): buckets by floor(log2(list length)).
+void launch_tile_order(const uint2* ranges, int ntiles, uint32_t* order, cudaStream_t s);
 
 // Per-pixel forward state kept for the backward pass.
 struct PixelState {
