@@ -69,8 +69,8 @@ __global__ void __launch_bounds__(kBlock / PPT) blend_bwd_kernel(DevMap m, DevCa
   __shared__ int s_slot;
   const int tid = threadIdx.x;
   const int lane = tid & 31;
-  const int lx = tid & (kTile - 1);
-  const int ly0 = (tid >> 4) * PPT;  // first tile row of this thread's strip
+  int lx, ly0;  // this thread's column and first row in the tile
+  thread_pixels<PPT>(tid, lx, ly0);
   const int ntiles = c.tiles_x * c.tiles_y;
 
   for (int tile = next_tile(tl, ntiles, &s_slot); tile >= 0; tile = next_tile(tl, ntiles, &s_slot)) {

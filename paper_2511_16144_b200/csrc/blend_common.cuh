@@ -35,6 +35,16 @@ __device__ __forceinline__ bool in_rect(uint2 r, int px, int py) {
          py <= (int)(r.y >> 16);
 }
 
+// Pixels of thread `tid` inside the 16x16 tile when each thread owns PPT vertically stacked pixels:
+// column lx, rows ly0 .. ly0 + PPT - 1.  A warp covers a compact 8-column block (8 x 4 PPT pixels)
+// rather than a 16-wide strip, so a small splat's footprint fills more of the warp's lanes.
+template <int PPT>
+__device__ __forceinline__ void thread_pixels(int tid, int& lx, int& ly0) {
+  const int warp = tid >> 5, lane = tid & 31;
+  lx = (warp & 1) * 8 + (lane & 7);
+  ly0 = (warp >> 1) * (4 * PPT) + (lane >> 3) * PPT;
+}
+
 // Persistent-CTA tile scheduler: CTAs pull tile slots from a global counter; slot i is the i-th
 // longest tile list (TileLists::order), so the long tiles start first and the tail is short.
 __device__ __forceinline__ int next_tile(const TileLists& tl, int ntiles, int* s_slot) {

@@ -42,8 +42,8 @@ __global__ void __launch_bounds__(kBlock / PPT) blend_fwd_kernel(DevMap m, DevCa
   __shared__ float s_loss[NT / 32];
   __shared__ int s_slot;
   const int tid = threadIdx.x;
-  const int lx = tid & (kTile - 1);
-  const int ly0 = (tid >> 4) * PPT;
+  int lx, ly0;  // this thread's column and first row in the tile
+  thread_pixels<PPT>(tid, lx, ly0);
   const int ntiles = c.tiles_x * c.tiles_y;
   float loss = 0.f;
 
