@@ -51,9 +51,21 @@ void launch_pack_map(const float* pos, const float* rot, const float* log_s, con
 // ------------------------------------------------------------------------------------------
 // K1
 // ------------------------------------------------------------------------------------------
+constexpr int kPreThreads = 128;
+
 template <int DEG>
-__global__ void __launch_bounds__(256) preprocess_kernel(DevMap m, DevCam c, ViewBufs v) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(kPreThreads) preprocess_kernel(DevMap m, DevCam c, ViewBufs v) {
+  constexpr int KS = 3 * (DEG + 1) * (DEG + 1);
+  constexpr int SS = KS + 1 - KS % 2;  // odd row stride: conflict-free per-thread rows
+  __shared__ float s_sh[DEG > 0 ? kPreThreads * SS : 1];
+  const int64_t i0 = (int64_t)blockIdx.x * kPreThreads;
+  const int64_t i = i0 + threadIdx.x;
+  if (DEG > 0) {  // the CTA's [128][K][3] SH block, loaded coalesced
+    const int nloc = (int)min((int64_t)kPreThreads, m.n - i0);
+    const float* src = m.sh + i0 * KS;
+    for (int j = threadIdx.x; j < nloc * KS; j += kPreThreads) s_sh[(j / KS) * SS + j % KS] = __ldg(src + j);
+    __syncthreads();
+  }
   if (i >= m.n) return;
   v.iota[i] = (uint32_t)i;
   const float4 po = m.pos_opa[i];
@@ -145,11 +157,12 @@ __global__ void __launch_bounds__(256) preprocess_kernel(DevMap m, DevCam c, Vie
 
   // colour (renderer.cpp:128; SH extension)
   constexpr int K = (DEG + 1) * (DEG + 1);
-  const float* sh = m.sh + i * (K * 3);
   float col[3];
   if (DEG == 0) {
+    const float* sh = m.sh + i * 3;
     col[0] = sh[0]; col[1] = sh[1]; col[2] = sh[2];
   } else {
+    const float* sh = s_sh + threadIdx.x * SS;
     float dx = P0 - c.cc[0], dy = P1 - c.cc[1], dz = P2 - c.cc[2];
     const float dn = sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
     const float idn = 1.0f / dn;
@@ -158,9 +171,9 @@ __global__ void __launch_bounds__(256) preprocess_kernel(DevMap m, DevCam c, Vie
     sh_basis_f32(DEG, dx, dy, dz, b);
 #pragma unroll
     for (int ch = 0; ch < 3; ++ch) {
-      float acc = __ldg(sh + ch);
+      float acc = sh[ch];
 #pragma unroll
-      for (int k = 1; k < K; ++k) acc = fmaf(b[k], __ldg(sh + k * 3 + ch), acc);
+      for (int k = 1; k < K; ++k) acc = fmaf(b[k], sh[k * 3 + ch], acc);
       col[ch] = acc;
     }
   }
@@ -169,7 +182,7 @@ __global__ void __launch_bounds__(256) preprocess_kernel(DevMap m, DevCam c, Vie
 
 void launch_preprocess(const DevMap& m, const DevCam& c, const ViewBufs& v, cudaStream_t s) {
   if (m.n == 0) return;
-  const int threads = 256;
+  const int threads = kPreThreads;
   const unsigned blocks = (unsigned)((m.n + threads - 1) / threads);
   switch (m.deg) {
     case 0: preprocess_kernel<0><<<blocks, threads, 0, s>>>(m, c, v); break;

@@ -15,27 +15,56 @@
 
 namespace lgs {
 
+constexpr int kPbThreads = 128;
+
+// Shared-memory row stride (floats) of the per-Gaussian SH block: odd, so thread t's row starts in
+// bank t * stride mod 32 and the 32 lanes of a warp hit 32 different banks.
+template <int DEG>
+constexpr int sh_stride() { return 3 * (DEG + 1) * (DEG + 1) + 1 - (3 * (DEG + 1) * (DEG + 1)) % 2; }
+
+// AoS <-> per-thread rows through shared memory: global side fully coalesced.
+__device__ __forceinline__ void stage_in(float* s, int stride, const float* __restrict__ src, int nloc, int width) {
+  for (int j = threadIdx.x; j < nloc * width; j += blockDim.x) s[(j / width) * stride + j % width] = __ldg(src + j);
+}
+__device__ __forceinline__ void stage_out(const float* s, int stride, float* dst, int nloc, int width, bool accum) {
+  for (int j = threadIdx.x; j < nloc * width; j += blockDim.x) {
+    const float val = s[(j / width) * stride + j % width];
+    if (accum) dst[j] += val;
+    else dst[j] = val;
+  }
+}
+
 template <int DEG, int DP, int SLOTS>
-__global__ void __launch_bounds__(256) preprocess_bwd_kernel(DevMap m, DevCam c, ViewBufs v,
-                                                               const float* __restrict__ gacc, GradOut g) {
+__global__ void __launch_bounds__(kPbThreads) preprocess_bwd_kernel(DevMap m, DevCam c, ViewBufs v,
+                                                                      const float* __restrict__ gacc, GradOut g) {
   constexpr int K = (DEG + 1) * (DEG + 1);
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  constexpr int KS = 3 * K;
+  constexpr int SS = sh_stride<DEG>();
+  __shared__ float s_sh[kPbThreads * SS];  // SH coefficients in, SH gradients out (in place)
+  __shared__ float s_pos[kPbThreads * 3];
+  __shared__ float s_ls[kPbThreads * 3];
+  const int tid = threadIdx.x;
+  const int64_t i0 = (int64_t)blockIdx.x * kPbThreads;
+  const int64_t i = i0 + tid;
   const int64_t n = m.n;
+  const int nloc = (int)min((int64_t)kPbThreads, n - i0);
+  if (DEG > 0) stage_in(s_sh, SS, m.sh + i0 * KS, nloc, KS);
+  __syncthreads();
+  float* my_sh = s_sh + tid * SS;
   float pose[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  const bool accum = g.accumulate != 0;
   if (i < n) {
     float o_pos[3] = {0.f, 0.f, 0.f}, o_rot[4] = {0.f, 0.f, 0.f, 0.f}, o_ls[3] = {0.f, 0.f, 0.f};
     float o_op = 0.f;
-    const bool accum = g.accumulate != 0;
-    // results are streamed out as soon as they are final (keeps the register footprint small)
     auto store = [accum](float* p, int64_t idx, float val) {
       if (accum) p[idx] += val;
       else p[idx] = val;
     };
     const bool visible = v.tiles[i] != 0;
-    if (!visible && !accum) {
-      if (g.sh)
-        for (int k = 0; k < K * 3; ++k) g.sh[i * (K * 3) + k] = 0.f;
-      if (DP > 0 && g.feature)
+    if (!visible) {
+#pragma unroll
+      for (int k = 0; k < KS; ++k) my_sh[k] = 0.f;
+      if (DP > 0 && g.feature && !accum)
         for (int k = 0; k < m.d; ++k) g.feature[(int64_t)k * n + i] = 0.f;
     }
 
@@ -62,13 +91,11 @@ __global__ void __launch_bounds__(256) preprocess_bwd_kernel(DevMap m, DevCam c,
       // ---- colour -> SH (renderer.cpp:259-261 for K = 1) ------------------------------------
       const float gc[3] = {a2.x, a2.y, a2.z};
       if (DEG == 0 || (gc[0] == 0.f && gc[1] == 0.f && gc[2] == 0.f)) {
-        if (g.sh) {
-          store(g.sh, i * (K * 3) + 0, gc[0]);
-          store(g.sh, i * (K * 3) + 1, gc[1]);
-          store(g.sh, i * (K * 3) + 2, gc[2]);
-          if (!accum)
-            for (int k = 3; k < K * 3; ++k) g.sh[i * (K * 3) + k] = 0.f;
-        }
+        my_sh[0] = gc[0];
+        my_sh[1] = gc[1];
+        my_sh[2] = gc[2];
+#pragma unroll
+        for (int k = 3; k < KS; ++k) my_sh[k] = 0.f;
       } else {
         const float dr[3] = {P[0] - c.cc[0], P[1] - c.cc[1], P[2] - c.cc[2]};
         const float nr = sqrtf(dr[0] * dr[0] + dr[1] * dr[1] + dr[2] * dr[2]);
@@ -78,15 +105,14 @@ __global__ void __launch_bounds__(256) preprocess_bwd_kernel(DevMap m, DevCam c,
         float db[16][3];
         sh_basis_f32(DEG, dn[0], dn[1], dn[2], b);
         sh_basis_grad_f32(DEG, dn[0], dn[1], dn[2], db);
-        const float* coef = m.sh + (size_t)i * K * 3;
         float gdn[3] = {0.f, 0.f, 0.f};
 #pragma unroll
         for (int k = 0; k < K; ++k) {
           float s = 0.f;
 #pragma unroll
           for (int ch = 0; ch < 3; ++ch) {
-            if (g.sh) store(g.sh, i * (K * 3) + k * 3 + ch, b[k] * gc[ch]);
-            s = fmaf(__ldg(coef + k * 3 + ch), gc[ch], s);
+            s = fmaf(my_sh[k * 3 + ch], gc[ch], s);  // coefficient (staged), then overwritten by its grad
+            my_sh[k * 3 + ch] = b[k] * gc[ch];
           }
           gdn[0] = fmaf(db[k][0], s, gdn[0]);
           gdn[1] = fmaf(db[k][1], s, gdn[1]);
@@ -278,20 +304,30 @@ __global__ void __launch_bounds__(256) preprocess_bwd_kernel(DevMap m, DevCam c,
     }
 
     // ---- dense writes in the reference layouts (zeros for culled Gaussians) -------------------
-    if (g.position)
 #pragma unroll
-      for (int a = 0; a < 3; ++a) store(g.position, i * 3 + a, o_pos[a]);
-    if (g.rotation)
-#pragma unroll
-      for (int a = 0; a < 4; ++a) store(g.rotation, i * 4 + a, o_rot[a]);
-    if (g.log_scale)
-#pragma unroll
-      for (int a = 0; a < 3; ++a) store(g.log_scale, i * 3 + a, o_ls[a]);
+    for (int a = 0; a < 3; ++a) {
+      s_pos[tid * 3 + a] = o_pos[a];
+      s_ls[tid * 3 + a] = o_ls[a];
+    }
+    if (g.rotation) {  // (w,x,y,z), one 16-byte store
+      float4* rp = reinterpret_cast<float4*>(g.rotation) + i;
+      float4 r4 = make_float4(o_rot[0], o_rot[1], o_rot[2], o_rot[3]);
+      if (accum) {
+        const float4 old = *rp;
+        r4 = make_float4(old.x + r4.x, old.y + r4.y, old.z + r4.z, old.w + r4.w);
+      }
+      *rp = r4;
+    }
     if (g.opacity_logit) store(g.opacity_logit, i, o_op);
   }
+  __syncthreads();
+  // [N][3] and [N][K][3] blocks of this CTA's Gaussians leave through shared memory, coalesced
+  if (g.position) stage_out(s_pos, 3, g.position + i0 * 3, nloc, 3, accum);
+  if (g.log_scale) stage_out(s_ls, 3, g.log_scale + i0 * 3, nloc, 3, accum);
+  if (g.sh) stage_out(s_sh, SS, g.sh + i0 * KS, nloc, KS, accum);
 
   if (g.pose) {  // block reduction of the pose gradient, one double atomic per value per block
-    __shared__ float s_pose[8][6];
+    __shared__ float s_pose[kPbThreads / 32][6];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
     for (int a = 0; a < 6; ++a) {
@@ -312,8 +348,8 @@ __global__ void __launch_bounds__(256) preprocess_bwd_kernel(DevMap m, DevCam c,
 template <int DEG, int DP>
 static void launch_pb(const DevMap& m, const DevCam& c, const ViewBufs& v, const float* gacc, const GradOut& g,
                       cudaStream_t s) {
-  const unsigned blocks = (unsigned)((m.n + 255) / 256);
-  preprocess_bwd_kernel<DEG, DP, slots_for(DP)><<<blocks, 256, 0, s>>>(m, c, v, gacc, g);
+  const unsigned blocks = (unsigned)((m.n + kPbThreads - 1) / kPbThreads);
+  preprocess_bwd_kernel<DEG, DP, slots_for(DP)><<<blocks, kPbThreads, 0, s>>>(m, c, v, gacc, g);
 }
 
 template <int DEG>
