@@ -165,6 +165,53 @@ __device__ __forceinline__ void sh_basis_grad_f32(int deg, float x, float y, flo
   db[15][0] = kShC3[6] * (3.0f * xx - 3.0f * yy); db[15][1] = kShC3[6] * (-6.0f * x * y);
 }
 
+// Block-staged AoS transfers: a CTA's contiguous [nloc][W] float block (16-byte aligned base) moves
+// between global memory (float4 accesses, coalesced) and per-thread shared-memory rows of stride S
+// (odd S keeps each thread's row in distinct banks).
+template <int W, int S, int NT>
+__device__ __forceinline__ void stage_rows_in(float* __restrict__ s, const float* __restrict__ src, int nloc) {
+  const int total = nloc * W;
+  const int n4 = total >> 2;
+  const float4* src4 = reinterpret_cast<const float4*>(src);
+#pragma unroll 4
+  for (int j4 = threadIdx.x; j4 < n4; j4 += NT) {
+    const float4 v = __ldg(src4 + j4);
+    const int j = j4 * 4;
+    s[((j + 0) / W) * S + (j + 0) % W] = v.x;
+    s[((j + 1) / W) * S + (j + 1) % W] = v.y;
+    s[((j + 2) / W) * S + (j + 2) % W] = v.z;
+    s[((j + 3) / W) * S + (j + 3) % W] = v.w;
+  }
+  for (int j = n4 * 4 + threadIdx.x; j < total; j += NT) s[(j / W) * S + j % W] = __ldg(src + j);
+}
+
+template <int W, int S, int NT>
+__device__ __forceinline__ void stage_rows_out(const float* __restrict__ s, float* __restrict__ dst, int nloc,
+                                               bool accum) {
+  const int total = nloc * W;
+  const int n4 = total >> 2;
+  float4* dst4 = reinterpret_cast<float4*>(dst);
+  const bool aligned = (reinterpret_cast<uintptr_t>(dst) & 15u) == 0;
+  if (aligned) {
+#pragma unroll 4
+    for (int j4 = threadIdx.x; j4 < n4; j4 += NT) {
+      const int j = j4 * 4;
+      float4 v = make_float4(s[((j + 0) / W) * S + (j + 0) % W], s[((j + 1) / W) * S + (j + 1) % W],
+                             s[((j + 2) / W) * S + (j + 2) % W], s[((j + 3) / W) * S + (j + 3) % W]);
+      if (accum) {
+        const float4 o = dst4[j4];
+        v = make_float4(o.x + v.x, o.y + v.y, o.z + v.z, o.w + v.w);
+      }
+      dst4[j4] = v;
+    }
+  }
+  for (int j = (aligned ? n4 * 4 : 0) + threadIdx.x; j < total; j += NT) {
+    const float v = s[(j / W) * S + j % W];
+    if (accum) dst[j] += v;
+    else dst[j] = v;
+  }
+}
+
 __device__ __forceinline__ float fast_exp2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));

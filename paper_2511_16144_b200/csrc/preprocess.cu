@@ -60,10 +60,9 @@ __global__ void __launch_bounds__(kPreThreads) preprocess_kernel(DevMap m, DevCa
   __shared__ float s_sh[DEG > 0 ? kPreThreads * SS : 1];
   const int64_t i0 = (int64_t)blockIdx.x * kPreThreads;
   const int64_t i = i0 + threadIdx.x;
-  if (DEG > 0) {  // the CTA's [128][K][3] SH block, loaded coalesced
+  if (DEG > 0) {  // the CTA's [128][K][3] SH block, loaded coalesced (float4)
     const int nloc = (int)min((int64_t)kPreThreads, m.n - i0);
-    const float* src = m.sh + i0 * KS;
-    for (int j = threadIdx.x; j < nloc * KS; j += kPreThreads) s_sh[(j / KS) * SS + j % KS] = __ldg(src + j);
+    stage_rows_in<KS, SS, kPreThreads>(s_sh, m.sh + i0 * KS, nloc);
     __syncthreads();
   }
   if (i >= m.n) return;

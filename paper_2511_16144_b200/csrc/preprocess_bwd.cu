@@ -22,18 +22,6 @@ constexpr int kPbThreads = 128;
 template <int DEG>
 constexpr int sh_stride() { return 3 * (DEG + 1) * (DEG + 1) + 1 - (3 * (DEG + 1) * (DEG + 1)) % 2; }
 
-// AoS <-> per-thread rows through shared memory: global side fully coalesced.
-__device__ __forceinline__ void stage_in(float* s, int stride, const float* __restrict__ src, int nloc, int width) {
-  for (int j = threadIdx.x; j < nloc * width; j += blockDim.x) s[(j / width) * stride + j % width] = __ldg(src + j);
-}
-__device__ __forceinline__ void stage_out(const float* s, int stride, float* dst, int nloc, int width, bool accum) {
-  for (int j = threadIdx.x; j < nloc * width; j += blockDim.x) {
-    const float val = s[(j / width) * stride + j % width];
-    if (accum) dst[j] += val;
-    else dst[j] = val;
-  }
-}
-
 template <int DEG, int DP, int SLOTS>
 __global__ void __launch_bounds__(kPbThreads) preprocess_bwd_kernel(DevMap m, DevCam c, ViewBufs v,
                                                                       const float* __restrict__ gacc, GradOut g) {
@@ -48,7 +36,7 @@ __global__ void __launch_bounds__(kPbThreads) preprocess_bwd_kernel(DevMap m, De
   const int64_t i = i0 + tid;
   const int64_t n = m.n;
   const int nloc = (int)min((int64_t)kPbThreads, n - i0);
-  if (DEG > 0) stage_in(s_sh, SS, m.sh + i0 * KS, nloc, KS);
+  if (DEG > 0) stage_rows_in<KS, SS, kPbThreads>(s_sh, m.sh + i0 * KS, nloc);
   __syncthreads();
   float* my_sh = s_sh + tid * SS;
   float pose[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
@@ -309,22 +297,27 @@ __global__ void __launch_bounds__(kPbThreads) preprocess_bwd_kernel(DevMap m, De
       s_pos[tid * 3 + a] = o_pos[a];
       s_ls[tid * 3 + a] = o_ls[a];
     }
-    if (g.rotation) {  // (w,x,y,z), one 16-byte store
-      float4* rp = reinterpret_cast<float4*>(g.rotation) + i;
-      float4 r4 = make_float4(o_rot[0], o_rot[1], o_rot[2], o_rot[3]);
-      if (accum) {
-        const float4 old = *rp;
-        r4 = make_float4(old.x + r4.x, old.y + r4.y, old.z + r4.z, old.w + r4.w);
+    if (g.rotation) {  // (w,x,y,z): one 16-byte store when the buffer is 16-byte aligned
+      if ((reinterpret_cast<uintptr_t>(g.rotation) & 15u) == 0) {
+        float4* rp = reinterpret_cast<float4*>(g.rotation) + i;
+        float4 r4 = make_float4(o_rot[0], o_rot[1], o_rot[2], o_rot[3]);
+        if (accum) {
+          const float4 old = *rp;
+          r4 = make_float4(old.x + r4.x, old.y + r4.y, old.z + r4.z, old.w + r4.w);
+        }
+        *rp = r4;
+      } else {
+#pragma unroll
+        for (int a = 0; a < 4; ++a) store(g.rotation, i * 4 + a, o_rot[a]);
       }
-      *rp = r4;
     }
     if (g.opacity_logit) store(g.opacity_logit, i, o_op);
   }
   __syncthreads();
   // [N][3] and [N][K][3] blocks of this CTA's Gaussians leave through shared memory, coalesced
-  if (g.position) stage_out(s_pos, 3, g.position + i0 * 3, nloc, 3, accum);
-  if (g.log_scale) stage_out(s_ls, 3, g.log_scale + i0 * 3, nloc, 3, accum);
-  if (g.sh) stage_out(s_sh, SS, g.sh + i0 * KS, nloc, KS, accum);
+  if (g.position) stage_rows_out<3, 3, kPbThreads>(s_pos, g.position + i0 * 3, nloc, accum);
+  if (g.log_scale) stage_rows_out<3, 3, kPbThreads>(s_ls, g.log_scale + i0 * 3, nloc, accum);
+  if (g.sh) stage_rows_out<KS, SS, kPbThreads>(s_sh, g.sh + i0 * KS, nloc, accum);
 
   if (g.pose) {  // block reduction of the pose gradient, one double atomic per value per block
     __shared__ float s_pose[kPbThreads / 32][6];
