@@ -98,9 +98,18 @@ __device__ __forceinline__ void for_each_pair(const uint2* __restrict__ rect, co
       const uint32_t gj = __shfl_sync(0xffffffffu, g, j);
       const uint32_t oj = __shfl_sync(0xffffffffu, org, j);
       const uint32_t wj = __shfl_sync(0xffffffffu, tw, j);
-      for (uint32_t i = lane; i < cj; i += 32) {
-        const uint32_t ry = i / wj;
-        f(gj, ((oj >> 16) + ry) * (uint32_t)tiles_x + (oj & 0xffffu) + (i - ry * wj));
+      const uint32_t base = (oj >> 16) * (uint32_t)tiles_x + (oj & 0xffffu);
+      const uint32_t hj = cj / wj;  // tile rows (warp-uniform)
+      if (wj <= 32) {
+        // lanes tile (32 / w) rows at a time: lane -> (row, col) computed once per Gaussian
+        const uint32_t rpi = 32u / wj;
+        const uint32_t r0 = (uint32_t)lane / wj;
+        const uint32_t col = (uint32_t)lane - r0 * wj;
+        if (r0 < rpi)
+          for (uint32_t ry = r0; ry < hj; ry += rpi) f(gj, base + ry * (uint32_t)tiles_x + col);
+      } else {
+        for (uint32_t ry = 0; ry < hj; ++ry)
+          for (uint32_t cx = lane; cx < wj; cx += 32) f(gj, base + ry * (uint32_t)tiles_x + cx);
       }
       __syncwarp();
     }
