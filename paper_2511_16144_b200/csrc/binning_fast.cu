@@ -75,42 +75,53 @@ __device__ __forceinline__ void warp_slice(const uint32_t* __restrict__ excl, co
   s1 = warp == kWarps - 1 ? hi : lower_bound_excl(excl, lo, hi, base + (uint32_t)(warp + 1) * kPairsPerWarp);
 }
 
-// Visit the (Gaussian, tile) pairs of sorted Gaussians [s0, s1) in depth order; f(g, tile) is
-// called by the lanes of one Gaussian at a time (distinct tiles), __syncwarp between Gaussians.
+// Visit the (Gaussian, tile) pairs of sorted Gaussians [s0, s1) in stream (= depth) order, 32
+// consecutive pairs per step with one pair per lane, across Gaussian boundaries (most Gaussians
+// touch fewer than 32 tiles, so one-Gaussian-per-step would leave most lanes idle).  The warp's
+// Gaussian records are loaded 32 at a time (coalesced); each lane finds the Gaussian owning its
+// pair by a 5-step shuffle search over the batch's stream offsets.  f(valid, g, tile) is called
+// by all 32 lanes; lanes are in stream order, __syncwarp between steps.
 template <typename F>
 __device__ __forceinline__ void for_each_pair(const uint2* __restrict__ rect, const uint32_t* __restrict__ tiles,
-                                              const uint32_t* __restrict__ idx_sorted, uint32_t s0, uint32_t s1,
-                                              int lane, int tiles_x, F&& f) {
+                                              const uint32_t* __restrict__ idx_sorted,
+                                              const uint32_t* __restrict__ excl, uint32_t s0, uint32_t s1, int lane,
+                                              int tiles_x, F&& f) {
   for (uint32_t b = s0; b < s1; b += 32) {
     const uint32_t s = b + lane;
-    uint32_t g = 0, cnt = 0, org = 0, tw = 1;
+    uint32_t g = 0, ex = 0xffffffffu, org = 0, tw = 1, cnt = 0;
     if (s < s1) {
       g = __ldg(idx_sorted + s);
+      ex = __ldg(excl + s);
       cnt = __ldg(tiles + g);
       const uint2 rc = __ldg(rect + g);
       const uint32_t tx0 = (rc.x & 0xffffu) / kTile, ty0 = (rc.y & 0xffffu) / kTile;
       org = tx0 | (ty0 << 16);
       tw = (rc.x >> 16) / kTile - tx0 + 1;
     }
+    const float inv_tw = 1.0f / (float)tw;
     const int nb = (int)min(32u, s1 - b);
-    for (int j = 0; j < nb; ++j) {
-      const uint32_t cj = __shfl_sync(0xffffffffu, cnt, j);
+    const uint32_t q_begin = __shfl_sync(0xffffffffu, ex, 0);
+    const uint32_t q_end = __shfl_sync(0xffffffffu, ex + cnt, nb - 1);
+    for (uint32_t qw = q_begin; qw < q_end; qw += 32) {
+      const uint32_t q = qw + (uint32_t)lane;
+      const bool valid = q < q_end;
+      int j = 0;  // last lane whose Gaussian starts at or before q
+#pragma unroll
+      for (int step = 16; step >= 1; step >>= 1) {
+        const uint32_t v = __shfl_sync(0xffffffffu, ex, j + step);
+        if (v <= q) j += step;
+      }
       const uint32_t gj = __shfl_sync(0xffffffffu, g, j);
       const uint32_t oj = __shfl_sync(0xffffffffu, org, j);
       const uint32_t wj = __shfl_sync(0xffffffffu, tw, j);
-      const uint32_t base = (oj >> 16) * (uint32_t)tiles_x + (oj & 0xffffu);
-      const uint32_t hj = cj / wj;  // tile rows (warp-uniform)
-      if (wj <= 32) {
-        // lanes tile (32 / w) rows at a time: lane -> (row, col) computed once per Gaussian
-        const uint32_t rpi = 32u / wj;
-        const uint32_t r0 = (uint32_t)lane / wj;
-        const uint32_t col = (uint32_t)lane - r0 * wj;
-        if (r0 < rpi)
-          for (uint32_t ry = r0; ry < hj; ry += rpi) f(gj, base + ry * (uint32_t)tiles_x + col);
-      } else {
-        for (uint32_t ry = 0; ry < hj; ++ry)
-          for (uint32_t cx = lane; cx < wj; cx += 32) f(gj, base + ry * (uint32_t)tiles_x + cx);
-      }
+      const uint32_t ej = __shfl_sync(0xffffffffu, ex, j);
+      const float iw = __shfl_sync(0xffffffffu, inv_tw, j);
+      const uint32_t local = q - ej;
+      uint32_t ry = __float2uint_rz((float)local * iw);  // local / wj, then exact correction
+      if (ry * wj > local) --ry;
+      else if ((ry + 1) * wj <= local) ++ry;
+      const uint32_t t = ((oj >> 16) + ry) * (uint32_t)tiles_x + (oj & 0xffffu) + (local - ry * wj);
+      f(valid, gj, t);
       __syncwarp();
     }
   }
@@ -129,8 +140,9 @@ __global__ void __launch_bounds__(kWarps * 32) tile_count_kernel(const uint2* __
   uint32_t s0, s1;
   warp_slice(excl, chunk_first, blockIdx.x, warp, s0, s1);
   __syncthreads();
-  for_each_pair(rect, tiles, idx_sorted, s0, s1, lane, tiles_x,
-                [&](uint32_t, uint32_t t) { atomicAdd(&s_hist[t], 1u); });
+  for_each_pair(rect, tiles, idx_sorted, excl, s0, s1, lane, tiles_x, [&](bool valid, uint32_t, uint32_t t) {
+    if (valid) atomicAdd(&s_hist[t], 1u);
+  });
   __syncthreads();
   for (int t = threadIdx.x; t < ntiles; t += blockDim.x) counts[(size_t)t * nchunks + blockIdx.x] = s_hist[t];
 }
@@ -162,9 +174,12 @@ __global__ void __launch_bounds__(kWarps * 32) tile_scatter_kernel(const uint2* 
   uint32_t s0, s1;
   warp_slice(excl, chunk_first, blockIdx.x, warp, s0, s1);
   __syncwarp();
-  // pass 1: this warp's per-tile pair counts (distinct tiles per Gaussian: no atomics)
-  for_each_pair(rect, tiles, idx_sorted, s0, s1, lane, tiles_x,
-                [&](uint32_t, uint32_t t) { my[t] = (uint16_t)(my[t] + 1); });
+  // pass 1: this warp's per-tile pair counts; lanes of one step that share a tile are grouped by
+  // __match_any_sync and their leader adds the group size (no atomics, u16 table)
+  for_each_pair(rect, tiles, idx_sorted, excl, s0, s1, lane, tiles_x, [&](bool valid, uint32_t, uint32_t t) {
+    const uint32_t peers = __match_any_sync(0xffffffffu, valid ? t : 0xffffffffu);
+    if (valid && lane == __ffs(peers) - 1) my[t] = (uint16_t)(my[t] + __popc(peers));
+  });
   __syncthreads();
   // per tile: offset of each warp within the chunk = counts of the earlier warps
   for (int t = threadIdx.x; t < ntiles; t += blockDim.x) {
@@ -177,11 +192,18 @@ __global__ void __launch_bounds__(kWarps * 32) tile_scatter_kernel(const uint2* 
     }
   }
   __syncthreads();
-  // pass 2: depth-ordered writes
-  for_each_pair(rect, tiles, idx_sorted, s0, s1, lane, tiles_x, [&](uint32_t g, uint32_t t) {
-    const uint32_t r = my[t];
-    my[t] = (uint16_t)(r + 1);
-    vals[s_coff[t] + r] = g;
+  // pass 2: depth-ordered writes.  Lanes are in stream order, so a lane's rank among the lanes of
+  // its step that share its tile (popc of the lower peers) keeps the stable (depth, index) order.
+  for_each_pair(rect, tiles, idx_sorted, excl, s0, s1, lane, tiles_x, [&](bool valid, uint32_t g, uint32_t t) {
+    const uint32_t peers = __match_any_sync(0xffffffffu, valid ? t : 0xffffffffu);
+    const int leader = __ffs(peers) - 1;
+    uint32_t base = 0;
+    if (valid && lane == leader) {
+      base = my[t];
+      my[t] = (uint16_t)(base + __popc(peers));
+    }
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (valid) vals[s_coff[t] + base + __popc(peers & ((1u << lane) - 1u))] = g;
   });
 }
 
