@@ -34,45 +34,33 @@ constexpr int kPairsPerWarp = 1024;
 constexpr int kPairsPerChunk = kWarps * kPairsPerWarp;
 constexpr int kMaxFastTiles = 8192;  // warp tables: 8 x 8192 x u16 = 128 KB shared memory
 
-// excl[s] (in place over the gathered counts) and chunk_first[c] = first sorted Gaussian whose
-// stream offset is >= c * kPairsPerChunk (c in [0, nchunks]); culled Gaussians (count 0, sorted
-// last) map past the last chunk.
+// excl[s] (in place over the gathered counts) and slice_first[w] = first sorted Gaussian whose
+// stream offset is >= w * kPairsPerWarp, for every warp slice w in [0, nchunks * kWarps]; culled
+// Gaussians (count 0, sorted last) map past the last slice.
 __global__ void chunk_bounds_kernel(uint32_t* __restrict__ cnt_to_excl, const uint32_t* __restrict__ incl, int64_t n,
-                                    int nchunks, uint32_t* __restrict__ chunk_first) {
+                                    int nslices, uint32_t* __restrict__ slice_first) {
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n) return;
   const uint32_t cnt = cnt_to_excl[s];
   const uint32_t excl = incl[s] - cnt;
-  const int c = cnt ? (int)(excl / kPairsPerChunk) : nchunks;
+  const int c = cnt ? (int)(excl / kPairsPerWarp) : nslices;
   int cp = -1;
   if (s > 0) {
     const uint32_t cntp = incl[s - 1] - (s > 1 ? incl[s - 2] : 0u);
-    cp = cntp ? (int)((incl[s - 1] - cntp) / kPairsPerChunk) : nchunks;
+    cp = cntp ? (int)((incl[s - 1] - cntp) / kPairsPerWarp) : nslices;
   }
-  for (int cc = cp + 1; cc <= c; ++cc) chunk_first[cc] = (uint32_t)s;
+  for (int cc = cp + 1; cc <= c; ++cc) slice_first[cc] = (uint32_t)s;
   if (s == n - 1)
-    for (int cc = c + 1; cc <= nchunks; ++cc) chunk_first[cc] = (uint32_t)n;
+    for (int cc = c + 1; cc <= nslices; ++cc) slice_first[cc] = (uint32_t)n;
   cnt_to_excl[s] = excl;
 }
 
-// first s in [lo, hi) with excl[s] >= key (excl is non-decreasing over visible Gaussians)
-__device__ __forceinline__ uint32_t lower_bound_excl(const uint32_t* __restrict__ excl, uint32_t lo, uint32_t hi,
-                                                     uint32_t key) {
-  while (lo < hi) {
-    const uint32_t mid = (lo + hi) >> 1;
-    if (__ldg(excl + mid) < key) lo = mid + 1;
-    else hi = mid;
-  }
-  return lo;
-}
-
 // Sorted-Gaussian range [s0, s1) of warp `warp` of chunk `c`.
-__device__ __forceinline__ void warp_slice(const uint32_t* __restrict__ excl, const uint32_t* __restrict__ chunk_first,
-                                           int c, int warp, uint32_t& s0, uint32_t& s1) {
-  const uint32_t lo = __ldg(chunk_first + c), hi = __ldg(chunk_first + c + 1);
-  const uint32_t base = (uint32_t)c * kPairsPerChunk;
-  s0 = warp == 0 ? lo : lower_bound_excl(excl, lo, hi, base + (uint32_t)warp * kPairsPerWarp);
-  s1 = warp == kWarps - 1 ? hi : lower_bound_excl(excl, lo, hi, base + (uint32_t)(warp + 1) * kPairsPerWarp);
+__device__ __forceinline__ void warp_slice(const uint32_t* __restrict__ slice_first, int c, int warp, uint32_t& s0,
+                                           uint32_t& s1) {
+  const int w = c * kWarps + warp;
+  s0 = __ldg(slice_first + w);
+  s1 = __ldg(slice_first + w + 1);
 }
 
 // Visit the (Gaussian, tile) pairs of sorted Gaussians [s0, s1) in stream (= depth) order, 32
@@ -138,7 +126,7 @@ __global__ void __launch_bounds__(kWarps * 32) tile_count_kernel(const uint2* __
   for (int t = threadIdx.x; t < ntiles; t += blockDim.x) s_hist[t] = 0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t s0, s1;
-  warp_slice(excl, chunk_first, blockIdx.x, warp, s0, s1);
+  warp_slice(chunk_first, blockIdx.x, warp, s0, s1);
   __syncthreads();
   for_each_pair(rect, tiles, idx_sorted, excl, s0, s1, lane, tiles_x, [&](bool valid, uint32_t, uint32_t t) {
     if (valid) atomicAdd(&s_hist[t], 1u);
@@ -172,7 +160,7 @@ __global__ void __launch_bounds__(kWarps * 32) tile_scatter_kernel(const uint2* 
   for (int t = lane; t < ntiles; t += 32) my[t] = 0;
   for (int t = threadIdx.x; t < ntiles; t += blockDim.x) s_coff[t] = offs[(size_t)t * nchunks + blockIdx.x];
   uint32_t s0, s1;
-  warp_slice(excl, chunk_first, blockIdx.x, warp, s0, s1);
+  warp_slice(chunk_first, blockIdx.x, warp, s0, s1);
   __syncwarp();
   // pass 1: this warp's per-tile pair counts; lanes of one step that share a tile are grouped by
   // __match_any_sync and their leader adds the group size (no atomics, u16 table)
@@ -249,7 +237,7 @@ size_t fast_binning_scratch_bytes(int64_t pairs, int ntiles) {
   const size_t cells = (size_t)nchunks_for(pairs) * (size_t)ntiles;
   size_t scan = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, scan, (uint32_t*)nullptr, (uint32_t*)nullptr, (int)cells);
-  return sizeof(uint32_t) * (cells * 2 + (size_t)nchunks_for(pairs) + 1) + scan + 256;
+  return sizeof(uint32_t) * (cells * 2 + (size_t)nchunks_for(pairs) * kWarps + 1) + scan + 256;
 }
 
 void launch_fast_binning(const ViewBufs& v, const uint32_t* idx_sorted, uint32_t* cnt_sorted, const uint32_t* incl,
@@ -264,7 +252,7 @@ void launch_fast_binning(const ViewBufs& v, const uint32_t* idx_sorted, uint32_t
   uint32_t* counts = scratch;
   uint32_t* offs = counts + cells;
   uint32_t* chunk_first = offs + cells;
-  void* temp = chunk_first + nchunks + 1;
+  void* temp = chunk_first + nchunks * kWarps + 1;
   size_t temp_bytes = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, temp_bytes, counts, offs, (int)cells);
   static bool attr_set = false;
@@ -276,7 +264,7 @@ void launch_fast_binning(const ViewBufs& v, const uint32_t* idx_sorted, uint32_t
     attr_set = true;
   }
   const uint32_t* excl = cnt_sorted;  // rewritten in place by chunk_bounds_kernel
-  chunk_bounds_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(cnt_sorted, incl, n, nchunks, chunk_first);
+  chunk_bounds_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(cnt_sorted, incl, n, nchunks * kWarps, chunk_first);
   const int threads = kWarps * 32;
   tile_count_kernel<<<nchunks, threads, sizeof(uint32_t) * ntiles, s>>>(v.rect, v.tiles, idx_sorted, excl, chunk_first,
                                                                         ntiles, tiles_x, nchunks, counts);
