@@ -63,53 +63,46 @@ __device__ __forceinline__ void warp_slice(const uint32_t* __restrict__ slice_fi
   s1 = __ldg(slice_first + w + 1);
 }
 
-// Visit the (Gaussian, tile) pairs of sorted Gaussians [s0, s1) in stream (= depth) order, 32
-// consecutive pairs per step with one pair per lane, across Gaussian boundaries (most Gaussians
-// touch fewer than 32 tiles, so one-Gaussian-per-step would leave most lanes idle).  The warp's
-// Gaussian records are loaded 32 at a time (coalesced); each lane finds the Gaussian owning its
-// pair by a 5-step shuffle search over the batch's stream offsets.  f(valid, g, tile) is called
-// by all 32 lanes; lanes are in stream order, __syncwarp between steps.
+// Visit the (Gaussian, tile) pairs of sorted Gaussians [s0, s1) in depth order, one Gaussian per
+// warp step: lane l takes column l mod w of rows l / w, l / w + 32 / w, ... of the Gaussian's
+// w x h tile rect (the lane's row / column come from one float multiply by 1/w: exact for
+// lane < 32, w <= 512), so a Gaussian's lanes hit distinct tiles and f(g, tile) needs no
+// atomics or ranking; __syncwarp orders consecutive Gaussians.  The warp's records are loaded
+// 32 at a time (coalesced) and broadcast by shuffle.
 template <typename F>
 __device__ __forceinline__ void for_each_pair(const uint2* __restrict__ rect, const uint32_t* __restrict__ tiles,
-                                              const uint32_t* __restrict__ idx_sorted,
-                                              const uint32_t* __restrict__ excl, uint32_t s0, uint32_t s1, int lane,
-                                              int tiles_x, F&& f) {
+                                              const uint32_t* __restrict__ idx_sorted, uint32_t s0, uint32_t s1,
+                                              int lane, int tiles_x, F&& f) {
   for (uint32_t b = s0; b < s1; b += 32) {
     const uint32_t s = b + lane;
-    uint32_t g = 0, ex = 0xffffffffu, org = 0, tw = 1, cnt = 0;
+    uint32_t g = 0, base = 0, wh = 0;  // wh = w | h << 16
+    float inv_w = 1.0f;
     if (s < s1) {
       g = __ldg(idx_sorted + s);
-      ex = __ldg(excl + s);
-      cnt = __ldg(tiles + g);
       const uint2 rc = __ldg(rect + g);
       const uint32_t tx0 = (rc.x & 0xffffu) / kTile, ty0 = (rc.y & 0xffffu) / kTile;
-      org = tx0 | (ty0 << 16);
-      tw = (rc.x >> 16) / kTile - tx0 + 1;
+      const uint32_t w = (rc.x >> 16) / kTile - tx0 + 1, h = (rc.y >> 16) / kTile - ty0 + 1;
+      base = ty0 * (uint32_t)tiles_x + tx0;
+      wh = w | (h << 16);
+      inv_w = 1.0f / (float)w;
     }
-    const float inv_tw = 1.0f / (float)tw;
     const int nb = (int)min(32u, s1 - b);
-    const uint32_t q_begin = __shfl_sync(0xffffffffu, ex, 0);
-    const uint32_t q_end = __shfl_sync(0xffffffffu, ex + cnt, nb - 1);
-    for (uint32_t qw = q_begin; qw < q_end; qw += 32) {
-      const uint32_t q = qw + (uint32_t)lane;
-      const bool valid = q < q_end;
-      int j = 0;  // last lane whose Gaussian starts at or before q
-#pragma unroll
-      for (int step = 16; step >= 1; step >>= 1) {
-        const uint32_t v = __shfl_sync(0xffffffffu, ex, j + step);
-        if (v <= q) j += step;
-      }
+    for (int j = 0; j < nb; ++j) {
       const uint32_t gj = __shfl_sync(0xffffffffu, g, j);
-      const uint32_t oj = __shfl_sync(0xffffffffu, org, j);
-      const uint32_t wj = __shfl_sync(0xffffffffu, tw, j);
-      const uint32_t ej = __shfl_sync(0xffffffffu, ex, j);
-      const float iw = __shfl_sync(0xffffffffu, inv_tw, j);
-      const uint32_t local = q - ej;
-      uint32_t ry = __float2uint_rz((float)local * iw);  // local / wj, then exact correction
-      if (ry * wj > local) --ry;
-      else if ((ry + 1) * wj <= local) ++ry;
-      const uint32_t t = ((oj >> 16) + ry) * (uint32_t)tiles_x + (oj & 0xffffu) + (local - ry * wj);
-      f(valid, gj, t);
+      const uint32_t bj = __shfl_sync(0xffffffffu, base, j);
+      const uint32_t whj = __shfl_sync(0xffffffffu, wh, j);
+      const float iw = __shfl_sync(0xffffffffu, inv_w, j);
+      const uint32_t w = whj & 0xffffu, h = whj >> 16;
+      if (w <= 32) {
+        const uint32_t rpi = __float2uint_rz(32.5f * iw);           // rows per step = 32 / w
+        const uint32_t r0 = __float2uint_rz(((float)lane + 0.5f) * iw);  // lane / w
+        const uint32_t col = (uint32_t)lane - r0 * w;
+        if (r0 < rpi)
+          for (uint32_t ry = r0; ry < h; ry += rpi) f(gj, bj + ry * (uint32_t)tiles_x + col);
+      } else {
+        for (uint32_t ry = 0; ry < h; ++ry)
+          for (uint32_t cx = lane; cx < w; cx += 32) f(gj, bj + ry * (uint32_t)tiles_x + cx);
+      }
       __syncwarp();
     }
   }
@@ -128,9 +121,7 @@ __global__ void __launch_bounds__(kWarps * 32) tile_count_kernel(const uint2* __
   uint32_t s0, s1;
   warp_slice(chunk_first, blockIdx.x, warp, s0, s1);
   __syncthreads();
-  for_each_pair(rect, tiles, idx_sorted, excl, s0, s1, lane, tiles_x, [&](bool valid, uint32_t, uint32_t t) {
-    if (valid) atomicAdd(&s_hist[t], 1u);
-  });
+  for_each_pair(rect, tiles, idx_sorted, s0, s1, lane, tiles_x, [&](uint32_t, uint32_t t) { atomicAdd(&s_hist[t], 1u); });
   __syncthreads();
   for (int t = threadIdx.x; t < ntiles; t += blockDim.x) counts[(size_t)t * nchunks + blockIdx.x] = s_hist[t];
 }
@@ -162,12 +153,9 @@ __global__ void __launch_bounds__(kWarps * 32) tile_scatter_kernel(const uint2* 
   uint32_t s0, s1;
   warp_slice(chunk_first, blockIdx.x, warp, s0, s1);
   __syncwarp();
-  // pass 1: this warp's per-tile pair counts; lanes of one step that share a tile are grouped by
-  // __match_any_sync and their leader adds the group size (no atomics, u16 table)
-  for_each_pair(rect, tiles, idx_sorted, excl, s0, s1, lane, tiles_x, [&](bool valid, uint32_t, uint32_t t) {
-    const uint32_t peers = __match_any_sync(0xffffffffu, valid ? t : 0xffffffffu);
-    if (valid && lane == __ffs(peers) - 1) my[t] = (uint16_t)(my[t] + __popc(peers));
-  });
+  // pass 1: this warp's per-tile pair counts (distinct tiles per step: no atomics, u16 table)
+  for_each_pair(rect, tiles, idx_sorted, s0, s1, lane, tiles_x,
+                [&](uint32_t, uint32_t t) { my[t] = (uint16_t)(my[t] + 1); });
   __syncthreads();
   // per tile: offset of each warp within the chunk = counts of the earlier warps
   for (int t = threadIdx.x; t < ntiles; t += blockDim.x) {
@@ -180,18 +168,11 @@ __global__ void __launch_bounds__(kWarps * 32) tile_scatter_kernel(const uint2* 
     }
   }
   __syncthreads();
-  // pass 2: depth-ordered writes.  Lanes are in stream order, so a lane's rank among the lanes of
-  // its step that share its tile (popc of the lower peers) keeps the stable (depth, index) order.
-  for_each_pair(rect, tiles, idx_sorted, excl, s0, s1, lane, tiles_x, [&](bool valid, uint32_t g, uint32_t t) {
-    const uint32_t peers = __match_any_sync(0xffffffffu, valid ? t : 0xffffffffu);
-    const int leader = __ffs(peers) - 1;
-    uint32_t base = 0;
-    if (valid && lane == leader) {
-      base = my[t];
-      my[t] = (uint16_t)(base + __popc(peers));
-    }
-    base = __shfl_sync(0xffffffffu, base, leader);
-    if (valid) vals[s_coff[t] + base + __popc(peers & ((1u << lane) - 1u))] = g;
+  // pass 2: depth-ordered writes (one Gaussian per step, consecutive steps ordered by __syncwarp)
+  for_each_pair(rect, tiles, idx_sorted, s0, s1, lane, tiles_x, [&](uint32_t g, uint32_t t) {
+    const uint32_t r = my[t];
+    my[t] = (uint16_t)(r + 1);
+    vals[s_coff[t] + r] = g;
   });
 }
 
