@@ -16,6 +16,8 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
+#include <algorithm>
+
 #include "lgs_internal.cuh"
 #include "lgs_kernels.h"
 
@@ -36,6 +38,31 @@ void launch_depth_sort(const ViewBufs& v, int64_t n, uint32_t* dkey_sorted, uint
                        size_t temp_bytes, cudaStream_t s) {
   if (n == 0) return;
   cub::DeviceRadixSort::SortPairs(temp, temp_bytes, v.dkey, dkey_sorted, v.iota, idx_sorted, (int)n, 0, 32, s);
+}
+
+// out[0] = sum of tiles[0..n) (the pair count P): block reduction + one atomic per block.
+__global__ void __launch_bounds__(256) sum_tiles_kernel(const uint32_t* __restrict__ tiles, int64_t n,
+                                                        uint32_t* __restrict__ out) {
+  __shared__ uint32_t s_w[8];
+  uint32_t acc = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    acc += tiles[i];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t t = 0;
+    for (int w = 0; w < 8; ++w) t += s_w[w];
+    atomicAdd(out, t);
+  }
+}
+
+void launch_sum_tiles(const uint32_t* tiles, int64_t n, uint32_t* out, cudaStream_t s) {
+  cudaMemsetAsync(out, 0, sizeof(uint32_t), s);
+  if (n == 0) return;
+  const int64_t blocks = std::min<int64_t>((n + 255) / 256, 148 * 8);
+  sum_tiles_kernel<<<(unsigned)blocks, 256, 0, s>>>(tiles, n, out);
 }
 
 __global__ void gather_tiles_kernel(const uint32_t* __restrict__ tiles, const uint32_t* __restrict__ idx_sorted,

@@ -79,6 +79,8 @@ struct lgs_ctx {
   std::atomic<int> refs{1};
   std::atomic<int64_t> launches{0};
   uint32_t* host_u32 = nullptr;  // pinned scalar readback
+  uint32_t* dev_u32 = nullptr;   // device scalar (pair count)
+  cudaEvent_t pairs_ready = nullptr;
   // phase profiling
   bool profiling = false;
   std::vector<PhaseMark> marks;
@@ -159,6 +161,8 @@ void ctx_release(lgs_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     if (ctx->host_u32) cudaFreeHost(ctx->host_u32);
+    if (ctx->dev_u32) cudaFree(ctx->dev_u32);
+    if (ctx->pairs_ready) cudaEventDestroy(ctx->pairs_ready);
     for (auto& m : ctx->marks) {
       cudaEventDestroy(m.a);
       cudaEventDestroy(m.b);
@@ -367,9 +371,10 @@ LGS_API lgs_status lgs_ctx_create(int32_t device, void* stream, lgs_ctx** out) {
     uint64_t thr = UINT64_MAX;
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
   }
-  if (cudaMallocHost(&ctx->host_u32, 64) != cudaSuccess) {
-    delete ctx;
-    return fail(LGS_ENOMEM, "cudaMallocHost failed");
+  if (cudaMallocHost(&ctx->host_u32, 64) != cudaSuccess || cudaMalloc(&ctx->dev_u32, 64) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->pairs_ready, cudaEventDisableTiming) != cudaSuccess) {
+    ctx_release(ctx);
+    return fail(LGS_ENOMEM, "context allocation failed");
   }
   *out = ctx;
   return LGS_OK;
@@ -520,8 +525,15 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
   {
     PhaseScope ph(ctx, PH_PREPROCESS);
     launch_preprocess(map->dm, dc, t->vb, s);
+    // the pair count P = sum of tiles touched sizes the tile lists; it is read back while the GPU
+    // is still busy with the depth sort queued below, so the host wait never idles the GPU
+    launch_sum_tiles(t->vb.tiles, n, ctx->dev_u32, s);
   }
-  ctx->launches++;
+  ctx->launches += 2;
+  if (n > 0) {
+    CUDAB(cudaMemcpyAsync(ctx->host_u32, ctx->dev_u32, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    CUDAB(cudaEventRecord(ctx->pairs_ready, s));
+  }
 
   // depth sort + scan
   uint32_t *dkey_sorted = nullptr, *idx_sorted = nullptr, *incl = nullptr;
@@ -540,8 +552,7 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
   ctx->launches += n > 0 ? 6 : 0;
   int64_t P = 0;
   if (n > 0) {
-    CUDAB(cudaMemcpyAsync(ctx->host_u32, incl + (n - 1), sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-    CUDAB(cudaStreamSynchronize(s));
+    CUDAB(cudaEventSynchronize(ctx->pairs_ready));
     P = ctx->host_u32[0];
   }
   t->pairs = P;

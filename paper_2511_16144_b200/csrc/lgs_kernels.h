@@ -70,6 +70,7 @@ void launch_preprocess(const DevMap& m, const DevCam& c, const ViewBufs& v, cuda
 // Binning (binning.cu).  The pair count is read back once per view (host sync) to size the
 // pair arrays and the sort.
 size_t binning_temp_bytes(int64_t n, int64_t pairs_cap, int tile_bits);
+void launch_sum_tiles(const uint32_t* tiles, int64_t n, uint32_t* out, cudaStream_t s);
 void launch_depth_sort(const ViewBufs& v, int64_t n, uint32_t* dkey_sorted, uint32_t* idx_sorted,
                        void* temp, size_t temp_bytes, cudaStream_t s);
 void launch_scan_tiles(const uint32_t* tiles, const uint32_t* idx_sorted, int64_t n, uint32_t* scratch,
