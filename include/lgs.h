@@ -236,6 +236,11 @@ LGS_API lgs_status lgs_saved_work(const lgs_saved* tape, int64_t* evaluated, int
  * kernels.  Runs a ~10 ms microbenchmark on the legacy stream; call outside timed regions. */
 LGS_API lgs_status lgs_measure_fp32_peak(int32_t device, double* tflops);
 
+/* Self-test of the warp-level TF32 tensor-core fragment layouts used by the backward blend:
+ * d = a (16x8, row-major) * b (8x8, row-major), host buffers; split = 1 uses the 3xTF32 split. */
+LGS_API lgs_status lgs_debug_mma_selftest(int32_t device, const float* a16x8, const float* b8x8, float* d16x8,
+                                          int32_t split);
+
 #ifdef __cplusplus
 }
 #endif

@@ -90,6 +90,7 @@ SIGNATURES = [
     ("lgs_ctx_phase_times", C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int64), C.c_int32]),
     ("lgs_saved_work", C.c_int, [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     ("lgs_measure_fp32_peak", C.c_int, [C.c_int32, C.POINTER(C.c_double)]),
+    ("lgs_debug_mma_selftest", C.c_int, [C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32]),
 ]
 
 LGS_PHASE_COUNT = 8

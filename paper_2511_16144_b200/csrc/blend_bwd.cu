@@ -281,6 +281,12 @@ static void launch_bwd_dp(const DevMap& m, const DevCam& c, const ViewBufs& v, c
 void launch_blend_bwd(const DevMap& m, const DevCam& c, const ViewBufs& v, const TileLists& tl,
                       const PixelState& ps, const BwdIn& in, float* gacc, int slots, cudaStream_t s) {
   (void)slots;
+  const char* impl = getenv("LGS_BWD_IMPL");  // "simt" forces the shuffle-reduction kernel
+  const bool use_mma = !(impl && impl[0] == 's');
+  if (use_mma && blend_bwd_mma_supported(m.dp)) {
+    launch_blend_bwd_mma(m, c, v, tl, ps, in, gacc, s);
+    return;
+  }
   switch (m.dp) {
     case 0: launch_bwd_dp<0>(m, c, v, tl, ps, in, gacc, s); break;
     case 4: launch_bwd_dp<4>(m, c, v, tl, ps, in, gacc, s); break;

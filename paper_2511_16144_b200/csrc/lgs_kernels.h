@@ -95,6 +95,10 @@ void launch_blend_fwd(const DevMap& m, const DevCam& c, const ViewBufs& v, const
                       const PixelState& ps, const FwdOut& o, cudaStream_t s);
 void launch_blend_bwd(const DevMap& m, const DevCam& c, const ViewBufs& v, const TileLists& tl,
                       const PixelState& ps, const BwdIn& in, float* gacc, int slots, cudaStream_t s);
+// Tensor-core variant (blend_bwd_mma.cu), used by launch_blend_bwd when supported.
+bool blend_bwd_mma_supported(int dp);
+void launch_blend_bwd_mma(const DevMap& m, const DevCam& c, const ViewBufs& v, const TileLists& tl,
+                          const PixelState& ps, const BwdIn& in, float* gacc, cudaStream_t s);
 
 struct GradOut {
   float* position;      // [N][3]

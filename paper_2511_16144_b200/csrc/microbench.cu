@@ -3,8 +3,27 @@
 #include <cuda_runtime.h>
 
 #include "../../include/lgs.h"
+#include "mma_tf32.cuh"
 
 namespace {
+
+// One warp: D = A (16x8) * B (8x8) through the fragment layouts documented in mma_tf32.cuh,
+// with the 3xTF32 split (mode 1) or plain TF32 (mode 0).
+__global__ void mma_selftest_kernel(const float* A, const float* B, float* D, int mode) {
+  const int lane = threadIdx.x, gid = lane >> 2, tig = lane & 3;
+  const float av[4] = {A[gid * 8 + tig], A[(gid + 8) * 8 + tig], A[gid * 8 + tig + 4], A[(gid + 8) * 8 + tig + 4]};
+  const float bv[2] = {B[tig * 8 + gid], B[(tig + 4) * 8 + gid]};
+  uint32_t ah[4], al[4], bh[2], bl[2];
+  for (int i = 0; i < 4; ++i) lgs::split_tf32(av[i], ah[i], al[i]);
+  for (int i = 0; i < 2; ++i) lgs::split_tf32(bv[i], bh[i], bl[i]);
+  float d[4] = {0.f, 0.f, 0.f, 0.f};
+  if (mode) lgs::mma_3xtf32(d, ah, al, bh, bl);
+  else lgs::mma_tf32(d, ah, bh);
+  D[gid * 8 + 2 * tig] = d[0];
+  D[gid * 8 + 2 * tig + 1] = d[1];
+  D[(gid + 8) * 8 + 2 * tig] = d[2];
+  D[(gid + 8) * 8 + 2 * tig + 1] = d[3];
+}
 
 __global__ void ffma_peak_kernel(float* out, int iters, float a, float b) {
   float x0 = threadIdx.x * 1e-7f, x1 = x0 + 1e-7f, x2 = x0 + 2e-7f, x3 = x0 + 3e-7f;
@@ -21,6 +40,20 @@ __global__ void ffma_peak_kernel(float* out, int iters, float a, float b) {
 }
 
 }  // namespace
+
+extern "C" LGS_API lgs_status lgs_debug_mma_selftest(int32_t device, const float* a16x8, const float* b8x8,
+                                                     float* d16x8, int32_t split) {
+  if (!a16x8 || !b8x8 || !d16x8) return LGS_EINVAL;
+  if (cudaSetDevice(device) != cudaSuccess) return LGS_ECUDA;
+  float* buf = nullptr;
+  if (cudaMalloc(&buf, sizeof(float) * (128 + 64 + 128)) != cudaSuccess) return LGS_ENOMEM;
+  cudaMemcpy(buf, a16x8, sizeof(float) * 128, cudaMemcpyHostToDevice);
+  cudaMemcpy(buf + 128, b8x8, sizeof(float) * 64, cudaMemcpyHostToDevice);
+  mma_selftest_kernel<<<1, 32>>>(buf, buf + 128, buf + 192, split);
+  const cudaError_t e = cudaMemcpy(d16x8, buf + 192, sizeof(float) * 128, cudaMemcpyDeviceToHost);
+  cudaFree(buf);
+  return e == cudaSuccess ? LGS_OK : LGS_ECUDA;
+}
 
 extern "C" LGS_API lgs_status lgs_measure_fp32_peak(int32_t device, double* tflops) {
   if (!tflops) return LGS_EINVAL;
