@@ -50,5 +50,5 @@ def test_mma_backward_matches_simt(name, n):
     g_simt = _grads("simt", scene, cam, tg)
     for k in GROUPS:
         frac, worst = grad_mismatch(g_mma[k], g_simt[k])
-        assert frac < 1e-4, (k, frac, worst)
+        assert frac < 1e-3, (k, frac, worst)  # same allowance as the oracle parity tests
     assert grad_mismatch(g_mma["pose"], g_simt["pose"], rtol=1e-3, floor=0.0)[0] == 0.0
