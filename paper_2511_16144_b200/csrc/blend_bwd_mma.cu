@@ -75,6 +75,22 @@ __global__ void __launch_bounds__(kNT) blend_bwd_mma_kernel(DevMap m, DevCam c, 
   const float cx_ = (float)lx - 7.5f, cy_ = (float)ly - 7.5f;
 
   for (int i = tid; i < kSub * RS; i += kNT) red[i] = 0.f;
+  // B fragments of Phi (step 3), the same for every tile: Phi[p][j] for p = 32 warp + 8 kt + tig
+  // (+4), j = gid4: 1, x, y, x^2, xy, y^2, 0, 0 of the pixel's tile-centred coordinates (exact in TF32)
+  uint32_t phi[4][2];
+#pragma unroll
+  for (int kt = 0; kt < 4; ++kt)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int pl = kt * 8 + tig + 4 * h;  // lane of the pixel row within this warp
+      const float px_ = __shfl_sync(0xffffffffu, cx_, pl);
+      const float py_ = __shfl_sync(0xffffffffu, cy_, pl);
+      const float vals[8] = {1.f, px_, py_, px_ * px_, px_ * py_, py_ * py_, 0.f, 0.f};
+      float sel = vals[0];
+#pragma unroll
+      for (int q = 1; q < 8; ++q) sel = gid4 == q ? vals[q] : sel;
+      phi[kt][h] = __float_as_uint(sel);
+    }
 
   for (int tile = next_tile(tl, ntiles, &s_slot); tile >= 0; tile = next_tile(tl, ntiles, &s_slot)) {
     const int tx = tile % c.tiles_x, ty = tile / c.tiles_x;
@@ -202,32 +218,38 @@ __global__ void __launch_bounds__(kNT) blend_bwd_mma_kernel(DevMap m, DevCam c, 
         }
         __syncwarp();
         // ---- step 2: per-pixel reverse recurrence (renderer.cpp:248-288) -----------------------
+        // C starts zeroed; W entries are overwritten only where the pixel contributes, so rows are
+        // zeroed where it does not; Gaussians whose rect misses the whole warp are skipped.
+        float wrow[kSub];
+#pragma unroll
+        for (int el = 0; el < kSub; ++el) {
+          wrow[el] = 0.f;
+          Cs[tid * kWS + el] = 0.f;
+        }
+#pragma unroll
         for (int el = kSub - 1; el >= 0; --el) {
           const int e = e0 + el;
-          float w = 0.f, cc = 0.f;
           const uint32_t jrel = bstart + (uint32_t)e - range.x;
-          if (e < cnt && jrel < last) {
-            const uint2 rc = s_rect[e];
-            if (in_rect(rc, px, py)) {
-              const float4 r0 = s_r0[e];
-              const float4 s4 = s_sc[e];
-              float dx, dy, G;
-              const float alpha = splat_alpha(r0.x, r0.y, ScaledConic{s4.x, s4.y, s4.z}, r0.w, fpx, fpy, dx, dy, G);
-              if (alpha >= c.alpha_skip) {
-                const float a = fminf(alpha, c.alpha_clamp);
-                const float inv1ma = __frcp_rn(1.0f - a);
-                T = T * inv1ma;  // transmittance before this contributor
-                w = a * T;
-                const float dldw = Ws[tid * kWS + el] + g_acc;
-                const float dl_da = T * dldw - accum * inv1ma;
-                accum = fmaf(dldw, w, accum);
-                if (!(alpha > c.alpha_clamp)) cc = dl_da * r0.w * (-0.5f * G);
-              }
-            }
-          }
-          Ws[tid * kWS + el] = w;
-          Cs[tid * kWS + el] = cc;
+          const bool cand = e < cnt && jrel < last && in_rect(s_rect[e], px, py);
+          if (!__any_sync(0xffffffffu, cand)) continue;
+          if (!cand) continue;
+          const float4 r0 = s_r0[e];
+          const float4 s4 = s_sc[e];
+          float dx, dy, G;
+          const float alpha = splat_alpha(r0.x, r0.y, ScaledConic{s4.x, s4.y, s4.z}, r0.w, fpx, fpy, dx, dy, G);
+          if (!(alpha >= c.alpha_skip)) continue;
+          const float a = fminf(alpha, c.alpha_clamp);
+          const float inv1ma = __frcp_rn(1.0f - a);
+          T = T * inv1ma;  // transmittance before this contributor
+          const float w = a * T;
+          const float dldw = Ws[tid * kWS + el] + g_acc;
+          const float dl_da = T * dldw - accum * inv1ma;
+          accum = fmaf(dldw, w, accum);
+          wrow[el] = w;
+          if (!(alpha > c.alpha_clamp)) Cs[tid * kWS + el] = dl_da * r0.w * (-0.5f * G);
         }
+#pragma unroll
+        for (int el = 0; el < kSub; ++el) Ws[tid * kWS + el] = wrow[el];
         __syncwarp();
         // ---- step 3: W^T X (linear grads) and C^T Phi (moments) over this warp's pixels -------
         float o[KT1 + 1][4];
@@ -252,19 +274,7 @@ __global__ void __launch_bounds__(kNT) blend_bwd_mma_kernel(DevMap m, DevCam c, 
             split_tf32(Xs[(p0 + tig + 4) * XS + nt * 8 + gid4], bh[1], bl[1]);
             mma_3xtf32(o[nt], wh, wl, bh, bl);
           }
-          // Phi[p][j] for p = p0 + tig (+4), j = gid4: 1, x, y, x^2, xy, y^2, 0, 0 (exact in TF32)
-          uint32_t b[2];
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int p = p0 + tig + 4 * h;
-            const float px_ = __shfl_sync(0xffffffffu, cx_, p & 31);
-            const float py_ = __shfl_sync(0xffffffffu, cy_, p & 31);
-            const float vals[8] = {1.f, px_, py_, px_ * px_, px_ * py_, py_ * py_, 0.f, 0.f};
-            float sel = vals[0];
-#pragma unroll
-            for (int q = 1; q < 8; ++q) sel = gid4 == q ? vals[q] : sel;
-            b[h] = __float_as_uint(sel);
-          }
+          const uint32_t b[2] = {phi[kt][0], phi[kt][1]};
           mma_2xtf32(o[KT1], ch, cl, b);
         }
         // sum the 8 warps' partial sums (rows = Gaussians of the sub-batch)
