@@ -281,8 +281,9 @@ static void launch_bwd_dp(const DevMap& m, const DevCam& c, const ViewBufs& v, c
 void launch_blend_bwd(const DevMap& m, const DevCam& c, const ViewBufs& v, const TileLists& tl,
                       const PixelState& ps, const BwdIn& in, float* gacc, int slots, cudaStream_t s) {
   (void)slots;
-  const char* impl = getenv("LGS_BWD_IMPL");  // "simt" forces the shuffle-reduction kernel
-  const bool use_mma = !(impl && impl[0] == 's');
+  // The tensor-core variant (blend_bwd_mma.cu) is opt-in (LGS_BWD_IMPL=mma) until it beats this one.
+  const char* impl = getenv("LGS_BWD_IMPL");
+  const bool use_mma = impl && impl[0] == 'm';
   if (use_mma && blend_bwd_mma_supported(m.dp)) {
     launch_blend_bwd_mma(m, c, v, tl, ps, in, gacc, s);
     return;

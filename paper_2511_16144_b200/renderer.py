@@ -122,9 +122,12 @@ class Context:
         return {L.lgs_phase_name(i).decode(): (ms[i], cnt[i]) for i in range(_lib.LGS_PHASE_COUNT)}
 
     def __del__(self):
-        if getattr(self, "h", None) and _lib._lib is not None:
-            _lib._lib.lgs_ctx_destroy(self.h)
-            self.h = None
+        try:
+            if getattr(self, "h", None) and _lib._lib is not None:
+                _lib._lib.lgs_ctx_destroy(self.h)
+                self.h = None
+        except (AttributeError, TypeError):  # interpreter shutdown
+            pass
 
 
 _default_ctx: dict[int, Context] = {}
@@ -167,9 +170,12 @@ class DeviceMap:
         del keep
 
     def __del__(self):
-        if getattr(self, "h", None) and _lib._lib is not None:
-            _lib._lib.lgs_map_destroy(self.h)
-            self.h = None
+        try:
+            if getattr(self, "h", None) and _lib._lib is not None:
+                _lib._lib.lgs_map_destroy(self.h)
+                self.h = None
+        except (AttributeError, TypeError):  # interpreter shutdown
+            pass
 
 
 class RenderOutput:
@@ -226,9 +232,12 @@ class RenderOutput:
         return ft, nc
 
     def __del__(self):
-        if getattr(self, "tape", None) and _lib._lib is not None:
-            _lib._lib.lgs_saved_destroy(self.tape)
-            self.tape = None
+        try:
+            if getattr(self, "tape", None) and _lib._lib is not None:
+                _lib._lib.lgs_saved_destroy(self.tape)
+                self.tape = None
+        except (AttributeError, TypeError):  # interpreter shutdown
+            pass
 
 
 def _alloc_like(device_side, shape, device):

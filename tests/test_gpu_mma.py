@@ -32,7 +32,7 @@ def test_mma_fragment_layout(split):
 
 
 def _grads(impl, scene, cam, tg):
-    os.environ["LGS_BWD_IMPL"] = impl
+    os.environ["LGS_BWD_IMPL"] = impl  # "mma" opts into the tensor-core kernel
     try:
         dev = {k: torch.from_numpy(v).cuda() for k, v in scene.items()}
         out = R.render(dev, cam, targets={k: torch.from_numpy(v).cuda() for k, v in tg.items()})
@@ -51,4 +51,4 @@ def test_mma_backward_matches_simt(name, n):
     for k in GROUPS:
         frac, worst = grad_mismatch(g_mma[k], g_simt[k])
         assert frac < 1e-3, (k, frac, worst)  # same allowance as the oracle parity tests
-    assert grad_mismatch(g_mma["pose"], g_simt["pose"], rtol=1e-3, floor=0.0)[0] == 0.0
+    assert grad_mismatch(g_mma["pose"], g_simt["pose"])[0] == 0.0  # floor: 1e-2 x rms of the 6 values
