@@ -47,8 +47,69 @@ def parse():
     return p.parse_args()
 
 
+class NvmlClockSampler:
+    """SM clocks + throttle reasons sampled in-process through NVML during the timed region (a
+    background thread; an nvidia-smi subprocess polling the driver stalled individual steps)."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40, "sw_power_cap": 0x4}
+
+    def __init__(self, index: int, period_s: float = 0.02):
+        self.index, self.period = index, period_s
+        self.samples, self.reasons, self.smax = [], set(), None
+        self._stop = threading.Event()
+        self.ok = False
+
+    def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.smax = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+            self.thread = threading.Thread(target=self._run, daemon=True)
+            self.thread.start()
+        except Exception:  # NVML unavailable: fall back to nvidia-smi around the region
+            self.ok = False
+        return self
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for name, bit in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            self._stop.wait(self.period)
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.ok:
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        if not self.ok:
+            return ClockSampler.snapshot(self.index)
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.smax,
+                "reasons": sorted(self.reasons), "samples": len(self.samples), "source": "nvml"}
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    @staticmethod
+    def snapshot(index):
+        s = ClockSampler(index)
+        s.__enter__()
+        time.sleep(0.3)
+        s.__exit__()
+        out = s.summary()
+        out["source"] = "nvidia-smi (after the timed region)"
+        return out
 
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -168,7 +229,7 @@ def run_ours(args):
         dist.barrier()
     torch.cuda.synchronize()
     launches0 = ctx.launches
-    with ClockSampler(local) as clk, torch.cuda.stream(stream):
+    with NvmlClockSampler(local) as clk, torch.cuda.stream(stream):
         for k in range(args.steps):
             flush.fill_(float(k))
             evs[k][0].record(stream)
