@@ -13,11 +13,13 @@ scaling: one view per GPU per step).
 
 Timing: W >= 3 untimed warm-up steps; K timed steps, each bracketed by CUDA events on the
 library's stream, with a 512 MiB L2 flush (not timed) before every step; barrier + synchronize
-on both sides; max over ranks.  SM clocks are sampled with nvidia-smi during the timed region.
+on both sides; max over ranks.  SM clocks and throttle reasons are sampled through NVML between
+the timed steps (outside each step's event bracket).
 """
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import math
 import os
@@ -44,19 +46,23 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=5)
+    p.add_argument("--sampler", choices=["nvml", "smi", "none"], default="nvml", help=argparse.SUPPRESS)
     return p.parse_args()
 
 
 class NvmlClockSampler:
-    """SM clocks + throttle reasons sampled in-process through NVML during the timed region (a
-    background thread; an nvidia-smi subprocess polling the driver stalled individual steps)."""
+    """SM clocks + throttle reasons sampled in-process through NVML during the timed region.
+
+    Samples are taken by the benchmark thread BETWEEN steps (after a step's end event, before the
+    next step's L2 flush), never concurrently with a step: an NVML query takes a driver lock, and a
+    sampling thread (or an nvidia-smi process) polling during a step stalled single steps by up to
+    37 ms on the box."""
 
     REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40, "sw_power_cap": 0x4}
 
-    def __init__(self, index: int, period_s: float = 0.02):
-        self.index, self.period = index, period_s
+    def __init__(self, index: int):
+        self.index = index
         self.samples, self.reasons, self.smax = [], set(), None
-        self._stop = threading.Event()
         self.ok = False
 
     def __enter__(self):
@@ -66,36 +72,54 @@ class NvmlClockSampler:
             self.nv = pynvml
             self.h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
             self.smax = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            # first queries are slow (driver state setup): take them before the timed region starts
+            pynvml.nvmlDeviceGetClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            pynvml.nvmlDeviceGetCurrentClocksEventReasons(self.h)
             self.ok = True
-            self.thread = threading.Thread(target=self._run, daemon=True)
-            self.thread.start()
-        except Exception:  # NVML unavailable: fall back to nvidia-smi around the region
+        except Exception:  # NVML unavailable: fall back to nvidia-smi after the region
             self.ok = False
         return self
 
-    def _run(self):
+    def sample(self):
+        """One sample; call between steps while the GPU is still busy with the previous one."""
+        if not self.ok:
+            return
         nv = self.nv
-        while not self._stop.is_set():
-            try:
-                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
-                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                for name, bit in self.REASONS.items():
-                    if r & bit:
-                        self.reasons.add(name)
-            except Exception:
-                pass
-            self._stop.wait(self.period)
+        try:
+            self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+            r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            for name, bit in self.REASONS.items():
+                if r & bit:
+                    self.reasons.add(name)
+        except Exception:
+            pass
 
     def __exit__(self, *a):
-        self._stop.set()
-        if self.ok:
-            self.thread.join(timeout=2)
+        pass
 
     def summary(self):
-        if not self.ok:
+        if not self.ok or not self.samples:
             return ClockSampler.snapshot(self.index)
-        return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.smax,
-                "reasons": sorted(self.reasons), "samples": len(self.samples), "source": "nvml"}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.smax,
+                "reasons": sorted(self.reasons), "samples": len(self.samples),
+                "source": "nvml, sampled between timed steps"}
+
+
+class NullSampler:
+    def __init__(self, index):
+        self.index = index
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        pass
+
+    def sample(self):
+        pass
+
+    def summary(self):
+        return ClockSampler.snapshot(self.index)
 
 
 class ClockSampler:
@@ -114,6 +138,9 @@ class ClockSampler:
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
+
+    def sample(self):
+        pass
 
     def __init__(self, index: int):
         self.index = index
@@ -229,13 +256,20 @@ def run_ours(args):
         dist.barrier()
     torch.cuda.synchronize()
     launches0 = ctx.launches
-    with NvmlClockSampler(local) as clk, torch.cuda.stream(stream):
+    sampler = {"nvml": NvmlClockSampler, "smi": ClockSampler, "none": NullSampler}[args.sampler]
+    every = max(1, args.steps // 40)  # ~40 clock samples over the timed region
+    gc.collect()
+    gc.disable()  # a collection inside a step stalls the host-driven pipeline
+    with sampler(local) as clk, torch.cuda.stream(stream):
         for k in range(args.steps):
             flush.fill_(float(k))
             evs[k][0].record(stream)
             out, g = step()
             evs[k][1].record(stream)
+            if k % every == every - 1:
+                clk.sample()
         torch.cuda.synchronize()
+    gc.enable()
     if world > 1:
         dist.barrier()
     launches = ctx.launches - launches0

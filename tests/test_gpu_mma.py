@@ -52,4 +52,6 @@ def test_mma_backward_matches_simt(name, n):
         frac, worst = grad_mismatch(g_mma[k], g_simt[k])
         assert frac < 1e-3, (k, frac, worst)  # same allowance as the oracle parity tests
     # the pose gradient sums every Gaussian; near-zero components carry cancellation noise
-    assert grad_mismatch(g_mma["pose"], g_simt["pose"], rtol=1e-2)[0] == 0.0
+    # (L1 cotangents: every Gaussian's term is O(1) while the sum is small), so compare as a 6-vector
+    a, b = (np.asarray(g["pose"], np.float64) for g in (g_mma, g_simt))
+    assert np.linalg.norm(a - b) <= 1e-2 * np.linalg.norm(b), (a, b)
