@@ -168,17 +168,18 @@ __global__ void __launch_bounds__(kBlock / PPT) blend_bwd_kernel(DevMap m, DevCa
         const float4 r0 = sm.r0[e];
         const float4 s4 = sm.sc[e];
         const ScaledConic sc{s4.x, s4.y, s4.z};
+        // Branch-free over the PPT pixels: independent chains the scheduler can interleave.  A
+        // pixel that does not contribute gets alpha = 0 (T / accum / colour / feature terms add
+        // exactly +0) and a zero dL/dalpha mask for the opacity, mean and conic terms.
         float alphas[PPT], Gs[PPT], dxs[PPT], dys[PPT];
         bool any = false;
 #pragma unroll
         for (int k = 0; k < PPT; ++k) {
           const int py = py0 + k;
-          alphas[k] = 0.f;
-          if (col_in && jrel < last[k] && py >= ry0 && py <= ry1) {
-            alphas[k] = splat_alpha(r0.x, r0.y, sc, r0.w, fpx, (float)py, dxs[k], dys[k], Gs[k]);
-            if (!(alphas[k] >= c.alpha_skip)) alphas[k] = 0.f;
-            else any = true;
-          }
+          const float al = splat_alpha(r0.x, r0.y, sc, r0.w, fpx, (float)py, dxs[k], dys[k], Gs[k]);
+          const bool ok = col_in && jrel < last[k] && py >= ry0 && py <= ry1 && al >= c.alpha_skip;
+          alphas[k] = ok ? al : 0.f;
+          any = any || ok;
         }
         if (!__any_sync(0xffffffffu, any)) continue;
         // phase 2: contributions, summed over this thread's pixels, then one warp reduction
@@ -187,55 +188,62 @@ __global__ void __launch_bounds__(kBlock / PPT) blend_bwd_kernel(DevMap m, DevCa
         for (int q = 0; q < SLOTS; ++q) vals[q] = 0.f;
         const float4 r1 = sm.r1[e];
         const float4 col = sm.col[e];
+        const float o = r0.w;
+        const float do_dlogit = o * (1.0f - o);
+        const float twoA = 2.0f * r1.x, twoB = 2.0f * r1.y, twoC = 2.0f * r1.z;
+        float w[PPT], dldw[PPT], inv1ma[PPT];
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) {
+          const float a = fminf(alphas[k], c.alpha_clamp);
+          inv1ma[k] = fast_rcp(1.0f - a);
+          T[k] = T[k] * inv1ma[k];  // transmittance before this contributor (unchanged when a = 0)
+          w[k] = a * T[k];
+          float dl = fmaf(g_draw[k], r0.z, g_acc[k]);
+          dl = fmaf(g_rgb[k][0], col.x, dl);
+          dl = fmaf(g_rgb[k][1], col.y, dl);
+          dl = fmaf(g_rgb[k][2], col.z, dl);
+          dldw[k] = dl;
+        }
+        if (DP > 0) {
+#pragma unroll
+          for (int q = 0; q < DQ; ++q) {
+            const float4 fv = sm.feat[e][q];
+#pragma unroll
+            for (int k = 0; k < PPT; ++k) {
+              const int lp = (ly0 + k) * kTile + lx;
+              const float4 gv = sm.gfeat[q][lp];
+              dldw[k] = fmaf(gv.x, fv.x, dldw[k]);
+              dldw[k] = fmaf(gv.y, fv.y, dldw[k]);
+              dldw[k] = fmaf(gv.z, fv.z, dldw[k]);
+              dldw[k] = fmaf(gv.w, fv.w, dldw[k]);
+              vals[kSlotFeat + q * 4 + 0] = fmaf(gv.x, w[k], vals[kSlotFeat + q * 4 + 0]);
+              vals[kSlotFeat + q * 4 + 1] = fmaf(gv.y, w[k], vals[kSlotFeat + q * 4 + 1]);
+              vals[kSlotFeat + q * 4 + 2] = fmaf(gv.z, w[k], vals[kSlotFeat + q * 4 + 2]);
+              vals[kSlotFeat + q * 4 + 3] = fmaf(gv.w, w[k], vals[kSlotFeat + q * 4 + 3]);
+            }
+          }
+        }
 #pragma unroll
         for (int k = 0; k < PPT; ++k) {
           const float alpha = alphas[k];
-          if (alpha == 0.f) continue;
           const float dx = dxs[k], dy = dys[k], G = Gs[k];
-          const float a = fminf(alpha, c.alpha_clamp);
-          const float inv1ma = __frcp_rn(1.0f - a);
-          T[k] = T[k] * inv1ma;  // transmittance before this contributor
-          const float w = a * T[k];
-          float dldw = fmaf(g_draw[k], r0.z, g_acc[k]);
-          dldw = fmaf(g_rgb[k][0], col.x, dldw);
-          dldw = fmaf(g_rgb[k][1], col.y, dldw);
-          dldw = fmaf(g_rgb[k][2], col.z, dldw);
-          if (DP > 0) {
-            const int lp = (ly0 + k) * kTile + lx;
-#pragma unroll
-            for (int q = 0; q < DQ; ++q) {
-              const float4 fv = sm.feat[e][q];
-              const float4 gv = sm.gfeat[q][lp];
-              dldw = fmaf(gv.x, fv.x, dldw);
-              dldw = fmaf(gv.y, fv.y, dldw);
-              dldw = fmaf(gv.z, fv.z, dldw);
-              dldw = fmaf(gv.w, fv.w, dldw);
-              vals[kSlotFeat + q * 4 + 0] = fmaf(gv.x, w, vals[kSlotFeat + q * 4 + 0]);
-              vals[kSlotFeat + q * 4 + 1] = fmaf(gv.y, w, vals[kSlotFeat + q * 4 + 1]);
-              vals[kSlotFeat + q * 4 + 2] = fmaf(gv.z, w, vals[kSlotFeat + q * 4 + 2]);
-              vals[kSlotFeat + q * 4 + 3] = fmaf(gv.w, w, vals[kSlotFeat + q * 4 + 3]);
-            }
-          }
-          const float dl_da = T[k] * dldw - accum[k] * inv1ma;
-          accum[k] = fmaf(dldw, w, accum[k]);
-          vals[kSlotColor + 0] = fmaf(g_rgb[k][0], w, vals[kSlotColor + 0]);
-          vals[kSlotColor + 1] = fmaf(g_rgb[k][1], w, vals[kSlotColor + 1]);
-          vals[kSlotColor + 2] = fmaf(g_rgb[k][2], w, vals[kSlotColor + 2]);
-          vals[kSlotZ] = fmaf(g_draw[k], w, vals[kSlotZ]);
-          if (!(alpha > c.alpha_clamp)) {
-            const float o = r0.w;
-            vals[kSlotOpac] = fmaf(dl_da * G, o * (1.0f - o), vals[kSlotOpac]);
-            const float cf = dl_da * o * (-0.5f * G);  // dl_dg * dg_dq
-            const float twoB = 2.0f * r1.y;
-            const float dq_ddx = fmaf(2.0f * r1.x, dx, twoB * dy);
-            const float dq_ddy = fmaf(2.0f * r1.z, dy, twoB * dx);
-            vals[kSlotMuX] = fmaf(-cf, dq_ddx, vals[kSlotMuX]);
-            vals[kSlotMuY] = fmaf(-cf, dq_ddy, vals[kSlotMuY]);
-            const float cdx = cf * dx;
-            vals[kSlotConA] = fmaf(cdx, dx, vals[kSlotConA]);
-            vals[kSlotConB] = fmaf(cdx, dy, vals[kSlotConB]);
-            vals[kSlotConC] = fmaf(cf * dy, dy, vals[kSlotConC]);
-          }
+          // the clamped contributor (and a non-contributing pixel) gets no opacity/mean/conic grad
+          const float dl_da = (alpha != 0.f && !(alpha > c.alpha_clamp)) ? T[k] * dldw[k] - accum[k] * inv1ma[k] : 0.f;
+          accum[k] = fmaf(dldw[k], w[k], accum[k]);
+          vals[kSlotColor + 0] = fmaf(g_rgb[k][0], w[k], vals[kSlotColor + 0]);
+          vals[kSlotColor + 1] = fmaf(g_rgb[k][1], w[k], vals[kSlotColor + 1]);
+          vals[kSlotColor + 2] = fmaf(g_rgb[k][2], w[k], vals[kSlotColor + 2]);
+          vals[kSlotZ] = fmaf(g_draw[k], w[k], vals[kSlotZ]);
+          vals[kSlotOpac] = fmaf(dl_da * G, do_dlogit, vals[kSlotOpac]);
+          const float cf = dl_da * o * (-0.5f * G);  // dl_dg * dg_dq
+          const float dq_ddx = fmaf(twoA, dx, twoB * dy);
+          const float dq_ddy = fmaf(twoC, dy, twoB * dx);
+          vals[kSlotMuX] = fmaf(-cf, dq_ddx, vals[kSlotMuX]);
+          vals[kSlotMuY] = fmaf(-cf, dq_ddy, vals[kSlotMuY]);
+          const float cdx = cf * dx;
+          vals[kSlotConA] = fmaf(cdx, dx, vals[kSlotConA]);
+          vals[kSlotConB] = fmaf(cdx, dy, vals[kSlotConB]);
+          vals[kSlotConC] = fmaf(cf * dy, dy, vals[kSlotConC]);
         }
         warp_transpose_reduce<SLOTS>(vals, lane);
         float* dst = gacc + (size_t)sm.gid[e] * SLOTS + lane * (SLOTS / 32);

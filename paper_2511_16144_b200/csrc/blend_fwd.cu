@@ -98,36 +98,54 @@ __global__ void __launch_bounds__(kBlock / PPT) blend_fwd_kernel(DevMap m, DevCa
         const float4 r0 = sm.r0[e];
         const float4 s4 = sm.sc[e];
         const ScaledConic sc{s4.x, s4.y, s4.z};
+        // Evaluate the PPT pixels branch-free (independent chains the scheduler can interleave),
+        // then composite all of them at once: a pixel that does not contribute gets alpha = 0,
+        // which leaves T, the accumulators and the counters exactly unchanged (w = +0).
+        float a[PPT];
+        bool ok[PPT];
+        bool any = false;
 #pragma unroll
         for (int k = 0; k < PPT; ++k) {
           const int py = py0 + k;
-          if (done[k] || py < ry0 || py > ry1) continue;
           float dx, dy, G;
-          float alpha = splat_alpha(r0.x, r0.y, sc, r0.w, fpx, (float)py, dx, dy, G);
-          ++n_eval[k];
-          if (!(alpha >= c.alpha_skip)) continue;
-          ++n_contrib[k];
-          alpha = fminf(alpha, c.alpha_clamp);
-          const float w = __fmul_rn(alpha, T[k]);
-          const float4 col = sm.col[e];
-          cr[k] = fmaf(w, col.x, cr[k]);
-          cg[k] = fmaf(w, col.y, cg[k]);
-          cb[k] = fmaf(w, col.z, cb[k]);
-          draw[k] = fmaf(w, r0.z, draw[k]);
-          acc[k] += w;
-          if (DP > 0) {
+          const float alpha = splat_alpha(r0.x, r0.y, sc, r0.w, fpx, (float)py, dx, dy, G);
+          const bool in = !done[k] && py >= ry0 && py <= ry1;
+          ok[k] = in && alpha >= c.alpha_skip;
+          n_eval[k] += in ? 1u : 0u;
+          n_contrib[k] += ok[k] ? 1u : 0u;
+          a[k] = ok[k] ? fminf(alpha, c.alpha_clamp) : 0.f;
+          any = any || ok[k];
+        }
+        if (!any) continue;
+        const float4 col = sm.col[e];
+        float w[PPT];
 #pragma unroll
-            for (int q = 0; q < DQ; ++q) {
-              const float4 fv = sm.feat[e][q];
-              f[k][q * 4 + 0] = fmaf(w, fv.x, f[k][q * 4 + 0]);
-              f[k][q * 4 + 1] = fmaf(w, fv.y, f[k][q * 4 + 1]);
-              f[k][q * 4 + 2] = fmaf(w, fv.z, f[k][q * 4 + 2]);
-              f[k][q * 4 + 3] = fmaf(w, fv.w, f[k][q * 4 + 3]);
+        for (int k = 0; k < PPT; ++k) {
+          w[k] = __fmul_rn(a[k], T[k]);
+          cr[k] = fmaf(w[k], col.x, cr[k]);
+          cg[k] = fmaf(w[k], col.y, cg[k]);
+          cb[k] = fmaf(w[k], col.z, cb[k]);
+          draw[k] = fmaf(w[k], r0.z, draw[k]);
+          acc[k] += w[k];
+        }
+        if (DP > 0) {
+#pragma unroll
+          for (int q = 0; q < DQ; ++q) {
+            const float4 fv = sm.feat[e][q];
+#pragma unroll
+            for (int k = 0; k < PPT; ++k) {
+              f[k][q * 4 + 0] = fmaf(w[k], fv.x, f[k][q * 4 + 0]);
+              f[k][q * 4 + 1] = fmaf(w[k], fv.y, f[k][q * 4 + 1]);
+              f[k][q * 4 + 2] = fmaf(w[k], fv.z, f[k][q * 4 + 2]);
+              f[k][q * 4 + 3] = fmaf(w[k], fv.w, f[k][q * 4 + 3]);
             }
           }
-          T[k] = __fmul_rn(T[k], __fsub_rn(1.0f, alpha));
-          last[k] = base + e + 1 - range.x;
-          if (T[k] < c.t_min) done[k] = true;
+        }
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) {
+          T[k] = __fmul_rn(T[k], __fsub_rn(1.0f, a[k]));
+          if (ok[k]) last[k] = base + e + 1 - range.x;
+          done[k] = done[k] || T[k] < c.t_min;
         }
         all_done = true;
 #pragma unroll

@@ -218,6 +218,14 @@ __device__ __forceinline__ float fast_exp2(float x) {
   return y;
 }
 
+// 1/x to ~1 ulp (MUFU.RCP, no IEEE slow path): used where the result feeds only gradients
+// (toleranced), never a threshold test that decides the contributor set.
+__device__ __forceinline__ float fast_rcp(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 constexpr float kNegHalfLog2e = -0.72134752044448170368f;  // -0.5 * log2(e)
 
 }  // namespace lgs
