@@ -41,13 +41,14 @@ __global__ void chunk_bounds_kernel(uint32_t* __restrict__ cnt_to_excl, const ui
                                     int nslices, uint32_t* __restrict__ slice_first) {
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n) return;
+  // slices past the capacity (pairs > cap: the host re-runs with exact buffers) are clamped
   const uint32_t cnt = cnt_to_excl[s];
   const uint32_t excl = incl[s] - cnt;
-  const int c = cnt ? (int)(excl / kPairsPerWarp) : nslices;
+  const int c = cnt ? (int)min((uint32_t)nslices, excl / kPairsPerWarp) : nslices;
   int cp = -1;
   if (s > 0) {
     const uint32_t cntp = incl[s - 1] - (s > 1 ? incl[s - 2] : 0u);
-    cp = cntp ? (int)((incl[s - 1] - cntp) / kPairsPerWarp) : nslices;
+    cp = cntp ? (int)min((uint32_t)nslices, (incl[s - 1] - cntp) / kPairsPerWarp) : nslices;
   }
   for (int cc = cp + 1; cc <= c; ++cc) slice_first[cc] = (uint32_t)s;
   if (s == n - 1)
@@ -126,10 +127,21 @@ __global__ void __launch_bounds__(kWarps * 32) tile_count_kernel(const uint2* __
   for (int t = threadIdx.x; t < ntiles; t += blockDim.x) counts[(size_t)t * nchunks + blockIdx.x] = s_hist[t];
 }
 
-__global__ void tile_ranges_kernel(const uint32_t* __restrict__ offs, int nchunks, int ntiles, uint32_t pairs,
-                                   uint2* __restrict__ ranges) {
+// The pair count P is read on the device (the host sized the buffers from a capacity, not from P).
+// P > cap: every list is emptied (the blend kernels then do nothing) and the overflow flag tells the
+// host to re-run the binning with exact buffers.
+__global__ void tile_ranges_kernel(const uint32_t* __restrict__ offs, int nchunks, int ntiles,
+                                   const uint32_t* __restrict__ dev_pairs, uint32_t cap,
+                                   uint32_t* __restrict__ overflow, uint2* __restrict__ ranges) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= ntiles) return;
+  const uint32_t pairs = *dev_pairs;
+  if (pairs > cap) {
+    ranges[t] = make_uint2(0u, 0u);
+    if (t == 0) *overflow = 1u;
+    return;
+  }
+  if (t == 0) *overflow = 0u;
   const uint32_t b = offs[(size_t)t * nchunks];
   const uint32_t e = t + 1 < ntiles ? offs[(size_t)(t + 1) * nchunks] : pairs;
   ranges[t] = make_uint2(b, e);
@@ -142,7 +154,7 @@ __global__ void __launch_bounds__(kWarps * 32) tile_scatter_kernel(const uint2* 
                                                                     const uint32_t* __restrict__ chunk_first,
                                                                     int ntiles, int tiles_x, int nchunks,
                                                                     const uint32_t* __restrict__ offs,
-                                                                    uint32_t* __restrict__ vals) {
+                                                                    uint32_t cap, uint32_t* __restrict__ vals) {
   extern __shared__ uint32_t s_dyn[];
   uint32_t* s_coff = s_dyn;                                       // [ntiles] chunk start slot per tile
   uint16_t* s_tab = reinterpret_cast<uint16_t*>(s_dyn + ntiles);  // [kWarps][ntiles] offsets within chunk
@@ -172,7 +184,8 @@ __global__ void __launch_bounds__(kWarps * 32) tile_scatter_kernel(const uint2* 
   for_each_pair(rect, tiles, idx_sorted, s0, s1, lane, tiles_x, [&](uint32_t g, uint32_t t) {
     const uint32_t r = my[t];
     my[t] = (uint16_t)(r + 1);
-    vals[s_coff[t] + r] = g;
+    const uint32_t slot = s_coff[t] + r;
+    if (slot < cap) vals[slot] = g;
   });
 }
 
@@ -223,12 +236,13 @@ size_t fast_binning_scratch_bytes(int64_t pairs, int ntiles) {
 
 void launch_fast_binning(const ViewBufs& v, const uint32_t* idx_sorted, uint32_t* cnt_sorted, const uint32_t* incl,
                          int64_t n, int ntiles, int tiles_x, uint32_t* scratch, uint32_t* vals, uint2* ranges,
-                         uint32_t pairs, cudaStream_t s) {
-  if (n == 0 || pairs == 0) {
+                         uint32_t cap, const uint32_t* dev_pairs, uint32_t* dev_overflow, cudaStream_t s) {
+  if (n == 0 || cap == 0) {
     cudaMemsetAsync(ranges, 0, sizeof(uint2) * (size_t)ntiles, s);
+    cudaMemsetAsync(dev_overflow, 0, sizeof(uint32_t), s);
     return;
   }
-  const int nchunks = nchunks_for(pairs);
+  const int nchunks = nchunks_for(cap);
   const size_t cells = (size_t)nchunks * (size_t)ntiles;
   uint32_t* counts = scratch;
   uint32_t* offs = counts + cells;
@@ -250,9 +264,9 @@ void launch_fast_binning(const ViewBufs& v, const uint32_t* idx_sorted, uint32_t
   tile_count_kernel<<<nchunks, threads, sizeof(uint32_t) * ntiles, s>>>(v.rect, v.tiles, idx_sorted, excl, chunk_first,
                                                                         ntiles, tiles_x, nchunks, counts);
   cub::DeviceScan::ExclusiveSum(temp, temp_bytes, counts, offs, (int)cells, s);
-  tile_ranges_kernel<<<(ntiles + 255) / 256, 256, 0, s>>>(offs, nchunks, ntiles, pairs, ranges);
+  tile_ranges_kernel<<<(ntiles + 255) / 256, 256, 0, s>>>(offs, nchunks, ntiles, dev_pairs, cap, dev_overflow, ranges);
   tile_scatter_kernel<<<nchunks, threads, sizeof(uint32_t) * ntiles + sizeof(uint16_t) * ntiles * kWarps, s>>>(
-      v.rect, v.tiles, idx_sorted, excl, chunk_first, ntiles, tiles_x, nchunks, offs, vals);
+      v.rect, v.tiles, idx_sorted, excl, chunk_first, ntiles, tiles_x, nchunks, offs, cap, vals);
 }
 
 }  // namespace lgs

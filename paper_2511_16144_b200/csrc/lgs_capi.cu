@@ -79,8 +79,9 @@ struct lgs_ctx {
   std::atomic<int> refs{1};
   std::atomic<int64_t> launches{0};
   uint32_t* host_u32 = nullptr;  // pinned scalar readback
-  uint32_t* dev_u32 = nullptr;   // device scalar (pair count)
+  uint32_t* dev_u32 = nullptr;   // device scalars: [0] pair count, [1] binning overflow flag
   cudaEvent_t pairs_ready = nullptr;
+  int64_t pairs_cap = 0;  // tile-list capacity for the next render (0: size from the exact count)
   // phase profiling
   bool profiling = false;
   std::vector<PhaseMark> marks;
@@ -550,60 +551,8 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
     launch_scan_tiles(t->vb.tiles, idx_sorted, n, dkey_sorted, incl, temp, temp_bytes, s);
   }
   ctx->launches += n > 0 ? 6 : 0;
-  int64_t P = 0;
-  if (n > 0) {
-    CUDAB(cudaEventSynchronize(ctx->pairs_ready));
-    P = ctx->host_u32[0];
-  }
-  t->pairs = P;
-  TRYB(dalloc(ctx, &t->vals, P));
-  if (fast_binning_supported(ntiles)) {
-    // stable counting sort by tile straight into the final lists (binning.cu fast path)
-    uint32_t* scratch = nullptr;
-    TRYB(dalloc(ctx, reinterpret_cast<uint8_t**>(&scratch), fast_binning_scratch_bytes(P, ntiles)));
-    {
-      PhaseScope ph(ctx, PH_TILE_SORT);
-      launch_fast_binning(t->vb, idx_sorted, dkey_sorted, incl, n, ntiles, dc.tiles_x, scratch, t->vals, t->ranges,
-                          (uint32_t)P, s);
-    }
-    ctx->launches += P > 0 ? 6 : 0;
-    dfree(ctx, scratch);
-  } else {
-    uint16_t* keys_in = nullptr;
-    uint32_t* vals_in = nullptr;
-    TRYB(dalloc(ctx, &keys_in, P));
-    TRYB(dalloc(ctx, &vals_in, P));
-    TRYB(dalloc(ctx, &t->keys, P));
-    {
-      PhaseScope ph(ctx, PH_DUPLICATE);
-      launch_duplicate(t->vb, idx_sorted, incl, n, dc.tiles_x, keys_in, vals_in, s);
-    }
-    const size_t sort_bytes = binning_temp_bytes(0, P, tile_bits);
-    if (sort_bytes > temp_bytes) {
-      dfree(ctx, temp);
-      temp_bytes = sort_bytes;
-      TRYB(dalloc(ctx, reinterpret_cast<uint8_t**>(&temp), temp_bytes));
-    }
-    {
-      PhaseScope ph(ctx, PH_TILE_SORT);
-      launch_tile_sort(keys_in, t->keys, vals_in, t->vals, P, tile_bits, temp, temp_bytes, s);
-      launch_ranges(t->keys, P, ntiles, t->ranges, s);
-    }
-    ctx->launches += (n > 0 ? 1 : 0) + (P > 0 ? 5 : 0);
-    dfree(ctx, keys_in);
-    dfree(ctx, vals_in);
-  }
-  dfree(ctx, temp);
-  {
-    PhaseScope ph(ctx, PH_TILE_SORT);
-    launch_tile_order(t->ranges, ntiles, t->order, s);  // longest tile list first
-  }
-  ctx->launches++;
-  dfree(ctx, dkey_sorted);
-  dfree(ctx, idx_sorted);
-  dfree(ctx, incl);
 
-  // K5 (+ fused L1)
+  // K5 (+ fused L1) buffers
   FwdOut fo{};
   DeviceImages di;
   const bool host_out = out && out->memory == LGS_MEM_HOST;
@@ -623,7 +572,6 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
   if (targets) {
     TRYB(dalloc(ctx, &t->cot, npix * (4 + dp)));
     TRYB(dalloc(ctx, &t->loss, 1));
-    CUDAB(cudaMemsetAsync(t->loss, 0, sizeof(double), s));
     fo.t_rgb = targets->rgb; fo.t_depth = targets->depth; fo.t_feat = targets->feat;
     if (targets->memory == LGS_MEM_HOST) {
       TRYB(dalloc(ctx, &tstage, npix * (4 + d)));
@@ -636,12 +584,92 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
     fo.cot = t->cot;
     fo.loss = t->loss;
   }
-  {
-    PhaseScope ph(ctx, PH_BLEND_FWD);
-    launch_blend_fwd(map->dm, dc, t->vb, TileLists{t->vals, t->ranges, t->order, t->counter}, t->ps, fo, s);
+
+  // Binning + blend.  With a capacity from earlier renders on this context, everything is enqueued
+  // without waiting for the pair count P: the binning reads P on the device, and the host checks it
+  // (and an overflow flag) only after the whole forward is queued, when the GPU is far ahead of the
+  // check.  P > capacity (or the first render) runs the binning again with buffers of exactly P.
+  const bool fast = fast_binning_supported(ntiles);
+  auto bin_and_blend = [&](int64_t cap, bool exact) -> lgs_status {
+    if (!exact) {  // re-run: the fast binning consumed the scanned tile counts in place
+      launch_scan_tiles(t->vb.tiles, idx_sorted, n, dkey_sorted, incl, temp, temp_bytes, s);
+      ctx->launches += n > 0 ? 3 : 0;
+    }
+    dfree(ctx, t->vals);
+    dfree(ctx, t->keys);
+    LGS_TRY(dalloc(ctx, &t->vals, cap));
+    if (fast) {
+      // stable counting sort by tile straight into the final lists (binning_fast.cu)
+      uint32_t* scratch = nullptr;
+      LGS_TRY(dalloc(ctx, reinterpret_cast<uint8_t**>(&scratch), fast_binning_scratch_bytes(cap, ntiles)));
+      {
+        PhaseScope ph(ctx, PH_TILE_SORT);
+        launch_fast_binning(t->vb, idx_sorted, dkey_sorted, incl, n, ntiles, dc.tiles_x, scratch, t->vals, t->ranges,
+                            (uint32_t)cap, ctx->dev_u32, ctx->dev_u32 + 1, s);
+      }
+      ctx->launches += cap > 0 ? 6 : 0;
+      dfree(ctx, scratch);
+    } else {
+      uint16_t* keys_in = nullptr;
+      uint32_t* vals_in = nullptr;
+      LGS_TRY(dalloc(ctx, &keys_in, cap));
+      LGS_TRY(dalloc(ctx, &vals_in, cap));
+      LGS_TRY(dalloc(ctx, &t->keys, cap));
+      {
+        PhaseScope ph(ctx, PH_DUPLICATE);
+        launch_duplicate(t->vb, idx_sorted, incl, n, dc.tiles_x, keys_in, vals_in, s);
+      }
+      const size_t sort_bytes = binning_temp_bytes(0, cap, tile_bits);
+      void* stemp = nullptr;
+      LGS_TRY(dalloc(ctx, reinterpret_cast<uint8_t**>(&stemp), sort_bytes));
+      {
+        PhaseScope ph(ctx, PH_TILE_SORT);
+        launch_tile_sort(keys_in, t->keys, vals_in, t->vals, cap, tile_bits, stemp, sort_bytes, s);
+        launch_ranges(t->keys, cap, ntiles, t->ranges, s);
+      }
+      ctx->launches += (n > 0 ? 1 : 0) + (cap > 0 ? 5 : 0);
+      dfree(ctx, stemp);
+      dfree(ctx, keys_in);
+      dfree(ctx, vals_in);
+    }
+    {
+      PhaseScope ph(ctx, PH_TILE_SORT);
+      launch_tile_order(t->ranges, ntiles, t->order, s);  // longest tile list first
+    }
+    ctx->launches++;
+    if (targets) LGS_CUDA(cudaMemsetAsync(t->loss, 0, sizeof(double), s));
+    {
+      PhaseScope ph(ctx, PH_BLEND_FWD);
+      launch_blend_fwd(map->dm, dc, t->vb, TileLists{t->vals, t->ranges, t->order, t->counter}, t->ps, fo, s);
+    }
+    ctx->launches++;
+    LGS_CUDA(cudaGetLastError());
+    return LGS_OK;
+  };
+
+  int64_t P = 0;
+  const bool speculate = fast && n > 0 && ctx->pairs_cap > 0;
+  if (speculate) {
+    TRYB(bin_and_blend(ctx->pairs_cap, true));
+    CUDAB(cudaEventSynchronize(ctx->pairs_ready));  // long done: the GPU is busy with the queued forward
+    P = ctx->host_u32[0];
+    if (P > ctx->pairs_cap) {
+      ctx->pairs_cap = P + P / 4;
+      TRYB(bin_and_blend(P, false));
+    }
+  } else {
+    if (n > 0) {
+      CUDAB(cudaEventSynchronize(ctx->pairs_ready));
+      P = ctx->host_u32[0];
+    }
+    TRYB(bin_and_blend(P, true));
+    if (fast) ctx->pairs_cap = std::max<int64_t>(ctx->pairs_cap, P + P / 4);
   }
-  ctx->launches++;
-  CUDAB(cudaGetLastError());
+  t->pairs = P;
+  dfree(ctx, temp);
+  dfree(ctx, dkey_sorted);
+  dfree(ctx, idx_sorted);
+  dfree(ctx, incl);
   if (tstage) dfree(ctx, tstage);
   if (di.staged) {
     if (di.rgb) CUDAB(cudaMemcpyAsync(out->rgb, di.rgb, sizeof(float) * npix * 3, cudaMemcpyDeviceToHost, s));

@@ -84,12 +84,14 @@ void launch_ranges(const uint16_t* keys, int64_t pairs, int ntiles, uint2* range
 // Fast binning (stable counting sort by tile; binning.cu): writes the sorted list `vals` and the
 // per-tile `ranges` directly.  `cnt_sorted` holds tiles[idx_sorted[s]] (launch_scan_tiles'
 // scratch; overwritten), `incl` its inclusive scan; `scratch` must hold
-// fast_binning_scratch_bytes(pairs, ntiles).
+// fast_binning_scratch_bytes(cap, ntiles) and `vals` cap entries.  The pair count itself is read on
+// the device (`dev_pairs`), so the host never waits for it: if it exceeds `cap`, every tile list is
+// left empty and *dev_overflow = 1 (the host then re-runs with exact buffers).
 bool fast_binning_supported(int ntiles);
-size_t fast_binning_scratch_bytes(int64_t pairs, int ntiles);
+size_t fast_binning_scratch_bytes(int64_t cap, int ntiles);
 void launch_fast_binning(const ViewBufs& v, const uint32_t* idx_sorted, uint32_t* cnt_sorted, const uint32_t* incl,
                          int64_t n, int ntiles, int tiles_x, uint32_t* scratch, uint32_t* vals, uint2* ranges,
-                         uint32_t pairs, cudaStream_t s);
+                         uint32_t cap, const uint32_t* dev_pairs, uint32_t* dev_overflow, cudaStream_t s);
 
 void launch_blend_fwd(const DevMap& m, const DevCam& c, const ViewBufs& v, const TileLists& tl,
                       const PixelState& ps, const FwdOut& o, cudaStream_t s);

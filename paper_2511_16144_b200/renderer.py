@@ -89,11 +89,15 @@ CUDA_STREAM_LEGACY = 0x1  # cudaStreamLegacy
 
 class Context:
     """One CUDA stream + stream-ordered memory pool (lgs_ctx).  By default the library enqueues on
-    torch's current stream so torch tensors and library calls stay ordered."""
+    torch's current stream so torch tensors and library calls stay ordered; ``stream="own"`` gives
+    the context a private non-blocking stream (independent host threads rendering concurrently,
+    the reference's "concurrent renders between map mutations" contract)."""
 
     def __init__(self, device: int = 0, stream=None):
         L = _lib.load()
-        if stream is None and torch is not None and torch.cuda.is_available():
+        if stream == "own":
+            stream = None
+        elif stream is None and torch is not None and torch.cuda.is_available():
             with torch.cuda.device(device):
                 stream = torch.cuda.current_stream(device).cuda_stream
             if stream == 0:

@@ -371,3 +371,33 @@ def test_deterministic_images(c0):
     a = R.render(ds, cam)
     b = R.render(ds, cam)
     assert torch.equal(a.rgb, b.rgb) and torch.equal(a.feat, b.feat)
+
+
+def test_speculative_pair_capacity(oracle):
+    """The forward sizes the tile lists from earlier renders on the same context without waiting
+    for the pair count; a larger view overflows that capacity and is re-binned with exact buffers.
+    Both paths must give the bit-identical lists and images of a fresh context."""
+    small, scams, _ = scenes.make_config("c0", n=2000)
+    big, bcams, _ = scenes.make_config("c1", n=40_000)
+    ds, db = dev_scene(small), dev_scene(big)
+
+    def fresh(scene, cam):
+        out = R.render(scene, cam, ctx=R.Context(0))
+        torch.cuda.synchronize()
+        return out
+
+    ctx = R.Context(0)
+    first = R.render(ds, scams[0], ctx=ctx)          # exact (first render on ctx)
+    over = R.render(db, bcams[0], ctx=ctx)           # capacity from the small view: overflow -> re-bin
+    again = R.render(ds, scams[0], ctx=ctx)          # speculative, capacity now ample
+    torch.cuda.synchronize()
+    assert over.stats()["pairs"] > first.stats()["pairs"] * 1.25
+    for got, scene, cam in ((over, db, bcams[0]), (again, ds, scams[0])):
+        ref = fresh(scene, cam)
+        for a, b in zip(got.tile_keys(), ref.tile_keys()):
+            assert np.array_equal(a, b)
+        assert torch.equal(got.rgb, ref.rgb) and torch.equal(got.feat, ref.feat)
+        assert torch.equal(got.depth, ref.depth)
+    okeys, ovals, oranges = oracle.bin_f32(oracle.preprocess_f32(big, bcams[0]), bcams[0]["width"], bcams[0]["height"])
+    keys, vals, ranges = over.tile_keys()
+    assert np.array_equal(keys, okeys) and np.array_equal(vals, ovals) and np.array_equal(ranges, oranges)
