@@ -237,13 +237,16 @@ def run_ours(args):
         grads = R.alloc_grads(n, d, K, device=local)
         flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
     del dscene
+    comm = None
+    if world > 1:
+        from paper_2511_16144_b200.multiview import NativeComm
+        comm = NativeComm(ctx)  # liblgs.so's own NCCL communicator (torch.distributed only bootstraps it)
 
     def step():
         out = R.render(dmap, cam, targets=dtg, ctx=ctx)
         g = R.render_backward_l1(out, pose=True, into=grads)  # pose grad read back to the host
-        if world > 1:
-            with torch.cuda.stream(stream):
-                dist.all_reduce(grads["flat"])
+        if comm is not None:
+            comm.all_reduce(grads["flat"])  # 500k x 75 fp32 sum over NVLink, on the library's stream
         return out, g
 
     with torch.cuda.stream(stream):
@@ -363,7 +366,8 @@ def run_ours(args):
         "config": {"workload": args.config, "image": f"{cam['width']}x{cam['height']}", "gaussians": n,
                    "sh_degree": int(math.isqrt(K) - 1), "feature_dim": d, "views_per_gpu_per_step": 1,
                    "loss": "L1 rgb+depth+feat (fused)", "pose_grad": True,
-                   "parallelism": f"views over {world} GPU(s), NCCL all-reduce of fp32 grads" if world > 1 else "1 GPU",
+                   "parallelism": (f"views over {world} GPU(s), fp32 grad all-reduce by liblgs.so (NCCL)" if world > 1
+                                   else "1 GPU"),
                    "l2": "512 MiB L2 flush before every timed step"},
         "clocks": clk.summary(),
         "gpu_launches": int(launches),

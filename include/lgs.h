@@ -241,6 +241,24 @@ LGS_API lgs_status lgs_measure_fp32_peak(int32_t device, double* tflops);
 LGS_API lgs_status lgs_debug_mma_selftest(int32_t device, const float* a16x8, const float* b8x8, float* d16x8,
                                           int32_t split);
 
+/* ---- multi-view mapping batches --------------------------------------------
+ * New (the reference is single-threaded CPU code with no multi-view path).  Views are sharded
+ * over one process per GPU; each rank accumulates its views' gradients (lgs_map_grads.accumulate)
+ * and the batch gradient (a sum over views, renderer.cpp:259-353 is linear in the per-pixel
+ * cotangents) is one fp32 sum all-reduce over NCCL / NVLink on the context's stream.  NCCL is
+ * resolved at run time (libnccl.so.2, the copy the process already loaded if any).
+ * Rank 0 calls lgs_comm_unique_id and ships the 128 bytes to the other ranks out of band. */
+typedef struct {
+  uint8_t bytes[128];
+} lgs_comm_id;
+LGS_API lgs_status lgs_comm_unique_id(lgs_comm_id* id);
+LGS_API lgs_status lgs_comm_init(lgs_ctx* ctx, int32_t world_size, int32_t rank, const lgs_comm_id* id);
+LGS_API lgs_status lgs_comm_destroy(lgs_ctx* ctx);
+/* In-place sum over ranks of dense device gradients sized by `map` (one call when the six
+ * attribute buffers are one flat block, else one grouped NCCL launch). */
+LGS_API lgs_status lgs_allreduce_grads(lgs_ctx* ctx, const lgs_map* map, lgs_map_grads* grads);
+LGS_API lgs_status lgs_allreduce_f32(lgs_ctx* ctx, float* buf, int64_t count);
+
 #ifdef __cplusplus
 }
 #endif

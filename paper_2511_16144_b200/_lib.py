@@ -58,6 +58,10 @@ class LgsRenderStats(C.Structure):
     _fields_ = [("visible", C.c_int64), ("pairs", C.c_int64), ("tiles", C.c_int64), ("max_tile_list", C.c_int64)]
 
 
+class LgsCommId(C.Structure):
+    _fields_ = [("bytes", C.c_uint8 * 128)]
+
+
 # (name, restype, argtypes) for every symbol declared in include/lgs.h
 SIGNATURES = [
     ("lgs_version", C.c_char_p, []),
@@ -91,6 +95,11 @@ SIGNATURES = [
     ("lgs_saved_work", C.c_int, [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     ("lgs_measure_fp32_peak", C.c_int, [C.c_int32, C.POINTER(C.c_double)]),
     ("lgs_debug_mma_selftest", C.c_int, [C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32]),
+    ("lgs_comm_unique_id", C.c_int, [C.POINTER(LgsCommId)]),
+    ("lgs_comm_init", C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.POINTER(LgsCommId)]),
+    ("lgs_comm_destroy", C.c_int, [C.c_void_p]),
+    ("lgs_allreduce_grads", C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(LgsMapGrads)]),
+    ("lgs_allreduce_f32", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64]),
 ]
 
 LGS_PHASE_COUNT = 8

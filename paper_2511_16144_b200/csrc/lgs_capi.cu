@@ -19,6 +19,7 @@
 #include "../../include/lgs.h"
 #include "lgs_internal.cuh"
 #include "lgs_kernels.h"
+#include "nccl_dyn.h"
 
 using namespace lgs;
 
@@ -82,6 +83,9 @@ struct lgs_ctx {
   uint32_t* dev_u32 = nullptr;   // device scalars: [0] pair count, [1] binning overflow flag
   cudaEvent_t pairs_ready = nullptr;
   int64_t pairs_cap = 0;  // tile-list capacity for the next render (0: size from the exact count)
+  // multi-view gradient all-reduce (lgs_comm_*): one NCCL communicator per context / GPU
+  ncclComm_t comm = nullptr;
+  int32_t comm_world = 0, comm_rank = 0;
   // phase profiling
   bool profiling = false;
   std::vector<PhaseMark> marks;
@@ -160,6 +164,9 @@ void ctx_release(lgs_ctx* ctx) {
   if (ctx->refs.fetch_sub(1) == 1) {
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
+    if (ctx->comm) {
+      if (const NcclApi* nc = nccl_api(nullptr)) nc->CommDestroy(ctx->comm);
+    }
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     if (ctx->host_u32) cudaFreeHost(ctx->host_u32);
     if (ctx->dev_u32) cudaFree(ctx->dev_u32);
@@ -1011,5 +1018,98 @@ LGS_API lgs_status lgs_debug_pixel_state(lgs_ctx* ctx, const lgs_saved* t, float
   LGS_CUDA(cudaStreamSynchronize(ctx->stream));
   return LGS_OK;
 }
+
+
+// -------------------------------------------------------------------------------------------
+// multi-view mapping batches: NCCL all-reduce of the per-Gaussian gradients
+// -------------------------------------------------------------------------------------------
+#define LGS_NCCL(call)                                                                     \
+  do {                                                                                     \
+    ncclResult_t r_ = (call);                                                              \
+    if (r_ != ncclSuccess) return fail(LGS_ECUDA, "%s: %s", #call, nc->GetErrorString(r_)); \
+  } while (0)
+
+LGS_API lgs_status lgs_comm_unique_id(lgs_comm_id* id) {
+  if (!id) return fail(LGS_EINVAL, "id is NULL");
+  std::string err;
+  const NcclApi* nc = nccl_api(&err);
+  if (!nc) return fail(LGS_ENODEV, "%s", err.c_str());
+  static_assert(sizeof(ncclUniqueId) == sizeof(id->bytes), "ncclUniqueId size");
+  ncclUniqueId u;
+  LGS_NCCL(nc->GetUniqueId(&u));
+  std::memcpy(id->bytes, &u, sizeof u);
+  return LGS_OK;
+}
+
+LGS_API lgs_status lgs_comm_init(lgs_ctx* ctx, int32_t world_size, int32_t rank, const lgs_comm_id* id) {
+  if (!ctx || !id) return fail(LGS_EINVAL, "ctx/id is NULL");
+  if (world_size < 1 || rank < 0 || rank >= world_size) return fail(LGS_EINVAL, "rank %d of %d", rank, world_size);
+  if (ctx->comm) return fail(LGS_EINVAL, "context already has a communicator");
+  std::string err;
+  const NcclApi* nc = nccl_api(&err);
+  if (!nc) return fail(LGS_ENODEV, "%s", err.c_str());
+  LGS_CUDA(cudaSetDevice(ctx->device));
+  ncclUniqueId u;
+  std::memcpy(&u, id->bytes, sizeof u);
+  LGS_NCCL(nc->CommInitRank(&ctx->comm, world_size, u, rank));
+  ctx->comm_world = world_size;
+  ctx->comm_rank = rank;
+  return LGS_OK;
+}
+
+LGS_API lgs_status lgs_comm_destroy(lgs_ctx* ctx) {
+  if (!ctx) return fail(LGS_EINVAL, "ctx is NULL");
+  if (!ctx->comm) return LGS_OK;
+  const NcclApi* nc = nccl_api(nullptr);
+  LGS_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (nc) LGS_NCCL(nc->CommDestroy(ctx->comm));
+  ctx->comm = nullptr;
+  ctx->comm_world = ctx->comm_rank = 0;
+  return LGS_OK;
+}
+
+LGS_API lgs_status lgs_allreduce_f32(lgs_ctx* ctx, float* buf, int64_t count) {
+  if (!ctx || (!buf && count > 0) || count < 0) return fail(LGS_EINVAL, "bad all-reduce arguments");
+  if (!ctx->comm) return fail(LGS_EINVAL, "lgs_comm_init was not called on this context");
+  if (count == 0) return LGS_OK;
+  const NcclApi* nc = nccl_api(nullptr);
+  LGS_NCCL(nc->AllReduce(buf, buf, (size_t)count, ncclFloat32, ncclSum, ctx->comm, ctx->stream));
+  return LGS_OK;
+}
+
+LGS_API lgs_status lgs_allreduce_grads(lgs_ctx* ctx, const lgs_map* map, lgs_map_grads* grads) {
+  if (!ctx || !map || !grads) return fail(LGS_EINVAL, "ctx/map/grads is NULL");
+  if (grads->memory != LGS_MEM_DEVICE) return fail(LGS_EINVAL, "all-reduce needs device gradient buffers");
+  if (!ctx->comm) return fail(LGS_EINVAL, "lgs_comm_init was not called on this context");
+  const NcclApi* nc = nccl_api(nullptr);
+  const size_t n = (size_t)map->dm.n, K = (size_t)map->dm.K, d = (size_t)map->dm.d;
+  float* ptr[6] = {grads->position, grads->rotation, grads->log_scale, grads->opacity_logit, grads->sh,
+                   grads->feature};
+  const size_t cnt[6] = {n * 3, n * 4, n * 3, n, n * K * 3, n * d};
+  // The usual layout (one flat buffer, renderer.py alloc_grads) is reduced in ONE call; otherwise
+  // the attribute buffers are grouped into a single NCCL launch.
+  bool flat = true;
+  size_t total = 0;
+  for (int k = 0; k < 6; ++k) {
+    if (!ptr[k] || ptr[0] + total != ptr[k]) flat = flat && (cnt[k] == 0);
+    total += cnt[k];
+  }
+  if (flat && ptr[0]) {
+    LGS_NCCL(nc->AllReduce(ptr[0], ptr[0], total, ncclFloat32, ncclSum, ctx->comm, ctx->stream));
+    return LGS_OK;
+  }
+  LGS_NCCL(nc->GroupStart());
+  for (int k = 0; k < 6; ++k)
+    if (ptr[k] && cnt[k]) {
+      ncclResult_t r = nc->AllReduce(ptr[k], ptr[k], cnt[k], ncclFloat32, ncclSum, ctx->comm, ctx->stream);
+      if (r != ncclSuccess) {
+        nc->GroupEnd();
+        return fail(LGS_ECUDA, "ncclAllReduce: %s", nc->GetErrorString(r));
+      }
+    }
+  LGS_NCCL(nc->GroupEnd());
+  return LGS_OK;
+}
+#undef LGS_NCCL
 
 }  // extern "C"

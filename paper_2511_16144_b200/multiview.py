@@ -36,6 +36,61 @@ def assign_views(n_views: int, world: int, rank: int, costs: Sequence[float] | N
     return [v for v in range(n_views) if owner[v] == rank]
 
 
+class NativeComm:
+    """The library's own NCCL communicator on a rasterizer context (lgs_comm_* in include/lgs.h).
+
+    The 128-byte NCCL id made by rank 0 is shipped to the other ranks over the process group
+    (``torch.distributed`` with any backend -- gloo here, nccl on the box -- is only the bootstrap);
+    the gradient all-reduce itself is enqueued by liblgs.so on the context's stream, so a mapping
+    step (render -> backward -> all-reduce) never leaves the C ABI."""
+
+    def __init__(self, ctx, group=None, world: int | None = None, rank: int | None = None):
+        import ctypes as C
+
+        from . import _lib
+
+        self.ctx = ctx
+        L = _lib.load()
+        if world is None:
+            import torch.distributed as dist
+
+            world, rank = dist.get_world_size(group), dist.get_rank(group)
+            cid = _lib.LgsCommId()
+            payload = [None]
+            if rank == 0:
+                _lib.check(L.lgs_comm_unique_id(C.byref(cid)))
+                payload = [bytes(cid.bytes)]
+            dist.broadcast_object_list(payload, src=dist.get_global_rank(group, 0) if group is not None else 0,
+                                       group=group)
+            C.memmove(cid.bytes, payload[0], 128)
+        else:  # single process (world 1) or an id exchanged by the caller
+            cid = _lib.LgsCommId()
+            _lib.check(L.lgs_comm_unique_id(C.byref(cid)))
+        _lib.check(L.lgs_comm_init(ctx.h, int(world), int(rank or 0), C.byref(cid)))
+        self.world, self.rank = int(world), int(rank or 0)
+
+    def all_reduce(self, flat):
+        """In-place fp32 sum over ranks of a contiguous CUDA tensor, on the context's stream."""
+        from . import _lib
+
+        assert flat.is_cuda and flat.dtype.is_floating_point and flat.is_contiguous()
+        _lib.check(_lib.load().lgs_allreduce_f32(self.ctx.h, flat.data_ptr(), flat.numel()))
+
+    def all_reduce_grads(self, dmap, grads):
+        from . import _lib
+        from .renderer import _grads_struct
+
+        gs = _grads_struct(grads, False)
+        _lib.check(_lib.load().lgs_allreduce_grads(self.ctx.h, dmap.h, gs))
+
+    def close(self):
+        from . import _lib
+
+        if getattr(self, "ctx", None) is not None:
+            _lib.check(_lib.load().lgs_comm_destroy(self.ctx.h))
+            self.ctx = None
+
+
 class MultiViewStep:
     """One data-parallel mapping step: local views fwd+bwd into a flat gradient, then all-reduce.
 
@@ -44,11 +99,12 @@ class MultiViewStep:
     the oracle to exercise the sharding / reduction logic without a GPU).
     """
 
-    def __init__(self, views: Sequence[int], view_grads: Callable, grads: dict, group=None):
+    def __init__(self, views: Sequence[int], view_grads: Callable, grads: dict, group=None, comm=None):
         self.views = list(views)
         self.view_grads = view_grads
         self.grads = grads
         self.group = group
+        self.comm = comm  # NativeComm: the library's NCCL all-reduce; None: torch.distributed
 
     def step(self):
         import torch.distributed as dist
@@ -57,7 +113,9 @@ class MultiViewStep:
         flat.zero_()
         for v in self.views:
             self.view_grads(v, self.grads, True)
-        if dist.is_available() and dist.is_initialized() and dist.get_world_size(self.group) > 1:
+        if self.comm is not None:
+            self.comm.all_reduce(flat)
+        elif dist.is_available() and dist.is_initialized() and dist.get_world_size(self.group) > 1:
             dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=self.group)
         return self.grads
 

@@ -64,3 +64,18 @@ def test_ctx_create_without_gpu_fails_cleanly():
 
 def test_version():
     assert b"sm_100a" in _lib.load().lgs_version()
+
+
+def test_comm_unique_id_and_argument_checks():
+    """lgs_comm_* (multi-view all-reduce): NCCL ids come from the dynamically loaded libnccl.so.2
+    (no GPU needed); the GPU-side entry points reject missing contexts before touching CUDA."""
+    L = _lib.load()
+    a, b = _lib.LgsCommId(), _lib.LgsCommId()
+    assert L.lgs_comm_unique_id(C.byref(a)) == _lib.LGS_OK
+    assert L.lgs_comm_unique_id(C.byref(b)) == _lib.LGS_OK
+    assert any(a.bytes) and bytes(a.bytes) != bytes(b.bytes)
+    assert L.lgs_comm_unique_id(None) == _lib.LGS_EINVAL
+    assert L.lgs_comm_init(None, 2, 0, C.byref(a)) == _lib.LGS_EINVAL
+    assert L.lgs_allreduce_f32(None, None, 0) == _lib.LGS_EINVAL
+    assert L.lgs_allreduce_grads(None, None, None) == _lib.LGS_EINVAL
+    assert L.lgs_comm_destroy(None) == _lib.LGS_EINVAL
