@@ -220,8 +220,9 @@ LGS_API int64_t lgs_ctx_launch_count(const lgs_ctx* ctx);
 
 /* ---- phase profiling (CUDA events recorded on the context stream around each phase) -------
  * Phases: 0 preprocess, 1 depth sort + scan, 2 key duplication, 3 tile sort + ranges,
- * 4 blend forward, 5 blend backward, 6 preprocess backward, 7 map upload (pack). */
-enum { LGS_PHASE_COUNT = 8 };
+ * 4 blend forward, 5 blend backward, 6 preprocess backward, 7 map upload (pack), 8 mapping loss,
+ * 9 Adam step, 10 gradient all-reduce, 11 coverage mask. */
+enum { LGS_PHASE_COUNT = 12 };
 LGS_API const char* lgs_phase_name(int32_t phase);
 LGS_API lgs_status lgs_ctx_profile(lgs_ctx* ctx, int32_t enable);
 /* Accumulated device milliseconds and launch counts per phase since the last reset
@@ -240,6 +241,54 @@ LGS_API lgs_status lgs_measure_fp32_peak(int32_t device, double* tflops);
  * d = a (16x8, row-major) * b (8x8, row-major), host buffers; split = 1 uses the 3xTF32 split. */
 LGS_API lgs_status lgs_debug_mma_selftest(int32_t device, const float* a16x8, const float* b8x8, float* d16x8,
                                           int32_t split);
+
+/* ---- mapping losses (SPEC.md:418-426 compute_losses) ------------------
+ * l_rgb = w_l1 L1(rgb, kf.rgb) + (1 - w_l1)(1 - SSIM)/2 (11x11 Gaussian window, sigma 1.5, C1 =
+ * 0.01^2, C2 = 0.03^2, statistics at the valid window positions, channel-averaged);
+ * l_depth = mean |depth - kf.depth| over pixels with a valid measurement (finite, > 0) and
+ * rendered acc > 0.5; l_feat = mean |decode(feat) - feat_gt| with the frozen decoder
+ * decode(z) = W2 relu(W1 z + b1) + b2 (proj/src/codec.cpp:135-149); l_total = l_rgb +
+ * w_depth l_depth + w_feat l_feat.  lgs_mapping_loss writes d l_total / d (rgb, depth, feat) into
+ * the tape (the decoder chain is codec.cpp:167-188 decode_backward_input), which
+ * lgs_render_backward_loss then back-propagates to the map.  New in this layer: the reference
+ * specifies these losses but leaves mapping.cpp / metrics.cpp unimplemented. */
+typedef struct {
+  int32_t high_dim; /* D: teacher feature channels (32 in the reference design) */
+  int32_t hidden;   /* hidden width (64) */
+  int32_t low_dim;  /* d: must equal the map's feature dim */
+  const float* w1;  /* [hidden][d] row-major (codec.hpp wd1_) */
+  const float* b1;  /* [hidden] */
+  const float* w2;  /* [D][hidden] row-major (wd2_) */
+  const float* b2;  /* [D] */
+  int32_t memory;
+} lgs_decoder;
+typedef struct {
+  const float* rgb;     /* [H][W][3] */
+  const float* depth;   /* [H][W]; a pixel is valid iff finite and > 0 */
+  const float* feat_gt; /* [H][W][D] teacher features */
+  int32_t memory;
+} lgs_keyframe;
+typedef struct {
+  double w_l1;    /* 0.8: L1 share of l_rgb, D-SSIM gets 1 - w_l1 */
+  double w_depth; /* 0.5 */
+  double w_feat;  /* 1.0 */
+} lgs_loss_weights;
+typedef struct {
+  double l_rgb, l_depth, l_feat, l_total;
+  double ssim;          /* channel-averaged mean SSIM */
+  int64_t depth_pixels; /* pixels in the depth mask */
+} lgs_loss_breakdown;
+LGS_API lgs_loss_weights lgs_loss_weights_default(void);
+/* `rendered` = the images lgs_render_forward wrote for `tape` (rgb and feat are read; depth and
+ * acc come from the tape).  `out` may be NULL (no host synchronization). */
+LGS_API lgs_status lgs_mapping_loss(lgs_ctx* ctx, lgs_saved* tape, const lgs_images* rendered,
+                                    const lgs_keyframe* kf, const lgs_decoder* dec, const lgs_loss_weights* w,
+                                    lgs_loss_breakdown* out);
+/* Debug/parity: copy the tape's cotangents to host HWC buffers (any may be NULL).  Synchronizes. */
+LGS_API lgs_status lgs_debug_cotangents(lgs_ctx* ctx, const lgs_saved* tape, float* rgb, float* depth, float* feat);
+/* Back-propagates the cotangents stored in the tape (fused L1 or lgs_mapping_loss) to the map. */
+LGS_API lgs_status lgs_render_backward_loss(lgs_ctx* ctx, const lgs_saved* tape, lgs_map_grads* grads,
+                                            float* pose_grad);
 
 /* ---- multi-view mapping batches --------------------------------------------
  * New (the reference is single-threaded CPU code with no multi-view path).  Views are sharded

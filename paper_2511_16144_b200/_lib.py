@@ -58,6 +58,24 @@ class LgsRenderStats(C.Structure):
     _fields_ = [("visible", C.c_int64), ("pairs", C.c_int64), ("tiles", C.c_int64), ("max_tile_list", C.c_int64)]
 
 
+class LgsDecoder(C.Structure):
+    _fields_ = [("high_dim", C.c_int32), ("hidden", C.c_int32), ("low_dim", C.c_int32), ("w1", C.c_void_p),
+                ("b1", C.c_void_p), ("w2", C.c_void_p), ("b2", C.c_void_p), ("memory", C.c_int32)]
+
+
+class LgsKeyframe(C.Structure):
+    _fields_ = [("rgb", C.c_void_p), ("depth", C.c_void_p), ("feat_gt", C.c_void_p), ("memory", C.c_int32)]
+
+
+class LgsLossWeights(C.Structure):
+    _fields_ = [("w_l1", C.c_double), ("w_depth", C.c_double), ("w_feat", C.c_double)]
+
+
+class LgsLossBreakdown(C.Structure):
+    _fields_ = [("l_rgb", C.c_double), ("l_depth", C.c_double), ("l_feat", C.c_double), ("l_total", C.c_double),
+                ("ssim", C.c_double), ("depth_pixels", C.c_int64)]
+
+
 class LgsCommId(C.Structure):
     _fields_ = [("bytes", C.c_uint8 * 128)]
 
@@ -95,6 +113,11 @@ SIGNATURES = [
     ("lgs_saved_work", C.c_int, [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     ("lgs_measure_fp32_peak", C.c_int, [C.c_int32, C.POINTER(C.c_double)]),
     ("lgs_debug_mma_selftest", C.c_int, [C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32]),
+    ("lgs_loss_weights_default", LgsLossWeights, []),
+    ("lgs_mapping_loss", C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(LgsImages), C.POINTER(LgsKeyframe),
+                                   C.POINTER(LgsDecoder), C.POINTER(LgsLossWeights), C.POINTER(LgsLossBreakdown)]),
+    ("lgs_render_backward_loss", C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(LgsMapGrads), _fp]),
+    ("lgs_debug_cotangents", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     ("lgs_comm_unique_id", C.c_int, [C.POINTER(LgsCommId)]),
     ("lgs_comm_init", C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.POINTER(LgsCommId)]),
     ("lgs_comm_destroy", C.c_int, [C.c_void_p]),
@@ -102,7 +125,7 @@ SIGNATURES = [
     ("lgs_allreduce_f32", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64]),
 ]
 
-LGS_PHASE_COUNT = 8
+LGS_PHASE_COUNT = 12
 
 _lib = None
 

@@ -126,7 +126,7 @@ struct PhaseScope {
 };
 
 enum { PH_PREPROCESS = 0, PH_DEPTH_SORT, PH_DUPLICATE, PH_TILE_SORT, PH_BLEND_FWD, PH_BLEND_BWD, PH_PREPROCESS_BWD,
-       PH_UPLOAD };
+       PH_UPLOAD, PH_LOSS, PH_ADAM, PH_ALLREDUCE, PH_COVERAGE };
 
 }  // namespace
 
@@ -152,8 +152,9 @@ struct lgs_saved {
   uint32_t* order = nullptr;  // tiles by decreasing list length
   int* counter = nullptr;     // persistent-scheduler slot counter
   PixelState ps{};
-  float* cot = nullptr;     // fused L1 cotangents [H][W][4 + DP]
+  float* cot = nullptr;     // loss cotangents [H][W][4 + DP] (fused L1 or lgs_mapping_loss)
   double* loss = nullptr;
+  double* loss_sums = nullptr;  // lgs_mapping_loss partial sums [LOSS_COUNT]
   int64_t pairs = 0;
   int ntiles = 0;
 };
@@ -322,6 +323,7 @@ void free_saved(lgs_saved* t) {
   dfree(ctx, t->ps.work);
   dfree(ctx, t->cot);
   dfree(ctx, t->loss);
+  dfree(ctx, t->loss_sums);
   if (t->owned_map) free_map(t->owned_map);
   delete t;
   ctx_release(ctx);
@@ -848,6 +850,133 @@ LGS_API lgs_status lgs_render_backward_l1(lgs_ctx* ctx, const lgs_saved* tape, l
   return run_backward(ctx, tape, in, grads, pose_grad);
 }
 
+LGS_API lgs_status lgs_render_backward_loss(lgs_ctx* ctx, const lgs_saved* tape, lgs_map_grads* grads,
+                                            float* pose_grad) {
+  return lgs_render_backward_l1(ctx, tape, grads, pose_grad);
+}
+
+LGS_API lgs_loss_weights lgs_loss_weights_default(void) {
+  lgs_loss_weights w;
+  w.w_l1 = 0.8;     // SPEC.md:454 rgb mix 0.8 L1 + 0.2 D-SSIM
+  w.w_depth = 0.5;
+  w.w_feat = 1.0;
+  return w;
+}
+
+LGS_API lgs_status lgs_mapping_loss(lgs_ctx* ctx, lgs_saved* t, const lgs_images* rendered, const lgs_keyframe* kf,
+                                    const lgs_decoder* dec, const lgs_loss_weights* w_in, lgs_loss_breakdown* out) {
+  if (!ctx || !t || !rendered || !kf) return fail(LGS_EINVAL, "ctx/tape/rendered/keyframe is NULL");
+  const int H = t->cam.H, W = t->cam.W, d = t->dm.d, dp = t->dm.dp;
+  if (H < 11 || W < 11) return fail(LGS_EINVAL, "ssim: image %dx%d smaller than the 11x11 window", W, H);
+  if (!rendered->rgb || !kf->rgb || !kf->depth) return fail(LGS_EINVAL, "rendered rgb / keyframe rgb, depth needed");
+  if (d > 0) {
+    if (!rendered->feat || !kf->feat_gt || !dec) return fail(LGS_EINVAL, "feature loss needs feat, feat_gt, decoder");
+    if (dec->low_dim != d) return fail(LGS_EINVAL, "decoder low_dim %d != map feature dim %d", dec->low_dim, d);
+    if (!dec->w1 || !dec->b1 || !dec->w2 || !dec->b2) return fail(LGS_EINVAL, "decoder weights missing");
+    if (!decoder_supported(dec->hidden, dp, dec->high_dim))
+      return fail(LGS_EINVAL, "decoder hidden %d / D %d not supported (hidden 64, D <= 640)", dec->hidden,
+                  dec->high_dim);
+  }
+  const lgs_loss_weights w = w_in ? *w_in : lgs_loss_weights_default();
+  LGS_CUDA(cudaSetDevice(ctx->device));
+  cudaStream_t s = ctx->stream;
+  const size_t npix = (size_t)H * W;
+  const int D = d > 0 ? dec->high_dim : 0, hid = d > 0 ? dec->hidden : 0;
+  if (!t->cot) LGS_TRY(dalloc(ctx, &t->cot, npix * (4 + dp)));
+  if (!t->loss_sums) LGS_TRY(dalloc(ctx, &t->loss_sums, LOSS_COUNT));
+  // host inputs are staged (the reference API takes host images); device inputs are used in place
+  std::vector<float*> staged;
+  auto dev_in = [&](const float* p, size_t count, int memory, const float** outp) -> lgs_status {
+    if (memory != LGS_MEM_HOST || !p) {
+      *outp = p;
+      return LGS_OK;
+    }
+    float* q = nullptr;
+    LGS_TRY(dalloc(ctx, &q, count));
+    LGS_CUDA(cudaMemcpyAsync(q, p, sizeof(float) * count, cudaMemcpyHostToDevice, s));
+    staged.push_back(q);
+    *outp = q;
+    return LGS_OK;
+  };
+  LossArgs a;
+  a.H = H; a.W = W; a.d = d; a.dp = dp; a.D = D; a.hidden = hid;
+  a.depth = t->ps.depth;
+  a.acc = t->ps.acc;
+  lgs_status st = LGS_OK;
+  auto cleanup = [&]() {
+    for (float* q : staged) dfree(ctx, q);
+  };
+#define LOSS_TRY(expr)          \
+  do {                          \
+    st = (expr);                \
+    if (st != LGS_OK) {         \
+      cleanup();                \
+      return st;                \
+    }                           \
+  } while (0)
+  LOSS_TRY(dev_in(rendered->rgb, npix * 3, rendered->memory, &a.rgb));
+  if (d > 0) LOSS_TRY(dev_in(rendered->feat, npix * d, rendered->memory, &a.feat));
+  LOSS_TRY(dev_in(kf->rgb, npix * 3, kf->memory, &a.rgb_gt));
+  LOSS_TRY(dev_in(kf->depth, npix, kf->memory, &a.depth_gt));
+  if (d > 0) {
+    LOSS_TRY(dev_in(kf->feat_gt, npix * D, kf->memory, &a.feat_gt));
+    LOSS_TRY(dev_in(dec->w1, (size_t)hid * d, dec->memory, &a.w1));
+    LOSS_TRY(dev_in(dec->b1, (size_t)hid, dec->memory, &a.b1));
+    LOSS_TRY(dev_in(dec->w2, (size_t)D * hid, dec->memory, &a.w2));
+    LOSS_TRY(dev_in(dec->b2, (size_t)D, dec->memory, &a.b2));
+  }
+  float* abc = nullptr;
+  LOSS_TRY(dalloc(ctx, &abc, npix * 9));
+  staged.push_back(abc);
+  a.abc = abc;
+  a.sums = t->loss_sums;
+  a.cot = t->cot;
+  a.cot_stride = 4 + dp;
+  a.w_l1 = w.w_l1; a.w_depth = w.w_depth; a.w_feat = d > 0 ? w.w_feat : 0.0;
+  {
+    PhaseScope ph(ctx, PH_LOSS);
+    if (launch_mapping_loss(a, s) != 0) {
+      cleanup();
+      return fail(LGS_ECUDA, "mapping loss launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+    }
+  }
+  ctx->launches += 3 + (d > 0 ? 1 : 0);
+  LOSS_TRY(cudaGetLastError() == cudaSuccess ? LGS_OK : fail(LGS_ECUDA, "mapping loss kernels failed"));
+  cleanup();
+#undef LOSS_TRY
+  if (out) {
+    double h[LOSS_COUNT];
+    LGS_CUDA(cudaMemcpyAsync(h, t->loss_sums, sizeof h, cudaMemcpyDeviceToHost, s));
+    LGS_CUDA(cudaStreamSynchronize(s));
+    const double npos = (double)(H - 10) * (double)(W - 10);
+    out->ssim = h[LOSS_SSIM] / (3.0 * npos);
+    out->l_rgb = w.w_l1 * h[LOSS_L1_RGB] / (3.0 * (double)npix) + (1.0 - w.w_l1) * (1.0 - out->ssim) / 2.0;
+    out->depth_pixels = (int64_t)h[LOSS_DEPTH_CNT];
+    out->l_depth = out->depth_pixels ? h[LOSS_DEPTH_ABS] / h[LOSS_DEPTH_CNT] : 0.0;
+    out->l_feat = d > 0 ? h[LOSS_FEAT_ABS] / ((double)npix * D) : 0.0;
+    out->l_total = out->l_rgb + w.w_depth * out->l_depth + w.w_feat * out->l_feat;
+  }
+  return LGS_OK;
+}
+
+LGS_API lgs_status lgs_debug_cotangents(lgs_ctx* ctx, const lgs_saved* t, float* rgb, float* depth, float* feat) {
+  if (!ctx || !t) return fail(LGS_EINVAL, "ctx/tape is NULL");
+  if (!t->cot) return fail(LGS_EINVAL, "tape holds no cotangents");
+  const size_t npix = (size_t)t->cam.H * t->cam.W;
+  const int stride = 4 + t->dm.dp, d = t->dm.d;
+  std::vector<float> h(npix * stride);
+  LGS_CUDA(cudaSetDevice(ctx->device));
+  LGS_CUDA(cudaMemcpyAsync(h.data(), t->cot, sizeof(float) * h.size(), cudaMemcpyDeviceToHost, ctx->stream));
+  LGS_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (size_t p = 0; p < npix; ++p) {
+    const float* c = h.data() + p * stride;
+    if (rgb) std::memcpy(rgb + p * 3, c, sizeof(float) * 3);
+    if (depth) depth[p] = c[3];
+    if (feat && d) std::memcpy(feat + p * d, c + 4, sizeof(float) * d);
+  }
+  return LGS_OK;
+}
+
 LGS_API lgs_status lgs_saved_l1_loss(lgs_ctx* ctx, const lgs_saved* tape, double* loss) {
   if (!ctx || !tape || !loss) return fail(LGS_EINVAL, "NULL argument");
   if (!tape->loss) return fail(LGS_EINVAL, "tape has no fused L1 loss");
@@ -898,7 +1027,8 @@ LGS_API lgs_status lgs_saved_work(const lgs_saved* tape, int64_t* evaluated, int
 
 LGS_API const char* lgs_phase_name(int32_t phase) {
   static const char* names[LGS_PHASE_COUNT] = {"preprocess", "depth_sort_scan", "duplicate_keys", "tile_sort_ranges",
-                                               "blend_fwd", "blend_bwd", "preprocess_bwd", "map_upload"};
+                                               "blend_fwd", "blend_bwd", "preprocess_bwd", "map_upload",
+                                               "mapping_loss", "adam", "allreduce", "coverage"};
   return (phase >= 0 && phase < LGS_PHASE_COUNT) ? names[phase] : "?";
 }
 

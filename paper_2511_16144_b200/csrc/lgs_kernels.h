@@ -115,4 +115,26 @@ struct GradOut {
 void launch_preprocess_bwd(const DevMap& m, const DevCam& c, const ViewBufs& v, const float* gacc, int slots,
                            const GradOut& g, cudaStream_t s);
 
+// K8 mapping losses (loss.cu): SSIM + L1 on rgb, masked depth L1, decoder chain on features.
+enum { LOSS_L1_RGB = 0, LOSS_SSIM = 1, LOSS_DEPTH_ABS = 2, LOSS_DEPTH_CNT = 3, LOSS_FEAT_ABS = 4, LOSS_COUNT = 8 };
+struct LossArgs {
+  int H = 0, W = 0;
+  int d = 0, dp = 0, D = 0, hidden = 0;
+  const float* rgb = nullptr;       // rendered [H][W][3]
+  const float* depth = nullptr;     // rendered, alpha-normalized [H][W]
+  const float* acc = nullptr;       // [H][W]
+  const float* feat = nullptr;      // rendered [H][W][d]
+  const float* rgb_gt = nullptr;    // keyframe [H][W][3]
+  const float* depth_gt = nullptr;  // keyframe [H][W]
+  const float* feat_gt = nullptr;   // keyframe [H][W][D]
+  const float *w1 = nullptr, *b1 = nullptr, *w2 = nullptr, *b2 = nullptr;  // decoder
+  double w_l1 = 0.8, w_depth = 0.5, w_feat = 1.0;
+  float* abc = nullptr;             // scratch [9][H][W]
+  double* sums = nullptr;           // [LOSS_COUNT]
+  float* cot = nullptr;             // [H][W][cot_stride] = g_rgb 3 | g_depth | g_feat DP
+  int cot_stride = 0;
+};
+bool decoder_supported(int hidden, int dp, int D);
+int launch_mapping_loss(const LossArgs& a, cudaStream_t s);  // 0 ok, else a CUDA error
+
 }  // namespace lgs

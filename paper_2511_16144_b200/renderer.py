@@ -235,6 +235,16 @@ class RenderOutput:
         check(_lib.load().lgs_debug_pixel_state(self.ctx.h, self.tape, ft.ctypes.data, nc.ctypes.data))
         return ft, nc
 
+    def cotangents(self):
+        """(g_rgb [H,W,3], g_depth [H,W], g_feat [H,W,d]) held by the tape (fused L1 / mapping loss)."""
+        H, W = self.camera.height, self.camera.width
+        r = np.zeros((H, W, 3), np.float32)
+        dd = np.zeros((H, W), np.float32)
+        f = np.zeros((H, W, self.d), np.float32)
+        check(_lib.load().lgs_debug_cotangents(self.ctx.h, self.tape, r.ctypes.data, dd.ctypes.data,
+                                               f.ctypes.data if self.d else None))
+        return r, dd, f
+
     def __del__(self):
         try:
             if getattr(self, "tape", None) and _lib._lib is not None:
@@ -357,6 +367,47 @@ def render_backward_l1(out: RenderOutput, pose: bool = False, into: dict | None 
     gs = _grads_struct(g, accumulate)
     pg = (C.c_float * 6)() if pose else None
     check(_lib.load().lgs_render_backward_l1(out.ctx.h, out.tape, C.byref(gs), pg))
+    if pose:
+        g["pose"] = np.array(list(pg), dtype=np.float64)
+    return g
+
+
+def mapping_loss(out: RenderOutput, keyframe: dict, decoder=None, w_l1: float = 0.8, w_depth: float = 0.5,
+                 w_feat: float = 1.0, readback: bool = True):
+    """SPEC.md:418-426 compute_losses on the GPU (lgs_mapping_loss): stores d l_total / d images in
+    the tape for render_backward_loss and returns the LossBreakdown (or None without readback).
+
+    ``keyframe``: rgb [H,W,3], depth [H,W] (<= 0 / non-finite = invalid), feat_gt [H,W,D];
+    ``decoder``: (w1 [hidden,d], b1 [hidden], w2 [D,hidden], b2 [D]) -- the frozen codec decoder."""
+    H, W, d = out.camera.height, out.camera.width, out.d
+    keep = {k: _f32(keyframe[k]) for k in ("rgb", "depth") if keyframe.get(k) is not None}
+    kmem = _mem(keep["rgb"])
+    if d:
+        keep["feat_gt"] = _f32(keyframe["feat_gt"])
+        w1, b1, w2, b2 = (_f32(x) for x in decoder)
+        keep.update(w1=w1, b1=b1, w2=w2, b2=b2)
+        dec = _lib.LgsDecoder(int(w2.shape[0]), int(w1.shape[0]), int(w1.shape[1]), _ptr(w1), _ptr(b1), _ptr(w2),
+                              _ptr(b2), _mem(w1))
+    kf = _lib.LgsKeyframe(_ptr(keep["rgb"]), _ptr(keep["depth"]), _ptr(keep.get("feat_gt")), kmem)
+    rendered = _lib.LgsImages(_ptr(out.rgb), None, _ptr(out.feat) if d else None, None, _mem(out.rgb))
+    w = _lib.LgsLossWeights(w_l1, w_depth, w_feat)
+    br = _lib.LgsLossBreakdown() if readback else None
+    check(_lib.load().lgs_mapping_loss(out.ctx.h, out.tape, C.byref(rendered), C.byref(kf),
+                                       C.byref(dec) if d else None, C.byref(w), C.byref(br) if br else None))
+    del keep
+    if br is None:
+        return None
+    return dict(l_rgb=br.l_rgb, l_depth=br.l_depth, l_feat=br.l_feat, l_total=br.l_total, ssim=br.ssim,
+                depth_pixels=br.depth_pixels)
+
+
+def render_backward_loss(out: RenderOutput, pose: bool = False, into: dict | None = None, accumulate: bool = False):
+    """Backward of the loss whose cotangents the tape holds (fused L1 or mapping_loss)."""
+    dev = _is_torch(out.rgb) and out.rgb.is_cuda
+    g = into or alloc_grads(out.n, out.d, out.K, device=out.ctx.device if dev else None)
+    gs = _grads_struct(g, accumulate)
+    pg = (C.c_float * 6)() if pose else None
+    check(_lib.load().lgs_render_backward_loss(out.ctx.h, out.tape, C.byref(gs), pg))
     if pose:
         g["pose"] = np.array(list(pg), dtype=np.float64)
     return g
