@@ -64,6 +64,7 @@ enum { LGS_TILE = 16, LGS_MAX_FEATURE_DIM = 32, LGS_MAX_SH_DEGREE = 3 };
 typedef struct lgs_ctx lgs_ctx;
 typedef struct lgs_map lgs_map;
 typedef struct lgs_saved lgs_saved;
+typedef struct lgs_adam lgs_adam;
 
 /* renderer.hpp:15-22; defaults from lgs_render_config_default(). */
 typedef struct {
@@ -289,6 +290,25 @@ LGS_API lgs_status lgs_debug_cotangents(lgs_ctx* ctx, const lgs_saved* tape, flo
 /* Back-propagates the cotangents stored in the tape (fused L1 or lgs_mapping_loss) to the map. */
 LGS_API lgs_status lgs_render_backward_loss(lgs_ctx* ctx, const lgs_saved* tape, lgs_map_grads* grads,
                                             float* pose_grad);
+
+/* ---- Adam step on the resident map (SPEC.md:430 mapping_round) ---------
+ * Per-attribute learning rates of SPEC.md:430; standard bias-corrected Adam (beta1 0.9, beta2
+ * 0.999, eps 1e-8: the SPEC names only the optimizer).  SH bands above DC use lr_sh_rest
+ * (colour lr / 20 by default; SH0 maps are the reference's colour).  Moments live on the device
+ * in the map's packed layout; gradients are the dense device lgs_map_grads of a backward (after
+ * lgs_allreduce_grads in a multi-GPU batch: every rank then applies the identical update). */
+typedef struct {
+  double lr_position, lr_rotation, lr_log_scale, lr_opacity, lr_color, lr_sh_rest, lr_feature;
+  double beta1, beta2, eps;
+} lgs_adam_config;
+LGS_API lgs_adam_config lgs_adam_config_default(void);
+LGS_API lgs_status lgs_adam_create(lgs_ctx* ctx, const lgs_map* map, const lgs_adam_config* cfg, lgs_adam** out);
+LGS_API lgs_status lgs_adam_destroy(lgs_adam* adam);
+LGS_API int64_t lgs_adam_steps(const lgs_adam* adam);
+LGS_API lgs_status lgs_adam_step(lgs_ctx* ctx, lgs_adam* adam, lgs_map* map, const lgs_map_grads* grads);
+/* Copy the resident map back out in the reference layouts (`dst` shape must match; host or
+ * device memory; NULL members skipped). */
+LGS_API lgs_status lgs_map_download(lgs_ctx* ctx, const lgs_map* map, lgs_gaussians* dst);
 
 /* ---- multi-view mapping batches --------------------------------------------
  * New (the reference is single-threaded CPU code with no multi-view path).  Views are sharded

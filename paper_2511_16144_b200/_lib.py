@@ -76,6 +76,11 @@ class LgsLossBreakdown(C.Structure):
                 ("ssim", C.c_double), ("depth_pixels", C.c_int64)]
 
 
+class LgsAdamConfig(C.Structure):
+    _fields_ = [(n, C.c_double) for n in ("lr_position", "lr_rotation", "lr_log_scale", "lr_opacity", "lr_color",
+                                          "lr_sh_rest", "lr_feature", "beta1", "beta2", "eps")]
+
+
 class LgsCommId(C.Structure):
     _fields_ = [("bytes", C.c_uint8 * 128)]
 
@@ -118,6 +123,12 @@ SIGNATURES = [
                                    C.POINTER(LgsDecoder), C.POINTER(LgsLossWeights), C.POINTER(LgsLossBreakdown)]),
     ("lgs_render_backward_loss", C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(LgsMapGrads), _fp]),
     ("lgs_debug_cotangents", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("lgs_adam_config_default", LgsAdamConfig, []),
+    ("lgs_adam_create", C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(LgsAdamConfig), C.POINTER(C.c_void_p)]),
+    ("lgs_adam_destroy", C.c_int, [C.c_void_p]),
+    ("lgs_adam_steps", C.c_int64, [C.c_void_p]),
+    ("lgs_adam_step", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(LgsMapGrads)]),
+    ("lgs_map_download", C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(LgsGaussians)]),
     ("lgs_comm_unique_id", C.c_int, [C.POINTER(LgsCommId)]),
     ("lgs_comm_init", C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.POINTER(LgsCommId)]),
     ("lgs_comm_destroy", C.c_int, [C.c_void_p]),

@@ -140,6 +140,17 @@ struct lgs_map {
   float* feat = nullptr;
 };
 
+struct lgs_adam {
+  lgs_ctx* ctx = nullptr;
+  int64_t n = 0;
+  int d = 0, dp = 0, K = 1;
+  lgs_adam_config cfg{};
+  int64_t step = 0;
+  // first / second moments in the map's packed layout
+  float4 *m_po = nullptr, *m_rot = nullptr, *m_sc = nullptr, *v_po = nullptr, *v_rot = nullptr, *v_sc = nullptr;
+  float *m_sh = nullptr, *v_sh = nullptr, *m_ft = nullptr, *v_ft = nullptr;
+};
+
 struct lgs_saved {
   lgs_ctx* ctx = nullptr;
   lgs_map* owned_map = nullptr;  // lgs_render convenience path
@@ -1241,5 +1252,151 @@ LGS_API lgs_status lgs_allreduce_grads(lgs_ctx* ctx, const lgs_map* map, lgs_map
   return LGS_OK;
 }
 #undef LGS_NCCL
+
+}  // extern "C"
+
+// -------------------------------------------------------------------------------------------
+// Adam step on the resident map and the map download
+// -------------------------------------------------------------------------------------------
+namespace {
+
+MapParams map_params(lgs_map* m) {
+  MapParams p;
+  p.n = m->dm.n; p.d = m->dm.d; p.dp = m->dm.dp; p.K = m->dm.K;
+  p.pos_opa = m->pos_opa; p.rot = m->rot; p.scale = m->scale; p.sh = m->sh; p.feat = m->feat;
+  return p;
+}
+
+void free_adam(lgs_adam* a) {
+  lgs_ctx* ctx = a->ctx;
+  cudaSetDevice(ctx->device);
+  dfree(ctx, a->m_po); dfree(ctx, a->m_rot); dfree(ctx, a->m_sc); dfree(ctx, a->m_sh); dfree(ctx, a->m_ft);
+  dfree(ctx, a->v_po); dfree(ctx, a->v_rot); dfree(ctx, a->v_sc); dfree(ctx, a->v_sh); dfree(ctx, a->v_ft);
+  delete a;
+  ctx_release(ctx);
+}
+
+}  // namespace
+
+extern "C" {
+
+LGS_API lgs_adam_config lgs_adam_config_default(void) {
+  lgs_adam_config c;
+  c.lr_position = 1.6e-4;
+  c.lr_rotation = 1e-3;
+  c.lr_log_scale = 5e-3;
+  c.lr_opacity = 5e-2;
+  c.lr_color = 2.5e-3;
+  c.lr_sh_rest = 2.5e-3 / 20.0;
+  c.lr_feature = 2.5e-3;
+  c.beta1 = 0.9;
+  c.beta2 = 0.999;
+  c.eps = 1e-8;
+  return c;
+}
+
+LGS_API lgs_status lgs_adam_create(lgs_ctx* ctx, const lgs_map* map, const lgs_adam_config* cfg, lgs_adam** out) {
+  if (!ctx || !map || !out) return fail(LGS_EINVAL, "ctx/map/out is NULL");
+  *out = nullptr;
+  const lgs_adam_config c = cfg ? *cfg : lgs_adam_config_default();
+  if (!(c.beta1 >= 0.0 && c.beta1 < 1.0 && c.beta2 >= 0.0 && c.beta2 < 1.0 && c.eps > 0.0))
+    return fail(LGS_EINVAL, "Adam: need 0 <= beta < 1 and eps > 0");
+  LGS_CUDA(cudaSetDevice(ctx->device));
+  lgs_adam* a = new lgs_adam();
+  a->ctx = ctx;
+  ctx->refs++;
+  a->n = map->dm.n; a->d = map->dm.d; a->dp = map->dm.dp; a->K = map->dm.K;
+  a->cfg = c;
+  const size_t n = (size_t)a->n, ks = n * a->K * 3, fs = n * (a->dp > 0 ? a->dp : 1);
+  lgs_status st = LGS_OK;
+  if ((st = dalloc(ctx, &a->m_po, n)) != LGS_OK || (st = dalloc(ctx, &a->m_rot, n)) != LGS_OK ||
+      (st = dalloc(ctx, &a->m_sc, n)) != LGS_OK || (st = dalloc(ctx, &a->m_sh, ks)) != LGS_OK ||
+      (st = dalloc(ctx, &a->m_ft, fs)) != LGS_OK || (st = dalloc(ctx, &a->v_po, n)) != LGS_OK ||
+      (st = dalloc(ctx, &a->v_rot, n)) != LGS_OK || (st = dalloc(ctx, &a->v_sc, n)) != LGS_OK ||
+      (st = dalloc(ctx, &a->v_sh, ks)) != LGS_OK || (st = dalloc(ctx, &a->v_ft, fs)) != LGS_OK) {
+    free_adam(a);
+    return st;
+  }
+  cudaStream_t s = ctx->stream;
+  cudaMemsetAsync(a->m_po, 0, sizeof(float4) * n, s); cudaMemsetAsync(a->v_po, 0, sizeof(float4) * n, s);
+  cudaMemsetAsync(a->m_rot, 0, sizeof(float4) * n, s); cudaMemsetAsync(a->v_rot, 0, sizeof(float4) * n, s);
+  cudaMemsetAsync(a->m_sc, 0, sizeof(float4) * n, s); cudaMemsetAsync(a->v_sc, 0, sizeof(float4) * n, s);
+  cudaMemsetAsync(a->m_sh, 0, sizeof(float) * ks, s); cudaMemsetAsync(a->v_sh, 0, sizeof(float) * ks, s);
+  cudaMemsetAsync(a->m_ft, 0, sizeof(float) * fs, s); cudaMemsetAsync(a->v_ft, 0, sizeof(float) * fs, s);
+  LGS_CUDA(cudaGetLastError());
+  *out = a;
+  return LGS_OK;
+}
+
+LGS_API lgs_status lgs_adam_destroy(lgs_adam* adam) {
+  if (adam) free_adam(adam);
+  return LGS_OK;
+}
+
+LGS_API int64_t lgs_adam_steps(const lgs_adam* adam) { return adam ? adam->step : -1; }
+
+LGS_API lgs_status lgs_adam_step(lgs_ctx* ctx, lgs_adam* a, lgs_map* map, const lgs_map_grads* grads) {
+  if (!ctx || !a || !map || !grads) return fail(LGS_EINVAL, "ctx/adam/map/grads is NULL");
+  if (a->n != map->dm.n || a->d != map->dm.d || a->K != map->dm.K)
+    return fail(LGS_EINVAL, "Adam state was created for a different map shape");
+  if (grads->memory != LGS_MEM_DEVICE) return fail(LGS_EINVAL, "Adam step needs device gradients");
+  if (!grads->position || !grads->rotation || !grads->log_scale || !grads->opacity_logit || !grads->sh ||
+      (a->d > 0 && !grads->feature))
+    return fail(LGS_EINVAL, "Adam step needs every gradient group");
+  LGS_CUDA(cudaSetDevice(ctx->device));
+  MapParams p = map_params(map), m = p, v = p;
+  m.pos_opa = a->m_po; m.rot = a->m_rot; m.scale = a->m_sc; m.sh = a->m_sh; m.feat = a->m_ft;
+  v.pos_opa = a->v_po; v.rot = a->v_rot; v.scale = a->v_sc; v.sh = a->v_sh; v.feat = a->v_ft;
+  GradIn g;
+  g.position = grads->position; g.rotation = grads->rotation; g.log_scale = grads->log_scale;
+  g.opacity = grads->opacity_logit; g.sh = grads->sh; g.feature = grads->feature;
+  const lgs_adam_config& c = a->cfg;
+  AdamLr lr{(float)c.lr_position, (float)c.lr_rotation, (float)c.lr_log_scale, (float)c.lr_opacity,
+            (float)c.lr_color, (float)c.lr_sh_rest, (float)c.lr_feature};
+  ++a->step;
+  {
+    PhaseScope ph(ctx, PH_ADAM);
+    launch_adam(p, m, v, g, 0, a->n, lr, c.beta1, c.beta2, c.eps, a->step, ctx->stream);
+  }
+  ctx->launches += a->n > 0 ? 1 : 0;
+  LGS_CUDA(cudaGetLastError());
+  return LGS_OK;
+}
+
+LGS_API lgs_status lgs_map_download(lgs_ctx* ctx, const lgs_map* map, lgs_gaussians* dst) {
+  if (!ctx || !map || !dst) return fail(LGS_EINVAL, "ctx/map/dst is NULL");
+  if (dst->n != map->dm.n || dst->feature_dim != map->dm.d || dst->sh_degree != map->dm.deg)
+    return fail(LGS_EINVAL, "lgs_map_download: destination shape differs from the map");
+  LGS_CUDA(cudaSetDevice(ctx->device));
+  cudaStream_t s = ctx->stream;
+  const size_t n = (size_t)map->dm.n;
+  const size_t sz[6] = {n * 3, n * 4, n * 3, n, n * map->dm.K * 3, n * map->dm.d};
+  float* outs[6] = {(float*)dst->positions, (float*)dst->rotations, (float*)dst->log_scales,
+                    (float*)dst->opacity_logits, (float*)dst->sh, (float*)dst->features};
+  float* dev[6] = {};
+  const bool host = dst->memory == LGS_MEM_HOST;
+  float* stage = nullptr;
+  if (host) {
+    LGS_TRY(dalloc(ctx, &stage, sz[0] + sz[1] + sz[2] + sz[3] + sz[4] + sz[5]));
+    float* q = stage;
+    for (int k = 0; k < 6; ++k) {
+      dev[k] = outs[k] ? q : nullptr;
+      q += sz[k];
+    }
+  } else {
+    for (int k = 0; k < 6; ++k) dev[k] = outs[k];
+  }
+  launch_unpack_map(map_params(const_cast<lgs_map*>(map)), dev[0], dev[1], dev[2], dev[3], dev[4],
+                    map->dm.d > 0 ? dev[5] : nullptr, s);
+  ctx->launches += n > 0 ? 1 : 0;
+  if (host) {
+    for (int k = 0; k < 6; ++k)
+      if (outs[k] && sz[k]) LGS_CUDA(cudaMemcpyAsync(outs[k], dev[k], sizeof(float) * sz[k], cudaMemcpyDeviceToHost, s));
+    dfree(ctx, stage);
+    LGS_CUDA(cudaStreamSynchronize(s));
+  }
+  LGS_CUDA(cudaGetLastError());
+  return LGS_OK;
+}
 
 }  // extern "C"

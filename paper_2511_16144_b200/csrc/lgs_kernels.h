@@ -137,4 +137,31 @@ struct LossArgs {
 bool decoder_supported(int hidden, int dp, int D);
 int launch_mapping_loss(const LossArgs& a, cudaStream_t s);  // 0 ok, else a CUDA error
 
+// K10 Adam step / map unpack (optim.cu).  MapParams: writable view of packed map arrays (the map
+// itself, or one of the Adam moment buffers, which share its layout).
+struct MapParams {
+  int64_t n = 0;
+  int d = 0, dp = 0, K = 1;
+  float4* pos_opa = nullptr;
+  float4* rot = nullptr;
+  float4* scale = nullptr;
+  float* sh = nullptr;
+  float* feat = nullptr;
+};
+struct GradIn {  // reference layouts (renderer.hpp:59-68)
+  const float* position = nullptr;   // [N][3]
+  const float* rotation = nullptr;   // [N][4] w,x,y,z
+  const float* log_scale = nullptr;  // [N][3]
+  const float* opacity = nullptr;    // [N]
+  const float* sh = nullptr;         // [N][K][3]
+  const float* feature = nullptr;    // [d][N]
+};
+struct AdamLr {
+  float position, rotation, log_scale, opacity, sh_dc, sh_rest, feature;
+};
+void launch_adam(const MapParams& p, const MapParams& m, const MapParams& v, const GradIn& g, int64_t g0, int64_t g1,
+                 const AdamLr& lr, double beta1, double beta2, double eps, int64_t step, cudaStream_t s);
+void launch_unpack_map(const MapParams& p, float* pos, float* rot, float* log_s, float* opac, float* sh, float* feat_dn,
+                       cudaStream_t s);
+
 }  // namespace lgs

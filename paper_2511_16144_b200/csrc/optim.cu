@@ -1,0 +1,140 @@
+// optim.cu -- K9b/K10: the per-attribute Adam step on the resident map and the map unpack.
+//
+// SURVEY.md §8f row 2 (SPEC.md:430 mapping_round: "apply one Adam step per attribute group (lr:
+// position 1.6e-4, rotation 1e-3, log-scale 5e-3, opacity-logit 5e-2, color 2.5e-3, feature
+// 2.5e-3)").  The reference leaves mapping.cpp unimplemented; the Adam form is the standard one
+// (bias-corrected first and second moments), defaults beta1 0.9, beta2 0.999, eps 1e-8; SH bands
+// above the DC term use colour lr / 20 (the usual splatting convention; SH0 == the reference colour).
+//
+// One thread per Gaussian over a range [g0, g1) (the whole map, or this rank's shard after a
+// reduce-scatter).  Parameters and both moments live in the map's packed layout (float4 position
+// + opacity logit, float4 rotation x,y,z,w, float4 log-scale, SH [N][K][3], feature [N][DP]); the
+// gradients arrive in the reference layouts (renderer.hpp:59-68: rotation w,x,y,z, feature
+// [d][N]).  Bytes per Gaussian: parameters + two moments read and written (6 x 304 B at SH3,
+// d = 16) + gradients read (300 B) -- HBM-bound.
+#include <cmath>
+
+#include "lgs_internal.cuh"
+#include "lgs_kernels.h"
+
+namespace lgs {
+
+namespace {
+
+struct AdamF {
+  float b1, b2, eps, c1, c2;  // c1 = 1 / (1 - b1^t), c2 = 1 / (1 - b2^t)
+};
+
+__device__ __forceinline__ float adam1(float& p, float& m, float& v, float g, float lr, const AdamF& a) {
+  m = fmaf(a.b1, m, (1.f - a.b1) * g);
+  v = fmaf(a.b2, v, (1.f - a.b2) * g * g);
+  const float mh = m * a.c1, vh = v * a.c2;
+  p -= lr * mh / (sqrtf(vh) + a.eps);
+  return p;
+}
+
+__device__ __forceinline__ void adam4(float4& p, float4& m, float4& v, const float (&g)[4], int nc, float lr,
+                                      const AdamF& a) {
+  float* pp = reinterpret_cast<float*>(&p);
+  float* mm = reinterpret_cast<float*>(&m);
+  float* vv = reinterpret_cast<float*>(&v);
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if (k < nc) adam1(pp[k], mm[k], vv[k], g[k], lr, a);
+}
+
+__global__ void adam_kernel(MapParams p, MapParams m, MapParams v, GradIn g, int64_t g0, int64_t g1, AdamLr lr,
+                            AdamF a) {
+  const int64_t i = g0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= g1) return;
+  const int64_t n = p.n;
+  // position xyz + opacity logit (float4)
+  {
+    float4 pp = p.pos_opa[i], mm = m.pos_opa[i], vv = v.pos_opa[i];
+    const float gp[4] = {g.position[i * 3 + 0], g.position[i * 3 + 1], g.position[i * 3 + 2], 0.f};
+    adam4(pp, mm, vv, gp, 3, lr.position, a);
+    adam1(pp.w, mm.w, vv.w, g.opacity[i], lr.opacity, a);
+    p.pos_opa[i] = pp; m.pos_opa[i] = mm; v.pos_opa[i] = vv;
+  }
+  // rotation: stored x,y,z,w; gradient ordered w,x,y,z (renderer.hpp:61)
+  {
+    float4 pp = p.rot[i], mm = m.rot[i], vv = v.rot[i];
+    const float4 gr = reinterpret_cast<const float4*>(g.rotation)[i];
+    const float gq[4] = {gr.y, gr.z, gr.w, gr.x};
+    adam4(pp, mm, vv, gq, 4, lr.rotation, a);
+    p.rot[i] = pp; m.rot[i] = mm; v.rot[i] = vv;
+  }
+  {
+    float4 pp = p.scale[i], mm = m.scale[i], vv = v.scale[i];
+    const float gs[4] = {g.log_scale[i * 3 + 0], g.log_scale[i * 3 + 1], g.log_scale[i * 3 + 2], 0.f};
+    adam4(pp, mm, vv, gs, 3, lr.log_scale, a);
+    p.scale[i] = pp; m.scale[i] = mm; v.scale[i] = vv;
+  }
+  // SH [K][3]: DC at colour lr, higher bands at sh_rest lr
+  {
+    const int ks = 3 * p.K;
+    float* ps = p.sh + i * ks;
+    float* ms = m.sh + i * ks;
+    float* vs = v.sh + i * ks;
+    const float* gs = g.sh + i * ks;
+    for (int k = 0; k < ks; ++k) {
+      float pk = ps[k], mk = ms[k], vk = vs[k];
+      adam1(pk, mk, vk, gs[k], k < 3 ? lr.sh_dc : lr.sh_rest, a);
+      ps[k] = pk; ms[k] = mk; vs[k] = vk;
+    }
+  }
+  // feature: packed [N][DP] (zero padding untouched), gradient [d][N]
+  if (p.d > 0) {
+    float* pf = p.feat + i * p.dp;
+    float* mf = m.feat + i * p.dp;
+    float* vf = v.feat + i * p.dp;
+    for (int c = 0; c < p.d; ++c) {
+      float pk = pf[c], mk = mf[c], vk = vf[c];
+      adam1(pk, mk, vk, g.feature[(int64_t)c * n + i], lr.feature, a);
+      pf[c] = pk; mf[c] = mk; vf[c] = vk;
+    }
+  }
+}
+
+__global__ void unpack_map_kernel(MapParams p, float* __restrict__ pos, float* __restrict__ rot,
+                                  float* __restrict__ log_s, float* __restrict__ opac, float* __restrict__ sh,
+                                  float* __restrict__ feat_dn) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= p.n) return;
+  const float4 po = p.pos_opa[i], r = p.rot[i], s = p.scale[i];
+  if (pos) { pos[i * 3 + 0] = po.x; pos[i * 3 + 1] = po.y; pos[i * 3 + 2] = po.z; }
+  if (opac) opac[i] = po.w;
+  if (rot) reinterpret_cast<float4*>(rot)[i] = r;  // x,y,z,w storage order (gaussian_map.hpp)
+  if (log_s) { log_s[i * 3 + 0] = s.x; log_s[i * 3 + 1] = s.y; log_s[i * 3 + 2] = s.z; }
+  if (sh) {
+    const int ks = 3 * p.K;
+    for (int k = 0; k < ks; ++k) sh[i * ks + k] = p.sh[i * ks + k];
+  }
+  if (feat_dn)
+    for (int c = 0; c < p.d; ++c) feat_dn[(int64_t)c * p.n + i] = p.feat[i * p.dp + c];
+}
+
+}  // namespace
+
+void launch_adam(const MapParams& p, const MapParams& m, const MapParams& v, const GradIn& g, int64_t g0, int64_t g1,
+                 const AdamLr& lr, double beta1, double beta2, double eps, int64_t step, cudaStream_t s) {
+  if (g1 <= g0) return;
+  AdamF a;
+  a.b1 = (float)beta1;
+  a.b2 = (float)beta2;
+  a.eps = (float)eps;
+  a.c1 = (float)(1.0 / (1.0 - std::pow(beta1, (double)step)));
+  a.c2 = (float)(1.0 / (1.0 - std::pow(beta2, (double)step)));
+  const int threads = 256;
+  adam_kernel<<<(unsigned)((g1 - g0 + threads - 1) / threads), threads, 0, s>>>(p, m, v, g, g0, g1, lr, a);
+}
+
+void launch_unpack_map(const MapParams& p, float* pos, float* rot, float* log_s, float* opac, float* sh, float* feat_dn,
+                       cudaStream_t s) {
+  if (p.n == 0) return;
+  const int threads = 256;
+  unpack_map_kernel<<<(unsigned)((p.n + threads - 1) / threads), threads, 0, s>>>(p, pos, rot, log_s, opac, sh,
+                                                                                   feat_dn);
+}
+
+}  // namespace lgs

@@ -411,3 +411,47 @@ def render_backward_loss(out: RenderOutput, pose: bool = False, into: dict | Non
     if pose:
         g["pose"] = np.array(list(pg), dtype=np.float64)
     return g
+
+
+def map_download(dmap: DeviceMap, device: bool = False) -> dict:
+    """The resident map in the reference layouts (pos, rot x,y,z,w, log_s, opac, sh, feat [d,N])."""
+    n, d, K = dmap.n, dmap.d, dmap.K
+    shapes = {"pos": (n, 3), "rot": (n, 4), "log_s": (n, 3), "opac": (n,), "sh": (n, K, 3), "feat": (d, n)}
+    out = {k: _alloc_like(device, s, dmap.ctx.device) for k, s in shapes.items()}
+    g = _lib.LgsGaussians(n, d, dmap.sh_degree, _ptr(out["pos"]), _ptr(out["rot"]), _ptr(out["log_s"]),
+                          _ptr(out["opac"]), _ptr(out["sh"]), _ptr(out["feat"]) if d else None,
+                          LGS_MEM_DEVICE if device else LGS_MEM_HOST)
+    check(_lib.load().lgs_map_download(dmap.ctx.h, dmap.h, C.byref(g)))
+    return out
+
+
+class Adam:
+    """Per-attribute Adam on a resident map (lgs_adam_*; SPEC.md:430 learning rates)."""
+
+    def __init__(self, dmap: DeviceMap, **cfg):
+        L = _lib.load()
+        c = L.lgs_adam_config_default()
+        for k, v in cfg.items():
+            if not hasattr(c, k):
+                raise TypeError(f"unknown Adam option {k}")
+            setattr(c, k, float(v))
+        self.config = {k: getattr(c, k) for k, _ in _lib.LgsAdamConfig._fields_}
+        h = C.c_void_p()
+        check(L.lgs_adam_create(dmap.ctx.h, dmap.h, C.byref(c), C.byref(h)))
+        self.h, self.map = h, dmap
+
+    @property
+    def steps(self) -> int:
+        return int(_lib.load().lgs_adam_steps(self.h))
+
+    def step(self, grads: dict):
+        gs = _grads_struct(grads, False)
+        check(_lib.load().lgs_adam_step(self.map.ctx.h, self.h, self.map.h, C.byref(gs)))
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None) and _lib._lib is not None:
+                _lib._lib.lgs_adam_destroy(self.h)
+                self.h = None
+        except (AttributeError, TypeError):  # interpreter shutdown
+            pass
