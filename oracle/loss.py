@@ -153,19 +153,3 @@ def compute_losses(rgb, depth, feat, acc, kf_rgb, kf_depth, kf_feat, dec, w_dept
     br = dict(l_rgb=float(l_rgb), l_depth=l_depth, l_feat=l_feat, l_total=float(l_total), ssim=float(s),
               depth_pixels=cnt)
     return br, g_rgb, g_depth, g_feat
-
-
-def make_decoder(D, hidden, d, seed):
-    """Seeded decoder weights with the reference's Xavier-uniform init scale (codec.cpp:16-23) and
-    small random biases (a pretrained decoder has non-zero biases)."""
-    r = np.random.default_rng(seed)
-
-    def xavier(rows, cols):
-        a = np.sqrt(6.0 / (rows + cols))
-        return r.uniform(-a, a, size=(rows, cols))
-
-    w1 = xavier(hidden, d)
-    w2 = xavier(D, hidden)
-    b1 = r.normal(0.0, 0.05, size=hidden)
-    b2 = r.normal(0.0, 0.05, size=D)
-    return tuple(x.astype(np.float32) for x in (w1, b1, w2, b2))

@@ -1358,7 +1358,7 @@ LGS_API lgs_status lgs_adam_step(lgs_ctx* ctx, lgs_adam* a, lgs_map* map, const 
     PhaseScope ph(ctx, PH_ADAM);
     launch_adam(p, m, v, g, 0, a->n, lr, c.beta1, c.beta2, c.eps, a->step, ctx->stream);
   }
-  ctx->launches += a->n > 0 ? 1 : 0;
+  ctx->launches += a->n > 0 ? 2 : 0;
   LGS_CUDA(cudaGetLastError());
   return LGS_OK;
 }

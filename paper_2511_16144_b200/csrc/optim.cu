@@ -70,28 +70,50 @@ __global__ void adam_kernel(MapParams p, MapParams m, MapParams v, GradIn g, int
     adam4(pp, mm, vv, gs, 3, lr.log_scale, a);
     p.scale[i] = pp; m.scale[i] = mm; v.scale[i] = vv;
   }
-  // SH [K][3]: DC at colour lr, higher bands at sh_rest lr
-  {
-    const int ks = 3 * p.K;
-    float* ps = p.sh + i * ks;
-    float* ms = m.sh + i * ks;
-    float* vs = v.sh + i * ks;
-    const float* gs = g.sh + i * ks;
-    for (int k = 0; k < ks; ++k) {
-      float pk = ps[k], mk = ms[k], vk = vs[k];
-      adam1(pk, mk, vk, gs[k], k < 3 ? lr.sh_dc : lr.sh_rest, a);
-      ps[k] = pk; ms[k] = mk; vs[k] = vk;
-    }
-  }
+  // SH [K][3]: parameters, moments and gradients share one layout -> adam_sh_kernel (flat, float4)
   // feature: packed [N][DP] (zero padding untouched), gradient [d][N]
   if (p.d > 0) {
-    float* pf = p.feat + i * p.dp;
-    float* mf = m.feat + i * p.dp;
-    float* vf = v.feat + i * p.dp;
-    for (int c = 0; c < p.d; ++c) {
-      float pk = pf[c], mk = mf[c], vk = vf[c];
-      adam1(pk, mk, vk, g.feature[(int64_t)c * n + i], lr.feature, a);
-      pf[c] = pk; mf[c] = mk; vf[c] = vk;
+    float4* pf = reinterpret_cast<float4*>(p.feat + i * p.dp);
+    float4* mf = reinterpret_cast<float4*>(m.feat + i * p.dp);
+    float4* vf = reinterpret_cast<float4*>(v.feat + i * p.dp);
+    for (int c4 = 0; c4 < p.dp / 4; ++c4) {
+      float gv[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int c = c4 * 4 + k;
+        gv[k] = c < p.d ? g.feature[(int64_t)c * n + i] : 0.f;
+      }
+      float4 pp = pf[c4], mm = mf[c4], vv = vf[c4];
+      adam4(pp, mm, vv, gv, min(4, p.d - c4 * 4), lr.feature, a);
+      pf[c4] = pp; mf[c4] = mm; vf[c4] = vv;
+    }
+  }
+}
+
+__global__ void adam_sh_kernel(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
+                               const float* __restrict__ g, int64_t e0, int64_t e1, int ks, float lr_dc,
+                               float lr_rest, AdamF a) {
+  const int64_t q = e0 / 4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // float4 index
+  const int64_t e = q * 4;
+  if (e >= e1) return;
+  if (e + 4 <= e1 && (e0 & 3) == 0) {
+    float4 pp = reinterpret_cast<float4*>(p)[q], mm = reinterpret_cast<float4*>(m)[q],
+           vv = reinterpret_cast<float4*>(v)[q];
+    const float4 gg = reinterpret_cast<const float4*>(g)[q];
+    const float gv[4] = {gg.x, gg.y, gg.z, gg.w};
+    float* pa = reinterpret_cast<float*>(&pp);
+    float* ma = reinterpret_cast<float*>(&mm);
+    float* va = reinterpret_cast<float*>(&vv);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) adam1(pa[k], ma[k], va[k], gv[k], (int)((e + k) % ks) < 3 ? lr_dc : lr_rest, a);
+    reinterpret_cast<float4*>(p)[q] = pp;
+    reinterpret_cast<float4*>(m)[q] = mm;
+    reinterpret_cast<float4*>(v)[q] = vv;
+  } else {
+    for (int64_t j = max(e, e0); j < min(e + 4, e1); ++j) {
+      float pk = p[j], mk = m[j], vk = v[j];
+      adam1(pk, mk, vk, g[j], (int)(j % ks) < 3 ? lr_dc : lr_rest, a);
+      p[j] = pk; m[j] = mk; v[j] = vk;
     }
   }
 }
@@ -127,6 +149,11 @@ void launch_adam(const MapParams& p, const MapParams& m, const MapParams& v, con
   a.c2 = (float)(1.0 / (1.0 - std::pow(beta2, (double)step)));
   const int threads = 256;
   adam_kernel<<<(unsigned)((g1 - g0 + threads - 1) / threads), threads, 0, s>>>(p, m, v, g, g0, g1, lr, a);
+  const int ks = 3 * p.K;
+  const int64_t e0 = g0 * ks, e1 = g1 * ks;
+  const int64_t nq = (e1 + 3) / 4 - e0 / 4;
+  adam_sh_kernel<<<(unsigned)((nq + threads - 1) / threads), threads, 0, s>>>(p.sh, m.sh, v.sh, g.sh, e0, e1, ks,
+                                                                           lr.sh_dc, lr.sh_rest, a);
 }
 
 void launch_unpack_map(const MapParams& p, float* pos, float* rot, float* log_s, float* opac, float* sh, float* feat_dn,

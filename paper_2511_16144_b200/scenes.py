@@ -188,3 +188,21 @@ def l1_cotangents(rgb, depth, feat, targets):
     g_depth = np.sign(depth - targets["depth"]) / depth.size
     g_feat = np.sign(feat - targets["feat"]) / max(feat.size, 1)
     return g_rgb, g_depth, g_feat
+
+
+def make_decoder(D: int, hidden: int, d: int, seed: int):
+    """Seeded stand-in for a pretrained codec decoder (no checkpoint ships with the reference):
+    (w1 [hidden, d], b1 [hidden], w2 [D, hidden], b2 [D]) float32, weights with the reference's
+    Xavier-uniform scale (proj/src/codec.cpp:16-23), small random biases (a pretrained decoder has
+    non-zero biases)."""
+    r = np.random.default_rng(seed)
+
+    def xavier(rows, cols):
+        a = np.sqrt(6.0 / (rows + cols))
+        return r.uniform(-a, a, size=(rows, cols))
+
+    w1 = xavier(hidden, d)
+    w2 = xavier(D, hidden)
+    b1 = r.normal(0.0, 0.05, size=hidden)
+    b2 = r.normal(0.0, 0.05, size=D)
+    return tuple(x.astype(np.float32) for x in (w1, b1, w2, b2))

@@ -86,7 +86,7 @@ def test_mapping_loop_reduces_loss():
     target["sh"] = np.clip(target["sh"] + r.normal(0, 0.15, target["sh"].shape), 0, 1).astype(np.float32)
     target["opac"] = (target["opac"] + r.normal(0, 0.5, target["opac"].shape)).astype(np.float32)
     kf_out = R.render(_dev(target), cam)
-    dec = OL.make_decoder(32, 64, 16, 1)
+    dec = scenes.make_decoder(32, 64, 16, 1)
     kf = {"rgb": kf_out.rgb.clone(), "depth": kf_out.depth.clone(),
           "feat_gt": torch.from_numpy(OL.decode(kf_out.feat.cpu().numpy(), *dec).astype(np.float32)).cuda()}
     dm = R.DeviceMap(_dev(scene))

@@ -37,7 +37,7 @@ def _setup(name="c0", n=None, seed=3, invalid_frac=0.2):
     kf_depth[r.uniform(size=(H, W)) < invalid_frac] = 0.0
     kf = {"rgb": r.uniform(0, 1, (H, W, 3)).astype(np.float32), "depth": kf_depth,
           "feat_gt": r.normal(0, 0.5, (H, W, D_TEACHER)).astype(np.float32)}
-    dec = OL.make_decoder(D_TEACHER, HIDDEN, out.d, seed)
+    dec = scenes.make_decoder(D_TEACHER, HIDDEN, out.d, seed)
     return out, kf, dec
 
 

@@ -6,6 +6,7 @@ import numpy as np
 import pytest
 
 from oracle import loss as L
+from paper_2511_16144_b200 import scenes
 
 
 def _rng(seed=0):
@@ -50,7 +51,7 @@ def _frame(seed, H=20, W=24, d=4, D=6, hidden=8):
     kf_depth = r.uniform(1, 3, (H, W))
     kf_depth[r.uniform(size=(H, W)) < 0.2] = 0.0  # invalid measurements
     kf_feat = r.normal(0, 1, (H, W, D))
-    dec = tuple(np.asarray(x, np.float64) for x in L.make_decoder(D, hidden, d, seed))
+    dec = tuple(np.asarray(x, np.float64) for x in scenes.make_decoder(D, hidden, d, seed))
     return rgb, depth, feat, acc, kf_rgb, kf_depth, kf_feat, dec
 
 
@@ -103,7 +104,7 @@ def test_total_decomposition_and_zero_feature_weight():
 
 def test_decoder_zero_in_zero_out_and_pixel_independence():
     """zero input through a zero-bias decoder -> zero; 1x1 image = single vector."""
-    w1, b1, w2, b2 = (np.asarray(x, np.float64) for x in L.make_decoder(6, 8, 4, 5))
+    w1, b1, w2, b2 = (np.asarray(x, np.float64) for x in scenes.make_decoder(6, 8, 4, 5))
     assert not L.decode(np.zeros((3, 3, 4)), w1, 0 * b1, w2, 0 * b2).any()
     z = _rng(5).normal(size=(5, 7, 4))
     full = L.decode(z, w1, b1, w2, b2)
