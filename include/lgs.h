@@ -54,7 +54,8 @@ typedef enum {
   LGS_EINVAL = 1, /* bad argument / shape mismatch (reference: std::invalid_argument) */
   LGS_ECUDA = 2,  /* CUDA runtime error; see lgs_last_error() */
   LGS_ENOMEM = 3, /* device or host allocation failed */
-  LGS_ENODEV = 4  /* no usable sm_100 device */
+  LGS_ENODEV = 4, /* no usable sm_100 device */
+  LGS_EIO = 5     /* map file error (reference: lego::IoError, errors.hpp:21) */
 } lgs_status;
 
 enum { LGS_MEM_HOST = 0, LGS_MEM_DEVICE = 1 };
@@ -287,6 +288,12 @@ LGS_API lgs_status lgs_mapping_loss(lgs_ctx* ctx, lgs_saved* tape, const lgs_ima
                                     lgs_loss_breakdown* out);
 /* Debug/parity: copy the tape's cotangents to host HWC buffers (any may be NULL).  Synchronizes. */
 LGS_API lgs_status lgs_debug_cotangents(lgs_ctx* ctx, const lgs_saved* tape, float* rgb, float* depth, float* feat);
+/* Insertion coverage mask: mask[p] = 1 iff the rendered acc <
+ * 0.5 or (the measured depth is valid -- finite, > 0 -- and |rendered depth - measured| >
+ * max(0.05 m, 0.05 measured)).  Reads acc / depth from the tape; mask is uint8 [H][W] (host or
+ * device); count (may be NULL) receives the number of selected pixels (synchronizes). */
+LGS_API lgs_status lgs_coverage_mask(lgs_ctx* ctx, const lgs_saved* tape, const float* measured_depth,
+                                     int32_t memory, uint8_t* mask, int32_t mask_memory, int64_t* count);
 /* Back-propagates the cotangents stored in the tape (fused L1 or lgs_mapping_loss) to the map. */
 LGS_API lgs_status lgs_render_backward_loss(lgs_ctx* ctx, const lgs_saved* tape, lgs_map_grads* grads,
                                             float* pose_grad);
@@ -309,6 +316,23 @@ LGS_API lgs_status lgs_adam_step(lgs_ctx* ctx, lgs_adam* adam, lgs_map* map, con
 /* Copy the resident map back out in the reference layouts (`dst` shape must match; host or
  * device memory; NULL members skipped). */
 LGS_API lgs_status lgs_map_download(lgs_ctx* ctx, const lgs_map* map, lgs_gaussians* dst);
+
+/* ---- LEGOMAP1 map files (proj/src/gaussian_map.cpp:196-259) ------------
+ * Format: "LEGOMAP1", u32 feature dim (1..4096), u64 count, then per Gaussian f32 position[3],
+ * rotation w,x,y,z, log_scale[3], opacity logit, colour[3], feature[d], u64 anchor keyframe id.
+ * Colour is SH degree 0 (the format has no higher bands).  Errors are LGS_EIO with the
+ * reference's messages ("bad map file magic", "truncated reading ...", "map feature dimension
+ * mismatch ...").  On read, a rotation whose norm is off unit by more than 1e-6 is renormalized
+ * (GaussianMap::insert, gaussian_map.cpp:21-23); unit ones stay bit-exact. */
+LGS_API lgs_status lgs_map_file_info(const char* path, int32_t* feature_dim, int64_t* count);
+/* Reads into caller-owned HOST buffers in the reference layouts (dst->n, feature_dim from
+ * lgs_map_file_info; sh_degree 0; memory LGS_MEM_HOST).  expected_dim <= 0 accepts any. */
+LGS_API lgs_status lgs_map_file_read(const char* path, int32_t expected_dim, lgs_gaussians* dst, uint64_t* anchors);
+/* Writes a host or device map in the reference layouts (sh_degree 0); anchors may be NULL (0). */
+LGS_API lgs_status lgs_map_file_write(const char* path, const lgs_gaussians* src, const uint64_t* anchors);
+/* File <-> resident device map. */
+LGS_API lgs_status lgs_map_load(lgs_ctx* ctx, const char* path, int32_t expected_dim, lgs_map** out);
+LGS_API lgs_status lgs_map_save(lgs_ctx* ctx, const lgs_map* map, const char* path, const uint64_t* anchors);
 
 /* ---- multi-view mapping batches --------------------------------------------
  * New (the reference is single-threaded CPU code with no multi-view path).  Views are sharded

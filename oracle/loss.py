@@ -153,3 +153,16 @@ def compute_losses(rgb, depth, feat, acc, kf_rgb, kf_depth, kf_feat, dec, w_dept
     br = dict(l_rgb=float(l_rgb), l_depth=l_depth, l_feat=l_feat, l_total=float(l_total), ssim=float(s),
               depth_pixels=cnt)
     return br, g_rgb, g_depth, g_feat
+
+
+def coverage_mask(acc, depth, measured):
+    """SPEC.md:225 insertion coverage: acc < 0.5 OR (measured valid and |depth - measured| >
+    max(0.05 m, 0.05 measured)), evaluated in float32 like the kernel (so masks compare exactly)."""
+    f = np.float32
+    acc = np.asarray(acc, f)
+    depth = np.asarray(depth, f)
+    m = np.asarray(measured, f)
+    valid = np.isfinite(m) & (m > f(0))
+    with np.errstate(invalid="ignore"):
+        err = np.abs(depth - m) > np.maximum(f(0.05), f(0.05) * m)
+    return ((acc < f(0.5)) | (valid & err)).astype(np.uint8)

@@ -11,7 +11,7 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "liblgs.so")
 
-LGS_OK, LGS_EINVAL, LGS_ECUDA, LGS_ENOMEM, LGS_ENODEV = range(5)
+LGS_OK, LGS_EINVAL, LGS_ECUDA, LGS_ENOMEM, LGS_ENODEV, LGS_EIO = range(6)
 LGS_MEM_HOST, LGS_MEM_DEVICE = 0, 1
 
 _fp = C.POINTER(C.c_float)
@@ -123,12 +123,19 @@ SIGNATURES = [
                                    C.POINTER(LgsDecoder), C.POINTER(LgsLossWeights), C.POINTER(LgsLossBreakdown)]),
     ("lgs_render_backward_loss", C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(LgsMapGrads), _fp]),
     ("lgs_debug_cotangents", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("lgs_coverage_mask", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_int32,
+                                    C.POINTER(C.c_int64)]),
     ("lgs_adam_config_default", LgsAdamConfig, []),
     ("lgs_adam_create", C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(LgsAdamConfig), C.POINTER(C.c_void_p)]),
     ("lgs_adam_destroy", C.c_int, [C.c_void_p]),
     ("lgs_adam_steps", C.c_int64, [C.c_void_p]),
     ("lgs_adam_step", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(LgsMapGrads)]),
     ("lgs_map_download", C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(LgsGaussians)]),
+    ("lgs_map_file_info", C.c_int, [C.c_char_p, C.POINTER(C.c_int32), C.POINTER(C.c_int64)]),
+    ("lgs_map_file_read", C.c_int, [C.c_char_p, C.c_int32, C.POINTER(LgsGaussians), C.c_void_p]),
+    ("lgs_map_file_write", C.c_int, [C.c_char_p, C.POINTER(LgsGaussians), C.c_void_p]),
+    ("lgs_map_load", C.c_int, [C.c_void_p, C.c_char_p, C.c_int32, C.POINTER(C.c_void_p)]),
+    ("lgs_map_save", C.c_int, [C.c_void_p, C.c_void_p, C.c_char_p, C.c_void_p]),
     ("lgs_comm_unique_id", C.c_int, [C.POINTER(LgsCommId)]),
     ("lgs_comm_init", C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.POINTER(LgsCommId)]),
     ("lgs_comm_destroy", C.c_int, [C.c_void_p]),
@@ -149,6 +156,10 @@ class LgsError(RuntimeError):
 
 class LgsInvalidArgument(LgsError, ValueError):
     """LGS_EINVAL -- the reference's std::invalid_argument (renderer.cpp:176-178)."""
+
+
+class LgsIoError(LgsError, OSError):
+    """LGS_EIO -- the reference's lego::IoError (errors.hpp:21) for map files."""
 
 
 def load(path: str | None = None):
@@ -173,4 +184,6 @@ def check(status):
         msg = load().lgs_last_error().decode(errors="replace")
         if status == LGS_EINVAL:
             raise LgsInvalidArgument(status, msg)
+        if status == LGS_EIO:
+            raise LgsIoError(status, msg)
         raise LgsError(status, msg)

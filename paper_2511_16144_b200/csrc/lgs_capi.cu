@@ -13,6 +13,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <fstream>
 #include <string>
 #include <vector>
 
@@ -988,6 +989,40 @@ LGS_API lgs_status lgs_debug_cotangents(lgs_ctx* ctx, const lgs_saved* t, float*
   return LGS_OK;
 }
 
+LGS_API lgs_status lgs_coverage_mask(lgs_ctx* ctx, const lgs_saved* t, const float* measured_depth, int32_t memory,
+                                     uint8_t* mask, int32_t mask_memory, int64_t* count) {
+  if (!ctx || !t || !measured_depth || !mask) return fail(LGS_EINVAL, "ctx/tape/depth/mask is NULL");
+  LGS_CUDA(cudaSetDevice(ctx->device));
+  cudaStream_t s = ctx->stream;
+  const size_t npix = (size_t)t->cam.H * t->cam.W;
+  const float* md = measured_depth;
+  float* stage = nullptr;
+  if (memory == LGS_MEM_HOST) {
+    LGS_TRY(dalloc(ctx, &stage, npix));
+    LGS_CUDA(cudaMemcpyAsync(stage, measured_depth, sizeof(float) * npix, cudaMemcpyHostToDevice, s));
+    md = stage;
+  }
+  uint8_t* dmask = mask;
+  if (mask_memory == LGS_MEM_HOST) LGS_TRY(dalloc(ctx, &dmask, npix));
+  unsigned long long* dcount = nullptr;
+  LGS_TRY(dalloc(ctx, &dcount, 1));
+  {
+    PhaseScope ph(ctx, PH_COVERAGE);
+    launch_coverage(t->ps.acc, t->ps.depth, md, (int64_t)npix, dmask, dcount, s);
+  }
+  ctx->launches += npix ? 1 : 0;
+  unsigned long long hcount = 0;
+  if (mask_memory == LGS_MEM_HOST) LGS_CUDA(cudaMemcpyAsync(mask, dmask, npix, cudaMemcpyDeviceToHost, s));
+  if (count) LGS_CUDA(cudaMemcpyAsync(&hcount, dcount, sizeof hcount, cudaMemcpyDeviceToHost, s));
+  if (mask_memory == LGS_MEM_HOST) dfree(ctx, dmask);
+  dfree(ctx, stage);
+  dfree(ctx, dcount);
+  if (count || mask_memory == LGS_MEM_HOST || memory == LGS_MEM_HOST) LGS_CUDA(cudaStreamSynchronize(s));
+  if (count) *count = (int64_t)hcount;
+  LGS_CUDA(cudaGetLastError());
+  return LGS_OK;
+}
+
 LGS_API lgs_status lgs_saved_l1_loss(lgs_ctx* ctx, const lgs_saved* tape, double* loss) {
   if (!ctx || !tape || !loss) return fail(LGS_EINVAL, "NULL argument");
   if (!tape->loss) return fail(LGS_EINVAL, "tape has no fused L1 loss");
@@ -1397,6 +1432,184 @@ LGS_API lgs_status lgs_map_download(lgs_ctx* ctx, const lgs_map* map, lgs_gaussi
   }
   LGS_CUDA(cudaGetLastError());
   return LGS_OK;
+}
+
+}  // extern "C"
+
+// -------------------------------------------------------------------------------------------
+// LEGOMAP1 files (gaussian_map.cpp:196-259)
+// -------------------------------------------------------------------------------------------
+namespace {
+
+constexpr char kMapMagic[8] = {'L', 'E', 'G', 'O', 'M', 'A', 'P', '1'};
+constexpr size_t kMapHeader = 8 + 4 + 8;
+
+struct MapFileHeader {
+  uint32_t dim = 0;
+  uint64_t count = 0;
+};
+
+lgs_status read_header(std::ifstream& is, const char* path, MapFileHeader* h) {
+  char magic[8];
+  is.read(magic, sizeof magic);
+  if (!is || std::memcmp(magic, kMapMagic, sizeof magic) != 0) return fail(LGS_EIO, "bad map file magic: %s", path);
+  is.read(reinterpret_cast<char*>(&h->dim), sizeof h->dim);
+  if (!is) return fail(LGS_EIO, "map file truncated reading feature dim");
+  if (h->dim == 0 || h->dim > 4096) return fail(LGS_EIO, "map file declares unreasonable feature dim");
+  is.read(reinterpret_cast<char*>(&h->count), sizeof h->count);
+  if (!is) return fail(LGS_EIO, "map file truncated reading count");
+  return LGS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+LGS_API lgs_status lgs_map_file_info(const char* path, int32_t* feature_dim, int64_t* count) {
+  if (!path) return fail(LGS_EINVAL, "path is NULL");
+  std::ifstream is(path, std::ios::binary);
+  if (!is) return fail(LGS_EIO, "cannot open map file: %s", path);
+  MapFileHeader h;
+  LGS_TRY(read_header(is, path, &h));
+  if (feature_dim) *feature_dim = (int32_t)h.dim;
+  if (count) *count = (int64_t)h.count;
+  return LGS_OK;
+}
+
+LGS_API lgs_status lgs_map_file_read(const char* path, int32_t expected_dim, lgs_gaussians* dst, uint64_t* anchors) {
+  if (!path || !dst) return fail(LGS_EINVAL, "path/dst is NULL");
+  if (dst->memory != LGS_MEM_HOST) return fail(LGS_EINVAL, "lgs_map_file_read fills host buffers");
+  std::ifstream is(path, std::ios::binary);
+  if (!is) return fail(LGS_EIO, "cannot open map file: %s", path);
+  MapFileHeader h;
+  LGS_TRY(read_header(is, path, &h));
+  if (expected_dim > 0 && (int32_t)h.dim != expected_dim)
+    return fail(LGS_EIO, "map feature dimension mismatch: file has %u, expected %d", h.dim, expected_dim);
+  if (dst->n != (int64_t)h.count || dst->feature_dim != (int32_t)h.dim || dst->sh_degree != 0)
+    return fail(LGS_EINVAL, "destination must hold %llu Gaussians of dim %u, sh_degree 0",
+                (unsigned long long)h.count, h.dim);
+  const uint32_t d = h.dim;
+  const size_t rec = sizeof(float) * (3 + 4 + 3 + 1 + 3 + d) + sizeof(uint64_t);
+  std::vector<char> buf(rec);
+  const char* what[] = {"position", "rotation", "scale", "opacity", "color", "feature", "anchor"};
+  const size_t off[] = {0, 12, 28, 40, 44, 56, 56 + 4 * (size_t)d};
+  float* pos = (float*)dst->positions;
+  float* rot = (float*)dst->rotations;
+  float* ls = (float*)dst->log_scales;
+  float* op = (float*)dst->opacity_logits;
+  float* col = (float*)dst->sh;
+  float* ft = (float*)dst->features;
+  for (uint64_t i = 0; i < h.count; ++i) {
+    is.read(buf.data(), (std::streamsize)rec);
+    if (!is) {  // name the first field that ran out, like read_pod (gaussian_map.cpp:187-192)
+      const size_t got = (size_t)is.gcount();
+      int f = 0;
+      while (f < 6 && got >= off[f + 1]) ++f;
+      return fail(LGS_EIO, "map file truncated reading %s", what[f]);
+    }
+    float v[14];
+    std::memcpy(v, buf.data(), sizeof v);
+    for (int a = 0; a < 3; ++a) pos[i * 3 + a] = v[a];
+    // file order w,x,y,z -> Eigen storage x,y,z,w; renormalize only when off-unit (gaussian_map.cpp:21-23)
+    double qw = v[3], qx = v[4], qy = v[5], qz = v[6];
+    const double nrm = std::sqrt(qw * qw + qx * qx + qy * qy + qz * qz);
+    if (std::abs(nrm - 1.0) > 1e-6 && nrm > 0.0) {
+      qw /= nrm; qx /= nrm; qy /= nrm; qz /= nrm;
+    }
+    rot[i * 4 + 0] = (float)qx; rot[i * 4 + 1] = (float)qy; rot[i * 4 + 2] = (float)qz; rot[i * 4 + 3] = (float)qw;
+    for (int a = 0; a < 3; ++a) ls[i * 3 + a] = v[7 + a];
+    op[i] = v[10];
+    for (int a = 0; a < 3; ++a) col[i * 3 + a] = v[11 + a];
+    for (uint32_t c = 0; c < d; ++c) {
+      float f;
+      std::memcpy(&f, buf.data() + 56 + 4 * (size_t)c, 4);
+      ft[(size_t)c * h.count + i] = f;  // features [d][N]
+    }
+    if (anchors) std::memcpy(&anchors[i], buf.data() + off[6], sizeof(uint64_t));
+  }
+  return LGS_OK;
+}
+
+LGS_API lgs_status lgs_map_file_write(const char* path, const lgs_gaussians* src, const uint64_t* anchors) {
+  if (!path || !src) return fail(LGS_EINVAL, "path/src is NULL");
+  if (src->n < 0 || src->feature_dim <= 0 || src->feature_dim > 4096)
+    return fail(LGS_EINVAL, "LEGOMAP1 needs 1 <= feature_dim <= 4096");
+  if (src->sh_degree != 0) return fail(LGS_EINVAL, "LEGOMAP1 stores SH degree 0 colour only");
+  const size_t n = (size_t)src->n, d = (size_t)src->feature_dim;
+  if (n > 0 && (!src->positions || !src->rotations || !src->log_scales || !src->opacity_logits || !src->sh ||
+                !src->features))
+    return fail(LGS_EINVAL, "a map attribute pointer is NULL");
+  // device sources are copied out first
+  std::vector<float> hp, hr, hl, ho, hc, hf;
+  const float *pos = (const float*)src->positions, *rot = (const float*)src->rotations,
+              *ls = (const float*)src->log_scales, *op = (const float*)src->opacity_logits,
+              *col = (const float*)src->sh, *ft = (const float*)src->features;
+  if (src->memory == LGS_MEM_DEVICE && n > 0) {
+    auto pull = [&](std::vector<float>& v, const float*& p, size_t count) -> lgs_status {
+      v.resize(count);
+      LGS_CUDA(cudaMemcpy(v.data(), p, sizeof(float) * count, cudaMemcpyDeviceToHost));
+      p = v.data();
+      return LGS_OK;
+    };
+    LGS_TRY(pull(hp, pos, n * 3)); LGS_TRY(pull(hr, rot, n * 4)); LGS_TRY(pull(hl, ls, n * 3));
+    LGS_TRY(pull(ho, op, n)); LGS_TRY(pull(hc, col, n * 3)); LGS_TRY(pull(hf, ft, n * d));
+  }
+  std::ofstream os(path, std::ios::binary);
+  if (!os) return fail(LGS_EIO, "cannot open map file for writing: %s", path);
+  os.write(kMapMagic, sizeof kMapMagic);
+  const uint32_t dim = (uint32_t)d;
+  const uint64_t count = n;
+  os.write(reinterpret_cast<const char*>(&dim), sizeof dim);
+  os.write(reinterpret_cast<const char*>(&count), sizeof count);
+  std::vector<char> buf(sizeof(float) * (14 + d) + sizeof(uint64_t));
+  for (size_t i = 0; i < n; ++i) {
+    float v[14];
+    for (int a = 0; a < 3; ++a) v[a] = pos[i * 3 + a];
+    v[3] = rot[i * 4 + 3]; v[4] = rot[i * 4 + 0]; v[5] = rot[i * 4 + 1]; v[6] = rot[i * 4 + 2];  // w,x,y,z
+    for (int a = 0; a < 3; ++a) v[7 + a] = ls[i * 3 + a];
+    v[10] = op[i];
+    for (int a = 0; a < 3; ++a) v[11 + a] = col[i * 3 + a];
+    std::memcpy(buf.data(), v, sizeof v);
+    for (size_t c = 0; c < d; ++c) std::memcpy(buf.data() + 56 + 4 * c, &ft[c * n + i], 4);
+    const uint64_t an = anchors ? anchors[i] : 0;
+    std::memcpy(buf.data() + 56 + 4 * d, &an, sizeof an);
+    os.write(buf.data(), (std::streamsize)buf.size());
+  }
+  if (!os) return fail(LGS_EIO, "failed writing map file: %s", path);
+  return LGS_OK;
+}
+
+LGS_API lgs_status lgs_map_load(lgs_ctx* ctx, const char* path, int32_t expected_dim, lgs_map** out) {
+  if (!ctx || !out) return fail(LGS_EINVAL, "ctx/out is NULL");
+  *out = nullptr;
+  int32_t dim = 0;
+  int64_t count = 0;
+  LGS_TRY(lgs_map_file_info(path, &dim, &count));
+  if (expected_dim > 0 && dim != expected_dim)
+    return fail(LGS_EIO, "map feature dimension mismatch: file has %d, expected %d", dim, expected_dim);
+  if (dim > LGS_MAX_FEATURE_DIM)
+    return fail(LGS_EINVAL, "feature dim %d exceeds the rasterizer's %d", dim, LGS_MAX_FEATURE_DIM);
+  const size_t n = (size_t)count;
+  std::vector<float> pos(n * 3), rot(n * 4), ls(n * 3), op(n), col(n * 3), ft(n * dim);
+  lgs_gaussians g{};
+  g.n = count; g.feature_dim = dim; g.sh_degree = 0;
+  g.positions = pos.data(); g.rotations = rot.data(); g.log_scales = ls.data(); g.opacity_logits = op.data();
+  g.sh = col.data(); g.features = ft.data(); g.memory = LGS_MEM_HOST;
+  LGS_TRY(lgs_map_file_read(path, expected_dim, &g, nullptr));
+  return lgs_map_create(ctx, &g, out);  // host source: synchronizes before the vectors go away
+}
+
+LGS_API lgs_status lgs_map_save(lgs_ctx* ctx, const lgs_map* map, const char* path, const uint64_t* anchors) {
+  if (!ctx || !map) return fail(LGS_EINVAL, "ctx/map is NULL");
+  if (map->dm.deg != 0) return fail(LGS_EINVAL, "LEGOMAP1 stores SH degree 0 colour only");
+  const size_t n = (size_t)map->dm.n, d = (size_t)map->dm.d;
+  std::vector<float> pos(n * 3), rot(n * 4), ls(n * 3), op(n), col(n * 3), ft(n * d);
+  lgs_gaussians g{};
+  g.n = map->dm.n; g.feature_dim = map->dm.d; g.sh_degree = 0;
+  g.positions = pos.data(); g.rotations = rot.data(); g.log_scales = ls.data(); g.opacity_logits = op.data();
+  g.sh = col.data(); g.features = ft.data(); g.memory = LGS_MEM_HOST;
+  LGS_TRY(lgs_map_download(ctx, map, &g));
+  return lgs_map_file_write(path, &g, anchors);
 }
 
 }  // extern "C"

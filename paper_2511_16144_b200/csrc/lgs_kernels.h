@@ -135,6 +135,8 @@ struct LossArgs {
   int cot_stride = 0;
 };
 bool decoder_supported(int hidden, int dp, int D);
+void launch_coverage(const float* acc, const float* depth, const float* measured, int64_t npix, uint8_t* mask,
+                     unsigned long long* count, cudaStream_t s);
 int launch_mapping_loss(const LossArgs& a, cudaStream_t s);  // 0 ok, else a CUDA error
 
 // K10 Adam step / map unpack (optim.cu).  MapParams: writable view of packed map arrays (the map

@@ -344,7 +344,35 @@ int launch_decoder_dp(const LossArgs& a, cudaStream_t s) {
   return 0;
 }
 
+// Insertion coverage mask: pixel selected iff rendered acc < 0.5 OR the measured
+// depth is valid (finite, > 0) and |rendered depth - measured| > max(0.05 m, 0.05 measured).
+__global__ void __launch_bounds__(256) coverage_kernel(const float* __restrict__ acc, const float* __restrict__ depth,
+                                                       const float* __restrict__ measured, int64_t npix,
+                                                       uint8_t* __restrict__ mask, unsigned long long* __restrict__ count) {
+  unsigned c = 0;
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < npix; p += (int64_t)gridDim.x * blockDim.x) {
+    const float m = measured[p];
+    bool sel = acc[p] < 0.5f;
+    if (!sel && isfinite(m) && m > 0.f) sel = fabsf(depth[p] - m) > fmaxf(0.05f, 0.05f * m);
+    mask[p] = sel ? 1 : 0;
+    c += sel ? 1u : 0u;
+  }
+  for (int off = 16; off > 0; off >>= 1) c += __shfl_xor_sync(0xffffffffu, c, off);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, (unsigned long long)c);
+}
+
 }  // namespace
+
+void launch_coverage(const float* acc, const float* depth, const float* measured, int64_t npix, uint8_t* mask,
+                     unsigned long long* count, cudaStream_t s) {
+  cudaMemsetAsync(count, 0, sizeof(unsigned long long), s);
+  if (npix == 0) return;
+  int sms = 148, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t blocks = std::min<int64_t>((npix + 255) / 256, (int64_t)sms * 8);
+  coverage_kernel<<<(unsigned)blocks, 256, 0, s>>>(acc, depth, measured, npix, mask, count);
+}
 
 bool decoder_supported(int hidden, int dp, int D) {
   return hidden == 64 && (dp == 4 || dp == 8 || dp == 16 || dp == 32) && D >= 1 &&

@@ -455,3 +455,68 @@ class Adam:
                 self.h = None
         except (AttributeError, TypeError):  # interpreter shutdown
             pass
+
+
+def map_file_info(path: str):
+    """(feature_dim, count) of a LEGOMAP1 file (gaussian_map.cpp:220-237 header)."""
+    d, n = C.c_int32(), C.c_int64()
+    check(_lib.load().lgs_map_file_info(str(path).encode(), C.byref(d), C.byref(n)))
+    return d.value, n.value
+
+
+def map_file_read(path: str, expected_dim: int = 0):
+    """lego::deserialize_map (gaussian_map.cpp:220-259) -> (scene dict in the reference layouts,
+    anchors u64 [N]).  Raises LgsIoError (an OSError) like the reference's IoError."""
+    d, n = map_file_info(path)
+    scene = {"pos": np.zeros((n, 3), np.float32), "rot": np.zeros((n, 4), np.float32),
+             "log_s": np.zeros((n, 3), np.float32), "opac": np.zeros(n, np.float32),
+             "sh": np.zeros((n, 1, 3), np.float32), "feat": np.zeros((d, n), np.float32)}
+    anchors = np.zeros(n, np.uint64)
+    g = _lib.LgsGaussians(n, d, 0, *(scene[k].ctypes.data for k in ("pos", "rot", "log_s", "opac", "sh", "feat")),
+                          LGS_MEM_HOST)
+    check(_lib.load().lgs_map_file_read(str(path).encode(), int(expected_dim), C.byref(g), anchors.ctypes.data))
+    return scene, anchors
+
+
+def map_file_write(path: str, scene, anchors=None):
+    """lego::serialize_map (gaussian_map.cpp:196-218) from a scene dict (SH degree 0)."""
+    g, keep = _gaussians_struct(scene)
+    a = None if anchors is None else np.ascontiguousarray(anchors, np.uint64)
+    check(_lib.load().lgs_map_file_write(str(path).encode(), C.byref(g), a.ctypes.data if a is not None else None))
+    del keep
+
+
+def map_load(path: str, ctx: Context | None = None, expected_dim: int = 0) -> DeviceMap:
+    """LEGOMAP1 file -> resident device map (lgs_map_load)."""
+    ctx = ctx or default_context()
+    dm = DeviceMap.__new__(DeviceMap)
+    h = C.c_void_p()
+    check(_lib.load().lgs_map_load(ctx.h, str(path).encode(), int(expected_dim), C.byref(h)))
+    dm.ctx, dm.h, dm._arrs = ctx, h, None
+    dm.d, dm.n = map_file_info(path)
+    dm.sh_degree, dm.K = 0, 1
+    return dm
+
+
+def map_save(dmap: DeviceMap, path: str, anchors=None):
+    a = None if anchors is None else np.ascontiguousarray(anchors, np.uint64)
+    check(_lib.load().lgs_map_save(dmap.ctx.h, dmap.h, str(path).encode(), a.ctypes.data if a is not None else None))
+
+
+def coverage_mask(out: RenderOutput, measured_depth):
+    """SPEC.md:225 insertion coverage mask on the GPU: (uint8 mask [H, W], selected count).  The
+    mask is a CUDA tensor for device depth input, numpy otherwise."""
+    H, W = out.camera.height, out.camera.width
+    md = _f32(measured_depth)
+    if tuple(md.shape) != (H, W):
+        raise ValueError("coverage_mask: measured depth must be [H, W]")
+    dev = _is_torch(md) and md.is_cuda
+    mask = torch.empty((H, W), dtype=torch.uint8, device=md.device) if dev else np.empty((H, W), np.uint8)
+    cnt = C.c_int64()
+    check(_lib.load().lgs_coverage_mask(out.ctx.h, out.tape, _ptr(md), _mem(md), _ptr_any(mask), _mem(mask),
+                                        C.byref(cnt)))
+    return mask, cnt.value
+
+
+def _ptr_any(x):
+    return x.data_ptr() if _is_torch(x) else x.ctypes.data

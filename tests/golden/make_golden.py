@@ -10,6 +10,8 @@ CUDA path (GPU) still reproduce them.
   sh3_pose.npz  400 Gaussians, SH degree 3, d = 16, 64x48, rotated camera, L1 cotangents:
                 images, gradients and the pose gradient (EXT features, parity unpinned by the
                 reference).
+  map_small.legomap  a 3-Gaussian LEGOMAP1 file (d = 4) written field by field with struct per
+                proj/src/gaussian_map.cpp:196-218 (tests/test_map_io.py reads it through the C ABI).
 """
 import os
 import sys
@@ -49,7 +51,21 @@ def sh3_pose():
                 acc=out.acc, **{f"g_{k}": v for k, v in g.items()})
 
 
+def map_small(path):
+    import struct
+    rows = [  # position, rotation (w, x, y, z), log-scale, opacity logit, colour, feature, anchor
+        ((0.0, 0.0, 2.0), (1.0, 0.0, 0.0, 0.0), (-3.0, -3.0, -3.0), 0.0, (0.2, 0.4, 0.6), (1.0, 0.0, 0.0, 0.0), 0),
+        ((1.5, -2.0, 3.25), (0.5, 0.5, 0.5, 0.5), (-2.5, -3.5, -4.0), 1.5, (1.0, 0.0, 0.5), (0.0, 1.0, 0.0, 0.0), 5),
+        ((-1.0, 0.5, 4.0), (0.0, 0.0, 1.0, 0.0), (-1.0, -2.0, -3.0), -2.0, (0.1, 0.1, 0.1), (0.5, -0.5, 0.25, 1.0), 7),
+    ]
+    with open(path, "wb") as f:
+        f.write(b"LEGOMAP1" + struct.pack("<IQ", 4, len(rows)))
+        for p, q, s, o, c, ft, a in rows:
+            f.write(struct.pack("<3f4f3ff3f4fQ", *p, *q, *s, o, *c, *ft, a))
+
+
 if __name__ == "__main__":
+    map_small(os.path.join(HERE, "map_small.legomap"))
     np.savez_compressed(os.path.join(HERE, "grad101.npz"), **grad101())
     np.savez_compressed(os.path.join(HERE, "sh3_pose.npz"), **sh3_pose())
     print("wrote", sorted(f for f in os.listdir(HERE) if f.endswith(".npz")))

@@ -133,3 +133,11 @@ def test_cotangents_match_finite_differences():
             args_m = {"rgb": (am, depth, feat), "depth": (rgb, am, feat), "feat": (rgb, depth, am)}[name]
             fd = (total(*args_p) - total(*args_m)) / (2 * h)
             assert abs(fd - g[idx]) <= 1e-3 * (abs(fd) + 1e-6), (name, idx, fd, g[idx])
+
+
+def test_coverage_mask_rule():
+    """selected iff acc < 0.5 OR |depth - measured| > max(0.05 m, 0.05 depth)."""
+    acc = np.array([0.4, 0.9, 0.9, 0.9, 0.9, 0.9])
+    depth = np.array([1.0, 1.0, 1.0, 4.0, 4.0, 1.0])
+    meas = np.array([1.0, 1.04, 1.06, 4.19, 4.25, 0.0])
+    assert list(L.coverage_mask(acc, depth, meas)) == [1, 0, 1, 0, 1, 0]
