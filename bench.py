@@ -243,16 +243,34 @@ def run_ours(args):
         from paper_2511_16144_b200.multiview import NativeComm
         comm = NativeComm(ctx)  # liblgs.so's own NCCL communicator (torch.distributed only bootstraps it)
 
-    def step():
-        out = R.render(dmap, cam, targets=dtg, ctx=ctx)
-        g = R.render_backward_l1(out, pose=True, into=grads)  # pose grad read back to the host
+    pose_host = torch.zeros(6, dtype=torch.float32, pin_memory=True)
+    H, W = cam["height"], cam["width"]
+    with torch.cuda.stream(stream):
+        imgs = {"rgb": torch.empty(H, W, 3, device=f"cuda:{local}"), "depth": torch.empty(H, W, device=f"cuda:{local}"),
+                "feat": torch.empty(H, W, d, device=f"cuda:{local}"), "acc": torch.empty(H, W, device=f"cuda:{local}")}
+        # the step as ONE CUDA graph: render (fused L1, images written) -> backward (all map grads,
+        # pose grad copied to pinned host memory in stream order); lgs_plan, include/lgs.h
+        plan = R.Plan(dmap, cam, dtg, grads, images=imgs, pose_out=pose_host)
+
+    def enqueue():
+        plan.run()
         if comm is not None:
             comm.all_reduce(grads["flat"])  # 500k x 75 fp32 sum over NVLink, on the library's stream
-        return out, g
+        return None
+
+    def step():
+        """Eager (uncaptured) step through the same API: used for the per-phase profile."""
+        out = R.render(dmap, cam, targets=dtg, ctx=ctx)
+        R.render_backward_loss_async(out, into=grads, pose_out=pose_host)
+        if comm is not None:
+            comm.all_reduce(grads["flat"])
+        torch.cuda.current_stream().synchronize()
+        return out, grads
 
     with torch.cuda.stream(stream):
         for _ in range(max(args.warmup, 3)):
-            step()
+            enqueue()
+            plan.sync()
     torch.cuda.synchronize()
 
     # ---- timed region --------------------------------------------------------------------------
@@ -266,11 +284,15 @@ def run_ours(args):
     gc.collect()
     gc.disable()  # a collection inside a step stalls the host-driven pipeline
     with sampler(local) as clk, torch.cuda.stream(stream):
+        host_ms = []
         for k in range(args.steps):
             flush.fill_(float(k))
             evs[k][0].record(stream)
-            out, g = step()
-            evs[k][1].record(stream)
+            h0 = time.perf_counter()
+            out = enqueue()
+            evs[k][1].record(stream)  # on the stream before the host waits: host wake-up is outside
+            host_ms.append(1e3 * (time.perf_counter() - h0))
+            plan.sync()  # the step's pose gradient has reached the host (re-captures on overflow)
             if k % every == every - 1:
                 clk.sample()
         torch.cuda.synchronize()
@@ -376,6 +398,7 @@ def run_ours(args):
         "work": {"visible": V, "pairs": P, "evaluated": evaluated, "contributed": contributed,
                  "max_tile_list": st["max_tile_list"]},
         "per_step_ms": [round(x, 4) for x in per_step],
+        "host_enqueue_ms": [round(x, 3) for x in host_ms],
     }
 
     if not args.no_mapping:

@@ -66,6 +66,7 @@ typedef struct lgs_ctx lgs_ctx;
 typedef struct lgs_map lgs_map;
 typedef struct lgs_saved lgs_saved;
 typedef struct lgs_adam lgs_adam;
+typedef struct lgs_plan lgs_plan;
 
 /* renderer.hpp:15-22; defaults from lgs_render_config_default(). */
 typedef struct {
@@ -297,6 +298,10 @@ LGS_API lgs_status lgs_coverage_mask(lgs_ctx* ctx, const lgs_saved* tape, const 
 /* Back-propagates the cotangents stored in the tape (fused L1 or lgs_mapping_loss) to the map. */
 LGS_API lgs_status lgs_render_backward_loss(lgs_ctx* ctx, const lgs_saved* tape, lgs_map_grads* grads,
                                             float* pose_grad);
+/* Same, fully asynchronous: device gradients only; pose_grad (NULL, device or PINNED host memory)
+ * is written in stream order and valid after lgs_ctx_synchronize / an event on the stream. */
+LGS_API lgs_status lgs_render_backward_loss_async(lgs_ctx* ctx, const lgs_saved* tape, lgs_map_grads* grads,
+                                                  float* pose_grad);
 
 /* ---- Adam step on the resident map (SPEC.md:430 mapping_round) ---------
  * Per-attribute learning rates of SPEC.md:430; standard bias-corrected Adam (beta1 0.9, beta2
@@ -333,6 +338,24 @@ LGS_API lgs_status lgs_map_file_write(const char* path, const lgs_gaussians* src
 /* File <-> resident device map. */
 LGS_API lgs_status lgs_map_load(lgs_ctx* ctx, const char* path, int32_t expected_dim, lgs_map** out);
 LGS_API lgs_status lgs_map_save(lgs_ctx* ctx, const lgs_map* map, const char* path, const uint64_t* anchors);
+
+/* ---- captured steps (CUDA graphs) ---------------------------------------------------------------
+ * A plan is one forward (fused L1 against device targets) + backward (device gradients, pose
+ * gradient to pinned-host / device memory or NULL) on a resident map and a fixed camera,
+ * captured once into a CUDA graph and replayed with one launch (no host work inside the step).
+ * The tile-list capacity comes from an eager warm-up step; lgs_plan_sync waits for the replay and
+ * re-captures + re-runs it if the pair count outgrew the capacity.  Map contents, targets and
+ * gradient buffers may change between replays (same pointers); a new camera re-captures. */
+LGS_API lgs_status lgs_plan_create(lgs_ctx* ctx, lgs_map* map, const lgs_camera* cam, const lgs_render_config* cfg,
+                                   const lgs_l1_targets* targets, const lgs_images* images /* device or NULL */,
+                                   lgs_map_grads* grads, float* pose_grad, lgs_plan** out);
+LGS_API lgs_status lgs_plan_run(lgs_ctx* ctx, lgs_plan* plan);
+LGS_API lgs_status lgs_plan_sync(lgs_ctx* ctx, lgs_plan* plan, int64_t* pairs);
+LGS_API lgs_status lgs_plan_set_camera(lgs_ctx* ctx, lgs_plan* plan, const lgs_camera* cam);
+/* Device time of the last replay, from events recorded as the graph's first and last nodes. */
+LGS_API lgs_status lgs_plan_elapsed_ms(const lgs_plan* plan, float* ms);
+LGS_API int64_t lgs_plan_launches(const lgs_plan* plan);
+LGS_API lgs_status lgs_plan_destroy(lgs_plan* plan);
 
 /* ---- multi-view mapping batches --------------------------------------------
  * New (the reference is single-threaded CPU code with no multi-view path).  Views are sharded

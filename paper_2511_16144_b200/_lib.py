@@ -122,6 +122,7 @@ SIGNATURES = [
     ("lgs_mapping_loss", C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(LgsImages), C.POINTER(LgsKeyframe),
                                    C.POINTER(LgsDecoder), C.POINTER(LgsLossWeights), C.POINTER(LgsLossBreakdown)]),
     ("lgs_render_backward_loss", C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(LgsMapGrads), _fp]),
+    ("lgs_render_backward_loss_async", C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(LgsMapGrads), C.c_void_p]),
     ("lgs_debug_cotangents", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     ("lgs_coverage_mask", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_int32,
                                     C.POINTER(C.c_int64)]),
@@ -136,6 +137,15 @@ SIGNATURES = [
     ("lgs_map_file_write", C.c_int, [C.c_char_p, C.POINTER(LgsGaussians), C.c_void_p]),
     ("lgs_map_load", C.c_int, [C.c_void_p, C.c_char_p, C.c_int32, C.POINTER(C.c_void_p)]),
     ("lgs_map_save", C.c_int, [C.c_void_p, C.c_void_p, C.c_char_p, C.c_void_p]),
+    ("lgs_plan_create", C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(LgsCamera), C.POINTER(LgsRenderConfig),
+                                  C.POINTER(LgsL1Targets), C.POINTER(LgsImages), C.POINTER(LgsMapGrads), C.c_void_p,
+                                  C.POINTER(C.c_void_p)]),
+    ("lgs_plan_run", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("lgs_plan_sync", C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_int64)]),
+    ("lgs_plan_set_camera", C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(LgsCamera)]),
+    ("lgs_plan_elapsed_ms", C.c_int, [C.c_void_p, C.POINTER(C.c_float)]),
+    ("lgs_plan_launches", C.c_int64, [C.c_void_p]),
+    ("lgs_plan_destroy", C.c_int, [C.c_void_p]),
     ("lgs_comm_unique_id", C.c_int, [C.POINTER(LgsCommId)]),
     ("lgs_comm_init", C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.POINTER(LgsCommId)]),
     ("lgs_comm_destroy", C.c_int, [C.c_void_p]),

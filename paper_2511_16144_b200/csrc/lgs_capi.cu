@@ -83,6 +83,8 @@ struct lgs_ctx {
   uint32_t* host_u32 = nullptr;  // pinned scalar readback
   uint32_t* dev_u32 = nullptr;   // device scalars: [0] pair count, [1] binning overflow flag
   cudaEvent_t pairs_ready = nullptr;
+  cudaMemPool_t pool = nullptr;  // this context's stream-ordered arena (no cross-context reuse waits)
+  bool capturing = false;        // inside lgs_plan capture: no host waits, graph memory nodes
   int64_t pairs_cap = 0;  // tile-list capacity for the next render (0: size from the exact count)
   // multi-view gradient all-reduce (lgs_comm_*): one NCCL communicator per context / GPU
   ncclComm_t comm = nullptr;
@@ -112,7 +114,7 @@ struct PhaseScope {
     cudaEventCreate(&e);
     return e;
   }
-  PhaseScope(lgs_ctx* c, int phase) : ctx(c), on(c->profiling) {
+  PhaseScope(lgs_ctx* c, int phase) : ctx(c), on(c->profiling && !c->capturing) {
     if (!on) return;
     m.phase = phase;
     m.a = take();
@@ -181,6 +183,7 @@ void ctx_release(lgs_ctx* ctx) {
       if (const NcclApi* nc = nccl_api(nullptr)) nc->CommDestroy(ctx->comm);
     }
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    if (ctx->pool) cudaMemPoolDestroy(ctx->pool);
     if (ctx->host_u32) cudaFreeHost(ctx->host_u32);
     if (ctx->dev_u32) cudaFree(ctx->dev_u32);
     if (ctx->pairs_ready) cudaEventDestroy(ctx->pairs_ready);
@@ -197,7 +200,10 @@ template <typename T>
 lgs_status dalloc(lgs_ctx* ctx, T** p, size_t count) {
   *p = nullptr;
   if (count == 0) count = 1;
-  LGS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(p), sizeof(T) * count, ctx->stream));
+  if (ctx->capturing)  // captured into a graph memory node (graph-owned memory)
+    LGS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(p), sizeof(T) * count, ctx->stream));
+  else
+    LGS_CUDA(cudaMallocFromPoolAsync(reinterpret_cast<void**>(p), sizeof(T) * count, ctx->pool, ctx->stream));
   return LGS_OK;
 }
 
@@ -388,10 +394,22 @@ LGS_API lgs_status lgs_ctx_create(int32_t device, void* stream, lgs_ctx** out) {
     }
     ctx->own_stream = true;
   }
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+  // A private pool per context: blocks freed on this context's stream are reused only by it, so
+  // contexts rendering concurrently on different streams never acquire each other's frees (the
+  // shared default pool would insert cross-stream waits and serialize them).  Release threshold
+  // raised: steady-state iterations reuse blocks without new cudaMalloc calls.
+  {
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    if (cudaMemPoolCreate(&ctx->pool, &props) != cudaSuccess) {
+      if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+      delete ctx;
+      return fail(LGS_ENOMEM, "cudaMemPoolCreate failed");
+    }
     uint64_t thr = UINT64_MAX;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    cudaMemPoolSetAttribute(ctx->pool, cudaMemPoolAttrReleaseThreshold, &thr);
   }
   if (cudaMallocHost(&ctx->host_u32, 64) != cudaSuccess || cudaMalloc(&ctx->dev_u32, 64) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->pairs_ready, cudaEventDisableTiming) != cudaSuccess) {
@@ -554,7 +572,7 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
   ctx->launches += 2;
   if (n > 0) {
     CUDAB(cudaMemcpyAsync(ctx->host_u32, ctx->dev_u32, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-    CUDAB(cudaEventRecord(ctx->pairs_ready, s));
+    if (!ctx->capturing) CUDAB(cudaEventRecord(ctx->pairs_ready, s));
   }
 
   // depth sort + scan
@@ -670,7 +688,11 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
 
   int64_t P = 0;
   const bool speculate = fast && n > 0 && ctx->pairs_cap > 0;
-  if (speculate) {
+  if (ctx->capturing) {  // lgs_plan: P is checked after each replay (lgs_plan_sync)
+    if (!speculate) return bail(fail(LGS_EINVAL, "plan capture needs the fast binning and a known capacity"));
+    TRYB(bin_and_blend(ctx->pairs_cap, true));
+    P = ctx->pairs_cap;
+  } else if (speculate) {
     TRYB(bin_and_blend(ctx->pairs_cap, true));
     CUDAB(cudaEventSynchronize(ctx->pairs_ready));  // long done: the GPU is busy with the queued forward
     P = ctx->host_u32[0];
@@ -731,7 +753,8 @@ LGS_API lgs_status lgs_render(lgs_ctx* ctx, const lgs_gaussians* src, const lgs_
 // -------------------------------------------------------------------------------------------
 namespace {
 
-lgs_status run_backward(lgs_ctx* ctx, const lgs_saved* t, const BwdIn& in_dev, lgs_map_grads* grads, float* pose_grad) {
+lgs_status run_backward(lgs_ctx* ctx, const lgs_saved* t, const BwdIn& in_dev, lgs_map_grads* grads, float* pose_grad,
+                        bool async_pose = false) {
   cudaStream_t s = ctx->stream;
   const int64_t n = t->dm.n;
   const int d = t->dm.d, K = t->dm.K;
@@ -793,12 +816,19 @@ lgs_status run_backward(lgs_ctx* ctx, const lgs_saved* t, const BwdIn& in_dev, l
         LGS_CUDA(cudaMemcpyAsync(dst[k], src[k], sizeof(float) * szs[k], cudaMemcpyDeviceToHost, s));
   }
   double hpose[6];
-  if (pose_grad) LGS_CUDA(cudaMemcpyAsync(hpose, dpose, sizeof hpose, cudaMemcpyDeviceToHost, s));
+  if (pose_grad && async_pose) {
+    // stream-ordered: fp64 accumulator -> float, copied to pinned-host or device memory
+    launch_pose_to_float(dpose, reinterpret_cast<float*>(dpose), s);
+    LGS_CUDA(cudaMemcpyAsync(pose_grad, dpose, sizeof(float) * 6, cudaMemcpyDefault, s));
+    ctx->launches++;
+  } else if (pose_grad) {
+    LGS_CUDA(cudaMemcpyAsync(hpose, dpose, sizeof hpose, cudaMemcpyDeviceToHost, s));
+  }
   dfree(ctx, gacc);
   dfree(ctx, gstage);
   dfree(ctx, dpose);
-  if (host || pose_grad) LGS_CUDA(cudaStreamSynchronize(s));
-  if (pose_grad)
+  if (host || (pose_grad && !async_pose)) LGS_CUDA(cudaStreamSynchronize(s));
+  if (pose_grad && !async_pose)
     for (int a = 0; a < 6; ++a) pose_grad[a] = (float)hpose[a];
   return LGS_OK;
 }
@@ -865,6 +895,18 @@ LGS_API lgs_status lgs_render_backward_l1(lgs_ctx* ctx, const lgs_saved* tape, l
 LGS_API lgs_status lgs_render_backward_loss(lgs_ctx* ctx, const lgs_saved* tape, lgs_map_grads* grads,
                                             float* pose_grad) {
   return lgs_render_backward_l1(ctx, tape, grads, pose_grad);
+}
+
+LGS_API lgs_status lgs_render_backward_loss_async(lgs_ctx* ctx, const lgs_saved* tape, lgs_map_grads* grads,
+                                                  float* pose_grad) {
+  if (!ctx || !tape) return fail(LGS_EINVAL, "ctx/tape is NULL");
+  if (!tape->cot) return fail(LGS_EINVAL, "tape holds no loss cotangents");
+  if (grads && grads->memory != LGS_MEM_DEVICE) return fail(LGS_EINVAL, "async backward needs device gradients");
+  LGS_CUDA(cudaSetDevice(ctx->device));
+  BwdIn in{};
+  in.g_rgb = tape->cot;
+  in.cot_stride = 4 + tape->dm.dp;
+  return run_backward(ctx, tape, in, grads, pose_grad, true);
 }
 
 LGS_API lgs_loss_weights lgs_loss_weights_default(void) {
@@ -1610,6 +1652,177 @@ LGS_API lgs_status lgs_map_save(lgs_ctx* ctx, const lgs_map* map, const char* pa
   g.sh = col.data(); g.features = ft.data(); g.memory = LGS_MEM_HOST;
   LGS_TRY(lgs_map_download(ctx, map, &g));
   return lgs_map_file_write(path, &g, anchors);
+}
+
+}  // extern "C"
+
+// -------------------------------------------------------------------------------------------
+// lgs_plan: one fwd (fused L1) + bwd step captured into a CUDA graph and replayed
+// -------------------------------------------------------------------------------------------
+struct lgs_plan {
+  lgs_ctx* ctx = nullptr;
+  lgs_map* map = nullptr;
+  lgs_camera cam{};
+  lgs_render_config cfg{};
+  lgs_l1_targets targets{};
+  lgs_map_grads grads{};
+  lgs_images images{};
+  bool has_images = false;
+  float* pose = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  cudaStream_t cap_stream = nullptr;  // private capture stream (the context's may be the legacy one)
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  int64_t cap = 0;
+  int64_t launches_per_run = 0;
+};
+
+namespace {
+
+lgs_status plan_capture(lgs_plan* p) {
+  lgs_ctx* ctx = p->ctx;
+  if (p->exec) {
+    cudaGraphExecDestroy(p->exec);
+    p->exec = nullptr;
+  }
+  // capture on a private stream (the graph is launched on the context's stream)
+  cudaStream_t s = p->cap_stream;
+  const cudaStream_t saved = ctx->stream;
+  const int64_t l0 = ctx->launches.load();
+  LGS_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  ctx->stream = s;
+  ctx->capturing = true;
+  lgs_status st = LGS_OK;
+  lgs_saved* tape = nullptr;
+  if (cudaEventRecordWithFlags(p->ev0, s, cudaEventRecordExternal) != cudaSuccess)
+    st = fail(LGS_ECUDA, "event record in capture failed");
+  if (st == LGS_OK)
+    st = lgs_render_forward(ctx, p->map, &p->cam, &p->cfg, &p->targets, p->has_images ? &p->images : nullptr, &tape);
+  if (st == LGS_OK) {
+    BwdIn in{};
+    in.g_rgb = tape->cot;
+    in.cot_stride = 4 + tape->dm.dp;
+    st = run_backward(ctx, tape, in, &p->grads, p->pose, true);
+  }
+  if (tape) lgs_saved_destroy(tape);  // stream-ordered frees: captured as graph free nodes
+  if (st == LGS_OK && cudaEventRecordWithFlags(p->ev1, s, cudaEventRecordExternal) != cudaSuccess)
+    st = fail(LGS_ECUDA, "event record in capture failed");
+  ctx->capturing = false;
+  ctx->stream = saved;
+  cudaGraph_t graph = nullptr;
+  const cudaError_t ec = cudaStreamEndCapture(s, &graph);
+  if (st != LGS_OK) {
+    if (graph) cudaGraphDestroy(graph);
+    return st;
+  }
+  if (ec != cudaSuccess) return fail(LGS_ECUDA, "stream capture failed: %s", cudaGetErrorString(ec));
+  const cudaError_t ei = cudaGraphInstantiate(&p->exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (ei != cudaSuccess) return fail(LGS_ECUDA, "graph instantiate failed: %s", cudaGetErrorString(ei));
+  p->cap = ctx->pairs_cap;
+  p->launches_per_run = ctx->launches.load() - l0;
+  ctx->launches -= p->launches_per_run;  // counted per replay
+  return LGS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+LGS_API lgs_status lgs_plan_create(lgs_ctx* ctx, lgs_map* map, const lgs_camera* cam, const lgs_render_config* cfg,
+                                   const lgs_l1_targets* targets, const lgs_images* images, lgs_map_grads* grads,
+                                   float* pose_grad, lgs_plan** out) {
+  if (!ctx || !map || !cam || !targets || !grads || !out) return fail(LGS_EINVAL, "NULL argument");
+  *out = nullptr;
+  if (targets->memory != LGS_MEM_DEVICE || grads->memory != LGS_MEM_DEVICE ||
+      (images && images->memory != LGS_MEM_DEVICE))
+    return fail(LGS_EINVAL, "a plan reads device targets and writes device images / gradients");
+  if (grads->accumulate) return fail(LGS_EINVAL, "a plan overwrites its gradients (accumulate = 0)");
+  LGS_CUDA(cudaSetDevice(ctx->device));
+  lgs_plan* p = new lgs_plan();
+  p->ctx = ctx;
+  p->map = map;
+  p->cam = *cam;
+  p->cfg = cfg ? *cfg : lgs_render_config_default();
+  p->targets = *targets;
+  p->grads = *grads;
+  if (images) {
+    p->images = *images;
+    p->has_images = true;
+  }
+  p->pose = pose_grad;
+  ctx->refs++;
+  auto bail = [&](lgs_status st) {
+    if (p->exec) cudaGraphExecDestroy(p->exec);
+    if (p->ev0) cudaEventDestroy(p->ev0);
+    if (p->ev1) cudaEventDestroy(p->ev1);
+    if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
+    ctx_release(ctx);
+    delete p;
+    return st;
+  };
+  if (cudaEventCreate(&p->ev0) != cudaSuccess || cudaEventCreate(&p->ev1) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&p->cap_stream, cudaStreamNonBlocking) != cudaSuccess)
+    return bail(fail(LGS_ECUDA, "event / stream creation failed"));
+  // one eager step sizes the tile-list capacity (and runs every one-time kernel setup)
+  lgs_saved* tape = nullptr;
+  lgs_status st =
+      lgs_render_forward(ctx, map, &p->cam, &p->cfg, &p->targets, p->has_images ? &p->images : nullptr, &tape);
+  if (st == LGS_OK) st = lgs_render_backward_loss_async(ctx, tape, &p->grads, p->pose);
+  if (tape) lgs_saved_destroy(tape);
+  if (st != LGS_OK) return bail(st);
+  if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return bail(fail(LGS_ECUDA, "warm-up step failed"));
+  if ((st = plan_capture(p)) != LGS_OK) return bail(st);
+  *out = p;
+  return LGS_OK;
+}
+
+LGS_API lgs_status lgs_plan_run(lgs_ctx* ctx, lgs_plan* p) {
+  if (!ctx || !p || ctx != p->ctx) return fail(LGS_EINVAL, "plan / context mismatch");
+  LGS_CUDA(cudaGraphLaunch(p->exec, ctx->stream));
+  ctx->launches += p->launches_per_run;
+  return LGS_OK;
+}
+
+LGS_API lgs_status lgs_plan_sync(lgs_ctx* ctx, lgs_plan* p, int64_t* pairs) {
+  if (!ctx || !p || ctx != p->ctx) return fail(LGS_EINVAL, "plan / context mismatch");
+  LGS_CUDA(cudaStreamSynchronize(ctx->stream));
+  const int64_t P = ctx->host_u32[0];
+  if (P > p->cap) {  // the replay ran on empty tile lists: grow, re-capture, redo the step
+    ctx->pairs_cap = P + P / 4;
+    LGS_TRY(plan_capture(p));
+    LGS_TRY(lgs_plan_run(ctx, p));
+    LGS_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  if (pairs) *pairs = P;
+  return LGS_OK;
+}
+
+LGS_API lgs_status lgs_plan_set_camera(lgs_ctx* ctx, lgs_plan* p, const lgs_camera* cam) {
+  if (!ctx || !p || !cam || ctx != p->ctx) return fail(LGS_EINVAL, "bad argument");
+  p->cam = *cam;  // the camera is baked into the kernel parameters: re-capture
+  return plan_capture(p);
+}
+
+LGS_API lgs_status lgs_plan_elapsed_ms(const lgs_plan* p, float* ms) {
+  if (!p || !ms) return fail(LGS_EINVAL, "NULL argument");
+  LGS_CUDA(cudaEventElapsedTime(ms, p->ev0, p->ev1));
+  return LGS_OK;
+}
+
+LGS_API int64_t lgs_plan_launches(const lgs_plan* p) { return p ? p->launches_per_run : -1; }
+
+LGS_API lgs_status lgs_plan_destroy(lgs_plan* p) {
+  if (!p) return LGS_OK;
+  lgs_ctx* ctx = p->ctx;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  if (p->exec) cudaGraphExecDestroy(p->exec);
+  if (p->ev0) cudaEventDestroy(p->ev0);
+  if (p->ev1) cudaEventDestroy(p->ev1);
+  if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
+  delete p;
+  ctx_release(ctx);
+  return LGS_OK;
 }
 
 }  // extern "C"

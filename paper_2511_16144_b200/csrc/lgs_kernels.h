@@ -135,6 +135,7 @@ struct LossArgs {
   int cot_stride = 0;
 };
 bool decoder_supported(int hidden, int dp, int D);
+void launch_pose_to_float(double* pose, float* same_storage, cudaStream_t s);
 void launch_coverage(const float* acc, const float* depth, const float* measured, int64_t npix, uint8_t* mask,
                      unsigned long long* count, cudaStream_t s);
 int launch_mapping_loss(const LossArgs& a, cudaStream_t s);  // 0 ok, else a CUDA error

@@ -369,4 +369,18 @@ void launch_preprocess_bwd(const DevMap& m, const DevCam& c, const ViewBufs& v, 
   }
 }
 
+// fp64 pose accumulator [6] -> float [6] in place (the floats overwrite the first 24 bytes).
+__global__ void pose_to_float_kernel(double* __restrict__ pose) {
+  if (threadIdx.x == 0) {
+    float f[6];
+    for (int a = 0; a < 6; ++a) f[a] = (float)pose[a];
+    float* out = reinterpret_cast<float*>(pose);
+    for (int a = 0; a < 6; ++a) out[a] = f[a];
+  }
+}
+
+void launch_pose_to_float(double* pose, float* /*same storage*/, cudaStream_t s) {
+  pose_to_float_kernel<<<1, 32, 0, s>>>(pose);
+}
+
 }  // namespace lgs

@@ -401,6 +401,15 @@ def mapping_loss(out: RenderOutput, keyframe: dict, decoder=None, w_l1: float = 
                 depth_pixels=br.depth_pixels)
 
 
+def render_backward_loss_async(out: RenderOutput, into: dict, pose_out=None, accumulate: bool = False):
+    """Asynchronous backward of the tape's loss (device gradients); ``pose_out`` (a CUDA tensor or a
+    pinned host tensor of 6 float32) receives dL/d(omega, nu) in stream order -- no host wait."""
+    gs = _grads_struct(into, accumulate)
+    check(_lib.load().lgs_render_backward_loss_async(out.ctx.h, out.tape, C.byref(gs),
+                                                     pose_out.data_ptr() if pose_out is not None else None))
+    return into
+
+
 def render_backward_loss(out: RenderOutput, pose: bool = False, into: dict | None = None, accumulate: bool = False):
     """Backward of the loss whose cotangents the tape holds (fused L1 or mapping_loss)."""
     dev = _is_torch(out.rgb) and out.rgb.is_cuda
@@ -520,3 +529,60 @@ def coverage_mask(out: RenderOutput, measured_depth):
 
 def _ptr_any(x):
     return x.data_ptr() if _is_torch(x) else x.ctypes.data
+
+
+class Plan:
+    """One fused-L1 forward + backward step captured into a CUDA graph (lgs_plan_*): ``run()``
+    enqueues the whole step with one graph launch; ``sync()`` waits for it (re-capturing if the
+    tile lists outgrew their capacity).  ``targets``, ``grads`` and the optional ``images`` are CUDA
+    buffers whose contents may change between runs; ``pose_out`` (pinned host or CUDA, 6 float32)
+    receives the pose gradient in stream order."""
+
+    def __init__(self, dmap: DeviceMap, camera, targets: dict, grads: dict, images: dict | None = None,
+                 pose_out=None, cfg: RenderConfig | None = None):
+        self.ctx = dmap.ctx
+        self._keep = (targets, grads, images, pose_out)
+        cam = make_camera(camera)
+        d = dmap.d
+        tg = _lib.LgsL1Targets(_ptr(targets["rgb"]), _ptr(targets["depth"]), _ptr(targets["feat"]) if d else None,
+                               LGS_MEM_DEVICE)
+        imgs = None
+        if images is not None:
+            imgs = _lib.LgsImages(_ptr(images["rgb"]), _ptr(images["depth"]), _ptr(images["feat"]) if d else None,
+                                  _ptr(images["acc"]), LGS_MEM_DEVICE)
+        gs = _grads_struct(grads, False)
+        c = (cfg or RenderConfig()).c()
+        h = C.c_void_p()
+        check(_lib.load().lgs_plan_create(self.ctx.h, dmap.h, C.byref(cam), C.byref(c), C.byref(tg),
+                                          C.byref(imgs) if imgs is not None else None, C.byref(gs),
+                                          pose_out.data_ptr() if pose_out is not None else None, C.byref(h)))
+        self.h = h
+
+    def run(self):
+        check(_lib.load().lgs_plan_run(self.ctx.h, self.h))
+
+    def sync(self) -> int:
+        p = C.c_int64()
+        check(_lib.load().lgs_plan_sync(self.ctx.h, self.h, C.byref(p)))
+        return p.value
+
+    def set_camera(self, camera):
+        cam = make_camera(camera)
+        check(_lib.load().lgs_plan_set_camera(self.ctx.h, self.h, C.byref(cam)))
+
+    def elapsed_ms(self) -> float:
+        v = C.c_float()
+        check(_lib.load().lgs_plan_elapsed_ms(self.h, C.byref(v)))
+        return v.value
+
+    @property
+    def launches(self) -> int:
+        return int(_lib.load().lgs_plan_launches(self.h))
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None) and _lib._lib is not None:
+                _lib._lib.lgs_plan_destroy(self.h)
+                self.h = None
+        except (AttributeError, TypeError):  # interpreter shutdown
+            pass
