@@ -1484,7 +1484,6 @@ LGS_API lgs_status lgs_map_download(lgs_ctx* ctx, const lgs_map* map, lgs_gaussi
 namespace {
 
 constexpr char kMapMagic[8] = {'L', 'E', 'G', 'O', 'M', 'A', 'P', '1'};
-constexpr size_t kMapHeader = 8 + 4 + 8;
 
 struct MapFileHeader {
   uint32_t dim = 0;
