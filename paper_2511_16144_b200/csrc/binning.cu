@@ -79,6 +79,13 @@ void launch_scan_tiles(const uint32_t* tiles, const uint32_t* idx_sorted, int64_
   cub::DeviceScan::InclusiveSum(temp, temp_bytes, scratch, incl, (int)n, s);
 }
 
+// incl = inclusive scan of counts already in depth order (depth_order.cu gathers them).
+void launch_scan_counts(const uint32_t* cnt_sorted, int64_t n, uint32_t* incl, void* temp, size_t temp_bytes,
+                        cudaStream_t s) {
+  if (n == 0) return;
+  cub::DeviceScan::InclusiveSum(temp, temp_bytes, cnt_sorted, incl, (int)n, s);
+}
+
 // Each CTA owns 256 consecutive depth-sorted Gaussians and writes their pairs cooperatively:
 // thread t handles output slots chunk_begin + t, + 256, ... and finds the owning Gaussian by a
 // binary search over the chunk's inclusive offsets in shared memory, so the key/value stores of a

@@ -24,36 +24,49 @@
 // bit-identical to the oracle's stable sort of those keys.
 #include <cub/device/device_scan.cuh>
 
+#include <algorithm>
+
 #include "lgs_internal.cuh"
 #include "lgs_kernels.h"
 
 namespace lgs {
 
 constexpr int kWarps = 8;
-constexpr int kPairsPerWarp = 1024;
-constexpr int kPairsPerChunk = kWarps * kPairsPerWarp;
+// Warp slices are balanced by a cost that counts every Gaussian as kGaussCost pairs on top of its
+// real pairs: a warp walks one Gaussian per step, so a slice of 1-tile far-away splats costs as
+// many sequential steps as a slice of the same pair count in 32-tile near ones would cost in
+// pairs / 32.  (Balancing by pairs alone left warps of the depth-order tail with ~1000 steps.)
+constexpr int kGaussCost = 32;
+constexpr int kCostPerWarp = 2048;
+constexpr int kCostPerChunk = kWarps * kCostPerWarp;
 constexpr int kMaxFastTiles = 8192;  // warp tables: 8 x 8192 x u16 = 128 KB shared memory
 
 // excl[s] (in place over the gathered counts) and slice_first[w] = first sorted Gaussian whose
-// stream offset is >= w * kPairsPerWarp, for every warp slice w in [0, nchunks * kWarps]; culled
-// Gaussians (count 0, sorted last) map past the last slice.
+// cost offset excl[s] + kGaussCost * s is >= w * kCostPerWarp, for every warp slice w in
+// [0, nchunks * kWarps]; culled Gaussians (count 0, sorted last) map past the last slice.
+__device__ __forceinline__ int slice_of(uint32_t cnt, uint32_t excl, int64_t s, int nslices) {
+  if (!cnt) return nslices;
+  const uint64_t cost = (uint64_t)excl + (uint64_t)kGaussCost * (uint64_t)s;
+  return (int)min((uint64_t)nslices, cost / kCostPerWarp);
+}
+
+// slice_first[w] = first sorted Gaussian with slice_of(s) >= w (slice_of is non-decreasing in s:
+// culled Gaussians come last): one binary search per slice, reading the counts from incl only.
+// The gathered counts are rewritten in place as exclusive offsets.
 __global__ void chunk_bounds_kernel(uint32_t* __restrict__ cnt_to_excl, const uint32_t* __restrict__ incl, int64_t n,
                                     int nslices, uint32_t* __restrict__ slice_first) {
-  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= n) return;
-  // slices past the capacity (pairs > cap: the host re-runs with exact buffers) are clamped
-  const uint32_t cnt = cnt_to_excl[s];
-  const uint32_t excl = incl[s] - cnt;
-  const int c = cnt ? (int)min((uint32_t)nslices, excl / kPairsPerWarp) : nslices;
-  int cp = -1;
-  if (s > 0) {
-    const uint32_t cntp = incl[s - 1] - (s > 1 ? incl[s - 2] : 0u);
-    cp = cntp ? (int)min((uint32_t)nslices, (incl[s - 1] - cntp) / kPairsPerWarp) : nslices;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i <= nslices) {
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      const uint32_t ex = mid ? incl[mid - 1] : 0u;
+      if (slice_of(incl[mid] - ex, ex, mid, nslices) >= (int)i) hi = mid;
+      else lo = mid + 1;
+    }
+    slice_first[i] = (uint32_t)lo;
   }
-  for (int cc = cp + 1; cc <= c; ++cc) slice_first[cc] = (uint32_t)s;
-  if (s == n - 1)
-    for (int cc = c + 1; cc <= nslices; ++cc) slice_first[cc] = (uint32_t)n;
-  cnt_to_excl[s] = excl;
+  if (i < n) cnt_to_excl[i] = i ? incl[i - 1] : 0u;
 }
 
 // Sorted-Gaussian range [s0, s1) of warp `warp` of chunk `c`.
@@ -225,13 +238,18 @@ void launch_tile_order(const uint2* ranges, int ntiles, uint32_t* order, cudaStr
 
 bool fast_binning_supported(int ntiles) { return ntiles <= kMaxFastTiles; }
 
-static int nchunks_for(int64_t pairs) { return (int)((pairs + kPairsPerChunk - 1) / kPairsPerChunk); }
+// chunks covering the largest possible total cost: P <= pairs, at most n Gaussians with pairs
+static int nchunks_for(int64_t pairs, int64_t n) {
+  const int64_t cost = pairs + (int64_t)kGaussCost * std::min(n, pairs);
+  return (int)((cost + kCostPerChunk - 1) / kCostPerChunk);
+}
 
-size_t fast_binning_scratch_bytes(int64_t pairs, int ntiles) {
-  const size_t cells = (size_t)nchunks_for(pairs) * (size_t)ntiles;
+size_t fast_binning_scratch_bytes(int64_t pairs, int64_t n, int ntiles) {
+  const int nchunks = nchunks_for(pairs, n);
+  const size_t cells = (size_t)nchunks * (size_t)ntiles;
   size_t scan = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, scan, (uint32_t*)nullptr, (uint32_t*)nullptr, (int)cells);
-  return sizeof(uint32_t) * (cells * 2 + (size_t)nchunks_for(pairs) * kWarps + 1) + scan + 256;
+  return sizeof(uint32_t) * (cells * 2 + (size_t)nchunks * kWarps + 1) + scan + 256;
 }
 
 void launch_fast_binning(const ViewBufs& v, const uint32_t* idx_sorted, uint32_t* cnt_sorted, const uint32_t* incl,
@@ -242,7 +260,7 @@ void launch_fast_binning(const ViewBufs& v, const uint32_t* idx_sorted, uint32_t
     cudaMemsetAsync(dev_overflow, 0, sizeof(uint32_t), s);
     return;
   }
-  const int nchunks = nchunks_for(cap);
+  const int nchunks = nchunks_for(cap, n);
   const size_t cells = (size_t)nchunks * (size_t)ntiles;
   uint32_t* counts = scratch;
   uint32_t* offs = counts + cells;
@@ -259,7 +277,9 @@ void launch_fast_binning(const ViewBufs& v, const uint32_t* idx_sorted, uint32_t
     attr_set = true;
   }
   const uint32_t* excl = cnt_sorted;  // rewritten in place by chunk_bounds_kernel
-  chunk_bounds_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(cnt_sorted, incl, n, nchunks * kWarps, chunk_first);
+  const int64_t nb_threads = std::max<int64_t>(n, (int64_t)nchunks * kWarps + 1);
+  chunk_bounds_kernel<<<(unsigned)((nb_threads + 255) / 256), 256, 0, s>>>(cnt_sorted, incl, n, nchunks * kWarps,
+                                                                           chunk_first);
   const int threads = kWarps * 32;
   tile_count_kernel<<<nchunks, threads, sizeof(uint32_t) * ntiles, s>>>(v.rect, v.tiles, idx_sorted, excl, chunk_first,
                                                                         ntiles, tiles_x, nchunks, counts);

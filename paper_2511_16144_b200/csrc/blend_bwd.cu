@@ -132,7 +132,10 @@ __global__ void __launch_bounds__(kBlock / PPT) blend_bwd_kernel(DevMap m, DevCa
     }
     if (tid == 0) s_max = 0;
     __syncthreads();
-    if (my_max) atomicMax(&s_max, my_max);
+    // this warp's traversal length: entries past every one of its pixels' last contributor are
+    // skipped without evaluation (warp-uniform)
+    const uint32_t warp_last = __reduce_max_sync(0xffffffffu, my_max);
+    if (lane == 0 && warp_last) atomicMax(&s_max, warp_last);
     __syncthreads();
     const uint32_t end = range.x + s_max;
 
@@ -157,7 +160,8 @@ __global__ void __launch_bounds__(kBlock / PPT) blend_bwd_kernel(DevMap m, DevCa
         }
       }
       __syncthreads();
-      for (int e = cnt - 1; e >= 0; --e) {
+      const int e_top = (int)min((int64_t)cnt - 1, (int64_t)range.x + (int64_t)warp_last - 1 - (int64_t)bstart);
+      for (int e = e_top; e >= 0; --e) {
         const uint32_t jrel = bstart + (uint32_t)e - range.x;
         const uint2 rc = sm.rect[e];
         const int ry0 = (int)(rc.y & 0xffffu), ry1 = (int)(rc.y >> 16);

@@ -584,12 +584,24 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
   TRYB(dalloc(ctx, &idx_sorted, n));
   TRYB(dalloc(ctx, &incl, n));
   TRYB(dalloc(ctx, reinterpret_cast<uint8_t**>(&temp), temp_bytes));
+  // LGS_DEPTH_SORT=cub selects the device radix sort (A/B and cross-check of depth_order.cu)
+  const char* dsort = getenv("LGS_DEPTH_SORT");
+  const bool cub_depth = dsort && dsort[0] == 'c';
+  void* otemp = nullptr;
+  const size_t otemp_bytes = cub_depth ? 0 : depth_order_temp_bytes(n);
+  if (!cub_depth) TRYB(dalloc(ctx, reinterpret_cast<uint8_t**>(&otemp), otemp_bytes));
   {
     PhaseScope ph(ctx, PH_DEPTH_SORT);
-    launch_depth_sort(t->vb, n, dkey_sorted, idx_sorted, temp, temp_bytes, s);
-    launch_scan_tiles(t->vb.tiles, idx_sorted, n, dkey_sorted, incl, temp, temp_bytes, s);
+    if (cub_depth) {
+      launch_depth_sort(t->vb, n, dkey_sorted, idx_sorted, temp, temp_bytes, s);
+      launch_scan_tiles(t->vb.tiles, idx_sorted, n, dkey_sorted, incl, temp, temp_bytes, s);
+    } else {
+      launch_depth_order(t->vb, n, dc.near_plane, otemp, otemp_bytes, idx_sorted, dkey_sorted, s);
+      launch_scan_counts(dkey_sorted, n, incl, temp, temp_bytes, s);
+    }
   }
-  ctx->launches += n > 0 ? 6 : 0;
+  ctx->launches += n > 0 ? (cub_depth ? 6 : 7) : 0;
+  if (otemp) dfree(ctx, otemp);
 
   // K5 (+ fused L1) buffers
   FwdOut fo{};
@@ -640,7 +652,7 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
     if (fast) {
       // stable counting sort by tile straight into the final lists (binning_fast.cu)
       uint32_t* scratch = nullptr;
-      LGS_TRY(dalloc(ctx, reinterpret_cast<uint8_t**>(&scratch), fast_binning_scratch_bytes(cap, ntiles)));
+      LGS_TRY(dalloc(ctx, reinterpret_cast<uint8_t**>(&scratch), fast_binning_scratch_bytes(cap, n, ntiles)));
       {
         PhaseScope ph(ctx, PH_TILE_SORT);
         launch_fast_binning(t->vb, idx_sorted, dkey_sorted, incl, n, ntiles, dc.tiles_x, scratch, t->vals, t->ranges,

@@ -75,6 +75,13 @@ void launch_depth_sort(const ViewBufs& v, int64_t n, uint32_t* dkey_sorted, uint
                        void* temp, size_t temp_bytes, cudaStream_t s);
 void launch_scan_tiles(const uint32_t* tiles, const uint32_t* idx_sorted, int64_t n, uint32_t* scratch,
                        uint32_t* incl, void* temp, size_t temp_bytes, cudaStream_t s);
+void launch_scan_counts(const uint32_t* cnt_sorted, int64_t n, uint32_t* incl, void* temp, size_t temp_bytes,
+                        cudaStream_t s);
+// Global (depth, index) order without a device radix sort (depth_order.cu): idx_sorted = visible
+// Gaussians in (depth key, map index) order, then the culled ones; cnt_sorted = their tile counts.
+size_t depth_order_temp_bytes(int64_t n);
+void launch_depth_order(const ViewBufs& v, int64_t n, float near_plane, void* temp, size_t temp_bytes,
+                        uint32_t* idx_sorted, uint32_t* cnt_sorted, cudaStream_t s);
 void launch_duplicate(const ViewBufs& v, const uint32_t* idx_sorted, const uint32_t* incl, int64_t n,
                       int tiles_x, uint16_t* key_out, uint32_t* val_out, cudaStream_t s);
 void launch_tile_sort(uint16_t* keys_in, uint16_t* keys_out, uint32_t* vals_in, uint32_t* vals_out,
@@ -84,11 +91,11 @@ void launch_ranges(const uint16_t* keys, int64_t pairs, int ntiles, uint2* range
 // Fast binning (stable counting sort by tile; binning.cu): writes the sorted list `vals` and the
 // per-tile `ranges` directly.  `cnt_sorted` holds tiles[idx_sorted[s]] (launch_scan_tiles'
 // scratch; overwritten), `incl` its inclusive scan; `scratch` must hold
-// fast_binning_scratch_bytes(cap, ntiles) and `vals` cap entries.  The pair count itself is read on
+// fast_binning_scratch_bytes(cap, n, ntiles) and `vals` cap entries.  The pair count itself is read on
 // the device (`dev_pairs`), so the host never waits for it: if it exceeds `cap`, every tile list is
 // left empty and *dev_overflow = 1 (the host then re-runs with exact buffers).
 bool fast_binning_supported(int ntiles);
-size_t fast_binning_scratch_bytes(int64_t cap, int ntiles);
+size_t fast_binning_scratch_bytes(int64_t cap, int64_t n, int ntiles);
 void launch_fast_binning(const ViewBufs& v, const uint32_t* idx_sorted, uint32_t* cnt_sorted, const uint32_t* incl,
                          int64_t n, int ntiles, int tiles_x, uint32_t* scratch, uint32_t* vals, uint2* ranges,
                          uint32_t cap, const uint32_t* dev_pairs, uint32_t* dev_overflow, cudaStream_t s);

@@ -401,3 +401,34 @@ def test_speculative_pair_capacity(oracle):
     okeys, ovals, oranges = oracle.bin_f32(oracle.preprocess_f32(big, bcams[0]), bcams[0]["width"], bcams[0]["height"])
     keys, vals, ranges = over.tile_keys()
     assert np.array_equal(keys, okeys) and np.array_equal(vals, ovals) and np.array_equal(ranges, oranges)
+
+
+def test_depth_order_ties_and_big_buckets(oracle):
+    """The bucketed depth order (depth_order.cu) on adversarial depths: 3000 splats at one identical
+    depth (a tie group far larger than the rank kernel's bucket limit: bitonic path), 1500 more a
+    few ulps apart (one crowded bucket), and 2000 spread ones.  Tile lists must still equal the
+    oracle's stable (tile, depth) sort, and the device radix-sort path bit for bit."""
+    import os
+
+    scene, cams, _ = scenes.make_config("c0", n=6500)
+    pos = scene["pos"].copy()
+    pos[:3000, 2] = np.float32(3.0)
+    base = np.float32(2.5)
+    pos[3000:4500, 2] = base + (np.arange(1500) % 7).astype(np.float32) * np.spacing(base)
+    scene = dict(scene, pos=pos)
+    cam = cams[0]
+    out = R.render(dev_scene(scene), cam, ctx=R.Context(0))
+    torch.cuda.synchronize()
+    keys, vals, ranges = out.tile_keys()
+    op = oracle.preprocess_f32(scene, cam)
+    okeys, ovals, oranges = oracle.bin_f32(op, cam["width"], cam["height"])
+    assert np.array_equal(keys, okeys) and np.array_equal(vals, ovals) and np.array_equal(ranges, oranges)
+    os.environ["LGS_DEPTH_SORT"] = "cub"
+    try:
+        ref = R.render(dev_scene(scene), cam, ctx=R.Context(0))
+        torch.cuda.synchronize()
+    finally:
+        del os.environ["LGS_DEPTH_SORT"]
+    for a, b in zip(out.tile_keys(), ref.tile_keys()):
+        assert np.array_equal(a, b)
+    assert torch.equal(out.rgb, ref.rgb)
