@@ -138,6 +138,8 @@ typedef struct {
   int64_t pairs;          /* P: (tile, Gaussian) pairs */
   int64_t tiles;          /* number of 16x16 tiles */
   int64_t max_tile_list;  /* longest per-tile list */
+  int64_t listed;         /* entries the tile lists hold: P with complete lists; with the depth-layered
+                             binning, saturated tiles keep only the prefix their pixels can reach */
 } lgs_render_stats;
 
 /* ---- library / context ---------------------------------------------------------------- */
@@ -149,6 +151,11 @@ LGS_API lgs_render_config lgs_render_config_default(void);
  * own non-blocking stream) or an existing cudaStream_t to enqueue on (e.g. torch's). */
 LGS_API lgs_status lgs_ctx_create(int32_t device, void* stream, lgs_ctx** out);
 LGS_API lgs_status lgs_ctx_destroy(lgs_ctx* ctx);
+/* Binning policy of the context's renders (default 0).  0: depth-layered binning -- the tile lists
+ * hold, per tile, the depth-order prefix its pixels can reach before saturating (T < T_min,
+ * renderer.cpp:140), completed for tiles that do not saturate; images and gradients are identical.
+ * 1: every (tile, Gaussian) pair is listed (parity checks of the complete sorted lists). */
+LGS_API lgs_status lgs_ctx_set_full_tile_lists(lgs_ctx* ctx, int32_t full);
 LGS_API lgs_status lgs_ctx_set_stream(lgs_ctx* ctx, void* stream);
 LGS_API lgs_status lgs_ctx_synchronize(lgs_ctx* ctx);
 
@@ -203,8 +210,9 @@ LGS_API lgs_status lgs_saved_destroy(lgs_saved* tape);
 LGS_API lgs_status lgs_debug_projected(lgs_ctx* ctx, const lgs_saved* tape, uint8_t* visible, float* u,
                                        float* v, float* depth, float* conic, float* radius, int32_t* bbox,
                                        float* opacity, float* color);
-/* Sorted tile key list: keys = (tile << 32) | f32bits(depth), vals = map index, ranges
- * [tiles][2] = [begin, end).  Host buffers; keys/vals of length lgs_render_stats.pairs. */
+/* Sorted tile key lists, concatenated in tile order: keys = (tile << 32) | f32bits(depth),
+ * vals = map index, ranges [tiles][2] = [begin, end).  Host buffers; keys/vals of length
+ * lgs_render_stats.listed (= pairs with lgs_ctx_set_full_tile_lists(ctx, 1)). */
 LGS_API lgs_status lgs_debug_tile_keys(lgs_ctx* ctx, const lgs_saved* tape, uint64_t* keys, uint32_t* vals,
                                        uint32_t* ranges);
 /* Per pixel: final transmittance and contributor-list end (index into the tile list,
@@ -239,6 +247,8 @@ LGS_API lgs_status lgs_saved_work(const lgs_saved* tape, int64_t* evaluated, int
 /* Measured FP32 FFMA throughput of `device` (TFLOP/s): the roofline denominator of the blend
  * kernels.  Runs a ~10 ms microbenchmark on the legacy stream; call outside timed regions. */
 LGS_API lgs_status lgs_measure_fp32_peak(int32_t device, double* tflops);
+/* Measured legacy tensor-core (mma.sync m16n8k8 TF32, fp32 accumulate) throughput, TFLOP/s. */
+LGS_API lgs_status lgs_measure_mma_tf32_peak(int32_t device, double* tflops);
 
 /* Self-test of the warp-level TF32 tensor-core fragment layouts used by the backward blend:
  * d = a (16x8, row-major) * b (8x8, row-major), host buffers; split = 1 uses the 3xTF32 split. */

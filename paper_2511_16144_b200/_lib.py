@@ -55,7 +55,8 @@ class LgsCotangents(C.Structure):
 
 
 class LgsRenderStats(C.Structure):
-    _fields_ = [("visible", C.c_int64), ("pairs", C.c_int64), ("tiles", C.c_int64), ("max_tile_list", C.c_int64)]
+    _fields_ = [("visible", C.c_int64), ("pairs", C.c_int64), ("tiles", C.c_int64), ("max_tile_list", C.c_int64),
+                ("listed", C.c_int64)]
 
 
 class LgsDecoder(C.Structure):
@@ -91,6 +92,7 @@ SIGNATURES = [
     ("lgs_last_error", C.c_char_p, []),
     ("lgs_render_config_default", LgsRenderConfig, []),
     ("lgs_ctx_create", C.c_int, [C.c_int32, C.c_void_p, C.POINTER(C.c_void_p)]),
+    ("lgs_ctx_set_full_tile_lists", C.c_int, [C.c_void_p, C.c_int32]),
     ("lgs_ctx_destroy", C.c_int, [C.c_void_p]),
     ("lgs_ctx_set_stream", C.c_int, [C.c_void_p, C.c_void_p]),
     ("lgs_ctx_synchronize", C.c_int, [C.c_void_p]),
@@ -117,6 +119,7 @@ SIGNATURES = [
     ("lgs_ctx_phase_times", C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int64), C.c_int32]),
     ("lgs_saved_work", C.c_int, [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     ("lgs_measure_fp32_peak", C.c_int, [C.c_int32, C.POINTER(C.c_double)]),
+    ("lgs_measure_mma_tf32_peak", C.c_int, [C.c_int32, C.POINTER(C.c_double)]),
     ("lgs_debug_mma_selftest", C.c_int, [C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32]),
     ("lgs_loss_weights_default", LgsLossWeights, []),
     ("lgs_mapping_loss", C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(LgsImages), C.POINTER(LgsKeyframe),

@@ -47,12 +47,14 @@ __device__ __forceinline__ void thread_pixels(int tid, int& lx, int& ly0) {
 
 // Persistent-CTA tile scheduler: CTAs pull tile slots from a global counter; slot i is the i-th
 // longest tile list (TileLists::order), so the long tiles start first and the tail is short.
+// With tl.count the order holds only *tl.count tiles (second pass of the layered binning).
 __device__ __forceinline__ int next_tile(const TileLists& tl, int ntiles, int* s_slot) {
   __syncthreads();
   if (threadIdx.x == 0) *s_slot = atomicAdd(tl.counter, 1);
   __syncthreads();
   const int slot = *s_slot;
-  return slot < ntiles ? (int)tl.order[slot] : -1;
+  const int active = tl.count ? (int)*tl.count : ntiles;
+  return slot < active ? (int)tl.order[slot] : -1;
 }
 
 }  // namespace lgs

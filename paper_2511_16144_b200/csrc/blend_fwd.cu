@@ -52,6 +52,9 @@ __global__ void __launch_bounds__(kBlock / PPT) blend_fwd_kernel(DevMap m, DevCa
     const int px = tx * kTile + lx;
     const int py0 = ty * kTile + ly0;
     const float fpx = (float)px;
+    float fpy[PPT];
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) fpy[k] = (float)(py0 + k);
     const uint2 range = tl.ranges[tile];
 
     float T[PPT], cr[PPT], cg[PPT], cb[PPT], draw[PPT], acc[PPT];
@@ -90,33 +93,23 @@ __global__ void __launch_bounds__(kBlock / PPT) blend_fwd_kernel(DevMap m, DevCa
       }
       __syncthreads();
       const int cnt = (int)min((uint32_t)kBlock, range.y - base);
-      for (int e = 0; e < cnt && !all_done; ++e) {
-        const uint2 rc = sm.rect[e];
-        if (px < (int)(rc.x & 0xffffu) || px > (int)(rc.x >> 16)) continue;
-        const int ry0 = (int)(rc.y & 0xffffu), ry1 = (int)(rc.y >> 16);
-        if (py0 > ry1 || py0 + PPT - 1 < ry0) continue;
-        const float4 r0 = sm.r0[e];
-        const float4 s4 = sm.sc[e];
-        const ScaledConic sc{s4.x, s4.y, s4.z};
-        // Evaluate the PPT pixels branch-free (independent chains the scheduler can interleave),
-        // then composite all of them at once: a pixel that does not contribute gets alpha = 0,
-        // which leaves T, the accumulators and the counters exactly unchanged (w = +0).
+      // Composite one staged entry given its pixels' alphas (evaluated earlier): a pixel that does
+      // not contribute gets alpha = 0, which leaves T, the accumulators and the counters exactly
+      // unchanged (w = +0).
+      auto composite = [&](int e, const float (&al)[PPT], const bool (&in)[PPT], float depth_z) {
         float a[PPT];
         bool ok[PPT];
         bool any = false;
 #pragma unroll
         for (int k = 0; k < PPT; ++k) {
-          const int py = py0 + k;
-          float dx, dy, G;
-          const float alpha = splat_alpha(r0.x, r0.y, sc, r0.w, fpx, (float)py, dx, dy, G);
-          const bool in = !done[k] && py >= ry0 && py <= ry1;
-          ok[k] = in && alpha >= c.alpha_skip;
-          n_eval[k] += in ? 1u : 0u;
+          const bool live = in[k] && !done[k];
+          ok[k] = live && al[k] >= c.alpha_skip;
+          n_eval[k] += live ? 1u : 0u;
           n_contrib[k] += ok[k] ? 1u : 0u;
-          a[k] = ok[k] ? fminf(alpha, c.alpha_clamp) : 0.f;
+          a[k] = ok[k] ? fminf(al[k], c.alpha_clamp) : 0.f;
           any = any || ok[k];
         }
-        if (!any) continue;
+        if (!any) return;
         const float4 col = sm.col[e];
         float w[PPT];
 #pragma unroll
@@ -125,7 +118,7 @@ __global__ void __launch_bounds__(kBlock / PPT) blend_fwd_kernel(DevMap m, DevCa
           cr[k] = fmaf(w[k], col.x, cr[k]);
           cg[k] = fmaf(w[k], col.y, cg[k]);
           cb[k] = fmaf(w[k], col.z, cb[k]);
-          draw[k] = fmaf(w[k], r0.z, draw[k]);
+          draw[k] = fmaf(w[k], depth_z, draw[k]);
           acc[k] += w[k];
         }
         if (DP > 0) {
@@ -147,12 +140,42 @@ __global__ void __launch_bounds__(kBlock / PPT) blend_fwd_kernel(DevMap m, DevCa
           if (ok[k]) last[k] = base + e + 1 - range.x;
           done[k] = done[k] || T[k] < c.t_min;
         }
+      };
+      // Two entries per step: both entries' alphas are evaluated first (independent chains the
+      // scheduler interleaves), then they are composited in list order.
+      for (int e = 0; e < cnt && !all_done; e += 2) {
+        const bool has1 = e + 1 < cnt;
+        const uint2 rc0 = sm.rect[e];
+        const uint2 rc1 = has1 ? sm.rect[e + 1] : make_uint2(0xffffu, 0xffffu);  // empty rect
+        const bool hit0 = px >= (int)(rc0.x & 0xffffu) && px <= (int)(rc0.x >> 16) &&
+                          py0 <= (int)(rc0.y >> 16) && py0 + PPT - 1 >= (int)(rc0.y & 0xffffu);
+        const bool hit1 = px >= (int)(rc1.x & 0xffffu) && px <= (int)(rc1.x >> 16) &&
+                          py0 <= (int)(rc1.y >> 16) && py0 + PPT - 1 >= (int)(rc1.y & 0xffffu);
+        if (!hit0 && !hit1) continue;
+        const float4 r00 = sm.r0[e], s00 = sm.sc[e];
+        const float4 r01 = has1 ? sm.r0[e + 1] : r00, s01 = has1 ? sm.sc[e + 1] : s00;
+        float al0[PPT], al1[PPT];
+        bool in0[PPT], in1[PPT];
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) {
+          float dx, dy, G;
+          al0[k] = splat_alpha(r00.x, r00.y, ScaledConic{s00.x, s00.y, s00.z}, r00.w, fpx, fpy[k], dx, dy, G);
+          al1[k] = splat_alpha(r01.x, r01.y, ScaledConic{s01.x, s01.y, s01.z}, r01.w, fpx, fpy[k], dx, dy, G);
+          const int py = py0 + k;
+          in0[k] = hit0 && py >= (int)(rc0.y & 0xffffu) && py <= (int)(rc0.y >> 16);
+          in1[k] = hit1 && py >= (int)(rc1.y & 0xffffu) && py <= (int)(rc1.y >> 16);
+        }
+        if (hit0) composite(e, al0, in0, r00.z);
+        if (hit1) composite(e + 1, al1, in1, r01.z);
         all_done = true;
 #pragma unroll
         for (int k = 0; k < PPT; ++k) all_done = all_done && done[k];
       }
     }
 
+    // layered first pass: a tile with an unsaturated pixel is rendered again on its complete list
+    const bool tile_done = o.unfinished ? __syncthreads_and(all_done) != 0 : true;
+    if (!tile_done && tid == 0) o.unfinished[tile] = 1u;
 #pragma unroll
     for (int k = 0; k < PPT; ++k) {
       const int py = py0 + k;
@@ -183,7 +206,7 @@ __global__ void __launch_bounds__(kBlock / PPT) blend_fwd_kernel(DevMap m, DevCa
             if (q < m.d) fo[q] = f[k][q];
         }
       }
-      if (L1) {
+      if (L1 && tile_done) {
         // L = mean|rgb - T| + mean|depth - T| + mean|feat - T|; cotangent sign(diff) / count
         const float npx = (float)c.W * (float)c.H;
         const float inv_rgb = 1.0f / (3.0f * npx), inv_d = 1.0f / npx;

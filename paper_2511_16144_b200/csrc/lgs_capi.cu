@@ -61,6 +61,9 @@ int pad_dim(int d) {
   return 32;
 }
 
+// layer A of the depth-layered binning owns ~1/kLayerDiv of the pairs (binning_fast.cu)
+constexpr uint32_t kLayerDiv = 16;
+
 int bits_for(int ntiles) {
   int b = 0;
   while ((1 << b) < ntiles) ++b;
@@ -86,6 +89,9 @@ struct lgs_ctx {
   cudaMemPool_t pool = nullptr;  // this context's stream-ordered arena (no cross-context reuse waits)
   bool capturing = false;        // inside lgs_plan capture: no host waits, graph memory nodes
   int64_t pairs_cap = 0;  // tile-list capacity for the next render (0: size from the exact count)
+  bool full_lists = false;  // lgs_ctx_set_full_tile_lists: single-pass binning of every pair
+  cudaStream_t cond_stream = nullptr;  // captures the body of a plan's conditional node
+  cudaStream_t cond_parent = nullptr;  // the capturing stream while a body is captured
   // multi-view gradient all-reduce (lgs_comm_*): one NCCL communicator per context / GPU
   ncclComm_t comm = nullptr;
   int32_t comm_world = 0, comm_rank = 0;
@@ -98,6 +104,48 @@ struct lgs_ctx {
 };
 
 namespace {
+
+// Conditional graph nodes inside a plan capture (CUDA 12.4+): cond_create makes the handle a
+// kernel sets with cudaGraphSetConditional, cond_begin adds an IF node after everything captured so
+// far and redirects the context's launches into its body graph, cond_end returns to the parent.
+lgs_status cond_create(lgs_ctx* ctx, cudaGraphConditionalHandle* h) {
+  cudaStreamCaptureStatus st;
+  cudaGraph_t g = nullptr;
+  LGS_CUDA(cudaStreamGetCaptureInfo(ctx->stream, &st, nullptr, &g, nullptr, nullptr));
+  if (st != cudaStreamCaptureStatusActive || !g) return fail(LGS_EINVAL, "conditional node outside a capture");
+  LGS_CUDA(cudaGraphConditionalHandleCreate(h, g, 0, cudaGraphCondAssignDefault));
+  return LGS_OK;
+}
+
+lgs_status cond_begin(lgs_ctx* ctx, cudaGraphConditionalHandle h) {
+  cudaStreamCaptureStatus st;
+  cudaGraph_t g = nullptr;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t ndeps = 0;
+  LGS_CUDA(cudaStreamGetCaptureInfo(ctx->stream, &st, nullptr, &g, &deps, &ndeps));
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeIf;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  LGS_CUDA(cudaGraphAddNode(&node, g, deps, ndeps, &cp));
+  LGS_CUDA(cudaStreamUpdateCaptureDependencies(ctx->stream, &node, 1, cudaStreamSetCaptureDependencies));
+  if (!ctx->cond_stream) LGS_CUDA(cudaStreamCreateWithFlags(&ctx->cond_stream, cudaStreamNonBlocking));
+  LGS_CUDA(cudaStreamBeginCaptureToGraph(ctx->cond_stream, cp.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                         cudaStreamCaptureModeThreadLocal));
+  ctx->cond_parent = ctx->stream;
+  ctx->stream = ctx->cond_stream;
+  return LGS_OK;
+}
+
+lgs_status cond_end(lgs_ctx* ctx) {
+  cudaGraph_t body = nullptr;
+  ctx->stream = ctx->cond_parent;
+  ctx->cond_parent = nullptr;
+  LGS_CUDA(cudaStreamEndCapture(ctx->cond_stream, &body));
+  return LGS_OK;
+}
 
 // RAII phase marker: records an event pair around a phase when profiling is on.
 struct PhaseScope {
@@ -170,6 +218,7 @@ struct lgs_saved {
   double* loss = nullptr;
   double* loss_sums = nullptr;  // lgs_mapping_loss partial sums [LOSS_COUNT]
   int64_t pairs = 0;
+  int64_t vals_count = 0;  // entries allocated in vals (the lists live at the ranges' offsets)
   int ntiles = 0;
 };
 
@@ -183,6 +232,7 @@ void ctx_release(lgs_ctx* ctx) {
       if (const NcclApi* nc = nccl_api(nullptr)) nc->CommDestroy(ctx->comm);
     }
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    if (ctx->cond_stream) cudaStreamDestroy(ctx->cond_stream);
     if (ctx->pool) cudaMemPoolDestroy(ctx->pool);
     if (ctx->host_u32) cudaFreeHost(ctx->host_u32);
     if (ctx->dev_u32) cudaFree(ctx->dev_u32);
@@ -420,6 +470,12 @@ LGS_API lgs_status lgs_ctx_create(int32_t device, void* stream, lgs_ctx** out) {
   return LGS_OK;
 }
 
+LGS_API lgs_status lgs_ctx_set_full_tile_lists(lgs_ctx* ctx, int32_t full) {
+  if (!ctx) return fail(LGS_EINVAL, "ctx is NULL");
+  ctx->full_lists = full != 0;
+  return LGS_OK;
+}
+
 LGS_API lgs_status lgs_ctx_destroy(lgs_ctx* ctx) {
   if (!ctx) return LGS_OK;
   ctx_release(ctx);
@@ -641,24 +697,108 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
   // (and an overflow flag) only after the whole forward is queued, when the GPU is far ahead of the
   // check.  P > capacity (or the first render) runs the binning again with buffers of exactly P.
   const bool fast = fast_binning_supported(ntiles);
+  const bool layered = fast && !ctx->full_lists && n > 0;
   auto bin_and_blend = [&](int64_t cap, bool exact) -> lgs_status {
-    if (!exact) {  // re-run: the fast binning consumed the scanned tile counts in place
+    if (!exact) {  // re-run with exact buffers: the tile counts in depth order again
       launch_scan_tiles(t->vb.tiles, idx_sorted, n, dkey_sorted, incl, temp, temp_bytes, s);
       ctx->launches += n > 0 ? 3 : 0;
     }
     dfree(ctx, t->vals);
     dfree(ctx, t->keys);
+    if (layered) {
+      // Depth-layered binning (binning_fast.cu): pass 1 bins the depth-order prefix owning
+      // ~P / kLayerDiv pairs for every tile and blends it; tiles left unsaturated get their
+      // complete lists (after layer A's, at vals + capA) and are blended again.
+      const uint32_t capA = (uint32_t)layer_a_cap(cap, ntiles, kLayerDiv);
+      const int64_t gcapA = std::min<int64_t>(n, std::max<int64_t>(4096, n / 32));
+      const size_t sat_n = (size_t)(dc.tiles_x + 1) * (dc.tiles_y + 1);
+      uint32_t *pa = nullptr, *unfinished = nullptr, *sat = nullptr, *order2 = nullptr, *count2 = nullptr;
+      uint32_t *scratch_a = nullptr, *scratch_b = nullptr;
+      LGS_TRY(dalloc(ctx, &t->vals, (size_t)capA + (size_t)cap));
+      t->vals_count = (int64_t)capA + cap;
+      LGS_TRY(dalloc(ctx, &pa, 1));
+      LGS_TRY(dalloc(ctx, &unfinished, ntiles));
+      LGS_TRY(dalloc(ctx, &sat, sat_n));
+      LGS_TRY(dalloc(ctx, &order2, ntiles));
+      LGS_TRY(dalloc(ctx, &count2, 2));  // [0] unfinished tiles, [1] pairs of the second pass
+      LGS_TRY(dalloc(ctx, reinterpret_cast<uint8_t**>(&scratch_a), fast_binning_scratch_bytes(capA, gcapA, ntiles)));
+      LGS_TRY(dalloc(ctx, reinterpret_cast<uint8_t**>(&scratch_b), fast_binning_scratch_bytes(cap, n, ntiles)));
+      LGS_CUDA(cudaMemsetAsync(unfinished, 0, sizeof(uint32_t) * ntiles, s));
+      {
+        PhaseScope ph(ctx, PH_TILE_SORT);
+        launch_layer_cut(incl, n, kLayerDiv, gcapA, pa, s);
+        BinPass a{incl, pa, gcapA, capA, 0u, nullptr};
+        a.clamp = pa;
+        launch_fast_binning(t->vb, idx_sorted, n, ntiles, dc.tiles_x, a, scratch_a, t->vals, t->ranges,
+                            ctx->dev_u32 + 1, s);
+        launch_tile_order(t->ranges, ntiles, t->order, s);  // longest tile list first
+      }
+      ctx->launches += 7;
+      if (targets) LGS_CUDA(cudaMemsetAsync(t->loss, 0, sizeof(double), s));
+      FwdOut fo1 = fo;
+      fo1.unfinished = unfinished;
+      {
+        PhaseScope ph(ctx, PH_BLEND_FWD);
+        launch_blend_fwd(map->dm, dc, t->vb, TileLists{t->vals, t->ranges, t->order, t->counter}, t->ps, fo1, s);
+      }
+      ctx->launches++;
+      // pass 2, inside a captured plan as the body of a conditional node (skipped when every tile
+      // saturated); eagerly its kernels find no unfinished tile and return at once
+      cudaGraphConditionalHandle cond{};
+      const bool use_cond = ctx->capturing;
+      if (use_cond) LGS_TRY(cond_create(ctx, &cond));
+      {
+        PhaseScope ph(ctx, PH_TILE_SORT);
+        launch_layer_prep(unfinished, t->ranges, dc.tiles_x, dc.tiles_y, sat, order2, count2, count2 + 1,
+                          use_cond ? &cond : nullptr, s);
+      }
+      ctx->launches++;
+      if (use_cond) LGS_TRY(cond_begin(ctx, cond));
+      lgs_status st2 = LGS_OK;
+      {
+        cudaStream_t s2 = ctx->stream;  // the conditional body's capture stream inside a plan
+        {
+          PhaseScope ph(ctx, PH_TILE_SORT);
+          launch_layer_count(t->vb, idx_sorted, n, dc.tiles_x, sat, count2, dkey_sorted, count2 + 1, s2);
+          launch_scan_counts(dkey_sorted, n, incl, temp, temp_bytes, s2);
+          const BinPass b{incl, count2 + 1, n, (uint32_t)cap, capA, unfinished, count2};
+          launch_fast_binning(t->vb, idx_sorted, n, ntiles, dc.tiles_x, b, scratch_b, t->vals, t->ranges,
+                              ctx->dev_u32 + 2, s2);
+        }
+        FwdOut fo2 = fo;
+        {
+          PhaseScope ph(ctx, PH_BLEND_FWD);
+          launch_blend_fwd(map->dm, dc, t->vb, TileLists{t->vals, t->ranges, order2, t->counter, count2}, t->ps, fo2,
+                           s2);
+        }
+        if (cudaGetLastError() != cudaSuccess) st2 = fail(LGS_ECUDA, "layered binning pass 2 launch failed");
+      }
+      ctx->launches += 9;
+      if (use_cond) LGS_TRY(cond_end(ctx));
+      LGS_TRY(st2);
+      dfree(ctx, scratch_b);
+      dfree(ctx, scratch_a);
+      dfree(ctx, count2);
+      dfree(ctx, order2);
+      dfree(ctx, sat);
+      dfree(ctx, unfinished);
+      dfree(ctx, pa);
+      LGS_CUDA(cudaGetLastError());
+      return LGS_OK;
+    }
     LGS_TRY(dalloc(ctx, &t->vals, cap));
+    t->vals_count = cap;
     if (fast) {
       // stable counting sort by tile straight into the final lists (binning_fast.cu)
       uint32_t* scratch = nullptr;
       LGS_TRY(dalloc(ctx, reinterpret_cast<uint8_t**>(&scratch), fast_binning_scratch_bytes(cap, n, ntiles)));
       {
         PhaseScope ph(ctx, PH_TILE_SORT);
-        launch_fast_binning(t->vb, idx_sorted, dkey_sorted, incl, n, ntiles, dc.tiles_x, scratch, t->vals, t->ranges,
-                            (uint32_t)cap, ctx->dev_u32, ctx->dev_u32 + 1, s);
+        const BinPass all{incl, incl + n - 1, n, (uint32_t)cap, 0u, nullptr};
+        launch_fast_binning(t->vb, idx_sorted, n, ntiles, dc.tiles_x, all, scratch, t->vals, t->ranges,
+                            ctx->dev_u32 + 1, s);
       }
-      ctx->launches += cap > 0 ? 6 : 0;
+      ctx->launches += cap > 0 ? 5 : 0;
       dfree(ctx, scratch);
     } else {
       uint16_t* keys_in = nullptr;
@@ -1098,13 +1238,20 @@ LGS_API lgs_status lgs_saved_stats(const lgs_saved* tape, lgs_render_stats* st) 
   LGS_CUDA(cudaMemcpyAsync(ranges.data(), tape->ranges, sizeof(uint2) * ranges.size(), cudaMemcpyDeviceToHost,
                            ctx->stream));
   LGS_CUDA(cudaStreamSynchronize(ctx->stream));
-  int64_t vis = 0, mx = 0;
-  for (uint32_t v : tiles) vis += v != 0;
-  for (const uint2& r : ranges) mx = std::max<int64_t>(mx, (int64_t)r.y - (int64_t)r.x);
+  int64_t vis = 0, mx = 0, pairs = 0, listed = 0;
+  for (uint32_t v : tiles) {
+    vis += v != 0;
+    pairs += v;
+  }
+  for (const uint2& r : ranges) {
+    mx = std::max<int64_t>(mx, (int64_t)r.y - (int64_t)r.x);
+    listed += (int64_t)r.y - (int64_t)r.x;
+  }
   st->visible = vis;
-  st->pairs = tape->pairs;
+  st->pairs = pairs;
   st->tiles = tape->ntiles;
   st->max_tile_list = mx;
+  st->listed = listed;
   return LGS_OK;
 }
 
@@ -1212,27 +1359,29 @@ LGS_API lgs_status lgs_debug_tile_keys(lgs_ctx* ctx, const lgs_saved* t, uint64_
   if (!ctx || !t) return fail(LGS_EINVAL, "NULL argument");
   LGS_CUDA(cudaSetDevice(ctx->device));
   cudaStream_t s = ctx->stream;
-  const size_t P = (size_t)t->pairs, n = (size_t)t->dm.n;
-  std::vector<uint16_t> k16(P);
-  std::vector<uint32_t> v32(P);
+  const size_t nv = (size_t)t->vals_count, n = (size_t)t->dm.n;
+  std::vector<uint32_t> v32(nv);
   std::vector<float4> r0(n);
   std::vector<uint2> rg((size_t)t->ntiles);
-  if (P) {
-    if (t->keys) LGS_CUDA(cudaMemcpyAsync(k16.data(), t->keys, sizeof(uint16_t) * P, cudaMemcpyDeviceToHost, s));
-    LGS_CUDA(cudaMemcpyAsync(v32.data(), t->vals, sizeof(uint32_t) * P, cudaMemcpyDeviceToHost, s));
-  }
+  if (nv) LGS_CUDA(cudaMemcpyAsync(v32.data(), t->vals, sizeof(uint32_t) * nv, cudaMemcpyDeviceToHost, s));
   if (n) LGS_CUDA(cudaMemcpyAsync(r0.data(), t->vb.rec0, sizeof(float4) * n, cudaMemcpyDeviceToHost, s));
   LGS_CUDA(cudaMemcpyAsync(rg.data(), t->ranges, sizeof(uint2) * t->ntiles, cudaMemcpyDeviceToHost, s));
   LGS_CUDA(cudaStreamSynchronize(s));
-  if (ranges) std::memcpy(ranges, rg.data(), sizeof(uint2) * rg.size());
-  if (!t->keys)  // fast binning keeps no per-pair tile ids: they are implied by the ranges
-    for (size_t tt = 0; tt < rg.size(); ++tt)
-      for (uint32_t i = rg[tt].x; i < rg[tt].y; ++i) k16[i] = (uint16_t)tt;
-  for (size_t i = 0; i < P; ++i) {
-    uint32_t db;
-    std::memcpy(&db, &r0[v32[i]].z, 4);
-    if (keys) keys[i] = ((uint64_t)k16[i] << 32) | db;
-    if (vals) vals[i] = v32[i];
+  // tile lists concatenated in tile order (with the depth-layered binning the lists of saturated
+  // tiles are prefixes and the regions of the two passes are not contiguous)
+  size_t o = 0;
+  for (size_t tt = 0; tt < rg.size(); ++tt) {
+    const uint32_t b = (uint32_t)o;
+    for (uint32_t i = rg[tt].x; i < rg[tt].y; ++i, ++o) {
+      uint32_t db;
+      std::memcpy(&db, &r0[v32[i]].z, 4);
+      if (keys) keys[o] = ((uint64_t)tt << 32) | db;
+      if (vals) vals[o] = v32[i];
+    }
+    if (ranges) {
+      ranges[2 * tt] = b;
+      ranges[2 * tt + 1] = (uint32_t)o;
+    }
   }
   return LGS_OK;
 }

@@ -27,6 +27,7 @@ struct TileLists {
   const uint2* ranges;     // [tiles] begin, end
   const uint32_t* order;   // [tiles] tile ids, longest list first (persistent scheduler)
   int* counter;            // scheduler slot counter (reset by the launcher)
+  const uint32_t* count = nullptr;  // device count of tiles in `order` (null: every tile)
 };
 
 // Longest-first tile order (binning_fast.cu): buckets by floor(log2(list length)).
@@ -52,6 +53,9 @@ struct FwdOut {
   const float* t_feat;
   float* cot;        // [H][W][4 + d]: g_rgb(3), g_depth, g_feat(d)
   double* loss;      // 1 double (atomic sum)
+  // depth-layered first pass: tiles not saturated by their (prefix) list are flagged here and get
+  // no loss / cotangents (the second pass renders them again on their complete lists)
+  uint32_t* unfinished = nullptr;
 };
 
 struct BwdIn {
@@ -88,17 +92,36 @@ void launch_tile_sort(uint16_t* keys_in, uint16_t* keys_out, uint32_t* vals_in, 
                       int64_t pairs, int tile_bits, void* temp, size_t temp_bytes, cudaStream_t s);
 void launch_ranges(const uint16_t* keys, int64_t pairs, int ntiles, uint2* ranges, cudaStream_t s);
 
-// Fast binning (stable counting sort by tile; binning.cu): writes the sorted list `vals` and the
-// per-tile `ranges` directly.  `cnt_sorted` holds tiles[idx_sorted[s]] (launch_scan_tiles'
-// scratch; overwritten), `incl` its inclusive scan; `scratch` must hold
-// fast_binning_scratch_bytes(cap, n, ntiles) and `vals` cap entries.  The pair count itself is read on
-// the device (`dev_pairs`), so the host never waits for it: if it exceeds `cap`, every tile list is
-// left empty and *dev_overflow = 1 (the host then re-runs with exact buffers).
+// Fast binning (stable counting sort by tile; binning_fast.cu): writes the sorted lists into
+// vals[base ..] and the per-tile `ranges` directly.  The pass's pair count is read on the device
+// (`dev_pairs`), so the host never waits for it: if it exceeds `cap`, the pass's tile lists are left
+// empty and *dev_overflow = 1 (the host then re-runs with exact buffers).  `scratch` must hold
+// fast_binning_scratch_bytes(cap, gauss_cap, ntiles).
+struct BinPass {
+  const uint32_t* incl;       // inclusive pair counts of the depth-ordered Gaussians (this pass)
+  const uint32_t* dev_pairs;  // this pass's pair count (device; = incl[n - 1])
+  int64_t gauss_cap;          // upper bound on the Gaussians owning pairs in this pass
+  uint32_t cap;               // list capacity of this pass
+  uint32_t base;              // first list slot of this pass in vals
+  const uint32_t* mask;       // tiles binned by this pass (null: all; else only ranges of masked tiles)
+  const uint32_t* active = nullptr;  // with a mask: device count of masked tiles (0: the pass is a no-op)
+  const uint32_t* clamp = nullptr;   // device pair total the inclusive counts are clamped at (layer A)
+};
 bool fast_binning_supported(int ntiles);
-size_t fast_binning_scratch_bytes(int64_t cap, int64_t n, int ntiles);
-void launch_fast_binning(const ViewBufs& v, const uint32_t* idx_sorted, uint32_t* cnt_sorted, const uint32_t* incl,
-                         int64_t n, int ntiles, int tiles_x, uint32_t* scratch, uint32_t* vals, uint2* ranges,
-                         uint32_t cap, const uint32_t* dev_pairs, uint32_t* dev_overflow, cudaStream_t s);
+size_t fast_binning_scratch_bytes(int64_t cap, int64_t gauss_cap, int ntiles);
+void launch_fast_binning(const ViewBufs& v, const uint32_t* idx_sorted, int64_t n, int ntiles, int tiles_x,
+                         const BinPass& bp, uint32_t* scratch, uint32_t* vals, uint2* ranges, uint32_t* dev_overflow,
+                         cudaStream_t s);
+// Depth-layered binning (binning_fast.cu): layer A = the depth-order prefix owning ~P / div pairs
+// (at most gauss_cap Gaussians), then the complete lists of the tiles layer A left unsaturated.
+size_t layer_a_cap(int64_t pairs_cap, int ntiles, uint32_t div);
+void launch_layer_cut(const uint32_t* incl, int64_t n, uint32_t div, int64_t gauss_cap, uint32_t* pa,
+                      cudaStream_t s);
+void launch_layer_prep(const uint32_t* unfinished, const uint2* ranges, int tiles_x, int tiles_y, uint32_t* sat,
+                       uint32_t* order2, uint32_t* count2, uint32_t* total2, const cudaGraphConditionalHandle* cond,
+                       cudaStream_t s);
+void launch_layer_count(const ViewBufs& v, const uint32_t* idx_sorted, int64_t n, int tiles_x, const uint32_t* sat,
+                        const uint32_t* count2, uint32_t* cnt_enum, uint32_t* total2, cudaStream_t s);
 
 void launch_blend_fwd(const DevMap& m, const DevCam& c, const ViewBufs& v, const TileLists& tl,
                       const PixelState& ps, const FwdOut& o, cudaStream_t s);

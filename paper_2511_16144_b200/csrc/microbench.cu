@@ -39,7 +39,49 @@ __global__ void ffma_peak_kernel(float* out, int iters, float a, float b) {
   if (s == 12345.678f) out[0] = s;  // keep the chains alive
 }
 
+// legacy-path (mma.sync, SASS HMMA) TF32 throughput: 8 independent m16n8k8 chains per warp
+__global__ void mma_peak_kernel(float* out, int iters) {
+  uint32_t a[4], b[2];
+  for (int i = 0; i < 4; ++i) a[i] = lgs::to_tf32(1e-3f * (threadIdx.x + i));
+  for (int i = 0; i < 2; ++i) b[i] = lgs::to_tf32(1e-3f * (threadIdx.x - i));
+  float d[8][4] = {};
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) lgs::mma_tf32(d[k], a, b);
+  }
+  float s = 0.f;
+  for (int k = 0; k < 8; ++k) s += d[k][0] + d[k][1] + d[k][2] + d[k][3];
+  if (s == 12345.678f) out[0] = s;
+}
+
 }  // namespace
+
+// Legacy tensor-core (mma.sync m16n8k8 TF32) throughput of this device, TFLOP/s.
+extern "C" LGS_API lgs_status lgs_measure_mma_tf32_peak(int32_t device, double* tflops) {
+  if (!tflops) return LGS_EINVAL;
+  if (cudaSetDevice(device) != cudaSuccess) return LGS_ECUDA;
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  float* out = nullptr;
+  if (cudaMalloc(&out, sizeof(float)) != cudaSuccess) return LGS_ENOMEM;
+  const int threads = 256, blocks = sms * 4, iters = 2048;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  mma_peak_kernel<<<blocks, threads>>>(out, 16);
+  cudaEventRecord(e0);
+  mma_peak_kernel<<<blocks, threads>>>(out, iters);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  const double flops = 2.0 * 16 * 8 * 8 * 8.0 * iters * (double)(threads / 32) * blocks;
+  *tflops = flops / (ms * 1e-3) / 1e12;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(out);
+  return cudaGetLastError() == cudaSuccess ? LGS_OK : LGS_ECUDA;
+}
 
 extern "C" LGS_API lgs_status lgs_debug_mma_selftest(int32_t device, const float* a16x8, const float* b8x8,
                                                      float* d16x8, int32_t split) {

@@ -93,7 +93,7 @@ class Context:
     the context a private non-blocking stream (independent host threads rendering concurrently,
     the reference's "concurrent renders between map mutations" contract)."""
 
-    def __init__(self, device: int = 0, stream=None):
+    def __init__(self, device: int = 0, stream=None, full_lists: bool = False):
         L = _lib.load()
         if stream == "own":
             stream = None
@@ -106,6 +106,8 @@ class Context:
         check(L.lgs_ctx_create(device, C.c_void_p(stream) if stream else None, C.byref(h)))
         self.h = h
         self.device = device
+        if full_lists:  # complete (tile, Gaussian) lists instead of the depth-layered binning
+            check(L.lgs_ctx_set_full_tile_lists(h, 1))
 
     def synchronize(self):
         check(_lib.load().lgs_ctx_synchronize(self.h))
@@ -195,7 +197,7 @@ class RenderOutput:
     def stats(self):
         s = _lib.LgsRenderStats()
         check(_lib.load().lgs_saved_stats(self.tape, C.byref(s)))
-        return dict(visible=s.visible, pairs=s.pairs, tiles=s.tiles, max_tile_list=s.max_tile_list)
+        return dict(visible=s.visible, pairs=s.pairs, tiles=s.tiles, max_tile_list=s.max_tile_list, listed=s.listed)
 
     def work(self):
         """(evaluated (pixel, Gaussian) pairs, contributing pairs) of this forward."""
@@ -221,12 +223,12 @@ class RenderOutput:
     def tile_keys(self):
         """(keys u64 = tile << 32 | f32bits(depth), vals u32 map index, ranges [tiles, 2])."""
         st = self.stats()
-        keys = np.zeros(max(st["pairs"], 1), np.uint64)
-        vals = np.zeros(max(st["pairs"], 1), np.uint32)
+        keys = np.zeros(max(st["listed"], 1), np.uint64)
+        vals = np.zeros(max(st["listed"], 1), np.uint32)
         ranges = np.zeros((st["tiles"], 2), np.uint32)
         check(_lib.load().lgs_debug_tile_keys(self.ctx.h, self.tape, keys.ctypes.data, vals.ctypes.data,
                                               ranges.ctypes.data))
-        return keys[:st["pairs"]], vals[:st["pairs"]], ranges
+        return keys[:st["listed"]], vals[:st["listed"]], ranges
 
     def pixel_state(self):
         H, W = self.camera.height, self.camera.width

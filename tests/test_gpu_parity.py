@@ -52,8 +52,9 @@ def _projected_equal(gp, op):
 @pytest.mark.parametrize("name,n", [("c0", None), ("c1", 50_000), ("c2", 50_000), ("c4", 60_000)])
 def test_preprocess_and_keys_bit_exact(oracle, name, n):
     scene, cams, info = scenes.make_config(name, n=n)
+    ctx = R.Context(0, full_lists=True)
     for cam in cams[:3]:
-        out = R.render(dev_scene(scene), cam)
+        out = R.render(dev_scene(scene), cam, ctx=ctx)
         torch.cuda.synchronize()
         gp = out.projected()
         op = oracle.preprocess_f32(scene, cam)
@@ -343,7 +344,7 @@ def test_feature_dims(oracle, d):
 def test_ragged_image_sizes(oracle, W, H):
     scene, cams, info = scenes.make_config("c0", n=2000)
     cam = dict(cams[0], width=W, height=H, cx=W / 2, cy=H / 2)
-    out = R.render(dev_scene(scene), cam)
+    out = R.render(dev_scene(scene), cam, ctx=R.Context(0, full_lists=True))
     ref, _ = _oracle_fwd_bwd(oracle, scene, cam)
     frac, mx = image_mismatch(out.rgb, ref.rgb)
     assert frac < 1e-3, mx
@@ -382,11 +383,11 @@ def test_speculative_pair_capacity(oracle):
     ds, db = dev_scene(small), dev_scene(big)
 
     def fresh(scene, cam):
-        out = R.render(scene, cam, ctx=R.Context(0))
+        out = R.render(scene, cam, ctx=R.Context(0, full_lists=True))
         torch.cuda.synchronize()
         return out
 
-    ctx = R.Context(0)
+    ctx = R.Context(0, full_lists=True)
     first = R.render(ds, scams[0], ctx=ctx)          # exact (first render on ctx)
     over = R.render(db, bcams[0], ctx=ctx)           # capacity from the small view: overflow -> re-bin
     again = R.render(ds, scams[0], ctx=ctx)          # speculative, capacity now ample
@@ -417,7 +418,7 @@ def test_depth_order_ties_and_big_buckets(oracle):
     pos[3000:4500, 2] = base + (np.arange(1500) % 7).astype(np.float32) * np.spacing(base)
     scene = dict(scene, pos=pos)
     cam = cams[0]
-    out = R.render(dev_scene(scene), cam, ctx=R.Context(0))
+    out = R.render(dev_scene(scene), cam, ctx=R.Context(0, full_lists=True))
     torch.cuda.synchronize()
     keys, vals, ranges = out.tile_keys()
     op = oracle.preprocess_f32(scene, cam)
@@ -425,10 +426,74 @@ def test_depth_order_ties_and_big_buckets(oracle):
     assert np.array_equal(keys, okeys) and np.array_equal(vals, ovals) and np.array_equal(ranges, oranges)
     os.environ["LGS_DEPTH_SORT"] = "cub"
     try:
-        ref = R.render(dev_scene(scene), cam, ctx=R.Context(0))
+        ref = R.render(dev_scene(scene), cam, ctx=R.Context(0, full_lists=True))
         torch.cuda.synchronize()
     finally:
         del os.environ["LGS_DEPTH_SORT"]
     for a, b in zip(out.tile_keys(), ref.tile_keys()):
         assert np.array_equal(a, b)
     assert torch.equal(out.rgb, ref.rgb)
+
+
+def _layered_vs_full(scene, cam, tg):
+    ds = dev_scene(scene)
+    dtg = {k: torch.from_numpy(v).cuda() for k, v in tg.items()}
+    res = []
+    for full in (False, True):
+        ctx = R.Context(0, full_lists=full)
+        out = R.render(ds, cam, targets=dtg, ctx=ctx)
+        g = R.render_backward_l1(out, pose=True)
+        torch.cuda.synchronize()
+        res.append((out, g))
+    (lo, lg), (fo, fg) = res
+    for k in ("rgb", "depth", "feat", "acc"):
+        assert torch.equal(getattr(lo, k), getattr(fo, k)), k
+    assert abs(lo.l1_loss() - fo.l1_loss()) <= 1e-7 * abs(fo.l1_loss())  # fp32 per-CTA partials, atomic order
+    # gradients: the same sums, accumulated by fp32 atomics in a different order (the same bound
+    # as two runs of one mode; the pose gradient, a sum over every splat with large cancellation
+    # on near-camera splats, varies by a few % between two identical runs on c2)
+    for k in GROUPS:
+        frac, worst = grad_mismatch(lg[k], fg[k])
+        assert frac < 1e-3, (k, frac, worst)
+    lk, lv, lr = lo.tile_keys()
+    fk, fv, fr = fo.tile_keys()
+    ft, nc = fo.pixel_state()
+    lst, fst = lo.stats(), fo.stats()
+    assert lst["pairs"] == fst["pairs"] == fst["listed"] and lst["listed"] <= fst["listed"]
+    H, W = cam["height"], cam["width"]
+    for t in range(lr.shape[0]):  # every layered list is a prefix of the complete list ...
+        a = lv[lr[t, 0]:lr[t, 1]]
+        b = fv[fr[t, 0]:fr[t, 1]]
+        assert np.array_equal(a, b[:a.size]), t
+        if a.size < b.size:  # ... cut only where every pixel of the tile saturated within it
+            ty, tx = divmod(t, (W + 15) // 16)
+            blk = ft[ty * 16:ty * 16 + 16, tx * 16:tx * 16 + 16]
+            assert (blk < 1e-4).all(), t
+            assert nc[ty * 16:ty * 16 + 16, tx * 16:tx * 16 + 16].max() <= a.size
+    return lst, fst
+
+
+@pytest.mark.parametrize("name,n", [("c1", 60_000), ("c0", None), ("c2", 60_000)])
+def test_layered_binning_matches_full_lists(name, n):
+    """Depth-layered binning (default) against complete lists: bitwise-identical images and loss,
+    gradients equal up to atomic-accumulation order; every list a prefix of the complete one, truncated only on saturated tiles.  c0
+    (sparse: most tiles never saturate) exercises the second pass on most tiles, c1 on few."""
+    scene, cams, info = scenes.make_config(name, n=n)
+    cam = cams[0]
+    tg = scenes.make_targets(cam, scene["feat"].shape[0], info["depth_range"], 3)
+    _layered_vs_full(scene, cam, tg)
+
+
+def test_layered_binning_mixed_saturation():
+    """Half the image covered by a dense near wall of splats (saturates on layer A), the other half
+    by sparse far splats (second pass): both passes in one frame."""
+    scene, cams, info = scenes.make_config("c1", n=40_000)
+    cam = dict(cams[0], width=320, height=240, cx=160.0, cy=120.0, fx=288.8, fy=288.8)
+    pos = scene["pos"].copy()
+    left = pos[:, 0] < 0
+    pos[left, 2] = 0.6 + 0.4 * (pos[left, 2] - 0.5) / 5.5  # dense, near
+    keep = left | (np.arange(pos.shape[0]) % 20 == 0)       # right half: 1 in 20 kept, far
+    scene = {k: (v[:, keep] if k == "feat" else v[keep]) for k, v in dict(scene, pos=pos).items()}
+    tg = scenes.make_targets(cam, scene["feat"].shape[0], info["depth_range"], 5)
+    lst, fst = _layered_vs_full(scene, cam, tg)
+    assert lst["listed"] < fst["listed"]

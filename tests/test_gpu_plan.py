@@ -16,8 +16,8 @@ from paper_2511_16144_b200 import scenes  # noqa: E402
 from tests.parity import GROUPS, grad_mismatch  # noqa: E402
 
 
-def _setup(n=30_000):
-    scene, cams, info = scenes.make_config("c1", n=n)
+def _setup(n=30_000, name="c1"):
+    scene, cams, info = scenes.make_config(name, n=n)
     cam = cams[0]
     ctx = R.Context(0)
     dm = R.DeviceMap({k: torch.from_numpy(v).cuda() for k, v in scene.items()}, ctx)
@@ -91,3 +91,23 @@ def test_plan_set_camera():
     plan.sync()
     out, g = _eager(dm, cam2, tg)
     _check(grads, pose, imgs, out, g)
+
+
+@pytest.mark.parametrize("name", ["c0", "c1"])
+def test_plan_layered_second_pass_toggles(name):
+    """The second pass of the depth-layered binning is a conditional node of the captured graph:
+    a replay where tiles stay unsaturated (tiny, faint splats) runs it, a dense one skips it; both
+    must reproduce the eager results."""
+    scene, cam, ctx, dm, tg = _setup(n=20_000, name=name)
+    grads = R.alloc_grads(dm.n, dm.d, dm.K, device=0)
+    imgs = _images(cam, dm.d)
+    pose = torch.zeros(6, dtype=torch.float32, pin_memory=True)
+    plan = R.Plan(dm, cam, tg, grads, images=imgs, pose_out=pose)
+    sparse = dict(scene, log_s=(scene["log_s"] - 0.5).astype(np.float32),
+                  opac=(scene["opac"] - 2.0).astype(np.float32))
+    for sc in (sparse, scene, sparse):
+        dm.update({k: torch.from_numpy(v).cuda() for k, v in sc.items()})
+        plan.run()
+        plan.sync()
+        out, g = _eager(dm, cam, tg)
+        _check(grads, pose, imgs, out, g)
