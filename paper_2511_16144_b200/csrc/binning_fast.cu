@@ -356,40 +356,20 @@ void launch_fast_binning(const ViewBufs& v, const uint32_t* idx_sorted, int64_t 
 // dense map every tile saturates on its nearest few hundred splats: at the headline config all 1200
 // tiles are saturated by the nearest 0.4% of the visible Gaussians, whose lists hold ~5% of the
 // 7.6M pairs.  So the lists are built in two passes:
-//   1. layer A = the depth-order prefix owning ~P / kLayerDiv pairs: binned for every tile and
-//      blended; a tile whose every pixel saturates is final (its list is an exact prefix of the
-//      complete list, and no later Gaussian can change any of its pixels or gradients);
+//   1. layer A = the depth-order prefix owning ~P / kLayerDiv pairs (depth_order.cu orders only
+//      these and builds their per-tile lists: one warp per tile compacts the candidates in
+//      order), blended for every tile; a tile whose every pixel saturates is final (its list is an
+//      exact prefix of the complete list, and no later Gaussian can change any of its pixels or
+//      gradients);
 //   2. the complete lists of the remaining (unfinished) tiles only: the Gaussians' counts are
 //      restricted to those tiles through a summed-area table of the unfinished-tile mask, binned
 //      after layer A's lists, then blended again from scratch.
 // Images, gradients and every list entry a kernel reads are identical to the single-pass binning.
 // ------------------------------------------------------------------------------------------
-constexpr uint32_t kLayerMinPairs = 1u << 16;
-
-// P_A = the pair total of layer A: the depth-order prefix up to the first Gaussian whose inclusive
-// count reaches max(min(P, kLayerMinPairs), P / div), at most gauss_cap Gaussians.  One thread per
-// candidate position; exactly one finds the crossing and writes P_A.
-__global__ void layer_cut_kernel(const uint32_t* __restrict__ incl, int64_t n, uint32_t div, int64_t gauss_cap,
-                                 uint32_t* __restrict__ pa) {
-  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t last = (gauss_cap < n ? gauss_cap : n) - 1;
-  if (s > last) return;
-  const uint32_t P = incl[n - 1];
-  const uint32_t target = max(min(P, kLayerMinPairs), P / div);
-  const uint32_t v = incl[s];
-  const bool crossing = v >= target && (s == 0 || incl[s - 1] < target);
-  if (crossing || (s == last && v < target)) *pa = v;
-}
-
 size_t layer_a_cap(int64_t pairs_cap, int ntiles, uint32_t div) {
   return (size_t)std::max<int64_t>(std::min<int64_t>(pairs_cap, kLayerMinPairs), pairs_cap / div) + ntiles + 1024;
 }
 
-void launch_layer_cut(const uint32_t* incl, int64_t n, uint32_t div, int64_t gauss_cap, uint32_t* pa, cudaStream_t s) {
-  if (n == 0) return;
-  const int64_t m = std::min(n, gauss_cap);
-  layer_cut_kernel<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(incl, n, div, gauss_cap, pa);
-}
 
 // One CTA: unfinished-tile summed-area table sat[(ty + 1) * (tiles_x + 1) + tx + 1], the unfinished
 // tiles in longest-list-first order (order2, count2) and, inside a captured plan, the conditional

@@ -54,7 +54,7 @@ __device__ __forceinline__ int next_tile(const TileLists& tl, int ntiles, int* s
   __syncthreads();
   const int slot = *s_slot;
   const int active = tl.count ? (int)*tl.count : ntiles;
-  return slot < active ? (int)tl.order[slot] : -1;
+  return slot < active ? (tl.order ? (int)tl.order[slot] : slot) : -1;
 }
 
 }  // namespace lgs

@@ -23,6 +23,7 @@
 // Roofline: HBM/L2 latency; ~(4 + 4) B read + written per Gaussian per step, ~20 B in total.
 #include <cub/device/device_scan.cuh>
 
+#include <algorithm>
 #include <cstring>
 
 #include "lgs_internal.cuh"
@@ -40,10 +41,17 @@ __device__ __forceinline__ uint32_t depth_bucket(uint32_t key, uint32_t base) {
   return b > base ? min(b - base, (uint32_t)kDepthBuckets - 1u) : 0u;
 }
 
-// Culled Gaussians all share one bucket: their slots are handed out per CTA (shared-memory
-// counter + one global atomic) instead of one global atomic each on a single address.
-__global__ void __launch_bounds__(256) depth_hist_kernel(const uint32_t* __restrict__ dkey, int64_t n, uint32_t base,
-                                                         uint32_t* __restrict__ hist, uint32_t* __restrict__ slot) {
+// Per bucket one u64: Gaussians << 32 | their tile pairs (the depth-layered binning cuts at a
+// bucket boundary by pairs); one 64-bit atomic per Gaussian returns its slot in the high word.
+// Culled Gaussians all share one bucket: their slots are handed out per CTA (shared-memory counter
+// + one global atomic) instead of one global atomic each on one address.
+typedef unsigned long long u64;
+__device__ __forceinline__ uint32_t cnt_of(u64 v) { return (uint32_t)(v >> 32); }
+__device__ __forceinline__ uint32_t prs_of(u64 v) { return (uint32_t)(v & 0xffffffffull); }
+
+__global__ void __launch_bounds__(256) depth_hist_kernel(const uint32_t* __restrict__ dkey,
+                                                         const uint32_t* __restrict__ tiles, int64_t n, uint32_t base,
+                                                         u64* __restrict__ hist, uint32_t* __restrict__ slot) {
   __shared__ uint32_t s_culled, s_base;
   if (threadIdx.x == 0) s_culled = 0;
   __syncthreads();
@@ -52,64 +60,120 @@ __global__ void __launch_bounds__(256) depth_hist_kernel(const uint32_t* __restr
   if (i < n) {
     b = depth_bucket(dkey[i], base);
     if (b == kDepthBuckets) local = atomicAdd(&s_culled, 1u);
-    else slot[i] = atomicAdd(hist + b, 1u);
+    else slot[i] = cnt_of(atomicAdd(hist + b, (1ull << 32) | tiles[i]));
   }
   __syncthreads();
-  if (threadIdx.x == 0 && s_culled) s_base = atomicAdd(hist + kDepthBuckets, s_culled);
+  if (threadIdx.x == 0 && s_culled) s_base = cnt_of(atomicAdd(hist + kDepthBuckets, (u64)s_culled << 32));
   __syncthreads();
   if (i < n && b == kDepthBuckets) slot[i] = s_base + local;
 }
 
+// Layer A of the depth-layered binning = buckets [0, cut[0]): the smallest bucket prefix whose
+// pairs reach max(min(P, min_pairs), P / div), shortened to at most gauss_cap Gaussians and cap_a
+// pairs.  cut[0] is pre-set to ~0 and lowered with atomicMin by the (unique) threads that find the
+// crossing / the last feasible bucket.
+__global__ void depth_cut_kernel(const u64* __restrict__ off, uint32_t div, uint32_t min_pairs, int64_t gauss_cap,
+                                 uint32_t cap_a, uint32_t* __restrict__ cut) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= kDepthBuckets) return;
+  const uint32_t P = prs_of(off[kDepthBuckets]);
+  const uint32_t target = max(min(P, min_pairs), P / div);
+  const u64 ex = off[b], in = off[b + 1];
+  if (prs_of(in) >= target && prs_of(ex) < target) atomicMin(cut, (uint32_t)b + 1u);
+  const bool feas = (int64_t)cnt_of(in) <= gauss_cap && prs_of(in) <= cap_a;
+  if (b == 0 && !feas) atomicMin(cut, 0u);
+  if (feas) {
+    bool next_feas = false;
+    if (b + 1 < kDepthBuckets) {
+      const u64 in2 = off[b + 2];
+      next_feas = (int64_t)cnt_of(in2) <= gauss_cap && prs_of(in2) <= cap_a;
+    }
+    if (!next_feas) atomicMin(cut, (uint32_t)b + 1u);
+  }
+}
+
+enum { kDepthAll = 0, kDepthLayerA = 1, kDepthRest = 2 };
+
+__device__ __forceinline__ bool bucket_selected(uint32_t b, int mode, uint32_t cut_end) {
+  return mode == kDepthAll || (mode == kDepthLayerA ? b < cut_end : b >= cut_end);
+}
+
 __global__ void depth_scatter_kernel(const uint32_t* __restrict__ dkey, int64_t n, uint32_t base,
-                                     const uint32_t* __restrict__ off, const uint32_t* __restrict__ slot,
-                                     uint2* __restrict__ tmp) {
+                                     const u64* __restrict__ off, const uint32_t* __restrict__ slot,
+                                     const uint32_t* __restrict__ cut, int mode, uint2* __restrict__ tmp,
+                                     uint32_t* __restrict__ ra_out) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i == 0 && ra_out) *ra_out = cnt_of(off[*cut]);  // R_A: Gaussians in layer A
   if (i >= n) return;
   const uint32_t k = dkey[i];
-  tmp[off[depth_bucket(k, base)] + slot[i]] = make_uint2(k, (uint32_t)i);
+  const uint32_t b = depth_bucket(k, base);
+  if (!bucket_selected(b, mode, cut ? *cut : 0u)) return;
+  tmp[cnt_of(off[b]) + slot[i]] = make_uint2(k, (uint32_t)i);
 }
 
 __device__ __forceinline__ bool precedes(uint2 a, uint2 b) { return a.x < b.x || (a.x == b.x && a.y < b.y); }
 
-// big[0] = number of big buckets, big[1 ..] their ids; big_cursor = scratch entries handed out
+// tile rect (tx0 | tx1 << 16, ty0 | ty1 << 16) of a pixel rect, for the forward's candidate scan
+__device__ __forceinline__ uint2 tile_rect(uint2 rc) {
+  return make_uint2(((rc.x & 0xffffu) / kTile) | (((rc.x >> 16) / kTile) << 16),
+                    ((rc.y & 0xffffu) / kTile) | (((rc.y >> 16) / kTile) << 16));
+}
+
+struct DepthOut {
+  uint32_t* idx_sorted;  // [n] map index in (depth, index) order (culled last, any order)
+  uint32_t* cnt_sorted;  // [n] or null: tile counts in that order
+  uint2* cand_rect;      // [n] or null: tile rects in that order (positions < R_A)
+};
+
+__device__ __forceinline__ void depth_emit(const DepthOut& o, const uint32_t* __restrict__ tiles,
+                                           const uint2* __restrict__ rect, uint32_t pos, uint32_t g,
+                                           uint32_t cand_end) {
+  o.idx_sorted[pos] = g;
+  if (o.cnt_sorted) o.cnt_sorted[pos] = tiles[g];
+  if (o.cand_rect && pos < cand_end) o.cand_rect[pos] = tile_rect(rect[g]);
+}
+
+// big[0] = number of big buckets, big[1 ..] their ids
 __global__ void depth_rank_kernel(const uint2* __restrict__ tmp, int64_t n, uint32_t base,
-                                  const uint32_t* __restrict__ off, const uint32_t* __restrict__ tiles,
-                                  uint32_t* __restrict__ idx_sorted, uint32_t* __restrict__ cnt_sorted,
-                                  uint32_t* __restrict__ big) {
-  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= n) return;
+                                  const u64* __restrict__ off, const uint32_t* __restrict__ tiles,
+                                  const uint2* __restrict__ rect, const uint32_t* __restrict__ cut, int mode,
+                                  DepthOut o, uint32_t* __restrict__ big) {
+  const int64_t p0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t ra = cut ? cnt_of(off[*cut]) : 0u;  // Gaussians in layer A
+  const int64_t p = mode == kDepthRest ? p0 + ra : p0;
+  if (p >= (mode == kDepthLayerA ? (int64_t)ra : n)) return;
   const uint2 me = tmp[p];
   const uint32_t b = depth_bucket(me.x, base);
   if (b == kDepthBuckets) {  // culled: no pairs, any order
-    idx_sorted[p] = me.y;
-    cnt_sorted[p] = 0u;
+    o.idx_sorted[p] = me.y;
+    if (o.cnt_sorted) o.cnt_sorted[p] = 0u;
     return;
   }
-  const uint32_t lo = off[b], hi = off[b + 1];
+  const uint32_t lo = cnt_of(off[b]), hi = cnt_of(off[b + 1]);
   if (hi - lo > kMaxRankBucket) {
     if (p == lo) big[1 + atomicAdd(big, 1u)] = b;
     return;
   }
   uint32_t rank = 0;
   for (uint32_t q = lo; q < hi; ++q) rank += precedes(tmp[q], me) ? 1u : 0u;
-  idx_sorted[lo + rank] = me.y;
-  cnt_sorted[lo + rank] = tiles[me.y];
+  depth_emit(o, tiles, rect, lo + rank, me.y, ra);
 }
 
 // One CTA per big bucket: bitonic sort of the padded composite keys in `scratch` (2 n entries:
 // the padded sizes of all big buckets sum to less than twice their element count).
-__global__ void __launch_bounds__(1024) depth_big_kernel(const uint2* __restrict__ tmp, const uint32_t* __restrict__ off,
+__global__ void __launch_bounds__(1024) depth_big_kernel(const uint2* __restrict__ tmp, const u64* __restrict__ off,
                                                          const uint32_t* __restrict__ tiles,
+                                                         const uint2* __restrict__ rect,
+                                                         const uint32_t* __restrict__ cut,
                                                          const uint32_t* __restrict__ big,
                                                          unsigned long long* __restrict__ scratch,
-                                                         uint32_t* __restrict__ cursor,
-                                                         uint32_t* __restrict__ idx_sorted,
-                                                         uint32_t* __restrict__ cnt_sorted) {
+                                                         uint32_t* __restrict__ cursor, DepthOut o) {
   const uint32_t nbig = big[0];
+  const uint32_t ra = cut ? cnt_of(off[*cut]) : 0u;
   __shared__ uint32_t s_base;
   for (uint32_t k = blockIdx.x; k < nbig; k += gridDim.x) {
     const uint32_t b = big[1 + k];
-    const uint32_t lo = off[b], m = off[b + 1] - lo;
+    const uint32_t lo = cnt_of(off[b]), m = cnt_of(off[b + 1]) - lo;
     uint32_t M = 1;
     while (M < m) M <<= 1;
     __syncthreads();
@@ -141,58 +205,185 @@ __global__ void __launch_bounds__(1024) depth_big_kernel(const uint2* __restrict
         __syncthreads();
       }
     }
-    for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
-      const uint32_t g = (uint32_t)(a[i] & 0xffffffffull);
-      idx_sorted[lo + i] = g;
-      cnt_sorted[lo + i] = tiles[g];
-    }
+    for (uint32_t i = threadIdx.x; i < m; i += blockDim.x)
+      depth_emit(o, tiles, rect, lo + i, (uint32_t)(a[i] & 0xffffffffull), ra);
   }
 }
 
-size_t depth_order_temp_bytes(int64_t n) {
+// ------------------------------------------------------------------------------------------
+// host side: one scratch block carved into the buffers below (DepthOrderState keeps the carving
+// so the second layered pass can finish the order later)
+// ------------------------------------------------------------------------------------------
+static size_t align_words(size_t w) { return (w + 63) & ~size_t(63); }
+
+static size_t scan_bytes_for() {
   size_t scan = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, scan, (uint32_t*)nullptr, (uint32_t*)nullptr, kDepthBuckets + 2);
-  const size_t words = 2 * (size_t)(kDepthBuckets + 2)  // hist, off
-                       + (size_t)n                      // slot
-                       + 2 * (size_t)n                  // tmp (uint2)
-                       + 4 * (size_t)n                  // scratch (2n u64)
-                       + (size_t)n / kMaxRankBucket + 2 // big list
-                       + 2;                             // cursor
-  return sizeof(uint32_t) * (words + 8 * 64) + scan + 1024;  // + per-region 256 B alignment
+  cub::DeviceScan::ExclusiveSum(nullptr, scan, (unsigned long long*)nullptr, (unsigned long long*)nullptr,
+                                kDepthBuckets + 2);
+  return scan;
 }
 
-static uint32_t* align256(uint8_t* p) {
-  return reinterpret_cast<uint32_t*>((reinterpret_cast<uintptr_t>(p) + 255) & ~uintptr_t(255));
+size_t depth_order_temp_bytes(int64_t n) {
+  const size_t nn = align_words((size_t)n);
+  const size_t words = 2 * 2 * align_words(kDepthBuckets + 2)  // hist, off (u64)
+                       + nn                                     // slot
+                       + 2 * nn                                 // tmp (uint2)
+                       + 4 * nn                                 // scratch (2n u64)
+                       + align_words((size_t)n / kMaxRankBucket + 2) * 2  // big lists (layer A, rest)
+                       + 64 * 3;                                // cursor, cut
+  return sizeof(uint32_t) * words + scan_bytes_for() + 1024;
 }
 
-void launch_depth_order(const ViewBufs& v, int64_t n, float near_plane, void* temp, size_t temp_bytes,
-                        uint32_t* idx_sorted, uint32_t* cnt_sorted, cudaStream_t s) {
-  if (n == 0) return;
-  const int nb = kDepthBuckets + 1;  // + culled bucket
-  uint32_t* hist = align256(static_cast<uint8_t*>(temp));
-  uint32_t* off = hist + ((nb + 1 + 63) & ~63);
-  uint32_t* slot = off + ((nb + 1 + 63) & ~63);
-  uint2* tmp = reinterpret_cast<uint2*>(slot + ((n + 63) & ~63ll));
-  unsigned long long* scratch = reinterpret_cast<unsigned long long*>(tmp + ((n + 63) & ~63ll));
-  uint32_t* big = reinterpret_cast<uint32_t*>(scratch + 2 * ((n + 63) & ~63ll));
-  uint32_t* cursor = big + ((n / kMaxRankBucket + 2 + 63) & ~63ll);
-  void* scan_temp = align256(reinterpret_cast<uint8_t*>(cursor + 64));
-  size_t scan_bytes = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, hist, off, nb + 1);
+struct DepthCarve {
+  unsigned long long *hist, *off;
+  uint2* tmp;
+  uint32_t *slot, *big_a, *big_r, *cursor, *cut;
+  unsigned long long* scratch;
+  void* scan_temp;
+  size_t scan_bytes;
+  uint32_t base;
+};
+
+static DepthCarve carve(void* temp, int64_t n, float near_plane) {
+  DepthCarve c;
+  uint32_t* w = reinterpret_cast<uint32_t*>((reinterpret_cast<uintptr_t>(temp) + 255) & ~uintptr_t(255));
+  const size_t nn = align_words((size_t)n), nb = align_words(kDepthBuckets + 2);
+  c.hist = reinterpret_cast<unsigned long long*>(w);
+  w += 2 * nb;
+  c.off = reinterpret_cast<unsigned long long*>(w);
+  w += 2 * nb;
+  c.slot = w;
+  w += nn;
+  c.tmp = reinterpret_cast<uint2*>(w);
+  w += 2 * nn;
+  c.scratch = reinterpret_cast<unsigned long long*>(w);
+  w += 4 * nn;
+  const size_t nbig = align_words((size_t)n / kMaxRankBucket + 2);
+  c.big_a = w;
+  w += nbig;
+  c.big_r = w;
+  w += nbig;
+  c.cursor = w;
+  w += 64;
+  c.cut = w;
+  w += 128;
+  c.scan_temp = w;
+  c.scan_bytes = scan_bytes_for();
   // near plane in key space: depths are > near, so buckets start there (2^13 per octave)
   const float nearp = near_plane > 0.f ? near_plane : 0.f;
   uint32_t nbits;
   memcpy(&nbits, &nearp, sizeof(nbits));
-  const uint32_t base = nbits >> kDepthShift;
-  cudaMemsetAsync(hist, 0, sizeof(uint32_t) * (nb + 1), s);
-  cudaMemsetAsync(big, 0, sizeof(uint32_t), s);
-  cudaMemsetAsync(cursor, 0, sizeof(uint32_t), s);
+  c.base = nbits >> kDepthShift;
+  return c;
+}
+
+static void depth_front(const ViewBufs& v, int64_t n, const DepthCarve& c, cudaStream_t s) {
+  cudaMemsetAsync(c.hist, 0, sizeof(unsigned long long) * (kDepthBuckets + 2), s);
+  cudaMemsetAsync(c.big_a, 0, sizeof(uint32_t), s);
+  cudaMemsetAsync(c.big_r, 0, sizeof(uint32_t), s);
+  cudaMemsetAsync(c.cursor, 0, sizeof(uint32_t), s);
+  depth_hist_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(v.dkey, v.tiles, n, c.base, c.hist, c.slot);
+  size_t sb = c.scan_bytes;
+  cub::DeviceScan::ExclusiveSum(c.scan_temp, sb, c.hist, c.off, kDepthBuckets + 2, s);
+}
+
+void launch_depth_order(const ViewBufs& v, int64_t n, float near_plane, void* temp, size_t temp_bytes,
+                        uint32_t* idx_sorted, uint32_t* cnt_sorted, cudaStream_t s) {
+  (void)temp_bytes;
+  if (n == 0) return;
+  const DepthCarve c = carve(temp, n, near_plane);
+  depth_front(v, n, c, s);
   const unsigned grid = (unsigned)((n + 255) / 256);
-  depth_hist_kernel<<<grid, 256, 0, s>>>(v.dkey, n, base, hist, slot);
-  cub::DeviceScan::ExclusiveSum(scan_temp, scan_bytes, hist, off, nb + 1, s);
-  depth_scatter_kernel<<<grid, 256, 0, s>>>(v.dkey, n, base, off, slot, tmp);
-  depth_rank_kernel<<<grid, 256, 0, s>>>(tmp, n, base, off, v.tiles, idx_sorted, cnt_sorted, big);
-  depth_big_kernel<<<8, 1024, 0, s>>>(tmp, off, v.tiles, big, scratch, cursor, idx_sorted, cnt_sorted);
+  const DepthOut o{idx_sorted, cnt_sorted, nullptr};
+  depth_scatter_kernel<<<grid, 256, 0, s>>>(v.dkey, n, c.base, c.off, c.slot, nullptr, kDepthAll, c.tmp, nullptr);
+  depth_rank_kernel<<<grid, 256, 0, s>>>(c.tmp, n, c.base, c.off, v.tiles, v.rect, nullptr, kDepthAll, o, c.big_a);
+  depth_big_kernel<<<8, 1024, 0, s>>>(c.tmp, c.off, v.tiles, v.rect, nullptr, c.big_a, c.scratch, c.cursor, o);
+}
+
+void launch_depth_order_layer_a(const ViewBufs& v, int64_t n, float near_plane, void* temp, uint32_t div,
+                                uint32_t min_pairs, int64_t gauss_cap, uint32_t cap_a, uint32_t* idx_sorted,
+                                uint2* cand_rect, uint32_t* ra, cudaStream_t s) {
+  if (n == 0) {
+    cudaMemsetAsync(ra, 0, sizeof(uint32_t), s);
+    return;
+  }
+  const DepthCarve c = carve(temp, n, near_plane);
+  depth_front(v, n, c, s);
+  cudaMemsetAsync(c.cut, 0xff, sizeof(uint32_t), s);
+  depth_cut_kernel<<<(kDepthBuckets + 255) / 256, 256, 0, s>>>(c.off, div, min_pairs, gauss_cap, cap_a, c.cut);
+  const DepthOut o{idx_sorted, nullptr, cand_rect};
+  const int64_t ga = std::min<int64_t>(n, gauss_cap);
+  depth_scatter_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(v.dkey, n, c.base, c.off, c.slot, c.cut,
+                                                                    kDepthLayerA, c.tmp, ra);
+  depth_rank_kernel<<<(unsigned)((ga + 255) / 256), 256, 0, s>>>(c.tmp, n, c.base, c.off, v.tiles, v.rect, c.cut,
+                                                                  kDepthLayerA, o, c.big_a);
+  depth_big_kernel<<<8, 1024, 0, s>>>(c.tmp, c.off, v.tiles, v.rect, c.cut, c.big_a, c.scratch, c.cursor, o);
+}
+
+// Layer-A tile lists: one CTA per tile; its 8 warps split the R_A depth-ordered candidates into
+// contiguous segments, count those whose tile rect holds the tile, take their offsets from a
+// shared-memory prefix (one atomic reserves the tile's list), then write them with an
+// order-preserving ballot compaction -- each list is the exact depth-order prefix of the tile's
+// complete list.  R_A is ~0.5-5% of the visible Gaussians: ~2-16k coalesced 8-byte reads per tile,
+// from L2.
+constexpr int kListWarps = 8;
+
+__global__ void __launch_bounds__(kListWarps * 32) layer_tile_lists_kernel(
+    const uint2* __restrict__ cand_rect, const uint32_t* __restrict__ cand_idx, const uint32_t* __restrict__ ra,
+    int tiles_x, uint32_t* __restrict__ cursor, uint32_t* __restrict__ vals, uint2* __restrict__ ranges) {
+  __shared__ uint32_t s_cnt[kListWarps], s_base;
+  const int t = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t n_cand = *ra;
+  const uint32_t tx = (uint32_t)(t % tiles_x), ty = (uint32_t)(t / tiles_x);
+  const uint32_t seg = ((n_cand + kListWarps * 32 - 1) / (kListWarps * 32)) * 32;
+  const uint32_t c0 = min(n_cand, warp * seg), c1 = min(n_cand, c0 + seg);
+  auto covers = [&](uint32_t i) {
+    const uint2 tr = __ldg(cand_rect + i);
+    return tx >= (tr.x & 0xffffu) && tx <= (tr.x >> 16) && ty >= (tr.y & 0xffffu) && ty <= (tr.y >> 16);
+  };
+  uint32_t cnt = 0;
+#pragma unroll 4
+  for (uint32_t i = c0 + lane; i < c1; i += 32) cnt += covers(i) ? 1u : 0u;
+  cnt = __reduce_add_sync(0xffffffffu, cnt);
+  if (lane == 0) s_cnt[warp] = cnt;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t tot = 0;
+    for (int w = 0; w < kListWarps; ++w) {
+      const uint32_t c = s_cnt[w];
+      s_cnt[w] = tot;
+      tot += c;
+    }
+    s_base = atomicAdd(cursor, tot);
+    ranges[t] = make_uint2(s_base, s_base + tot);
+  }
+  __syncthreads();
+  uint32_t pos = s_base + s_cnt[warp];
+  for (uint32_t i0 = c0; i0 < c1; i0 += 32) {
+    const uint32_t i = i0 + lane;
+    const bool hit = i < c1 && covers(i);
+    const unsigned bal = __ballot_sync(0xffffffffu, hit);
+    if (hit) vals[pos + __popc(bal & ((1u << lane) - 1u))] = __ldg(cand_idx + i);
+    pos += __popc(bal);
+  }
+}
+
+void launch_layer_tile_lists(const uint2* cand_rect, const uint32_t* cand_idx, const uint32_t* n_cand, int tiles_x,
+                             int ntiles, uint32_t* cursor, uint32_t* vals, uint2* ranges, cudaStream_t s) {
+  layer_tile_lists_kernel<<<ntiles, kListWarps * 32, 0, s>>>(cand_rect, cand_idx, n_cand, tiles_x, cursor, vals,
+                                                             ranges);
+}
+
+void launch_depth_order_rest(const ViewBufs& v, int64_t n, float near_plane, void* temp, uint32_t* idx_sorted,
+                             cudaStream_t s) {
+  if (n == 0) return;
+  const DepthCarve c = carve(temp, n, near_plane);
+  const unsigned grid = (unsigned)((n + 255) / 256);
+  const DepthOut o{idx_sorted, nullptr, nullptr};
+  depth_scatter_kernel<<<grid, 256, 0, s>>>(v.dkey, n, c.base, c.off, c.slot, c.cut, kDepthRest, c.tmp, nullptr);
+  depth_rank_kernel<<<grid, 256, 0, s>>>(c.tmp, n, c.base, c.off, v.tiles, v.rect, c.cut, kDepthRest, o, c.big_r);
+  depth_big_kernel<<<8, 1024, 0, s>>>(c.tmp, c.off, v.tiles, v.rect, c.cut, c.big_r, c.scratch, c.cursor, o);
 }
 
 }  // namespace lgs

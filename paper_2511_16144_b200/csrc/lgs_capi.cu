@@ -643,10 +643,14 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
   // LGS_DEPTH_SORT=cub selects the device radix sort (A/B and cross-check of depth_order.cu)
   const char* dsort = getenv("LGS_DEPTH_SORT");
   const bool cub_depth = dsort && dsort[0] == 'c';
+  const bool fast = fast_binning_supported(ntiles);
+  // depth-layered binning (binning_fast.cu, depth_order.cu): the depth order of layer A is built
+  // with the binning below; the complete order only when some tile needs the second pass
+  const bool layered = fast && !ctx->full_lists && n > 0 && !cub_depth;
   void* otemp = nullptr;
   const size_t otemp_bytes = cub_depth ? 0 : depth_order_temp_bytes(n);
   if (!cub_depth) TRYB(dalloc(ctx, reinterpret_cast<uint8_t**>(&otemp), otemp_bytes));
-  {
+  if (!layered) {
     PhaseScope ph(ctx, PH_DEPTH_SORT);
     if (cub_depth) {
       launch_depth_sort(t->vb, n, dkey_sorted, idx_sorted, temp, temp_bytes, s);
@@ -655,9 +659,8 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
       launch_depth_order(t->vb, n, dc.near_plane, otemp, otemp_bytes, idx_sorted, dkey_sorted, s);
       launch_scan_counts(dkey_sorted, n, incl, temp, temp_bytes, s);
     }
+    ctx->launches += n > 0 ? (cub_depth ? 6 : 7) : 0;
   }
-  ctx->launches += n > 0 ? (cub_depth ? 6 : 7) : 0;
-  if (otemp) dfree(ctx, otemp);
 
   // K5 (+ fused L1) buffers
   FwdOut fo{};
@@ -696,44 +699,47 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
   // without waiting for the pair count P: the binning reads P on the device, and the host checks it
   // (and an overflow flag) only after the whole forward is queued, when the GPU is far ahead of the
   // check.  P > capacity (or the first render) runs the binning again with buffers of exactly P.
-  const bool fast = fast_binning_supported(ntiles);
-  const bool layered = fast && !ctx->full_lists && n > 0;
   auto bin_and_blend = [&](int64_t cap, bool exact) -> lgs_status {
-    if (!exact) {  // re-run with exact buffers: the tile counts in depth order again
+    if (!exact && !layered) {  // re-run with exact buffers: the tile counts in depth order again
       launch_scan_tiles(t->vb.tiles, idx_sorted, n, dkey_sorted, incl, temp, temp_bytes, s);
       ctx->launches += n > 0 ? 3 : 0;
     }
     dfree(ctx, t->vals);
     dfree(ctx, t->keys);
     if (layered) {
-      // Depth-layered binning (binning_fast.cu): pass 1 bins the depth-order prefix owning
-      // ~P / kLayerDiv pairs for every tile and blends it; tiles left unsaturated get their
-      // complete lists (after layer A's, at vals + capA) and are blended again.
+      // Depth-layered binning.  Pass 1: the depth order of layer A only (the nearest Gaussians
+      // owning ~P / kLayerDiv pairs, depth_order.cu), their lists (one warp per tile compacting
+      // the depth-ordered candidates) and the forward, which flags every tile it could not
+      // saturate.  Those tiles get their complete lists (counting sort restricted to them, at
+      // vals + capA) and are blended again: pass 2, a conditional node of a captured plan.
       const uint32_t capA = (uint32_t)layer_a_cap(cap, ntiles, kLayerDiv);
       const int64_t gcapA = std::min<int64_t>(n, std::max<int64_t>(4096, n / 32));
       const size_t sat_n = (size_t)(dc.tiles_x + 1) * (dc.tiles_y + 1);
-      uint32_t *pa = nullptr, *unfinished = nullptr, *sat = nullptr, *order2 = nullptr, *count2 = nullptr;
-      uint32_t *scratch_a = nullptr, *scratch_b = nullptr;
+      uint32_t *ra = nullptr, *unfinished = nullptr, *sat = nullptr, *order2 = nullptr, *count2 = nullptr;
+      uint32_t* scratch_b = nullptr;
+      uint2* cand_rect = nullptr;
       LGS_TRY(dalloc(ctx, &t->vals, (size_t)capA + (size_t)cap));
       t->vals_count = (int64_t)capA + cap;
-      LGS_TRY(dalloc(ctx, &pa, 1));
+      LGS_TRY(dalloc(ctx, &ra, 2));  // [0] R_A, [1] list allocator
+      LGS_TRY(dalloc(ctx, &cand_rect, gcapA));
       LGS_TRY(dalloc(ctx, &unfinished, ntiles));
       LGS_TRY(dalloc(ctx, &sat, sat_n));
       LGS_TRY(dalloc(ctx, &order2, ntiles));
       LGS_TRY(dalloc(ctx, &count2, 2));  // [0] unfinished tiles, [1] pairs of the second pass
-      LGS_TRY(dalloc(ctx, reinterpret_cast<uint8_t**>(&scratch_a), fast_binning_scratch_bytes(capA, gcapA, ntiles)));
       LGS_TRY(dalloc(ctx, reinterpret_cast<uint8_t**>(&scratch_b), fast_binning_scratch_bytes(cap, n, ntiles)));
       LGS_CUDA(cudaMemsetAsync(unfinished, 0, sizeof(uint32_t) * ntiles, s));
+      LGS_CUDA(cudaMemsetAsync(ra + 1, 0, sizeof(uint32_t), s));
+      {
+        PhaseScope ph(ctx, PH_DEPTH_SORT);
+        launch_depth_order_layer_a(t->vb, n, dc.near_plane, otemp, kLayerDiv, kLayerMinPairs, gcapA, capA,
+                                   idx_sorted, cand_rect, ra, s);
+      }
       {
         PhaseScope ph(ctx, PH_TILE_SORT);
-        launch_layer_cut(incl, n, kLayerDiv, gcapA, pa, s);
-        BinPass a{incl, pa, gcapA, capA, 0u, nullptr};
-        a.clamp = pa;
-        launch_fast_binning(t->vb, idx_sorted, n, ntiles, dc.tiles_x, a, scratch_a, t->vals, t->ranges,
-                            ctx->dev_u32 + 1, s);
+        launch_layer_tile_lists(cand_rect, idx_sorted, ra, dc.tiles_x, ntiles, ra + 1, t->vals, t->ranges, s);
         launch_tile_order(t->ranges, ntiles, t->order, s);  // longest tile list first
       }
-      ctx->launches += 7;
+      ctx->launches += 8;
       if (targets) LGS_CUDA(cudaMemsetAsync(t->loss, 0, sizeof(double), s));
       FwdOut fo1 = fo;
       fo1.unfinished = unfinished;
@@ -759,6 +765,7 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
         cudaStream_t s2 = ctx->stream;  // the conditional body's capture stream inside a plan
         {
           PhaseScope ph(ctx, PH_TILE_SORT);
+          launch_depth_order_rest(t->vb, n, dc.near_plane, otemp, idx_sorted, s2);
           launch_layer_count(t->vb, idx_sorted, n, dc.tiles_x, sat, count2, dkey_sorted, count2 + 1, s2);
           launch_scan_counts(dkey_sorted, n, incl, temp, temp_bytes, s2);
           const BinPass b{incl, count2 + 1, n, (uint32_t)cap, capA, unfinished, count2};
@@ -773,16 +780,16 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
         }
         if (cudaGetLastError() != cudaSuccess) st2 = fail(LGS_ECUDA, "layered binning pass 2 launch failed");
       }
-      ctx->launches += 9;
+      ctx->launches += 12;
       if (use_cond) LGS_TRY(cond_end(ctx));
       LGS_TRY(st2);
       dfree(ctx, scratch_b);
-      dfree(ctx, scratch_a);
       dfree(ctx, count2);
       dfree(ctx, order2);
       dfree(ctx, sat);
       dfree(ctx, unfinished);
-      dfree(ctx, pa);
+      dfree(ctx, cand_rect);
+      dfree(ctx, ra);
       LGS_CUDA(cudaGetLastError());
       return LGS_OK;
     }
@@ -861,6 +868,7 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
     if (fast) ctx->pairs_cap = std::max<int64_t>(ctx->pairs_cap, P + P / 4);
   }
   t->pairs = P;
+  if (otemp) dfree(ctx, otemp);
   dfree(ctx, temp);
   dfree(ctx, dkey_sorted);
   dfree(ctx, idx_sorted);

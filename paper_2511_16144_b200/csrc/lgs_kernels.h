@@ -86,6 +86,18 @@ void launch_scan_counts(const uint32_t* cnt_sorted, int64_t n, uint32_t* incl, v
 size_t depth_order_temp_bytes(int64_t n);
 void launch_depth_order(const ViewBufs& v, int64_t n, float near_plane, void* temp, size_t temp_bytes,
                         uint32_t* idx_sorted, uint32_t* cnt_sorted, cudaStream_t s);
+// Depth-layered binning: order only layer A = the bucket prefix owning ~max(min(P, min_pairs), P / div)
+// pairs (at most gauss_cap Gaussians, cap_a pairs): idx_sorted[0, R_A), their tile rects cand_rect,
+// *ra = R_A.  launch_depth_order_rest (same temp) orders the remaining Gaussians afterwards.
+void launch_depth_order_layer_a(const ViewBufs& v, int64_t n, float near_plane, void* temp, uint32_t div,
+                                uint32_t min_pairs, int64_t gauss_cap, uint32_t cap_a, uint32_t* idx_sorted,
+                                uint2* cand_rect, uint32_t* ra, cudaStream_t s);
+void launch_depth_order_rest(const ViewBufs& v, int64_t n, float near_plane, void* temp, uint32_t* idx_sorted,
+                             cudaStream_t s);
+// Layer-A tile lists (one warp per tile scanning the depth-ordered candidates, order-preserving
+// compaction): vals[ranges[t]] for every tile; *cursor (zeroed by the caller) allocates list space.
+void launch_layer_tile_lists(const uint2* cand_rect, const uint32_t* cand_idx, const uint32_t* n_cand, int tiles_x,
+                             int ntiles, uint32_t* cursor, uint32_t* vals, uint2* ranges, cudaStream_t s);
 void launch_duplicate(const ViewBufs& v, const uint32_t* idx_sorted, const uint32_t* incl, int64_t n,
                       int tiles_x, uint16_t* key_out, uint32_t* val_out, cudaStream_t s);
 void launch_tile_sort(uint16_t* keys_in, uint16_t* keys_out, uint32_t* vals_in, uint32_t* vals_out,
@@ -114,9 +126,8 @@ void launch_fast_binning(const ViewBufs& v, const uint32_t* idx_sorted, int64_t 
                          cudaStream_t s);
 // Depth-layered binning (binning_fast.cu): layer A = the depth-order prefix owning ~P / div pairs
 // (at most gauss_cap Gaussians), then the complete lists of the tiles layer A left unsaturated.
+constexpr uint32_t kLayerMinPairs = 1u << 16;  // layer A takes at least this many pairs (or all)
 size_t layer_a_cap(int64_t pairs_cap, int ntiles, uint32_t div);
-void launch_layer_cut(const uint32_t* incl, int64_t n, uint32_t div, int64_t gauss_cap, uint32_t* pa,
-                      cudaStream_t s);
 void launch_layer_prep(const uint32_t* unfinished, const uint2* ranges, int tiles_x, int tiles_y, uint32_t* sat,
                        uint32_t* order2, uint32_t* count2, uint32_t* total2, const cudaGraphConditionalHandle* cond,
                        cudaStream_t s);
