@@ -31,8 +31,6 @@
 
 namespace lgs {
 
-constexpr int kDepthShift = 10;
-constexpr int kDepthBuckets = 1 << 18;  // visible buckets; bucket kDepthBuckets holds the culled
 constexpr int kMaxRankBucket = 1024;
 
 __device__ __forceinline__ uint32_t depth_bucket(uint32_t key, uint32_t base) {
@@ -101,13 +99,23 @@ __device__ __forceinline__ bool bucket_selected(uint32_t b, int mode, uint32_t c
 __global__ void depth_scatter_kernel(const uint32_t* __restrict__ dkey, int64_t n, uint32_t base,
                                      const u64* __restrict__ off, const uint32_t* __restrict__ slot,
                                      const uint32_t* __restrict__ cut, int mode, uint2* __restrict__ tmp,
-                                     uint32_t* __restrict__ ra_out) {
+                                     uint32_t* __restrict__ ra_out, uint32_t* __restrict__ culled_cursor) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i == 0 && ra_out) *ra_out = cnt_of(off[*cut]);  // R_A: Gaussians in layer A
   if (i >= n) return;
   const uint32_t k = dkey[i];
   const uint32_t b = depth_bucket(k, base);
   if (!bucket_selected(b, mode, cut ? *cut : 0u)) return;
+  if (culled_cursor && b == kDepthBuckets) {  // slots of culled Gaussians (any order) handed out here
+    const unsigned act = __activemask();
+    const unsigned peers = __match_any_sync(act, 1u);
+    const int leader = __ffs(peers) - 1;
+    uint32_t basep = 0;
+    if ((int)(threadIdx.x & 31) == leader) basep = atomicAdd(culled_cursor, (uint32_t)__popc(peers));
+    basep = __shfl_sync(peers, basep, leader);
+    tmp[cnt_of(off[b]) + basep + __popc(peers & ((1u << (threadIdx.x & 31)) - 1u))] = make_uint2(k, (uint32_t)i);
+    return;
+  }
   tmp[cnt_of(off[b]) + slot[i]] = make_uint2(k, (uint32_t)i);
 }
 
@@ -295,9 +303,33 @@ void launch_depth_order(const ViewBufs& v, int64_t n, float near_plane, void* te
   depth_front(v, n, c, s);
   const unsigned grid = (unsigned)((n + 255) / 256);
   const DepthOut o{idx_sorted, cnt_sorted, nullptr};
-  depth_scatter_kernel<<<grid, 256, 0, s>>>(v.dkey, n, c.base, c.off, c.slot, nullptr, kDepthAll, c.tmp, nullptr);
+  depth_scatter_kernel<<<grid, 256, 0, s>>>(v.dkey, n, c.base, c.off, c.slot, nullptr, kDepthAll, c.tmp, nullptr, nullptr);
   depth_rank_kernel<<<grid, 256, 0, s>>>(c.tmp, n, c.base, c.off, v.tiles, v.rect, nullptr, kDepthAll, o, c.big_a);
   depth_big_kernel<<<8, 1024, 0, s>>>(c.tmp, c.off, v.tiles, v.rect, nullptr, c.big_a, c.scratch, c.cursor, o);
+}
+
+void launch_depth_prepare(int64_t n, float near_plane, void* temp, ViewBufs* v, cudaStream_t s) {
+  const DepthCarve c = carve(temp, n, near_plane);
+  cudaMemsetAsync(c.hist, 0, sizeof(unsigned long long) * (kDepthBuckets + 2), s);
+  cudaMemsetAsync(c.big_a, 0, sizeof(uint32_t), s);
+  cudaMemsetAsync(c.big_r, 0, sizeof(uint32_t), s);
+  cudaMemsetAsync(c.cursor, 0, 2 * sizeof(uint32_t), s);
+  v->dhist = c.hist;
+  v->dslot = c.slot;
+  v->dbase = c.base;
+}
+
+// After K1 filled the visible buckets (the culled ones get their slots in the rest pass): bucket
+// offsets; *pairs_out = the low word of the offset past the last visible bucket = the pair total P.
+void launch_depth_scan(int64_t n, float near_plane, void* temp, const uint32_t** pairs_out, cudaStream_t s) {
+  const DepthCarve c = carve(temp, n, near_plane);
+  *pairs_out = reinterpret_cast<const uint32_t*>(c.off + kDepthBuckets);  // little endian: low word = pairs
+  if (n == 0) {
+    cudaMemsetAsync(c.off, 0, sizeof(unsigned long long) * (kDepthBuckets + 2), s);
+    return;
+  }
+  size_t sb = c.scan_bytes;
+  cub::DeviceScan::ExclusiveSum(c.scan_temp, sb, c.hist, c.off, kDepthBuckets + 2, s);
 }
 
 void launch_depth_order_layer_a(const ViewBufs& v, int64_t n, float near_plane, void* temp, uint32_t div,
@@ -308,13 +340,14 @@ void launch_depth_order_layer_a(const ViewBufs& v, int64_t n, float near_plane, 
     return;
   }
   const DepthCarve c = carve(temp, n, near_plane);
-  depth_front(v, n, c, s);
   cudaMemsetAsync(c.cut, 0xff, sizeof(uint32_t), s);
+  cudaMemsetAsync(c.big_a, 0, sizeof(uint32_t), s);
+  cudaMemsetAsync(c.cursor, 0, sizeof(uint32_t), s);  // bitonic scratch allocator
   depth_cut_kernel<<<(kDepthBuckets + 255) / 256, 256, 0, s>>>(c.off, div, min_pairs, gauss_cap, cap_a, c.cut);
   const DepthOut o{idx_sorted, nullptr, cand_rect};
   const int64_t ga = std::min<int64_t>(n, gauss_cap);
   depth_scatter_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(v.dkey, n, c.base, c.off, c.slot, c.cut,
-                                                                    kDepthLayerA, c.tmp, ra);
+                                                                    kDepthLayerA, c.tmp, ra, nullptr);
   depth_rank_kernel<<<(unsigned)((ga + 255) / 256), 256, 0, s>>>(c.tmp, n, c.base, c.off, v.tiles, v.rect, c.cut,
                                                                   kDepthLayerA, o, c.big_a);
   depth_big_kernel<<<8, 1024, 0, s>>>(c.tmp, c.off, v.tiles, v.rect, c.cut, c.big_a, c.scratch, c.cursor, o);
@@ -381,7 +414,10 @@ void launch_depth_order_rest(const ViewBufs& v, int64_t n, float near_plane, voi
   const DepthCarve c = carve(temp, n, near_plane);
   const unsigned grid = (unsigned)((n + 255) / 256);
   const DepthOut o{idx_sorted, nullptr, nullptr};
-  depth_scatter_kernel<<<grid, 256, 0, s>>>(v.dkey, n, c.base, c.off, c.slot, c.cut, kDepthRest, c.tmp, nullptr);
+  cudaMemsetAsync(c.big_r, 0, sizeof(uint32_t), s);
+  cudaMemsetAsync(c.cursor + 1, 0, sizeof(uint32_t), s);  // culled slots
+  depth_scatter_kernel<<<grid, 256, 0, s>>>(v.dkey, n, c.base, c.off, c.slot, c.cut, kDepthRest, c.tmp, nullptr,
+                                            c.cursor + 1);
   depth_rank_kernel<<<grid, 256, 0, s>>>(c.tmp, n, c.base, c.off, v.tiles, v.rect, c.cut, kDepthRest, o, c.big_r);
   depth_big_kernel<<<8, 1024, 0, s>>>(c.tmp, c.off, v.tiles, v.rect, c.cut, c.big_r, c.scratch, c.cursor, o);
 }

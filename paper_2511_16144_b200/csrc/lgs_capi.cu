@@ -617,17 +617,32 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
   TRYB(dalloc(ctx, &t->ps.acc, npix));
   TRYB(dalloc(ctx, &t->ps.work, npix));
 
+  // LGS_DEPTH_SORT=cub selects the device radix sort (A/B and cross-check of depth_order.cu)
+  const char* dsort = getenv("LGS_DEPTH_SORT");
+  const bool cub_depth = dsort && dsort[0] == 'c';
+  const bool fast = fast_binning_supported(ntiles);
+  // depth-layered binning (binning_fast.cu, depth_order.cu): K1 fills the depth-bucket histogram,
+  // the depth order of layer A is built with the binning below, the complete order only when some
+  // tile needs the second pass
+  const bool layered = fast && !ctx->full_lists && n > 0 && !cub_depth;
+  void* otemp = nullptr;
+  const size_t otemp_bytes = cub_depth ? 0 : depth_order_temp_bytes(n);
+  if (!cub_depth) TRYB(dalloc(ctx, reinterpret_cast<uint8_t**>(&otemp), otemp_bytes));
+  if (layered) launch_depth_prepare(n, dc.near_plane, otemp, &t->vb, s);
+
   // K1
+  const uint32_t* dev_pairs = ctx->dev_u32;
   {
     PhaseScope ph(ctx, PH_PREPROCESS);
     launch_preprocess(map->dm, dc, t->vb, s);
     // the pair count P = sum of tiles touched sizes the tile lists; it is read back while the GPU
-    // is still busy with the depth sort queued below, so the host wait never idles the GPU
-    launch_sum_tiles(t->vb.tiles, n, ctx->dev_u32, s);
+    // is still busy with the depth order queued below, so the host wait never idles the GPU
+    if (layered) launch_depth_scan(n, dc.near_plane, otemp, &dev_pairs, s);  // P = visible buckets' pairs
+    else launch_sum_tiles(t->vb.tiles, n, ctx->dev_u32, s);
   }
-  ctx->launches += 2;
+  ctx->launches += layered ? 3 : 2;
   if (n > 0) {
-    CUDAB(cudaMemcpyAsync(ctx->host_u32, ctx->dev_u32, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    CUDAB(cudaMemcpyAsync(ctx->host_u32, dev_pairs, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
     if (!ctx->capturing) CUDAB(cudaEventRecord(ctx->pairs_ready, s));
   }
 
@@ -640,16 +655,6 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
   TRYB(dalloc(ctx, &idx_sorted, n));
   TRYB(dalloc(ctx, &incl, n));
   TRYB(dalloc(ctx, reinterpret_cast<uint8_t**>(&temp), temp_bytes));
-  // LGS_DEPTH_SORT=cub selects the device radix sort (A/B and cross-check of depth_order.cu)
-  const char* dsort = getenv("LGS_DEPTH_SORT");
-  const bool cub_depth = dsort && dsort[0] == 'c';
-  const bool fast = fast_binning_supported(ntiles);
-  // depth-layered binning (binning_fast.cu, depth_order.cu): the depth order of layer A is built
-  // with the binning below; the complete order only when some tile needs the second pass
-  const bool layered = fast && !ctx->full_lists && n > 0 && !cub_depth;
-  void* otemp = nullptr;
-  const size_t otemp_bytes = cub_depth ? 0 : depth_order_temp_bytes(n);
-  if (!cub_depth) TRYB(dalloc(ctx, reinterpret_cast<uint8_t**>(&otemp), otemp_bytes));
   if (!layered) {
     PhaseScope ph(ctx, PH_DEPTH_SORT);
     if (cub_depth) {
@@ -885,6 +890,8 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
   // the tape no longer needs the sort keys of the depth pass
   dfree(ctx, t->vb.dkey);
   dfree(ctx, t->vb.iota);
+  t->vb.dhist = nullptr;  // lived in the depth-order scratch, freed above
+  t->vb.dslot = nullptr;
   if (tape) *tape = t;
   else free_saved(t);
   return LGS_OK;

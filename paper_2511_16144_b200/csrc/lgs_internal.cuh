@@ -15,6 +15,11 @@
 
 namespace lgs {
 
+// depth buckets of the bucketed depth order (depth_order.cu): key >> kDepthShift relative to the
+// near plane, 2^13 buckets per octave of depth; bucket kDepthBuckets holds the culled Gaussians
+constexpr int kDepthShift = 10;
+constexpr int kDepthBuckets = 1 << 18;
+
 constexpr int kTile = 16;
 constexpr int kBlock = kTile * kTile;
 

@@ -19,6 +19,11 @@ struct ViewBufs {
   uint32_t* tiles;  // tiles touched (0 = culled)
   uint32_t* dkey;   // f32 bits of depth (0xffffffff = culled) -> depth sort key
   uint32_t* iota;   // map index
+  // optional (depth-layered binning): K1 also adds each visible Gaussian to its depth bucket
+  // (depth_order.cu): dhist[bucket] += 1 << 32 | tiles, dslot[i] = its slot in the bucket
+  unsigned long long* dhist = nullptr;
+  uint32_t* dslot = nullptr;
+  uint32_t dbase = 0;  // near-plane bucket offset (depth_bucket)
 };
 
 // Tile lists for the blend kernels.
@@ -89,6 +94,11 @@ void launch_depth_order(const ViewBufs& v, int64_t n, float near_plane, void* te
 // Depth-layered binning: order only layer A = the bucket prefix owning ~max(min(P, min_pairs), P / div)
 // pairs (at most gauss_cap Gaussians, cap_a pairs): idx_sorted[0, R_A), their tile rects cand_rect,
 // *ra = R_A.  launch_depth_order_rest (same temp) orders the remaining Gaussians afterwards.
+// Split for the layered path: depth_prepare (before K1: zeroes the histogram, sets v.dhist/dslot/
+// dbase so K1 fills it), depth_scan (after K1: bucket offsets; *pairs_out = device address of the
+// visible pair total P), then launch_depth_order_layer_a (cut, scatter, rank of layer A).
+void launch_depth_prepare(int64_t n, float near_plane, void* temp, ViewBufs* v, cudaStream_t s);
+void launch_depth_scan(int64_t n, float near_plane, void* temp, const uint32_t** pairs_out, cudaStream_t s);
 void launch_depth_order_layer_a(const ViewBufs& v, int64_t n, float near_plane, void* temp, uint32_t div,
                                 uint32_t min_pairs, int64_t gauss_cap, uint32_t cap_a, uint32_t* idx_sorted,
                                 uint2* cand_rect, uint32_t* ra, cudaStream_t s);

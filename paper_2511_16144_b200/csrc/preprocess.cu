@@ -151,8 +151,14 @@ __global__ void __launch_bounds__(kPreThreads) preprocess_kernel(DevMap m, DevCa
   v.rec0[i] = make_float4(u, vv, t2, opacity);
   v.rec1[i] = make_float4(cc / det, -cb / det, ca / det, radius);
   v.rect[i] = make_uint2((uint32_t)x0 | ((uint32_t)x1 << 16), (uint32_t)y0 | ((uint32_t)y1 << 16));
-  v.tiles[i] = (uint32_t)((x1 / kTile - x0 / kTile + 1) * (y1 / kTile - y0 / kTile + 1));
+  const uint32_t ntl = (uint32_t)((x1 / kTile - x0 / kTile + 1) * (y1 / kTile - y0 / kTile + 1));
+  v.tiles[i] = ntl;
   v.dkey[i] = __float_as_uint(t2);
+  if (v.dhist) {  // depth bucket histogram of the layered binning (depth_order.cu depth_bucket)
+    const uint32_t b = __float_as_uint(t2) >> kDepthShift;
+    const uint32_t bk = b > v.dbase ? min(b - v.dbase, (uint32_t)kDepthBuckets - 1u) : 0u;
+    v.dslot[i] = (uint32_t)(atomicAdd(v.dhist + bk, (1ull << 32) | ntl) >> 32);
+  }
 
   // colour (renderer.cpp:128; SH extension)
   constexpr int K = (DEG + 1) * (DEG + 1);
