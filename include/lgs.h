@@ -241,7 +241,8 @@ LGS_API lgs_status lgs_ctx_profile(lgs_ctx* ctx, int32_t enable);
 LGS_API lgs_status lgs_ctx_phase_times(lgs_ctx* ctx, double* ms, int64_t* counts, int32_t reset);
 
 /* Work counters of a forward: (pixel, Gaussian) pairs that reached the alpha test and pairs
- * that contributed (the reference's pixel_contribs entries, renderer.cpp:157).  Synchronizes. */
+ * that contributed (the reference's pixel_contribs entries, renderer.cpp:157).  Synchronizes.
+ * Counted only by forwards run while the context profiles (lgs_ctx_profile); else LGS_EINVAL. */
 LGS_API lgs_status lgs_saved_work(const lgs_saved* tape, int64_t* evaluated, int64_t* contributed);
 
 /* Measured FP32 FFMA throughput of `device` (TFLOP/s): the roofline denominator of the blend
@@ -364,6 +365,12 @@ LGS_API lgs_status lgs_plan_sync(lgs_ctx* ctx, lgs_plan* plan, int64_t* pairs);
 LGS_API lgs_status lgs_plan_set_camera(lgs_ctx* ctx, lgs_plan* plan, const lgs_camera* cam);
 /* Device time of the last replay, from events recorded as the graph's first and last nodes. */
 LGS_API lgs_status lgs_plan_elapsed_ms(const lgs_plan* plan, float* ms);
+/* Profiling plans re-capture with an event-record node around every phase (each costs a few us
+ * per replay, so timed plans leave it off).  lgs_plan_phase_times: device ms per phase
+ * (LGS_PHASE_COUNT doubles, lgs_ctx_phase_times order) of the last replay; the conditional second
+ * pass of the layered binning is not split out. */
+LGS_API lgs_status lgs_plan_set_profiling(lgs_ctx* ctx, lgs_plan* plan, int32_t on);
+LGS_API lgs_status lgs_plan_phase_times(const lgs_plan* plan, double* ms);
 LGS_API int64_t lgs_plan_launches(const lgs_plan* plan);
 LGS_API lgs_status lgs_plan_destroy(lgs_plan* plan);
 

@@ -147,6 +147,8 @@ SIGNATURES = [
     ("lgs_plan_sync", C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_int64)]),
     ("lgs_plan_set_camera", C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(LgsCamera)]),
     ("lgs_plan_elapsed_ms", C.c_int, [C.c_void_p, C.POINTER(C.c_float)]),
+    ("lgs_plan_set_profiling", C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
+    ("lgs_plan_phase_times", C.c_int, [C.c_void_p, C.POINTER(C.c_double)]),
     ("lgs_plan_launches", C.c_int64, [C.c_void_p]),
     ("lgs_plan_destroy", C.c_int, [C.c_void_p]),
     ("lgs_comm_unique_id", C.c_int, [C.POINTER(LgsCommId)]),

@@ -23,22 +23,24 @@
 
 namespace lgs {
 
-template <int DP>
+template <int DP, int NB>
 struct FwdSmem {
-  float4 r0[kBlock];  // u, v, depth, opacity
-  float4 sc[kBlock];  // scaled conic a, b2, c, -
-  uint2 rect[kBlock];
-  float4 col[kBlock];
-  float4 feat[kBlock][DP > 0 ? DP / 4 : 1];
+  float4 r0[NB];  // u, v, depth, opacity
+  float4 sc[NB];  // scaled conic a, b2, c, -
+  uint2 rect[NB];
+  float4 col[NB];
+  float4 feat[NB][DP > 0 ? DP / 4 : 1];
 };
 
-template <int DP, bool L1, int PPT>
-__global__ void __launch_bounds__(kBlock / PPT) blend_fwd_kernel(DevMap m, DevCam c, ViewBufs v, TileLists tl,
-                                                                   PixelState ps, FwdOut o) {
+// NB: list entries staged per shared-memory batch; MINB: launch-bounds residency hint (0: none)
+// WORK: count evaluated / contributing (pixel, Gaussian) pairs per pixel (profiling only)
+template <int DP, bool L1, int PPT, int NB, int MINB, bool WORK>
+__global__ void __launch_bounds__(kBlock / PPT, MINB) blend_fwd_kernel(DevMap m, DevCam c, ViewBufs v, TileLists tl,
+                                                                         PixelState ps, FwdOut o) {
   constexpr int NT = kBlock / PPT;
   constexpr int DQ = DP > 0 ? DP / 4 : 1;
   constexpr int FD = DP > 0 ? DP : 1;
-  __shared__ FwdSmem<DP> sm;
+  __shared__ FwdSmem<DP, NB> sm;
   __shared__ float s_loss[NT / 32];
   __shared__ int s_slot;
   const int tid = threadIdx.x;
@@ -72,9 +74,9 @@ __global__ void __launch_bounds__(kBlock / PPT) blend_fwd_kernel(DevMap m, DevCa
       all_done = all_done && done[k];
     }
 
-    for (uint32_t base = range.x; base < range.y; base += kBlock) {
+    for (uint32_t base = range.x; base < range.y; base += NB) {
       if (__syncthreads_count(all_done) == NT) break;
-      for (int e = tid; e < kBlock; e += NT) {
+      for (int e = tid; e < NB; e += NT) {
         const uint32_t j = base + e;
         if (j < range.y) {
           const uint32_t g = __ldg(tl.vals + j);
@@ -92,7 +94,7 @@ __global__ void __launch_bounds__(kBlock / PPT) blend_fwd_kernel(DevMap m, DevCa
         }
       }
       __syncthreads();
-      const int cnt = (int)min((uint32_t)kBlock, range.y - base);
+      const int cnt = (int)min((uint32_t)NB, range.y - base);
       // Composite one staged entry given its pixels' alphas (evaluated earlier): a pixel that does
       // not contribute gets alpha = 0, which leaves T, the accumulators and the counters exactly
       // unchanged (w = +0).
@@ -104,8 +106,10 @@ __global__ void __launch_bounds__(kBlock / PPT) blend_fwd_kernel(DevMap m, DevCa
         for (int k = 0; k < PPT; ++k) {
           const bool live = in[k] && !done[k];
           ok[k] = live && al[k] >= c.alpha_skip;
-          n_eval[k] += live ? 1u : 0u;
-          n_contrib[k] += ok[k] ? 1u : 0u;
+          if (WORK) {
+            n_eval[k] += live ? 1u : 0u;
+            n_contrib[k] += ok[k] ? 1u : 0u;
+          }
           a[k] = ok[k] ? fminf(al[k], c.alpha_clamp) : 0.f;
           any = any || ok[k];
         }
@@ -186,7 +190,7 @@ __global__ void __launch_bounds__(kBlock / PPT) blend_fwd_kernel(DevMap m, DevCa
       ps.n_contrib[pix] = last[k];
       ps.depth[pix] = dnorm;
       ps.acc[pix] = acc[k];
-      ps.work[pix] = make_uint2(n_eval[k], n_contrib[k]);
+      if (WORK) ps.work[pix] = make_uint2(n_eval[k], n_contrib[k]);
       if (o.rgb) {
         o.rgb[pix * 3 + 0] = cr[k];
         o.rgb[pix * 3 + 1] = cg[k];
@@ -250,12 +254,13 @@ __global__ void __launch_bounds__(kBlock / PPT) blend_fwd_kernel(DevMap m, DevCa
   }
 }
 
-template <int DP, bool L1, int PPT>
-static void launch_fwd_cfg(const DevMap& m, const DevCam& c, const ViewBufs& v, const TileLists& tl,
-                           const PixelState& ps, const FwdOut& o, cudaStream_t s) {
+template <int DP, bool L1, int PPT, int NB, int MINB, bool WORK>
+static void launch_fwd_work(const DevMap& m, const DevCam& c, const ViewBufs& v, const TileLists& tl,
+                            const PixelState& ps, const FwdOut& o, cudaStream_t s) {
   static int ctas_per_sm = 0, sms = 0;
   if (!ctas_per_sm) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, blend_fwd_kernel<DP, L1, PPT>, kBlock / PPT, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, blend_fwd_kernel<DP, L1, PPT, NB, MINB, WORK>,
+                                                  kBlock / PPT, 0);
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -264,14 +269,22 @@ static void launch_fwd_cfg(const DevMap& m, const DevCam& c, const ViewBufs& v, 
   const int ntiles = c.tiles_x * c.tiles_y;
   const int grid = min(ntiles, ctas_per_sm * sms);
   cudaMemsetAsync(tl.counter, 0, sizeof(int), s);
-  blend_fwd_kernel<DP, L1, PPT><<<grid, kBlock / PPT, 0, s>>>(m, c, v, tl, ps, o);
+  blend_fwd_kernel<DP, L1, PPT, NB, MINB, WORK><<<grid, kBlock / PPT, 0, s>>>(m, c, v, tl, ps, o);
+}
+
+template <int DP, bool L1, int PPT, int NB, int MINB>
+static void launch_fwd_cfg(const DevMap& m, const DevCam& c, const ViewBufs& v, const TileLists& tl,
+                           const PixelState& ps, const FwdOut& o, cudaStream_t s) {
+  if (ps.work) launch_fwd_work<DP, L1, PPT, NB, MINB, true>(m, c, v, tl, ps, o, s);
+  else launch_fwd_work<DP, L1, PPT, NB, MINB, false>(m, c, v, tl, ps, o, s);
 }
 
 template <int DP>
 static void launch_fwd_dp(const DevMap& m, const DevCam& c, const ViewBufs& v, const TileLists& tl,
                           const PixelState& ps, const FwdOut& o, cudaStream_t s) {
-  if (o.cot) launch_fwd_cfg<DP, true, 2>(m, c, v, tl, ps, o, s);
-  else launch_fwd_cfg<DP, false, 2>(m, c, v, tl, ps, o, s);
+  constexpr int NB = DP > 16 ? 128 : 256;  // static shared memory stays under 48 KB
+  if (o.cot) launch_fwd_cfg<DP, true, 2, NB, 0>(m, c, v, tl, ps, o, s);
+  else launch_fwd_cfg<DP, false, 2, NB, 0>(m, c, v, tl, ps, o, s);
 }
 
 void launch_blend_fwd(const DevMap& m, const DevCam& c, const ViewBufs& v, const TileLists& tl,

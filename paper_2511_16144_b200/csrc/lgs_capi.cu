@@ -88,6 +88,7 @@ struct lgs_ctx {
   cudaEvent_t pairs_ready = nullptr;
   cudaMemPool_t pool = nullptr;  // this context's stream-ordered arena (no cross-context reuse waits)
   bool capturing = false;        // inside lgs_plan capture: no host waits, graph memory nodes
+  std::vector<PhaseMark>* capture_marks = nullptr;  // lgs_plan capture: phase events recorded as graph nodes
   int64_t pairs_cap = 0;  // tile-list capacity for the next render (0: size from the exact count)
   bool full_lists = false;  // lgs_ctx_set_full_tile_lists: single-pass binning of every pair
   cudaStream_t cond_stream = nullptr;  // captures the body of a plan's conditional node
@@ -162,14 +163,28 @@ struct PhaseScope {
     cudaEventCreate(&e);
     return e;
   }
-  PhaseScope(lgs_ctx* c, int phase) : ctx(c), on(c->profiling && !c->capturing) {
-    if (!on) return;
+  bool graph = false;  // inside a plan capture: external event-record nodes of the graph
+  PhaseScope(lgs_ctx* c, int phase)
+      : ctx(c), on(c->profiling && !c->capturing),
+        graph(c->capturing && c->capture_marks && !c->cond_parent) {
+    if (!on && !graph) return;
     m.phase = phase;
+    if (graph) {
+      cudaEventCreate(&m.a);
+      cudaEventCreate(&m.b);
+      cudaEventRecordWithFlags(m.a, ctx->stream, cudaEventRecordExternal);
+      return;
+    }
     m.a = take();
     m.b = take();
     cudaEventRecord(m.a, ctx->stream);
   }
   ~PhaseScope() {
+    if (graph) {
+      cudaEventRecordWithFlags(m.b, ctx->stream, cudaEventRecordExternal);
+      ctx->capture_marks->push_back(m);
+      return;
+    }
     if (!on) return;
     cudaEventRecord(m.b, ctx->stream);
     ctx->marks.push_back(m);
@@ -373,6 +388,7 @@ void free_saved(lgs_saved* t) {
   lgs_ctx* ctx = t->ctx;
   cudaSetDevice(ctx->device);
   dfree(ctx, t->vb.rec0);
+  dfree(ctx, t->vb.active);
   dfree(ctx, t->vb.rec1);
   dfree(ctx, t->vb.rect);
   dfree(ctx, t->vb.color);
@@ -615,7 +631,7 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
   TRYB(dalloc(ctx, &t->ps.n_contrib, npix));
   TRYB(dalloc(ctx, &t->ps.depth, npix));
   TRYB(dalloc(ctx, &t->ps.acc, npix));
-  TRYB(dalloc(ctx, &t->ps.work, npix));
+  if (ctx->profiling) TRYB(dalloc(ctx, &t->ps.work, npix));  // work counters: profiling renders only
 
   // LGS_DEPTH_SORT=cub selects the device radix sort (A/B and cross-check of depth_order.cu)
   const char* dsort = getenv("LGS_DEPTH_SORT");
@@ -628,7 +644,11 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
   void* otemp = nullptr;
   const size_t otemp_bytes = cub_depth ? 0 : depth_order_temp_bytes(n);
   if (!cub_depth) TRYB(dalloc(ctx, reinterpret_cast<uint8_t**>(&otemp), otemp_bytes));
-  if (layered) launch_depth_prepare(n, dc.near_plane, otemp, &t->vb, s);
+  if (layered) {
+    launch_depth_prepare(n, dc.near_plane, otemp, &t->vb, s);
+    TRYB(dalloc(ctx, &t->vb.active, n));  // tape-owned: the backward reads it
+    CUDAB(cudaMemsetAsync(t->vb.active, 0, (size_t)n, s));
+  }
 
   // K1
   const uint32_t* dev_pairs = ctx->dev_u32;
@@ -738,6 +758,7 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
         PhaseScope ph(ctx, PH_DEPTH_SORT);
         launch_depth_order_layer_a(t->vb, n, dc.near_plane, otemp, kLayerDiv, kLayerMinPairs, gcapA, capA,
                                    idx_sorted, cand_rect, ra, s);
+        launch_mark_active(idx_sorted, ra, gcapA, t->vb.active, s);
       }
       {
         PhaseScope ph(ctx, PH_TILE_SORT);
@@ -928,7 +949,7 @@ lgs_status run_backward(lgs_ctx* ctx, const lgs_saved* t, const BwdIn& in_dev, l
   const int slots = slots_for(t->dm.dp);
   float* gacc = nullptr;
   LGS_TRY(dalloc(ctx, &gacc, (size_t)n * slots));
-  LGS_CUDA(cudaMemsetAsync(gacc, 0, sizeof(float) * (size_t)n * slots, s));
+  launch_zero_active_rows(t->vb, n, gacc, slots, s);  // rows the blend kernel may add into
   {
     PhaseScope ph(ctx, PH_BLEND_BWD);
     launch_blend_bwd(t->dm, t->cam, t->vb, TileLists{t->vals, t->ranges, t->order, t->counter}, t->ps, in_dev, gacc, slots, s);
@@ -1274,6 +1295,7 @@ LGS_API lgs_status lgs_saved_work(const lgs_saved* tape, int64_t* evaluated, int
   if (!tape) return fail(LGS_EINVAL, "NULL argument");
   lgs_ctx* ctx = tape->ctx;
   LGS_CUDA(cudaSetDevice(ctx->device));
+  if (!tape->ps.work) return fail(LGS_EINVAL, "work counters are collected only while profiling (lgs_ctx_profile)");
   std::vector<uint2> w((size_t)tape->cam.W * tape->cam.H);
   LGS_CUDA(cudaMemcpyAsync(w.data(), tape->ps.work, sizeof(uint2) * w.size(), cudaMemcpyDeviceToHost, ctx->stream));
   LGS_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -1847,9 +1869,21 @@ struct lgs_plan {
   cudaGraphExec_t exec = nullptr;
   cudaStream_t cap_stream = nullptr;  // private capture stream (the context's may be the legacy one)
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::vector<PhaseMark> marks;  // per-phase events recorded inside the graph (profiling plans)
+  bool profile = false;
   int64_t cap = 0;
   int64_t launches_per_run = 0;
 };
+
+namespace {
+void plan_free_marks(lgs_plan* p) {
+  for (auto& m : p->marks) {
+    cudaEventDestroy(m.a);
+    cudaEventDestroy(m.b);
+  }
+  p->marks.clear();
+}
+}  // namespace
 
 namespace {
 
@@ -1866,6 +1900,8 @@ lgs_status plan_capture(lgs_plan* p) {
   LGS_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
   ctx->stream = s;
   ctx->capturing = true;
+  plan_free_marks(p);
+  ctx->capture_marks = p->profile ? &p->marks : nullptr;  // event nodes cost ~5 us each per replay
   lgs_status st = LGS_OK;
   lgs_saved* tape = nullptr;
   if (cudaEventRecordWithFlags(p->ev0, s, cudaEventRecordExternal) != cudaSuccess)
@@ -1882,6 +1918,7 @@ lgs_status plan_capture(lgs_plan* p) {
   if (st == LGS_OK && cudaEventRecordWithFlags(p->ev1, s, cudaEventRecordExternal) != cudaSuccess)
     st = fail(LGS_ECUDA, "event record in capture failed");
   ctx->capturing = false;
+  ctx->capture_marks = nullptr;
   ctx->stream = saved;
   cudaGraph_t graph = nullptr;
   const cudaError_t ec = cudaStreamEndCapture(s, &graph);
@@ -1986,6 +2023,25 @@ LGS_API lgs_status lgs_plan_elapsed_ms(const lgs_plan* p, float* ms) {
 
 LGS_API int64_t lgs_plan_launches(const lgs_plan* p) { return p ? p->launches_per_run : -1; }
 
+LGS_API lgs_status lgs_plan_set_profiling(lgs_ctx* ctx, lgs_plan* p, int32_t on) {
+  if (!ctx || !p || ctx != p->ctx) return fail(LGS_EINVAL, "plan / context mismatch");
+  if (p->profile == (on != 0)) return LGS_OK;
+  p->profile = on != 0;
+  return plan_capture(p);
+}
+
+LGS_API lgs_status lgs_plan_phase_times(const lgs_plan* p, double* ms) {
+  if (!p || !ms) return fail(LGS_EINVAL, "NULL argument");
+  if (!p->profile) return fail(LGS_EINVAL, "plan not profiling (lgs_plan_set_profiling)");
+  for (int i = 0; i < LGS_PHASE_COUNT; ++i) ms[i] = 0.0;
+  for (const auto& m : p->marks) {
+    float t = 0.f;
+    LGS_CUDA(cudaEventElapsedTime(&t, m.a, m.b));
+    ms[m.phase] += t;
+  }
+  return LGS_OK;
+}
+
 LGS_API lgs_status lgs_plan_destroy(lgs_plan* p) {
   if (!p) return LGS_OK;
   lgs_ctx* ctx = p->ctx;
@@ -1993,6 +2049,7 @@ LGS_API lgs_status lgs_plan_destroy(lgs_plan* p) {
   cudaStreamSynchronize(ctx->stream);
   if (p->exec) cudaGraphExecDestroy(p->exec);
   if (p->ev0) cudaEventDestroy(p->ev0);
+  plan_free_marks(p);
   if (p->ev1) cudaEventDestroy(p->ev1);
   if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
   delete p;

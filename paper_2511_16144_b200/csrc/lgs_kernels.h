@@ -24,7 +24,16 @@ struct ViewBufs {
   unsigned long long* dhist = nullptr;
   uint32_t* dslot = nullptr;
   uint32_t dbase = 0;  // near-plane bucket offset (depth_bucket)
+  // Gaussians that can hold a nonzero screen-space gradient (listed in some traversed tile list);
+  // null: every visible one.  The backward zeroes and reads only their accumulator rows.
+  uint8_t* active = nullptr;
 };
+
+// active[] of the depth-layered binning: the layer-A candidates idx_sorted[0, *ra) (the second
+// pass adds the Gaussians it lists); zero_active_rows clears their backward accumulator rows.
+void launch_mark_active(const uint32_t* idx_sorted, const uint32_t* ra, int64_t gauss_cap, uint8_t* active,
+                        cudaStream_t s);
+void launch_zero_active_rows(const ViewBufs& v, int64_t n, float* gacc, int slots, cudaStream_t s);
 
 // Tile lists for the blend kernels.
 struct TileLists {

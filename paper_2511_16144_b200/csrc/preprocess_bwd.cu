@@ -36,7 +36,9 @@ __global__ void __launch_bounds__(kPbThreads) preprocess_bwd_kernel(DevMap m, De
   const int64_t i = i0 + tid;
   const int64_t n = m.n;
   const int nloc = (int)min((int64_t)kPbThreads, n - i0);
-  if (DEG > 0) stage_rows_in<KS, SS, kPbThreads>(s_sh, m.sh + i0 * KS, nloc);
+  const bool live = i < n && (v.active ? v.active[i] != 0 : v.tiles[i] != 0);
+  // a block without a live Gaussian (most of them with the depth-layered binning) only writes zeros
+  if (DEG > 0 && __syncthreads_or(live)) stage_rows_in<KS, SS, kPbThreads>(s_sh, m.sh + i0 * KS, nloc);
   __syncthreads();
   float* my_sh = s_sh + tid * SS;
   float pose[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
@@ -48,7 +50,9 @@ __global__ void __launch_bounds__(kPbThreads) preprocess_bwd_kernel(DevMap m, De
       if (accum) p[idx] += val;
       else p[idx] = val;
     };
-    const bool visible = v.tiles[i] != 0;
+    // zero gradient unless the Gaussian sits in a traversed tile list (its accumulator row is then
+    // exactly zero: every term below vanishes)
+    const bool visible = live;
     if (!visible) {
 #pragma unroll
       for (int k = 0; k < KS; ++k) my_sh[k] = 0.f;
@@ -367,6 +371,34 @@ void launch_preprocess_bwd(const DevMap& m, const DevCam& c, const ViewBufs& v, 
     case 2: launch_pb_deg<2>(m, c, v, gacc, g, s); break;
     default: launch_pb_deg<3>(m, c, v, gacc, g, s); break;
   }
+}
+
+__global__ void mark_active_kernel(const uint32_t* __restrict__ idx_sorted, const uint32_t* __restrict__ ra,
+                                   uint8_t* __restrict__ active) {
+  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < *ra) active[idx_sorted[p]] = 1;
+}
+
+void launch_mark_active(const uint32_t* idx_sorted, const uint32_t* ra, int64_t gauss_cap, uint8_t* active,
+                        cudaStream_t s) {
+  if (gauss_cap <= 0) return;
+  mark_active_kernel<<<(unsigned)((gauss_cap + 255) / 256), 256, 0, s>>>(idx_sorted, ra, active);
+}
+
+// one warp per 32 rows: lanes clear the rows of live Gaussians, float4 at a time
+__global__ void zero_active_rows_kernel(const uint8_t* __restrict__ active, const uint32_t* __restrict__ tiles,
+                                        int64_t n, float4* __restrict__ gacc, int q_per_row) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (!(active ? active[i] != 0 : tiles[i] != 0)) return;
+  float4* row = gacc + i * q_per_row;
+  for (int q = 0; q < q_per_row; ++q) row[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
+void launch_zero_active_rows(const ViewBufs& v, int64_t n, float* gacc, int slots, cudaStream_t s) {
+  if (n == 0) return;
+  zero_active_rows_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(v.active, v.tiles, n,
+                                                                      reinterpret_cast<float4*>(gacc), slots / 4);
 }
 
 // fp64 pose accumulator [6] -> float [6] in place (the floats overwrite the first 24 bytes).

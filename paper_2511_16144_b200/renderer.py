@@ -572,6 +572,17 @@ class Plan:
         cam = make_camera(camera)
         check(_lib.load().lgs_plan_set_camera(self.ctx.h, self.h, C.byref(cam)))
 
+    def set_profiling(self, on: bool = True):
+        """Re-capture with per-phase event nodes (costs a few us per phase per replay)."""
+        check(_lib.load().lgs_plan_set_profiling(self.ctx.h, self.h, 1 if on else 0))
+
+    def phase_times(self) -> dict:
+        """Device ms per phase of the last replay (events recorded inside the graph)."""
+        L = _lib.load()
+        ms = (C.c_double * _lib.LGS_PHASE_COUNT)()
+        check(L.lgs_plan_phase_times(self.h, ms))
+        return {L.lgs_phase_name(i).decode(): ms[i] for i in range(_lib.LGS_PHASE_COUNT) if ms[i] > 0.0}
+
     def elapsed_ms(self) -> float:
         v = C.c_float()
         check(_lib.load().lgs_plan_elapsed_ms(self.h, C.byref(v)))

@@ -35,6 +35,12 @@ def main():
             plan.sync()
             ms.append(plan.elapsed_ms())
     print("plan launches", plan.launches, "ms per replay", [round(x, 4) for x in ms])
+    with torch.cuda.stream(stream):
+        plan.set_profiling(True)
+        plan.run()
+        plan.sync()
+    print("phases of a profiling replay (ms):", {k: round(v, 4) for k, v in plan.phase_times().items()},
+          "total", round(plan.elapsed_ms(), 4))
 
 
 if __name__ == "__main__":
