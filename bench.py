@@ -255,7 +255,10 @@ def run_ours(args):
     def enqueue():
         plan.run()
         if comm is not None:
-            comm.all_reduce(grads["flat"])  # 500k x 75 fp32 sum over NVLink, on the library's stream
+            # sum over ranks of the 500k x 75 fp32 gradient, exchanging only the rows some view
+            # reached (a few thousand with the depth-layered binning; lgs_allreduce_grads_sparse
+            # falls back to the dense NCCL all-reduce when they are not sparse)
+            comm.all_reduce_grads_sparse(dmap, grads)
         return None
 
     def step():
@@ -263,7 +266,7 @@ def run_ours(args):
         out = R.render(dmap, cam, targets=dtg, ctx=ctx)
         R.render_backward_loss_async(out, into=grads, pose_out=pose_host)
         if comm is not None:
-            comm.all_reduce(grads["flat"])
+            comm.all_reduce_grads_sparse(dmap, grads)
         torch.cuda.current_stream().synchronize()
         return out, grads
 
@@ -405,7 +408,8 @@ def run_ours(args):
         "config": {"workload": args.config, "image": f"{cam['width']}x{cam['height']}", "gaussians": n,
                    "sh_degree": int(math.isqrt(K) - 1), "feature_dim": d, "views_per_gpu_per_step": 1,
                    "loss": "L1 rgb+depth+feat (fused)", "pose_grad": True,
-                   "parallelism": (f"views over {world} GPU(s), fp32 grad all-reduce by liblgs.so (NCCL)" if world > 1
+                   "parallelism": (f"views over {world} GPU(s), fp32 row-sparse grad all-reduce by liblgs.so (NCCL)"
+                                   if world > 1
                                    else "1 GPU"),
                    "l2": "512 MiB L2 flush before every timed step"},
         "clocks": clk.summary(),

@@ -391,6 +391,13 @@ LGS_API lgs_status lgs_comm_destroy(lgs_ctx* ctx);
  * attribute buffers are one flat block, else one grouped NCCL launch). */
 LGS_API lgs_status lgs_allreduce_grads(lgs_ctx* ctx, const lgs_map* map, lgs_map_grads* grads);
 LGS_API lgs_status lgs_allreduce_f32(lgs_ctx* ctx, float* buf, int64_t count);
+/* Same result as lgs_allreduce_grads, exchanging only the rows (Gaussians) with a nonzero
+ * gradient on some rank: counts all-gathered (the host waits for them), then (index, row) records
+ * all-gathered and summed into every rank's dense buffer in rank order (identical on all ranks).
+ * Falls back to the dense all-reduce when the rows are not sparse; *rows_max (optional) = largest
+ * per-rank row count, -1 after a dense fallback. */
+LGS_API lgs_status lgs_allreduce_grads_sparse(lgs_ctx* ctx, const lgs_map* map, lgs_map_grads* grads,
+                                              int64_t* rows_max);
 
 #ifdef __cplusplus
 }

@@ -156,6 +156,7 @@ SIGNATURES = [
     ("lgs_comm_destroy", C.c_int, [C.c_void_p]),
     ("lgs_allreduce_grads", C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(LgsMapGrads)]),
     ("lgs_allreduce_f32", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64]),
+    ("lgs_allreduce_grads_sparse", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_int64)]),
 ]
 
 LGS_PHASE_COUNT = 12

@@ -1526,6 +1526,54 @@ LGS_API lgs_status lgs_allreduce_grads(lgs_ctx* ctx, const lgs_map* map, lgs_map
   LGS_NCCL(nc->GroupEnd());
   return LGS_OK;
 }
+LGS_API lgs_status lgs_allreduce_grads_sparse(lgs_ctx* ctx, const lgs_map* map, lgs_map_grads* grads,
+                                              int64_t* rows_max) {
+  if (!ctx || !map || !grads) return fail(LGS_EINVAL, "ctx/map/grads is NULL");
+  if (grads->memory != LGS_MEM_DEVICE) return fail(LGS_EINVAL, "all-reduce needs device gradient buffers");
+  if (!ctx->comm) return fail(LGS_EINVAL, "lgs_comm_init was not called on this context");
+  LGS_CUDA(cudaSetDevice(ctx->device));
+  const NcclApi* nc = nccl_api(nullptr);
+  cudaStream_t s = ctx->stream;
+  const int64_t n = map->dm.n;
+  const int world = ctx->comm_world;
+  float* ptr[6] = {grads->position, grads->rotation, grads->log_scale, grads->opacity_logit, grads->sh,
+                   grads->feature};
+  const int width[6] = {3, 4, 3, 1, 3 * map->dm.K, map->dm.d};
+  const int R = rows_values(width, ptr);
+  if (rows_max) *rows_max = 0;
+  if (n == 0 || R == 0) return LGS_OK;
+  uint32_t *list = nullptr, *cnt = nullptr;
+  LGS_TRY(dalloc(ctx, &list, (size_t)n));
+  LGS_TRY(dalloc(ctx, &cnt, (size_t)world + 1));  // [0] own count, [1 ..] all ranks'
+  launch_rows_scan(ptr, width, n, list, cnt, s);
+  LGS_NCCL(nc->AllGather(cnt, cnt + 1, 1, ncclUint32, ctx->comm, s));
+  std::vector<uint32_t> counts((size_t)world);
+  LGS_CUDA(cudaMemcpyAsync(counts.data(), cnt + 1, sizeof(uint32_t) * world, cudaMemcpyDeviceToHost, s));
+  LGS_CUDA(cudaStreamSynchronize(s));
+  int64_t maxc = 0;
+  for (uint32_t c : counts) maxc = std::max<int64_t>(maxc, c);
+  if (rows_max) *rows_max = maxc;
+  lgs_status st = LGS_OK;
+  if (maxc > 0) {
+    if (maxc * (int64_t)world * (R + 1) * 2 >= n * (int64_t)R) {  // not sparse enough: dense sum
+      st = lgs_allreduce_grads(ctx, map, grads);
+      if (rows_max) *rows_max = -1;
+    } else {
+      float *send = nullptr, *recv = nullptr;
+      LGS_TRY(dalloc(ctx, &send, (size_t)maxc * (R + 1)));
+      LGS_TRY(dalloc(ctx, &recv, (size_t)world * maxc * (R + 1)));
+      launch_rows_pack(ptr, width, n, list, cnt, maxc, send, s);
+      LGS_NCCL(nc->AllGather(send, recv, (size_t)maxc * (R + 1), ncclFloat32, ctx->comm, s));
+      launch_rows_apply(ptr, width, n, recv, cnt + 1, world, maxc, s);
+      dfree(ctx, send);
+      dfree(ctx, recv);
+    }
+  }
+  dfree(ctx, list);
+  dfree(ctx, cnt);
+  LGS_CUDA(cudaGetLastError());
+  return st;
+}
 #undef LGS_NCCL
 
 }  // extern "C"

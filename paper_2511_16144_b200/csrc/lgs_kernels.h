@@ -162,6 +162,16 @@ bool blend_bwd_mma_supported(int dp);
 void launch_blend_bwd_mma(const DevMap& m, const DevCam& c, const ViewBufs& v, const TileLists& tl,
                           const PixelState& ps, const BwdIn& in, float* gacc, cudaStream_t s);
 
+// Row-sparse gradient exchange (sparse_reduce.cu): ptr/width = the six MapGradients attributes
+// (feature is [d][N]).
+void launch_rows_scan(float* const ptr[6], const int width[6], int64_t n, uint32_t* list, uint32_t* count,
+                      cudaStream_t s);
+int rows_values(const int width[6], float* const ptr[6]);
+void launch_rows_pack(float* const ptr[6], const int width[6], int64_t n, const uint32_t* list, const uint32_t* count,
+                      int64_t max_rows, float* rec, cudaStream_t s);
+void launch_rows_apply(float* const ptr[6], const int width[6], int64_t n, const float* recs, const uint32_t* counts,
+                       int world, int64_t stride, cudaStream_t s);
+
 struct GradOut {
   float* position;      // [N][3]
   float* rotation;      // [N][4] w,x,y,z

@@ -83,6 +83,19 @@ class NativeComm:
         gs = _grads_struct(grads, False)
         _lib.check(_lib.load().lgs_allreduce_grads(self.ctx.h, dmap.h, gs))
 
+    def all_reduce_grads_sparse(self, dmap, grads) -> int:
+        """lgs_allreduce_grads_sparse: the dense sum, exchanging only the nonzero rows.  Returns the
+        largest per-rank row count (-1: fell back to the dense all-reduce)."""
+        import ctypes as C
+
+        from . import _lib
+        from .renderer import _grads_struct
+
+        gs = _grads_struct(grads, False)
+        rows = C.c_int64()
+        _lib.check(_lib.load().lgs_allreduce_grads_sparse(self.ctx.h, dmap.h, C.byref(gs), C.byref(rows)))
+        return rows.value
+
     def close(self):
         from . import _lib
 
@@ -132,3 +145,46 @@ def rasterizer_view_grads(dmap, cams, targets, ctx=None, pose_out: dict | None =
         return out
 
     return fn
+
+
+def sparse_sum_reference(rows_per_rank):
+    """Host restatement of lgs_allreduce_grads_sparse's merge (sparse_reduce.cu) for tests: given,
+    per rank, a dense [N][R] gradient, every rank's nonzero rows are zeroed and then re-added rank
+    by rank in rank order.  Returns the merged dense array (equal to the plain sum)."""
+    import numpy as np
+
+    out = np.array(rows_per_rank[0], dtype=np.float32, copy=True)
+    lists = [np.nonzero(np.any(g != 0, axis=1))[0] for g in rows_per_rank]
+    for idx in lists:
+        out[idx] = 0.0
+    for g, idx in zip(rows_per_rank, lists):
+        out[idx] = out[idx] + g[idx]
+    return out
+
+
+def sparse_all_reduce_host(dense, group=None):
+    """lgs_allreduce_grads_sparse's exchange over torch.distributed on host arrays (any backend;
+    the gloo tests run it): nonzero rows of a [N][R] float32 array are all-gathered as (index,
+    row) records and merged like sparse_sum_reference (listed rows zeroed, ranks added in rank
+    order), in place.  Returns the largest per-rank row count."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    idx = np.nonzero(np.any(dense != 0, axis=1))[0]
+    world = dist.get_world_size(group)
+    cnt = torch.tensor([idx.size], dtype=torch.int64)
+    counts = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(counts, cnt, group=group)
+    maxc = int(max(c.item() for c in counts))
+    rec = torch.zeros(maxc, dense.shape[1] + 1, dtype=torch.float32)
+    rec[:idx.size, 0] = torch.from_numpy(idx.astype(np.int32).view(np.float32))
+    rec[:idx.size, 1:] = torch.from_numpy(dense[idx])
+    recs = [torch.zeros_like(rec) for _ in range(world)]
+    dist.all_gather(recs, rec, group=group)
+    lists = [r[:int(c.item()), 0].numpy().view(np.int32) for r, c in zip(recs, counts)]
+    for li in lists:
+        dense[li] = 0.0
+    for r, c, li in zip(recs, counts, lists):
+        dense[li] += r[:int(c.item()), 1:].numpy()
+    return maxc

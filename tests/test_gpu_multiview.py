@@ -68,3 +68,29 @@ def test_native_comm_allreduce_grads_split_buffers():
         comm2 = multiview.NativeComm.__new__(multiview.NativeComm)
         comm2.ctx = ctx
         comm2.all_reduce(g["flat"])  # lgs_comm_destroy'd context: LGS_EINVAL
+
+
+def test_sparse_gradient_exchange_world1():
+    """lgs_allreduce_grads_sparse at world size 1: the scan / pack / zero / add kernels run (the
+    rows of the only rank) and must reproduce the gradient bit for bit; the row count is the number
+    of Gaussians with a nonzero gradient (a few thousand with the depth-layered binning)."""
+    ctx, dmap, cams, tgs = _setup(nviews=2)
+    comm = multiview.NativeComm(ctx, world=1, rank=0)
+    grads = R.alloc_grads(dmap.n, dmap.d, dmap.K, device=0)
+    for v in range(2):
+        out = R.render(dmap, cams[v], targets=tgs[v], ctx=ctx)
+        R.render_backward_l1(out, into=grads, accumulate=v > 0)
+    torch.cuda.synchronize()
+    before = grads["flat"].clone()
+    nz_rows = 0
+    for k in ("position", "rotation", "log_scale", "opacity_logit", "sh"):
+        g = grads[k].reshape(dmap.n, -1)
+        nz = g.ne(0).any(dim=1)
+        nz_rows = nz if isinstance(nz_rows, int) else nz_rows | nz
+    nz_rows = nz_rows | grads["feature"].reshape(-1, dmap.n).ne(0).any(dim=0)
+    rows = comm.all_reduce_grads_sparse(dmap, grads)
+    torch.cuda.synchronize()
+    assert rows == int(nz_rows.sum().item())
+    assert 0 < rows < dmap.n
+    assert torch.equal(grads["flat"], before)
+    comm.close()

@@ -102,3 +102,53 @@ def test_two_rank_allreduce_equals_single_process_sum():
         # fp32 sums in a different order (v0+v2, v1+v3, then the all-reduce): rounding only
         assert np.allclose(res[r], want, rtol=1e-5, atol=1e-6 * scale)
     assert np.array_equal(res[0], res[1])
+
+
+def _sparse_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    dense = _sparse_rank_grads(rank)
+    maxc = multiview.sparse_all_reduce_host(dense)
+    q.put((rank, dense.copy(), maxc))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _sparse_rank_grads(rank, n=5000, R=75):
+    """a rank's view gradient with the layered binning's shape: a few hundred nonzero rows,
+    overlapping between ranks"""
+    rng = np.random.default_rng(100 + rank)
+    g = np.zeros((n, R), np.float32)
+    rows = np.unique(np.concatenate([rng.choice(n, 300, replace=False), np.arange(40)]))
+    g[rows] = rng.standard_normal((rows.size, R)).astype(np.float32)
+    return g
+
+
+def test_sparse_gradient_exchange_equals_dense_sum():
+    """lgs_allreduce_grads_sparse's exchange (nonzero rows as (index, row) records, merged in rank
+    order) restated over gloo at world size 3: equal to the dense sum, bitwise identical on every
+    rank, and the same as the single-process merge (multiview.sparse_sum_reference)."""
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sparse_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r, dense, maxc = q.get(timeout=300)
+        res[r] = (dense, maxc)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    per_rank = [_sparse_rank_grads(r) for r in range(world)]
+    want = np.sum(per_rank, axis=0, dtype=np.float64)
+    merged = multiview.sparse_sum_reference(per_rank)
+    for r in range(world):
+        dense, maxc = res[r]
+        assert maxc == max(int(np.any(g != 0, axis=1).sum()) for g in per_rank)
+        assert np.array_equal(dense, res[0][0])
+        assert np.array_equal(dense, merged)
+        assert np.allclose(dense, want, rtol=1e-5, atol=1e-6)
