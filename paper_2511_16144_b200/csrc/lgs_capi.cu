@@ -234,6 +234,7 @@ struct lgs_saved {
   double* loss_sums = nullptr;  // lgs_mapping_loss partial sums [LOSS_COUNT]
   int64_t pairs = 0;
   int64_t vals_count = 0;  // entries allocated in vals (the lists live at the ranges' offsets)
+  bool lpt_order = true;    // `order` holds the longest-list-first tile order (else natural order)
   int ntiles = 0;
 };
 
@@ -763,15 +764,17 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
       {
         PhaseScope ph(ctx, PH_TILE_SORT);
         launch_layer_tile_lists(cand_rect, idx_sorted, ra, dc.tiles_x, ntiles, ra + 1, t->vals, t->ranges, s);
-        launch_tile_order(t->ranges, ntiles, t->order, s);  // longest tile list first
       }
-      ctx->launches += 8;
+      // Layered lists are short and even (every tile stops at its saturation): the blend kernels
+      // take tiles in natural order (measured as fast as longest-list-first, one launch less).
+      t->lpt_order = false;
+      ctx->launches += 7;
       if (targets) LGS_CUDA(cudaMemsetAsync(t->loss, 0, sizeof(double), s));
       FwdOut fo1 = fo;
       fo1.unfinished = unfinished;
       {
         PhaseScope ph(ctx, PH_BLEND_FWD);
-        launch_blend_fwd(map->dm, dc, t->vb, TileLists{t->vals, t->ranges, t->order, t->counter}, t->ps, fo1, s);
+        launch_blend_fwd(map->dm, dc, t->vb, TileLists{t->vals, t->ranges, nullptr, t->counter}, t->ps, fo1, s);
       }
       ctx->launches++;
       // pass 2, inside a captured plan as the body of a conditional node (skipped when every tile
@@ -952,7 +955,8 @@ lgs_status run_backward(lgs_ctx* ctx, const lgs_saved* t, const BwdIn& in_dev, l
   launch_zero_active_rows(t->vb, n, gacc, slots, s);  // rows the blend kernel may add into
   {
     PhaseScope ph(ctx, PH_BLEND_BWD);
-    launch_blend_bwd(t->dm, t->cam, t->vb, TileLists{t->vals, t->ranges, t->order, t->counter}, t->ps, in_dev, gacc, slots, s);
+    launch_blend_bwd(t->dm, t->cam, t->vb, TileLists{t->vals, t->ranges, t->lpt_order ? t->order : nullptr, t->counter},
+                     t->ps, in_dev, gacc, slots, s);
   }
   ctx->launches += 2;
 
