@@ -447,7 +447,8 @@ __global__ void __launch_bounds__(256) layer_count_kernel(const uint2* __restric
                                                           const uint32_t* __restrict__ count2,
                                                           uint32_t* __restrict__ cnt_enum,
                                                           uint32_t* __restrict__ total2,
-                                                          uint8_t* __restrict__ active) {
+                                                          uint8_t* __restrict__ active,
+                                                          float* __restrict__ gacc_zero) {
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   uint32_t c = 0, e = 0;
   if (s < n && *count2) {
@@ -460,7 +461,14 @@ __global__ void __launch_bounds__(256) layer_count_kernel(const uint2* __restric
       const uint32_t sw = (uint32_t)tiles_x + 1;
       c = sat[ty1 * sw + tx1] - sat[ty0 * sw + tx1] - sat[ty1 * sw + tx0] + sat[ty0 * sw + tx0];
       e = c ? tc : 0u;
-      if (c && active) active[g] = 1;  // listed for an unfinished tile: may receive gradients
+      if (c && active && !active[g]) {  // listed for an unfinished tile: may receive gradients
+        active[g] = 1;
+        if (gacc_zero) {  // fused step: its accumulator row is zeroed here (layer-A rows already were)
+          float4* row = reinterpret_cast<float4*>(gacc_zero + (size_t)g * 32);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) row[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
     }
   }
   if (s < n) cnt_enum[s] = e;
@@ -469,10 +477,11 @@ __global__ void __launch_bounds__(256) layer_count_kernel(const uint2* __restric
 }
 
 void launch_layer_count(const ViewBufs& v, const uint32_t* idx_sorted, int64_t n, int tiles_x, const uint32_t* sat,
-                        const uint32_t* count2, uint32_t* cnt_enum, uint32_t* total2, cudaStream_t s) {
+                        const uint32_t* count2, uint32_t* cnt_enum, uint32_t* total2, cudaStream_t s,
+                        float* gacc_zero) {
   if (n == 0) return;
   layer_count_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(v.rect, v.tiles, idx_sorted, n, tiles_x, sat, count2,
-                                                                 cnt_enum, total2, v.active);
+                                                                 cnt_enum, total2, v.active, gacc_zero);
 }
 
 }  // namespace lgs

@@ -235,6 +235,8 @@ struct lgs_saved {
   int64_t pairs = 0;
   int64_t vals_count = 0;  // entries allocated in vals (the lists live at the ranges' offsets)
   bool lpt_order = true;    // `order` holds the longest-list-first tile order (else natural order)
+  float* gacc = nullptr;    // fused-L1 step (blend_fused.cu): screen-space gradients of the forward
+  bool bwd_fused = false;
   int ntiles = 0;
 };
 
@@ -390,6 +392,7 @@ void free_saved(lgs_saved* t) {
   cudaSetDevice(ctx->device);
   dfree(ctx, t->vb.rec0);
   dfree(ctx, t->vb.active);
+  dfree(ctx, t->gacc);
   dfree(ctx, t->vb.rec1);
   dfree(ctx, t->vb.rect);
   dfree(ctx, t->vb.color);
@@ -761,6 +764,15 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
                                    idx_sorted, cand_rect, ra, s);
         launch_mark_active(idx_sorted, ra, gcapA, t->vb.active, s);
       }
+      // captured fused-L1 step: each tile's backward runs right after its forward (blend_fused.cu)
+      const bool fuse = ctx->capturing && targets && blend_fused_supported(dp) && slots_for(dp) == 32;
+      if (fuse) {
+        dfree(ctx, t->gacc);
+        LGS_TRY(dalloc(ctx, &t->gacc, (size_t)n * 32));
+        launch_zero_active_rows(t->vb, n, t->gacc, 32, s);
+        t->bwd_fused = true;
+        ctx->launches++;
+      }
       {
         PhaseScope ph(ctx, PH_TILE_SORT);
         launch_layer_tile_lists(cand_rect, idx_sorted, ra, dc.tiles_x, ntiles, ra + 1, t->vals, t->ranges, s);
@@ -774,7 +786,10 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
       fo1.unfinished = unfinished;
       {
         PhaseScope ph(ctx, PH_BLEND_FWD);
-        launch_blend_fwd(map->dm, dc, t->vb, TileLists{t->vals, t->ranges, nullptr, t->counter}, t->ps, fo1, s);
+        if (fuse)
+          launch_blend_fused_l1(map->dm, dc, t->vb, TileLists{t->vals, t->ranges, nullptr, t->counter}, fo1, t->gacc, s);
+        else
+          launch_blend_fwd(map->dm, dc, t->vb, TileLists{t->vals, t->ranges, nullptr, t->counter}, t->ps, fo1, s);
       }
       ctx->launches++;
       // pass 2, inside a captured plan as the body of a conditional node (skipped when every tile
@@ -795,7 +810,8 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
         {
           PhaseScope ph(ctx, PH_TILE_SORT);
           launch_depth_order_rest(t->vb, n, dc.near_plane, otemp, idx_sorted, s2);
-          launch_layer_count(t->vb, idx_sorted, n, dc.tiles_x, sat, count2, dkey_sorted, count2 + 1, s2);
+          launch_layer_count(t->vb, idx_sorted, n, dc.tiles_x, sat, count2, dkey_sorted, count2 + 1, s2,
+                             fuse ? t->gacc : nullptr);
           launch_scan_counts(dkey_sorted, n, incl, temp, temp_bytes, s2);
           const BinPass b{incl, count2 + 1, n, (uint32_t)cap, capA, unfinished, count2};
           launch_fast_binning(t->vb, idx_sorted, n, ntiles, dc.tiles_x, b, scratch_b, t->vals, t->ranges,
@@ -804,8 +820,12 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
         FwdOut fo2 = fo;
         {
           PhaseScope ph(ctx, PH_BLEND_FWD);
-          launch_blend_fwd(map->dm, dc, t->vb, TileLists{t->vals, t->ranges, order2, t->counter, count2}, t->ps, fo2,
-                           s2);
+          if (fuse)
+            launch_blend_fused_l1(map->dm, dc, t->vb, TileLists{t->vals, t->ranges, order2, t->counter, count2}, fo2,
+                                  t->gacc, s2);
+          else
+            launch_blend_fwd(map->dm, dc, t->vb, TileLists{t->vals, t->ranges, order2, t->counter, count2}, t->ps,
+                             fo2, s2);
         }
         if (cudaGetLastError() != cudaSuccess) st2 = fail(LGS_ECUDA, "layered binning pass 2 launch failed");
       }
@@ -951,14 +971,18 @@ lgs_status run_backward(lgs_ctx* ctx, const lgs_saved* t, const BwdIn& in_dev, l
   const int d = t->dm.d, K = t->dm.K;
   const int slots = slots_for(t->dm.dp);
   float* gacc = nullptr;
-  LGS_TRY(dalloc(ctx, &gacc, (size_t)n * slots));
-  launch_zero_active_rows(t->vb, n, gacc, slots, s);  // rows the blend kernel may add into
-  {
+  if (t->bwd_fused) {  // the fused-L1 forward already accumulated the screen-space gradients
+    gacc = t->gacc;
+  } else {
+    LGS_TRY(dalloc(ctx, &gacc, (size_t)n * slots));
+    launch_zero_active_rows(t->vb, n, gacc, slots, s);  // rows the blend kernel may add into
+  }
+  if (!t->bwd_fused) {
     PhaseScope ph(ctx, PH_BLEND_BWD);
     launch_blend_bwd(t->dm, t->cam, t->vb, TileLists{t->vals, t->ranges, t->lpt_order ? t->order : nullptr, t->counter},
                      t->ps, in_dev, gacc, slots, s);
+    ctx->launches += 2;
   }
-  ctx->launches += 2;
 
   GradOut go{};
   go.accumulate = grads ? grads->accumulate : 0;
@@ -1016,7 +1040,7 @@ lgs_status run_backward(lgs_ctx* ctx, const lgs_saved* t, const BwdIn& in_dev, l
   } else if (pose_grad) {
     LGS_CUDA(cudaMemcpyAsync(hpose, dpose, sizeof hpose, cudaMemcpyDeviceToHost, s));
   }
-  dfree(ctx, gacc);
+  if (!t->bwd_fused) dfree(ctx, gacc);
   dfree(ctx, gstage);
   dfree(ctx, dpose);
   if (host || (pose_grad && !async_pose)) LGS_CUDA(cudaStreamSynchronize(s));

@@ -151,10 +151,16 @@ void launch_layer_prep(const uint32_t* unfinished, const uint2* ranges, int tile
                        uint32_t* order2, uint32_t* count2, uint32_t* total2, const cudaGraphConditionalHandle* cond,
                        cudaStream_t s);
 void launch_layer_count(const ViewBufs& v, const uint32_t* idx_sorted, int64_t n, int tiles_x, const uint32_t* sat,
-                        const uint32_t* count2, uint32_t* cnt_enum, uint32_t* total2, cudaStream_t s);
+                        const uint32_t* count2, uint32_t* cnt_enum, uint32_t* total2, cudaStream_t s,
+                        float* gacc_zero = nullptr);
 
 void launch_blend_fwd(const DevMap& m, const DevCam& c, const ViewBufs& v, const TileLists& tl,
                       const PixelState& ps, const FwdOut& o, cudaStream_t s);
+// K5 + K6 fused for the fused-L1 loss (blend_fused.cu): images, loss and the screen-space
+// gradient accumulator gacc (rows of the listed Gaussians zeroed beforehand) in one pass per tile.
+bool blend_fused_supported(int dp);
+void launch_blend_fused_l1(const DevMap& m, const DevCam& c, const ViewBufs& v, const TileLists& tl, const FwdOut& o,
+                           float* gacc, cudaStream_t s);
 void launch_blend_bwd(const DevMap& m, const DevCam& c, const ViewBufs& v, const TileLists& tl,
                       const PixelState& ps, const BwdIn& in, float* gacc, int slots, cudaStream_t s);
 // Tensor-core variant (blend_bwd_mma.cu), used by launch_blend_bwd when supported.
