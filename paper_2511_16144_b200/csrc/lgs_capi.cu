@@ -1401,6 +1401,10 @@ LGS_API lgs_status lgs_debug_projected(lgs_ctx* ctx, const lgs_saved* t, uint8_t
   }
   LGS_CUDA(cudaStreamSynchronize(s));
   for (size_t i = 0; i < n; ++i) {
+    if (tiles[i] == 0) {  // K1 leaves a culled Gaussian's records unwritten: report zeros
+      r0[i] = r1[i] = col[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      rect[i] = make_uint2(0u, 0u);
+    }
     if (visible) visible[i] = tiles[i] != 0;
     if (u) u[i] = r0[i].x;
     if (v) v[i] = r0[i].y;

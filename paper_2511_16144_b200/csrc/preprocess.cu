@@ -57,10 +57,13 @@ template <int DEG>
 __global__ void __launch_bounds__(kPreThreads) preprocess_kernel(DevMap m, DevCam c, ViewBufs v) {
   constexpr int KS = 3 * (DEG + 1) * (DEG + 1);
   constexpr int SS = KS + 1 - KS % 2;  // odd row stride: conflict-free per-thread rows
-  __shared__ float s_sh[DEG > 0 ? kPreThreads * SS : 1];
+  // SH rows of 16-byte multiples (degrees 1 and 3) are read per visible Gaussian straight from
+  // HBM (the culled ones' coefficients are never fetched); other degrees stage the CTA's rows
+  constexpr bool DIRECT = DEG > 0 && KS % 4 == 0;
+  __shared__ float s_sh[DEG > 0 && !DIRECT ? kPreThreads * SS : 1];
   const int64_t i0 = (int64_t)blockIdx.x * kPreThreads;
   const int64_t i = i0 + threadIdx.x;
-  if (DEG > 0) {  // the CTA's [128][K][3] SH block, loaded coalesced (float4)
+  if (DEG > 0 && !DIRECT) {  // the CTA's [128][K][3] SH block, loaded coalesced (float4)
     const int nloc = (int)min((int64_t)kPreThreads, m.n - i0);
     stage_rows_in<KS, SS, kPreThreads>(s_sh, m.sh + i0 * KS, nloc);
     __syncthreads();
@@ -139,13 +142,9 @@ __global__ void __launch_bounds__(kPreThreads) preprocess_kernel(DevMap m, DevCa
     y1 = (int)fminf(fminf(Hf - 1.0f, ceilf(vv + radius)), ceilf(vv + ey));
     ok = x0 <= x1 && y0 <= y1;
   }
-  if (!ok) {
+  if (!ok) {  // culled: no tiles, sorts last; its records are never read (left unwritten)
     v.tiles[i] = 0;
     v.dkey[i] = 0xffffffffu;
-    v.rec0[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    v.rec1[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    v.rect[i] = make_uint2(0u, 0u);
-    v.color[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     return;
   }
   v.rec0[i] = make_float4(u, vv, t2, opacity);
@@ -167,19 +166,34 @@ __global__ void __launch_bounds__(kPreThreads) preprocess_kernel(DevMap m, DevCa
     const float* sh = m.sh + i * 3;
     col[0] = sh[0]; col[1] = sh[1]; col[2] = sh[2];
   } else {
-    const float* sh = s_sh + threadIdx.x * SS;
     float dx = P0 - c.cc[0], dy = P1 - c.cc[1], dz = P2 - c.cc[2];
     const float dn = sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
     const float idn = 1.0f / dn;
     dx *= idn; dy *= idn; dz *= idn;
     float b[16];
     sh_basis_f32(DEG, dx, dy, dz, b);
+    if (DIRECT) {
+      // element j = 3 k + ch of the [K][3] row: each channel still accumulates in k order
+      const float4* row = reinterpret_cast<const float4*>(m.sh + i * KS);
 #pragma unroll
-    for (int ch = 0; ch < 3; ++ch) {
-      float acc = sh[ch];
+      for (int q = 0; q < KS / 4; ++q) {
+        const float4 v4 = __ldg(row + q);
+        const float e4[4] = {v4.x, v4.y, v4.z, v4.w};
 #pragma unroll
-      for (int k = 1; k < K; ++k) acc = fmaf(b[k], sh[k * 3 + ch], acc);
-      col[ch] = acc;
+        for (int t = 0; t < 4; ++t) {
+          const int j = 4 * q + t, k = j / 3, ch = j % 3;
+          col[ch] = k == 0 ? e4[t] : fmaf(b[k], e4[t], col[ch]);
+        }
+      }
+    } else {
+      const float* sh = s_sh + threadIdx.x * SS;
+#pragma unroll
+      for (int ch = 0; ch < 3; ++ch) {
+        float acc = sh[ch];
+#pragma unroll
+        for (int k = 1; k < K; ++k) acc = fmaf(b[k], sh[k * 3 + ch], acc);
+        col[ch] = acc;
+      }
     }
   }
   v.color[i] = make_float4(col[0], col[1], col[2], 0.0f);
