@@ -371,21 +371,42 @@ size_t layer_a_cap(int64_t pairs_cap, int ntiles, uint32_t div) {
 }
 
 
-// One CTA: unfinished-tile summed-area table sat[(ty + 1) * (tiles_x + 1) + tx + 1], the unfinished
-// tiles in longest-list-first order (order2, count2) and, inside a captured plan, the conditional
-// that runs the second pass only when some tile is unfinished.
+// One CTA: the number of unfinished tiles, and inside a captured plan the conditional that runs the
+// second pass only when there is one.
+__global__ void __launch_bounds__(1024) layer_flag_kernel(const uint32_t* __restrict__ unfinished, int ntiles,
+                                                          uint32_t* __restrict__ count2, uint32_t* __restrict__ total2,
+                                                          cudaGraphConditionalHandle cond, int use_cond) {
+  __shared__ uint32_t s_w[32];
+  uint32_t c = 0;
+  for (int t = threadIdx.x; t < ntiles; t += blockDim.x) c += unfinished[t] ? 1u : 0u;
+  c = __reduce_add_sync(0xffffffffu, c);
+  if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t tot = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += s_w[w];
+    *count2 = tot;
+    *total2 = 0u;
+    if (use_cond) cudaGraphSetConditional(cond, tot ? 1u : 0u);
+  }
+}
+
+void launch_layer_flag(const uint32_t* unfinished, int ntiles, uint32_t* count2, uint32_t* total2,
+                       const cudaGraphConditionalHandle* cond, cudaStream_t s) {
+  layer_flag_kernel<<<1, 1024, 0, s>>>(unfinished, ntiles, count2, total2, cond ? *cond : cudaGraphConditionalHandle{},
+                                       cond ? 1 : 0);
+}
+
+// One CTA (first kernel of the second pass): unfinished-tile summed-area table
+// sat[(ty + 1) * (tiles_x + 1) + tx + 1] and the unfinished tiles in longest-list-first order.
 __global__ void __launch_bounds__(1024) layer_prep_kernel(const uint32_t* __restrict__ unfinished,
                                                           const uint2* __restrict__ ranges, int tiles_x, int tiles_y,
-                                                          uint32_t* __restrict__ sat, uint32_t* __restrict__ order2,
-                                                          uint32_t* __restrict__ count2,
-                                                          uint32_t* __restrict__ total2,
-                                                          cudaGraphConditionalHandle cond, int use_cond) {
+                                                          uint32_t* __restrict__ sat, uint32_t* __restrict__ order2) {
   extern __shared__ uint32_t s_sat[];  // (tiles_y + 1) x (tiles_x + 1)
   const int ntiles = tiles_x * tiles_y;
   const int sw = tiles_x + 1, nsat = sw * (tiles_y + 1);
-  __shared__ uint32_t s_cnt[33], s_pos[33], s_total;
+  __shared__ uint32_t s_cnt[33], s_pos[33];
   if (threadIdx.x < 33) s_cnt[threadIdx.x] = 0;
-  if (threadIdx.x == 0) s_total = 0;
   for (int i = threadIdx.x; i < nsat; i += blockDim.x) {
     const int y = i / sw, x = i - y * sw;
     s_sat[i] = (x && y && unfinished[(y - 1) * tiles_x + x - 1]) ? 1u : 0u;
@@ -402,7 +423,6 @@ __global__ void __launch_bounds__(1024) layer_prep_kernel(const uint32_t* __rest
     if (!unfinished[t]) continue;
     const uint32_t len = ranges[t].y - ranges[t].x;
     atomicAdd(&s_cnt[len ? 32 - __clz(len) : 0], 1u);
-    atomicAdd(&s_total, 1u);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -411,9 +431,6 @@ __global__ void __launch_bounds__(1024) layer_prep_kernel(const uint32_t* __rest
       s_pos[b] = run;
       run += s_cnt[b];
     }
-    *count2 = s_total;
-    *total2 = 0u;
-    if (use_cond) cudaGraphSetConditional(cond, s_total ? 1u : 0u);
   }
   __syncthreads();
   for (int t = threadIdx.x; t < ntiles; t += blockDim.x) {
@@ -424,8 +441,7 @@ __global__ void __launch_bounds__(1024) layer_prep_kernel(const uint32_t* __rest
 }
 
 void launch_layer_prep(const uint32_t* unfinished, const uint2* ranges, int tiles_x, int tiles_y, uint32_t* sat,
-                       uint32_t* order2, uint32_t* count2, uint32_t* total2, const cudaGraphConditionalHandle* cond,
-                       cudaStream_t s) {
+                       uint32_t* order2, cudaStream_t s) {
   const size_t smem = sizeof(uint32_t) * (size_t)(tiles_x + 1) * (tiles_y + 1);
   static bool attr_set = false;
   if (!attr_set) {
@@ -433,8 +449,7 @@ void launch_layer_prep(const uint32_t* unfinished, const uint2* ranges, int tile
                          (int)(sizeof(uint32_t) * 9 * 1024 * 4));
     attr_set = true;
   }
-  layer_prep_kernel<<<1, 1024, smem, s>>>(unfinished, ranges, tiles_x, tiles_y, sat, order2, count2, total2,
-                                       cond ? *cond : cudaGraphConditionalHandle{}, cond ? 1 : 0);
+  layer_prep_kernel<<<1, 1024, smem, s>>>(unfinished, ranges, tiles_x, tiles_y, sat, order2);
 }
 
 // Second layered pass: Gaussian s (depth order) takes part iff its tile rect holds an unfinished

@@ -131,6 +131,8 @@ struct DepthOut {
   uint32_t* idx_sorted;  // [n] map index in (depth, index) order (culled last, any order)
   uint32_t* cnt_sorted;  // [n] or null: tile counts in that order
   uint2* cand_rect;      // [n] or null: tile rects in that order (positions < R_A)
+  uint8_t* active;       // or null: layer-A Gaussians flagged for the backward (lgs_kernels.h) ...
+  float* gacc_zero;      // ... and, for the fused step, their accumulator rows (32 floats) zeroed
 };
 
 __device__ __forceinline__ void depth_emit(const DepthOut& o, const uint32_t* __restrict__ tiles,
@@ -138,7 +140,15 @@ __device__ __forceinline__ void depth_emit(const DepthOut& o, const uint32_t* __
                                            uint32_t cand_end) {
   o.idx_sorted[pos] = g;
   if (o.cnt_sorted) o.cnt_sorted[pos] = tiles[g];
-  if (o.cand_rect && pos < cand_end) o.cand_rect[pos] = tile_rect(rect[g]);
+  if (pos < cand_end) {
+    if (o.cand_rect) o.cand_rect[pos] = tile_rect(rect[g]);
+    if (o.active) o.active[g] = 1;
+    if (o.gacc_zero) {
+      float4* row = reinterpret_cast<float4*>(o.gacc_zero + (size_t)g * 32);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) row[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
 }
 
 // big[0] = number of big buckets, big[1 ..] their ids
@@ -302,7 +312,7 @@ void launch_depth_order(const ViewBufs& v, int64_t n, float near_plane, void* te
   const DepthCarve c = carve(temp, n, near_plane);
   depth_front(v, n, c, s);
   const unsigned grid = (unsigned)((n + 255) / 256);
-  const DepthOut o{idx_sorted, cnt_sorted, nullptr};
+  const DepthOut o{idx_sorted, cnt_sorted, nullptr, nullptr, nullptr};
   depth_scatter_kernel<<<grid, 256, 0, s>>>(v.dkey, n, c.base, c.off, c.slot, nullptr, kDepthAll, c.tmp, nullptr, nullptr);
   depth_rank_kernel<<<grid, 256, 0, s>>>(c.tmp, n, c.base, c.off, v.tiles, v.rect, nullptr, kDepthAll, o, c.big_a);
   depth_big_kernel<<<8, 1024, 0, s>>>(c.tmp, c.off, v.tiles, v.rect, nullptr, c.big_a, c.scratch, c.cursor, o);
@@ -334,7 +344,7 @@ void launch_depth_scan(int64_t n, float near_plane, void* temp, const uint32_t**
 
 void launch_depth_order_layer_a(const ViewBufs& v, int64_t n, float near_plane, void* temp, uint32_t div,
                                 uint32_t min_pairs, int64_t gauss_cap, uint32_t cap_a, uint32_t* idx_sorted,
-                                uint2* cand_rect, uint32_t* ra, cudaStream_t s) {
+                                uint2* cand_rect, uint32_t* ra, uint8_t* active, float* gacc_zero, cudaStream_t s) {
   if (n == 0) {
     cudaMemsetAsync(ra, 0, sizeof(uint32_t), s);
     return;
@@ -344,7 +354,7 @@ void launch_depth_order_layer_a(const ViewBufs& v, int64_t n, float near_plane, 
   cudaMemsetAsync(c.big_a, 0, sizeof(uint32_t), s);
   cudaMemsetAsync(c.cursor, 0, sizeof(uint32_t), s);  // bitonic scratch allocator
   depth_cut_kernel<<<(kDepthBuckets + 255) / 256, 256, 0, s>>>(c.off, div, min_pairs, gauss_cap, cap_a, c.cut);
-  const DepthOut o{idx_sorted, nullptr, cand_rect};
+  const DepthOut o{idx_sorted, nullptr, cand_rect, active, gacc_zero};
   const int64_t ga = std::min<int64_t>(n, gauss_cap);
   depth_scatter_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(v.dkey, n, c.base, c.off, c.slot, c.cut,
                                                                     kDepthLayerA, c.tmp, ra, nullptr);
@@ -413,7 +423,7 @@ void launch_depth_order_rest(const ViewBufs& v, int64_t n, float near_plane, voi
   if (n == 0) return;
   const DepthCarve c = carve(temp, n, near_plane);
   const unsigned grid = (unsigned)((n + 255) / 256);
-  const DepthOut o{idx_sorted, nullptr, nullptr};
+  const DepthOut o{idx_sorted, nullptr, nullptr, nullptr, nullptr};
   cudaMemsetAsync(c.big_r, 0, sizeof(uint32_t), s);
   cudaMemsetAsync(c.cursor + 1, 0, sizeof(uint32_t), s);  // culled slots
   depth_scatter_kernel<<<grid, 256, 0, s>>>(v.dkey, n, c.base, c.off, c.slot, c.cut, kDepthRest, c.tmp, nullptr,

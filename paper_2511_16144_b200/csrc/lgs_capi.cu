@@ -758,20 +758,18 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
       LGS_TRY(dalloc(ctx, reinterpret_cast<uint8_t**>(&scratch_b), fast_binning_scratch_bytes(cap, n, ntiles)));
       LGS_CUDA(cudaMemsetAsync(unfinished, 0, sizeof(uint32_t) * ntiles, s));
       LGS_CUDA(cudaMemsetAsync(ra + 1, 0, sizeof(uint32_t), s));
-      {
-        PhaseScope ph(ctx, PH_DEPTH_SORT);
-        launch_depth_order_layer_a(t->vb, n, dc.near_plane, otemp, kLayerDiv, kLayerMinPairs, gcapA, capA,
-                                   idx_sorted, cand_rect, ra, s);
-        launch_mark_active(idx_sorted, ra, gcapA, t->vb.active, s);
-      }
-      // captured fused-L1 step: each tile's backward runs right after its forward (blend_fused.cu)
+      // captured fused-L1 step: each tile's backward runs right after its forward (blend_fused.cu);
+      // the depth order flags the layer-A Gaussians active and zeroes their accumulator rows
       const bool fuse = ctx->capturing && targets && blend_fused_supported(dp) && slots_for(dp) == 32;
       if (fuse) {
         dfree(ctx, t->gacc);
         LGS_TRY(dalloc(ctx, &t->gacc, (size_t)n * 32));
-        launch_zero_active_rows(t->vb, n, t->gacc, 32, s);
         t->bwd_fused = true;
-        ctx->launches++;
+      }
+      {
+        PhaseScope ph(ctx, PH_DEPTH_SORT);
+        launch_depth_order_layer_a(t->vb, n, dc.near_plane, otemp, kLayerDiv, kLayerMinPairs, gcapA, capA,
+                                   idx_sorted, cand_rect, ra, t->vb.active, fuse ? t->gacc : nullptr, s);
       }
       {
         PhaseScope ph(ctx, PH_TILE_SORT);
@@ -780,7 +778,7 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
       // Layered lists are short and even (every tile stops at its saturation): the blend kernels
       // take tiles in natural order (measured as fast as longest-list-first, one launch less).
       t->lpt_order = false;
-      ctx->launches += 7;
+      ctx->launches += 6;
       if (targets) LGS_CUDA(cudaMemsetAsync(t->loss, 0, sizeof(double), s));
       FwdOut fo1 = fo;
       fo1.unfinished = unfinished;
@@ -799,8 +797,7 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
       if (use_cond) LGS_TRY(cond_create(ctx, &cond));
       {
         PhaseScope ph(ctx, PH_TILE_SORT);
-        launch_layer_prep(unfinished, t->ranges, dc.tiles_x, dc.tiles_y, sat, order2, count2, count2 + 1,
-                          use_cond ? &cond : nullptr, s);
+        launch_layer_flag(unfinished, ntiles, count2, count2 + 1, use_cond ? &cond : nullptr, s);
       }
       ctx->launches++;
       if (use_cond) LGS_TRY(cond_begin(ctx, cond));
@@ -809,6 +806,7 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
         cudaStream_t s2 = ctx->stream;  // the conditional body's capture stream inside a plan
         {
           PhaseScope ph(ctx, PH_TILE_SORT);
+          launch_layer_prep(unfinished, t->ranges, dc.tiles_x, dc.tiles_y, sat, order2, s2);
           launch_depth_order_rest(t->vb, n, dc.near_plane, otemp, idx_sorted, s2);
           launch_layer_count(t->vb, idx_sorted, n, dc.tiles_x, sat, count2, dkey_sorted, count2 + 1, s2,
                              fuse ? t->gacc : nullptr);
@@ -829,7 +827,7 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
         }
         if (cudaGetLastError() != cudaSuccess) st2 = fail(LGS_ECUDA, "layered binning pass 2 launch failed");
       }
-      ctx->launches += 12;
+      ctx->launches += 13;
       if (use_cond) LGS_TRY(cond_end(ctx));
       LGS_TRY(st2);
       dfree(ctx, scratch_b);

@@ -29,10 +29,8 @@ struct ViewBufs {
   uint8_t* active = nullptr;
 };
 
-// active[] of the depth-layered binning: the layer-A candidates idx_sorted[0, *ra) (the second
-// pass adds the Gaussians it lists); zero_active_rows clears their backward accumulator rows.
-void launch_mark_active(const uint32_t* idx_sorted, const uint32_t* ra, int64_t gauss_cap, uint8_t* active,
-                        cudaStream_t s);
+// active[] of the depth-layered binning: the layer-A candidates (flagged by the depth order; the
+// second pass adds the Gaussians it lists); zero_active_rows clears their backward accumulator rows.
 void launch_zero_active_rows(const ViewBufs& v, int64_t n, float* gacc, int slots, cudaStream_t s);
 
 // Tile lists for the blend kernels.
@@ -110,7 +108,7 @@ void launch_depth_prepare(int64_t n, float near_plane, void* temp, ViewBufs* v, 
 void launch_depth_scan(int64_t n, float near_plane, void* temp, const uint32_t** pairs_out, cudaStream_t s);
 void launch_depth_order_layer_a(const ViewBufs& v, int64_t n, float near_plane, void* temp, uint32_t div,
                                 uint32_t min_pairs, int64_t gauss_cap, uint32_t cap_a, uint32_t* idx_sorted,
-                                uint2* cand_rect, uint32_t* ra, cudaStream_t s);
+                                uint2* cand_rect, uint32_t* ra, uint8_t* active, float* gacc_zero, cudaStream_t s);
 void launch_depth_order_rest(const ViewBufs& v, int64_t n, float near_plane, void* temp, uint32_t* idx_sorted,
                              cudaStream_t s);
 // Layer-A tile lists (one warp per tile scanning the depth-ordered candidates, order-preserving
@@ -147,9 +145,13 @@ void launch_fast_binning(const ViewBufs& v, const uint32_t* idx_sorted, int64_t 
 // (at most gauss_cap Gaussians), then the complete lists of the tiles layer A left unsaturated.
 constexpr uint32_t kLayerMinPairs = 1u << 16;  // layer A takes at least this many pairs (or all)
 size_t layer_a_cap(int64_t pairs_cap, int ntiles, uint32_t div);
+// layer_flag: counts the unfinished tiles (count2), resets total2 and, inside a plan, sets the
+// conditional of the second pass; layer_prep (first kernel of that pass): summed-area table of the
+// unfinished mask and their longest-list-first order.
+void launch_layer_flag(const uint32_t* unfinished, int ntiles, uint32_t* count2, uint32_t* total2,
+                       const cudaGraphConditionalHandle* cond, cudaStream_t s);
 void launch_layer_prep(const uint32_t* unfinished, const uint2* ranges, int tiles_x, int tiles_y, uint32_t* sat,
-                       uint32_t* order2, uint32_t* count2, uint32_t* total2, const cudaGraphConditionalHandle* cond,
-                       cudaStream_t s);
+                       uint32_t* order2, cudaStream_t s);
 void launch_layer_count(const ViewBufs& v, const uint32_t* idx_sorted, int64_t n, int tiles_x, const uint32_t* sat,
                         const uint32_t* count2, uint32_t* cnt_enum, uint32_t* total2, cudaStream_t s,
                         float* gacc_zero = nullptr);

@@ -373,18 +373,6 @@ void launch_preprocess_bwd(const DevMap& m, const DevCam& c, const ViewBufs& v, 
   }
 }
 
-__global__ void mark_active_kernel(const uint32_t* __restrict__ idx_sorted, const uint32_t* __restrict__ ra,
-                                   uint8_t* __restrict__ active) {
-  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p < *ra) active[idx_sorted[p]] = 1;
-}
-
-void launch_mark_active(const uint32_t* idx_sorted, const uint32_t* ra, int64_t gauss_cap, uint8_t* active,
-                        cudaStream_t s) {
-  if (gauss_cap <= 0) return;
-  mark_active_kernel<<<(unsigned)((gauss_cap + 255) / 256), 256, 0, s>>>(idx_sorted, ra, active);
-}
-
 // one warp per 32 rows: lanes clear the rows of live Gaussians, float4 at a time
 __global__ void zero_active_rows_kernel(const uint8_t* __restrict__ active, const uint32_t* __restrict__ tiles,
                                         int64_t n, float4* __restrict__ gacc, int q_per_row) {
