@@ -66,10 +66,14 @@ __global__ void __launch_bounds__(256) depth_hist_kernel(const uint32_t* __restr
   if (i < n && b == kDepthBuckets) slot[i] = s_base + local;
 }
 
-// Layer A of the depth-layered binning = buckets [0, cut[0]): the smallest bucket prefix whose
+// Layer A of the depth-layered binning = buckets [0, cut_end): the smallest bucket prefix whose
 // pairs reach max(min(P, min_pairs), P / div), shortened to at most gauss_cap Gaussians and cap_a
-// pairs.  cut[0] is pre-set to ~0 and lowered with atomicMin by the (unique) threads that find the
-// crossing / the last feasible bucket.
+// pairs.  Stored as cut = kDepthBuckets + 1 - cut_end (zero-initialized with the other scalars) and
+// raised with atomicMax by the (unique) threads that find the crossing / the last feasible bucket.
+__device__ __forceinline__ uint32_t cut_end_of(const uint32_t* cut) {
+  return (uint32_t)kDepthBuckets + 1u - max(*cut, 1u);
+}
+
 __global__ void depth_cut_kernel(const u64* __restrict__ off, uint32_t div, uint32_t min_pairs, int64_t gauss_cap,
                                  uint32_t cap_a, uint32_t* __restrict__ cut) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
@@ -77,16 +81,17 @@ __global__ void depth_cut_kernel(const u64* __restrict__ off, uint32_t div, uint
   const uint32_t P = prs_of(off[kDepthBuckets]);
   const uint32_t target = max(min(P, min_pairs), P / div);
   const u64 ex = off[b], in = off[b + 1];
-  if (prs_of(in) >= target && prs_of(ex) < target) atomicMin(cut, (uint32_t)b + 1u);
+  auto offer = [&](uint32_t end) { atomicMax(cut, (uint32_t)kDepthBuckets + 1u - end); };
+  if (prs_of(in) >= target && prs_of(ex) < target) offer((uint32_t)b + 1u);
   const bool feas = (int64_t)cnt_of(in) <= gauss_cap && prs_of(in) <= cap_a;
-  if (b == 0 && !feas) atomicMin(cut, 0u);
+  if (b == 0 && !feas) offer(0u);
   if (feas) {
     bool next_feas = false;
     if (b + 1 < kDepthBuckets) {
       const u64 in2 = off[b + 2];
       next_feas = (int64_t)cnt_of(in2) <= gauss_cap && prs_of(in2) <= cap_a;
     }
-    if (!next_feas) atomicMin(cut, (uint32_t)b + 1u);
+    if (!next_feas) offer((uint32_t)b + 1u);
   }
 }
 
@@ -101,11 +106,11 @@ __global__ void depth_scatter_kernel(const uint32_t* __restrict__ dkey, int64_t 
                                      const uint32_t* __restrict__ cut, int mode, uint2* __restrict__ tmp,
                                      uint32_t* __restrict__ ra_out, uint32_t* __restrict__ culled_cursor) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i == 0 && ra_out) *ra_out = cnt_of(off[*cut]);  // R_A: Gaussians in layer A
+  if (i == 0 && ra_out) *ra_out = cnt_of(off[cut_end_of(cut)]);  // R_A: Gaussians in layer A
   if (i >= n) return;
   const uint32_t k = dkey[i];
   const uint32_t b = depth_bucket(k, base);
-  if (!bucket_selected(b, mode, cut ? *cut : 0u)) return;
+  if (!bucket_selected(b, mode, cut ? cut_end_of(cut) : 0u)) return;
   if (culled_cursor && b == kDepthBuckets) {  // slots of culled Gaussians (any order) handed out here
     const unsigned act = __activemask();
     const unsigned peers = __match_any_sync(act, 1u);
@@ -151,13 +156,13 @@ __device__ __forceinline__ void depth_emit(const DepthOut& o, const uint32_t* __
   }
 }
 
-// big[0] = number of big buckets, big[1 ..] their ids
+// big buckets: *big_n of them, ids in big_ids
 __global__ void depth_rank_kernel(const uint2* __restrict__ tmp, int64_t n, uint32_t base,
                                   const u64* __restrict__ off, const uint32_t* __restrict__ tiles,
                                   const uint2* __restrict__ rect, const uint32_t* __restrict__ cut, int mode,
-                                  DepthOut o, uint32_t* __restrict__ big) {
+                                  DepthOut o, uint32_t* __restrict__ big_n, uint32_t* __restrict__ big_ids) {
   const int64_t p0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const uint32_t ra = cut ? cnt_of(off[*cut]) : 0u;  // Gaussians in layer A
+  const uint32_t ra = cut ? cnt_of(off[cut_end_of(cut)]) : 0u;  // Gaussians in layer A
   const int64_t p = mode == kDepthRest ? p0 + ra : p0;
   if (p >= (mode == kDepthLayerA ? (int64_t)ra : n)) return;
   const uint2 me = tmp[p];
@@ -169,7 +174,7 @@ __global__ void depth_rank_kernel(const uint2* __restrict__ tmp, int64_t n, uint
   }
   const uint32_t lo = cnt_of(off[b]), hi = cnt_of(off[b + 1]);
   if (hi - lo > kMaxRankBucket) {
-    if (p == lo) big[1 + atomicAdd(big, 1u)] = b;
+    if (p == lo) big_ids[atomicAdd(big_n, 1u)] = b;
     return;
   }
   uint32_t rank = 0;
@@ -183,14 +188,15 @@ __global__ void __launch_bounds__(1024) depth_big_kernel(const uint2* __restrict
                                                          const uint32_t* __restrict__ tiles,
                                                          const uint2* __restrict__ rect,
                                                          const uint32_t* __restrict__ cut,
-                                                         const uint32_t* __restrict__ big,
+                                                         const uint32_t* __restrict__ big_n,
+                                                         const uint32_t* __restrict__ big_ids,
                                                          unsigned long long* __restrict__ scratch,
                                                          uint32_t* __restrict__ cursor, DepthOut o) {
-  const uint32_t nbig = big[0];
-  const uint32_t ra = cut ? cnt_of(off[*cut]) : 0u;
+  const uint32_t nbig = *big_n;
+  const uint32_t ra = cut ? cnt_of(off[cut_end_of(cut)]) : 0u;
   __shared__ uint32_t s_base;
   for (uint32_t k = blockIdx.x; k < nbig; k += gridDim.x) {
-    const uint32_t b = big[1 + k];
+    const uint32_t b = big_ids[k];
     const uint32_t lo = cnt_of(off[b]), m = cnt_of(off[b + 1]) - lo;
     uint32_t M = 1;
     while (M < m) M <<= 1;
@@ -248,14 +254,18 @@ size_t depth_order_temp_bytes(int64_t n) {
                        + 2 * nn                                 // tmp (uint2)
                        + 4 * nn                                 // scratch (2n u64)
                        + align_words((size_t)n / kMaxRankBucket + 2) * 2  // big lists (layer A, rest)
-                       + 64 * 3;                                // cursor, cut
+                       + 64;                                    // scalars
   return sizeof(uint32_t) * words + scan_bytes_for() + 1024;
 }
+
+// scalars (zeroed together): cut, big-bucket counts of layer A / the rest, bitonic scratch
+// allocator, culled-slot allocator
+enum { kScCut = 0, kScBigA = 1, kScBigR = 2, kScScratch = 3, kScCulled = 4, kScalars = 8 };
 
 struct DepthCarve {
   unsigned long long *hist, *off;
   uint2* tmp;
-  uint32_t *slot, *big_a, *big_r, *cursor, *cut;
+  uint32_t *slot, *big_a, *big_r, *sc;
   unsigned long long* scratch;
   void* scan_temp;
   size_t scan_bytes;
@@ -281,10 +291,8 @@ static DepthCarve carve(void* temp, int64_t n, float near_plane) {
   w += nbig;
   c.big_r = w;
   w += nbig;
-  c.cursor = w;
+  c.sc = w;
   w += 64;
-  c.cut = w;
-  w += 128;
   c.scan_temp = w;
   c.scan_bytes = scan_bytes_for();
   // near plane in key space: depths are > near, so buckets start there (2^13 per octave)
@@ -297,9 +305,7 @@ static DepthCarve carve(void* temp, int64_t n, float near_plane) {
 
 static void depth_front(const ViewBufs& v, int64_t n, const DepthCarve& c, cudaStream_t s) {
   cudaMemsetAsync(c.hist, 0, sizeof(unsigned long long) * (kDepthBuckets + 2), s);
-  cudaMemsetAsync(c.big_a, 0, sizeof(uint32_t), s);
-  cudaMemsetAsync(c.big_r, 0, sizeof(uint32_t), s);
-  cudaMemsetAsync(c.cursor, 0, sizeof(uint32_t), s);
+  cudaMemsetAsync(c.sc, 0, sizeof(uint32_t) * kScalars, s);
   depth_hist_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(v.dkey, v.tiles, n, c.base, c.hist, c.slot);
   size_t sb = c.scan_bytes;
   cub::DeviceScan::ExclusiveSum(c.scan_temp, sb, c.hist, c.off, kDepthBuckets + 2, s);
@@ -314,16 +320,15 @@ void launch_depth_order(const ViewBufs& v, int64_t n, float near_plane, void* te
   const unsigned grid = (unsigned)((n + 255) / 256);
   const DepthOut o{idx_sorted, cnt_sorted, nullptr, nullptr, nullptr};
   depth_scatter_kernel<<<grid, 256, 0, s>>>(v.dkey, n, c.base, c.off, c.slot, nullptr, kDepthAll, c.tmp, nullptr, nullptr);
-  depth_rank_kernel<<<grid, 256, 0, s>>>(c.tmp, n, c.base, c.off, v.tiles, v.rect, nullptr, kDepthAll, o, c.big_a);
-  depth_big_kernel<<<8, 1024, 0, s>>>(c.tmp, c.off, v.tiles, v.rect, nullptr, c.big_a, c.scratch, c.cursor, o);
+  depth_rank_kernel<<<grid, 256, 0, s>>>(c.tmp, n, c.base, c.off, v.tiles, v.rect, nullptr, kDepthAll, o,
+                                         c.sc + kScBigA, c.big_a);
+  depth_big_kernel<<<8, 1024, 0, s>>>(c.tmp, c.off, v.tiles, v.rect, nullptr, c.sc + kScBigA, c.big_a, c.scratch,
+                                      c.sc + kScScratch, o);
 }
 
 void launch_depth_prepare(int64_t n, float near_plane, void* temp, ViewBufs* v, cudaStream_t s) {
   const DepthCarve c = carve(temp, n, near_plane);
   cudaMemsetAsync(c.hist, 0, sizeof(unsigned long long) * (kDepthBuckets + 2), s);
-  cudaMemsetAsync(c.big_a, 0, sizeof(uint32_t), s);
-  cudaMemsetAsync(c.big_r, 0, sizeof(uint32_t), s);
-  cudaMemsetAsync(c.cursor, 0, 2 * sizeof(uint32_t), s);
   v->dhist = c.hist;
   v->dslot = c.slot;
   v->dbase = c.base;
@@ -350,17 +355,18 @@ void launch_depth_order_layer_a(const ViewBufs& v, int64_t n, float near_plane, 
     return;
   }
   const DepthCarve c = carve(temp, n, near_plane);
-  cudaMemsetAsync(c.cut, 0xff, sizeof(uint32_t), s);
-  cudaMemsetAsync(c.big_a, 0, sizeof(uint32_t), s);
-  cudaMemsetAsync(c.cursor, 0, sizeof(uint32_t), s);  // bitonic scratch allocator
-  depth_cut_kernel<<<(kDepthBuckets + 255) / 256, 256, 0, s>>>(c.off, div, min_pairs, gauss_cap, cap_a, c.cut);
+  cudaMemsetAsync(c.sc, 0, sizeof(uint32_t) * kScalars, s);  // cut, counts, allocators
+  depth_cut_kernel<<<(kDepthBuckets + 255) / 256, 256, 0, s>>>(c.off, div, min_pairs, gauss_cap, cap_a,
+                                                                c.sc + kScCut);
   const DepthOut o{idx_sorted, nullptr, cand_rect, active, gacc_zero};
   const int64_t ga = std::min<int64_t>(n, gauss_cap);
-  depth_scatter_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(v.dkey, n, c.base, c.off, c.slot, c.cut,
+  const uint32_t* cut = c.sc + kScCut;
+  depth_scatter_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(v.dkey, n, c.base, c.off, c.slot, cut,
                                                                     kDepthLayerA, c.tmp, ra, nullptr);
-  depth_rank_kernel<<<(unsigned)((ga + 255) / 256), 256, 0, s>>>(c.tmp, n, c.base, c.off, v.tiles, v.rect, c.cut,
-                                                                  kDepthLayerA, o, c.big_a);
-  depth_big_kernel<<<8, 1024, 0, s>>>(c.tmp, c.off, v.tiles, v.rect, c.cut, c.big_a, c.scratch, c.cursor, o);
+  depth_rank_kernel<<<(unsigned)((ga + 255) / 256), 256, 0, s>>>(c.tmp, n, c.base, c.off, v.tiles, v.rect, cut,
+                                                                  kDepthLayerA, o, c.sc + kScBigA, c.big_a);
+  depth_big_kernel<<<8, 1024, 0, s>>>(c.tmp, c.off, v.tiles, v.rect, cut, c.sc + kScBigA, c.big_a, c.scratch,
+                                      c.sc + kScScratch, o);
 }
 
 // Layer-A tile lists: one CTA per tile; its 8 warps split the R_A depth-ordered candidates into
@@ -424,12 +430,15 @@ void launch_depth_order_rest(const ViewBufs& v, int64_t n, float near_plane, voi
   const DepthCarve c = carve(temp, n, near_plane);
   const unsigned grid = (unsigned)((n + 255) / 256);
   const DepthOut o{idx_sorted, nullptr, nullptr, nullptr, nullptr};
-  cudaMemsetAsync(c.big_r, 0, sizeof(uint32_t), s);
-  cudaMemsetAsync(c.cursor + 1, 0, sizeof(uint32_t), s);  // culled slots
-  depth_scatter_kernel<<<grid, 256, 0, s>>>(v.dkey, n, c.base, c.off, c.slot, c.cut, kDepthRest, c.tmp, nullptr,
-                                            c.cursor + 1);
-  depth_rank_kernel<<<grid, 256, 0, s>>>(c.tmp, n, c.base, c.off, v.tiles, v.rect, c.cut, kDepthRest, o, c.big_r);
-  depth_big_kernel<<<8, 1024, 0, s>>>(c.tmp, c.off, v.tiles, v.rect, c.cut, c.big_r, c.scratch, c.cursor, o);
+  // the rest's big-bucket count, bitonic scratch allocator (layer A's sorts are done) and culled slots
+  cudaMemsetAsync(c.sc + kScBigR, 0, sizeof(uint32_t) * 3, s);
+  const uint32_t* cut = c.sc + kScCut;
+  depth_scatter_kernel<<<grid, 256, 0, s>>>(v.dkey, n, c.base, c.off, c.slot, cut, kDepthRest, c.tmp, nullptr,
+                                            c.sc + kScCulled);
+  depth_rank_kernel<<<grid, 256, 0, s>>>(c.tmp, n, c.base, c.off, v.tiles, v.rect, cut, kDepthRest, o,
+                                         c.sc + kScBigR, c.big_r);
+  depth_big_kernel<<<8, 1024, 0, s>>>(c.tmp, c.off, v.tiles, v.rect, cut, c.sc + kScBigR, c.big_r, c.scratch,
+                                      c.sc + kScScratch, o);
 }
 
 }  // namespace lgs

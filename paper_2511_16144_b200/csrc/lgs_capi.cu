@@ -749,15 +749,14 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
       uint2* cand_rect = nullptr;
       LGS_TRY(dalloc(ctx, &t->vals, (size_t)capA + (size_t)cap));
       t->vals_count = (int64_t)capA + cap;
-      LGS_TRY(dalloc(ctx, &ra, 2));  // [0] R_A, [1] list allocator
+      LGS_TRY(dalloc(ctx, &ra, 4 + (size_t)ntiles));  // [0] R_A, [1] list allocator, [4 ..] unfinished flags
+      unfinished = ra + 4;
       LGS_TRY(dalloc(ctx, &cand_rect, gcapA));
-      LGS_TRY(dalloc(ctx, &unfinished, ntiles));
       LGS_TRY(dalloc(ctx, &sat, sat_n));
       LGS_TRY(dalloc(ctx, &order2, ntiles));
       LGS_TRY(dalloc(ctx, &count2, 2));  // [0] unfinished tiles, [1] pairs of the second pass
       LGS_TRY(dalloc(ctx, reinterpret_cast<uint8_t**>(&scratch_b), fast_binning_scratch_bytes(cap, n, ntiles)));
-      LGS_CUDA(cudaMemsetAsync(unfinished, 0, sizeof(uint32_t) * ntiles, s));
-      LGS_CUDA(cudaMemsetAsync(ra + 1, 0, sizeof(uint32_t), s));
+      LGS_CUDA(cudaMemsetAsync(ra, 0, sizeof(uint32_t) * (4 + (size_t)ntiles), s));
       // captured fused-L1 step: each tile's backward runs right after its forward (blend_fused.cu);
       // the depth order flags the layer-A Gaussians active and zeroes their accumulator rows
       const bool fuse = ctx->capturing && targets && blend_fused_supported(dp) && slots_for(dp) == 32;
@@ -834,7 +833,6 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
       dfree(ctx, count2);
       dfree(ctx, order2);
       dfree(ctx, sat);
-      dfree(ctx, unfinished);
       dfree(ctx, cand_rect);
       dfree(ctx, ra);
       LGS_CUDA(cudaGetLastError());
