@@ -759,7 +759,10 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
       LGS_CUDA(cudaMemsetAsync(ra, 0, sizeof(uint32_t) * (4 + (size_t)ntiles), s));
       // captured fused-L1 step: each tile's backward runs right after its forward (blend_fused.cu);
       // the depth order flags the layer-A Gaussians active and zeroes their accumulator rows
-      const bool fuse = ctx->capturing && targets && blend_fused_supported(dp) && slots_for(dp) == 32;
+      // (LGS_FUSE_EAGER=1: the same in uncaptured renders, for profiling tools only -- the tape then
+      // holds the L1 gradients and any other cotangents passed to a backward are ignored)
+      static const bool fuse_eager = getenv("LGS_FUSE_EAGER") != nullptr;
+      const bool fuse = (ctx->capturing || fuse_eager) && targets && blend_fused_supported(dp) && slots_for(dp) == 32;
       if (fuse) {
         dfree(ctx, t->gacc);
         LGS_TRY(dalloc(ctx, &t->gacc, (size_t)n * 32));
