@@ -207,6 +207,17 @@ def rank_camera(base_cam, rank, world):
     return cam
 
 
+def traffic_for(phase):
+    """DRAM bytes per launch of the phase's kernel from one `ncu --set full` capture, committed in
+    profiles/traffic.json (bench.py cannot run ncu itself); None when not recorded."""
+    try:
+        rec = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+    except (OSError, ValueError):
+        return None
+    ent = rec.get(phase)
+    return int(ent["dram_bytes_per_launch"]) if ent else None
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -364,6 +375,9 @@ def run_ours(args):
         "blend_bwd": ("fp32", F_EVAL * evaluated + F_BWD * contributed),
         "preprocess_bwd": ("hbm", n * (16 * 3 + 12 * K + 16 + 128 + 4) + n * 4 * (11 + 3 * K + d)),
     }
+    if "blend_bwd" not in phases and "blend_fwd" in phases:  # captured fused-L1 step: one kernel
+        phases["blend_fused"] = phases.pop("blend_fwd")
+        work["blend_fused"] = ("fp32", 2 * F_EVAL * evaluated + (F_FWD + F_BWD) * contributed)
     phase_rows = {}
     for name, (pms, cnt) in phases.items():
         if name not in work:
@@ -394,7 +408,7 @@ def run_ours(args):
         "peak_source": hbm_src if dr["bound"] == "hbm" else "lgs_measure_fp32_peak (FFMA microbenchmark, this box)",
         "unit": dr["unit"],
         "frac": dr["frac"],
-        "traffic": None,
+        "traffic": traffic_for(dom),
         "step_t_roof_ms": round(t_roof * 1e3, 4),
         "step_frac": round(t_roof * 1e3 / ms_max, 4),
         "phases": phase_rows,
