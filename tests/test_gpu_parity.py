@@ -473,7 +473,7 @@ def _layered_vs_full(scene, cam, tg):
     return lst, fst
 
 
-@pytest.mark.parametrize("name,n", [("c1", 60_000), ("c0", None), ("c2", 60_000)])
+@pytest.mark.parametrize("name,n", [("c1", 60_000), ("c0", None), ("c2", 60_000), ("c1_500k", None)])
 def test_layered_binning_matches_full_lists(name, n):
     """Depth-layered binning (default) against complete lists: bitwise-identical images and loss,
     gradients equal up to atomic-accumulation order; every list a prefix of the complete one, truncated only on saturated tiles.  c0
