@@ -37,12 +37,35 @@ __global__ void __launch_bounds__(kPbThreads) preprocess_bwd_kernel(DevMap m, De
   const int64_t n = m.n;
   const int nloc = (int)min((int64_t)kPbThreads, n - i0);
   const bool live = i < n && (v.active ? v.active[i] != 0 : v.tiles[i] != 0);
-  // a block without a live Gaussian (most of them with the depth-layered binning) only writes zeros
-  if (DEG > 0 && __syncthreads_or(live)) stage_rows_in<KS, SS, kPbThreads>(s_sh, m.sh + i0 * KS, nloc);
+  const bool accum = g.accumulate != 0;
+  // A block without a live Gaussian (most of them with the depth-layered binning) has an all-zero
+  // gradient: nothing to add when accumulating, else streaming zero stores of its output rows.
+  if (!__syncthreads_or(live)) {
+    if (accum) return;
+    auto zero_rows = [&](float* base, int64_t count) {
+      if (!base) return;
+      if ((reinterpret_cast<uintptr_t>(base) & 15u) == 0) {
+        float4* b4 = reinterpret_cast<float4*>(base);
+        const int64_t n4 = count >> 2;
+        for (int64_t j = tid; j < n4; j += kPbThreads) b4[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int64_t j = n4 * 4 + tid; j < count; j += kPbThreads) base[j] = 0.f;
+      } else {
+        for (int64_t j = tid; j < count; j += kPbThreads) base[j] = 0.f;
+      }
+    };
+    zero_rows(g.position ? g.position + i0 * 3 : nullptr, (int64_t)nloc * 3);
+    zero_rows(g.rotation ? g.rotation + i0 * 4 : nullptr, (int64_t)nloc * 4);
+    zero_rows(g.log_scale ? g.log_scale + i0 * 3 : nullptr, (int64_t)nloc * 3);
+    zero_rows(g.opacity_logit ? g.opacity_logit + i0 : nullptr, nloc);
+    zero_rows(g.sh ? g.sh + i0 * KS : nullptr, (int64_t)nloc * KS);
+    if (DP > 0 && g.feature)
+      for (int k = 0; k < m.d; ++k) zero_rows(g.feature + (int64_t)k * n + i0, nloc);
+    return;
+  }
+  if (DEG > 0) stage_rows_in<KS, SS, kPbThreads>(s_sh, m.sh + i0 * KS, nloc);
   __syncthreads();
   float* my_sh = s_sh + tid * SS;
   float pose[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-  const bool accum = g.accumulate != 0;
   if (i < n) {
     float o_pos[3] = {0.f, 0.f, 0.f}, o_rot[4] = {0.f, 0.f, 0.f, 0.f}, o_ls[3] = {0.f, 0.f, 0.f};
     float o_op = 0.f;
