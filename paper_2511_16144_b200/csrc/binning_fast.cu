@@ -376,6 +376,7 @@ size_t layer_a_cap(int64_t pairs_cap, int ntiles, uint32_t div) {
 __global__ void __launch_bounds__(1024) layer_flag_kernel(const uint32_t* __restrict__ unfinished, int ntiles,
                                                           uint32_t* __restrict__ count2, uint32_t* __restrict__ total2,
                                                           cudaGraphConditionalHandle cond, int use_cond) {
+  griddep_wait();
   __shared__ uint32_t s_w[32];
   uint32_t c = 0;
   for (int t = threadIdx.x; t < ntiles; t += blockDim.x) c += unfinished[t] ? 1u : 0u;
@@ -393,8 +394,8 @@ __global__ void __launch_bounds__(1024) layer_flag_kernel(const uint32_t* __rest
 
 void launch_layer_flag(const uint32_t* unfinished, int ntiles, uint32_t* count2, uint32_t* total2,
                        const cudaGraphConditionalHandle* cond, cudaStream_t s) {
-  layer_flag_kernel<<<1, 1024, 0, s>>>(unfinished, ntiles, count2, total2, cond ? *cond : cudaGraphConditionalHandle{},
-                                       cond ? 1 : 0);
+  launch_pdl(layer_flag_kernel, dim3(1), dim3(1024), 0, s, unfinished, ntiles, count2, total2,
+             cond ? *cond : cudaGraphConditionalHandle{}, cond ? 1 : 0);
 }
 
 // One CTA (first kernel of the second pass): unfinished-tile summed-area table

@@ -48,6 +48,7 @@ __device__ __forceinline__ void fused_transpose_reduce(float (&v)[SLOTS], int la
 template <int DP>
 __global__ void __launch_bounds__(kBlock / 2) blend_fused_l1_kernel(DevMap m, DevCam c, ViewBufs v, TileLists tl,
                                                                       FwdOut o, float* __restrict__ gacc) {
+  griddep_wait();
   constexpr int PPT = 2;
   constexpr int NT = kBlock / PPT;
   constexpr int DQ = DP > 0 ? DP / 4 : 1;
@@ -387,7 +388,7 @@ bool blend_fused_supported(int dp) { return dp == 16 || dp == 8 || dp == 4 || dp
 
 template <int DP>
 static void launch_fused_dp(const DevMap& m, const DevCam& c, const ViewBufs& v, const TileLists& tl, const FwdOut& o,
-                            float* gacc, cudaStream_t s) {
+                            float* gacc, cudaStream_t s, bool counter_zeroed) {
   static int ctas_per_sm = 0, sms = 0;
   if (!ctas_per_sm) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, blend_fused_l1_kernel<DP>, kBlock / 2, 0);
@@ -398,17 +399,17 @@ static void launch_fused_dp(const DevMap& m, const DevCam& c, const ViewBufs& v,
   }
   const int ntiles = c.tiles_x * c.tiles_y;
   const int grid = min(ntiles, ctas_per_sm * sms);
-  cudaMemsetAsync(tl.counter, 0, sizeof(int), s);
-  blend_fused_l1_kernel<DP><<<grid, kBlock / 2, 0, s>>>(m, c, v, tl, o, gacc);
+  if (!counter_zeroed) cudaMemsetAsync(tl.counter, 0, sizeof(int), s);
+  launch_pdl(blend_fused_l1_kernel<DP>, dim3(grid), dim3(kBlock / 2), 0, s, m, c, v, tl, o, gacc);
 }
 
 void launch_blend_fused_l1(const DevMap& m, const DevCam& c, const ViewBufs& v, const TileLists& tl, const FwdOut& o,
-                           float* gacc, cudaStream_t s) {
+                           float* gacc, cudaStream_t s, bool counter_zeroed) {
   switch (m.dp) {
-    case 0: launch_fused_dp<0>(m, c, v, tl, o, gacc, s); break;
-    case 4: launch_fused_dp<4>(m, c, v, tl, o, gacc, s); break;
-    case 8: launch_fused_dp<8>(m, c, v, tl, o, gacc, s); break;
-    default: launch_fused_dp<16>(m, c, v, tl, o, gacc, s); break;
+    case 0: launch_fused_dp<0>(m, c, v, tl, o, gacc, s, counter_zeroed); break;
+    case 4: launch_fused_dp<4>(m, c, v, tl, o, gacc, s, counter_zeroed); break;
+    case 8: launch_fused_dp<8>(m, c, v, tl, o, gacc, s, counter_zeroed); break;
+    default: launch_fused_dp<16>(m, c, v, tl, o, gacc, s, counter_zeroed); break;
   }
 }
 

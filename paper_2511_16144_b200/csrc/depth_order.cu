@@ -76,6 +76,7 @@ __device__ __forceinline__ uint32_t cut_end_of(const uint32_t* cut) {
 
 __global__ void depth_cut_kernel(const u64* __restrict__ off, uint32_t div, uint32_t min_pairs, int64_t gauss_cap,
                                  uint32_t cap_a, uint32_t* __restrict__ cut) {
+  griddep_wait();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= kDepthBuckets) return;
   const uint32_t P = prs_of(off[kDepthBuckets]);
@@ -105,6 +106,7 @@ __global__ void depth_scatter_kernel(const uint32_t* __restrict__ dkey, int64_t 
                                      const u64* __restrict__ off, const uint32_t* __restrict__ slot,
                                      const uint32_t* __restrict__ cut, int mode, uint2* __restrict__ tmp,
                                      uint32_t* __restrict__ ra_out, uint32_t* __restrict__ culled_cursor) {
+  griddep_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i == 0 && ra_out) *ra_out = cnt_of(off[cut_end_of(cut)]);  // R_A: Gaussians in layer A
   if (i >= n) return;
@@ -161,6 +163,7 @@ __global__ void depth_rank_kernel(const uint2* __restrict__ tmp, int64_t n, uint
                                   const u64* __restrict__ off, const uint32_t* __restrict__ tiles,
                                   const uint2* __restrict__ rect, const uint32_t* __restrict__ cut, int mode,
                                   DepthOut o, uint32_t* __restrict__ big_n, uint32_t* __restrict__ big_ids) {
+  griddep_wait();
   const int64_t p0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const uint32_t ra = cut ? cnt_of(off[cut_end_of(cut)]) : 0u;  // Gaussians in layer A
   const int64_t p = mode == kDepthRest ? p0 + ra : p0;
@@ -192,6 +195,7 @@ __global__ void __launch_bounds__(1024) depth_big_kernel(const uint2* __restrict
                                                          const uint32_t* __restrict__ big_ids,
                                                          unsigned long long* __restrict__ scratch,
                                                          uint32_t* __restrict__ cursor, DepthOut o) {
+  griddep_wait();
   const uint32_t nbig = *big_n;
   const uint32_t ra = cut ? cnt_of(off[cut_end_of(cut)]) : 0u;
   __shared__ uint32_t s_base;
@@ -278,6 +282,8 @@ static DepthCarve carve(void* temp, int64_t n, float near_plane) {
   const size_t nn = align_words((size_t)n), nb = align_words(kDepthBuckets + 2);
   c.hist = reinterpret_cast<unsigned long long*>(w);
   w += 2 * nb;
+  c.sc = w;  // right after the histogram: one memset zeroes both
+  w += 64;
   c.off = reinterpret_cast<unsigned long long*>(w);
   w += 2 * nb;
   c.slot = w;
@@ -291,8 +297,6 @@ static DepthCarve carve(void* temp, int64_t n, float near_plane) {
   w += nbig;
   c.big_r = w;
   w += nbig;
-  c.sc = w;
-  w += 64;
   c.scan_temp = w;
   c.scan_bytes = scan_bytes_for();
   // near plane in key space: depths are > near, so buckets start there (2^13 per octave)
@@ -328,7 +332,8 @@ void launch_depth_order(const ViewBufs& v, int64_t n, float near_plane, void* te
 
 void launch_depth_prepare(int64_t n, float near_plane, void* temp, ViewBufs* v, cudaStream_t s) {
   const DepthCarve c = carve(temp, n, near_plane);
-  cudaMemsetAsync(c.hist, 0, sizeof(unsigned long long) * (kDepthBuckets + 2), s);
+  // histogram and the scalars behind it (layer A's cut, counts, allocators)
+  cudaMemsetAsync(c.hist, 0, (size_t)(reinterpret_cast<char*>(c.sc + kScalars) - reinterpret_cast<char*>(c.hist)), s);
   v->dhist = c.hist;
   v->dslot = c.slot;
   v->dbase = c.base;
@@ -349,24 +354,29 @@ void launch_depth_scan(int64_t n, float near_plane, void* temp, const uint32_t**
 
 void launch_depth_order_layer_a(const ViewBufs& v, int64_t n, float near_plane, void* temp, uint32_t div,
                                 uint32_t min_pairs, int64_t gauss_cap, uint32_t cap_a, uint32_t* idx_sorted,
-                                uint2* cand_rect, uint32_t* ra, uint8_t* active, float* gacc_zero, cudaStream_t s) {
+                                uint2* cand_rect, uint32_t* ra, uint8_t* active, float* gacc_zero, bool rerun,
+                                cudaStream_t s) {
   if (n == 0) {
     cudaMemsetAsync(ra, 0, sizeof(uint32_t), s);
     return;
   }
   const DepthCarve c = carve(temp, n, near_plane);
-  cudaMemsetAsync(c.sc, 0, sizeof(uint32_t) * kScalars, s);  // cut, counts, allocators
-  depth_cut_kernel<<<(kDepthBuckets + 255) / 256, 256, 0, s>>>(c.off, div, min_pairs, gauss_cap, cap_a,
-                                                                c.sc + kScCut);
+  // (the scalars were zeroed with the histogram by launch_depth_prepare; a re-run after a pair
+  // capacity overflow zeroes them again)
+  if (rerun) cudaMemsetAsync(c.sc, 0, sizeof(uint32_t) * kScalars, s);
+  launch_pdl(depth_cut_kernel, dim3((kDepthBuckets + 255) / 256), dim3(256), 0, s, (const u64*)c.off, div, min_pairs,
+             gauss_cap, cap_a, c.sc + kScCut);
   const DepthOut o{idx_sorted, nullptr, cand_rect, active, gacc_zero};
   const int64_t ga = std::min<int64_t>(n, gauss_cap);
   const uint32_t* cut = c.sc + kScCut;
-  depth_scatter_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(v.dkey, n, c.base, c.off, c.slot, cut,
-                                                                    kDepthLayerA, c.tmp, ra, nullptr);
-  depth_rank_kernel<<<(unsigned)((ga + 255) / 256), 256, 0, s>>>(c.tmp, n, c.base, c.off, v.tiles, v.rect, cut,
-                                                                  kDepthLayerA, o, c.sc + kScBigA, c.big_a);
-  depth_big_kernel<<<8, 1024, 0, s>>>(c.tmp, c.off, v.tiles, v.rect, cut, c.sc + kScBigA, c.big_a, c.scratch,
-                                      c.sc + kScScratch, o);
+  launch_pdl(depth_scatter_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, s, (const uint32_t*)v.dkey, n,
+             c.base, (const u64*)c.off, (const uint32_t*)c.slot, cut, (int)kDepthLayerA, c.tmp, ra, (uint32_t*)nullptr);
+  launch_pdl(depth_rank_kernel, dim3((unsigned)((ga + 255) / 256)), dim3(256), 0, s, (const uint2*)c.tmp, n, c.base,
+             (const u64*)c.off, (const uint32_t*)v.tiles, (const uint2*)v.rect, cut, (int)kDepthLayerA, o,
+             c.sc + kScBigA, c.big_a);
+  launch_pdl(depth_big_kernel, dim3(8), dim3(1024), 0, s, (const uint2*)c.tmp, (const u64*)c.off,
+             (const uint32_t*)v.tiles, (const uint2*)v.rect, cut, (const uint32_t*)(c.sc + kScBigA),
+             (const uint32_t*)c.big_a, c.scratch, c.sc + kScScratch, o);
 }
 
 // Layer-A tile lists: one CTA per tile; its 8 warps split the R_A depth-ordered candidates into
@@ -379,7 +389,13 @@ constexpr int kListWarps = 8;
 
 __global__ void __launch_bounds__(kListWarps * 32) layer_tile_lists_kernel(
     const uint2* __restrict__ cand_rect, const uint32_t* __restrict__ cand_idx, const uint32_t* __restrict__ ra,
-    int tiles_x, uint32_t* __restrict__ cursor, uint32_t* __restrict__ vals, uint2* __restrict__ ranges) {
+    int tiles_x, uint32_t* __restrict__ cursor, uint32_t* __restrict__ vals, uint2* __restrict__ ranges,
+    int* __restrict__ blend_counter, double* __restrict__ loss) {
+  griddep_wait();
+  if (blockIdx.x == 0 && threadIdx.x == 0) {  // for the blend launched next (no memset nodes between)
+    if (blend_counter) *blend_counter = 0;
+    if (loss) *loss = 0.0;
+  }
   __shared__ uint32_t s_cnt[kListWarps], s_base;
   const int t = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -419,9 +435,10 @@ __global__ void __launch_bounds__(kListWarps * 32) layer_tile_lists_kernel(
 }
 
 void launch_layer_tile_lists(const uint2* cand_rect, const uint32_t* cand_idx, const uint32_t* n_cand, int tiles_x,
-                             int ntiles, uint32_t* cursor, uint32_t* vals, uint2* ranges, cudaStream_t s) {
-  layer_tile_lists_kernel<<<ntiles, kListWarps * 32, 0, s>>>(cand_rect, cand_idx, n_cand, tiles_x, cursor, vals,
-                                                             ranges);
+                             int ntiles, uint32_t* cursor, uint32_t* vals, uint2* ranges, int* blend_counter,
+                             double* loss, cudaStream_t s) {
+  launch_pdl(layer_tile_lists_kernel, dim3(ntiles), dim3(kListWarps * 32), 0, s, cand_rect, cand_idx, n_cand, tiles_x,
+             cursor, vals, ranges, blend_counter, loss);
 }
 
 void launch_depth_order_rest(const ViewBufs& v, int64_t n, float near_plane, void* temp, uint32_t* idx_sorted,

@@ -771,23 +771,26 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
       {
         PhaseScope ph(ctx, PH_DEPTH_SORT);
         launch_depth_order_layer_a(t->vb, n, dc.near_plane, otemp, kLayerDiv, kLayerMinPairs, gcapA, capA,
-                                   idx_sorted, cand_rect, ra, t->vb.active, fuse ? t->gacc : nullptr, s);
+                                   idx_sorted, cand_rect, ra, t->vb.active, fuse ? t->gacc : nullptr, !exact, s);
       }
       {
         PhaseScope ph(ctx, PH_TILE_SORT);
-        launch_layer_tile_lists(cand_rect, idx_sorted, ra, dc.tiles_x, ntiles, ra + 1, t->vals, t->ranges, s);
+        // (the fused kernel follows directly: the list kernel zeroes its tile counter and the loss)
+        launch_layer_tile_lists(cand_rect, idx_sorted, ra, dc.tiles_x, ntiles, ra + 1, t->vals, t->ranges,
+                                fuse ? t->counter : nullptr, fuse && targets ? t->loss : nullptr, s);
       }
       // Layered lists are short and even (every tile stops at its saturation): the blend kernels
       // take tiles in natural order (measured as fast as longest-list-first, one launch less).
       t->lpt_order = false;
       ctx->launches += 6;
-      if (targets) LGS_CUDA(cudaMemsetAsync(t->loss, 0, sizeof(double), s));
+      if (targets && !fuse) LGS_CUDA(cudaMemsetAsync(t->loss, 0, sizeof(double), s));
       FwdOut fo1 = fo;
       fo1.unfinished = unfinished;
       {
         PhaseScope ph(ctx, PH_BLEND_FWD);
         if (fuse)
-          launch_blend_fused_l1(map->dm, dc, t->vb, TileLists{t->vals, t->ranges, nullptr, t->counter}, fo1, t->gacc, s);
+          launch_blend_fused_l1(map->dm, dc, t->vb, TileLists{t->vals, t->ranges, nullptr, t->counter}, fo1, t->gacc, s,
+                                true);
         else
           launch_blend_fwd(map->dm, dc, t->vb, TileLists{t->vals, t->ranges, nullptr, t->counter}, t->ps, fo1, s);
       }

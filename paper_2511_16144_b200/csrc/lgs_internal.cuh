@@ -13,6 +13,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 namespace lgs {
 
 // depth buckets of the bucketed depth order (depth_order.cu): key >> kDepthShift relative to the
@@ -225,6 +227,26 @@ __device__ __forceinline__ float fast_exp2(float x) {
 
 // 1/x to ~1 ulp (MUFU.RCP, no IEEE slow path): used where the result feeds only gradients
 // (toleranced), never a threshold test that decides the contributor set.
+// Programmatic dependent launch (sm_90+): kernels launched with launch_pdl may start while the
+// previous kernel of the stream / graph drains; griddep_wait() (first statement of every such
+// kernel) blocks until that kernel's memory operations are visible.  A no-op otherwise.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... P, typename... A>
+inline cudaError_t launch_pdl(void (*kernel)(P...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, A&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<A>(args)...);
+}
+
 __device__ __forceinline__ float fast_rcp(float x) {
   float y;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));

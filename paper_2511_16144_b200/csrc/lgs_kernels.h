@@ -108,13 +108,16 @@ void launch_depth_prepare(int64_t n, float near_plane, void* temp, ViewBufs* v, 
 void launch_depth_scan(int64_t n, float near_plane, void* temp, const uint32_t** pairs_out, cudaStream_t s);
 void launch_depth_order_layer_a(const ViewBufs& v, int64_t n, float near_plane, void* temp, uint32_t div,
                                 uint32_t min_pairs, int64_t gauss_cap, uint32_t cap_a, uint32_t* idx_sorted,
-                                uint2* cand_rect, uint32_t* ra, uint8_t* active, float* gacc_zero, cudaStream_t s);
+                                uint2* cand_rect, uint32_t* ra, uint8_t* active, float* gacc_zero, bool rerun,
+                                cudaStream_t s);
 void launch_depth_order_rest(const ViewBufs& v, int64_t n, float near_plane, void* temp, uint32_t* idx_sorted,
                              cudaStream_t s);
 // Layer-A tile lists (one warp per tile scanning the depth-ordered candidates, order-preserving
 // compaction): vals[ranges[t]] for every tile; *cursor (zeroed by the caller) allocates list space.
 void launch_layer_tile_lists(const uint2* cand_rect, const uint32_t* cand_idx, const uint32_t* n_cand, int tiles_x,
-                             int ntiles, uint32_t* cursor, uint32_t* vals, uint2* ranges, cudaStream_t s);
+                             int ntiles, uint32_t* cursor, uint32_t* vals, uint2* ranges, int* blend_counter,
+                             double* loss, cudaStream_t s);
+// blend_counter / loss (optional) are zeroed for the blend kernel launched next
 void launch_duplicate(const ViewBufs& v, const uint32_t* idx_sorted, const uint32_t* incl, int64_t n,
                       int tiles_x, uint16_t* key_out, uint32_t* val_out, cudaStream_t s);
 void launch_tile_sort(uint16_t* keys_in, uint16_t* keys_out, uint32_t* vals_in, uint32_t* vals_out,
@@ -162,7 +165,7 @@ void launch_blend_fwd(const DevMap& m, const DevCam& c, const ViewBufs& v, const
 // gradient accumulator gacc (rows of the listed Gaussians zeroed beforehand) in one pass per tile.
 bool blend_fused_supported(int dp);
 void launch_blend_fused_l1(const DevMap& m, const DevCam& c, const ViewBufs& v, const TileLists& tl, const FwdOut& o,
-                           float* gacc, cudaStream_t s);
+                           float* gacc, cudaStream_t s, bool counter_zeroed = false);
 void launch_blend_bwd(const DevMap& m, const DevCam& c, const ViewBufs& v, const TileLists& tl,
                       const PixelState& ps, const BwdIn& in, float* gacc, int slots, cudaStream_t s);
 // Tensor-core variant (blend_bwd_mma.cu), used by launch_blend_bwd when supported.
