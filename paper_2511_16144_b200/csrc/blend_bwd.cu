@@ -250,10 +250,9 @@ __global__ void __launch_bounds__(kBlock / PPT) blend_bwd_kernel(DevMap m, DevCa
           vals[kSlotConC] = fmaf(cf * dy, dy, vals[kSlotConC]);
         }
         warp_transpose_reduce<SLOTS>(vals, lane);
-        float* dst = gacc + (size_t)sm.gid[e] * SLOTS + lane * (SLOTS / 32);
+        float* row = gacc + (size_t)sm.gid[e] * SLOTS;
 #pragma unroll
-        for (int q = 0; q < SLOTS / 32; ++q)
-          if (vals[q] != 0.f) atomicAdd(dst + q, vals[q]);
+        for (int q = 0; q < SLOTS / 32; ++q) gacc_add(row, lane * (SLOTS / 32) + q, vals[q]);
       }
     }
   }

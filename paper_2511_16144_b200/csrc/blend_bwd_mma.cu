@@ -314,7 +314,7 @@ __global__ void __launch_bounds__(kNT) blend_bwd_mma_kernel(DevMap m, DevCam c, 
             else if (gq == 4) { val = mo[5] - 2.0f * vb * mo[2] + vb * vb * S0; slot = kSlotConC; }
             else { val = -2.0f * (1.0f - r0.w) * S0; slot = kSlotOpac; }
           }
-          if (val != 0.f) atomicAdd(gacc + (size_t)s_gid[e] * 32 + slot, val);
+          gacc_add(gacc + (size_t)s_gid[e] * 32, slot, val);
         }
         __syncthreads();
         for (int i = tid; i < kSub * RS; i += kNT) red[i] = 0.f;

@@ -368,7 +368,7 @@ __global__ void __launch_bounds__(kBlock / 2) blend_fused_l1_kernel(DevMap m, De
           vals[kSlotConC] = fmaf(cf * dy, dy, vals[kSlotConC]);
         }
         fused_transpose_reduce<SLOTS>(vals, lane);
-        if (vals[0] != 0.f) atomicAdd(gacc + (size_t)sm.gid[e] * SLOTS + lane, vals[0]);
+        gacc_add(gacc + (size_t)sm.gid[e] * SLOTS, lane, vals[0]);
       }
     }
   }

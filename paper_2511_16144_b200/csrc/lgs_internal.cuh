@@ -25,21 +25,32 @@ constexpr int kDepthBuckets = 1 << 18;
 constexpr int kTile = 16;
 constexpr int kBlock = kTile * kTile;
 
-// Backward accumulator slots (per Gaussian).  Slot order is shared by blend_bwd.cu and
-// preprocess_bwd.cu.
+// Backward accumulator slots (per Gaussian, one 128-byte line for SLOTS = 32).  Slot order is
+// shared by the blend kernels and preprocess_bwd.cu.  The geometric slots 0-5 accumulate as
+// DOUBLES in the first 48 bytes of the row (float slots 0-11): the mean, conic and opacity
+// gradients sum many pixel terms with heavy cancellation on near-camera splats, and fp32 atomics
+// made them depend on the accumulation order at the 1e-3 level; the rest accumulate as floats.
 enum : int {
-  kSlotMuX = 0,
+  kSlotMuX = 0,    // doubles (index into the row viewed as double[])
   kSlotMuY = 1,
-  kSlotConA = 2,  // dL/dconic(0,0)
-  kSlotConB = 3,  // dL/dconic(0,1) == dL/dconic(1,0) (renderer.cpp:286-287)
-  kSlotConC = 4,  // dL/dconic(1,1)
-  kSlotOpac = 5,  // dL/d opacity_logit
-  kSlotZ = 6,     // dL/d depth via the depth image (renderer.cpp:265)
-  kSlotColor = 8, // 3 slots
-  kSlotFeat = 12  // DP slots
+  kSlotConA = 2,   // dL/dconic(0,0)
+  kSlotConB = 3,   // dL/dconic(0,1) == dL/dconic(1,0) (renderer.cpp:286-287)
+  kSlotConC = 4,   // dL/dconic(1,1)
+  kSlotOpac = 5,   // dL/d opacity_logit
+  kSlotGeo = 6,    // number of double slots (floats 0 .. 2 kSlotGeo - 1)
+  kSlotZ = 12,     // floats: dL/d depth via the depth image (renderer.cpp:265)
+  kSlotColor = 13, // 3 slots
+  kSlotFeat = 16   // DP slots
 };
 
 __host__ __device__ constexpr int slots_for(int dp) { return (kSlotFeat + dp) <= 32 ? 32 : 64; }
+
+// add one reduced slot value into a Gaussian's accumulator row (doubles for the geometric slots)
+__device__ __forceinline__ void gacc_add(float* row, int slot, float v) {
+  if (v == 0.f) return;
+  if (slot < kSlotGeo) atomicAdd(reinterpret_cast<double*>(row) + slot, (double)v);
+  else atomicAdd(row + slot, v);
+}
 
 struct DevCam {
   float rcw[9];  // world -> camera rotation (row-major)

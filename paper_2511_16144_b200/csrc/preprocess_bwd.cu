@@ -85,9 +85,14 @@ __global__ void __launch_bounds__(kPbThreads) preprocess_bwd_kernel(DevMap m, De
 
     if (visible) {
       const float* ga = gacc + (size_t)i * SLOTS;
-      const float4 a0 = *reinterpret_cast<const float4*>(ga + 0);  // muX muY conA conB
-      const float4 a1 = *reinterpret_cast<const float4*>(ga + 4);  // conC opac z -
-      const float4 a2 = *reinterpret_cast<const float4*>(ga + 8);  // r g b -
+      // geometric slots: doubles (lgs_internal.cuh); z, colour and features: floats
+      const double2 d01 = *reinterpret_cast<const double2*>(ga + 0);  // muX muY
+      const double2 d23 = *reinterpret_cast<const double2*>(ga + 4);  // conA conB
+      const double2 d45 = *reinterpret_cast<const double2*>(ga + 8);  // conC opac
+      const float4 zc = *reinterpret_cast<const float4*>(ga + kSlotZ);  // z r g b
+      const float4 a0 = make_float4((float)d01.x, (float)d01.y, (float)d23.x, (float)d23.y);
+      const float4 a1 = make_float4((float)d45.x, (float)d45.y, zc.x, 0.f);
+      const float4 a2 = make_float4(zc.y, zc.z, zc.w, 0.f);
       if (DP > 0 && g.feature) {  // renderer.cpp:262-264, written as [d][N]
 #pragma unroll
         for (int q = 0; q < DP / 4; ++q) {

@@ -449,12 +449,12 @@ def _layered_vs_full(scene, cam, tg):
     for k in ("rgb", "depth", "feat", "acc"):
         assert torch.equal(getattr(lo, k), getattr(fo, k)), k
     assert abs(lo.l1_loss() - fo.l1_loss()) <= 1e-7 * abs(fo.l1_loss())  # fp32 per-CTA partials, atomic order
-    # gradients: the same sums, accumulated by fp32 atomics in a different order (the same bound
-    # as two runs of one mode; the pose gradient, a sum over every splat with large cancellation
-    # on near-camera splats, varies by a few % between two identical runs on c2)
+    # gradients: the same sums, accumulated by atomics in a different order (the geometric slots
+    # in fp64, lgs_internal.cuh), so they agree far inside the oracle tolerance, pose included
     for k in GROUPS:
         frac, worst = grad_mismatch(lg[k], fg[k])
         assert frac < 1e-3, (k, frac, worst)
+    assert np.allclose(lg["pose"], fg["pose"], rtol=1e-4, atol=1e-5 * np.abs(fg["pose"]).max())
     lk, lv, lr = lo.tile_keys()
     fk, fv, fr = fo.tile_keys()
     ft, nc = fo.pixel_state()

@@ -44,9 +44,9 @@ def _check(plan_grads, pose, imgs, out, g):
     for k in GROUPS:  # atomic accumulation order differs run to run (same allowance as the oracle tests)
         frac, worst = grad_mismatch(plan_grads[k], g[k])
         assert frac < 1e-3, (k, frac, worst)
-    # the pose gradient sums every splat's contribution, each accumulated by fp32 atomics in a
-    # run-dependent order, with heavy cancellation: bound the error by the vector's scale
-    assert np.allclose(pose.numpy(), g["pose"], rtol=1e-3, atol=2e-3 * np.abs(g["pose"]).max())
+    # the pose gradient sums every splat's contribution (the geometric accumulator slots are fp64,
+    # so the atomic order moves it only in the last float digits)
+    assert np.allclose(pose.numpy(), g["pose"], rtol=1e-4, atol=1e-5 * np.abs(g["pose"]).max())
 
 
 def test_plan_matches_eager_and_replays():
@@ -95,7 +95,7 @@ def test_plan_set_camera():
     _check(grads, pose, imgs, out, g)
 
 
-@pytest.mark.parametrize("name", ["c0", "c1"])
+@pytest.mark.parametrize("name", ["c0", "c1", "c2", "c4"])
 def test_plan_layered_second_pass_toggles(name):
     """The second pass of the depth-layered binning is a conditional node of the captured graph:
     a replay where tiles stay unsaturated (tiny, faint splats) runs it, a dense one skips it; both
