@@ -359,7 +359,7 @@ def run_ours(args):
 
     # algorithmic work per launch
     npix = cam["width"] * cam["height"]
-    V, P, LST = st["visible"], st["pairs"], st["listed"]
+    V, P, LST, A = st["visible"], st["pairs"], st["listed"], st["active"]
     ntiles = ((cam["width"] + 15) // 16) * ((cam["height"] + 15) // 16)
     F_EVAL, F_FWD, F_BWD = 13.0, 45.0, 100.0
     # algorithmic bytes: preprocess = parameters read + records written (+ the
@@ -373,7 +373,8 @@ def run_ours(args):
         "tile_sort_ranges": ("hbm", LST * 4 + ntiles * 8),
         "blend_fwd": ("fp32", F_EVAL * evaluated + F_FWD * contributed),
         "blend_bwd": ("fp32", F_EVAL * evaluated + F_BWD * contributed),
-        "preprocess_bwd": ("hbm", n * (16 * 3 + 12 * K + 16 + 128 + 4) + n * 4 * (11 + 3 * K + d)),
+        # every gradient row written (zeros outside the active set) + the active rows' inputs
+        "preprocess_bwd": ("hbm", n + A * (16 * 3 + 12 * K + 16 + 128) + n * 4 * (11 + 3 * K + d)),
     }
     if "blend_bwd" not in phases and "blend_fwd" in phases:  # captured fused-L1 step: one kernel
         phases["blend_fused"] = phases.pop("blend_fwd")
@@ -429,7 +430,7 @@ def run_ours(args):
         "clocks": clk.summary(),
         "gpu_launches": int(launches),
         "roofline": roofline,
-        "work": {"visible": V, "pairs": P, "listed": LST, "evaluated": evaluated, "contributed": contributed,
+        "work": {"visible": V, "pairs": P, "listed": LST, "active": A, "evaluated": evaluated, "contributed": contributed,
                  "max_tile_list": st["max_tile_list"]},
         "per_step_ms": [round(x, 4) for x in per_step],
         "host_enqueue_ms": [round(x, 3) for x in host_ms],

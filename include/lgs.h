@@ -140,6 +140,8 @@ typedef struct {
   int64_t max_tile_list;  /* longest per-tile list */
   int64_t listed;         /* entries the tile lists hold: P with complete lists; with the depth-layered
                              binning, saturated tiles keep only the prefix their pixels can reach */
+  int64_t active;         /* Gaussians whose gradient rows the backward computes (listed in a traversed
+                             tile list; = visible with complete lists); every other row is zero */
 } lgs_render_stats;
 
 /* ---- library / context ---------------------------------------------------------------- */

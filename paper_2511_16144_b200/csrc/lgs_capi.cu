@@ -61,6 +61,15 @@ int pad_dim(int d) {
   return 32;
 }
 
+// device gradient buffers of a lgs_map_grads as the kernels' GradOut (no pose)
+GradOut device_grad_out(const lgs_map_grads* g, int d) {
+  GradOut go{};
+  go.accumulate = g->accumulate;
+  go.position = g->position; go.rotation = g->rotation; go.log_scale = g->log_scale;
+  go.opacity_logit = g->opacity_logit; go.sh = g->sh; go.feature = d > 0 ? g->feature : nullptr;
+  return go;
+}
+
 // layer A of the depth-layered binning owns ~1/kLayerDiv of the pairs (binning_fast.cu)
 constexpr uint32_t kLayerDiv = 16;
 
@@ -93,6 +102,12 @@ struct lgs_ctx {
   bool full_lists = false;  // lgs_ctx_set_full_tile_lists: single-pass binning of every pair
   cudaStream_t cond_stream = nullptr;  // captures the body of a plan's conditional node
   cudaStream_t cond_parent = nullptr;  // the capturing stream while a body is captured
+  // lgs_plan capture: the zero rows of the plan's (non-accumulating) gradient buffers are written
+  // on a side branch forked after the preprocess and joined before the backward's chain kernel
+  const lgs_map_grads* prezero = nullptr;
+  bool prezero_forked = false;
+  cudaStream_t side_stream = nullptr;
+  cudaEvent_t side_fork = nullptr, side_join = nullptr;
   // multi-view gradient all-reduce (lgs_comm_*): one NCCL communicator per context / GPU
   ncclComm_t comm = nullptr;
   int32_t comm_world = 0, comm_rank = 0;
@@ -251,6 +266,9 @@ void ctx_release(lgs_ctx* ctx) {
     }
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     if (ctx->cond_stream) cudaStreamDestroy(ctx->cond_stream);
+    if (ctx->side_stream) cudaStreamDestroy(ctx->side_stream);
+    if (ctx->side_fork) cudaEventDestroy(ctx->side_fork);
+    if (ctx->side_join) cudaEventDestroy(ctx->side_join);
     if (ctx->pool) cudaMemPoolDestroy(ctx->pool);
     if (ctx->host_u32) cudaFreeHost(ctx->host_u32);
     if (ctx->dev_u32) cudaFree(ctx->dev_u32);
@@ -665,6 +683,17 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
     else launch_sum_tiles(t->vb.tiles, n, ctx->dev_u32, s);
   }
   ctx->launches += layered ? 3 : 2;
+  if (layered && ctx->capturing && ctx->prezero && !ctx->prezero_forked && n > 0) {
+    // side branch: the gradient buffers' zero rows stream out while the depth order and the
+    // blend run (the backward's chain then writes only the active rows)
+    CUDAB(cudaEventRecord(ctx->side_fork, s));
+    CUDAB(cudaStreamWaitEvent(ctx->side_stream, ctx->side_fork, 0));
+    launch_grad_zero(device_grad_out(ctx->prezero, map->dm.d), n, map->dm.K, map->dm.dp > 0 ? map->dm.d : 0,
+                     ctx->side_stream);
+    CUDAB(cudaEventRecord(ctx->side_join, ctx->side_stream));
+    ctx->prezero_forked = true;
+    ctx->launches++;
+  }
   if (n > 0) {
     CUDAB(cudaMemcpyAsync(ctx->host_u32, dev_pairs, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
     if (!ctx->capturing) CUDAB(cudaEventRecord(ctx->pairs_ready, s));
@@ -1008,8 +1037,7 @@ lgs_status run_backward(lgs_ctx* ctx, const lgs_saved* t, const BwdIn& in_dev, l
         p += szs[k];
       }
     } else {
-      go.position = grads->position; go.rotation = grads->rotation; go.log_scale = grads->log_scale;
-      go.opacity_logit = grads->opacity_logit; go.sh = grads->sh; go.feature = d > 0 ? grads->feature : nullptr;
+      go = device_grad_out(grads, d);
     }
   }
   double* dpose = nullptr;
@@ -1018,11 +1046,17 @@ lgs_status run_backward(lgs_ctx* ctx, const lgs_saved* t, const BwdIn& in_dev, l
     LGS_CUDA(cudaMemsetAsync(dpose, 0, sizeof(double) * 6, s));
     go.pose = dpose;
   }
+  // zero rows already enqueued on the plan's side branch (the forward forked it)?
+  const bool zeroed = ctx->prezero_forked && grads == ctx->prezero && !host && t->vb.active;
+  if (ctx->prezero_forked) {
+    LGS_CUDA(cudaStreamWaitEvent(s, ctx->side_join, 0));
+    ctx->prezero_forked = false;
+  }
   {
     PhaseScope ph(ctx, PH_PREPROCESS_BWD);
-    launch_preprocess_bwd(t->dm, t->cam, t->vb, gacc, slots, go, s);
+    launch_preprocess_bwd(t->dm, t->cam, t->vb, gacc, slots, go, zeroed, s);
   }
-  ctx->launches++;
+  ctx->launches += (t->vb.active && !zeroed && !go.accumulate) ? 2 : 1;
   LGS_CUDA(cudaGetLastError());
   if (host) {
     float* dst[6] = {grads->position, grads->rotation, grads->log_scale, grads->opacity_logit, grads->sh,
@@ -1303,8 +1337,12 @@ LGS_API lgs_status lgs_saved_stats(const lgs_saved* tape, lgs_render_stats* st) 
                              ctx->stream));
   LGS_CUDA(cudaMemcpyAsync(ranges.data(), tape->ranges, sizeof(uint2) * ranges.size(), cudaMemcpyDeviceToHost,
                            ctx->stream));
+  std::vector<uint8_t> act(tape->vb.active ? (size_t)tape->dm.n : 0);
+  if (!act.empty())
+    LGS_CUDA(cudaMemcpyAsync(act.data(), tape->vb.active, act.size(), cudaMemcpyDeviceToHost, ctx->stream));
   LGS_CUDA(cudaStreamSynchronize(ctx->stream));
-  int64_t vis = 0, mx = 0, pairs = 0, listed = 0;
+  int64_t vis = 0, mx = 0, pairs = 0, listed = 0, active = 0;
+  for (uint8_t a : act) active += a != 0;
   for (uint32_t v : tiles) {
     vis += v != 0;
     pairs += v;
@@ -1318,6 +1356,7 @@ LGS_API lgs_status lgs_saved_stats(const lgs_saved* tape, lgs_render_stats* st) 
   st->tiles = tape->ntiles;
   st->max_tile_list = mx;
   st->listed = listed;
+  st->active = tape->vb.active ? active : vis;
   return LGS_OK;
 }
 
@@ -1969,6 +2008,11 @@ void plan_free_marks(lgs_plan* p) {
 
 namespace {
 
+bool prezero_disabled() {  // LGS_PLAN_PREZERO=0: zero rows in the backward (A/B measurements)
+  const char* e = getenv("LGS_PLAN_PREZERO");
+  return e && e[0] == '0';
+}
+
 lgs_status plan_capture(lgs_plan* p) {
   lgs_ctx* ctx = p->ctx;
   if (p->exec) {
@@ -1979,9 +2023,16 @@ lgs_status plan_capture(lgs_plan* p) {
   cudaStream_t s = p->cap_stream;
   const cudaStream_t saved = ctx->stream;
   const int64_t l0 = ctx->launches.load();
+  if (!ctx->side_stream) {
+    LGS_CUDA(cudaStreamCreateWithFlags(&ctx->side_stream, cudaStreamNonBlocking));
+    LGS_CUDA(cudaEventCreateWithFlags(&ctx->side_fork, cudaEventDisableTiming));
+    LGS_CUDA(cudaEventCreateWithFlags(&ctx->side_join, cudaEventDisableTiming));
+  }
   LGS_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
   ctx->stream = s;
   ctx->capturing = true;
+  ctx->prezero = (p->grads.memory != LGS_MEM_HOST && !p->grads.accumulate && !prezero_disabled()) ? &p->grads : nullptr;
+  ctx->prezero_forked = false;
   plan_free_marks(p);
   ctx->capture_marks = p->profile ? &p->marks : nullptr;  // event nodes cost ~5 us each per replay
   lgs_status st = LGS_OK;
@@ -1999,6 +2050,11 @@ lgs_status plan_capture(lgs_plan* p) {
   if (tape) lgs_saved_destroy(tape);  // stream-ordered frees: captured as graph free nodes
   if (st == LGS_OK && cudaEventRecordWithFlags(p->ev1, s, cudaEventRecordExternal) != cudaSuccess)
     st = fail(LGS_ECUDA, "event record in capture failed");
+  if (ctx->prezero_forked) {  // forward captured but the backward failed: join the side branch
+    cudaStreamWaitEvent(s, ctx->side_join, 0);
+    ctx->prezero_forked = false;
+  }
+  ctx->prezero = nullptr;
   ctx->capturing = false;
   ctx->capture_marks = nullptr;
   ctx->stream = saved;

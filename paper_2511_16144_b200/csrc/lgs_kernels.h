@@ -193,8 +193,12 @@ struct GradOut {
   int accumulate;
   double* pose;         // 6 doubles (device, atomically accumulated) or null
 };
+// With v.active (depth-layered binning) only the active rows run the chain; every other row is
+// written zero by launch_grad_zero first (skipped when `zeroed`: the caller already enqueued it).
 void launch_preprocess_bwd(const DevMap& m, const DevCam& c, const ViewBufs& v, const float* gacc, int slots,
-                           const GradOut& g, cudaStream_t s);
+                           const GradOut& g, bool zeroed, cudaStream_t s);
+// zero rows of every output attribute (no-op when g.accumulate)
+void launch_grad_zero(const GradOut& g, int64_t n, int K, int d, cudaStream_t s);
 
 // K8 mapping losses (loss.cu): SSIM + L1 on rgb, masked depth L1, decoder chain on features.
 enum { LOSS_L1_RGB = 0, LOSS_SSIM = 1, LOSS_DEPTH_ABS = 2, LOSS_DEPTH_CNT = 3, LOSS_FEAT_ABS = 4, LOSS_COUNT = 8 };

@@ -22,6 +22,261 @@ constexpr int kPbThreads = 128;
 template <int DEG>
 constexpr int sh_stride() { return 3 * (DEG + 1) * (DEG + 1) + 1 - (3 * (DEG + 1) * (DEG + 1)) % 2; }
 
+
+// The chain for one live Gaussian i (its accumulator row is read; culled / unlisted Gaussians
+// never get here).  my_sh holds its SH coefficients on entry (DEG > 0) and their gradients on exit;
+// features are stored (or added) straight into g.feature; pose accumulates the pose gradient.
+template <int DEG, int DP, int SLOTS>
+__device__ __forceinline__ void gaussian_bwd(const DevMap& m, const DevCam& c, const ViewBufs& v,
+                                             const float* __restrict__ gacc, const GradOut& g, int64_t i,
+                                             bool accum, float* my_sh, float (&o_pos)[3], float (&o_rot)[4],
+                                             float (&o_ls)[3], float& o_op, float (&pose)[6]) {
+  constexpr int K = (DEG + 1) * (DEG + 1);
+  constexpr int KS = 3 * K;
+  const int64_t n = m.n;
+  auto store = [accum](float* p, int64_t idx, float val) {
+    if (accum) p[idx] += val;
+    else p[idx] = val;
+  };
+  const float* ga = gacc + (size_t)i * SLOTS;
+  // geometric slots: doubles (lgs_internal.cuh); z, colour and features: floats
+  const double2 d01 = *reinterpret_cast<const double2*>(ga + 0);  // muX muY
+  const double2 d23 = *reinterpret_cast<const double2*>(ga + 4);  // conA conB
+  const double2 d45 = *reinterpret_cast<const double2*>(ga + 8);  // conC opac
+  const float4 zc = *reinterpret_cast<const float4*>(ga + kSlotZ);  // z r g b
+  const float4 a0 = make_float4((float)d01.x, (float)d01.y, (float)d23.x, (float)d23.y);
+  const float4 a1 = make_float4((float)d45.x, (float)d45.y, zc.x, 0.f);
+  const float4 a2 = make_float4(zc.y, zc.z, zc.w, 0.f);
+  if (DP > 0 && g.feature) {  // renderer.cpp:262-264, written as [d][N]
+#pragma unroll
+    for (int q = 0; q < DP / 4; ++q) {
+      const float4 fv = *reinterpret_cast<const float4*>(ga + kSlotFeat + q * 4);
+      const float f4[4] = {fv.x, fv.y, fv.z, fv.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (q * 4 + e < m.d) store(g.feature, (int64_t)(q * 4 + e) * n + i, f4[e]);
+    }
+  }
+  o_op = a1.y;
+  const float4 po = m.pos_opa[i];
+  const float P[3] = {po.x, po.y, po.z};
+  float gpos[3] = {0.f, 0.f, 0.f};
+
+  // ---- colour -> SH (renderer.cpp:259-261 for K = 1) ------------------------------------
+  const float gc[3] = {a2.x, a2.y, a2.z};
+  if (DEG == 0 || (gc[0] == 0.f && gc[1] == 0.f && gc[2] == 0.f)) {
+    my_sh[0] = gc[0];
+    my_sh[1] = gc[1];
+    my_sh[2] = gc[2];
+#pragma unroll
+    for (int k = 3; k < KS; ++k) my_sh[k] = 0.f;
+  } else {
+    const float dr[3] = {P[0] - c.cc[0], P[1] - c.cc[1], P[2] - c.cc[2]};
+    const float nr = sqrtf(dr[0] * dr[0] + dr[1] * dr[1] + dr[2] * dr[2]);
+    const float inr = 1.0f / nr;
+    const float dn[3] = {dr[0] * inr, dr[1] * inr, dr[2] * inr};
+    float b[16];
+    float db[16][3];
+    sh_basis_f32(DEG, dn[0], dn[1], dn[2], b);
+    sh_basis_grad_f32(DEG, dn[0], dn[1], dn[2], db);
+    float gdn[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      float s = 0.f;
+#pragma unroll
+      for (int ch = 0; ch < 3; ++ch) {
+        s = fmaf(my_sh[k * 3 + ch], gc[ch], s);  // coefficient (staged), then overwritten by its grad
+        my_sh[k * 3 + ch] = b[k] * gc[ch];
+      }
+      gdn[0] = fmaf(db[k][0], s, gdn[0]);
+      gdn[1] = fmaf(db[k][1], s, gdn[1]);
+      gdn[2] = fmaf(db[k][2], s, gdn[2]);
+    }
+    const float dd = dn[0] * gdn[0] + dn[1] * gdn[1] + dn[2] * gdn[2];
+    float gdir[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      gdir[a] = (gdn[a] - dn[a] * dd) * inr;
+      gpos[a] += gdir[a];
+    }
+    if (g.pose) {  // dir = p - c with c' = c + omega x c + nu
+      pose[0] += gdir[1] * c.cc[2] - gdir[2] * c.cc[1];
+      pose[1] += gdir[2] * c.cc[0] - gdir[0] * c.cc[2];
+      pose[2] += gdir[0] * c.cc[1] - gdir[1] * c.cc[0];
+      pose[3] -= gdir[0];
+      pose[4] -= gdir[1];
+      pose[5] -= gdir[2];
+    }
+  }
+
+  // ---- screen-space -> 3D (renderer.cpp:297-354) ----------------------------------------
+  const float gmu0 = a0.x, gmu1 = a0.y, gA = a0.z, gB = a0.w, gC = a1.x, gz = a1.z;
+  if (gmu0 != 0.f || gmu1 != 0.f || gA != 0.f || gB != 0.f || gC != 0.f || gz != 0.f) {
+    const float* R = c.rcw;
+    float t[3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) t[r] = R[r * 3 + 0] * P[0] + R[r * 3 + 1] * P[1] + R[r * 3 + 2] * P[2] + c.tcw[r];
+    const float z = t[2];
+    const float4 qr = m.rot[i];  // x,y,z,w
+    const float qv[4] = {qr.w, qr.x, qr.y, qr.z};
+    const float norm = sqrtf(qv[0] * qv[0] + qv[1] * qv[1] + qv[2] * qv[2] + qv[3] * qv[3]);
+    const float inorm = 1.0f / norm;
+    const float qh[4] = {qv[0] * inorm, qv[1] * inorm, qv[2] * inorm, qv[3] * inorm};
+    const float w = qh[0], x = qh[1], y = qh[2], zq = qh[3];
+    float W[9];  // R_g (rotation of the Gaussian)
+    {
+      const float tx = 2 * x, ty = 2 * y, tz = 2 * zq;
+      const float twx = tx * w, twy = ty * w, twz = tz * w, txx = tx * x, txy = ty * x, txz = tz * x;
+      const float tyy = ty * y, tyz = tz * y, tzz = tz * zq;
+      W[0] = 1 - (tyy + tzz); W[1] = txy - twz;       W[2] = txz + twy;
+      W[3] = txy + twz;       W[4] = 1 - (txx + tzz); W[5] = tyz - twx;
+      W[6] = txz - twy;       W[7] = tyz + twx;       W[8] = 1 - (txx + tyy);
+    }
+    const float4 ls = m.scale[i];
+    const float s2[3] = {__expf(2.f * ls.x), __expf(2.f * ls.y), __expf(2.f * ls.z)};
+    // Sigma3 = W S^2 W^T, Sigma_c = R Sigma3 R^T
+    float S3[9], RS[9], Sc[9];
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int cc = 0; cc < 3; ++cc)
+        S3[r * 3 + cc] = W[r * 3 + 0] * s2[0] * W[cc * 3 + 0] + W[r * 3 + 1] * s2[1] * W[cc * 3 + 1] +
+                         W[r * 3 + 2] * s2[2] * W[cc * 3 + 2];
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int cc = 0; cc < 3; ++cc)
+        RS[r * 3 + cc] = R[r * 3 + 0] * S3[0 * 3 + cc] + R[r * 3 + 1] * S3[1 * 3 + cc] + R[r * 3 + 2] * S3[2 * 3 + cc];
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int cc = 0; cc < 3; ++cc)
+        Sc[r * 3 + cc] = RS[r * 3 + 0] * R[cc * 3 + 0] + RS[r * 3 + 1] * R[cc * 3 + 1] + RS[r * 3 + 2] * R[cc * 3 + 2];
+    const float iz = 1.0f / z;
+    const float J[6] = {c.fx * iz, 0.f, -c.fx * t[0] * iz * iz, 0.f, c.fy * iz, -c.fy * t[1] * iz * iz};
+
+    // g_Sigma2 = -C gC C, C = conic (symmetric), gC = [[gA, gB], [gB, gC]]
+    const float4 r1 = v.rec1[i];
+    const float C0 = r1.x, C1 = r1.y, C3 = r1.z;
+    const float cg00 = C0 * gA + C1 * gB, cg01 = C0 * gB + C1 * gC;
+    const float cg10 = C1 * gA + C3 * gB, cg11 = C1 * gB + C3 * gC;
+    const float gs[4] = {-(cg00 * C0 + cg01 * C1), -(cg00 * C1 + cg01 * C3), -(cg10 * C0 + cg11 * C1),
+                         -(cg10 * C1 + cg11 * C3)};
+    // g_Sigma_c = J^T gs J
+    float gSc[9];
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int cc = 0; cc < 3; ++cc)
+        gSc[r * 3 + cc] = J[0 * 3 + r] * (gs[0] * J[0 * 3 + cc] + gs[1] * J[1 * 3 + cc]) +
+                          J[1 * 3 + r] * (gs[2] * J[0 * 3 + cc] + gs[3] * J[1 * 3 + cc]);
+    // g_J = (gs + gs^T) J Sigma_c
+    const float sy[4] = {2.f * gs[0], gs[1] + gs[2], gs[2] + gs[1], 2.f * gs[3]};
+    float JS[6], gJ[6];
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int cc = 0; cc < 3; ++cc)
+        JS[r * 3 + cc] = J[r * 3 + 0] * Sc[0 * 3 + cc] + J[r * 3 + 1] * Sc[1 * 3 + cc] + J[r * 3 + 2] * Sc[2 * 3 + cc];
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int cc = 0; cc < 3; ++cc) gJ[r * 3 + cc] = sy[r * 2 + 0] * JS[0 * 3 + cc] + sy[r * 2 + 1] * JS[1 * 3 + cc];
+    // g_t (renderer.cpp:320-327)
+    float gt[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) gt[a] = J[0 * 3 + a] * gmu0 + J[1 * 3 + a] * gmu1;
+    const float iz2 = iz * iz, iz3 = iz2 * iz;
+    gt[0] += gJ[2] * (-c.fx * iz2);
+    gt[1] += gJ[5] * (-c.fy * iz2);
+    gt[2] += gJ[0] * (-c.fx * iz2) + gJ[2] * (2.f * c.fx * t[0] * iz3) + gJ[4] * (-c.fy * iz2) +
+             gJ[5] * (2.f * c.fy * t[1] * iz3);
+    gt[2] += gz;
+    // g_p = R^T g_t (renderer.cpp:329)
+    float gw[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      gw[a] = R[0 * 3 + a] * gt[0] + R[1 * 3 + a] * gt[1] + R[2 * 3 + a] * gt[2];
+      gpos[a] += gw[a];
+    }
+    // G3 = R^T gSc R (symmetric)
+    float tmp[9], G3[9];
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int cc = 0; cc < 3; ++cc)
+        tmp[r * 3 + cc] = R[0 * 3 + r] * gSc[0 * 3 + cc] + R[1 * 3 + r] * gSc[1 * 3 + cc] + R[2 * 3 + r] * gSc[2 * 3 + cc];
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int cc = 0; cc < 3; ++cc)
+        G3[r * 3 + cc] = tmp[r * 3 + 0] * R[0 * 3 + cc] + tmp[r * 3 + 1] * R[1 * 3 + cc] + tmp[r * 3 + 2] * R[2 * 3 + cc];
+    // Y = G3 W; g_logs_a = (W^T G3 W)_aa 2 s2_a; g_rot = (G3 + G3^T) W S^2
+    float Y[9];
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int cc = 0; cc < 3; ++cc)
+        Y[r * 3 + cc] = G3[r * 3 + 0] * W[0 * 3 + cc] + G3[r * 3 + 1] * W[1 * 3 + cc] + G3[r * 3 + 2] * W[2 * 3 + cc];
+    float grot[9];
+    // (G3 + G3^T) = 2 G3 only if symmetric; use the explicit sum for fidelity
+    float Yt[9];
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int cc = 0; cc < 3; ++cc)
+        Yt[r * 3 + cc] = G3[0 * 3 + r] * W[0 * 3 + cc] + G3[1 * 3 + r] * W[1 * 3 + cc] + G3[2 * 3 + r] * W[2 * 3 + cc];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      o_ls[a] = (W[0 * 3 + a] * Y[0 * 3 + a] + W[1 * 3 + a] * Y[1 * 3 + a] + W[2 * 3 + a] * Y[2 * 3 + a]) * 2.f * s2[a];
+#pragma unroll
+      for (int r = 0; r < 3; ++r) grot[r * 3 + a] = (Y[r * 3 + a] + Yt[r * 3 + a]) * s2[a];
+    }
+    // rotation_derivatives (renderer.cpp:28-40), all scaled by 2
+    const float dw[9] = {0, -zq, y, zq, 0, -x, -y, x, 0};
+    const float dxm[9] = {0, y, zq, y, -2 * x, -w, zq, w, -2 * x};
+    const float dym[9] = {-2 * y, x, w, x, 0, zq, -w, zq, -2 * y};
+    const float dzm[9] = {-2 * zq, -w, x, w, -2 * zq, y, x, y, 0};
+    float gq[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int e = 0; e < 9; ++e) {
+      gq[0] = fmaf(grot[e], dw[e], gq[0]);
+      gq[1] = fmaf(grot[e], dxm[e], gq[1]);
+      gq[2] = fmaf(grot[e], dym[e], gq[2]);
+      gq[3] = fmaf(grot[e], dzm[e], gq[3]);
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a) gq[a] *= 2.f;
+    const float dot = qh[0] * gq[0] + qh[1] * gq[1] + qh[2] * gq[2] + qh[3] * gq[3];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) o_rot[a] = (gq[a] - qh[a] * dot) * inorm;
+
+    if (g.pose) {
+      // t' = R_cw (p - omega x p - nu) + t_cw: g_omega += g_w x p, g_nu -= g_w
+      pose[0] += gw[1] * P[2] - gw[2] * P[1];
+      pose[1] += gw[2] * P[0] - gw[0] * P[2];
+      pose[2] += gw[0] * P[1] - gw[1] * P[0];
+      pose[3] -= gw[0];
+      pose[4] -= gw[1];
+      pose[5] -= gw[2];
+      // Sigma3' = (I - [omega]x) Sigma3 (I + [omega]x): A = Sigma3 G3 - G3 Sigma3, vee(A - A^T)
+      float A1[9], A2[9];
+#pragma unroll
+      for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int cc = 0; cc < 3; ++cc) {
+          A1[r * 3 + cc] = S3[r * 3 + 0] * G3[0 * 3 + cc] + S3[r * 3 + 1] * G3[1 * 3 + cc] + S3[r * 3 + 2] * G3[2 * 3 + cc];
+          A2[r * 3 + cc] = G3[r * 3 + 0] * S3[0 * 3 + cc] + G3[r * 3 + 1] * S3[1 * 3 + cc] + G3[r * 3 + 2] * S3[2 * 3 + cc];
+        }
+      pose[0] += (A1[7] - A2[7]) - (A1[5] - A2[5]);
+      pose[1] += (A1[2] - A2[2]) - (A1[6] - A2[6]);
+      pose[2] += (A1[3] - A2[3]) - (A1[1] - A2[1]);
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 3; ++a) o_pos[a] = gpos[a];
+}
+
 template <int DEG, int DP, int SLOTS>
 __global__ void __launch_bounds__(kPbThreads) preprocess_bwd_kernel(DevMap m, DevCam c, ViewBufs v,
                                                                       const float* __restrict__ gacc, GradOut g) {
@@ -81,246 +336,8 @@ __global__ void __launch_bounds__(kPbThreads) preprocess_bwd_kernel(DevMap m, De
       for (int k = 0; k < KS; ++k) my_sh[k] = 0.f;
       if (DP > 0 && g.feature && !accum)
         for (int k = 0; k < m.d; ++k) g.feature[(int64_t)k * n + i] = 0.f;
-    }
-
-    if (visible) {
-      const float* ga = gacc + (size_t)i * SLOTS;
-      // geometric slots: doubles (lgs_internal.cuh); z, colour and features: floats
-      const double2 d01 = *reinterpret_cast<const double2*>(ga + 0);  // muX muY
-      const double2 d23 = *reinterpret_cast<const double2*>(ga + 4);  // conA conB
-      const double2 d45 = *reinterpret_cast<const double2*>(ga + 8);  // conC opac
-      const float4 zc = *reinterpret_cast<const float4*>(ga + kSlotZ);  // z r g b
-      const float4 a0 = make_float4((float)d01.x, (float)d01.y, (float)d23.x, (float)d23.y);
-      const float4 a1 = make_float4((float)d45.x, (float)d45.y, zc.x, 0.f);
-      const float4 a2 = make_float4(zc.y, zc.z, zc.w, 0.f);
-      if (DP > 0 && g.feature) {  // renderer.cpp:262-264, written as [d][N]
-#pragma unroll
-        for (int q = 0; q < DP / 4; ++q) {
-          const float4 fv = *reinterpret_cast<const float4*>(ga + kSlotFeat + q * 4);
-          const float f4[4] = {fv.x, fv.y, fv.z, fv.w};
-#pragma unroll
-          for (int e = 0; e < 4; ++e)
-            if (q * 4 + e < m.d) store(g.feature, (int64_t)(q * 4 + e) * n + i, f4[e]);
-        }
-      }
-      o_op = a1.y;
-      const float4 po = m.pos_opa[i];
-      const float P[3] = {po.x, po.y, po.z};
-      float gpos[3] = {0.f, 0.f, 0.f};
-
-      // ---- colour -> SH (renderer.cpp:259-261 for K = 1) ------------------------------------
-      const float gc[3] = {a2.x, a2.y, a2.z};
-      if (DEG == 0 || (gc[0] == 0.f && gc[1] == 0.f && gc[2] == 0.f)) {
-        my_sh[0] = gc[0];
-        my_sh[1] = gc[1];
-        my_sh[2] = gc[2];
-#pragma unroll
-        for (int k = 3; k < KS; ++k) my_sh[k] = 0.f;
-      } else {
-        const float dr[3] = {P[0] - c.cc[0], P[1] - c.cc[1], P[2] - c.cc[2]};
-        const float nr = sqrtf(dr[0] * dr[0] + dr[1] * dr[1] + dr[2] * dr[2]);
-        const float inr = 1.0f / nr;
-        const float dn[3] = {dr[0] * inr, dr[1] * inr, dr[2] * inr};
-        float b[16];
-        float db[16][3];
-        sh_basis_f32(DEG, dn[0], dn[1], dn[2], b);
-        sh_basis_grad_f32(DEG, dn[0], dn[1], dn[2], db);
-        float gdn[3] = {0.f, 0.f, 0.f};
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-          float s = 0.f;
-#pragma unroll
-          for (int ch = 0; ch < 3; ++ch) {
-            s = fmaf(my_sh[k * 3 + ch], gc[ch], s);  // coefficient (staged), then overwritten by its grad
-            my_sh[k * 3 + ch] = b[k] * gc[ch];
-          }
-          gdn[0] = fmaf(db[k][0], s, gdn[0]);
-          gdn[1] = fmaf(db[k][1], s, gdn[1]);
-          gdn[2] = fmaf(db[k][2], s, gdn[2]);
-        }
-        const float dd = dn[0] * gdn[0] + dn[1] * gdn[1] + dn[2] * gdn[2];
-        float gdir[3];
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-          gdir[a] = (gdn[a] - dn[a] * dd) * inr;
-          gpos[a] += gdir[a];
-        }
-        if (g.pose) {  // dir = p - c with c' = c + omega x c + nu
-          pose[0] += gdir[1] * c.cc[2] - gdir[2] * c.cc[1];
-          pose[1] += gdir[2] * c.cc[0] - gdir[0] * c.cc[2];
-          pose[2] += gdir[0] * c.cc[1] - gdir[1] * c.cc[0];
-          pose[3] -= gdir[0];
-          pose[4] -= gdir[1];
-          pose[5] -= gdir[2];
-        }
-      }
-
-      // ---- screen-space -> 3D (renderer.cpp:297-354) ----------------------------------------
-      const float gmu0 = a0.x, gmu1 = a0.y, gA = a0.z, gB = a0.w, gC = a1.x, gz = a1.z;
-      if (gmu0 != 0.f || gmu1 != 0.f || gA != 0.f || gB != 0.f || gC != 0.f || gz != 0.f) {
-        const float* R = c.rcw;
-        float t[3];
-#pragma unroll
-        for (int r = 0; r < 3; ++r) t[r] = R[r * 3 + 0] * P[0] + R[r * 3 + 1] * P[1] + R[r * 3 + 2] * P[2] + c.tcw[r];
-        const float z = t[2];
-        const float4 qr = m.rot[i];  // x,y,z,w
-        const float qv[4] = {qr.w, qr.x, qr.y, qr.z};
-        const float norm = sqrtf(qv[0] * qv[0] + qv[1] * qv[1] + qv[2] * qv[2] + qv[3] * qv[3]);
-        const float inorm = 1.0f / norm;
-        const float qh[4] = {qv[0] * inorm, qv[1] * inorm, qv[2] * inorm, qv[3] * inorm};
-        const float w = qh[0], x = qh[1], y = qh[2], zq = qh[3];
-        float W[9];  // R_g (rotation of the Gaussian)
-        {
-          const float tx = 2 * x, ty = 2 * y, tz = 2 * zq;
-          const float twx = tx * w, twy = ty * w, twz = tz * w, txx = tx * x, txy = ty * x, txz = tz * x;
-          const float tyy = ty * y, tyz = tz * y, tzz = tz * zq;
-          W[0] = 1 - (tyy + tzz); W[1] = txy - twz;       W[2] = txz + twy;
-          W[3] = txy + twz;       W[4] = 1 - (txx + tzz); W[5] = tyz - twx;
-          W[6] = txz - twy;       W[7] = tyz + twx;       W[8] = 1 - (txx + tyy);
-        }
-        const float4 ls = m.scale[i];
-        const float s2[3] = {__expf(2.f * ls.x), __expf(2.f * ls.y), __expf(2.f * ls.z)};
-        // Sigma3 = W S^2 W^T, Sigma_c = R Sigma3 R^T
-        float S3[9], RS[9], Sc[9];
-#pragma unroll
-        for (int r = 0; r < 3; ++r)
-#pragma unroll
-          for (int cc = 0; cc < 3; ++cc)
-            S3[r * 3 + cc] = W[r * 3 + 0] * s2[0] * W[cc * 3 + 0] + W[r * 3 + 1] * s2[1] * W[cc * 3 + 1] +
-                             W[r * 3 + 2] * s2[2] * W[cc * 3 + 2];
-#pragma unroll
-        for (int r = 0; r < 3; ++r)
-#pragma unroll
-          for (int cc = 0; cc < 3; ++cc)
-            RS[r * 3 + cc] = R[r * 3 + 0] * S3[0 * 3 + cc] + R[r * 3 + 1] * S3[1 * 3 + cc] + R[r * 3 + 2] * S3[2 * 3 + cc];
-#pragma unroll
-        for (int r = 0; r < 3; ++r)
-#pragma unroll
-          for (int cc = 0; cc < 3; ++cc)
-            Sc[r * 3 + cc] = RS[r * 3 + 0] * R[cc * 3 + 0] + RS[r * 3 + 1] * R[cc * 3 + 1] + RS[r * 3 + 2] * R[cc * 3 + 2];
-        const float iz = 1.0f / z;
-        const float J[6] = {c.fx * iz, 0.f, -c.fx * t[0] * iz * iz, 0.f, c.fy * iz, -c.fy * t[1] * iz * iz};
-
-        // g_Sigma2 = -C gC C, C = conic (symmetric), gC = [[gA, gB], [gB, gC]]
-        const float4 r1 = v.rec1[i];
-        const float C0 = r1.x, C1 = r1.y, C3 = r1.z;
-        const float cg00 = C0 * gA + C1 * gB, cg01 = C0 * gB + C1 * gC;
-        const float cg10 = C1 * gA + C3 * gB, cg11 = C1 * gB + C3 * gC;
-        const float gs[4] = {-(cg00 * C0 + cg01 * C1), -(cg00 * C1 + cg01 * C3), -(cg10 * C0 + cg11 * C1),
-                             -(cg10 * C1 + cg11 * C3)};
-        // g_Sigma_c = J^T gs J
-        float gSc[9];
-#pragma unroll
-        for (int r = 0; r < 3; ++r)
-#pragma unroll
-          for (int cc = 0; cc < 3; ++cc)
-            gSc[r * 3 + cc] = J[0 * 3 + r] * (gs[0] * J[0 * 3 + cc] + gs[1] * J[1 * 3 + cc]) +
-                              J[1 * 3 + r] * (gs[2] * J[0 * 3 + cc] + gs[3] * J[1 * 3 + cc]);
-        // g_J = (gs + gs^T) J Sigma_c
-        const float sy[4] = {2.f * gs[0], gs[1] + gs[2], gs[2] + gs[1], 2.f * gs[3]};
-        float JS[6], gJ[6];
-#pragma unroll
-        for (int r = 0; r < 2; ++r)
-#pragma unroll
-          for (int cc = 0; cc < 3; ++cc)
-            JS[r * 3 + cc] = J[r * 3 + 0] * Sc[0 * 3 + cc] + J[r * 3 + 1] * Sc[1 * 3 + cc] + J[r * 3 + 2] * Sc[2 * 3 + cc];
-#pragma unroll
-        for (int r = 0; r < 2; ++r)
-#pragma unroll
-          for (int cc = 0; cc < 3; ++cc) gJ[r * 3 + cc] = sy[r * 2 + 0] * JS[0 * 3 + cc] + sy[r * 2 + 1] * JS[1 * 3 + cc];
-        // g_t (renderer.cpp:320-327)
-        float gt[3];
-#pragma unroll
-        for (int a = 0; a < 3; ++a) gt[a] = J[0 * 3 + a] * gmu0 + J[1 * 3 + a] * gmu1;
-        const float iz2 = iz * iz, iz3 = iz2 * iz;
-        gt[0] += gJ[2] * (-c.fx * iz2);
-        gt[1] += gJ[5] * (-c.fy * iz2);
-        gt[2] += gJ[0] * (-c.fx * iz2) + gJ[2] * (2.f * c.fx * t[0] * iz3) + gJ[4] * (-c.fy * iz2) +
-                 gJ[5] * (2.f * c.fy * t[1] * iz3);
-        gt[2] += gz;
-        // g_p = R^T g_t (renderer.cpp:329)
-        float gw[3];
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-          gw[a] = R[0 * 3 + a] * gt[0] + R[1 * 3 + a] * gt[1] + R[2 * 3 + a] * gt[2];
-          gpos[a] += gw[a];
-        }
-        // G3 = R^T gSc R (symmetric)
-        float tmp[9], G3[9];
-#pragma unroll
-        for (int r = 0; r < 3; ++r)
-#pragma unroll
-          for (int cc = 0; cc < 3; ++cc)
-            tmp[r * 3 + cc] = R[0 * 3 + r] * gSc[0 * 3 + cc] + R[1 * 3 + r] * gSc[1 * 3 + cc] + R[2 * 3 + r] * gSc[2 * 3 + cc];
-#pragma unroll
-        for (int r = 0; r < 3; ++r)
-#pragma unroll
-          for (int cc = 0; cc < 3; ++cc)
-            G3[r * 3 + cc] = tmp[r * 3 + 0] * R[0 * 3 + cc] + tmp[r * 3 + 1] * R[1 * 3 + cc] + tmp[r * 3 + 2] * R[2 * 3 + cc];
-        // Y = G3 W; g_logs_a = (W^T G3 W)_aa 2 s2_a; g_rot = (G3 + G3^T) W S^2
-        float Y[9];
-#pragma unroll
-        for (int r = 0; r < 3; ++r)
-#pragma unroll
-          for (int cc = 0; cc < 3; ++cc)
-            Y[r * 3 + cc] = G3[r * 3 + 0] * W[0 * 3 + cc] + G3[r * 3 + 1] * W[1 * 3 + cc] + G3[r * 3 + 2] * W[2 * 3 + cc];
-        float grot[9];
-        // (G3 + G3^T) = 2 G3 only if symmetric; use the explicit sum for fidelity
-        float Yt[9];
-#pragma unroll
-        for (int r = 0; r < 3; ++r)
-#pragma unroll
-          for (int cc = 0; cc < 3; ++cc)
-            Yt[r * 3 + cc] = G3[0 * 3 + r] * W[0 * 3 + cc] + G3[1 * 3 + r] * W[1 * 3 + cc] + G3[2 * 3 + r] * W[2 * 3 + cc];
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-          o_ls[a] = (W[0 * 3 + a] * Y[0 * 3 + a] + W[1 * 3 + a] * Y[1 * 3 + a] + W[2 * 3 + a] * Y[2 * 3 + a]) * 2.f * s2[a];
-#pragma unroll
-          for (int r = 0; r < 3; ++r) grot[r * 3 + a] = (Y[r * 3 + a] + Yt[r * 3 + a]) * s2[a];
-        }
-        // rotation_derivatives (renderer.cpp:28-40), all scaled by 2
-        const float dw[9] = {0, -zq, y, zq, 0, -x, -y, x, 0};
-        const float dxm[9] = {0, y, zq, y, -2 * x, -w, zq, w, -2 * x};
-        const float dym[9] = {-2 * y, x, w, x, 0, zq, -w, zq, -2 * y};
-        const float dzm[9] = {-2 * zq, -w, x, w, -2 * zq, y, x, y, 0};
-        float gq[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-        for (int e = 0; e < 9; ++e) {
-          gq[0] = fmaf(grot[e], dw[e], gq[0]);
-          gq[1] = fmaf(grot[e], dxm[e], gq[1]);
-          gq[2] = fmaf(grot[e], dym[e], gq[2]);
-          gq[3] = fmaf(grot[e], dzm[e], gq[3]);
-        }
-#pragma unroll
-        for (int a = 0; a < 4; ++a) gq[a] *= 2.f;
-        const float dot = qh[0] * gq[0] + qh[1] * gq[1] + qh[2] * gq[2] + qh[3] * gq[3];
-#pragma unroll
-        for (int a = 0; a < 4; ++a) o_rot[a] = (gq[a] - qh[a] * dot) * inorm;
-
-        if (g.pose) {
-          // t' = R_cw (p - omega x p - nu) + t_cw: g_omega += g_w x p, g_nu -= g_w
-          pose[0] += gw[1] * P[2] - gw[2] * P[1];
-          pose[1] += gw[2] * P[0] - gw[0] * P[2];
-          pose[2] += gw[0] * P[1] - gw[1] * P[0];
-          pose[3] -= gw[0];
-          pose[4] -= gw[1];
-          pose[5] -= gw[2];
-          // Sigma3' = (I - [omega]x) Sigma3 (I + [omega]x): A = Sigma3 G3 - G3 Sigma3, vee(A - A^T)
-          float A1[9], A2[9];
-#pragma unroll
-          for (int r = 0; r < 3; ++r)
-#pragma unroll
-            for (int cc = 0; cc < 3; ++cc) {
-              A1[r * 3 + cc] = S3[r * 3 + 0] * G3[0 * 3 + cc] + S3[r * 3 + 1] * G3[1 * 3 + cc] + S3[r * 3 + 2] * G3[2 * 3 + cc];
-              A2[r * 3 + cc] = G3[r * 3 + 0] * S3[0 * 3 + cc] + G3[r * 3 + 1] * S3[1 * 3 + cc] + G3[r * 3 + 2] * S3[2 * 3 + cc];
-            }
-          pose[0] += (A1[7] - A2[7]) - (A1[5] - A2[5]);
-          pose[1] += (A1[2] - A2[2]) - (A1[6] - A2[6]);
-          pose[2] += (A1[3] - A2[3]) - (A1[1] - A2[1]);
-        }
-      }
-#pragma unroll
-      for (int a = 0; a < 3; ++a) o_pos[a] = gpos[a];
+    } else {
+      gaussian_bwd<DEG, DP, SLOTS>(m, c, v, gacc, g, i, accum, my_sh, o_pos, o_rot, o_ls, o_op, pose);
     }
 
     // ---- dense writes in the reference layouts (zeros for culled Gaussians) -------------------
@@ -370,34 +387,174 @@ __global__ void __launch_bounds__(kPbThreads) preprocess_bwd_kernel(DevMap m, De
   }
 }
 
+// ---- sparse variant (depth-layered binning): only the active Gaussians have nonzero gradients --
+// With the layered lists ~15k of 500k Gaussians are active (the layer-A candidates + the second
+// pass's), spread over nearly every 128-row block of the dense kernel, which then pays its full
+// staging and divergent compute for a few live rows per warp.  Instead: (1) a streaming kernel
+// writes the zero rows of every Gaussian (nothing when accumulating) -- inside a captured plan it
+// runs on a side branch forked after the preprocess, off the critical path (lgs_capi.cu); (2) a
+// kernel whose blocks each compact the active rows of a contiguous range into a shared queue and
+// run the chain one queue entry per thread, storing (or adding) each active row.  Same values as
+// the dense kernel per row.
+constexpr int kZeroRows = 256;
+
+__global__ void __launch_bounds__(kZeroRows) grad_zero_kernel(GradOut g, int64_t n, int KS, int d) {
+  const int tid = threadIdx.x;
+  const int64_t i0 = (int64_t)blockIdx.x * kZeroRows;
+  const int nloc = (int)min((int64_t)kZeroRows, n - i0);
+  auto zero_rows = [&](float* base, int64_t cnt) {
+    if (!base) return;
+    int64_t j0 = 0;
+    if ((reinterpret_cast<uintptr_t>(base) & 15u) == 0) {
+      float4* b4 = reinterpret_cast<float4*>(base);
+      const int64_t n4 = cnt >> 2;
+      for (int64_t j = tid; j < n4; j += kZeroRows) __stcs(b4 + j, make_float4(0.f, 0.f, 0.f, 0.f));
+      j0 = n4 * 4;
+    }
+    for (int64_t j = j0 + tid; j < cnt; j += kZeroRows) base[j] = 0.f;
+  };
+  zero_rows(g.position ? g.position + i0 * 3 : nullptr, (int64_t)nloc * 3);
+  zero_rows(g.rotation ? g.rotation + i0 * 4 : nullptr, (int64_t)nloc * 4);
+  zero_rows(g.log_scale ? g.log_scale + i0 * 3 : nullptr, (int64_t)nloc * 3);
+  zero_rows(g.opacity_logit ? g.opacity_logit + i0 : nullptr, nloc);
+  zero_rows(g.sh ? g.sh + i0 * KS : nullptr, (int64_t)nloc * KS);
+  if (g.feature)
+    for (int k = 0; k < d; ++k) zero_rows(g.feature + (int64_t)k * n + i0, nloc);
+}
+
+void launch_grad_zero(const GradOut& g, int64_t n, int K, int d, cudaStream_t s) {
+  if (n == 0 || g.accumulate) return;
+  grad_zero_kernel<<<(unsigned)((n + kZeroRows - 1) / kZeroRows), kZeroRows, 0, s>>>(g, n, 3 * K, d);
+}
+
+constexpr int kActFlags = 16;                         // active flags per thread (one 16-byte load)
+constexpr int kActRange = kPbThreads * kActFlags;       // rows per block
+
+template <int DEG, int DP, int SLOTS>
+__global__ void __launch_bounds__(kPbThreads) preprocess_bwd_active_kernel(DevMap m, DevCam c, ViewBufs v,
+                                                                             const float* __restrict__ gacc, GradOut g) {
+  constexpr int K = (DEG + 1) * (DEG + 1);
+  constexpr int KS = 3 * K;
+  constexpr int SS = sh_stride<DEG>();
+  __shared__ float s_sh[kPbThreads * SS];
+  __shared__ uint32_t s_q[kActRange];
+  __shared__ int s_wsum[kPbThreads / 32];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  float* my_sh = s_sh + tid * SS;
+  const bool accum = g.accumulate != 0;
+  float pose[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+
+  // compact this block's active rows into s_q (ascending), one 16-byte flag load per thread
+  const int64_t f0 = (int64_t)blockIdx.x * kActRange + (int64_t)tid * kActFlags;
+  uint32_t bits = 0;
+  if (f0 + kActFlags <= m.n && (reinterpret_cast<uintptr_t>(v.active + f0) & 15u) == 0) {
+    const uint4 w = *reinterpret_cast<const uint4*>(v.active + f0);
+    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) bits |= (((ws[k] >> (8 * b)) & 0xffu) != 0u) << (k * 4 + b);
+  } else {
+    for (int k = 0; k < kActFlags && f0 + k < m.n; ++k) bits |= (v.active[f0 + k] != 0) << k;
+  }
+  const int cnt = __popc(bits);
+  int incl = cnt;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += y;
+  }
+  if (lane == 31) s_wsum[wid] = incl;
+  __syncthreads();
+  int base = incl - cnt, total = 0;
+#pragma unroll
+  for (int w2 = 0; w2 < kPbThreads / 32; ++w2) {
+    base += w2 < wid ? s_wsum[w2] : 0;
+    total += s_wsum[w2];
+  }
+  for (uint32_t b2 = bits; b2; b2 &= b2 - 1) s_q[base++] = (uint32_t)(f0 + __ffs(b2) - 1);
+  __syncthreads();
+
+  for (int q0 = 0; q0 < total; q0 += kPbThreads) {  // the chain, one active row per thread
+    if (q0 + tid >= total) break;
+    const int64_t i = s_q[q0 + tid];
+    if (DEG > 0) {
+      const float* src = m.sh + i * KS;
+#pragma unroll
+      for (int q = 0; q < KS; ++q) my_sh[q] = __ldg(src + q);
+    }
+    float o_pos[3] = {0.f, 0.f, 0.f}, o_rot[4] = {0.f, 0.f, 0.f, 0.f}, o_ls[3] = {0.f, 0.f, 0.f};
+    float o_op = 0.f;
+    gaussian_bwd<DEG, DP, SLOTS>(m, c, v, gacc, g, i, accum, my_sh, o_pos, o_rot, o_ls, o_op, pose);
+    auto put = [accum](float* p, int64_t idx, float val) {
+      if (accum) p[idx] += val;
+      else p[idx] = val;
+    };
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      if (g.position) put(g.position, i * 3 + a, o_pos[a]);
+      if (g.log_scale) put(g.log_scale, i * 3 + a, o_ls[a]);
+    }
+    if (g.rotation)
+#pragma unroll
+      for (int a = 0; a < 4; ++a) put(g.rotation, i * 4 + a, o_rot[a]);
+    if (g.opacity_logit) put(g.opacity_logit, i, o_op);
+    if (g.sh)
+#pragma unroll
+      for (int q = 0; q < KS; ++q) put(g.sh, i * KS + q, my_sh[q]);
+  }
+  if (g.pose) {  // block reduction of the pose gradient, one double atomic per value per block
+    __shared__ float s_pose[kPbThreads / 32][6];
+#pragma unroll
+    for (int a = 0; a < 6; ++a) {
+      float p = pose[a];
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) p += __shfl_xor_sync(0xffffffffu, p, off);
+      if (lane == 0) s_pose[wid][a] = p;
+    }
+    __syncthreads();
+    if (threadIdx.x < 6) {
+      double s = 0.0;
+      for (int w2 = 0; w2 < kPbThreads / 32; ++w2) s += (double)s_pose[w2][threadIdx.x];
+      if (s != 0.0) atomicAdd(g.pose + threadIdx.x, s);
+    }
+  }
+}
+
 template <int DEG, int DP>
 static void launch_pb(const DevMap& m, const DevCam& c, const ViewBufs& v, const float* gacc, const GradOut& g,
-                      cudaStream_t s) {
+                      bool zeroed, cudaStream_t s) {
+  if (v.active) {
+    if (!zeroed) launch_grad_zero(g, m.n, m.K, DP > 0 ? m.d : 0, s);
+    preprocess_bwd_active_kernel<DEG, DP, slots_for(DP)>
+        <<<(unsigned)((m.n + kActRange - 1) / kActRange), kPbThreads, 0, s>>>(m, c, v, gacc, g);
+    return;
+  }
   const unsigned blocks = (unsigned)((m.n + kPbThreads - 1) / kPbThreads);
   preprocess_bwd_kernel<DEG, DP, slots_for(DP)><<<blocks, kPbThreads, 0, s>>>(m, c, v, gacc, g);
 }
 
 template <int DEG>
 static void launch_pb_deg(const DevMap& m, const DevCam& c, const ViewBufs& v, const float* gacc, const GradOut& g,
-                          cudaStream_t s) {
+                          bool zeroed, cudaStream_t s) {
   switch (m.dp) {
-    case 0: launch_pb<DEG, 0>(m, c, v, gacc, g, s); break;
-    case 4: launch_pb<DEG, 4>(m, c, v, gacc, g, s); break;
-    case 8: launch_pb<DEG, 8>(m, c, v, gacc, g, s); break;
-    case 16: launch_pb<DEG, 16>(m, c, v, gacc, g, s); break;
-    default: launch_pb<DEG, 32>(m, c, v, gacc, g, s); break;
+    case 0: launch_pb<DEG, 0>(m, c, v, gacc, g, zeroed, s); break;
+    case 4: launch_pb<DEG, 4>(m, c, v, gacc, g, zeroed, s); break;
+    case 8: launch_pb<DEG, 8>(m, c, v, gacc, g, zeroed, s); break;
+    case 16: launch_pb<DEG, 16>(m, c, v, gacc, g, zeroed, s); break;
+    default: launch_pb<DEG, 32>(m, c, v, gacc, g, zeroed, s); break;
   }
 }
 
 void launch_preprocess_bwd(const DevMap& m, const DevCam& c, const ViewBufs& v, const float* gacc, int slots,
-                           const GradOut& g, cudaStream_t s) {
+                           const GradOut& g, bool zeroed, cudaStream_t s) {
   (void)slots;
   if (m.n == 0) return;
   switch (m.deg) {
-    case 0: launch_pb_deg<0>(m, c, v, gacc, g, s); break;
-    case 1: launch_pb_deg<1>(m, c, v, gacc, g, s); break;
-    case 2: launch_pb_deg<2>(m, c, v, gacc, g, s); break;
-    default: launch_pb_deg<3>(m, c, v, gacc, g, s); break;
+    case 0: launch_pb_deg<0>(m, c, v, gacc, g, zeroed, s); break;
+    case 1: launch_pb_deg<1>(m, c, v, gacc, g, zeroed, s); break;
+    case 2: launch_pb_deg<2>(m, c, v, gacc, g, zeroed, s); break;
+    default: launch_pb_deg<3>(m, c, v, gacc, g, zeroed, s); break;
   }
 }
 

@@ -197,7 +197,8 @@ class RenderOutput:
     def stats(self):
         s = _lib.LgsRenderStats()
         check(_lib.load().lgs_saved_stats(self.tape, C.byref(s)))
-        return dict(visible=s.visible, pairs=s.pairs, tiles=s.tiles, max_tile_list=s.max_tile_list, listed=s.listed)
+        return dict(visible=s.visible, pairs=s.pairs, tiles=s.tiles, max_tile_list=s.max_tile_list, listed=s.listed,
+                    active=s.active)
 
     def work(self):
         """(evaluated (pixel, Gaussian) pairs, contributing pairs) of this forward."""

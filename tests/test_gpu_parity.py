@@ -497,3 +497,29 @@ def test_layered_binning_mixed_saturation():
     tg = scenes.make_targets(cam, scene["feat"].shape[0], info["depth_range"], 5)
     lst, fst = _layered_vs_full(scene, cam, tg)
     assert lst["listed"] < fst["listed"]
+
+
+def test_layered_capacity_overflow_and_ties():
+    """Depth-layered binning on a context whose pair capacity comes from a small view: the larger
+    view overflows it and is re-run with exact buffers (layer-A scalars re-zeroed), and a map
+    whose nearest splats share one depth (a tie group in layer A's first bucket, bitonic path)
+    still renders exactly like a fresh context with complete lists."""
+    small, scams, _ = scenes.make_config("c0", n=2000)
+    big, bcams, info = scenes.make_config("c1", n=40_000)
+    pos = big["pos"].copy()
+    near = np.argsort(pos[:, 2])[:3000]
+    pos[near, 2] = np.float32(0.6)  # 3000 splats at one depth, all in layer A
+    big = dict(big, pos=pos)
+    ctx = R.Context(0)
+    R.render(dev_scene(small), scams[0], ctx=ctx)
+    over = R.render(dev_scene(big), bcams[0], ctx=ctx)
+    torch.cuda.synchronize()
+    ref = R.render(dev_scene(big), bcams[0], ctx=R.Context(0, full_lists=True))
+    torch.cuda.synchronize()
+    for k in ("rgb", "depth", "feat", "acc"):
+        assert torch.equal(getattr(over, k), getattr(ref, k)), k
+    lk, lv, lr = over.tile_keys()
+    fk, fv, fr = ref.tile_keys()
+    for t in range(lr.shape[0]):
+        a = lv[lr[t, 0]:lr[t, 1]]
+        assert np.array_equal(a, fv[fr[t, 0]:fr[t, 0] + a.size]), t
