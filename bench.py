@@ -364,11 +364,13 @@ def run_ours(args):
     F_EVAL, F_FWD, F_BWD = 13.0, 45.0, 100.0
     # algorithmic bytes: preprocess = parameters read + records written (+ the
     # 8 B depth-bucket slot / atomic); depth order = the 2^18-bucket u64 scan, key read and
-    # (key, index) scatter of the visible Gaussians; binning (depth-layered) = the listed pairs
+    # (key, index) scatter of the visible Gaussians, + the listed Gaussians' SH rows and colours; binning (depth-layered) = the listed pairs
     # written and ranges, each tile reading the layer-A candidate rects is not counted
     work = {
-        "preprocess": ("hbm", n * (16 * 3 + 12 * K) + n * (16 * 3 + 8 + 12) + V * 8),
-        "depth_sort_scan": ("hbm", 2 * 8 * (1 << 18) + n * 4 + V * 8),
+        # (layered: K1 reads no SH and writes no colour; the colours of the A active Gaussians are
+        # evaluated where the depth order first lists them)
+        "preprocess": ("hbm", n * 16 * 3 + n * (16 * 2 + 8 + 12) + V * 8),
+        "depth_sort_scan": ("hbm", 2 * 8 * (1 << 18) + n * 4 + V * 8 + A * (12 * K + 16)),
         "duplicate_keys": ("hbm", V * 16 + P * 6),
         "tile_sort_ranges": ("hbm", LST * 4 + ntiles * 8),
         "blend_fwd": ("fp32", F_EVAL * evaluated + F_FWD * contributed),

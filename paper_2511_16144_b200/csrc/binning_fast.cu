@@ -464,7 +464,7 @@ __global__ void __launch_bounds__(256) layer_count_kernel(const uint2* __restric
                                                           uint32_t* __restrict__ cnt_enum,
                                                           uint32_t* __restrict__ total2,
                                                           uint8_t* __restrict__ active,
-                                                          float* __restrict__ gacc_zero) {
+                                                          float* __restrict__ gacc_zero, ColorJob cj) {
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   uint32_t c = 0, e = 0;
   if (s < n && *count2) {
@@ -477,6 +477,7 @@ __global__ void __launch_bounds__(256) layer_count_kernel(const uint2* __restric
       const uint32_t sw = (uint32_t)tiles_x + 1;
       c = sat[ty1 * sw + tx1] - sat[ty0 * sw + tx1] - sat[ty1 * sw + tx0] + sat[ty0 * sw + tx0];
       e = c ? tc : 0u;
+      if (c && cj.color && (!active || !active[g])) color_job_run(cj, g);  // first listed here
       if (c && active && !active[g]) {  // listed for an unfinished tile: may receive gradients
         active[g] = 1;
         if (gacc_zero) {  // fused step: its accumulator row is zeroed here (layer-A rows already were)
@@ -494,10 +495,10 @@ __global__ void __launch_bounds__(256) layer_count_kernel(const uint2* __restric
 
 void launch_layer_count(const ViewBufs& v, const uint32_t* idx_sorted, int64_t n, int tiles_x, const uint32_t* sat,
                         const uint32_t* count2, uint32_t* cnt_enum, uint32_t* total2, cudaStream_t s,
-                        float* gacc_zero) {
+                        float* gacc_zero, const ColorJob& cj) {
   if (n == 0) return;
   layer_count_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(v.rect, v.tiles, idx_sorted, n, tiles_x, sat, count2,
-                                                                 cnt_enum, total2, v.active, gacc_zero);
+                                                                 cnt_enum, total2, v.active, gacc_zero, cj);
 }
 
 }  // namespace lgs

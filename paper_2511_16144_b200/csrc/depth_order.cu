@@ -140,6 +140,7 @@ struct DepthOut {
   uint2* cand_rect;      // [n] or null: tile rects in that order (positions < R_A)
   uint8_t* active;       // or null: layer-A Gaussians flagged for the backward (lgs_kernels.h) ...
   float* gacc_zero;      // ... and, for the fused step, their accumulator rows (32 floats) zeroed
+  ColorJob cj;           // lazy colours: computed here for the layer-A Gaussians (cj.color null: off)
 };
 
 __device__ __forceinline__ void depth_emit(const DepthOut& o, const uint32_t* __restrict__ tiles,
@@ -150,6 +151,7 @@ __device__ __forceinline__ void depth_emit(const DepthOut& o, const uint32_t* __
   if (pos < cand_end) {
     if (o.cand_rect) o.cand_rect[pos] = tile_rect(rect[g]);
     if (o.active) o.active[g] = 1;
+    if (o.cj.color) color_job_run(o.cj, g);
     if (o.gacc_zero) {
       float4* row = reinterpret_cast<float4*>(o.gacc_zero + (size_t)g * 32);
 #pragma unroll
@@ -355,7 +357,7 @@ void launch_depth_scan(int64_t n, float near_plane, void* temp, const uint32_t**
 void launch_depth_order_layer_a(const ViewBufs& v, int64_t n, float near_plane, void* temp, uint32_t div,
                                 uint32_t min_pairs, int64_t gauss_cap, uint32_t cap_a, uint32_t* idx_sorted,
                                 uint2* cand_rect, uint32_t* ra, uint8_t* active, float* gacc_zero, bool rerun,
-                                cudaStream_t s) {
+                                const ColorJob& cj, cudaStream_t s) {
   if (n == 0) {
     cudaMemsetAsync(ra, 0, sizeof(uint32_t), s);
     return;
@@ -366,7 +368,7 @@ void launch_depth_order_layer_a(const ViewBufs& v, int64_t n, float near_plane, 
   if (rerun) cudaMemsetAsync(c.sc, 0, sizeof(uint32_t) * kScalars, s);
   launch_pdl(depth_cut_kernel, dim3((kDepthBuckets + 255) / 256), dim3(256), 0, s, (const u64*)c.off, div, min_pairs,
              gauss_cap, cap_a, c.sc + kScCut);
-  const DepthOut o{idx_sorted, nullptr, cand_rect, active, gacc_zero};
+  const DepthOut o{idx_sorted, nullptr, cand_rect, active, gacc_zero, cj};
   const int64_t ga = std::min<int64_t>(n, gauss_cap);
   const uint32_t* cut = c.sc + kScCut;
   launch_pdl(depth_scatter_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, s, (const uint32_t*)v.dkey, n,

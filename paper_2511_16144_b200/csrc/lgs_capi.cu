@@ -666,6 +666,14 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
   void* otemp = nullptr;
   const size_t otemp_bytes = cub_depth ? 0 : depth_order_temp_bytes(n);
   if (!cub_depth) TRYB(dalloc(ctx, reinterpret_cast<uint8_t**>(&otemp), otemp_bytes));
+  ColorJob cj;  // layered: colours of just the listed Gaussians, computed where first listed
+  if (layered) {
+    cj.sh = map->dm.sh;
+    cj.pos_opa = map->dm.pos_opa;
+    for (int a = 0; a < 3; ++a) cj.cc[a] = dc.cc[a];
+    cj.deg = map->dm.deg;
+    cj.color = t->vb.color;
+  }
   if (layered) {
     launch_depth_prepare(n, dc.near_plane, otemp, &t->vb, s);
     TRYB(dalloc(ctx, &t->vb.active, n));  // tape-owned: the backward reads it
@@ -676,7 +684,7 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
   const uint32_t* dev_pairs = ctx->dev_u32;
   {
     PhaseScope ph(ctx, PH_PREPROCESS);
-    launch_preprocess(map->dm, dc, t->vb, s);
+    launch_preprocess(map->dm, dc, t->vb, !layered, s);
     // the pair count P = sum of tiles touched sizes the tile lists; it is read back while the GPU
     // is still busy with the depth order queued below, so the host wait never idles the GPU
     if (layered) launch_depth_scan(n, dc.near_plane, otemp, &dev_pairs, s);  // P = visible buckets' pairs
@@ -800,7 +808,7 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
       {
         PhaseScope ph(ctx, PH_DEPTH_SORT);
         launch_depth_order_layer_a(t->vb, n, dc.near_plane, otemp, kLayerDiv, kLayerMinPairs, gcapA, capA,
-                                   idx_sorted, cand_rect, ra, t->vb.active, fuse ? t->gacc : nullptr, !exact, s);
+                                   idx_sorted, cand_rect, ra, t->vb.active, fuse ? t->gacc : nullptr, !exact, cj, s);
       }
       {
         PhaseScope ph(ctx, PH_TILE_SORT);
@@ -843,7 +851,7 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
           launch_layer_prep(unfinished, t->ranges, dc.tiles_x, dc.tiles_y, sat, order2, s2);
           launch_depth_order_rest(t->vb, n, dc.near_plane, otemp, idx_sorted, s2);
           launch_layer_count(t->vb, idx_sorted, n, dc.tiles_x, sat, count2, dkey_sorted, count2 + 1, s2,
-                             fuse ? t->gacc : nullptr);
+                             fuse ? t->gacc : nullptr, cj);
           launch_scan_counts(dkey_sorted, n, incl, temp, temp_bytes, s2);
           const BinPass b{incl, count2 + 1, n, (uint32_t)cap, capA, unfinished, count2};
           launch_fast_binning(t->vb, idx_sorted, n, ntiles, dc.tiles_x, b, scratch_b, t->vals, t->ranges,
@@ -1434,6 +1442,7 @@ LGS_API lgs_status lgs_debug_projected(lgs_ctx* ctx, const lgs_saved* t, uint8_t
   std::vector<uint32_t> tiles(n);
   cudaStream_t s = ctx->stream;
   if (n) {
+    if (t->vb.active) launch_colors(t->dm, t->cam, t->vb, s);  // layered: K1 left colours to the listing
     LGS_CUDA(cudaMemcpyAsync(r0.data(), t->vb.rec0, sizeof(float4) * n, cudaMemcpyDeviceToHost, s));
     LGS_CUDA(cudaMemcpyAsync(r1.data(), t->vb.rec1, sizeof(float4) * n, cudaMemcpyDeviceToHost, s));
     LGS_CUDA(cudaMemcpyAsync(col.data(), t->vb.color, sizeof(float4) * n, cudaMemcpyDeviceToHost, s));

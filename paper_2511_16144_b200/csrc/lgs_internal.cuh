@@ -155,6 +155,93 @@ __device__ __forceinline__ void sh_basis_f32(int deg, float x, float y, float z,
   }
 }
 
+// The colour of Gaussian i (renderer.cpp:128; SH extension), with every operation explicitly
+// rounded (__fmul_rn / __fadd_rn / __fsub_rn are never contracted into FMAs): bit-identical in
+// every translation unit whatever its -fmad setting, and equal to the -fmad=false K1 arithmetic
+// that oracle B restates (orc32_sh_color).  Used by K1 and, with the depth-layered binning, for
+// just the Gaussians that get listed (ColorJob).
+__device__ __forceinline__ void sh_basis_rn(int deg, float x, float y, float z, float b[16]) {
+  b[0] = 1.0f;
+  if (deg >= 1) {
+    b[1] = __fmul_rn(-kShC1, y);
+    b[2] = __fmul_rn(kShC1, z);
+    b[3] = __fmul_rn(-kShC1, x);
+  }
+  if (deg >= 2) {
+    const float xx = __fmul_rn(x, x), yy = __fmul_rn(y, y), zz = __fmul_rn(z, z);
+    b[4] = __fmul_rn(kShC2[0], __fmul_rn(x, y));
+    b[5] = __fmul_rn(kShC2[1], __fmul_rn(y, z));
+    b[6] = __fmul_rn(kShC2[2], __fsub_rn(__fsub_rn(__fadd_rn(zz, zz), xx), yy));
+    b[7] = __fmul_rn(kShC2[3], __fmul_rn(x, z));
+    b[8] = __fmul_rn(kShC2[4], __fsub_rn(xx, yy));
+    if (deg >= 3) {
+      b[9] = __fmul_rn(__fmul_rn(kShC3[0], y), __fsub_rn(__fmul_rn(3.0f, xx), yy));
+      b[10] = __fmul_rn(__fmul_rn(kShC3[1], __fmul_rn(x, y)), z);
+      b[11] = __fmul_rn(__fmul_rn(kShC3[2], y), __fsub_rn(__fsub_rn(__fmul_rn(4.0f, zz), xx), yy));
+      b[12] = __fmul_rn(__fmul_rn(kShC3[3], z),
+                        __fsub_rn(__fsub_rn(__fmul_rn(2.0f, zz), __fmul_rn(3.0f, xx)), __fmul_rn(3.0f, yy)));
+      b[13] = __fmul_rn(__fmul_rn(kShC3[4], x), __fsub_rn(__fsub_rn(__fmul_rn(4.0f, zz), xx), yy));
+      b[14] = __fmul_rn(__fmul_rn(kShC3[5], z), __fsub_rn(xx, yy));
+      b[15] = __fmul_rn(__fmul_rn(kShC3[6], x), __fsub_rn(xx, __fmul_rn(3.0f, yy)));
+    }
+  }
+}
+
+template <int DEG>
+__device__ __forceinline__ float4 gaussian_color(const float* __restrict__ sh_all, float4 po, const float cc[3],
+                                                 int64_t i) {
+  constexpr int K = (DEG + 1) * (DEG + 1);
+  constexpr int KS = 3 * K;
+  const float* sh = sh_all + i * KS;
+  if (DEG == 0) return make_float4(__ldg(sh), __ldg(sh + 1), __ldg(sh + 2), 0.0f);
+  float dx = __fsub_rn(po.x, cc[0]), dy = __fsub_rn(po.y, cc[1]), dz = __fsub_rn(po.z, cc[2]);
+  const float dn = sqrtf(fmaf(dx, dx, fmaf(dy, dy, __fmul_rn(dz, dz))));
+  const float idn = __fdiv_rn(1.0f, dn);
+  dx = __fmul_rn(dx, idn); dy = __fmul_rn(dy, idn); dz = __fmul_rn(dz, idn);
+  float b[16];
+  sh_basis_rn(DEG, dx, dy, dz, b);
+  float e[KS];
+  if (KS % 4 == 0) {
+    const float4* row = reinterpret_cast<const float4*>(sh);
+#pragma unroll
+    for (int q = 0; q < KS / 4; ++q) {
+      const float4 v4 = __ldg(row + q);
+      e[4 * q] = v4.x; e[4 * q + 1] = v4.y; e[4 * q + 2] = v4.z; e[4 * q + 3] = v4.w;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < KS; ++j) e[j] = __ldg(sh + j);
+  }
+  float col[3] = {e[0], e[1], e[2]};  // each channel accumulates in k order
+#pragma unroll
+  for (int k = 1; k < K; ++k)
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) col[ch] = fmaf(b[k], e[3 * k + ch], col[ch]);
+  return make_float4(col[0], col[1], col[2], 0.0f);
+}
+
+// Lazy colours of the depth-layered binning: K1 skips the SH evaluation and the kernels that
+// first list a Gaussian (layer-A depth order, second-pass counting) compute its colour.
+struct ColorJob {
+  const float* sh = nullptr;
+  const float4* pos_opa = nullptr;
+  float cc[3] = {0.f, 0.f, 0.f};
+  int deg = 0;
+  float4* color = nullptr;  // null: colours were written by K1
+};
+
+__device__ __forceinline__ void color_job_run(const ColorJob& j, uint32_t g) {
+  const float4 po = j.pos_opa[g];
+  float4 col;
+  switch (j.deg) {
+    case 0: col = gaussian_color<0>(j.sh, po, j.cc, g); break;
+    case 1: col = gaussian_color<1>(j.sh, po, j.cc, g); break;
+    case 2: col = gaussian_color<2>(j.sh, po, j.cc, g); break;
+    default: col = gaussian_color<3>(j.sh, po, j.cc, g); break;
+  }
+  j.color[g] = col;
+}
+
 // d b_k / d(x, y, z) (unnormalized direction components treated as independent)
 __device__ __forceinline__ void sh_basis_grad_f32(int deg, float x, float y, float z, float db[16][3]) {
 #pragma unroll

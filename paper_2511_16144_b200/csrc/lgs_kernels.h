@@ -9,6 +9,7 @@ namespace lgs {
 
 struct DevCam;
 struct DevMap;
+struct ColorJob;
 
 // Per-view projected records, indexed by map index (written by K1).
 struct ViewBufs {
@@ -81,7 +82,10 @@ void launch_pack_map(const float* pos, const float* rot, const float* log_s, con
                      const float* feat_dn, int64_t n, int d, int dp, float4* pos_opa, float4* rot4,
                      float4* scale4, float* feat_nd, cudaStream_t s);
 
-void launch_preprocess(const DevMap& m, const DevCam& c, const ViewBufs& v, cudaStream_t s);
+// color = false (depth-layered binning): colours are computed lazily (ColorJob) for the listed ones
+void launch_preprocess(const DevMap& m, const DevCam& c, const ViewBufs& v, bool color, cudaStream_t s);
+// colours of every visible Gaussian (debug exports of a layered render)
+void launch_colors(const DevMap& m, const DevCam& c, const ViewBufs& v, cudaStream_t s);
 
 // Binning (binning.cu).  The pair count is read back once per view (host sync) to size the
 // pair arrays and the sort.
@@ -109,7 +113,7 @@ void launch_depth_scan(int64_t n, float near_plane, void* temp, const uint32_t**
 void launch_depth_order_layer_a(const ViewBufs& v, int64_t n, float near_plane, void* temp, uint32_t div,
                                 uint32_t min_pairs, int64_t gauss_cap, uint32_t cap_a, uint32_t* idx_sorted,
                                 uint2* cand_rect, uint32_t* ra, uint8_t* active, float* gacc_zero, bool rerun,
-                                cudaStream_t s);
+                                const ColorJob& cj, cudaStream_t s);
 void launch_depth_order_rest(const ViewBufs& v, int64_t n, float near_plane, void* temp, uint32_t* idx_sorted,
                              cudaStream_t s);
 // Layer-A tile lists (one warp per tile scanning the depth-ordered candidates, order-preserving
@@ -157,7 +161,7 @@ void launch_layer_prep(const uint32_t* unfinished, const uint2* ranges, int tile
                        uint32_t* order2, cudaStream_t s);
 void launch_layer_count(const ViewBufs& v, const uint32_t* idx_sorted, int64_t n, int tiles_x, const uint32_t* sat,
                         const uint32_t* count2, uint32_t* cnt_enum, uint32_t* total2, cudaStream_t s,
-                        float* gacc_zero = nullptr);
+                        float* gacc_zero, const ColorJob& cj);
 
 void launch_blend_fwd(const DevMap& m, const DevCam& c, const ViewBufs& v, const TileLists& tl,
                       const PixelState& ps, const FwdOut& o, cudaStream_t s);

@@ -53,21 +53,11 @@ void launch_pack_map(const float* pos, const float* rot, const float* log_s, con
 // ------------------------------------------------------------------------------------------
 constexpr int kPreThreads = 128;
 
-template <int DEG>
+// COLOR = false (depth-layered binning): no SH read here; the colours of the Gaussians that get
+// listed are computed where they are first listed (ColorJob, lgs_internal.cuh)
+template <int DEG, bool COLOR>
 __global__ void __launch_bounds__(kPreThreads) preprocess_kernel(DevMap m, DevCam c, ViewBufs v) {
-  constexpr int KS = 3 * (DEG + 1) * (DEG + 1);
-  constexpr int SS = KS + 1 - KS % 2;  // odd row stride: conflict-free per-thread rows
-  // SH rows of 16-byte multiples (degrees 1 and 3) are read per visible Gaussian straight from
-  // HBM (the culled ones' coefficients are never fetched); other degrees stage the CTA's rows
-  constexpr bool DIRECT = DEG > 0 && KS % 4 == 0;
-  __shared__ float s_sh[DEG > 0 && !DIRECT ? kPreThreads * SS : 1];
-  const int64_t i0 = (int64_t)blockIdx.x * kPreThreads;
-  const int64_t i = i0 + threadIdx.x;
-  if (DEG > 0 && !DIRECT) {  // the CTA's [128][K][3] SH block, loaded coalesced (float4)
-    const int nloc = (int)min((int64_t)kPreThreads, m.n - i0);
-    stage_rows_in<KS, SS, kPreThreads>(s_sh, m.sh + i0 * KS, nloc);
-    __syncthreads();
-  }
+  const int64_t i = (int64_t)blockIdx.x * kPreThreads + threadIdx.x;
   if (i >= m.n) return;
   v.iota[i] = (uint32_t)i;
   const float4 po = m.pos_opa[i];
@@ -160,54 +150,43 @@ __global__ void __launch_bounds__(kPreThreads) preprocess_kernel(DevMap m, DevCa
   }
 
   // colour (renderer.cpp:128; SH extension)
-  constexpr int K = (DEG + 1) * (DEG + 1);
-  float col[3];
-  if (DEG == 0) {
-    const float* sh = m.sh + i * 3;
-    col[0] = sh[0]; col[1] = sh[1]; col[2] = sh[2];
-  } else {
-    float dx = P0 - c.cc[0], dy = P1 - c.cc[1], dz = P2 - c.cc[2];
-    const float dn = sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz)));
-    const float idn = 1.0f / dn;
-    dx *= idn; dy *= idn; dz *= idn;
-    float b[16];
-    sh_basis_f32(DEG, dx, dy, dz, b);
-    if (DIRECT) {
-      // element j = 3 k + ch of the [K][3] row: each channel still accumulates in k order
-      const float4* row = reinterpret_cast<const float4*>(m.sh + i * KS);
-#pragma unroll
-      for (int q = 0; q < KS / 4; ++q) {
-        const float4 v4 = __ldg(row + q);
-        const float e4[4] = {v4.x, v4.y, v4.z, v4.w};
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          const int j = 4 * q + t, k = j / 3, ch = j % 3;
-          col[ch] = k == 0 ? e4[t] : fmaf(b[k], e4[t], col[ch]);
-        }
-      }
-    } else {
-      const float* sh = s_sh + threadIdx.x * SS;
-#pragma unroll
-      for (int ch = 0; ch < 3; ++ch) {
-        float acc = sh[ch];
-#pragma unroll
-        for (int k = 1; k < K; ++k) acc = fmaf(b[k], sh[k * 3 + ch], acc);
-        col[ch] = acc;
-      }
-    }
-  }
-  v.color[i] = make_float4(col[0], col[1], col[2], 0.0f);
+  if (COLOR) v.color[i] = gaussian_color<DEG>(m.sh, po, c.cc, i);
 }
 
-void launch_preprocess(const DevMap& m, const DevCam& c, const ViewBufs& v, cudaStream_t s) {
+// colours of every visible Gaussian (debug exports of a layered render)
+template <int DEG>
+__global__ void colors_kernel(DevMap m, DevCam c, ViewBufs v) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m.n || v.tiles[i] == 0) return;
+  v.color[i] = gaussian_color<DEG>(m.sh, m.pos_opa[i], c.cc, i);
+}
+
+void launch_colors(const DevMap& m, const DevCam& c, const ViewBufs& v, cudaStream_t s) {
   if (m.n == 0) return;
-  const int threads = kPreThreads;
-  const unsigned blocks = (unsigned)((m.n + threads - 1) / threads);
+  const unsigned blocks = (unsigned)((m.n + 255) / 256);
   switch (m.deg) {
-    case 0: preprocess_kernel<0><<<blocks, threads, 0, s>>>(m, c, v); break;
-    case 1: preprocess_kernel<1><<<blocks, threads, 0, s>>>(m, c, v); break;
-    case 2: preprocess_kernel<2><<<blocks, threads, 0, s>>>(m, c, v); break;
-    default: preprocess_kernel<3><<<blocks, threads, 0, s>>>(m, c, v); break;
+    case 0: colors_kernel<0><<<blocks, 256, 0, s>>>(m, c, v); break;
+    case 1: colors_kernel<1><<<blocks, 256, 0, s>>>(m, c, v); break;
+    case 2: colors_kernel<2><<<blocks, 256, 0, s>>>(m, c, v); break;
+    default: colors_kernel<3><<<blocks, 256, 0, s>>>(m, c, v); break;
+  }
+}
+
+template <int DEG>
+static void launch_pre(const DevMap& m, const DevCam& c, const ViewBufs& v, bool color, unsigned blocks,
+                       cudaStream_t s) {
+  if (color) preprocess_kernel<DEG, true><<<blocks, kPreThreads, 0, s>>>(m, c, v);
+  else preprocess_kernel<DEG, false><<<blocks, kPreThreads, 0, s>>>(m, c, v);
+}
+
+void launch_preprocess(const DevMap& m, const DevCam& c, const ViewBufs& v, bool color, cudaStream_t s) {
+  if (m.n == 0) return;
+  const unsigned blocks = (unsigned)((m.n + kPreThreads - 1) / kPreThreads);
+  switch (m.deg) {
+    case 0: launch_pre<0>(m, c, v, color, blocks, s); break;
+    case 1: launch_pre<1>(m, c, v, color, blocks, s); break;
+    case 2: launch_pre<2>(m, c, v, color, blocks, s); break;
+    default: launch_pre<3>(m, c, v, color, blocks, s); break;
   }
 }
 
