@@ -375,8 +375,10 @@ def run_ours(args):
         "tile_sort_ranges": ("hbm", LST * 4 + ntiles * 8),
         "blend_fwd": ("fp32", F_EVAL * evaluated + F_FWD * contributed),
         "blend_bwd": ("fp32", F_EVAL * evaluated + F_BWD * contributed),
-        # every gradient row written (zeros outside the active set) + the active rows' inputs
-        "preprocess_bwd": ("hbm", n + A * (16 * 3 + 12 * K + 16 + 128) + n * 4 * (11 + 3 * K + d)),
+        # the chain over the A active rows (flags scanned, accumulator + map rows read, rows written);
+        # the zero rows of every other Gaussian stream out in grad_zero (a side branch in the plan)
+        "preprocess_bwd": ("hbm", n + A * (16 * 3 + 12 * K + 16 + 128) + A * 4 * (11 + 3 * K + d)),
+        "grad_zero": ("hbm", n * 4 * (11 + 3 * K + d)),
     }
     if "blend_bwd" not in phases and "blend_fwd" in phases:  # captured fused-L1 step: one kernel
         phases["blend_fused"] = phases.pop("blend_fwd")
@@ -522,7 +524,7 @@ def run_mapping_step(args, dmap, cam, ctx, stream, flush, info, hbm_peak, fp32, 
         t = ph["adam"] * 1e-3
         rows["adam"] = {"ms": round(ph["adam"], 4), "bound": "hbm", "algorithmic_bytes": adam_bytes,
                         "achieved_gbs": round(adam_bytes / t / 1e9, 1), "frac": round(adam_bytes / t / 1e9 / hbm_peak, 4)}
-    for k in ("preprocess", "depth_sort_scan", "tile_sort_ranges", "blend_fwd", "blend_bwd", "preprocess_bwd"):
+    for k in ("preprocess", "depth_sort_scan", "tile_sort_ranges", "blend_fwd", "blend_bwd", "grad_zero", "preprocess_bwd"):
         if k in ph:
             rows[k] = {"ms": round(ph[k], 4)}
     return {"metric": "mapping iterations/s (render + loss + backward + Adam), same map and view", "value":

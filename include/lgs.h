@@ -234,8 +234,10 @@ LGS_API int64_t lgs_ctx_launch_count(const lgs_ctx* ctx);
 /* ---- phase profiling (CUDA events recorded on the context stream around each phase) -------
  * Phases: 0 preprocess, 1 depth sort + scan, 2 key duplication, 3 tile sort + ranges,
  * 4 blend forward, 5 blend backward, 6 preprocess backward, 7 map upload (pack), 8 mapping loss,
- * 9 Adam step, 10 gradient all-reduce, 11 coverage mask. */
-enum { LGS_PHASE_COUNT = 12 };
+ * 9 Adam step, 10 gradient all-reduce, 11 coverage mask, 12 zero rows of the gradient buffers
+ * (depth-layered binning: the backward chain writes only the active rows; in a plan this phase
+ * runs on a side branch concurrent with the forward). */
+enum { LGS_PHASE_COUNT = 13 };
 LGS_API const char* lgs_phase_name(int32_t phase);
 LGS_API lgs_status lgs_ctx_profile(lgs_ctx* ctx, int32_t enable);
 /* Accumulated device milliseconds and launch counts per phase since the last reset

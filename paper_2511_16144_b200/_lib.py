@@ -159,7 +159,7 @@ SIGNATURES = [
     ("lgs_allreduce_grads_sparse", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_int64)]),
 ]
 
-LGS_PHASE_COUNT = 12
+LGS_PHASE_COUNT = 13
 
 _lib = None
 

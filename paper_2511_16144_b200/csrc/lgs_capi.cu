@@ -179,35 +179,36 @@ struct PhaseScope {
     return e;
   }
   bool graph = false;  // inside a plan capture: external event-record nodes of the graph
-  PhaseScope(lgs_ctx* c, int phase)
+  cudaStream_t st;
+  PhaseScope(lgs_ctx* c, int phase, cudaStream_t on_stream = nullptr)
       : ctx(c), on(c->profiling && !c->capturing),
-        graph(c->capturing && c->capture_marks && !c->cond_parent) {
+        graph(c->capturing && c->capture_marks && !c->cond_parent), st(on_stream ? on_stream : c->stream) {
     if (!on && !graph) return;
     m.phase = phase;
     if (graph) {
       cudaEventCreate(&m.a);
       cudaEventCreate(&m.b);
-      cudaEventRecordWithFlags(m.a, ctx->stream, cudaEventRecordExternal);
+      cudaEventRecordWithFlags(m.a, st, cudaEventRecordExternal);
       return;
     }
     m.a = take();
     m.b = take();
-    cudaEventRecord(m.a, ctx->stream);
+    cudaEventRecord(m.a, st);
   }
   ~PhaseScope() {
     if (graph) {
-      cudaEventRecordWithFlags(m.b, ctx->stream, cudaEventRecordExternal);
+      cudaEventRecordWithFlags(m.b, st, cudaEventRecordExternal);
       ctx->capture_marks->push_back(m);
       return;
     }
     if (!on) return;
-    cudaEventRecord(m.b, ctx->stream);
+    cudaEventRecord(m.b, st);
     ctx->marks.push_back(m);
   }
 };
 
 enum { PH_PREPROCESS = 0, PH_DEPTH_SORT, PH_DUPLICATE, PH_TILE_SORT, PH_BLEND_FWD, PH_BLEND_BWD, PH_PREPROCESS_BWD,
-       PH_UPLOAD, PH_LOSS, PH_ADAM, PH_ALLREDUCE, PH_COVERAGE };
+       PH_UPLOAD, PH_LOSS, PH_ADAM, PH_ALLREDUCE, PH_COVERAGE, PH_GRAD_ZERO };
 
 }  // namespace
 
@@ -696,8 +697,11 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
     // blend run (the backward's chain then writes only the active rows)
     CUDAB(cudaEventRecord(ctx->side_fork, s));
     CUDAB(cudaStreamWaitEvent(ctx->side_stream, ctx->side_fork, 0));
-    launch_grad_zero(device_grad_out(ctx->prezero, map->dm.d), n, map->dm.K, map->dm.dp > 0 ? map->dm.d : 0,
-                     ctx->side_stream);
+    {
+      PhaseScope ph(ctx, PH_GRAD_ZERO, ctx->side_stream);
+      launch_grad_zero(device_grad_out(ctx->prezero, map->dm.d), n, map->dm.K, map->dm.dp > 0 ? map->dm.d : 0,
+                       ctx->side_stream);
+    }
     CUDAB(cudaEventRecord(ctx->side_join, ctx->side_stream));
     ctx->prezero_forked = true;
     ctx->launches++;
@@ -1055,16 +1059,22 @@ lgs_status run_backward(lgs_ctx* ctx, const lgs_saved* t, const BwdIn& in_dev, l
     go.pose = dpose;
   }
   // zero rows already enqueued on the plan's side branch (the forward forked it)?
-  const bool zeroed = ctx->prezero_forked && grads == ctx->prezero && !host && t->vb.active;
+  bool zeroed = ctx->prezero_forked && grads == ctx->prezero && !host && t->vb.active;
   if (ctx->prezero_forked) {
     LGS_CUDA(cudaStreamWaitEvent(s, ctx->side_join, 0));
     ctx->prezero_forked = false;
+  }
+  if (t->vb.active && !zeroed) {  // sparse chain below: the zero rows first (none when accumulating)
+    PhaseScope ph(ctx, PH_GRAD_ZERO);
+    launch_grad_zero(go, n, K, t->dm.dp > 0 ? d : 0, s);
+    if (!go.accumulate) ctx->launches++;
+    zeroed = true;
   }
   {
     PhaseScope ph(ctx, PH_PREPROCESS_BWD);
     launch_preprocess_bwd(t->dm, t->cam, t->vb, gacc, slots, go, zeroed, s);
   }
-  ctx->launches += (t->vb.active && !zeroed && !go.accumulate) ? 2 : 1;
+  ctx->launches++;
   LGS_CUDA(cudaGetLastError());
   if (host) {
     float* dst[6] = {grads->position, grads->rotation, grads->log_scale, grads->opacity_logit, grads->sh,
@@ -1389,7 +1399,7 @@ LGS_API lgs_status lgs_saved_work(const lgs_saved* tape, int64_t* evaluated, int
 LGS_API const char* lgs_phase_name(int32_t phase) {
   static const char* names[LGS_PHASE_COUNT] = {"preprocess", "depth_sort_scan", "duplicate_keys", "tile_sort_ranges",
                                                "blend_fwd", "blend_bwd", "preprocess_bwd", "map_upload",
-                                               "mapping_loss", "adam", "allreduce", "coverage"};
+                                               "mapping_loss", "adam", "allreduce", "coverage", "grad_zero"};
   return (phase >= 0 && phase < LGS_PHASE_COUNT) ? names[phase] : "?";
 }
 

@@ -523,3 +523,14 @@ def test_layered_capacity_overflow_and_ties():
     for t in range(lr.shape[0]):
         a = lv[lr[t, 0]:lr[t, 1]]
         assert np.array_equal(a, fv[fr[t, 0]:fr[t, 0] + a.size]), t
+
+
+@pytest.mark.parametrize("deg", [1, 2])
+def test_layered_lazy_colours_sh_degrees(deg):
+    """The layered path evaluates colours where a Gaussian is first listed (not in K1): SH degrees
+    1 and 2 (degree 2's 27-float rows take the scalar-load path) render bitwise like K1's colours."""
+    scene, cams, info = scenes.make_config("c1", n=30_000)
+    k = (deg + 1) ** 2
+    scene = dict(scene, sh=np.ascontiguousarray(scene["sh"][:, :k]))
+    tg = scenes.make_targets(cams[0], scene["feat"].shape[0], info["depth_range"], 7)
+    _layered_vs_full(scene, cams[0], tg)
