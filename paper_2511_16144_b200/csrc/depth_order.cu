@@ -381,13 +381,15 @@ void launch_depth_order_layer_a(const ViewBufs& v, int64_t n, float near_plane, 
              (const uint32_t*)c.big_a, c.scratch, c.sc + kScScratch, o);
 }
 
-// Layer-A tile lists: one CTA per tile; its 8 warps split the R_A depth-ordered candidates into
-// contiguous segments, count those whose tile rect holds the tile, take their offsets from a
-// shared-memory prefix (one atomic reserves the tile's list), then write them with an
-// order-preserving ballot compaction -- each list is the exact depth-order prefix of the tile's
-// complete list.  R_A is ~0.5-5% of the visible Gaussians: ~2-16k coalesced 8-byte reads per tile,
-// from L2.
-constexpr int kListWarps = 8;
+// Layer-A tile lists: one CTA per run of kSegTiles tiles of a tile row.  Its warps split the R_A
+// depth-ordered candidates into contiguous segments; a lane turns its candidate's tile rect into
+// a bitmask of the run's tiles it covers, and per tile one ballot counts (pass 1) or places (pass
+// 2, order-preserving compaction) the warp's 32 candidates.  The run's lists are reserved with one
+// atomic and laid out tile after tile; within a tile, warp segments follow each other, so every
+// list is the exact depth-order prefix of the tile's complete list.  R_A is ~0.5-5% of the visible
+// Gaussians (a few thousand), read twice per run from L2.
+constexpr int kListWarps = 16;
+constexpr int kSegTiles = 8;
 
 __global__ void __launch_bounds__(kListWarps * 32) layer_tile_lists_kernel(
     const uint2* __restrict__ cand_rect, const uint32_t* __restrict__ cand_idx, const uint32_t* __restrict__ ra,
@@ -398,48 +400,82 @@ __global__ void __launch_bounds__(kListWarps * 32) layer_tile_lists_kernel(
     if (blend_counter) *blend_counter = 0;
     if (loss) *loss = 0.0;
   }
-  __shared__ uint32_t s_cnt[kListWarps], s_base;
-  const int t = blockIdx.x;
+  __shared__ uint32_t s_cnt[kListWarps][kSegTiles];
+  __shared__ uint32_t s_base;
+  const int nseg = (tiles_x + kSegTiles - 1) / kSegTiles;
+  const uint32_t ty = blockIdx.x / nseg;
+  const uint32_t tx0 = (blockIdx.x % nseg) * kSegTiles;
+  const uint32_t ntl = min((uint32_t)kSegTiles, (uint32_t)tiles_x - tx0);  // tiles in this run
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t n_cand = *ra;
-  const uint32_t tx = (uint32_t)(t % tiles_x), ty = (uint32_t)(t / tiles_x);
   const uint32_t seg = ((n_cand + kListWarps * 32 - 1) / (kListWarps * 32)) * 32;
   const uint32_t c0 = min(n_cand, warp * seg), c1 = min(n_cand, c0 + seg);
-  auto covers = [&](uint32_t i) {
+  // bit j: candidate i's tile rect holds tile (tx0 + j, ty)
+  auto mask_of = [&](uint32_t i) -> uint32_t {
+    if (i >= c1) return 0u;
     const uint2 tr = __ldg(cand_rect + i);
-    return tx >= (tr.x & 0xffffu) && tx <= (tr.x >> 16) && ty >= (tr.y & 0xffffu) && ty <= (tr.y >> 16);
+    const uint32_t y0 = tr.y & 0xffffu, y1 = tr.y >> 16;
+    if (ty < y0 || ty > y1) return 0u;
+    const int lo = max((int)(tr.x & 0xffffu) - (int)tx0, 0);
+    const int hi = min((int)(tr.x >> 16) - (int)tx0, (int)ntl - 1);
+    return lo > hi ? 0u : ((2u << hi) - 1u) & ~((1u << lo) - 1u);
   };
-  uint32_t cnt = 0;
-#pragma unroll 4
-  for (uint32_t i = c0 + lane; i < c1; i += 32) cnt += covers(i) ? 1u : 0u;
-  cnt = __reduce_add_sync(0xffffffffu, cnt);
-  if (lane == 0) s_cnt[warp] = cnt;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    uint32_t tot = 0;
-    for (int w = 0; w < kListWarps; ++w) {
-      const uint32_t c = s_cnt[w];
-      s_cnt[w] = tot;
-      tot += c;
-    }
-    s_base = atomicAdd(cursor, tot);
-    ranges[t] = make_uint2(s_base, s_base + tot);
+  uint32_t cnt[kSegTiles];
+#pragma unroll
+  for (int j = 0; j < kSegTiles; ++j) cnt[j] = 0;
+#pragma unroll 2
+  for (uint32_t i0 = c0; i0 < c1; i0 += 32) {
+    const uint32_t m = mask_of(i0 + lane);
+#pragma unroll
+    for (int j = 0; j < kSegTiles; ++j) cnt[j] += __popc(__ballot_sync(0xffffffffu, (m >> j) & 1u));
+  }
+  if (lane < kSegTiles) {
+    uint32_t mine = 0;
+#pragma unroll
+    for (int j = 0; j < kSegTiles; ++j) mine = lane == j ? cnt[j] : mine;
+    s_cnt[warp][lane] = mine;
   }
   __syncthreads();
-  uint32_t pos = s_base + s_cnt[warp];
+  if (threadIdx.x == 0) {  // run-level layout: tile after tile, warp segments in order within a tile
+    uint32_t tot = 0;
+    uint32_t start[kSegTiles];
+    for (uint32_t j = 0; j < ntl; ++j) {
+      start[j] = tot;
+      for (int w = 0; w < kListWarps; ++w) {
+        const uint32_t c = s_cnt[w][j];
+        s_cnt[w][j] = tot;
+        tot += c;
+      }
+    }
+    s_base = atomicAdd(cursor, tot);
+    for (uint32_t j = 0; j < ntl; ++j)
+      ranges[ty * tiles_x + tx0 + j] = make_uint2(s_base + start[j], s_base + (j + 1 < ntl ? start[j + 1] : tot));
+  }
+  __syncthreads();
+  uint32_t pos[kSegTiles];
+#pragma unroll
+  for (int j = 0; j < kSegTiles; ++j) pos[j] = s_base + (j < (int)ntl ? s_cnt[warp][j] : 0u);
+  const unsigned lt = (1u << lane) - 1u;
   for (uint32_t i0 = c0; i0 < c1; i0 += 32) {
     const uint32_t i = i0 + lane;
-    const bool hit = i < c1 && covers(i);
-    const unsigned bal = __ballot_sync(0xffffffffu, hit);
-    if (hit) vals[pos + __popc(bal & ((1u << lane) - 1u))] = __ldg(cand_idx + i);
-    pos += __popc(bal);
+    const uint32_t m = mask_of(i);
+    const uint32_t g = m ? __ldg(cand_idx + i) : 0u;
+#pragma unroll
+    for (int j = 0; j < kSegTiles; ++j) {
+      const bool hit = (m >> j) & 1u;
+      const unsigned bal = __ballot_sync(0xffffffffu, hit);
+      if (hit) vals[pos[j] + __popc(bal & lt)] = g;
+      pos[j] += __popc(bal);
+    }
   }
 }
 
 void launch_layer_tile_lists(const uint2* cand_rect, const uint32_t* cand_idx, const uint32_t* n_cand, int tiles_x,
                              int ntiles, uint32_t* cursor, uint32_t* vals, uint2* ranges, int* blend_counter,
                              double* loss, cudaStream_t s) {
-  launch_pdl(layer_tile_lists_kernel, dim3(ntiles), dim3(kListWarps * 32), 0, s, cand_rect, cand_idx, n_cand, tiles_x,
+  const int tiles_y = ntiles / tiles_x;
+  const int runs = tiles_y * ((tiles_x + kSegTiles - 1) / kSegTiles);
+  launch_pdl(layer_tile_lists_kernel, dim3(runs), dim3(kListWarps * 32), 0, s, cand_rect, cand_idx, n_cand, tiles_x,
              cursor, vals, ranges, blend_counter, loss);
 }
 

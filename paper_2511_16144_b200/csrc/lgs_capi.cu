@@ -692,20 +692,28 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
     else launch_sum_tiles(t->vb.tiles, n, ctx->dev_u32, s);
   }
   ctx->launches += layered ? 3 : 2;
-  if (layered && ctx->capturing && ctx->prezero && !ctx->prezero_forked && n > 0) {
-    // side branch: the gradient buffers' zero rows stream out while the depth order and the
-    // blend run (the backward's chain then writes only the active rows)
-    CUDAB(cudaEventRecord(ctx->side_fork, s));
-    CUDAB(cudaStreamWaitEvent(ctx->side_stream, ctx->side_fork, 0));
+  // side branch of a plan: the gradient buffers' zero rows stream out beside the forward (the
+  // backward's chain then writes only the active rows).  Forked after K1 or, by default, right
+  // before the first blend, which is issue-bound and leaves HBM to the stores.
+  static const bool prezero_at_k1 = [] {
+    const char* e = getenv("LGS_PREZERO_AT");
+    return e && strcmp(e, "k1") == 0;
+  }();
+  auto fork_prezero = [&]() -> lgs_status {
+    if (!(layered && ctx->capturing && ctx->prezero && !ctx->prezero_forked && n > 0)) return LGS_OK;
+    LGS_CUDA(cudaEventRecord(ctx->side_fork, s));
+    LGS_CUDA(cudaStreamWaitEvent(ctx->side_stream, ctx->side_fork, 0));
     {
       PhaseScope ph(ctx, PH_GRAD_ZERO, ctx->side_stream);
       launch_grad_zero(device_grad_out(ctx->prezero, map->dm.d), n, map->dm.K, map->dm.dp > 0 ? map->dm.d : 0,
                        ctx->side_stream);
     }
-    CUDAB(cudaEventRecord(ctx->side_join, ctx->side_stream));
+    LGS_CUDA(cudaEventRecord(ctx->side_join, ctx->side_stream));
     ctx->prezero_forked = true;
     ctx->launches++;
-  }
+    return LGS_OK;
+  };
+  if (prezero_at_k1) TRYB(fork_prezero());
   if (n > 0) {
     CUDAB(cudaMemcpyAsync(ctx->host_u32, dev_pairs, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
     if (!ctx->capturing) CUDAB(cudaEventRecord(ctx->pairs_ready, s));
@@ -827,6 +835,7 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
       if (targets && !fuse) LGS_CUDA(cudaMemsetAsync(t->loss, 0, sizeof(double), s));
       FwdOut fo1 = fo;
       fo1.unfinished = unfinished;
+      TRYB(fork_prezero());
       {
         PhaseScope ph(ctx, PH_BLEND_FWD);
         if (fuse)

@@ -396,35 +396,40 @@ __global__ void __launch_bounds__(kPbThreads) preprocess_bwd_kernel(DevMap m, De
 // kernel whose blocks each compact the active rows of a contiguous range into a shared queue and
 // run the chain one queue entry per thread, storing (or adding) each active row.  Same values as
 // the dense kernel per row.
-constexpr int kZeroRows = 256;
+struct ZeroSegs {
+  float* ptr[6];  // position, rotation, log-scale, opacity, SH, feature ([d][N]: one contiguous block)
+  int64_t count[6];
+};
 
-__global__ void __launch_bounds__(kZeroRows) grad_zero_kernel(GradOut g, int64_t n, int KS, int d) {
-  const int tid = threadIdx.x;
-  const int64_t i0 = (int64_t)blockIdx.x * kZeroRows;
-  const int nloc = (int)min((int64_t)kZeroRows, n - i0);
-  auto zero_rows = [&](float* base, int64_t cnt) {
-    if (!base) return;
-    int64_t j0 = 0;
-    if ((reinterpret_cast<uintptr_t>(base) & 15u) == 0) {
-      float4* b4 = reinterpret_cast<float4*>(base);
-      const int64_t n4 = cnt >> 2;
-      for (int64_t j = tid; j < n4; j += kZeroRows) __stcs(b4 + j, make_float4(0.f, 0.f, 0.f, 0.f));
-      j0 = n4 * 4;
-    }
-    for (int64_t j = j0 + tid; j < cnt; j += kZeroRows) base[j] = 0.f;
-  };
-  zero_rows(g.position ? g.position + i0 * 3 : nullptr, (int64_t)nloc * 3);
-  zero_rows(g.rotation ? g.rotation + i0 * 4 : nullptr, (int64_t)nloc * 4);
-  zero_rows(g.log_scale ? g.log_scale + i0 * 3 : nullptr, (int64_t)nloc * 3);
-  zero_rows(g.opacity_logit ? g.opacity_logit + i0 : nullptr, nloc);
-  zero_rows(g.sh ? g.sh + i0 * KS : nullptr, (int64_t)nloc * KS);
-  if (g.feature)
-    for (int k = 0; k < d; ++k) zero_rows(g.feature + (int64_t)k * n + i0, nloc);
+// grid-stride 16-byte streaming stores over each contiguous attribute block (scalar head / tail).
+// A small grid (2 CTAs per SM): stores are fire-and-forget, so a few warps per SM saturate HBM
+// writes while leaving the SMs to the kernels it runs beside (a side branch of the plan).
+__global__ void __launch_bounds__(256) grad_zero_kernel(ZeroSegs z) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+#pragma unroll
+  for (int a = 0; a < 6; ++a) {
+    float* p = z.ptr[a];
+    if (!p) continue;
+    const int64_t cnt = z.count[a];
+    const int64_t head = min(cnt, (int64_t)(((16u - (reinterpret_cast<uintptr_t>(p) & 15u)) & 15u) >> 2));
+    if (t < head) p[t] = 0.f;
+    float4* p4 = reinterpret_cast<float4*>(p + head);
+    const int64_t n4 = (cnt - head) >> 2;
+    for (int64_t j = t; j < n4; j += stride) __stcs(p4 + j, make_float4(0.f, 0.f, 0.f, 0.f));
+    const int64_t tail = head + n4 * 4 + t;
+    if (tail < cnt) p[tail] = 0.f;
+  }
 }
 
 void launch_grad_zero(const GradOut& g, int64_t n, int K, int d, cudaStream_t s) {
   if (n == 0 || g.accumulate) return;
-  grad_zero_kernel<<<(unsigned)((n + kZeroRows - 1) / kZeroRows), kZeroRows, 0, s>>>(g, n, 3 * K, d);
+  const ZeroSegs z{{g.position, g.rotation, g.log_scale, g.opacity_logit, g.sh, d > 0 ? g.feature : nullptr},
+                   {n * 3, n * 4, n * 3, n, n * 3 * K, n * d}};
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  grad_zero_kernel<<<(unsigned)(sms * 2), 256, 0, s>>>(z);
 }
 
 constexpr int kActFlags = 16;                         // active flags per thread (one 16-byte load)
