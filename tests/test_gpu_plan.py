@@ -57,9 +57,11 @@ def test_plan_matches_eager_and_replays():
     plan = R.Plan(dm, cam, tg, grads, images=imgs, pose_out=pose)
     assert plan.launches > 10
     out, g = _eager(dm, cam, tg)
-    for _ in range(3):  # replays are stable
+    for _ in range(3):  # replays are stable, and every gradient row is written (zero rows included)
+        grads["flat"].fill_(float("nan"))
         plan.run()
         pairs = plan.sync()
+        assert not torch.isnan(grads["flat"]).any()
         _check(grads, pose, imgs, out, g)
     assert pairs == out.stats()["pairs"]
     assert plan.elapsed_ms() > 0.0
@@ -113,3 +115,19 @@ def test_plan_layered_second_pass_toggles(name):
         plan.sync()
         out, g = _eager(dm, cam, tg)
         _check(grads, pose, imgs, out, g)
+
+
+def test_eager_backward_overwrites_every_row():
+    """The layered backward writes the chain's rows for the active Gaussians only and streams zeros
+    into every other row: a gradient buffer full of NaN comes back equal to a fresh one."""
+    scene, cam, ctx, dm, tg = _setup()
+    out, g = _eager(dm, cam, tg)
+    dirty = R.alloc_grads(dm.n, dm.d, dm.K, device=0)
+    dirty["flat"].fill_(float("nan"))
+    out2 = R.render(dm, cam, targets=tg)
+    R.render_backward_l1(out2, into=dirty)
+    torch.cuda.synchronize()
+    assert not torch.isnan(dirty["flat"]).any()
+    for k in GROUPS:
+        frac, worst = grad_mismatch(dirty[k], g[k])
+        assert frac < 1e-3, (k, frac, worst)
