@@ -446,6 +446,9 @@ def run_ours(args):
     # ---- end to end through the public API with host buffers -----------------------------------
     if not args.no_e2e:
         result["e2e"] = run_e2e(args, scene, cam, tg, R, local)
+        # the same with the whole map copied every step (LGS_MEM_HOST): 150 MB more H2D per step
+        full = run_e2e(args, scene, cam, tg, R, local, mapped=False)
+        result["e2e"]["whole_map_copied"] = {k: full[k] for k in ("value", "ms_per_step", "h2d_bytes_per_step")}
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         result["cpu_baseline"] = cpu_baseline(scene, cam, tg, args)
@@ -539,14 +542,18 @@ def pinned_like(a):
     return t.numpy()
 
 
-def run_e2e(args, scene, cam, tg, R, device):
+def run_e2e(args, scene, cam, tg, R, device, mapped=True):
     """Same step through the reference-facing API with HOST buffers: every step uploads the map
     and targets (H2D), renders, reads back the images, the gradients, the pose gradient and the
     loss (D2H).  PCIe, not the GPU, bounds this path (~350 MB moved per step), so the headline
     number runs ``--e2e-threads`` host threads, each with its own context / stream and its own
     output buffers, rendering concurrently as the reference API allows (renders are pure with
     respect to the map): one thread's gradient download overlaps the next
-    thread's map upload on the full-duplex link.  The single-thread number is reported beside it."""
+    thread's map upload on the full-duplex link.  The single-thread number is reported beside it.
+
+    ``mapped`` (the headline): the host map is page-locked and passed as LGS_MEM_HOST_MAPPED, so
+    positions / rotations / scales / opacities are copied (22 MB) while the SH rows and features of
+    just the listed Gaussians are read in place over PCIe; otherwise the whole map is copied."""
     import numpy as np
     import torch
 
@@ -570,7 +577,7 @@ def run_e2e(args, scene, cam, tg, R, device):
             self.loss = None
 
         def step(self):
-            out = R.render(hscene, cam, targets=htg, ctx=self.ctx, out=self.img)
+            out = R.render(hscene, cam, targets=htg, ctx=self.ctx, out=self.img, host_mapped=mapped)
             R.render_backward_l1(out, pose=True, into=self.grads)
             self.loss = out.l1_loss()
 
@@ -604,12 +611,17 @@ def run_e2e(args, scene, cam, tg, R, device):
     workers = [Worker() for _ in range(nthreads)]
     ms = timed(workers, args.e2e_steps)
     ms1 = timed(workers[:1], args.e2e_steps) if nthreads > 1 else ms
-    h2d = sum(v.nbytes for v in hscene.values()) + sum(v.nbytes for v in htg.values())
+    if mapped:  # copied attributes + the listed Gaussians' SH rows and features read in place
+        act = R.render(hscene, cam, ctx=workers[0].ctx, host_mapped=True).stats()["active"]
+        h2d = 4 * n * 11 + sum(v.nbytes for v in htg.values()) + act * 4 * (3 * K + d)
+    else:
+        h2d = sum(v.nbytes for v in hscene.values()) + sum(v.nbytes for v in htg.values())
     d2h = sum(v.nbytes for v in workers[0].img.values()) + workers[0].flat.nbytes + 6 * 4 + 8
     return {"value": round(1000.0 / ms, 3), "unit": UNIT, "ms_per_step": round(ms, 3), "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "host_threads": nthreads,
             "single_thread": {"value": round(1000.0 / ms1, 3), "ms_per_step": round(ms1, 3)},
-            "api": "renderer.render(host numpy map, host targets) + render_backward_l1(host grads) + l1_loss(); "
+            "api": f"renderer.render(host numpy map{', host_mapped' if mapped else ''}, host targets) + "
+                   "render_backward_l1(host grads) + l1_loss(); "
                    f"{nthreads} host threads x own lgs_ctx/stream, wall clock over all steps"}
 
 

@@ -58,7 +58,14 @@ typedef enum {
   LGS_EIO = 5     /* map file error (reference: lego::IoError, errors.hpp:21) */
 } lgs_status;
 
-enum { LGS_MEM_HOST = 0, LGS_MEM_DEVICE = 1 };
+enum { LGS_MEM_HOST = 0, LGS_MEM_DEVICE = 1, LGS_MEM_HOST_MAPPED = 2 };
+/* LGS_MEM_HOST_MAPPED (lgs_gaussians only): page-locked host memory (cudaHostAlloc /
+ * cudaHostRegister, device-addressable under UVA) that the device reads in place where few rows
+ * are needed.  Positions, rotations, scales and opacities are copied as for LGS_MEM_HOST; the SH
+ * coefficients and the features are NOT: with the depth-layered binning only the listed Gaussians'
+ * rows cross PCIe (their colours and features are fetched where they are first listed).  The
+ * caller keeps the buffers alive and unchanged while the map and its tapes are in use (no
+ * synchronization at create/update).  Render-only: Adam, download and save reject such a map. */
 
 enum { LGS_TILE = 16, LGS_MAX_FEATURE_DIM = 32, LGS_MAX_SH_DEGREE = 3 };
 
@@ -98,7 +105,7 @@ typedef struct {
   const float* opacity_logits; /* [N] */
   const float* sh;             /* [N][K][3] */
   const float* features;       /* [d][N] */
-  int32_t memory;              /* LGS_MEM_HOST / LGS_MEM_DEVICE */
+  int32_t memory;              /* LGS_MEM_HOST / LGS_MEM_DEVICE / LGS_MEM_HOST_MAPPED */
 } lgs_gaussians;
 
 /* Caller-owned output images, HWC.  Any pointer may be NULL (not written). */

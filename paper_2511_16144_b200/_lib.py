@@ -12,7 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "liblgs.so")
 
 LGS_OK, LGS_EINVAL, LGS_ECUDA, LGS_ENOMEM, LGS_ENODEV, LGS_EIO = range(6)
-LGS_MEM_HOST, LGS_MEM_DEVICE = 0, 1
+LGS_MEM_HOST, LGS_MEM_DEVICE, LGS_MEM_HOST_MAPPED = 0, 1, 2
 
 _fp = C.POINTER(C.c_float)
 

@@ -220,6 +220,8 @@ struct lgs_map {
   float4* scale = nullptr;
   float* sh = nullptr;
   float* feat = nullptr;
+  bool mapped = false;             // LGS_MEM_HOST_MAPPED: dm.sh and feat_src point into page-locked host memory
+  const float* feat_src = nullptr;  // [d][N], device-addressable (features gathered lazily)
 };
 
 struct lgs_adam {
@@ -352,23 +354,42 @@ lgs_status copy_in(lgs_ctx* ctx, void* dst, const void* src, size_t bytes, int m
   return LGS_OK;
 }
 
+// device address of page-locked host memory (LGS_MEM_HOST_MAPPED), or an error
+lgs_status mapped_ptr(const float* p, const float** dev, const char* what) {
+  *dev = nullptr;
+  if (!p) return LGS_OK;
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess || a.type != cudaMemoryTypeHost || !a.devicePointer) {
+    cudaGetLastError();
+    return fail(LGS_EINVAL, "LGS_MEM_HOST_MAPPED: %s is not page-locked host memory", what);
+  }
+  *dev = static_cast<const float*>(a.devicePointer);
+  return LGS_OK;
+}
+
 lgs_status map_upload(lgs_ctx* ctx, lgs_map* m, const lgs_gaussians* src) {
   const int64_t n = m->dm.n;
   const int d = m->dm.d, K = m->dm.K;
-  // the SH block has the same layout on both sides
-  LGS_TRY(copy_in(ctx, m->sh, src->sh, sizeof(float) * (size_t)n * K * 3, src->memory));
+  const bool mapped = src->memory == LGS_MEM_HOST_MAPPED;
+  const int mem = mapped ? LGS_MEM_HOST : src->memory;
+  if (mapped) {  // read in place: the SH rows of the listed Gaussians, their features gathered lazily
+    LGS_TRY(mapped_ptr(src->sh, &m->dm.sh, "sh"));
+    LGS_TRY(mapped_ptr(d > 0 ? src->features : nullptr, &m->feat_src, "features"));
+  } else {  // the SH block has the same layout on both sides
+    LGS_TRY(copy_in(ctx, m->sh, src->sh, sizeof(float) * (size_t)n * K * 3, src->memory));
+  }
   const float *pos = src->positions, *rot = src->rotations, *ls = src->log_scales, *op = src->opacity_logits,
-              *ft = src->features;
+              *ft = mapped ? nullptr : src->features;
   float* stage = nullptr;
-  if (src->memory == LGS_MEM_HOST) {
-    const size_t tot = (size_t)n * (3 + 4 + 3 + 1 + d);
+  if (mem == LGS_MEM_HOST) {
+    const size_t tot = (size_t)n * (3 + 4 + 3 + 1 + (mapped ? 0 : d));
     LGS_TRY(dalloc(ctx, &stage, tot));
     float* p = stage;
     LGS_TRY(copy_in(ctx, p, src->positions, sizeof(float) * n * 3, LGS_MEM_HOST)); pos = p; p += n * 3;
     LGS_TRY(copy_in(ctx, p, src->rotations, sizeof(float) * n * 4, LGS_MEM_HOST)); rot = p; p += n * 4;
     LGS_TRY(copy_in(ctx, p, src->log_scales, sizeof(float) * n * 3, LGS_MEM_HOST)); ls = p; p += n * 3;
     LGS_TRY(copy_in(ctx, p, src->opacity_logits, sizeof(float) * n, LGS_MEM_HOST)); op = p; p += n;
-    if (d > 0) { LGS_TRY(copy_in(ctx, p, src->features, sizeof(float) * n * d, LGS_MEM_HOST)); ft = p; }
+    if (d > 0 && !mapped) { LGS_TRY(copy_in(ctx, p, src->features, sizeof(float) * n * d, LGS_MEM_HOST)); ft = p; }
   }
   {
     PhaseScope ph(ctx, PH_UPLOAD);
@@ -390,7 +411,8 @@ lgs_status check_gaussians(const lgs_gaussians* src) {
   if (src->n > 0 && (!src->positions || !src->rotations || !src->log_scales || !src->opacity_logits || !src->sh ||
                      (src->feature_dim > 0 && !src->features)))
     return fail(LGS_EINVAL, "a map attribute pointer is NULL");
-  if (src->memory != LGS_MEM_HOST && src->memory != LGS_MEM_DEVICE) return fail(LGS_EINVAL, "bad memory kind");
+  if (src->memory != LGS_MEM_HOST && src->memory != LGS_MEM_DEVICE && src->memory != LGS_MEM_HOST_MAPPED)
+    return fail(LGS_EINVAL, "bad memory kind");
   return LGS_OK;
 }
 
@@ -556,9 +578,11 @@ LGS_API lgs_status lgs_map_create(lgs_ctx* ctx, const lgs_gaussians* src, lgs_ma
   m->dm.deg = src->sh_degree;
   m->dm.K = (src->sh_degree + 1) * (src->sh_degree + 1);
   const size_t n = (size_t)src->n;
+  m->mapped = src->memory == LGS_MEM_HOST_MAPPED;
   lgs_status st = LGS_OK;
   if ((st = dalloc(ctx, &m->pos_opa, n)) != LGS_OK || (st = dalloc(ctx, &m->rot, n)) != LGS_OK ||
-      (st = dalloc(ctx, &m->scale, n)) != LGS_OK || (st = dalloc(ctx, &m->sh, n * m->dm.K * 3)) != LGS_OK ||
+      (st = dalloc(ctx, &m->scale, n)) != LGS_OK ||
+      (!m->mapped && (st = dalloc(ctx, &m->sh, n * m->dm.K * 3)) != LGS_OK) ||
       (st = dalloc(ctx, &m->feat, n * (m->dm.dp > 0 ? m->dm.dp : 1))) != LGS_OK ||
       (st = map_upload(ctx, m, src)) != LGS_OK) {
     free_map(m);
@@ -567,7 +591,7 @@ LGS_API lgs_status lgs_map_create(lgs_ctx* ctx, const lgs_gaussians* src, lgs_ma
   m->dm.pos_opa = m->pos_opa;
   m->dm.rot = m->rot;
   m->dm.scale = m->scale;
-  m->dm.sh = m->sh;
+  if (!m->mapped) m->dm.sh = m->sh;
   m->dm.feat = m->feat;
   if (src->memory == LGS_MEM_HOST) LGS_CUDA(cudaStreamSynchronize(ctx->stream));
   *out = m;
@@ -579,6 +603,8 @@ LGS_API lgs_status lgs_map_update(lgs_ctx* ctx, lgs_map* map, const lgs_gaussian
   LGS_TRY(check_gaussians(src));
   if (src->n != map->dm.n || src->feature_dim != map->dm.d || src->sh_degree != map->dm.deg)
     return fail(LGS_EINVAL, "lgs_map_update: shape differs from the map");
+  if (map->mapped != (src->memory == LGS_MEM_HOST_MAPPED))
+    return fail(LGS_EINVAL, "lgs_map_update: a host-mapped map is updated from host-mapped memory only");
   LGS_CUDA(cudaSetDevice(ctx->device));
   LGS_TRY(map_upload(ctx, map, src));
   if (src->memory == LGS_MEM_HOST) LGS_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -674,6 +700,17 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
     for (int a = 0; a < 3; ++a) cj.cc[a] = dc.cc[a];
     cj.deg = map->dm.deg;
     cj.color = t->vb.color;
+    if (map->mapped && map->feat_src) {
+      cj.feat_src = map->feat_src;
+      cj.feat_dst = map->feat;
+      cj.n = n;
+      cj.d = map->dm.d;
+      cj.dp = map->dm.dp;
+    }
+  }
+  if (map->mapped && map->feat_src && !layered) {  // every Gaussian may be listed: gather all features
+    launch_gather_features(map->feat_src, map->feat, n, map->dm.d, map->dm.dp, s);
+    ctx->launches++;
   }
   if (layered) {
     launch_depth_prepare(n, dc.near_plane, otemp, &t->vb, s);
@@ -1721,6 +1758,7 @@ LGS_API lgs_adam_config lgs_adam_config_default(void) {
 
 LGS_API lgs_status lgs_adam_create(lgs_ctx* ctx, const lgs_map* map, const lgs_adam_config* cfg, lgs_adam** out) {
   if (!ctx || !map || !out) return fail(LGS_EINVAL, "ctx/map/out is NULL");
+  if (map->mapped) return fail(LGS_EINVAL, "Adam needs a device map (this one is LGS_MEM_HOST_MAPPED)");
   *out = nullptr;
   const lgs_adam_config c = cfg ? *cfg : lgs_adam_config_default();
   if (!(c.beta1 >= 0.0 && c.beta1 < 1.0 && c.beta2 >= 0.0 && c.beta2 < 1.0 && c.eps > 0.0))
@@ -1761,6 +1799,7 @@ LGS_API int64_t lgs_adam_steps(const lgs_adam* adam) { return adam ? adam->step 
 
 LGS_API lgs_status lgs_adam_step(lgs_ctx* ctx, lgs_adam* a, lgs_map* map, const lgs_map_grads* grads) {
   if (!ctx || !a || !map || !grads) return fail(LGS_EINVAL, "ctx/adam/map/grads is NULL");
+  if (map->mapped) return fail(LGS_EINVAL, "Adam needs a device map (this one is LGS_MEM_HOST_MAPPED)");
   if (a->n != map->dm.n || a->d != map->dm.d || a->K != map->dm.K)
     return fail(LGS_EINVAL, "Adam state was created for a different map shape");
   if (grads->memory != LGS_MEM_DEVICE) return fail(LGS_EINVAL, "Adam step needs device gradients");
@@ -1789,6 +1828,7 @@ LGS_API lgs_status lgs_adam_step(lgs_ctx* ctx, lgs_adam* a, lgs_map* map, const 
 
 LGS_API lgs_status lgs_map_download(lgs_ctx* ctx, const lgs_map* map, lgs_gaussians* dst) {
   if (!ctx || !map || !dst) return fail(LGS_EINVAL, "ctx/map/dst is NULL");
+  if (map->mapped) return fail(LGS_EINVAL, "lgs_map_download: the map is LGS_MEM_HOST_MAPPED (its source is the host copy)");
   if (dst->n != map->dm.n || dst->feature_dim != map->dm.d || dst->sh_degree != map->dm.deg)
     return fail(LGS_EINVAL, "lgs_map_download: destination shape differs from the map");
   LGS_CUDA(cudaSetDevice(ctx->device));

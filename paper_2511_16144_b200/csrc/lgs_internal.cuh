@@ -228,9 +228,30 @@ struct ColorJob {
   float cc[3] = {0.f, 0.f, 0.f};
   int deg = 0;
   float4* color = nullptr;  // null: colours were written by K1
+  // host-mapped map (LGS_MEM_HOST_MAPPED): the listed Gaussian's features are gathered from the
+  // page-locked [d][N] source into the packed [N][dp] array (feat_src null: packed at upload)
+  const float* feat_src = nullptr;
+  float* feat_dst = nullptr;
+  int64_t n = 0;
+  int d = 0, dp = 0;
 };
 
+__device__ __forceinline__ void gather_features(const float* __restrict__ src, float* __restrict__ dst, int64_t n,
+                                                int d, int dp, int64_t g) {
+  float4* fo = reinterpret_cast<float4*>(dst + g * dp);
+  for (int c4 = 0; c4 < dp / 4; ++c4) {
+    float v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int c = c4 * 4 + k;
+      v[k] = c < d ? src[(int64_t)c * n + g] : 0.0f;
+    }
+    fo[c4] = make_float4(v[0], v[1], v[2], v[3]);
+  }
+}
+
 __device__ __forceinline__ void color_job_run(const ColorJob& j, uint32_t g) {
+  if (j.feat_src) gather_features(j.feat_src, j.feat_dst, j.n, j.d, j.dp, g);
   const float4 po = j.pos_opa[g];
   float4 col;
   switch (j.deg) {

@@ -84,6 +84,9 @@ void launch_pack_map(const float* pos, const float* rot, const float* log_s, con
 
 // color = false (depth-layered binning): colours are computed lazily (ColorJob) for the listed ones
 void launch_preprocess(const DevMap& m, const DevCam& c, const ViewBufs& v, bool color, cudaStream_t s);
+// [d][N] -> packed [N][dp] features of every Gaussian (a host-mapped map rendered without the
+// layered binning)
+void launch_gather_features(const float* src, float* dst, int64_t n, int d, int dp, cudaStream_t s);
 // colours of every visible Gaussian (debug exports of a layered render)
 void launch_colors(const DevMap& m, const DevCam& c, const ViewBufs& v, cudaStream_t s);
 

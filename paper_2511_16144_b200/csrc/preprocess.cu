@@ -26,16 +26,18 @@ __global__ void pack_map_kernel(const float* __restrict__ pos, const float* __re
   pos_opa[i] = make_float4(pos[i * 3 + 0], pos[i * 3 + 1], pos[i * 3 + 2], opac[i]);
   rot4[i] = make_float4(rot[i * 4 + 0], rot[i * 4 + 1], rot[i * 4 + 2], rot[i * 4 + 3]);
   scale4[i] = make_float4(log_s[i * 3 + 0], log_s[i * 3 + 1], log_s[i * 3 + 2], 0.0f);
-  float4* fo = reinterpret_cast<float4*>(feat_nd + i * dp);
-  for (int c4 = 0; c4 < dp / 4; ++c4) {
-    float v[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int c = c4 * 4 + k;
-      v[k] = c < d ? feat_dn[(int64_t)c * n + i] : 0.0f;
-    }
-    fo[c4] = make_float4(v[0], v[1], v[2], v[3]);
-  }
+  if (feat_dn) gather_features(feat_dn, feat_nd, n, d, dp, i);  // null: host-mapped, gathered lazily
+}
+
+__global__ void gather_features_kernel(const float* __restrict__ src, float* __restrict__ dst, int64_t n, int d,
+                                       int dp) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) gather_features(src, dst, n, d, dp, i);
+}
+
+void launch_gather_features(const float* src, float* dst, int64_t n, int d, int dp, cudaStream_t s) {
+  if (n == 0 || dp == 0) return;
+  gather_features_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(src, dst, n, d, dp);
 }
 
 void launch_pack_map(const float* pos, const float* rot, const float* log_s, const float* opac,

@@ -24,7 +24,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
-from ._lib import LGS_MEM_DEVICE, LGS_MEM_HOST, check
+from ._lib import LGS_MEM_DEVICE, LGS_MEM_HOST, LGS_MEM_HOST_MAPPED, check
 
 try:
     import torch
@@ -145,13 +145,16 @@ def default_context(device: int = 0) -> Context:
     return _default_ctx[device]
 
 
-def _gaussians_struct(scene):
+def _gaussians_struct(scene, host_mapped=False):
     arrs = {k: _f32(scene[k]) for k in ("pos", "rot", "log_s", "opac", "sh", "feat")}
     n = int(arrs["pos"].shape[0])
     d = int(arrs["feat"].shape[0]) if arrs["feat"].ndim == 2 else 0
     K = int(arrs["sh"].shape[1])
     deg = {1: 0, 4: 1, 9: 2, 16: 3}[K]
     mem = _mem(arrs["pos"])
+    if host_mapped:
+        assert mem == LGS_MEM_HOST, "host_mapped needs a host (page-locked) scene"
+        mem = LGS_MEM_HOST_MAPPED
     g = _lib.LgsGaussians(n, d, deg, _ptr(arrs["pos"]), _ptr(arrs["rot"]), _ptr(arrs["log_s"]), _ptr(arrs["opac"]),
                           _ptr(arrs["sh"]), _ptr(arrs["feat"]) if d else None, mem)
     return g, arrs
@@ -160,15 +163,20 @@ def _gaussians_struct(scene):
 class DeviceMap:
     """A Gaussian map resident in HBM in the kernels' packed layout (lgs_map)."""
 
-    def __init__(self, scene, ctx: Context | None = None):
+    def __init__(self, scene, ctx: Context | None = None, host_mapped: bool = False):
+        """``host_mapped``: the scene is page-locked host memory that the device reads in place
+        (LGS_MEM_HOST_MAPPED: SH rows and features of just the listed Gaussians cross PCIe); the
+        arrays must stay unchanged while this map and its renders are alive (they are referenced)."""
         self.ctx = ctx or default_context()
-        g, self._arrs = _gaussians_struct(scene)
+        self.host_mapped = host_mapped
+        g, self._arrs = _gaussians_struct(scene, host_mapped)
         self.n, self.d, self.sh_degree = g.n, g.feature_dim, g.sh_degree
         self.K = (self.sh_degree + 1) ** 2
         h = C.c_void_p()
         check(_lib.load().lgs_map_create(self.ctx.h, C.byref(g), C.byref(h)))
         self.h = h
-        self._arrs = None  # the library copied (host) or packed (device) the attributes
+        if not host_mapped:
+            self._arrs = None  # the library copied (host) or packed (device) the attributes
 
     def update(self, scene):
         g, keep = _gaussians_struct(scene)
@@ -264,8 +272,10 @@ def _alloc_like(device_side, shape, device):
 
 
 def render(map_, camera, cfg: RenderConfig | None = None, targets=None, ctx: Context | None = None,
-           out: dict | None = None) -> RenderOutput:
+           out: dict | None = None, host_mapped: bool = False) -> RenderOutput:
     """lego::render (renderer.hpp:55-56).  ``map_``: DeviceMap or scene dict (numpy / CUDA tensors).
+    ``host_mapped``: a host scene in page-locked memory is read in place where few rows are
+    needed (DeviceMap(host_mapped=True)) instead of being copied whole.
 
     ``targets`` (optional dict rgb/depth/feat) fuses the L1 loss of SURVEY.md §8d into the forward.
     Output images are CUDA tensors when the map is device-resident, numpy otherwise (or ``out``).
@@ -275,7 +285,7 @@ def render(map_, camera, cfg: RenderConfig | None = None, targets=None, ctx: Con
     host_scene = False
     if dmap is None:
         host_scene = _mem(map_["pos"]) == LGS_MEM_HOST
-        dmap = DeviceMap(map_, ctx)
+        dmap = DeviceMap(map_, ctx, host_mapped=host_mapped and host_scene)
     cam = make_camera(camera)
     H, W, d = cam.height, cam.width, dmap.d
     if out is None:
