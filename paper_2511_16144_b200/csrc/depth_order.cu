@@ -105,8 +105,10 @@ __device__ __forceinline__ bool bucket_selected(uint32_t b, int mode, uint32_t c
 __global__ void depth_scatter_kernel(const uint32_t* __restrict__ dkey, int64_t n, uint32_t base,
                                      const u64* __restrict__ off, const uint32_t* __restrict__ slot,
                                      const uint32_t* __restrict__ cut, int mode, uint2* __restrict__ tmp,
-                                     uint32_t* __restrict__ ra_out, uint32_t* __restrict__ culled_cursor) {
+                                     uint32_t* __restrict__ ra_out, uint32_t* __restrict__ culled_cursor,
+                                     const uint32_t* __restrict__ gate) {
   griddep_wait();
+  if (gate && *gate == 0u) return;  // second layered pass with no unfinished tile (eager path)
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i == 0 && ra_out) *ra_out = cnt_of(off[cut_end_of(cut)]);  // R_A: Gaussians in layer A
   if (i >= n) return;
@@ -141,6 +143,7 @@ struct DepthOut {
   uint8_t* active;       // or null: layer-A Gaussians flagged for the backward (lgs_kernels.h) ...
   float* gacc_zero;      // ... and, for the fused step, their accumulator rows (32 floats) zeroed
   ColorJob cj;           // lazy colours: computed here for the layer-A Gaussians (cj.color null: off)
+  const uint32_t* gate = nullptr;  // rest pass: nothing to do when *gate == 0 (no unfinished tile)
 };
 
 __device__ __forceinline__ void depth_emit(const DepthOut& o, const uint32_t* __restrict__ tiles,
@@ -166,6 +169,7 @@ __global__ void depth_rank_kernel(const uint2* __restrict__ tmp, int64_t n, uint
                                   const uint2* __restrict__ rect, const uint32_t* __restrict__ cut, int mode,
                                   DepthOut o, uint32_t* __restrict__ big_n, uint32_t* __restrict__ big_ids) {
   griddep_wait();
+  if (o.gate && *o.gate == 0u) return;
   const int64_t p0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const uint32_t ra = cut ? cnt_of(off[cut_end_of(cut)]) : 0u;  // Gaussians in layer A
   const int64_t p = mode == kDepthRest ? p0 + ra : p0;
@@ -325,7 +329,8 @@ void launch_depth_order(const ViewBufs& v, int64_t n, float near_plane, void* te
   depth_front(v, n, c, s);
   const unsigned grid = (unsigned)((n + 255) / 256);
   const DepthOut o{idx_sorted, cnt_sorted, nullptr, nullptr, nullptr};
-  depth_scatter_kernel<<<grid, 256, 0, s>>>(v.dkey, n, c.base, c.off, c.slot, nullptr, kDepthAll, c.tmp, nullptr, nullptr);
+  depth_scatter_kernel<<<grid, 256, 0, s>>>(v.dkey, n, c.base, c.off, c.slot, nullptr, kDepthAll, c.tmp, nullptr, nullptr,
+                                            nullptr);
   depth_rank_kernel<<<grid, 256, 0, s>>>(c.tmp, n, c.base, c.off, v.tiles, v.rect, nullptr, kDepthAll, o,
                                          c.sc + kScBigA, c.big_a);
   depth_big_kernel<<<8, 1024, 0, s>>>(c.tmp, c.off, v.tiles, v.rect, nullptr, c.sc + kScBigA, c.big_a, c.scratch,
@@ -372,7 +377,8 @@ void launch_depth_order_layer_a(const ViewBufs& v, int64_t n, float near_plane, 
   const int64_t ga = std::min<int64_t>(n, gauss_cap);
   const uint32_t* cut = c.sc + kScCut;
   launch_pdl(depth_scatter_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, s, (const uint32_t*)v.dkey, n,
-             c.base, (const u64*)c.off, (const uint32_t*)c.slot, cut, (int)kDepthLayerA, c.tmp, ra, (uint32_t*)nullptr);
+             c.base, (const u64*)c.off, (const uint32_t*)c.slot, cut, (int)kDepthLayerA, c.tmp, ra, (uint32_t*)nullptr,
+             (const uint32_t*)nullptr);
   launch_pdl(depth_rank_kernel, dim3((unsigned)((ga + 255) / 256)), dim3(256), 0, s, (const uint2*)c.tmp, n, c.base,
              (const u64*)c.off, (const uint32_t*)v.tiles, (const uint2*)v.rect, cut, (int)kDepthLayerA, o,
              c.sc + kScBigA, c.big_a);
@@ -480,16 +486,17 @@ void launch_layer_tile_lists(const uint2* cand_rect, const uint32_t* cand_idx, c
 }
 
 void launch_depth_order_rest(const ViewBufs& v, int64_t n, float near_plane, void* temp, uint32_t* idx_sorted,
-                             cudaStream_t s) {
+                             const uint32_t* gate, cudaStream_t s) {
   if (n == 0) return;
   const DepthCarve c = carve(temp, n, near_plane);
   const unsigned grid = (unsigned)((n + 255) / 256);
-  const DepthOut o{idx_sorted, nullptr, nullptr, nullptr, nullptr};
+  DepthOut o{idx_sorted, nullptr, nullptr, nullptr, nullptr};
+  o.gate = gate;
   // the rest's big-bucket count, bitonic scratch allocator (layer A's sorts are done) and culled slots
   cudaMemsetAsync(c.sc + kScBigR, 0, sizeof(uint32_t) * 3, s);
   const uint32_t* cut = c.sc + kScCut;
   depth_scatter_kernel<<<grid, 256, 0, s>>>(v.dkey, n, c.base, c.off, c.slot, cut, kDepthRest, c.tmp, nullptr,
-                                            c.sc + kScCulled);
+                                            c.sc + kScCulled, gate);
   depth_rank_kernel<<<grid, 256, 0, s>>>(c.tmp, n, c.base, c.off, v.tiles, v.rect, cut, kDepthRest, o,
                                          c.sc + kScBigR, c.big_r);
   depth_big_kernel<<<8, 1024, 0, s>>>(c.tmp, c.off, v.tiles, v.rect, cut, c.sc + kScBigR, c.big_r, c.scratch,

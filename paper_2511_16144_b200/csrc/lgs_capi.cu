@@ -899,7 +899,7 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
         {
           PhaseScope ph(ctx, PH_TILE_SORT);
           launch_layer_prep(unfinished, t->ranges, dc.tiles_x, dc.tiles_y, sat, order2, s2);
-          launch_depth_order_rest(t->vb, n, dc.near_plane, otemp, idx_sorted, s2);
+          launch_depth_order_rest(t->vb, n, dc.near_plane, otemp, idx_sorted, count2, s2);
           launch_layer_count(t->vb, idx_sorted, n, dc.tiles_x, sat, count2, dkey_sorted, count2 + 1, s2,
                              fuse ? t->gacc : nullptr, cj);
           launch_scan_counts(dkey_sorted, n, incl, temp, temp_bytes, s2);

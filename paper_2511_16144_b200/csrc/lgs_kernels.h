@@ -117,8 +117,9 @@ void launch_depth_order_layer_a(const ViewBufs& v, int64_t n, float near_plane, 
                                 uint32_t min_pairs, int64_t gauss_cap, uint32_t cap_a, uint32_t* idx_sorted,
                                 uint2* cand_rect, uint32_t* ra, uint8_t* active, float* gacc_zero, bool rerun,
                                 const ColorJob& cj, cudaStream_t s);
+// gate (device, may be null): the kernels return at once when *gate == 0 (no unfinished tile)
 void launch_depth_order_rest(const ViewBufs& v, int64_t n, float near_plane, void* temp, uint32_t* idx_sorted,
-                             cudaStream_t s);
+                             const uint32_t* gate, cudaStream_t s);
 // Layer-A tile lists (one warp per tile scanning the depth-ordered candidates, order-preserving
 // compaction): vals[ranges[t]] for every tile; *cursor (zeroed by the caller) allocates list space.
 void launch_layer_tile_lists(const uint2* cand_rect, const uint32_t* cand_idx, const uint32_t* n_cand, int tiles_x,
