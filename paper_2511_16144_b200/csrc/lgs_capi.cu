@@ -730,12 +730,9 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
   }
   ctx->launches += layered ? 3 : 2;
   // side branch of a plan: the gradient buffers' zero rows stream out beside the forward (the
-  // backward's chain then writes only the active rows).  Forked after K1 or, by default, right
-  // before the first blend, which is issue-bound and leaves HBM to the stores.
-  static const bool prezero_at_k1 = [] {
-    const char* e = getenv("LGS_PREZERO_AT");
-    return e && strcmp(e, "k1") == 0;
-  }();
+  // backward's chain then writes only the active rows).  Forked right before the first blend,
+  // which is issue-bound and leaves HBM to the stores (forking after K1 instead, beside the
+  // latency-bound depth order, measured 10-15 us slower per replay).
   auto fork_prezero = [&]() -> lgs_status {
     if (!(layered && ctx->capturing && ctx->prezero && !ctx->prezero_forked && n > 0)) return LGS_OK;
     LGS_CUDA(cudaEventRecord(ctx->side_fork, s));
@@ -750,7 +747,6 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
     ctx->launches++;
     return LGS_OK;
   };
-  if (prezero_at_k1) TRYB(fork_prezero());
   if (n > 0) {
     CUDAB(cudaMemcpyAsync(ctx->host_u32, dev_pairs, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
     if (!ctx->capturing) CUDAB(cudaEventRecord(ctx->pairs_ready, s));
