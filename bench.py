@@ -218,6 +218,19 @@ def traffic_for(phase):
     return int(ent["dram_bytes_per_launch"]) if ent else None
 
 
+def measure_fp32_peak(device):
+    """FFMA throughput of this device (TFLOP/s) from the bench-only microbenchmark library
+    (paper_2511_16144_b200/bench_csrc, built by build.py; not part of liblgs.so)."""
+    import ctypes as C
+    lib = C.CDLL(os.path.join(ROOT, "paper_2511_16144_b200", "libbench_peak.so"))
+    lib.bench_measure_fp32_peak.restype = C.c_int
+    lib.bench_measure_fp32_peak.argtypes = [C.c_int, C.POINTER(C.c_double)]
+    v = C.c_double()
+    if lib.bench_measure_fp32_peak(device, C.byref(v)) != 0:
+        raise RuntimeError("FP32 peak microbenchmark failed")
+    return v.value
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -352,10 +365,7 @@ def run_ours(args):
         pass
     hbm_peak = float(peak.get("hbm_gbs", 6650.0))
     hbm_src = "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peak else "B200_PROFILING.md fallback"
-    import ctypes as C
-    v = C.c_double()
-    _lib.check(_lib.load().lgs_measure_fp32_peak(local, C.byref(v)))
-    fp32 = v.value
+    fp32 = measure_fp32_peak(local)
 
     # algorithmic work per launch
     npix = cam["width"] * cam["height"]
@@ -410,7 +420,7 @@ def run_ours(args):
         "bound": dr["bound"],
         "achieved": dr["achieved"],
         "peak": round(hbm_peak if dr["bound"] == "hbm" else fp32, 2),
-        "peak_source": hbm_src if dr["bound"] == "hbm" else "lgs_measure_fp32_peak (FFMA microbenchmark, this box)",
+        "peak_source": hbm_src if dr["bound"] == "hbm" else "bench_measure_fp32_peak (FFMA microbenchmark, this box; libbench_peak.so)",
         "unit": dr["unit"],
         "frac": dr["frac"],
         "traffic": traffic_for(dom),

@@ -165,6 +165,15 @@ LGS_API lgs_status lgs_ctx_destroy(lgs_ctx* ctx);
  * renderer.cpp:140), completed for tiles that do not saturate; images and gradients are identical.
  * 1: every (tile, Gaussian) pair is listed (parity checks of the complete sorted lists). */
 LGS_API lgs_status lgs_ctx_set_full_tile_lists(lgs_ctx* ctx, int32_t full);
+/* Context options (the library reads no environment variables):
+ *   LGS_OPT_FULL_TILE_LISTS    same as lgs_ctx_set_full_tile_lists;
+ *   LGS_OPT_RADIX_DEPTH_ORDER  1: the depth order by a device radix sort over (depth, index) keys
+ *                              with complete lists (cross-check of the bucketed order; same result);
+ *   LGS_OPT_FUSED_EAGER        1: an uncaptured render with L1 targets runs the fused forward+backward
+ *                              kernel of lgs_plan (for profilers that cannot see inside a graph); its
+ *                              tape accepts only lgs_render_backward_l1 / _loss (else LGS_EINVAL). */
+enum { LGS_OPT_FULL_TILE_LISTS = 0, LGS_OPT_RADIX_DEPTH_ORDER = 1, LGS_OPT_FUSED_EAGER = 2 };
+LGS_API lgs_status lgs_ctx_set_option(lgs_ctx* ctx, int32_t option, int64_t value);
 LGS_API lgs_status lgs_ctx_set_stream(lgs_ctx* ctx, void* stream);
 LGS_API lgs_status lgs_ctx_synchronize(lgs_ctx* ctx);
 
@@ -255,17 +264,6 @@ LGS_API lgs_status lgs_ctx_phase_times(lgs_ctx* ctx, double* ms, int64_t* counts
  * that contributed (the reference's pixel_contribs entries, renderer.cpp:157).  Synchronizes.
  * Counted only by forwards run while the context profiles (lgs_ctx_profile); else LGS_EINVAL. */
 LGS_API lgs_status lgs_saved_work(const lgs_saved* tape, int64_t* evaluated, int64_t* contributed);
-
-/* Measured FP32 FFMA throughput of `device` (TFLOP/s): the roofline denominator of the blend
- * kernels.  Runs a ~10 ms microbenchmark on the legacy stream; call outside timed regions. */
-LGS_API lgs_status lgs_measure_fp32_peak(int32_t device, double* tflops);
-/* Measured legacy tensor-core (mma.sync m16n8k8 TF32, fp32 accumulate) throughput, TFLOP/s. */
-LGS_API lgs_status lgs_measure_mma_tf32_peak(int32_t device, double* tflops);
-
-/* Self-test of the warp-level TF32 tensor-core fragment layouts used by the backward blend:
- * d = a (16x8, row-major) * b (8x8, row-major), host buffers; split = 1 uses the 3xTF32 split. */
-LGS_API lgs_status lgs_debug_mma_selftest(int32_t device, const float* a16x8, const float* b8x8, float* d16x8,
-                                          int32_t split);
 
 /* ---- mapping losses (SPEC.md:418-426 compute_losses) ------------------
  * l_rgb = w_l1 L1(rgb, kf.rgb) + (1 - w_l1)(1 - SSIM)/2 (11x11 Gaussian window, sigma 1.5, C1 =

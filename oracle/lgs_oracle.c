@@ -118,6 +118,14 @@ typedef struct {
   double rcw[9], tcw[3], cc[3];
   int64_t evaluated; /* (pixel, gaussian) pairs that reached the alpha test */
   int64_t contributions;
+  /* EXT (injected records only): fp32 decision twin.  pix_flag [H*W]: bit 0 an alpha-skip
+   * decision (renderer.cpp:147), bit 1 a transmittance decision (:140), bit 2 a backward clamp
+   * decision (:274) differs between fp64 and the kernel's fp32 arithmetic, or the fp32 value lies
+   * within its rounding band of the threshold.  g_flag [N] (map index): bit 0 the Gaussian took
+   * part in such a decision, bit 1 it contributes at a pixel with bit 0|1 set (its gradient sees
+   * the flipped compositing chain), bit 2 its clamp decision was marginal at some pixel. */
+  uint8_t* pix_flag;
+  uint8_t* g_flag;
 } orc_render;
 
 /* ------------------------------------------------------------------------ */
@@ -330,6 +338,33 @@ static void list_push(orc_list* l, int32_t v) {
   l->idx[l->n++] = v;
 }
 
+/* EXT fp32 decision twin: the kernels' per-(tile, entry) conic frame (blend_common.cuh
+ * stage_frame), the same IEEE fp64 operations in the same order (-ffp-contract=off), rounded to
+ * fp32: out = S0, T0, ux, uy, wx, wy, dxc, dyc. */
+static void twin_frame(float u, float v, float A, float B, float C, float xc, float yc, float out[8]) {
+  const double a = A, b = B, c = C, k = 0.72134752044448170368;
+  const double h = 0.5 * (a - c);
+  const double r = sqrt(fma(h, h, b * b));
+  const double l1 = 0.5 * (a + c) + r;
+  double l2 = fma(a, c, -(b * b)) / l1;
+  if (!(l2 > 0.0)) l2 = 0.0;
+  double ex, ey;
+  if (h >= 0.0) { ex = h + r; ey = b; } else { ex = b; ey = r - h; }
+  const double nrm = sqrt(fma(ex, ex, ey * ey));
+  double cx = 1.0, cy = 0.0;
+  if (nrm > 0.0) { cx = ex / nrm; cy = ey / nrm; }
+  const double a1 = sqrt(k * l1), a2 = sqrt(k * l2);
+  const double dxc = (double)xc - (double)u, dyc = (double)yc - (double)v;
+  out[0] = (float)(a1 * fma(cx, dxc, cy * dyc));
+  out[1] = (float)(a2 * fma(cx, dyc, -(cy * dxc)));
+  out[2] = (float)(a1 * cx);
+  out[3] = (float)(a1 * cy);
+  out[4] = (float)(-(a2 * cy));
+  out[5] = (float)(a2 * cx);
+  out[6] = (float)dxc;
+  out[7] = (float)dyc;
+}
+
 /* ------------------------------------------------------------------------ */
 /* (A) render -- renderer.cpp:94-167                                          */
 /* rgb [H][W][3], depth [H][W], feat [H][W][d], acc [H][W] (HWC, image.hpp).  */
@@ -390,6 +425,17 @@ ORC_API orc_render* orc_render_forward(const orc_map* m, const orc_camera* cam, 
 
   const int wx0 = R->win[0], wy0 = R->win[1], wx1 = R->win[2] - 1, wy1 = R->win[3] - 1;
   int64_t evaluated = 0, contributions = 0;
+  /* EXT fp32 decision twin (see orc_render.pix_flag): the kernel's per-pair arithmetic
+   * (blend_common.cuh splat_alpha: conic pre-scaled by -log2(e)/2, _rn products, exp2) */
+  float* t32 = NULL;
+  const float skip_f = (float)cfg->alpha_skip, tmin_f = (float)cfg->transmittance_min;
+  const float clamp_f = (float)cfg->alpha_clamp;
+  if (inj) {
+    t32 = (float*)malloc(sizeof(float) * npix);
+    for (size_t i = 0; i < npix; ++i) t32[i] = 1.0f;
+    R->pix_flag = (uint8_t*)calloc(npix, 1);
+    R->g_flag = (uint8_t*)calloc((size_t)(m->n > 0 ? m->n : 1), 1);
+  }
   for (int64_t gi = 0; gi < np; ++gi) { /* :125-161 */
     const orc_proj* g = &R->proj[gi];
     const double opacity = g->opacity;
@@ -398,10 +444,56 @@ ORC_API orc_render* orc_render_forward(const orc_map* m, const orc_camera* cam, 
     const int x0 = g->x0 > wx0 ? g->x0 : wx0, x1 = g->x1 < wx1 ? g->x1 : wx1;
     const int y0 = g->y0 > wy0 ? g->y0 : wy0, y1 = g->y1 < wy1 ? g->y1 : wy1;
     const double cs = g->conic[1] + g->conic[2];
+    int frame_tile = -1; /* EXT fp32 twin: conic frame of the current tile */
+    float frame[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     for (int y = y0; y <= y1; ++y) {
       for (int x = x0; x <= x1; ++x) {
         const size_t pix = (size_t)y * W + x;
         double* t_pix = &trans[pix];
+        float a32 = 0.0f;
+        int skip32 = 1;
+        if (t32) { /* EXT fp32 twin of the decisions at this pair */
+          const int tskip32 = t32[pix] < tmin_f;
+          if (tskip32 != (*t_pix < cfg->transmittance_min)) {
+            R->pix_flag[pix] |= 2;
+            R->g_flag[mi] |= 1;
+          }
+          if (!tskip32) {
+            /* the kernels' conic frame of this (tile, Gaussian), blend_common.cuh stage_frame */
+            const int tid_ = (y / 16) * 65536 + (x / 16);
+            if (tid_ != frame_tile) {
+              frame_tile = tid_;
+              twin_frame((float)g->u, (float)g->v, (float)g->conic[0], (float)g->conic[1], (float)g->conic[3],
+                         (float)((x / 16) * 16) + 7.5f, (float)((y / 16) * 16) + 7.5f, frame);
+            }
+            const float fex = (float)(x % 16) - 7.5f, fey = (float)(y % 16) - 7.5f;
+            const float S = fmaf(frame[2], fex, fmaf(frame[3], fey, frame[0]));
+            const float Tt = fmaf(frame[4], fex, fmaf(frame[5], fey, frame[1]));
+            const float p = -fmaf(S, S, Tt * Tt);
+            a32 = (float)opacity * exp2f(p);
+            skip32 = !(a32 >= skip_f);
+            const double qq = g->conic[0] * (x - g->u) * (x - g->u) + cs * (x - g->u) * (y - g->v) +
+                              g->conic[3] * (y - g->v) * (y - g->v);
+            const double a64 = opacity * exp(-0.5 * qq);
+            if (*t_pix >= cfg->transmittance_min &&
+                (skip32 != !(a64 >= cfg->alpha_skip) || fabsf(a32 - skip_f) <= 4e-6f * skip_f)) {
+              R->pix_flag[pix] |= 1;
+              R->g_flag[mi] |= 1;
+            }
+            if (!skip32) {
+              const double g64 = exp(-0.5 * qq);
+              if (((opacity * g64 > cfg->alpha_clamp) != (a32 > clamp_f)) || fabsf(a32 - clamp_f) <= 4e-6f * clamp_f) {
+                R->pix_flag[pix] |= 4;
+                R->g_flag[mi] |= 4;
+              }
+              t32[pix] = t32[pix] * (1.0f - fminf(a32, clamp_f));
+              if (fabsf(t32[pix] - tmin_f) <= 2e-5f * tmin_f) {
+                R->pix_flag[pix] |= 2;
+                R->g_flag[mi] |= 1;
+              }
+            }
+          }
+        }
         if (*t_pix < cfg->transmittance_min) continue; /* :140 */
         ++evaluated;
         const double dx = x - g->u, dy = y - g->v;
@@ -424,6 +516,14 @@ ORC_API orc_render* orc_render_forward(const orc_map* m, const orc_camera* cam, 
   }
   for (size_t pix = 0; pix < npix; ++pix) /* :163-165 */
     depth[pix] = draw[pix] / fmax(acc[pix], 1e-6);
+  if (t32) { /* EXT: every contributor of a pixel whose compositing chain may differ */
+    for (size_t pix = 0; pix < npix; ++pix) {
+      if (!(R->pix_flag[pix] & 3)) continue;
+      const orc_list* cl = &R->contrib[pix];
+      for (int32_t ci = 0; ci < cl->n; ++ci) R->g_flag[R->proj[cl->idx[ci]].index] |= 2;
+    }
+    free(t32);
+  }
   free(trans);
   free(draw);
   R->evaluated = evaluated;
@@ -441,6 +541,15 @@ ORC_API void orc_render_contrib_counts(const orc_render* R, int32_t* out) {
   for (size_t i = 0; i < npix; ++i) out[i] = R->contrib[i].n;
 }
 
+/* EXT: fp32 decision-twin flags (injected renders only; returns 0 when absent) */
+ORC_API int orc_render_flags(const orc_render* R, uint8_t* pix_flag, uint8_t* g_flag) {
+  if (!R->pix_flag) return 0;
+  const size_t npix = (size_t)R->cam.width * R->cam.height;
+  if (pix_flag) memcpy(pix_flag, R->pix_flag, npix);
+  if (g_flag) memcpy(g_flag, R->g_flag, (size_t)R->map.n);
+  return 1;
+}
+
 /* sorted projected map indices */
 ORC_API void orc_render_sorted_indices(const orc_render* R, int64_t* out) {
   for (int64_t i = 0; i < R->np; ++i) out[i] = R->proj[i].index;
@@ -452,6 +561,8 @@ ORC_API void orc_render_free(orc_render* R) {
   for (size_t i = 0; i < npix; ++i) free(R->contrib[i].idx);
   free(R->contrib);
   free(R->proj);
+  free(R->pix_flag);
+  free(R->g_flag);
   free(R);
 }
 

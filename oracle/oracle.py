@@ -84,6 +84,8 @@ def lib():
             getattr(L, f).restype = C.c_int64
             getattr(L, f).argtypes = [C.c_void_p]
         L.orc_render_contrib_counts.argtypes = [C.c_void_p, _i32p]
+        L.orc_render_flags.restype = C.c_int
+        L.orc_render_flags.argtypes = [C.c_void_p, _u8p, _u8p]
         L.orc_render_sorted_indices.argtypes = [C.c_void_p, C.POINTER(C.c_int64)]
         L.orc_project_gaussian.restype = C.c_int
         L.orc_project_gaussian.argtypes = [C.POINTER(OrcMap), C.c_int64, C.POINTER(OrcCamera),
@@ -190,6 +192,15 @@ class Render:
         out = np.zeros(self.depth.shape[:2], np.int32)
         lib().orc_render_contrib_counts(self._h, _ptr(out, _i32p))
         return out
+
+    def flags(self):
+        """fp32 decision-twin flags of an injected render (lgs_oracle.c orc_render.pix_flag):
+        (pixel flags [H,W] uint8, Gaussian flags [N] uint8), or None without injection."""
+        pf = np.zeros(self.depth.shape[:2], np.uint8)
+        gf = np.zeros(max(self.n, 1), np.uint8)
+        if not lib().orc_render_flags(self._h, _ptr(pf, _u8p), _ptr(gf, _u8p)):
+            return None
+        return pf, gf[:self.n]
 
     def sorted_indices(self):
         out = np.zeros(self.num_projected, np.int64)

@@ -13,6 +13,7 @@ LIB_PATH = os.path.join(HERE, "liblgs.so")
 
 LGS_OK, LGS_EINVAL, LGS_ECUDA, LGS_ENOMEM, LGS_ENODEV, LGS_EIO = range(6)
 LGS_MEM_HOST, LGS_MEM_DEVICE, LGS_MEM_HOST_MAPPED = 0, 1, 2
+LGS_OPT_FULL_TILE_LISTS, LGS_OPT_RADIX_DEPTH_ORDER, LGS_OPT_FUSED_EAGER = 0, 1, 2
 
 _fp = C.POINTER(C.c_float)
 
@@ -93,6 +94,7 @@ SIGNATURES = [
     ("lgs_render_config_default", LgsRenderConfig, []),
     ("lgs_ctx_create", C.c_int, [C.c_int32, C.c_void_p, C.POINTER(C.c_void_p)]),
     ("lgs_ctx_set_full_tile_lists", C.c_int, [C.c_void_p, C.c_int32]),
+    ("lgs_ctx_set_option", C.c_int, [C.c_void_p, C.c_int32, C.c_int64]),
     ("lgs_ctx_destroy", C.c_int, [C.c_void_p]),
     ("lgs_ctx_set_stream", C.c_int, [C.c_void_p, C.c_void_p]),
     ("lgs_ctx_synchronize", C.c_int, [C.c_void_p]),
@@ -118,9 +120,6 @@ SIGNATURES = [
     ("lgs_ctx_profile", C.c_int, [C.c_void_p, C.c_int32]),
     ("lgs_ctx_phase_times", C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int64), C.c_int32]),
     ("lgs_saved_work", C.c_int, [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
-    ("lgs_measure_fp32_peak", C.c_int, [C.c_int32, C.POINTER(C.c_double)]),
-    ("lgs_measure_mma_tf32_peak", C.c_int, [C.c_int32, C.POINTER(C.c_double)]),
-    ("lgs_debug_mma_selftest", C.c_int, [C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32]),
     ("lgs_loss_weights_default", LgsLossWeights, []),
     ("lgs_mapping_loss", C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(LgsImages), C.POINTER(LgsKeyframe),
                                    C.POINTER(LgsDecoder), C.POINTER(LgsLossWeights), C.POINTER(LgsLossBreakdown)]),

@@ -18,6 +18,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "liblgs.so")
+# bench-only helpers (FP32 peak microbenchmark): a separate library, never linked into liblgs.so
+BENCH_CSRC = os.path.join(HERE, "bench_csrc")
+BENCH_LIB = os.path.join(HERE, "libbench_peak.so")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -63,6 +66,14 @@ def build(verbose: bool = False, force: bool = False) -> str:
         list(pool.map(run, cmds))
     if force or not os.path.exists(LIB) or any(os.path.getmtime(o) > os.path.getmtime(LIB) for o in objs):
         cmd = [nvcc, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.run(cmd, check=True)
+    bench_srcs = sorted(os.path.join(BENCH_CSRC, f) for f in os.listdir(BENCH_CSRC) if f.endswith(".cu"))
+    if force or not os.path.exists(BENCH_LIB) or any(os.path.getmtime(f) > os.path.getmtime(BENCH_LIB)
+                                                      for f in bench_srcs):
+        cmd = [nvcc, *ARCH, "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-shared", "-cudart", "static", "-o", BENCH_LIB,
+               *bench_srcs]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)

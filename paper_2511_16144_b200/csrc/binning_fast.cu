@@ -28,6 +28,7 @@
 
 #include "lgs_internal.cuh"
 #include "lgs_kernels.h"
+#include "dev_cache.h"
 
 namespace lgs {
 
@@ -316,15 +317,13 @@ void launch_fast_binning(const ViewBufs& v, const uint32_t* idx_sorted, int64_t 
   void* temp = chunk_first + nchunks * kWarps + 1;
   size_t temp_bytes = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, temp_bytes, counts, offs, (int)cells);
-  static bool attr_set = false;
-  if (!attr_set) {
+  {
     const int cnt_smem = (int)(sizeof(uint32_t) * kMaxFastTiles);
     const int sct_smem = (int)(sizeof(uint32_t) * kMaxFastTiles + sizeof(uint16_t) * kMaxFastTiles * kWarps);
-    cudaFuncSetAttribute(tile_count_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, cnt_smem);
-    cudaFuncSetAttribute(tile_count_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, cnt_smem);
-    cudaFuncSetAttribute(tile_scatter_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sct_smem);
-    cudaFuncSetAttribute(tile_scatter_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sct_smem);
-    attr_set = true;
+    ensure_dyn_smem(reinterpret_cast<const void*>(tile_count_kernel<false>), cnt_smem);
+    ensure_dyn_smem(reinterpret_cast<const void*>(tile_count_kernel<true>), cnt_smem);
+    ensure_dyn_smem(reinterpret_cast<const void*>(tile_scatter_kernel<false>), sct_smem);
+    ensure_dyn_smem(reinterpret_cast<const void*>(tile_scatter_kernel<true>), sct_smem);
   }
   const int nslices = nchunks * kWarps;
   const uint32_t cpw = cost_per_warp(bp.cap, bp.gauss_cap);
@@ -444,12 +443,7 @@ __global__ void __launch_bounds__(1024) layer_prep_kernel(const uint32_t* __rest
 void launch_layer_prep(const uint32_t* unfinished, const uint2* ranges, int tiles_x, int tiles_y, uint32_t* sat,
                        uint32_t* order2, cudaStream_t s) {
   const size_t smem = sizeof(uint32_t) * (size_t)(tiles_x + 1) * (tiles_y + 1);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(layer_prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(sizeof(uint32_t) * 9 * 1024 * 4));
-    attr_set = true;
-  }
+  ensure_dyn_smem(reinterpret_cast<const void*>(layer_prep_kernel), (int)(sizeof(uint32_t) * 9 * 1024 * 4));
   layer_prep_kernel<<<1, 1024, smem, s>>>(unfinished, ranges, tiles_x, tiles_y, sat, order2);
 }
 

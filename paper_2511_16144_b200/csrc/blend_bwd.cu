@@ -23,6 +23,7 @@
 #include <cstdlib>
 
 #include "blend_common.cuh"
+#include "dev_cache.h"
 
 namespace lgs {
 
@@ -49,8 +50,8 @@ constexpr int bwd_batch() { return DP > 16 ? 64 : 128; }
 template <int DP>
 struct BwdSmem {
   float4 r0[bwd_batch<DP>()];  // u, v, depth, opacity
-  float4 r1[bwd_batch<DP>()];  // A, B, C, -
-  float4 sc[bwd_batch<DP>()];  // scaled conic a, b2, c, -
+  float4 fa[bwd_batch<DP>()];  // conic frame S0, T0, ux, uy (blend_common.cuh stage_frame)
+  float4 fb[bwd_batch<DP>()];  // conic frame wx, wy, dxc, dyc
   uint2 rect[bwd_batch<DP>()];
   float4 col[bwd_batch<DP>()];
   uint32_t gid[bwd_batch<DP>()];
@@ -77,7 +78,12 @@ __global__ void __launch_bounds__(kBlock / PPT) blend_bwd_kernel(DevMap m, DevCa
     const int tx = tile % c.tiles_x, ty = tile / c.tiles_x;
     const int px = tx * kTile + lx;
     const int py0 = ty * kTile + ly0;
-    const float fpx = (float)px;
+    // pixel offsets from the tile centre (the conic frames' origin)
+    const float xc = (float)(tx * kTile) + 7.5f, yc = (float)(ty * kTile) + 7.5f;
+    const float ex = (float)lx - 7.5f;
+    float ey[PPT];
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) ey[k] = (float)(ly0 + k) - 7.5f;
     const uint2 range = tl.ranges[tile];
 
     float T[PPT], accum[PPT], g_rgb[PPT][3], g_draw[PPT], g_acc[PPT];
@@ -146,11 +152,12 @@ __global__ void __launch_bounds__(kBlock / PPT) blend_bwd_kernel(DevMap m, DevCa
       for (int e = tid; e < cnt; e += NT) {
         const uint32_t g = __ldg(tl.vals + bstart + e);
         sm.gid[e] = g;
-        sm.r0[e] = __ldg(v.rec0 + g);
+        const float4 r0 = __ldg(v.rec0 + g);
+        sm.r0[e] = r0;
         const float4 r1 = __ldg(v.rec1 + g);
-        sm.r1[e] = r1;
-        const ScaledConic s = scale_conic(r1.x, r1.y, r1.z);
-        sm.sc[e] = make_float4(s.a, s.b2, s.c, 0.f);
+        const ConicFrame f = stage_frame(r0.x, r0.y, r1.x, r1.y, r1.z, xc, yc);
+        sm.fa[e] = f.a;
+        sm.fb[e] = f.b;
         sm.rect[e] = __ldg(v.rect + g);
         sm.col[e] = __ldg(v.color + g);
         if (DP > 0) {
@@ -170,17 +177,18 @@ __global__ void __launch_bounds__(kBlock / PPT) blend_bwd_kernel(DevMap m, DevCa
         if (!__any_sync(0xffffffffu, col_in)) continue;  // no pixel of this warp inside the Gaussian's rect
         // phase 1: alphas of this thread's pixels (cheap); most rect hits fail the alpha test
         const float4 r0 = sm.r0[e];
-        const float4 s4 = sm.sc[e];
-        const ScaledConic sc{s4.x, s4.y, s4.z};
+        const float4 fa = sm.fa[e], fb = sm.fb[e];
         // Branch-free over the PPT pixels: independent chains the scheduler can interleave.  A
         // pixel that does not contribute gets alpha = 0 (T / accum / colour / feature terms add
         // exactly +0) and a zero dL/dalpha mask for the opacity, mean and conic terms.
-        float alphas[PPT], Gs[PPT], dxs[PPT], dys[PPT];
+        float alphas[PPT], Gs[PPT], Ss[PPT], Ts[PPT];
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) alphas[k] = frame_alpha(fa, fb, r0.w, ex, ey[k], Ss[k], Ts[k], Gs[k]);
         bool any = false;
 #pragma unroll
         for (int k = 0; k < PPT; ++k) {
           const int py = py0 + k;
-          const float al = splat_alpha(r0.x, r0.y, sc, r0.w, fpx, (float)py, dxs[k], dys[k], Gs[k]);
+          const float al = alphas[k];
           const bool ok = col_in && jrel < last[k] && py >= ry0 && py <= ry1 && al >= c.alpha_skip;
           alphas[k] = ok ? al : 0.f;
           any = any || ok;
@@ -190,11 +198,9 @@ __global__ void __launch_bounds__(kBlock / PPT) blend_bwd_kernel(DevMap m, DevCa
         float vals[SLOTS];
 #pragma unroll
         for (int q = 0; q < SLOTS; ++q) vals[q] = 0.f;
-        const float4 r1 = sm.r1[e];
         const float4 col = sm.col[e];
         const float o = r0.w;
         const float do_dlogit = o * (1.0f - o);
-        const float twoA = 2.0f * r1.x, twoB = 2.0f * r1.y, twoC = 2.0f * r1.z;
         float w[PPT], dldw[PPT], inv1ma[PPT];
 #pragma unroll
         for (int k = 0; k < PPT; ++k) {
@@ -230,7 +236,10 @@ __global__ void __launch_bounds__(kBlock / PPT) blend_bwd_kernel(DevMap m, DevCa
 #pragma unroll
         for (int k = 0; k < PPT; ++k) {
           const float alpha = alphas[k];
-          const float dx = dxs[k], dy = dys[k], G = Gs[k];
+          const float G = Gs[k];
+          const float dx = fb.z + ex, dy = fb.w + ey[k];  // pixel - mean (renderer.cpp:141-142)
+          float dq_ddx, dq_ddy;
+          frame_dq(fa, fb, Ss[k], Ts[k], dq_ddx, dq_ddy);
           // the clamped contributor (and a non-contributing pixel) gets no opacity/mean/conic grad
           const float dl_da = (alpha != 0.f && !(alpha > c.alpha_clamp)) ? T[k] * dldw[k] - accum[k] * inv1ma[k] : 0.f;
           accum[k] = fmaf(dldw[k], w[k], accum[k]);
@@ -240,8 +249,6 @@ __global__ void __launch_bounds__(kBlock / PPT) blend_bwd_kernel(DevMap m, DevCa
           vals[kSlotZ] = fmaf(g_draw[k], w[k], vals[kSlotZ]);
           vals[kSlotOpac] = fmaf(dl_da * G, do_dlogit, vals[kSlotOpac]);
           const float cf = dl_da * o * (-0.5f * G);  // dl_dg * dg_dq
-          const float dq_ddx = fmaf(twoA, dx, twoB * dy);
-          const float dq_ddy = fmaf(twoC, dy, twoB * dx);
           vals[kSlotMuX] = fmaf(-cf, dq_ddx, vals[kSlotMuX]);
           vals[kSlotMuY] = fmaf(-cf, dq_ddy, vals[kSlotMuY]);
           const float cdx = cf * dx;
@@ -261,14 +268,8 @@ __global__ void __launch_bounds__(kBlock / PPT) blend_bwd_kernel(DevMap m, DevCa
 template <int DP, int SLOTS, int PPT>
 static void launch_bwd_cfg(const DevMap& m, const DevCam& c, const ViewBufs& v, const TileLists& tl,
                            const PixelState& ps, const BwdIn& in, float* gacc, cudaStream_t s) {
-  static int ctas_per_sm = 0, sms = 0;
-  if (!ctas_per_sm) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, blend_bwd_kernel<DP, SLOTS, PPT>, kBlock / PPT, 0);
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (ctas_per_sm < 1) ctas_per_sm = 1;
-  }
+  const int ctas_per_sm = kernel_ctas_per_sm(reinterpret_cast<const void*>(blend_bwd_kernel<DP, SLOTS, PPT>), kBlock / PPT, 0);
+  const int sms = device_sm_count();
   const int ntiles = c.tiles_x * c.tiles_y;
   const int grid = min(ntiles, ctas_per_sm * sms);
   cudaMemsetAsync(tl.counter, 0, sizeof(int), s);
@@ -278,27 +279,13 @@ static void launch_bwd_cfg(const DevMap& m, const DevCam& c, const ViewBufs& v, 
 template <int DP>
 static void launch_bwd_dp(const DevMap& m, const DevCam& c, const ViewBufs& v, const TileLists& tl,
                           const PixelState& ps, const BwdIn& in, float* gacc, cudaStream_t s) {
-  constexpr int SLOTS = slots_for(DP);
-  static const int ppt = [] {
-    const char* e = getenv("LGS_BWD_PPT");  // tuning knob (1, 2 or 4 pixels per thread)
-    const int val = e ? atoi(e) : 2;
-    return (val == 1 || val == 2 || val == 4) ? val : 2;
-  }();
-  if (ppt == 1) launch_bwd_cfg<DP, SLOTS, 1>(m, c, v, tl, ps, in, gacc, s);
-  else if (ppt == 4) launch_bwd_cfg<DP, SLOTS, 4>(m, c, v, tl, ps, in, gacc, s);
-  else launch_bwd_cfg<DP, SLOTS, 2>(m, c, v, tl, ps, in, gacc, s);
+  // 2 pixels per thread (1 and 4 measured slower: DESIGN.md section 5)
+  launch_bwd_cfg<DP, slots_for(DP), 2>(m, c, v, tl, ps, in, gacc, s);
 }
 
 void launch_blend_bwd(const DevMap& m, const DevCam& c, const ViewBufs& v, const TileLists& tl,
                       const PixelState& ps, const BwdIn& in, float* gacc, int slots, cudaStream_t s) {
   (void)slots;
-  // The tensor-core variant (blend_bwd_mma.cu) is opt-in (LGS_BWD_IMPL=mma) until it beats this one.
-  const char* impl = getenv("LGS_BWD_IMPL");
-  const bool use_mma = impl && impl[0] == 'm';
-  if (use_mma && blend_bwd_mma_supported(m.dp)) {
-    launch_blend_bwd_mma(m, c, v, tl, ps, in, gacc, s);
-    return;
-  }
   switch (m.dp) {
     case 0: launch_bwd_dp<0>(m, c, v, tl, ps, in, gacc, s); break;
     case 4: launch_bwd_dp<4>(m, c, v, tl, ps, in, gacc, s); break;

@@ -13,6 +13,7 @@
 // boundary, and keeps both phases' latency in one CTA.  The first layered pass leaves unsaturated
 // tiles (flagged) without backward; the second pass renders them here on their complete lists.
 #include "blend_common.cuh"
+#include "dev_cache.h"
 
 namespace lgs {
 
@@ -20,8 +21,8 @@ template <int DP>
 struct FusedSmem {
   static constexpr int NB = 192;  // list entries per staged batch (static shared memory < 48 KB)
   float4 r0[NB];                  // u, v, depth, opacity
-  float4 sc[NB];                  // scaled conic a, b2, c, -
-  float4 r1[NB];                  // conic A, B, C, radius
+  float4 fa[NB];                  // conic frame S0, T0, ux, uy (blend_common.cuh stage_frame)
+  float4 fb[NB];                  // conic frame wx, wy, dxc, dyc
   uint2 rect[NB];
   float4 col[NB];
   uint32_t gid[NB];
@@ -70,16 +71,18 @@ __global__ void __launch_bounds__(kBlock / 2) blend_fused_l1_kernel(DevMap m, De
   const float inv_rgb = 1.0f / (3.0f * npx), inv_d = 1.0f / npx;
   const float inv_f = m.d > 0 ? 1.0f / ((float)m.d * npx) : 0.f;
 
-  // stage list entries [b0, b0 + cnt) of the tile's list (range.x-relative positions)
-  auto stage = [&](uint32_t list0, int cnt) {
+  // stage list entries [b0, b0 + cnt) of the tile's list (range.x-relative positions); (xc, yc) =
+  // the tile centre the conic frames are centred on
+  auto stage = [&](uint32_t list0, int cnt, float xc, float yc) {
     for (int e = tid; e < cnt; e += NT) {
       const uint32_t g = __ldg(tl.vals + list0 + e);
       sm.gid[e] = g;
-      sm.r0[e] = __ldg(v.rec0 + g);
+      const float4 r0 = __ldg(v.rec0 + g);
+      sm.r0[e] = r0;
       const float4 r1 = __ldg(v.rec1 + g);
-      sm.r1[e] = r1;
-      const ScaledConic s = scale_conic(r1.x, r1.y, r1.z);
-      sm.sc[e] = make_float4(s.a, s.b2, s.c, 0.f);
+      const ConicFrame f = stage_frame(r0.x, r0.y, r1.x, r1.y, r1.z, xc, yc);
+      sm.fa[e] = f.a;
+      sm.fb[e] = f.b;
       sm.rect[e] = __ldg(v.rect + g);
       sm.col[e] = __ldg(v.color + g);
       if (DP > 0) {
@@ -94,10 +97,12 @@ __global__ void __launch_bounds__(kBlock / 2) blend_fused_l1_kernel(DevMap m, De
     const int tx = tile % c.tiles_x, ty = tile / c.tiles_x;
     const int px = tx * kTile + lx;
     const int py0 = ty * kTile + ly0;
-    const float fpx = (float)px;
-    float fpy[PPT];
+    // pixel offsets from the tile centre (the conic frames' origin)
+    const float xc = (float)(tx * kTile) + 7.5f, yc = (float)(ty * kTile) + 7.5f;
+    const float ex = (float)lx - 7.5f;
+    float ey[PPT];
 #pragma unroll
-    for (int k = 0; k < PPT; ++k) fpy[k] = (float)(py0 + k);
+    for (int k = 0; k < PPT; ++k) ey[k] = (float)(ly0 + k) - 7.5f;
     const uint2 range = tl.ranges[tile];
     const uint32_t len = range.y - range.x;
 
@@ -120,7 +125,7 @@ __global__ void __launch_bounds__(kBlock / 2) blend_fused_l1_kernel(DevMap m, De
     for (uint32_t pos = 0; pos < len; pos += NB) {
       if (__syncthreads_count(all_done) == NT) break;
       const int cnt = (int)min((uint32_t)NB, len - pos);
-      stage(range.x + pos, cnt);
+      stage(range.x + pos, cnt, xc, yc);
       res_batch = (int)(pos / NB);
       __syncthreads();
       auto composite = [&](int e, const float (&al)[PPT], const bool (&in)[PPT], float depth_z) {
@@ -175,15 +180,18 @@ __global__ void __launch_bounds__(kBlock / 2) blend_fused_l1_kernel(DevMap m, De
         const bool hit1 = px >= (int)(rc1.x & 0xffffu) && px <= (int)(rc1.x >> 16) &&
                           py0 <= (int)(rc1.y >> 16) && py0 + PPT - 1 >= (int)(rc1.y & 0xffffu);
         if (!hit0 && !hit1) continue;
-        const float4 r00 = sm.r0[e], s00 = sm.sc[e];
-        const float4 r01 = has1 ? sm.r0[e + 1] : r00, s01 = has1 ? sm.sc[e + 1] : s00;
+        const float4 r00 = sm.r0[e], fa0 = sm.fa[e], fb0 = sm.fb[e];
+        const float4 r01 = has1 ? sm.r0[e + 1] : r00, fa1 = has1 ? sm.fa[e + 1] : fa0, fb1 = has1 ? sm.fb[e + 1] : fb0;
         float al0[PPT], al1[PPT];
         bool in0[PPT], in1[PPT];
 #pragma unroll
         for (int k = 0; k < PPT; ++k) {
-          float dx, dy, G;
-          al0[k] = splat_alpha(r00.x, r00.y, ScaledConic{s00.x, s00.y, s00.z}, r00.w, fpx, fpy[k], dx, dy, G);
-          al1[k] = splat_alpha(r01.x, r01.y, ScaledConic{s01.x, s01.y, s01.z}, r01.w, fpx, fpy[k], dx, dy, G);
+          float S, T, G;
+          al0[k] = frame_alpha(fa0, fb0, r00.w, ex, ey[k], S, T, G);
+          al1[k] = frame_alpha(fa1, fb1, r01.w, ex, ey[k], S, T, G);
+        }
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) {
           const int py = py0 + k;
           in0[k] = hit0 && py >= (int)(rc0.y & 0xffffu) && py <= (int)(rc0.y >> 16);
           in1[k] = hit1 && py >= (int)(rc1.y & 0xffffu) && py <= (int)(rc1.y >> 16);
@@ -280,7 +288,7 @@ __global__ void __launch_bounds__(kBlock / 2) blend_fused_l1_kernel(DevMap m, De
       const int cnt = (int)min((uint32_t)NB, len - bpos);
       if (b != res_batch) {  // restage (long traversals only); the resident batch is reused
         __syncthreads();
-        stage(range.x + bpos, cnt);
+        stage(range.x + bpos, cnt, xc, yc);
         res_batch = b;
         __syncthreads();
       }
@@ -293,14 +301,15 @@ __global__ void __launch_bounds__(kBlock / 2) blend_fused_l1_kernel(DevMap m, De
             px >= (int)(rc.x & 0xffffu) && px <= (int)(rc.x >> 16) && py0 <= ry1 && py0 + PPT - 1 >= ry0;
         if (!__any_sync(0xffffffffu, col_in)) continue;
         const float4 r0 = sm.r0[e];
-        const float4 s4 = sm.sc[e];
-        const ScaledConic sc{s4.x, s4.y, s4.z};
-        float alphas[PPT], Gs[PPT], dxs[PPT], dys[PPT];
+        const float4 fa = sm.fa[e], fb = sm.fb[e];
+        float alphas[PPT], Gs[PPT], Ss[PPT], Ts[PPT];
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) alphas[k] = frame_alpha(fa, fb, r0.w, ex, ey[k], Ss[k], Ts[k], Gs[k]);
         bool any = false;
 #pragma unroll
         for (int k = 0; k < PPT; ++k) {
           const int py = py0 + k;
-          const float al = splat_alpha(r0.x, r0.y, sc, r0.w, fpx, fpy[k], dxs[k], dys[k], Gs[k]);
+          const float al = alphas[k];
           const bool ok = col_in && jrel < last[k] && py >= ry0 && py <= ry1 && al >= c.alpha_skip;
           alphas[k] = ok ? al : 0.f;
           any = any || ok;
@@ -309,11 +318,9 @@ __global__ void __launch_bounds__(kBlock / 2) blend_fused_l1_kernel(DevMap m, De
         float vals[SLOTS];
 #pragma unroll
         for (int q = 0; q < SLOTS; ++q) vals[q] = 0.f;
-        const float4 r1 = sm.r1[e];
         const float4 col = sm.col[e];
         const float op = r0.w;
         const float do_dlogit = op * (1.0f - op);
-        const float twoA = 2.0f * r1.x, twoB = 2.0f * r1.y, twoC = 2.0f * r1.z;
         float w[PPT], dldw[PPT], inv1ma[PPT];
 #pragma unroll
         for (int k = 0; k < PPT; ++k) {
@@ -349,7 +356,10 @@ __global__ void __launch_bounds__(kBlock / 2) blend_fused_l1_kernel(DevMap m, De
 #pragma unroll
         for (int k = 0; k < PPT; ++k) {
           const float alpha = alphas[k];
-          const float dx = dxs[k], dy = dys[k], G = Gs[k];
+          const float G = Gs[k];
+          const float dx = fb.z + ex, dy = fb.w + ey[k];  // pixel - mean (renderer.cpp:141-142)
+          float dq_ddx, dq_ddy;
+          frame_dq(fa, fb, Ss[k], Ts[k], dq_ddx, dq_ddy);
           const float dl_da = (alpha != 0.f && !(alpha > c.alpha_clamp)) ? T[k] * dldw[k] - accum[k] * inv1ma[k] : 0.f;
           accum[k] = fmaf(dldw[k], w[k], accum[k]);
           vals[kSlotColor + 0] = fmaf(g_rgb[k][0], w[k], vals[kSlotColor + 0]);
@@ -358,8 +368,6 @@ __global__ void __launch_bounds__(kBlock / 2) blend_fused_l1_kernel(DevMap m, De
           vals[kSlotZ] = fmaf(g_draw[k], w[k], vals[kSlotZ]);
           vals[kSlotOpac] = fmaf(dl_da * G, do_dlogit, vals[kSlotOpac]);
           const float cf = dl_da * op * (-0.5f * G);
-          const float dq_ddx = fmaf(twoA, dx, twoB * dy);
-          const float dq_ddy = fmaf(twoC, dy, twoB * dx);
           vals[kSlotMuX] = fmaf(-cf, dq_ddx, vals[kSlotMuX]);
           vals[kSlotMuY] = fmaf(-cf, dq_ddy, vals[kSlotMuY]);
           const float cdx = cf * dx;
@@ -389,14 +397,8 @@ bool blend_fused_supported(int dp) { return dp == 16 || dp == 8 || dp == 4 || dp
 template <int DP>
 static void launch_fused_dp(const DevMap& m, const DevCam& c, const ViewBufs& v, const TileLists& tl, const FwdOut& o,
                             float* gacc, cudaStream_t s, bool counter_zeroed) {
-  static int ctas_per_sm = 0, sms = 0;
-  if (!ctas_per_sm) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, blend_fused_l1_kernel<DP>, kBlock / 2, 0);
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (ctas_per_sm < 1) ctas_per_sm = 1;
-  }
+  const int ctas_per_sm = kernel_ctas_per_sm(reinterpret_cast<const void*>(blend_fused_l1_kernel<DP>), kBlock / 2, 0);
+  const int sms = device_sm_count();
   const int ntiles = c.tiles_x * c.tiles_y;
   const int grid = min(ntiles, ctas_per_sm * sms);
   if (!counter_zeroed) cudaMemsetAsync(tl.counter, 0, sizeof(int), s);

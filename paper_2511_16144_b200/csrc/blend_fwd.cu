@@ -20,13 +20,15 @@
 // cotangents the backward reads and one loss partial per CTA.
 // Roofline: FP32/SFU; ~13 FLOP + 1 EX2 per evaluated (pixel, Gaussian), +45 per contribution.
 #include "blend_common.cuh"
+#include "dev_cache.h"
 
 namespace lgs {
 
 template <int DP, int NB>
 struct FwdSmem {
   float4 r0[NB];  // u, v, depth, opacity
-  float4 sc[NB];  // scaled conic a, b2, c, -
+  float4 fa[NB];  // conic frame S0, T0, ux, uy (blend_common.cuh stage_frame)
+  float4 fb[NB];  // conic frame wx, wy, dxc, dyc
   uint2 rect[NB];
   float4 col[NB];
   float4 feat[NB][DP > 0 ? DP / 4 : 1];
@@ -53,10 +55,12 @@ __global__ void __launch_bounds__(kBlock / PPT, MINB) blend_fwd_kernel(DevMap m,
     const int tx = tile % c.tiles_x, ty = tile / c.tiles_x;
     const int px = tx * kTile + lx;
     const int py0 = ty * kTile + ly0;
-    const float fpx = (float)px;
-    float fpy[PPT];
+    // pixel offsets from the tile centre (the conic frames' origin)
+    const float xc = (float)(tx * kTile) + 7.5f, yc = (float)(ty * kTile) + 7.5f;
+    const float ex = (float)lx - 7.5f;
+    float ey[PPT];
 #pragma unroll
-    for (int k = 0; k < PPT; ++k) fpy[k] = (float)(py0 + k);
+    for (int k = 0; k < PPT; ++k) ey[k] = (float)(ly0 + k) - 7.5f;
     const uint2 range = tl.ranges[tile];
 
     float T[PPT], cr[PPT], cg[PPT], cb[PPT], draw[PPT], acc[PPT];
@@ -80,10 +84,12 @@ __global__ void __launch_bounds__(kBlock / PPT, MINB) blend_fwd_kernel(DevMap m,
         const uint32_t j = base + e;
         if (j < range.y) {
           const uint32_t g = __ldg(tl.vals + j);
-          sm.r0[e] = __ldg(v.rec0 + g);
+          const float4 r0 = __ldg(v.rec0 + g);
+          sm.r0[e] = r0;
           const float4 r1 = __ldg(v.rec1 + g);
-          const ScaledConic s = scale_conic(r1.x, r1.y, r1.z);
-          sm.sc[e] = make_float4(s.a, s.b2, s.c, 0.f);
+          const ConicFrame f = stage_frame(r0.x, r0.y, r1.x, r1.y, r1.z, xc, yc);
+          sm.fa[e] = f.a;
+          sm.fb[e] = f.b;
           sm.rect[e] = __ldg(v.rect + g);
           sm.col[e] = __ldg(v.color + g);
           if (DP > 0) {
@@ -156,15 +162,18 @@ __global__ void __launch_bounds__(kBlock / PPT, MINB) blend_fwd_kernel(DevMap m,
         const bool hit1 = px >= (int)(rc1.x & 0xffffu) && px <= (int)(rc1.x >> 16) &&
                           py0 <= (int)(rc1.y >> 16) && py0 + PPT - 1 >= (int)(rc1.y & 0xffffu);
         if (!hit0 && !hit1) continue;
-        const float4 r00 = sm.r0[e], s00 = sm.sc[e];
-        const float4 r01 = has1 ? sm.r0[e + 1] : r00, s01 = has1 ? sm.sc[e + 1] : s00;
+        const float4 r00 = sm.r0[e], fa0 = sm.fa[e], fb0 = sm.fb[e];
+        const float4 r01 = has1 ? sm.r0[e + 1] : r00, fa1 = has1 ? sm.fa[e + 1] : fa0, fb1 = has1 ? sm.fb[e + 1] : fb0;
         float al0[PPT], al1[PPT];
         bool in0[PPT], in1[PPT];
 #pragma unroll
         for (int k = 0; k < PPT; ++k) {
-          float dx, dy, G;
-          al0[k] = splat_alpha(r00.x, r00.y, ScaledConic{s00.x, s00.y, s00.z}, r00.w, fpx, fpy[k], dx, dy, G);
-          al1[k] = splat_alpha(r01.x, r01.y, ScaledConic{s01.x, s01.y, s01.z}, r01.w, fpx, fpy[k], dx, dy, G);
+          float S, T, G;
+          al0[k] = frame_alpha(fa0, fb0, r00.w, ex, ey[k], S, T, G);
+          al1[k] = frame_alpha(fa1, fb1, r01.w, ex, ey[k], S, T, G);
+        }
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) {
           const int py = py0 + k;
           in0[k] = hit0 && py >= (int)(rc0.y & 0xffffu) && py <= (int)(rc0.y >> 16);
           in1[k] = hit1 && py >= (int)(rc1.y & 0xffffu) && py <= (int)(rc1.y >> 16);
@@ -257,15 +266,8 @@ __global__ void __launch_bounds__(kBlock / PPT, MINB) blend_fwd_kernel(DevMap m,
 template <int DP, bool L1, int PPT, int NB, int MINB, bool WORK>
 static void launch_fwd_work(const DevMap& m, const DevCam& c, const ViewBufs& v, const TileLists& tl,
                             const PixelState& ps, const FwdOut& o, cudaStream_t s) {
-  static int ctas_per_sm = 0, sms = 0;
-  if (!ctas_per_sm) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, blend_fwd_kernel<DP, L1, PPT, NB, MINB, WORK>,
-                                                  kBlock / PPT, 0);
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (ctas_per_sm < 1) ctas_per_sm = 1;
-  }
+  const int ctas_per_sm = kernel_ctas_per_sm(reinterpret_cast<const void*>(blend_fwd_kernel<DP, L1, PPT, NB, MINB, WORK>), kBlock / PPT, 0);
+  const int sms = device_sm_count();
   const int ntiles = c.tiles_x * c.tiles_y;
   const int grid = min(ntiles, ctas_per_sm * sms);
   cudaMemsetAsync(tl.counter, 0, sizeof(int), s);

@@ -14,6 +14,8 @@
 #include <cstdio>
 #include <cstring>
 #include <fstream>
+#include <new>
+#include <stdexcept>
 #include <string>
 #include <vector>
 
@@ -100,6 +102,8 @@ struct lgs_ctx {
   std::vector<PhaseMark>* capture_marks = nullptr;  // lgs_plan capture: phase events recorded as graph nodes
   int64_t pairs_cap = 0;  // tile-list capacity for the next render (0: size from the exact count)
   bool full_lists = false;  // lgs_ctx_set_full_tile_lists: single-pass binning of every pair
+  bool radix_depth = false;  // LGS_OPT_RADIX_DEPTH_ORDER: CUB radix sort for the depth order (cross-check)
+  bool fused_eager = false;  // LGS_OPT_FUSED_EAGER: uncaptured fused-L1 renders run the fused kernel
   cudaStream_t cond_stream = nullptr;  // captures the body of a plan's conditional node
   cudaStream_t cond_parent = nullptr;  // the capturing stream while a body is captured
   // lgs_plan capture: the zero rows of the plan's (non-accumulating) gradient buffers are written
@@ -326,13 +330,19 @@ lgs_status make_devcam(const lgs_camera* cam, const lgs_render_config* cfg, DevC
   w /= nrm; x /= nrm; y /= nrm; z /= nrm;
   double rcw[9];
   quat_to_rot(w, -x, -y, -z, rcw);
-  for (int i = 0; i < 9; ++i) out->rcw[i] = (float)rcw[i];
+  for (int i = 0; i < 9; ++i) {
+    out->rcw[i] = (float)rcw[i];
+    out->rcw_d[i] = rcw[i];
+  }
   for (int i = 0; i < 3; ++i) {
     const double tcw = -(rcw[i * 3 + 0] * cam->t[0] + rcw[i * 3 + 1] * cam->t[1] + rcw[i * 3 + 2] * cam->t[2]);
     out->tcw[i] = (float)tcw;
     out->cc[i] = (float)cam->t[i];
+    out->tcw_d[i] = tcw;
+    out->cc_d[i] = cam->t[i];
   }
   out->fx = (float)cam->fx; out->fy = (float)cam->fy;
+  out->fx_d = cam->fx; out->fy_d = cam->fy;
   out->cx = (float)cam->cx; out->cy = (float)cam->cy;
   out->W = cam->width; out->H = cam->height;
   out->tiles_x = (cam->width + kTile - 1) / kTile;
@@ -537,6 +547,16 @@ LGS_API lgs_status lgs_ctx_set_full_tile_lists(lgs_ctx* ctx, int32_t full) {
   return LGS_OK;
 }
 
+LGS_API lgs_status lgs_ctx_set_option(lgs_ctx* ctx, int32_t option, int64_t value) {
+  if (!ctx) return fail(LGS_EINVAL, "ctx is NULL");
+  switch (option) {
+    case LGS_OPT_FULL_TILE_LISTS: ctx->full_lists = value != 0; return LGS_OK;
+    case LGS_OPT_RADIX_DEPTH_ORDER: ctx->radix_depth = value != 0; return LGS_OK;
+    case LGS_OPT_FUSED_EAGER: ctx->fused_eager = value != 0; return LGS_OK;
+    default: return fail(LGS_EINVAL, "unknown context option");
+  }
+}
+
 LGS_API lgs_status lgs_ctx_destroy(lgs_ctx* ctx) {
   if (!ctx) return LGS_OK;
   ctx_release(ctx);
@@ -682,9 +702,8 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
   TRYB(dalloc(ctx, &t->ps.acc, npix));
   if (ctx->profiling) TRYB(dalloc(ctx, &t->ps.work, npix));  // work counters: profiling renders only
 
-  // LGS_DEPTH_SORT=cub selects the device radix sort (A/B and cross-check of depth_order.cu)
-  const char* dsort = getenv("LGS_DEPTH_SORT");
-  const bool cub_depth = dsort && dsort[0] == 'c';
+  // LGS_OPT_RADIX_DEPTH_ORDER selects the device radix sort (cross-check of depth_order.cu)
+  const bool cub_depth = ctx->radix_depth;
   const bool fast = fast_binning_supported(ntiles);
   // depth-layered binning (binning_fast.cu, depth_order.cu): K1 fills the depth-bucket histogram,
   // the depth order of layer A is built with the binning below, the complete order only when some
@@ -841,10 +860,11 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
       LGS_CUDA(cudaMemsetAsync(ra, 0, sizeof(uint32_t) * (4 + (size_t)ntiles), s));
       // captured fused-L1 step: each tile's backward runs right after its forward (blend_fused.cu);
       // the depth order flags the layer-A Gaussians active and zeroes their accumulator rows
-      // (LGS_FUSE_EAGER=1: the same in uncaptured renders, for profiling tools only -- the tape then
-      // holds the L1 gradients and any other cotangents passed to a backward are ignored)
-      static const bool fuse_eager = getenv("LGS_FUSE_EAGER") != nullptr;
-      const bool fuse = (ctx->capturing || fuse_eager) && targets && blend_fused_supported(dp) && slots_for(dp) == 32;
+      // (LGS_OPT_FUSED_EAGER: the same in uncaptured renders, for profilers that cannot see inside
+      // graphs -- the tape then holds the L1 gradients, and a backward with other cotangents is
+      // rejected with LGS_EINVAL)
+      const bool fuse = (ctx->capturing || ctx->fused_eager) && targets && blend_fused_supported(dp) &&
+                        slots_for(dp) == 32;
       if (fuse) {
         dfree(ctx, t->gacc);
         LGS_TRY(dalloc(ctx, &t->gacc, (size_t)n * 32));
@@ -1157,6 +1177,8 @@ lgs_status check_shape(const int32_t shape[3], int H, int W, int C, const char* 
 LGS_API lgs_status lgs_render_backward(lgs_ctx* ctx, const lgs_saved* tape, const lgs_cotangents* cot,
                                        lgs_map_grads* grads, float* pose_grad) {
   if (!ctx || !tape) return fail(LGS_EINVAL, "ctx/tape is NULL");
+  if (tape->bwd_fused)
+    return fail(LGS_EINVAL, "tape of a fused-L1 render (LGS_OPT_FUSED_EAGER): use lgs_render_backward_l1");
   const int H = tape->cam.H, W = tape->cam.W, d = tape->dm.d;
   const size_t npix = (size_t)W * H;
   BwdIn in{};
@@ -1232,6 +1254,7 @@ LGS_API lgs_loss_weights lgs_loss_weights_default(void) {
 LGS_API lgs_status lgs_mapping_loss(lgs_ctx* ctx, lgs_saved* t, const lgs_images* rendered, const lgs_keyframe* kf,
                                     const lgs_decoder* dec, const lgs_loss_weights* w_in, lgs_loss_breakdown* out) {
   if (!ctx || !t || !rendered || !kf) return fail(LGS_EINVAL, "ctx/tape/rendered/keyframe is NULL");
+  if (t->bwd_fused) return fail(LGS_EINVAL, "tape of a fused-L1 render (LGS_OPT_FUSED_EAGER) carries the L1 loss");
   const int H = t->cam.H, W = t->cam.W, d = t->dm.d, dp = t->dm.dp;
   if (H < 11 || W < 11) return fail(LGS_EINVAL, "ssim: image %dx%d smaller than the 11x11 window", W, H);
   if (!rendered->rgb || !kf->rgb || !kf->depth) return fail(LGS_EINVAL, "rendered rgb / keyframe rgb, depth needed");
@@ -1837,12 +1860,11 @@ LGS_API lgs_status lgs_map_download(lgs_ctx* ctx, const lgs_map* map, lgs_gaussi
   const bool host = dst->memory == LGS_MEM_HOST;
   float* stage = nullptr;
   if (host) {
-    LGS_TRY(dalloc(ctx, &stage, sz[0] + sz[1] + sz[2] + sz[3] + sz[4] + sz[5]));
-    float* q = stage;
-    for (int k = 0; k < 6; ++k) {
-      dev[k] = outs[k] ? q : nullptr;
-      q += sz[k];
-    }
+    // staged segments start on 16-byte boundaries (the rotation rows are stored as float4)
+    size_t off[7] = {0};
+    for (int k = 0; k < 6; ++k) off[k + 1] = off[k] + ((sz[k] + 3) & ~(size_t)3);
+    LGS_TRY(dalloc(ctx, &stage, off[6]));
+    for (int k = 0; k < 6; ++k) dev[k] = outs[k] ? stage + off[k] : nullptr;
   } else {
     for (int k = 0; k < 6; ++k) dev[k] = outs[k];
   }
@@ -1885,6 +1907,37 @@ lgs_status read_header(std::ifstream& is, const char* path, MapFileHeader* h) {
   return LGS_OK;
 }
 
+// The byte size a file of `count` records needs; when the file is shorter, the error the
+// record-by-record reader (gaussian_map.cpp:187-192, read_pod) would raise at the first missing
+// field -- checked before anything is sized from the header's count.
+lgs_status check_map_file_size(std::ifstream& is, const char* path, const MapFileHeader& h) {
+  const std::streampos here = is.tellg();
+  is.seekg(0, std::ios::end);
+  const uint64_t size = (uint64_t)is.tellg();
+  is.seekg(here);
+  if (!is) return fail(LGS_EIO, "cannot size map file: %s", path);
+  const uint64_t rec = 4ull * (14 + h.dim) + 8ull, body = size > 20 ? size - 20 : 0;
+  if (h.count <= body / rec) return LGS_OK;
+  const uint64_t got = body % rec;  // bytes of the first incomplete record
+  const char* what[] = {"position", "rotation", "scale", "opacity", "color", "feature", "anchor"};
+  const uint64_t off[] = {0, 12, 28, 40, 44, 56, 56 + 4ull * h.dim};
+  int f = 0;
+  while (f < 6 && got >= off[f + 1]) ++f;
+  return fail(LGS_EIO, "map file truncated reading %s", what[f]);
+}
+
+// No C++ exception crosses the ABI: allocation failures of host containers become LGS_ENOMEM.
+template <class F>
+lgs_status guarded(F&& f) {
+  try {
+    return f();
+  } catch (const std::bad_alloc&) {
+    return fail(LGS_ENOMEM, "host allocation failed");
+  } catch (const std::exception& e) {
+    return fail(LGS_EIO, "%s", e.what());
+  }
+}
+
 }  // namespace
 
 extern "C" {
@@ -1895,145 +1948,155 @@ LGS_API lgs_status lgs_map_file_info(const char* path, int32_t* feature_dim, int
   if (!is) return fail(LGS_EIO, "cannot open map file: %s", path);
   MapFileHeader h;
   LGS_TRY(read_header(is, path, &h));
+  LGS_TRY(check_map_file_size(is, path, h));
   if (feature_dim) *feature_dim = (int32_t)h.dim;
   if (count) *count = (int64_t)h.count;
   return LGS_OK;
 }
 
 LGS_API lgs_status lgs_map_file_read(const char* path, int32_t expected_dim, lgs_gaussians* dst, uint64_t* anchors) {
-  if (!path || !dst) return fail(LGS_EINVAL, "path/dst is NULL");
-  if (dst->memory != LGS_MEM_HOST) return fail(LGS_EINVAL, "lgs_map_file_read fills host buffers");
-  std::ifstream is(path, std::ios::binary);
-  if (!is) return fail(LGS_EIO, "cannot open map file: %s", path);
-  MapFileHeader h;
-  LGS_TRY(read_header(is, path, &h));
-  if (expected_dim > 0 && (int32_t)h.dim != expected_dim)
-    return fail(LGS_EIO, "map feature dimension mismatch: file has %u, expected %d", h.dim, expected_dim);
-  if (dst->n != (int64_t)h.count || dst->feature_dim != (int32_t)h.dim || dst->sh_degree != 0)
-    return fail(LGS_EINVAL, "destination must hold %llu Gaussians of dim %u, sh_degree 0",
-                (unsigned long long)h.count, h.dim);
-  const uint32_t d = h.dim;
-  const size_t rec = sizeof(float) * (3 + 4 + 3 + 1 + 3 + d) + sizeof(uint64_t);
-  std::vector<char> buf(rec);
-  const char* what[] = {"position", "rotation", "scale", "opacity", "color", "feature", "anchor"};
-  const size_t off[] = {0, 12, 28, 40, 44, 56, 56 + 4 * (size_t)d};
-  float* pos = (float*)dst->positions;
-  float* rot = (float*)dst->rotations;
-  float* ls = (float*)dst->log_scales;
-  float* op = (float*)dst->opacity_logits;
-  float* col = (float*)dst->sh;
-  float* ft = (float*)dst->features;
-  for (uint64_t i = 0; i < h.count; ++i) {
-    is.read(buf.data(), (std::streamsize)rec);
-    if (!is) {  // name the first field that ran out, like read_pod (gaussian_map.cpp:187-192)
-      const size_t got = (size_t)is.gcount();
-      int f = 0;
-      while (f < 6 && got >= off[f + 1]) ++f;
-      return fail(LGS_EIO, "map file truncated reading %s", what[f]);
+  return guarded([&]() -> lgs_status {
+    if (!path || !dst) return fail(LGS_EINVAL, "path/dst is NULL");
+    if (dst->memory != LGS_MEM_HOST) return fail(LGS_EINVAL, "lgs_map_file_read fills host buffers");
+    std::ifstream is(path, std::ios::binary);
+    if (!is) return fail(LGS_EIO, "cannot open map file: %s", path);
+    MapFileHeader h;
+    LGS_TRY(read_header(is, path, &h));
+    if (expected_dim > 0 && (int32_t)h.dim != expected_dim)
+      return fail(LGS_EIO, "map feature dimension mismatch: file has %u, expected %d", h.dim, expected_dim);
+    LGS_TRY(check_map_file_size(is, path, h));
+    if (dst->n != (int64_t)h.count || dst->feature_dim != (int32_t)h.dim || dst->sh_degree != 0)
+      return fail(LGS_EINVAL, "destination must hold %llu Gaussians of dim %u, sh_degree 0",
+                  (unsigned long long)h.count, h.dim);
+    const uint32_t d = h.dim;
+    const size_t rec = sizeof(float) * (3 + 4 + 3 + 1 + 3 + d) + sizeof(uint64_t);
+    std::vector<char> buf(rec);
+    const char* what[] = {"position", "rotation", "scale", "opacity", "color", "feature", "anchor"};
+    const size_t off[] = {0, 12, 28, 40, 44, 56, 56 + 4 * (size_t)d};
+    float* pos = (float*)dst->positions;
+    float* rot = (float*)dst->rotations;
+    float* ls = (float*)dst->log_scales;
+    float* op = (float*)dst->opacity_logits;
+    float* col = (float*)dst->sh;
+    float* ft = (float*)dst->features;
+    for (uint64_t i = 0; i < h.count; ++i) {
+      is.read(buf.data(), (std::streamsize)rec);
+      if (!is) {  // name the first field that ran out, like read_pod (gaussian_map.cpp:187-192)
+        const size_t got = (size_t)is.gcount();
+        int f = 0;
+        while (f < 6 && got >= off[f + 1]) ++f;
+        return fail(LGS_EIO, "map file truncated reading %s", what[f]);
+      }
+      float v[14];
+      std::memcpy(v, buf.data(), sizeof v);
+      for (int a = 0; a < 3; ++a) pos[i * 3 + a] = v[a];
+      // file order w,x,y,z -> Eigen storage x,y,z,w; renormalize only when off-unit (gaussian_map.cpp:21-23)
+      double qw = v[3], qx = v[4], qy = v[5], qz = v[6];
+      const double nrm = std::sqrt(qw * qw + qx * qx + qy * qy + qz * qz);
+      if (std::abs(nrm - 1.0) > 1e-6 && nrm > 0.0) {
+        qw /= nrm; qx /= nrm; qy /= nrm; qz /= nrm;
+      }
+      rot[i * 4 + 0] = (float)qx; rot[i * 4 + 1] = (float)qy; rot[i * 4 + 2] = (float)qz; rot[i * 4 + 3] = (float)qw;
+      for (int a = 0; a < 3; ++a) ls[i * 3 + a] = v[7 + a];
+      op[i] = v[10];
+      for (int a = 0; a < 3; ++a) col[i * 3 + a] = v[11 + a];
+      for (uint32_t c = 0; c < d; ++c) {
+        float f;
+        std::memcpy(&f, buf.data() + 56 + 4 * (size_t)c, 4);
+        ft[(size_t)c * h.count + i] = f;  // features [d][N]
+      }
+      if (anchors) std::memcpy(&anchors[i], buf.data() + off[6], sizeof(uint64_t));
     }
-    float v[14];
-    std::memcpy(v, buf.data(), sizeof v);
-    for (int a = 0; a < 3; ++a) pos[i * 3 + a] = v[a];
-    // file order w,x,y,z -> Eigen storage x,y,z,w; renormalize only when off-unit (gaussian_map.cpp:21-23)
-    double qw = v[3], qx = v[4], qy = v[5], qz = v[6];
-    const double nrm = std::sqrt(qw * qw + qx * qx + qy * qy + qz * qz);
-    if (std::abs(nrm - 1.0) > 1e-6 && nrm > 0.0) {
-      qw /= nrm; qx /= nrm; qy /= nrm; qz /= nrm;
-    }
-    rot[i * 4 + 0] = (float)qx; rot[i * 4 + 1] = (float)qy; rot[i * 4 + 2] = (float)qz; rot[i * 4 + 3] = (float)qw;
-    for (int a = 0; a < 3; ++a) ls[i * 3 + a] = v[7 + a];
-    op[i] = v[10];
-    for (int a = 0; a < 3; ++a) col[i * 3 + a] = v[11 + a];
-    for (uint32_t c = 0; c < d; ++c) {
-      float f;
-      std::memcpy(&f, buf.data() + 56 + 4 * (size_t)c, 4);
-      ft[(size_t)c * h.count + i] = f;  // features [d][N]
-    }
-    if (anchors) std::memcpy(&anchors[i], buf.data() + off[6], sizeof(uint64_t));
-  }
-  return LGS_OK;
+    return LGS_OK;
+  });
 }
 
 LGS_API lgs_status lgs_map_file_write(const char* path, const lgs_gaussians* src, const uint64_t* anchors) {
-  if (!path || !src) return fail(LGS_EINVAL, "path/src is NULL");
-  if (src->n < 0 || src->feature_dim <= 0 || src->feature_dim > 4096)
-    return fail(LGS_EINVAL, "LEGOMAP1 needs 1 <= feature_dim <= 4096");
-  if (src->sh_degree != 0) return fail(LGS_EINVAL, "LEGOMAP1 stores SH degree 0 colour only");
-  const size_t n = (size_t)src->n, d = (size_t)src->feature_dim;
-  if (n > 0 && (!src->positions || !src->rotations || !src->log_scales || !src->opacity_logits || !src->sh ||
-                !src->features))
-    return fail(LGS_EINVAL, "a map attribute pointer is NULL");
-  // device sources are copied out first
-  std::vector<float> hp, hr, hl, ho, hc, hf;
-  const float *pos = (const float*)src->positions, *rot = (const float*)src->rotations,
-              *ls = (const float*)src->log_scales, *op = (const float*)src->opacity_logits,
-              *col = (const float*)src->sh, *ft = (const float*)src->features;
-  if (src->memory == LGS_MEM_DEVICE && n > 0) {
-    auto pull = [&](std::vector<float>& v, const float*& p, size_t count) -> lgs_status {
-      v.resize(count);
-      LGS_CUDA(cudaMemcpy(v.data(), p, sizeof(float) * count, cudaMemcpyDeviceToHost));
-      p = v.data();
-      return LGS_OK;
-    };
-    LGS_TRY(pull(hp, pos, n * 3)); LGS_TRY(pull(hr, rot, n * 4)); LGS_TRY(pull(hl, ls, n * 3));
-    LGS_TRY(pull(ho, op, n)); LGS_TRY(pull(hc, col, n * 3)); LGS_TRY(pull(hf, ft, n * d));
-  }
-  std::ofstream os(path, std::ios::binary);
-  if (!os) return fail(LGS_EIO, "cannot open map file for writing: %s", path);
-  os.write(kMapMagic, sizeof kMapMagic);
-  const uint32_t dim = (uint32_t)d;
-  const uint64_t count = n;
-  os.write(reinterpret_cast<const char*>(&dim), sizeof dim);
-  os.write(reinterpret_cast<const char*>(&count), sizeof count);
-  std::vector<char> buf(sizeof(float) * (14 + d) + sizeof(uint64_t));
-  for (size_t i = 0; i < n; ++i) {
-    float v[14];
-    for (int a = 0; a < 3; ++a) v[a] = pos[i * 3 + a];
-    v[3] = rot[i * 4 + 3]; v[4] = rot[i * 4 + 0]; v[5] = rot[i * 4 + 1]; v[6] = rot[i * 4 + 2];  // w,x,y,z
-    for (int a = 0; a < 3; ++a) v[7 + a] = ls[i * 3 + a];
-    v[10] = op[i];
-    for (int a = 0; a < 3; ++a) v[11 + a] = col[i * 3 + a];
-    std::memcpy(buf.data(), v, sizeof v);
-    for (size_t c = 0; c < d; ++c) std::memcpy(buf.data() + 56 + 4 * c, &ft[c * n + i], 4);
-    const uint64_t an = anchors ? anchors[i] : 0;
-    std::memcpy(buf.data() + 56 + 4 * d, &an, sizeof an);
-    os.write(buf.data(), (std::streamsize)buf.size());
-  }
-  if (!os) return fail(LGS_EIO, "failed writing map file: %s", path);
-  return LGS_OK;
+  return guarded([&]() -> lgs_status {
+    if (!path || !src) return fail(LGS_EINVAL, "path/src is NULL");
+    if (src->n < 0 || src->feature_dim <= 0 || src->feature_dim > 4096)
+      return fail(LGS_EINVAL, "LEGOMAP1 needs 1 <= feature_dim <= 4096");
+    if (src->sh_degree != 0) return fail(LGS_EINVAL, "LEGOMAP1 stores SH degree 0 colour only");
+    const size_t n = (size_t)src->n, d = (size_t)src->feature_dim;
+    if (n > 0 && (!src->positions || !src->rotations || !src->log_scales || !src->opacity_logits || !src->sh ||
+                  !src->features))
+      return fail(LGS_EINVAL, "a map attribute pointer is NULL");
+    // device sources are copied out first
+    std::vector<float> hp, hr, hl, ho, hc, hf;
+    const float *pos = (const float*)src->positions, *rot = (const float*)src->rotations,
+                *ls = (const float*)src->log_scales, *op = (const float*)src->opacity_logits,
+                *col = (const float*)src->sh, *ft = (const float*)src->features;
+    if (src->memory == LGS_MEM_DEVICE && n > 0) {
+      auto pull = [&](std::vector<float>& v, const float*& p, size_t count) -> lgs_status {
+        v.resize(count);
+        LGS_CUDA(cudaMemcpy(v.data(), p, sizeof(float) * count, cudaMemcpyDeviceToHost));
+        p = v.data();
+        return LGS_OK;
+      };
+      LGS_TRY(pull(hp, pos, n * 3)); LGS_TRY(pull(hr, rot, n * 4)); LGS_TRY(pull(hl, ls, n * 3));
+      LGS_TRY(pull(ho, op, n)); LGS_TRY(pull(hc, col, n * 3)); LGS_TRY(pull(hf, ft, n * d));
+    }
+    std::ofstream os(path, std::ios::binary);
+    if (!os) return fail(LGS_EIO, "cannot open map file for writing: %s", path);
+    os.write(kMapMagic, sizeof kMapMagic);
+    const uint32_t dim = (uint32_t)d;
+    const uint64_t count = n;
+    os.write(reinterpret_cast<const char*>(&dim), sizeof dim);
+    os.write(reinterpret_cast<const char*>(&count), sizeof count);
+    std::vector<char> buf(sizeof(float) * (14 + d) + sizeof(uint64_t));
+    for (size_t i = 0; i < n; ++i) {
+      float v[14];
+      for (int a = 0; a < 3; ++a) v[a] = pos[i * 3 + a];
+      v[3] = rot[i * 4 + 3]; v[4] = rot[i * 4 + 0]; v[5] = rot[i * 4 + 1]; v[6] = rot[i * 4 + 2];  // w,x,y,z
+      for (int a = 0; a < 3; ++a) v[7 + a] = ls[i * 3 + a];
+      v[10] = op[i];
+      for (int a = 0; a < 3; ++a) v[11 + a] = col[i * 3 + a];
+      std::memcpy(buf.data(), v, sizeof v);
+      for (size_t c = 0; c < d; ++c) std::memcpy(buf.data() + 56 + 4 * c, &ft[c * n + i], 4);
+      const uint64_t an = anchors ? anchors[i] : 0;
+      std::memcpy(buf.data() + 56 + 4 * d, &an, sizeof an);
+      os.write(buf.data(), (std::streamsize)buf.size());
+    }
+    if (!os) return fail(LGS_EIO, "failed writing map file: %s", path);
+    return LGS_OK;
+  });
 }
 
 LGS_API lgs_status lgs_map_load(lgs_ctx* ctx, const char* path, int32_t expected_dim, lgs_map** out) {
-  if (!ctx || !out) return fail(LGS_EINVAL, "ctx/out is NULL");
-  *out = nullptr;
-  int32_t dim = 0;
-  int64_t count = 0;
-  LGS_TRY(lgs_map_file_info(path, &dim, &count));
-  if (expected_dim > 0 && dim != expected_dim)
-    return fail(LGS_EIO, "map feature dimension mismatch: file has %d, expected %d", dim, expected_dim);
-  if (dim > LGS_MAX_FEATURE_DIM)
-    return fail(LGS_EINVAL, "feature dim %d exceeds the rasterizer's %d", dim, LGS_MAX_FEATURE_DIM);
-  const size_t n = (size_t)count;
-  std::vector<float> pos(n * 3), rot(n * 4), ls(n * 3), op(n), col(n * 3), ft(n * dim);
-  lgs_gaussians g{};
-  g.n = count; g.feature_dim = dim; g.sh_degree = 0;
-  g.positions = pos.data(); g.rotations = rot.data(); g.log_scales = ls.data(); g.opacity_logits = op.data();
-  g.sh = col.data(); g.features = ft.data(); g.memory = LGS_MEM_HOST;
-  LGS_TRY(lgs_map_file_read(path, expected_dim, &g, nullptr));
-  return lgs_map_create(ctx, &g, out);  // host source: synchronizes before the vectors go away
+  return guarded([&]() -> lgs_status {
+    if (!ctx || !out) return fail(LGS_EINVAL, "ctx/out is NULL");
+    *out = nullptr;
+    int32_t dim = 0;
+    int64_t count = 0;
+    LGS_TRY(lgs_map_file_info(path, &dim, &count));
+    if (expected_dim > 0 && dim != expected_dim)
+      return fail(LGS_EIO, "map feature dimension mismatch: file has %d, expected %d", dim, expected_dim);
+    if (dim > LGS_MAX_FEATURE_DIM)
+      return fail(LGS_EINVAL, "feature dim %d exceeds the rasterizer's %d", dim, LGS_MAX_FEATURE_DIM);
+    const size_t n = (size_t)count;
+    std::vector<float> pos(n * 3), rot(n * 4), ls(n * 3), op(n), col(n * 3), ft(n * dim);
+    lgs_gaussians g{};
+    g.n = count; g.feature_dim = dim; g.sh_degree = 0;
+    g.positions = pos.data(); g.rotations = rot.data(); g.log_scales = ls.data(); g.opacity_logits = op.data();
+    g.sh = col.data(); g.features = ft.data(); g.memory = LGS_MEM_HOST;
+    LGS_TRY(lgs_map_file_read(path, expected_dim, &g, nullptr));
+    return lgs_map_create(ctx, &g, out);  // host source: synchronizes before the vectors go away
+  });
 }
 
 LGS_API lgs_status lgs_map_save(lgs_ctx* ctx, const lgs_map* map, const char* path, const uint64_t* anchors) {
-  if (!ctx || !map) return fail(LGS_EINVAL, "ctx/map is NULL");
-  if (map->dm.deg != 0) return fail(LGS_EINVAL, "LEGOMAP1 stores SH degree 0 colour only");
-  const size_t n = (size_t)map->dm.n, d = (size_t)map->dm.d;
-  std::vector<float> pos(n * 3), rot(n * 4), ls(n * 3), op(n), col(n * 3), ft(n * d);
-  lgs_gaussians g{};
-  g.n = map->dm.n; g.feature_dim = map->dm.d; g.sh_degree = 0;
-  g.positions = pos.data(); g.rotations = rot.data(); g.log_scales = ls.data(); g.opacity_logits = op.data();
-  g.sh = col.data(); g.features = ft.data(); g.memory = LGS_MEM_HOST;
-  LGS_TRY(lgs_map_download(ctx, map, &g));
-  return lgs_map_file_write(path, &g, anchors);
+  return guarded([&]() -> lgs_status {
+    if (!ctx || !map) return fail(LGS_EINVAL, "ctx/map is NULL");
+    if (map->dm.deg != 0) return fail(LGS_EINVAL, "LEGOMAP1 stores SH degree 0 colour only");
+    const size_t n = (size_t)map->dm.n, d = (size_t)map->dm.d;
+    std::vector<float> pos(n * 3), rot(n * 4), ls(n * 3), op(n), col(n * 3), ft(n * d);
+    lgs_gaussians g{};
+    g.n = map->dm.n; g.feature_dim = map->dm.d; g.sh_degree = 0;
+    g.positions = pos.data(); g.rotations = rot.data(); g.log_scales = ls.data(); g.opacity_logits = op.data();
+    g.sh = col.data(); g.features = ft.data(); g.memory = LGS_MEM_HOST;
+    LGS_TRY(lgs_map_download(ctx, map, &g));
+    return lgs_map_file_write(path, &g, anchors);
+  });
 }
 
 }  // extern "C"
@@ -2072,11 +2135,6 @@ void plan_free_marks(lgs_plan* p) {
 
 namespace {
 
-bool prezero_disabled() {  // LGS_PLAN_PREZERO=0: zero rows in the backward (A/B measurements)
-  const char* e = getenv("LGS_PLAN_PREZERO");
-  return e && e[0] == '0';
-}
-
 lgs_status plan_capture(lgs_plan* p) {
   lgs_ctx* ctx = p->ctx;
   if (p->exec) {
@@ -2095,7 +2153,7 @@ lgs_status plan_capture(lgs_plan* p) {
   LGS_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
   ctx->stream = s;
   ctx->capturing = true;
-  ctx->prezero = (p->grads.memory != LGS_MEM_HOST && !p->grads.accumulate && !prezero_disabled()) ? &p->grads : nullptr;
+  ctx->prezero = (p->grads.memory != LGS_MEM_HOST && !p->grads.accumulate) ? &p->grads : nullptr;
   ctx->prezero_forked = false;
   plan_free_marks(p);
   ctx->capture_marks = p->profile ? &p->marks : nullptr;  // event nodes cost ~5 us each per replay

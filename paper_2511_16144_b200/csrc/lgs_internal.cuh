@@ -59,6 +59,8 @@ struct DevCam {
   float fx, fy, cx, cy;
   int W, H, tiles_x, tiles_y;
   float near_plane, dilation, radius_sigma, alpha_clamp, alpha_skip, t_min;
+  // fp64 copies for the backward's 2D -> 3D chain (preprocess_bwd.cu), which runs in fp64
+  double rcw_d[9], tcw_d[3], cc_d[3], fx_d, fy_d;
 };
 
 struct DevMap {
@@ -291,6 +293,66 @@ __device__ __forceinline__ void sh_basis_grad_f32(int deg, float x, float y, flo
   db[15][0] = kShC3[6] * (3.0f * xx - 3.0f * yy); db[15][1] = kShC3[6] * (-6.0f * x * y);
 }
 
+// fp64 basis values and their gradient (the backward's fp64 chain, preprocess_bwd.cu)
+constexpr double kShC1d = 0.4886025119029199;
+__device__ __constant__ static const double kShC2d[5] = {1.0925484305920792, -1.0925484305920792, 0.31539156525252005, -1.0925484305920792,
+                              0.5462742152960396};
+__device__ __constant__ static const double kShC3d[7] = {-0.5900435899266435, 2.890611442640554, -0.4570457994644658, 0.3731763325901154,
+                              -0.4570457994644658, 1.445305721320277, -0.5900435899266435};
+
+__device__ __forceinline__ void sh_basis_f64(int deg, double x, double y, double z, double b[16]) {
+  b[0] = 1.0;
+  if (deg >= 1) {
+    b[1] = -kShC1d * y;
+    b[2] = kShC1d * z;
+    b[3] = -kShC1d * x;
+  }
+  if (deg >= 2) {
+    const double xx = x * x, yy = y * y, zz = z * z;
+    b[4] = kShC2d[0] * (x * y);
+    b[5] = kShC2d[1] * (y * z);
+    b[6] = kShC2d[2] * ((zz + zz) - xx - yy);
+    b[7] = kShC2d[3] * (x * z);
+    b[8] = kShC2d[4] * (xx - yy);
+    if (deg >= 3) {
+      b[9] = kShC3d[0] * y * (3.0 * xx - yy);
+      b[10] = kShC3d[1] * (x * y) * z;
+      b[11] = kShC3d[2] * y * (4.0 * zz - xx - yy);
+      b[12] = kShC3d[3] * z * (2.0 * zz - 3.0 * xx - 3.0 * yy);
+      b[13] = kShC3d[4] * x * (4.0 * zz - xx - yy);
+      b[14] = kShC3d[5] * z * (xx - yy);
+      b[15] = kShC3d[6] * x * (xx - 3.0 * yy);
+    }
+  }
+}
+
+__device__ __forceinline__ void sh_basis_grad_f64(int deg, double x, double y, double z, double db[16][3]) {
+#pragma unroll
+  for (int k = 0; k < 16; ++k) db[k][0] = db[k][1] = db[k][2] = 0.0;
+  if (deg < 1) return;
+  db[1][1] = -kShC1d;
+  db[2][2] = kShC1d;
+  db[3][0] = -kShC1d;
+  if (deg < 2) return;
+  const double xx = x * x, yy = y * y, zz = z * z;
+  db[4][0] = kShC2d[0] * y; db[4][1] = kShC2d[0] * x;
+  db[5][1] = kShC2d[1] * z; db[5][2] = kShC2d[1] * y;
+  db[6][0] = -2.0 * kShC2d[2] * x; db[6][1] = -2.0 * kShC2d[2] * y; db[6][2] = 4.0 * kShC2d[2] * z;
+  db[7][0] = kShC2d[3] * z; db[7][2] = kShC2d[3] * x;
+  db[8][0] = 2.0 * kShC2d[4] * x; db[8][1] = -2.0 * kShC2d[4] * y;
+  if (deg < 3) return;
+  db[9][0] = kShC3d[0] * 6.0 * x * y; db[9][1] = kShC3d[0] * (3.0 * xx - 3.0 * yy);
+  db[10][0] = kShC3d[1] * y * z; db[10][1] = kShC3d[1] * x * z; db[10][2] = kShC3d[1] * x * y;
+  db[11][0] = kShC3d[2] * (-2.0 * x * y); db[11][1] = kShC3d[2] * (4.0 * zz - xx - 3.0 * yy);
+  db[11][2] = kShC3d[2] * 8.0 * y * z;
+  db[12][0] = kShC3d[3] * (-6.0 * x * z); db[12][1] = kShC3d[3] * (-6.0 * y * z);
+  db[12][2] = kShC3d[3] * (6.0 * zz - 3.0 * xx - 3.0 * yy);
+  db[13][0] = kShC3d[4] * (4.0 * zz - 3.0 * xx - yy); db[13][1] = kShC3d[4] * (-2.0 * x * y);
+  db[13][2] = kShC3d[4] * 8.0 * x * z;
+  db[14][0] = kShC3d[5] * 2.0 * x * z; db[14][1] = kShC3d[5] * (-2.0 * y * z); db[14][2] = kShC3d[5] * (xx - yy);
+  db[15][0] = kShC3d[6] * (3.0 * xx - 3.0 * yy); db[15][1] = kShC3d[6] * (-6.0 * x * y);
+}
+
 // Block-staged AoS transfers: a CTA's contiguous [nloc][W] float block (16-byte aligned base) moves
 // between global memory (float4 accesses, coalesced) and per-thread shared-memory rows of stride S
 // (odd S keeps each thread's row in distinct banks).
@@ -373,5 +435,6 @@ __device__ __forceinline__ float fast_rcp(float x) {
 }
 
 constexpr float kNegHalfLog2e = -0.72134752044448170368f;  // -0.5 * log2(e)
+constexpr double kNegHalfLog2eD = -0.72134752044448170368;
 
 }  // namespace lgs

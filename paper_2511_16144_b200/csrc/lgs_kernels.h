@@ -176,11 +176,6 @@ void launch_blend_fused_l1(const DevMap& m, const DevCam& c, const ViewBufs& v, 
                            float* gacc, cudaStream_t s, bool counter_zeroed = false);
 void launch_blend_bwd(const DevMap& m, const DevCam& c, const ViewBufs& v, const TileLists& tl,
                       const PixelState& ps, const BwdIn& in, float* gacc, int slots, cudaStream_t s);
-// Tensor-core variant (blend_bwd_mma.cu), used by launch_blend_bwd when supported.
-bool blend_bwd_mma_supported(int dp);
-void launch_blend_bwd_mma(const DevMap& m, const DevCam& c, const ViewBufs& v, const TileLists& tl,
-                          const PixelState& ps, const BwdIn& in, float* gacc, cudaStream_t s);
-
 // Row-sparse gradient exchange (sparse_reduce.cu): ptr/width = the six MapGradients attributes
 // (feature is [d][N]).
 void launch_rows_scan(float* const ptr[6], const int width[6], int64_t n, uint32_t* list, uint32_t* count,

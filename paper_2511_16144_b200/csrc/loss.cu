@@ -26,6 +26,7 @@
 
 #include "lgs_internal.cuh"
 #include "lgs_kernels.h"
+#include "dev_cache.h"
 
 namespace lgs {
 
@@ -326,16 +327,8 @@ template <int DP>
 int launch_decoder_dp(const LossArgs& a, cudaStream_t s) {
   constexpr int HID = 64;
   const size_t smem = sizeof(float) * ((size_t)HID * DP + HID + ((a.D + 3) & ~3) + (size_t)a.D * HID);
-  static int configured_for = -1;
-  if (configured_for < (int)smem) {
-    if (cudaFuncSetAttribute(decoder_l1_kernel<DP, HID>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-        cudaSuccess)
-      return 2;
-    configured_for = (int)smem;
-  }
-  int sms = 148, dev = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (ensure_dyn_smem(reinterpret_cast<const void*>(decoder_l1_kernel<DP, HID>), (int)smem) != cudaSuccess) return 2;
+  const int sms = device_sm_count();
   const int64_t npix = (int64_t)a.H * a.W;
   const int64_t blocks = std::min<int64_t>((npix + 127) / 128, (int64_t)sms * 8);
   const float gscale = (float)(a.w_feat / ((double)npix * a.D));
@@ -380,8 +373,8 @@ bool decoder_supported(int hidden, int dp, int D) {
 }
 
 int launch_mapping_loss(const LossArgs& a, cudaStream_t s) {
-  static bool win_set = false;
-  if (!win_set) {  // Gaussian window, sigma 1.5, normalized (oracle/loss.py gauss_window)
+  // Gaussian window, sigma 1.5, normalized (oracle/loss.py gauss_window); __constant__ is per device
+  const bool win_ok = once_per_device(reinterpret_cast<const void*>(&c_win), [] {
     double w[2 * kR + 1], sum = 0.0;
     for (int k = 0; k <= 2 * kR; ++k) {
       const double x = k - kR;
@@ -390,9 +383,9 @@ int launch_mapping_loss(const LossArgs& a, cudaStream_t s) {
     }
     float wf[2 * kR + 1];
     for (int k = 0; k <= 2 * kR; ++k) wf[k] = (float)(w[k] / sum);
-    if (cudaMemcpyToSymbol(c_win, wf, sizeof wf) != cudaSuccess) return 2;
-    win_set = true;
-  }
+    return cudaMemcpyToSymbol(c_win, wf, sizeof wf) == cudaSuccess;
+  });
+  if (!win_ok) return 2;
   const dim3 grid((a.W + kTW - 1) / kTW, (a.H + kTH - 1) / kTH);
   const double npos = (double)(a.H - 2 * kR) * (double)(a.W - 2 * kR);
   // d l_total / d S_p = -(1 - w_l1) / 2 / (3 npos)

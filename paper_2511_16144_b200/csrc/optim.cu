@@ -13,6 +13,7 @@
 // [d][N]).  Bytes per Gaussian: parameters + two moments read and written (6 x 304 B at SH3,
 // d = 16) + gradients read (300 B) -- HBM-bound.
 #include <cmath>
+#include <cstdint>
 
 #include "lgs_internal.cuh"
 #include "lgs_kernels.h"
@@ -59,8 +60,16 @@ __global__ void adam_kernel(MapParams p, MapParams m, MapParams v, GradIn g, int
   // rotation: stored x,y,z,w; gradient ordered w,x,y,z (renderer.hpp:61)
   {
     float4 pp = p.rot[i], mm = m.rot[i], vv = v.rot[i];
-    const float4 gr = reinterpret_cast<const float4*>(g.rotation)[i];
-    const float gq[4] = {gr.y, gr.z, gr.w, gr.x};
+    // caller-owned gradient buffers: one float4 load only where the row is 16-byte aligned (a flat
+    // MapGradients buffer puts rotation at float offset 3n)
+    float gq[4];
+    if ((reinterpret_cast<uintptr_t>(g.rotation) & 15) == 0) {
+      const float4 gr = reinterpret_cast<const float4*>(g.rotation)[i];
+      gq[0] = gr.y; gq[1] = gr.z; gq[2] = gr.w; gq[3] = gr.x;
+    } else {
+      const float* gr = g.rotation + i * 4;
+      gq[0] = gr[1]; gq[1] = gr[2]; gq[2] = gr[3]; gq[3] = gr[0];
+    }
     adam4(pp, mm, vv, gq, 4, lr.rotation, a);
     p.rot[i] = pp; m.rot[i] = mm; v.rot[i] = vv;
   }
@@ -92,11 +101,11 @@ __global__ void adam_kernel(MapParams p, MapParams m, MapParams v, GradIn g, int
 
 __global__ void adam_sh_kernel(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
                                const float* __restrict__ g, int64_t e0, int64_t e1, int ks, float lr_dc,
-                               float lr_rest, AdamF a) {
+                               float lr_rest, bool vec, AdamF a) {
   const int64_t q = e0 / 4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // float4 index
   const int64_t e = q * 4;
   if (e >= e1) return;
-  if (e + 4 <= e1 && (e0 & 3) == 0) {
+  if (vec && e + 4 <= e1 && (e0 & 3) == 0) {  // vec: all four arrays 16-byte aligned
     float4 pp = reinterpret_cast<float4*>(p)[q], mm = reinterpret_cast<float4*>(m)[q],
            vv = reinterpret_cast<float4*>(v)[q];
     const float4 gg = reinterpret_cast<const float4*>(g)[q];
@@ -126,7 +135,13 @@ __global__ void unpack_map_kernel(MapParams p, float* __restrict__ pos, float* _
   const float4 po = p.pos_opa[i], r = p.rot[i], s = p.scale[i];
   if (pos) { pos[i * 3 + 0] = po.x; pos[i * 3 + 1] = po.y; pos[i * 3 + 2] = po.z; }
   if (opac) opac[i] = po.w;
-  if (rot) reinterpret_cast<float4*>(rot)[i] = r;  // x,y,z,w storage order (gaussian_map.hpp)
+  if (rot) {  // x,y,z,w storage order (gaussian_map.hpp); caller buffers may be only 4-byte aligned
+    if ((reinterpret_cast<uintptr_t>(rot) & 15) == 0) {
+      reinterpret_cast<float4*>(rot)[i] = r;
+    } else {
+      rot[i * 4 + 0] = r.x; rot[i * 4 + 1] = r.y; rot[i * 4 + 2] = r.z; rot[i * 4 + 3] = r.w;
+    }
+  }
   if (log_s) { log_s[i * 3 + 0] = s.x; log_s[i * 3 + 1] = s.y; log_s[i * 3 + 2] = s.z; }
   if (sh) {
     const int ks = 3 * p.K;
@@ -152,8 +167,10 @@ void launch_adam(const MapParams& p, const MapParams& m, const MapParams& v, con
   const int ks = 3 * p.K;
   const int64_t e0 = g0 * ks, e1 = g1 * ks;
   const int64_t nq = (e1 + 3) / 4 - e0 / 4;
+  const bool vec = ((reinterpret_cast<uintptr_t>(p.sh) | reinterpret_cast<uintptr_t>(m.sh) |
+                    reinterpret_cast<uintptr_t>(v.sh) | reinterpret_cast<uintptr_t>(g.sh)) & 15) == 0;
   adam_sh_kernel<<<(unsigned)((nq + threads - 1) / threads), threads, 0, s>>>(p.sh, m.sh, v.sh, g.sh, e0, e1, ks,
-                                                                           lr.sh_dc, lr.sh_rest, a);
+                                                                           lr.sh_dc, lr.sh_rest, vec, a);
 }
 
 void launch_unpack_map(const MapParams& p, float* pos, float* rot, float* log_s, float* opac, float* sh, float* feat_dn,

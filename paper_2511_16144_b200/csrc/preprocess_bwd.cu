@@ -30,7 +30,7 @@ template <int DEG, int DP, int SLOTS>
 __device__ __forceinline__ void gaussian_bwd(const DevMap& m, const DevCam& c, const ViewBufs& v,
                                              const float* __restrict__ gacc, const GradOut& g, int64_t i,
                                              bool accum, float* my_sh, float (&o_pos)[3], float (&o_rot)[4],
-                                             float (&o_ls)[3], float& o_op, float (&pose)[6]) {
+                                             float (&o_ls)[3], float& o_op, double (&pose)[6]) {
   constexpr int K = (DEG + 1) * (DEG + 1);
   constexpr int KS = 3 * K;
   const int64_t n = m.n;
@@ -44,9 +44,7 @@ __device__ __forceinline__ void gaussian_bwd(const DevMap& m, const DevCam& c, c
   const double2 d23 = *reinterpret_cast<const double2*>(ga + 4);  // conA conB
   const double2 d45 = *reinterpret_cast<const double2*>(ga + 8);  // conC opac
   const float4 zc = *reinterpret_cast<const float4*>(ga + kSlotZ);  // z r g b
-  const float4 a0 = make_float4((float)d01.x, (float)d01.y, (float)d23.x, (float)d23.y);
-  const float4 a1 = make_float4((float)d45.x, (float)d45.y, zc.x, 0.f);
-  const float4 a2 = make_float4(zc.y, zc.z, zc.w, 0.f);
+  // the chain runs in fp64 (near-plane / needle splats: J ~ f/z, conic ~ 1/det, cancellations)
   if (DP > 0 && g.feature) {  // renderer.cpp:262-264, written as [d][N]
 #pragma unroll
     for (int q = 0; q < DP / 4; ++q) {
@@ -57,52 +55,52 @@ __device__ __forceinline__ void gaussian_bwd(const DevMap& m, const DevCam& c, c
         if (q * 4 + e < m.d) store(g.feature, (int64_t)(q * 4 + e) * n + i, f4[e]);
     }
   }
-  o_op = a1.y;
+  o_op = (float)d45.y;
   const float4 po = m.pos_opa[i];
-  const float P[3] = {po.x, po.y, po.z};
-  float gpos[3] = {0.f, 0.f, 0.f};
+  const double P[3] = {po.x, po.y, po.z};
+  double gpos[3] = {0.0, 0.0, 0.0};
 
   // ---- colour -> SH (renderer.cpp:259-261 for K = 1) ------------------------------------
-  const float gc[3] = {a2.x, a2.y, a2.z};
-  if (DEG == 0 || (gc[0] == 0.f && gc[1] == 0.f && gc[2] == 0.f)) {
-    my_sh[0] = gc[0];
-    my_sh[1] = gc[1];
-    my_sh[2] = gc[2];
+  const double gc[3] = {zc.y, zc.z, zc.w};
+  if (DEG == 0 || (gc[0] == 0.0 && gc[1] == 0.0 && gc[2] == 0.0)) {
+    my_sh[0] = (float)gc[0];
+    my_sh[1] = (float)gc[1];
+    my_sh[2] = (float)gc[2];
 #pragma unroll
-    for (int k = 3; k < KS; ++k) my_sh[k] = 0.f;
+    for (int k = 3; k < KS; ++k) my_sh[k] = 0.0;
   } else {
-    const float dr[3] = {P[0] - c.cc[0], P[1] - c.cc[1], P[2] - c.cc[2]};
-    const float nr = sqrtf(dr[0] * dr[0] + dr[1] * dr[1] + dr[2] * dr[2]);
-    const float inr = 1.0f / nr;
-    const float dn[3] = {dr[0] * inr, dr[1] * inr, dr[2] * inr};
-    float b[16];
-    float db[16][3];
-    sh_basis_f32(DEG, dn[0], dn[1], dn[2], b);
-    sh_basis_grad_f32(DEG, dn[0], dn[1], dn[2], db);
-    float gdn[3] = {0.f, 0.f, 0.f};
+    const double dr[3] = {P[0] - c.cc_d[0], P[1] - c.cc_d[1], P[2] - c.cc_d[2]};
+    const double nr = sqrt(dr[0] * dr[0] + dr[1] * dr[1] + dr[2] * dr[2]);
+    const double inr = 1.0 / nr;
+    const double dn[3] = {dr[0] * inr, dr[1] * inr, dr[2] * inr};
+    double b[16];
+    double db[16][3];
+    sh_basis_f64(DEG, dn[0], dn[1], dn[2], b);
+    sh_basis_grad_f64(DEG, dn[0], dn[1], dn[2], db);
+    double gdn[3] = {0.0, 0.0, 0.0};
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      float s = 0.f;
+      double s = 0.0;
 #pragma unroll
       for (int ch = 0; ch < 3; ++ch) {
-        s = fmaf(my_sh[k * 3 + ch], gc[ch], s);  // coefficient (staged), then overwritten by its grad
-        my_sh[k * 3 + ch] = b[k] * gc[ch];
+        s = fma(my_sh[k * 3 + ch], gc[ch], s);  // coefficient (staged), then overwritten by its grad
+        my_sh[k * 3 + ch] = (float)(b[k] * gc[ch]);
       }
-      gdn[0] = fmaf(db[k][0], s, gdn[0]);
-      gdn[1] = fmaf(db[k][1], s, gdn[1]);
-      gdn[2] = fmaf(db[k][2], s, gdn[2]);
+      gdn[0] = fma(db[k][0], s, gdn[0]);
+      gdn[1] = fma(db[k][1], s, gdn[1]);
+      gdn[2] = fma(db[k][2], s, gdn[2]);
     }
-    const float dd = dn[0] * gdn[0] + dn[1] * gdn[1] + dn[2] * gdn[2];
-    float gdir[3];
+    const double dd = dn[0] * gdn[0] + dn[1] * gdn[1] + dn[2] * gdn[2];
+    double gdir[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       gdir[a] = (gdn[a] - dn[a] * dd) * inr;
       gpos[a] += gdir[a];
     }
     if (g.pose) {  // dir = p - c with c' = c + omega x c + nu
-      pose[0] += gdir[1] * c.cc[2] - gdir[2] * c.cc[1];
-      pose[1] += gdir[2] * c.cc[0] - gdir[0] * c.cc[2];
-      pose[2] += gdir[0] * c.cc[1] - gdir[1] * c.cc[0];
+      pose[0] += gdir[1] * c.cc_d[2] - gdir[2] * c.cc_d[1];
+      pose[1] += gdir[2] * c.cc_d[0] - gdir[0] * c.cc_d[2];
+      pose[2] += gdir[0] * c.cc_d[1] - gdir[1] * c.cc_d[0];
       pose[3] -= gdir[0];
       pose[4] -= gdir[1];
       pose[5] -= gdir[2];
@@ -110,32 +108,32 @@ __device__ __forceinline__ void gaussian_bwd(const DevMap& m, const DevCam& c, c
   }
 
   // ---- screen-space -> 3D (renderer.cpp:297-354) ----------------------------------------
-  const float gmu0 = a0.x, gmu1 = a0.y, gA = a0.z, gB = a0.w, gC = a1.x, gz = a1.z;
-  if (gmu0 != 0.f || gmu1 != 0.f || gA != 0.f || gB != 0.f || gC != 0.f || gz != 0.f) {
-    const float* R = c.rcw;
-    float t[3];
+  const double gmu0 = d01.x, gmu1 = d01.y, gA = d23.x, gB = d23.y, gC = d45.x, gz = zc.x;
+  if (gmu0 != 0.0 || gmu1 != 0.0 || gA != 0.0 || gB != 0.0 || gC != 0.0 || gz != 0.0) {
+    const double* R = c.rcw_d;
+    double t[3];
 #pragma unroll
-    for (int r = 0; r < 3; ++r) t[r] = R[r * 3 + 0] * P[0] + R[r * 3 + 1] * P[1] + R[r * 3 + 2] * P[2] + c.tcw[r];
-    const float z = t[2];
+    for (int r = 0; r < 3; ++r) t[r] = R[r * 3 + 0] * P[0] + R[r * 3 + 1] * P[1] + R[r * 3 + 2] * P[2] + c.tcw_d[r];
+    const double z = t[2];
     const float4 qr = m.rot[i];  // x,y,z,w
-    const float qv[4] = {qr.w, qr.x, qr.y, qr.z};
-    const float norm = sqrtf(qv[0] * qv[0] + qv[1] * qv[1] + qv[2] * qv[2] + qv[3] * qv[3]);
-    const float inorm = 1.0f / norm;
-    const float qh[4] = {qv[0] * inorm, qv[1] * inorm, qv[2] * inorm, qv[3] * inorm};
-    const float w = qh[0], x = qh[1], y = qh[2], zq = qh[3];
-    float W[9];  // R_g (rotation of the Gaussian)
+    const double qv[4] = {qr.w, qr.x, qr.y, qr.z};
+    const double norm = sqrt(qv[0] * qv[0] + qv[1] * qv[1] + qv[2] * qv[2] + qv[3] * qv[3]);
+    const double inorm = 1.0 / norm;
+    const double qh[4] = {qv[0] * inorm, qv[1] * inorm, qv[2] * inorm, qv[3] * inorm};
+    const double w = qh[0], x = qh[1], y = qh[2], zq = qh[3];
+    double W[9];  // R_g (rotation of the Gaussian)
     {
-      const float tx = 2 * x, ty = 2 * y, tz = 2 * zq;
-      const float twx = tx * w, twy = ty * w, twz = tz * w, txx = tx * x, txy = ty * x, txz = tz * x;
-      const float tyy = ty * y, tyz = tz * y, tzz = tz * zq;
+      const double tx = 2 * x, ty = 2 * y, tz = 2 * zq;
+      const double twx = tx * w, twy = ty * w, twz = tz * w, txx = tx * x, txy = ty * x, txz = tz * x;
+      const double tyy = ty * y, tyz = tz * y, tzz = tz * zq;
       W[0] = 1 - (tyy + tzz); W[1] = txy - twz;       W[2] = txz + twy;
       W[3] = txy + twz;       W[4] = 1 - (txx + tzz); W[5] = tyz - twx;
       W[6] = txz - twy;       W[7] = tyz + twx;       W[8] = 1 - (txx + tyy);
     }
     const float4 ls = m.scale[i];
-    const float s2[3] = {__expf(2.f * ls.x), __expf(2.f * ls.y), __expf(2.f * ls.z)};
+    const double s2[3] = {exp(2.0 * (double)ls.x), exp(2.0 * ls.y), exp(2.0 * ls.z)};
     // Sigma3 = W S^2 W^T, Sigma_c = R Sigma3 R^T
-    float S3[9], RS[9], Sc[9];
+    double S3[9], RS[9], Sc[9];
 #pragma unroll
     for (int r = 0; r < 3; ++r)
 #pragma unroll
@@ -152,18 +150,18 @@ __device__ __forceinline__ void gaussian_bwd(const DevMap& m, const DevCam& c, c
 #pragma unroll
       for (int cc = 0; cc < 3; ++cc)
         Sc[r * 3 + cc] = RS[r * 3 + 0] * R[cc * 3 + 0] + RS[r * 3 + 1] * R[cc * 3 + 1] + RS[r * 3 + 2] * R[cc * 3 + 2];
-    const float iz = 1.0f / z;
-    const float J[6] = {c.fx * iz, 0.f, -c.fx * t[0] * iz * iz, 0.f, c.fy * iz, -c.fy * t[1] * iz * iz};
+    const double iz = 1.0 / z;
+    const double J[6] = {c.fx_d * iz, 0.0, -c.fx_d * t[0] * iz * iz, 0.0, c.fy_d * iz, -c.fy_d * t[1] * iz * iz};
 
     // g_Sigma2 = -C gC C, C = conic (symmetric), gC = [[gA, gB], [gB, gC]]
     const float4 r1 = v.rec1[i];
-    const float C0 = r1.x, C1 = r1.y, C3 = r1.z;
-    const float cg00 = C0 * gA + C1 * gB, cg01 = C0 * gB + C1 * gC;
-    const float cg10 = C1 * gA + C3 * gB, cg11 = C1 * gB + C3 * gC;
-    const float gs[4] = {-(cg00 * C0 + cg01 * C1), -(cg00 * C1 + cg01 * C3), -(cg10 * C0 + cg11 * C1),
+    const double C0 = r1.x, C1 = r1.y, C3 = r1.z;
+    const double cg00 = C0 * gA + C1 * gB, cg01 = C0 * gB + C1 * gC;
+    const double cg10 = C1 * gA + C3 * gB, cg11 = C1 * gB + C3 * gC;
+    const double gs[4] = {-(cg00 * C0 + cg01 * C1), -(cg00 * C1 + cg01 * C3), -(cg10 * C0 + cg11 * C1),
                          -(cg10 * C1 + cg11 * C3)};
     // g_Sigma_c = J^T gs J
-    float gSc[9];
+    double gSc[9];
 #pragma unroll
     for (int r = 0; r < 3; ++r)
 #pragma unroll
@@ -171,8 +169,8 @@ __device__ __forceinline__ void gaussian_bwd(const DevMap& m, const DevCam& c, c
         gSc[r * 3 + cc] = J[0 * 3 + r] * (gs[0] * J[0 * 3 + cc] + gs[1] * J[1 * 3 + cc]) +
                           J[1 * 3 + r] * (gs[2] * J[0 * 3 + cc] + gs[3] * J[1 * 3 + cc]);
     // g_J = (gs + gs^T) J Sigma_c
-    const float sy[4] = {2.f * gs[0], gs[1] + gs[2], gs[2] + gs[1], 2.f * gs[3]};
-    float JS[6], gJ[6];
+    const double sy[4] = {2.0 * gs[0], gs[1] + gs[2], gs[2] + gs[1], 2.0 * gs[3]};
+    double JS[6], gJ[6];
 #pragma unroll
     for (int r = 0; r < 2; ++r)
 #pragma unroll
@@ -183,24 +181,24 @@ __device__ __forceinline__ void gaussian_bwd(const DevMap& m, const DevCam& c, c
 #pragma unroll
       for (int cc = 0; cc < 3; ++cc) gJ[r * 3 + cc] = sy[r * 2 + 0] * JS[0 * 3 + cc] + sy[r * 2 + 1] * JS[1 * 3 + cc];
     // g_t (renderer.cpp:320-327)
-    float gt[3];
+    double gt[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) gt[a] = J[0 * 3 + a] * gmu0 + J[1 * 3 + a] * gmu1;
-    const float iz2 = iz * iz, iz3 = iz2 * iz;
-    gt[0] += gJ[2] * (-c.fx * iz2);
-    gt[1] += gJ[5] * (-c.fy * iz2);
-    gt[2] += gJ[0] * (-c.fx * iz2) + gJ[2] * (2.f * c.fx * t[0] * iz3) + gJ[4] * (-c.fy * iz2) +
-             gJ[5] * (2.f * c.fy * t[1] * iz3);
+    const double iz2 = iz * iz, iz3 = iz2 * iz;
+    gt[0] += gJ[2] * (-c.fx_d * iz2);
+    gt[1] += gJ[5] * (-c.fy_d * iz2);
+    gt[2] += gJ[0] * (-c.fx_d * iz2) + gJ[2] * (2.0 * c.fx_d * t[0] * iz3) + gJ[4] * (-c.fy_d * iz2) +
+             gJ[5] * (2.0 * c.fy_d * t[1] * iz3);
     gt[2] += gz;
     // g_p = R^T g_t (renderer.cpp:329)
-    float gw[3];
+    double gw[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       gw[a] = R[0 * 3 + a] * gt[0] + R[1 * 3 + a] * gt[1] + R[2 * 3 + a] * gt[2];
       gpos[a] += gw[a];
     }
     // G3 = R^T gSc R (symmetric)
-    float tmp[9], G3[9];
+    double tmp[9], G3[9];
 #pragma unroll
     for (int r = 0; r < 3; ++r)
 #pragma unroll
@@ -212,15 +210,15 @@ __device__ __forceinline__ void gaussian_bwd(const DevMap& m, const DevCam& c, c
       for (int cc = 0; cc < 3; ++cc)
         G3[r * 3 + cc] = tmp[r * 3 + 0] * R[0 * 3 + cc] + tmp[r * 3 + 1] * R[1 * 3 + cc] + tmp[r * 3 + 2] * R[2 * 3 + cc];
     // Y = G3 W; g_logs_a = (W^T G3 W)_aa 2 s2_a; g_rot = (G3 + G3^T) W S^2
-    float Y[9];
+    double Y[9];
 #pragma unroll
     for (int r = 0; r < 3; ++r)
 #pragma unroll
       for (int cc = 0; cc < 3; ++cc)
         Y[r * 3 + cc] = G3[r * 3 + 0] * W[0 * 3 + cc] + G3[r * 3 + 1] * W[1 * 3 + cc] + G3[r * 3 + 2] * W[2 * 3 + cc];
-    float grot[9];
+    double grot[9];
     // (G3 + G3^T) = 2 G3 only if symmetric; use the explicit sum for fidelity
-    float Yt[9];
+    double Yt[9];
 #pragma unroll
     for (int r = 0; r < 3; ++r)
 #pragma unroll
@@ -228,28 +226,28 @@ __device__ __forceinline__ void gaussian_bwd(const DevMap& m, const DevCam& c, c
         Yt[r * 3 + cc] = G3[0 * 3 + r] * W[0 * 3 + cc] + G3[1 * 3 + r] * W[1 * 3 + cc] + G3[2 * 3 + r] * W[2 * 3 + cc];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-      o_ls[a] = (W[0 * 3 + a] * Y[0 * 3 + a] + W[1 * 3 + a] * Y[1 * 3 + a] + W[2 * 3 + a] * Y[2 * 3 + a]) * 2.f * s2[a];
+      o_ls[a] = (float)((W[0 * 3 + a] * Y[0 * 3 + a] + W[1 * 3 + a] * Y[1 * 3 + a] + W[2 * 3 + a] * Y[2 * 3 + a]) * 2.0 * s2[a]);
 #pragma unroll
       for (int r = 0; r < 3; ++r) grot[r * 3 + a] = (Y[r * 3 + a] + Yt[r * 3 + a]) * s2[a];
     }
     // rotation_derivatives (renderer.cpp:28-40), all scaled by 2
-    const float dw[9] = {0, -zq, y, zq, 0, -x, -y, x, 0};
-    const float dxm[9] = {0, y, zq, y, -2 * x, -w, zq, w, -2 * x};
-    const float dym[9] = {-2 * y, x, w, x, 0, zq, -w, zq, -2 * y};
-    const float dzm[9] = {-2 * zq, -w, x, w, -2 * zq, y, x, y, 0};
-    float gq[4] = {0.f, 0.f, 0.f, 0.f};
+    const double dw[9] = {0, -zq, y, zq, 0, -x, -y, x, 0};
+    const double dxm[9] = {0, y, zq, y, -2 * x, -w, zq, w, -2 * x};
+    const double dym[9] = {-2 * y, x, w, x, 0, zq, -w, zq, -2 * y};
+    const double dzm[9] = {-2 * zq, -w, x, w, -2 * zq, y, x, y, 0};
+    double gq[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
     for (int e = 0; e < 9; ++e) {
-      gq[0] = fmaf(grot[e], dw[e], gq[0]);
-      gq[1] = fmaf(grot[e], dxm[e], gq[1]);
-      gq[2] = fmaf(grot[e], dym[e], gq[2]);
-      gq[3] = fmaf(grot[e], dzm[e], gq[3]);
+      gq[0] = fma(grot[e], dw[e], gq[0]);
+      gq[1] = fma(grot[e], dxm[e], gq[1]);
+      gq[2] = fma(grot[e], dym[e], gq[2]);
+      gq[3] = fma(grot[e], dzm[e], gq[3]);
     }
 #pragma unroll
-    for (int a = 0; a < 4; ++a) gq[a] *= 2.f;
-    const float dot = qh[0] * gq[0] + qh[1] * gq[1] + qh[2] * gq[2] + qh[3] * gq[3];
+    for (int a = 0; a < 4; ++a) gq[a] *= 2.0;
+    const double dot = qh[0] * gq[0] + qh[1] * gq[1] + qh[2] * gq[2] + qh[3] * gq[3];
 #pragma unroll
-    for (int a = 0; a < 4; ++a) o_rot[a] = (gq[a] - qh[a] * dot) * inorm;
+    for (int a = 0; a < 4; ++a) o_rot[a] = (float)((gq[a] - qh[a] * dot) * inorm);
 
     if (g.pose) {
       // t' = R_cw (p - omega x p - nu) + t_cw: g_omega += g_w x p, g_nu -= g_w
@@ -260,7 +258,7 @@ __device__ __forceinline__ void gaussian_bwd(const DevMap& m, const DevCam& c, c
       pose[4] -= gw[1];
       pose[5] -= gw[2];
       // Sigma3' = (I - [omega]x) Sigma3 (I + [omega]x): A = Sigma3 G3 - G3 Sigma3, vee(A - A^T)
-      float A1[9], A2[9];
+      double A1[9], A2[9];
 #pragma unroll
       for (int r = 0; r < 3; ++r)
 #pragma unroll
@@ -274,7 +272,7 @@ __device__ __forceinline__ void gaussian_bwd(const DevMap& m, const DevCam& c, c
     }
   }
 #pragma unroll
-  for (int a = 0; a < 3; ++a) o_pos[a] = gpos[a];
+  for (int a = 0; a < 3; ++a) o_pos[a] = (float)gpos[a];
 }
 
 template <int DEG, int DP, int SLOTS>
@@ -320,7 +318,7 @@ __global__ void __launch_bounds__(kPbThreads) preprocess_bwd_kernel(DevMap m, De
   if (DEG > 0) stage_rows_in<KS, SS, kPbThreads>(s_sh, m.sh + i0 * KS, nloc);
   __syncthreads();
   float* my_sh = s_sh + tid * SS;
-  float pose[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  double pose[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
   if (i < n) {
     float o_pos[3] = {0.f, 0.f, 0.f}, o_rot[4] = {0.f, 0.f, 0.f, 0.f}, o_ls[3] = {0.f, 0.f, 0.f};
     float o_op = 0.f;
@@ -369,11 +367,11 @@ __global__ void __launch_bounds__(kPbThreads) preprocess_bwd_kernel(DevMap m, De
   if (g.sh) stage_rows_out<KS, SS, kPbThreads>(s_sh, g.sh + i0 * KS, nloc, accum);
 
   if (g.pose) {  // block reduction of the pose gradient, one double atomic per value per block
-    __shared__ float s_pose[kPbThreads / 32][6];
+    __shared__ double s_pose[kPbThreads / 32][6];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
     for (int a = 0; a < 6; ++a) {
-      float p = pose[a];
+      double p = pose[a];
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) p += __shfl_xor_sync(0xffffffffu, p, off);
       if (lane == 0) s_pose[wid][a] = p;
@@ -381,7 +379,7 @@ __global__ void __launch_bounds__(kPbThreads) preprocess_bwd_kernel(DevMap m, De
     __syncthreads();
     if (threadIdx.x < 6) {
       double s = 0.0;
-      for (int w2 = 0; w2 < (int)(blockDim.x >> 5); ++w2) s += (double)s_pose[w2][threadIdx.x];
+      for (int w2 = 0; w2 < (int)(blockDim.x >> 5); ++w2) s += s_pose[w2][threadIdx.x];
       if (s != 0.0) atomicAdd(g.pose + threadIdx.x, s);
     }
   }
@@ -447,7 +445,7 @@ __global__ void __launch_bounds__(kPbThreads) preprocess_bwd_active_kernel(DevMa
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   float* my_sh = s_sh + tid * SS;
   const bool accum = g.accumulate != 0;
-  float pose[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  double pose[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
 
   // compact this block's active rows into s_q (ascending), one 16-byte flag load per thread
   const int64_t f0 = (int64_t)blockIdx.x * kActRange + (int64_t)tid * kActFlags;
@@ -509,10 +507,10 @@ __global__ void __launch_bounds__(kPbThreads) preprocess_bwd_active_kernel(DevMa
       for (int q = 0; q < KS; ++q) put(g.sh, i * KS + q, my_sh[q]);
   }
   if (g.pose) {  // block reduction of the pose gradient, one double atomic per value per block
-    __shared__ float s_pose[kPbThreads / 32][6];
+    __shared__ double s_pose[kPbThreads / 32][6];
 #pragma unroll
     for (int a = 0; a < 6; ++a) {
-      float p = pose[a];
+      double p = pose[a];
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) p += __shfl_xor_sync(0xffffffffu, p, off);
       if (lane == 0) s_pose[wid][a] = p;
@@ -520,7 +518,7 @@ __global__ void __launch_bounds__(kPbThreads) preprocess_bwd_active_kernel(DevMa
     __syncthreads();
     if (threadIdx.x < 6) {
       double s = 0.0;
-      for (int w2 = 0; w2 < kPbThreads / 32; ++w2) s += (double)s_pose[w2][threadIdx.x];
+      for (int w2 = 0; w2 < kPbThreads / 32; ++w2) s += s_pose[w2][threadIdx.x];
       if (s != 0.0) atomicAdd(g.pose + threadIdx.x, s);
     }
   }

@@ -93,7 +93,8 @@ class Context:
     the context a private non-blocking stream (independent host threads rendering concurrently,
     the reference's "concurrent renders between map mutations" contract)."""
 
-    def __init__(self, device: int = 0, stream=None, full_lists: bool = False):
+    def __init__(self, device: int = 0, stream=None, full_lists: bool = False, radix_depth_order: bool = False,
+                 fused_eager: bool = False):
         L = _lib.load()
         if stream == "own":
             stream = None
@@ -108,6 +109,11 @@ class Context:
         self.device = device
         if full_lists:  # complete (tile, Gaussian) lists instead of the depth-layered binning
             check(L.lgs_ctx_set_full_tile_lists(h, 1))
+        # context options of include/lgs.h (LGS_OPT_*): cross-check depth order, profiling-only fusion
+        if radix_depth_order:
+            check(L.lgs_ctx_set_option(h, _lib.LGS_OPT_RADIX_DEPTH_ORDER, 1))
+        if fused_eager:
+            check(L.lgs_ctx_set_option(h, _lib.LGS_OPT_FUSED_EAGER, 1))
 
     def synchronize(self):
         check(_lib.load().lgs_ctx_synchronize(self.h))

@@ -3,10 +3,11 @@
 proj/tests/test_renderer.cpp:14-36 (small_camera, splat_at, logit) and
 proj/tests/gradcheck.hpp:31-78 (make_grad_scene) + :80-148 (scene_loss,
 rel_err, gradcheck_scene).  Draws use the reference Rng (random.hpp) through
-the oracle.  C++ leaves constructor-argument evaluation order unspecified, so
-multi-draw constructors (Vec3(u(), u(), u())) are drawn left to right here;
-the quantities the reference pins are properties of the scene distribution
-(bounds, invariance, finite-difference agreement), not of particular values.
+the oracle.  C++ leaves constructor-argument evaluation order unspecified; the
+reference built here with g++ (oracle/_ref, tests/test_reference_build.py)
+evaluates them right to left, so multi-draw constructors (Vec3(u(), u(), u()),
+Quat(n(), n(), n(), n())) are drawn last argument first, which makes
+make_grad_scene reproduce the reference's seed-101 scene value for value.
 """
 import math
 
@@ -73,13 +74,16 @@ def make_grad_scene(o, n_gaussians, image_size, feat_dim, seed, sh_degree=0):
                cx=(image_size - 1) / 2.0, cy=(image_size - 1) / 2.0, width=image_size, height=image_size)
     cfg = dict(radius_sigma=1e3, alpha_skip=1e-12, transmittance_min=0.0)  # :41-43
     for _ in range(n_gaussians):
+        # constructor arguments in GCC's right-to-left evaluation order (see the module docstring)
         z = rng.uniform(0.8, 2.2)
-        p = [rng.uniform(-0.3, 0.3) * z, rng.uniform(-0.3, 0.3) * z, z]
-        q = np.array([rng.normal(), rng.normal(), rng.normal(), rng.normal()])  # Quat(w,x,y,z)
-        q /= np.linalg.norm(q)
-        ls = [math.log(rng.uniform(0.04, 0.12)) for _ in range(3)]
+        py_ = rng.uniform(-0.3, 0.3) * z
+        p = [rng.uniform(-0.3, 0.3) * z, py_, z]
+        q = np.array([rng.normal(), rng.normal(), rng.normal(), rng.normal()])[::-1].copy()  # Quat(w,x,y,z)
+        # q.normalize(): the norm summed in Eigen's storage order (x, y, z, w)
+        q /= math.sqrt(((q[1] * q[1] + q[2] * q[2]) + q[3] * q[3]) + q[0] * q[0])
+        ls = [math.log(rng.uniform(0.04, 0.12)) for _ in range(3)][::-1]
         ol = rng.uniform(0.5, 2.2)
-        col = [rng.uniform(0.05, 0.95) for _ in range(3)]
+        col = [rng.uniform(0.05, 0.95) for _ in range(3)][::-1]
         f = [0.5 * rng.normal() for _ in range(feat_dim)]
         mb.insert(p, q, ls, ol, col, f)
     scene = mb.scene()

@@ -424,12 +424,8 @@ def test_depth_order_ties_and_big_buckets(oracle):
     op = oracle.preprocess_f32(scene, cam)
     okeys, ovals, oranges = oracle.bin_f32(op, cam["width"], cam["height"])
     assert np.array_equal(keys, okeys) and np.array_equal(vals, ovals) and np.array_equal(ranges, oranges)
-    os.environ["LGS_DEPTH_SORT"] = "cub"
-    try:
-        ref = R.render(dev_scene(scene), cam, ctx=R.Context(0, full_lists=True))
-        torch.cuda.synchronize()
-    finally:
-        del os.environ["LGS_DEPTH_SORT"]
+    ref = R.render(dev_scene(scene), cam, ctx=R.Context(0, full_lists=True, radix_depth_order=True))
+    torch.cuda.synchronize()
     for a, b in zip(out.tile_keys(), ref.tile_keys()):
         assert np.array_equal(a, b)
     assert torch.equal(out.rgb, ref.rgb)

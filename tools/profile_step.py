@@ -23,7 +23,8 @@ def main():
     d = scene["feat"].shape[0]
     tg = scenes.make_targets(cam, d, info["depth_range"], 7)
     stream = torch.cuda.Stream()
-    ctx = R.Context(0, stream=stream.cuda_stream)
+    # FUSED=1: the fused forward+backward kernel of the captured step, uncaptured (LGS_OPT_FUSED_EAGER)
+    ctx = R.Context(0, stream=stream.cuda_stream, fused_eager=os.environ.get("FUSED", "0") == "1")
     with torch.cuda.stream(stream):
         dmap = R.DeviceMap({k: torch.from_numpy(v).cuda() for k, v in scene.items()}, ctx)
         dtg = {k: torch.from_numpy(v).cuda() for k, v in tg.items()}
