@@ -42,7 +42,11 @@ def parse():
     p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--config", default="c1_500k")
+    p.add_argument("--config", default="c1_500k",
+                   help="c0 | c1 | c1_500k (headline) | c2 | c4 (one view of the 16-view arc) | c3")
+    p.add_argument("--view", type=int, default=None, help="camera of the config (default 0; c4: 8, mid-arc)")
+    p.add_argument("--multiview", choices=["auto", "none", "c3", "c4"], default="auto",
+                   help="also time a multi-view mapping batch (BASELINE configs 3/4); auto: c3 with c1_500k")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-mapping", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -198,6 +202,16 @@ def dist_env():
     return rank, world, local
 
 
+def workload_metric(cam, n, d):
+    """BASELINE metric string for a workload (the headline's is METRIC)."""
+    ng = f"{n // 1000}k" if n < 1_000_000 else f"{n / 1e6:g}M"
+    return f"fwd+bwd render iters/s, {cam['width']}x{cam['height']} RGB+depth+{d}-D feat, {ng} Gaussians"
+
+
+def default_view(config):
+    return 8 if config == "c4" else 0
+
+
 def rank_camera(base_cam, rank, world):
     """Rank r renders the headline view translated by 2 cm per rank (same work, distinct views)."""
     import numpy as np
@@ -247,7 +261,8 @@ def run_ours(args):
     _lib.load()  # fails loudly without the CUDA library: there is no fallback
 
     scene, cams, info = scenes.make_config(args.config)
-    cam = rank_camera(cams[0], rank, world)
+    view = default_view(args.config) if args.view is None else args.view
+    cam = rank_camera(cams[view], rank, world)
     d = scene["feat"].shape[0]
     K = scene["sh"].shape[1]
     n = scene["pos"].shape[0]
@@ -279,11 +294,19 @@ def run_ours(args):
     def enqueue():
         plan.run()
         if comm is not None:
-            # sum over ranks of the 500k x 75 fp32 gradient, exchanging only the rows some view
-            # reached (a few thousand with the depth-layered binning; lgs_allreduce_grads_sparse
-            # falls back to the dense NCCL all-reduce when they are not sparse)
-            comm.all_reduce_grads_sparse(dmap, grads)
+            # the view's step must be final before the exchange (a re-run after a tile-list overflow
+            # would otherwise leave this rank's sum stale on every rank): wait, then enqueue the sum
+            # over ranks of the 500k x 75 fp32 gradient exchanging only the rows some view reached
+            # (lgs_allreduce_grads_sparse_async: capacity-sized row blocks, no host wait inside;
+            # dense NCCL all-reduce when the rows are not sparse)
+            plan.sync()
+            comm.all_reduce_grads_sparse_async(dmap, grads)
         return None
+
+    def finish():
+        plan.sync()  # the step's pose gradient has reached the host (re-captures on overflow)
+        if comm is not None:
+            comm.wait_grads_sparse(dmap, grads)  # exact re-run if a rank outgrew the capacity
 
     def step():
         """Eager (uncaptured) step through the same API: used for the per-phase profile."""
@@ -297,7 +320,7 @@ def run_ours(args):
     with torch.cuda.stream(stream):
         for _ in range(max(args.warmup, 3)):
             enqueue()
-            plan.sync()
+            finish()
     torch.cuda.synchronize()
 
     # ---- timed region --------------------------------------------------------------------------
@@ -319,7 +342,7 @@ def run_ours(args):
             out = enqueue()
             evs[k][1].record(stream)  # on the stream before the host waits: host wake-up is outside
             host_ms.append(1e3 * (time.perf_counter() - h0))
-            plan.sync()  # the step's pose gradient has reached the host (re-captures on overflow)
+            finish()
             if k % every == every - 1:
                 clk.sample()
         torch.cuda.synchronize()
@@ -345,7 +368,7 @@ def run_ours(args):
         for k in range(n_prof):
             flush.fill_(float(k))
             enqueue()
-            plan.sync()
+            finish()
             for name, v in plan.phase_times().items():
                 acc_ph[name] = acc_ph.get(name, 0.0) + v
     phases = {k: (v / n_prof, 1) for k, v in acc_ph.items()}
@@ -429,12 +452,16 @@ def run_ours(args):
         "phases": phase_rows,
     }
 
+    data = {"c0": "configs[0]", "c1": "configs[1]", "c1_500k": "configs[1] distributions at 500k",
+            "c2": "configs[2] (200 blobs, Replica-shaped)", "c3": "configs[3] map",
+            "c4": f"configs[4] (70% in a 0.5 m ball), view {view} of the 16-view arc"}[args.config]
     result = {
-        "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "metric": METRIC if args.config == "c1_500k" else workload_metric(cam, n, d), "value": round(value, 3),
+        "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": round(ms_max, 4), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic (seeded; BASELINE configs[1] distributions at 500k; no dataset ships with the reference)",
-        "config": {"workload": args.config, "image": f"{cam['width']}x{cam['height']}", "gaussians": n,
+        "data": f"synthetic (seeded; BASELINE {data}; no dataset ships with the reference)",
+        "config": {"workload": args.config, "view": view, "image": f"{cam['width']}x{cam['height']}", "gaussians": n,
                    "sh_degree": int(math.isqrt(K) - 1), "feature_dim": d, "views_per_gpu_per_step": 1,
                    "loss": "L1 rgb+depth+feat (fused)", "pose_grad": True,
                    "parallelism": (f"views over {world} GPU(s), fp32 row-sparse grad all-reduce by liblgs.so (NCCL)"
@@ -459,6 +486,10 @@ def run_ours(args):
         # the same with the whole map copied every step (LGS_MEM_HOST): 150 MB more H2D per step
         full = run_e2e(args, scene, cam, tg, R, local, mapped=False)
         result["e2e"]["whole_map_copied"] = {k: full[k] for k in ("value", "ms_per_step", "h2d_bytes_per_step")}
+
+    mv = args.multiview if args.multiview != "auto" else ("c3" if args.config == "c1_500k" else "none")
+    if mv != "none":
+        result["multiview_batch"] = run_multiview(args, mv, local, world, rank, flush)
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         result["cpu_baseline"] = cpu_baseline(scene, cam, tg, args)
@@ -543,6 +574,92 @@ def run_mapping_step(args, dmap, cam, ctx, stream, flush, info, hbm_peak, fp32, 
     return {"metric": "mapping iterations/s (render + loss + backward + Adam), same map and view", "value":
             round(1000.0 / ms, 3), "unit": "it/s", "ms_per_step": round(ms, 4), "steps": steps, "teacher_dim": D,
             "decoder": f"{dmap.d}->64->{D}", "phases": rows}
+
+
+def run_multiview(args, name, local, world, rank, flush):
+    """BASELINE configs[3] (c3: 500k Gaussians, 8 views on a 1 m circle) or configs[4] (c4: 3M, 16 views
+    on a 2 m arc) as one data-parallel mapping batch: the views are split over the ranks (longest
+    processing time first on their pair counts -- deterministic, so every rank derives the same
+    split), each rank runs its views as captured steps accumulating into one gradient buffer
+    (lgs_plan, accumulate), and the batch gradient is summed over ranks by the row-sparse exchange
+    (lgs_allreduce_grads_sparse_async).  T(N) = max over ranks of the batch step (device events);
+    value = views per second of the whole batch.  The view total is fixed (strong scaling)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2511_16144_b200 import multiview
+    from paper_2511_16144_b200 import renderer as R
+    from paper_2511_16144_b200 import scenes
+
+    scene, cams, info = scenes.make_config(name)
+    n, d, K = scene["pos"].shape[0], scene["feat"].shape[0], scene["sh"].shape[1]
+    stream = torch.cuda.Stream(device=local)
+    ctx = R.Context(local, stream=stream.cuda_stream)
+    with torch.cuda.stream(stream):
+        dmap = R.DeviceMap({k: torch.from_numpy(v).cuda(local) for k, v in scene.items()}, ctx)
+        tgs = [{k: torch.from_numpy(v).cuda(local) for k, v in
+                scenes.make_targets(c, d, info["depth_range"], 50 + v).items()} for v, c in enumerate(cams)]
+        grads = R.alloc_grads(n, d, K, device=local)
+        costs = [R.render(dmap, c, targets=tgs[v], ctx=ctx).stats()["pairs"] for v, c in enumerate(cams)]
+    del scene
+    mine = multiview.assign_views(len(cams), world, rank, costs)
+    comm = multiview.NativeComm(ctx) if world > 1 else None
+    poses = [torch.zeros(6, dtype=torch.float32, pin_memory=True) for _ in mine]
+    with torch.cuda.stream(stream):
+        plans = [R.Plan(dmap, cams[v], tgs[v], grads, pose_out=poses[i], accumulate=i > 0) for i, v in enumerate(mine)]
+
+    def step():
+        for p in plans:
+            p.run()
+        if comm is not None:
+            for p in plans:  # every view final before the exchange (an overflowed view re-runs here)
+                p.sync()
+            comm.all_reduce_grads_sparse_async(dmap, grads)
+
+    def finish():
+        for p in plans:
+            p.sync()
+        return comm.wait_grads_sparse(dmap, grads) if comm is not None else 0
+
+    with torch.cuda.stream(stream):
+        for _ in range(max(args.warmup, 3)):
+            step()
+            finish()
+    torch.cuda.synchronize()
+    steps = max(5, min(args.steps, 20))
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    rows = []
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(stream):
+        for k in range(steps):
+            flush.fill_(float(k))
+            evs[k][0].record(stream)
+            step()
+            evs[k][1].record(stream)
+            rows.append(finish())
+    torch.cuda.synchronize()
+    per = [a.elapsed_time(b) for a, b in evs]
+    ms = sum(per) / len(per)
+    t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        comm.close()
+    ms_max = float(t.item())
+    recaptures = sum(p.recaptures for p in plans)
+    del plans
+    return {"metric": f"views/s of the {len(cams)}-view mapping batch (fwd+bwd per view + gradient sum over ranks)",
+            "value": round(len(cams) * 1000.0 / ms_max, 3), "unit": "views/s", "n_gpus": world,
+            "ms_per_step": round(ms_max, 4), "steps": steps, "scaling": "strong",
+            "config": {"workload": name, "views": len(cams), "gaussians": n, "image": f"{cams[0]['width']}x"
+                       f"{cams[0]['height']}", "views_this_rank": mine, "pairs_per_view": [int(c) for c in costs],
+                       "exchange": "row-sparse all-gather (lgs_allreduce_grads_sparse_async)" if world > 1 else
+                       "none (1 GPU: the views accumulate into one buffer)",
+                       "l2": "512 MiB L2 flush before every timed step"},
+            "rows_max": int(max(rows)) if rows else 0, "plan_recaptures": int(recaptures),
+            "per_step_ms": [round(x, 4) for x in per]}
 
 
 def pinned_like(a):
@@ -642,50 +759,86 @@ def cpu_threads():
         return os.cpu_count() or 1
 
 
+def _ref_build():
+    """oracle/_ref/liblgs_ref.so: the reference's own renderer.cpp / geometry.cpp, unmodified, compiled by
+    oracle/Makefile (None where it was not built: then the oracle A port stands in)."""
+    try:
+        from oracle import ref
+        return ref if ref.available() else None
+    except Exception:  # noqa: BLE001 -- any load failure means "not available"
+        return None
+
+
+def _sh0(scene):
+    """The reference renders colours (SH degree 0): higher bands are dropped for its arm -- the
+    per-pixel work (the blend and its reverse pass) is the same, the colour is a per-Gaussian constant."""
+    import numpy as np
+    return dict(scene, sh=np.ascontiguousarray(scene["sh"][:, :1, :]))
+
+
 def reference_step(scene, cam, tg, threads):
-    """One full fwd+bwd of the reference algorithm (oracle A: fp64, global sort, per-pixel
-    contributor lists -- renderer.cpp:94-356) with the L1 cotangents, on `threads` row bands."""
+    """Seconds of one full fwd+bwd of the headline image on `threads` host threads (row bands) with
+    the L1 cotangents: the reference itself (lego::render + lego::render_backward per band,
+    ref_bridge.cpp ref_bench_bands) when oracle/_ref is built, else oracle A (the fp64 port of
+    renderer.cpp:94-356).  Returns (seconds, kind)."""
+    ref = _ref_build()
+    if ref is not None:
+        secs, _ = ref.bench_bands(_sh0(scene), cam, tg, threads, 1)
+        return secs, "reference"
     from oracle import oracle as orc
     t0 = time.perf_counter()
-    out = orc.fwd_bwd_bands(scene, cam, None, None, None, threads=threads, targets=tg)
-    return time.perf_counter() - t0, out
+    orc.fwd_bwd_bands(scene, cam, None, None, None, threads=threads, targets=tg)
+    return time.perf_counter() - t0, "port"
+
+
+def _sample_text(kind, threads, scene):
+    what = ("the reference's own renderer.cpp (oracle/_ref, unmodified, compiled here against a "
+            "self-written Eigen subset)" if kind == "reference" else "oracle A (fp64 port of renderer.cpp)")
+    sh = "" if scene["sh"].shape[1] == 1 else "; the reference has colours only (SH degree 0): its arm renders the DC band"
+    return f"{what}, full image fwd+bwd with L1 cotangents on {threads} row-band thread(s){sh}"
 
 
 def cpu_baseline(scene, cam, tg, args):
     threads = cpu_threads()
-    secs, _ = reference_step(scene, cam, tg, threads)
-    return {"value": round(1.0 / secs, 4), "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"1 full fwd+bwd step of the headline workload (oracle A, fp64 reference algorithm) on "
-                      f"{threads} row bands, {secs:.2f} s"}
+    secs, kind = reference_step(scene, cam, tg, threads)
+    res = {"value": round(1.0 / secs, 4), "unit": UNIT, "cores": threads, "kind": kind,
+           "sample": f"1 step ({secs:.2f} s): " + _sample_text(kind, threads, scene)}
+    if args.config == "c1_500k":  # single core, as the reference itself runs (~13 s here)
+        one, _ = reference_step(scene, cam, tg, 1)
+        res["single_core"] = {"value": round(1.0 / one, 4), "cores": 1, "sample": f"1 step ({one:.2f} s) on 1 thread"}
+    return res
 
 
 def run_reference(args):
-    """--impl reference: the reference's CPU algorithm (oracle A port; the reference itself cannot
-    be built here) on all host cores, same metric / config."""
+    """--impl reference: the reference's own CPU renderer (oracle/_ref) -- else the oracle A port -- on
+    all host cores (row bands), same metric / config.  Under torchrun only rank 0 runs."""
     rank, world, local = dist_env()
     if rank != 0:
         return
     from paper_2511_16144_b200 import scenes
     scene, cams, info = scenes.make_config(args.config)
-    cam = cams[0]
+    view = default_view(args.config) if args.view is None else args.view
+    cam = cams[view]
     d = scene["feat"].shape[0]
+    n = int(scene["pos"].shape[0])
     tg = scenes.make_targets(cam, d, info["depth_range"], 7)
     threads = cpu_threads()
     warm = 1  # one untimed step (page-in, allocator); each CPU step is seconds long
     for _ in range(warm):
-        reference_step(scene, cam, tg, threads)
+        kind = reference_step(scene, cam, tg, threads)[1]
     steps = max(1, min(args.steps, 5))
     times = [reference_step(scene, cam, tg, threads)[0] for _ in range(steps)]
     ms = 1e3 * sum(times) / len(times)
     v = 1000.0 / ms
-    res = {"metric": METRIC, "value": round(v, 4), "unit": UNIT, "n_gpus": world, "steps": steps, "warmup": warm,
+    res = {"metric": METRIC if args.config == "c1_500k" else workload_metric(cam, n, d), "value": round(v, 4),
+           "unit": UNIT, "n_gpus": world, "steps": steps, "warmup": warm,
            "ms_per_step": round(ms, 2), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
            "dtype": "f64", "data": "synthetic (seeded, same as --impl ours)", "impl": "reference",
-           "config": {"workload": args.config, "image": f"{cam['width']}x{cam['height']}",
-                      "gaussians": int(scene['pos'].shape[0])},
-           "cpu_baseline": {"value": round(v, 4), "unit": UNIT, "cores": threads, "kind": "port",
-                            "sample": f"{steps} full fwd+bwd steps (after {warm} warm-up) of oracle A on {threads} "
-                                      f"row bands; requested --steps {args.steps} capped at 5 to bound CPU time"},
+           "config": {"workload": args.config, "view": view, "image": f"{cam['width']}x{cam['height']}",
+                      "gaussians": n},
+           "cpu_baseline": {"value": round(v, 4), "unit": UNIT, "cores": threads, "kind": kind,
+                            "sample": f"{steps} steps (after {warm} warm-up), requested --steps {args.steps} capped "
+                                      f"at 5 to bound CPU time: " + _sample_text(kind, threads, scene)},
            "e2e": {"value": round(v, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(res), flush=True)
 

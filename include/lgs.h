@@ -365,7 +365,10 @@ LGS_API lgs_status lgs_map_save(lgs_ctx* ctx, const lgs_map* map, const char* pa
  * captured once into a CUDA graph and replayed with one launch (no host work inside the step).
  * The tile-list capacity comes from an eager warm-up step; lgs_plan_sync waits for the replay and
  * re-captures + re-runs it if the pair count outgrew the capacity.  Map contents, targets and
- * gradient buffers may change between replays (same pointers); a new camera re-captures. */
+ * gradient buffers may change between replays (same pointers); a new camera re-captures.
+ * grads->accumulate = 1: each replay adds its gradients into the buffers (the later views of a
+ * multi-view batch; an overflowed replay adds nothing before lgs_plan_sync re-runs it).  The eager
+ * warm-up step inside lgs_plan_create also writes (adds into) the gradient buffers. */
 LGS_API lgs_status lgs_plan_create(lgs_ctx* ctx, lgs_map* map, const lgs_camera* cam, const lgs_render_config* cfg,
                                    const lgs_l1_targets* targets, const lgs_images* images /* device or NULL */,
                                    lgs_map_grads* grads, float* pose_grad, lgs_plan** out);
@@ -381,6 +384,8 @@ LGS_API lgs_status lgs_plan_elapsed_ms(const lgs_plan* plan, float* ms);
 LGS_API lgs_status lgs_plan_set_profiling(lgs_ctx* ctx, lgs_plan* plan, int32_t on);
 LGS_API lgs_status lgs_plan_phase_times(const lgs_plan* plan, double* ms);
 LGS_API int64_t lgs_plan_launches(const lgs_plan* plan);
+/* Times lgs_plan_sync re-captured and re-ran the step (tile lists outgrew the capacity). */
+LGS_API int64_t lgs_plan_recaptures(const lgs_plan* plan);
 LGS_API lgs_status lgs_plan_destroy(lgs_plan* plan);
 
 /* ---- multi-view mapping batches --------------------------------------------
@@ -407,6 +412,32 @@ LGS_API lgs_status lgs_allreduce_f32(lgs_ctx* ctx, float* buf, int64_t count);
  * per-rank row count, -1 after a dense fallback. */
 LGS_API lgs_status lgs_allreduce_grads_sparse(lgs_ctx* ctx, const lgs_map* map, lgs_map_grads* grads,
                                               int64_t* rows_max);
+/* The same sum without a host wait inside the step: the row-record blocks are sized by a capacity
+ * learnt from earlier exchanges (the first call runs the exact form and sets it to 1.25 x the rows
+ * seen).  _async enqueues everything on the context's stream; _wait (after the step) returns once
+ * it has completed.  If some rank listed more rows than the capacity, the async exchange changed
+ * nothing (the kernels see every rank's count) and _wait re-runs it exactly with a larger capacity,
+ * so the result is always the sum over ranks.  *rows_max: the largest per-rank row count. */
+LGS_API lgs_status lgs_allreduce_grads_sparse_async(lgs_ctx* ctx, const lgs_map* map, lgs_map_grads* grads);
+LGS_API lgs_status lgs_allreduce_grads_sparse_wait(lgs_ctx* ctx, const lgs_map* map, lgs_map_grads* grads,
+                                                   int64_t* rows_max);
+
+/* Host waits inside a collective (the sparse exchange's count all-gather) give up after `ms`
+ * milliseconds (default 300000) or as soon as NCCL reports an asynchronous error: the communicator
+ * is then aborted (ncclCommAbort releases the peers blocked in the collective with an error), the
+ * context's communicator is dropped and the call returns LGS_ECUDA. */
+LGS_API lgs_status lgs_comm_set_timeout(lgs_ctx* ctx, int64_t ms);
+
+/* Debug/parity: the row-sparse exchange of lgs_allreduce_grads_sparse -- the same scan, pack and
+ * apply kernels and the same host logic -- over `world` ranks simulated in one process on this
+ * context's GPU (the all-gathers become device copies).  grads[r] are rank r's dense device
+ * buffers; on return every one holds the sum over ranks.  LGS_EINVAL when the rows are not sparse
+ * enough (the real exchange would take the dense all-reduce).  cap > 0 runs the capacity-speculative
+ * form of lgs_allreduce_grads_sparse_async (record blocks of `cap` rows, no host wait): when a rank
+ * has more rows, *overflowed = 1 and every buffer is left as it was. */
+LGS_API lgs_status lgs_debug_sparse_reduce_simulated(lgs_ctx* ctx, const lgs_map* map, lgs_map_grads* const* grads,
+                                                     int32_t world, int64_t cap, int64_t* rows_max,
+                                                     int32_t* overflowed);
 
 #ifdef __cplusplus
 }

@@ -48,6 +48,9 @@ def lib():
                                      C.POINTER(OrcCamera), C.POINTER(OrcConfig), _dp, _dp, _dp]
         L.ref_gradcheck.restype = C.c_double
         L.ref_gradcheck.argtypes = [C.c_int, C.c_int, C.c_int, C.c_uint64]
+        L.ref_bench_bands.restype = C.c_double
+        L.ref_bench_bands.argtypes = [C.POINTER(OrcMap), C.POINTER(OrcCamera), C.POINTER(OrcConfig), _dp, _dp, _dp,
+                                      C.c_int, C.c_int, _dp]
         L.ref_bench.restype = C.c_double
         L.ref_bench.argtypes = [C.POINTER(OrcMap), C.POINTER(OrcCamera), C.POINTER(OrcConfig), _dp, _dp, _dp, C.c_int,
                                 C.c_int, _dp]
@@ -170,4 +173,18 @@ def bench(scene, cam, targets, threads, iters, cfg=None):
     t = [np.ascontiguousarray(targets[k], dtype=np.float64) for k in ("rgb", "depth", "feat")]
     loss = np.zeros(1)
     sec = lib().ref_bench(C.byref(m), C.byref(c), C.byref(cfg), *(_ptr(x) for x in t), threads, iters, _ptr(loss))
+    return sec, float(loss[0])
+
+
+def bench_bands(scene, cam, targets, threads, iters, cfg=None):
+    """Seconds per step of the full image's fwd+bwd split into `threads` row bands, each band the
+    reference's own lego::render + render_backward (ref_bridge.cpp ref_bench_bands); and the L1 loss."""
+    _sh0(scene)
+    m, s = _scene64(scene)
+    c = make_camera(cam)
+    cfg = cfg if isinstance(cfg, OrcConfig) else make_config(**(cfg or {}))
+    t = [np.ascontiguousarray(targets[k], dtype=np.float64) for k in ("rgb", "depth", "feat")]
+    loss = np.zeros(1)
+    sec = lib().ref_bench_bands(C.byref(m), C.byref(c), C.byref(cfg), *(_ptr(x) for x in t), threads, iters,
+                                _ptr(loss))
     return sec, float(loss[0])

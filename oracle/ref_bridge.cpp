@@ -10,6 +10,7 @@
 // Flat layouts are oracle A's (lgs_oracle.c orc_map / orc_camera / orc_config): positions [N][3],
 // rotations [N][4] (x,y,z,w), log-scales [N][3], opacity logits [N], colours [N][3] (SH degree 0:
 // the reference has no higher bands), features [d][N]; images HWC; gradient rotations (w,x,y,z).
+#include <algorithm>
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -67,20 +68,29 @@ struct RefCamera {
   int32_t width, height;
 };
 
+// The map through its mutable SoA accessors (gaussian_map.hpp:57-68).  GaussianMap::insert would
+// conservativeResize the feature matrix once per Gaussian (quadratic in N); render and
+// render_backward read only these arrays.  Rotations are stored as given (already unit).
 lego::GaussianMap build_map(const RefMap* m) {
   lego::GaussianMap map(m->d);
-  for (int64_t i = 0; i < m->n; ++i) {
-    lego::LanguageGaussian g;
-    g.position = lego::Vec3(m->pos[i * 3], m->pos[i * 3 + 1], m->pos[i * 3 + 2]);
-    g.rotation = lego::Quat(m->rot[i * 4 + 3], m->rot[i * 4], m->rot[i * 4 + 1], m->rot[i * 4 + 2]);
-    g.log_scale = lego::Vec3(m->log_s[i * 3], m->log_s[i * 3 + 1], m->log_s[i * 3 + 2]);
-    g.opacity_logit = m->opac[i];
-    const int K = (m->sh_degree + 1) * (m->sh_degree + 1);
-    g.color = lego::Vec3(m->sh[i * K * 3], m->sh[i * K * 3 + 1], m->sh[i * K * 3 + 2]);
-    g.feature = Eigen::VectorXd(m->d);
-    for (int c = 0; c < m->d; ++c) g.feature[c] = m->feat[c * m->n + i];
-    map.insert(g, 0);
+  const auto n = static_cast<std::size_t>(m->n);
+  const int K = (m->sh_degree + 1) * (m->sh_degree + 1);
+  map.positions().reserve(n);
+  map.rotations().reserve(n);
+  map.log_scales().reserve(n);
+  map.opacity_logits().reserve(n);
+  map.colors().reserve(n);
+  for (std::size_t i = 0; i < n; ++i) {
+    map.positions().push_back(lego::Vec3(m->pos[i * 3], m->pos[i * 3 + 1], m->pos[i * 3 + 2]));
+    map.rotations().push_back(lego::Quat(m->rot[i * 4 + 3], m->rot[i * 4], m->rot[i * 4 + 1], m->rot[i * 4 + 2]));
+    map.log_scales().push_back(lego::Vec3(m->log_s[i * 3], m->log_s[i * 3 + 1], m->log_s[i * 3 + 2]));
+    map.opacity_logits().push_back(m->opac[i]);
+    map.colors().push_back(lego::Vec3(m->sh[i * K * 3], m->sh[i * K * 3 + 1], m->sh[i * K * 3 + 2]));
   }
+  Eigen::MatrixXd f(static_cast<Eigen::Index>(n), m->d);
+  for (int c = 0; c < m->d; ++c)
+    for (std::size_t i = 0; i < n; ++i) f(static_cast<Eigen::Index>(i), c) = m->feat[(std::size_t)c * n + i];
+  map.features() = f;
   return map;
 }
 
@@ -294,4 +304,65 @@ REF_API double ref_bench(const RefMap* m, const RefCamera* cam, const RefConfig*
   const double sec = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   if (loss) *loss = losses[0];
   return sec;
+}
+
+// CPU arm with all host threads: one step = the full image's fwd + bwd split into `threads` row
+// bands, each thread running the reference's own lego::render + lego::render_backward on its band
+// (the band camera is the full camera with cy shifted and the band's height: the reference culls
+// against the band, keeps the global (depth, index) order, and its pixels are exactly the full
+// image's rows; gradients are sums over pixels, so the bands' gradients sum to the full one).
+// This is the per-pixel data parallelism SPEC.md:298-299 allows.  Returns wall seconds per step;
+// *loss = the image's L1 loss of the last step.
+REF_API double ref_bench_bands(const RefMap* m, const RefCamera* cam, const RefConfig* cfg, const double* trgb,
+                               const double* tdepth, const double* tfeat, int threads, int iters, double* loss) {
+  const auto map = build_map(m);
+  const auto pose = to_pose(cam);
+  const auto rc = to_cfg(cfg);
+  const int H = cam->height, W = cam->width, d = m->d;
+  threads = std::max(1, std::min(threads, H));
+  std::vector<double> band_loss((size_t)threads, 0.0);
+  const double inv_rgb = 1.0 / (3.0 * W * H), inv_d = 1.0 / ((double)W * H), inv_f = d ? 1.0 / ((double)d * W * H) : 0;
+  auto sgn = [](double x) { return x > 0 ? 1.0 : (x < 0 ? -1.0 : 0.0); };
+  auto band = [&](int t) {
+    const int y0 = (int)((int64_t)H * t / threads), y1 = (int)((int64_t)H * (t + 1) / threads);
+    lego::CameraIntrinsics k = to_k(cam);
+    k.cy = cam->cy - y0;
+    k.height = y1 - y0;
+    if (k.height <= 0) return;
+    const auto out = lego::render(map, pose, k, rc);
+    lego::ImageD gr(k.height, W, 3), gd(k.height, W, 1), gf(k.height, W, d);
+    double l = 0.0;
+    const size_t off = (size_t)y0 * W;
+    for (size_t i = 0; i < gr.data.size(); ++i) {
+      const double df = out.rgb.data[i] - trgb[off * 3 + i];
+      gr.data[i] = sgn(df) * inv_rgb;
+      l += std::abs(df) * inv_rgb;
+    }
+    for (size_t i = 0; i < gd.data.size(); ++i) {
+      const double df = out.depth.data[i] - tdepth[off + i];
+      gd.data[i] = sgn(df) * inv_d;
+      l += std::abs(df) * inv_d;
+    }
+    for (size_t i = 0; i < gf.data.size(); ++i) {
+      const double df = out.feat.data[i] - tfeat[off * d + i];
+      gf.data[i] = sgn(df) * inv_f;
+      l += std::abs(df) * inv_f;
+    }
+    const auto g = lego::render_backward(map, out, gr, gd, gf);
+    band_loss[(size_t)t] = l + 0.0 * g.opacity_logit.size();
+  };
+  const auto t0 = std::chrono::steady_clock::now();
+  for (int it = 0; it < iters; ++it) {
+    std::vector<std::thread> pool;
+    for (int t = 1; t < threads; ++t) pool.emplace_back(band, t);
+    band(0);
+    for (auto& th : pool) th.join();
+  }
+  const double sec = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  if (loss) {
+    double s = 0.0;
+    for (double v : band_loss) s += v;
+    *loss = s;
+  }
+  return sec / std::max(1, iters);
 }

@@ -149,6 +149,7 @@ SIGNATURES = [
     ("lgs_plan_set_profiling", C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
     ("lgs_plan_phase_times", C.c_int, [C.c_void_p, C.POINTER(C.c_double)]),
     ("lgs_plan_launches", C.c_int64, [C.c_void_p]),
+    ("lgs_plan_recaptures", C.c_int64, [C.c_void_p]),
     ("lgs_plan_destroy", C.c_int, [C.c_void_p]),
     ("lgs_comm_unique_id", C.c_int, [C.POINTER(LgsCommId)]),
     ("lgs_comm_init", C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.POINTER(LgsCommId)]),
@@ -156,6 +157,13 @@ SIGNATURES = [
     ("lgs_allreduce_grads", C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(LgsMapGrads)]),
     ("lgs_allreduce_f32", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64]),
     ("lgs_allreduce_grads_sparse", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_int64)]),
+    ("lgs_comm_set_timeout", C.c_int, [C.c_void_p, C.c_int64]),
+    ("lgs_debug_sparse_reduce_simulated", C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.POINTER(LgsMapGrads)),
+                                                   C.c_int32, C.c_int64, C.POINTER(C.c_int64),
+                                                   C.POINTER(C.c_int32)]),
+    ("lgs_allreduce_grads_sparse_async", C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(LgsMapGrads)]),
+    ("lgs_allreduce_grads_sparse_wait", C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(LgsMapGrads),
+                                                 C.POINTER(C.c_int64)]),
 ]
 
 LGS_PHASE_COUNT = 13

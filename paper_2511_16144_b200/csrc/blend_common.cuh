@@ -90,6 +90,24 @@ __device__ __forceinline__ void frame_dq(const float4& fa, const float4& fb, flo
   dq_ddy = kTwoOverHalfLog2e * fmaf(S, fa.w, T * fb.y);
 }
 
+// ---- paired FP32 (sm_100 FFMA2 / FMUL2 / FADD2: two lanes of IEEE fp32 per instruction) ---------
+// A thread's two vertically stacked pixels (PPT = 2) are evaluated as one float2; every paired
+// operation is the per-lane IEEE operation of the scalar code, so the results are bit-identical.
+__device__ __forceinline__ float2 bc2(float x) { return make_float2(x, x); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+
+// frame_alpha for the pixel pair (ex, ey.x) and (ex, ey.y)
+__device__ __forceinline__ float2 frame_alpha2(const float4& fa, const float4& fb, float opacity, float2 ex2,
+                                               float2 ey2, float2& S, float2& T, float2& G) {
+  S = fma2(ex2, bc2(fa.z), fma2(ey2, bc2(fa.w), bc2(fa.x)));
+  T = fma2(ex2, bc2(fb.x), fma2(ey2, bc2(fb.y), bc2(fa.y)));
+  const float2 p = fma2(S, S, mul2(T, T));
+  G = make_float2(fast_exp2(-p.x), fast_exp2(-p.y));
+  return mul2(bc2(opacity), G);
+}
+
 // inclusive pixel rect test (renderer.cpp:131-136, intersected with the alpha box, preprocess.cu)
 __device__ __forceinline__ bool in_rect(uint2 r, int px, int py) {
   return px >= (int)(r.x & 0xffffu) && px <= (int)(r.x >> 16) && py >= (int)(r.y & 0xffffu) &&

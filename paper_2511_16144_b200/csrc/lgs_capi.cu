@@ -8,7 +8,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -17,6 +19,7 @@
 #include <new>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/lgs.h"
@@ -115,6 +118,13 @@ struct lgs_ctx {
   // multi-view gradient all-reduce (lgs_comm_*): one NCCL communicator per context / GPU
   ncclComm_t comm = nullptr;
   int32_t comm_world = 0, comm_rank = 0;
+  int64_t comm_timeout_ms = 300000;  // lgs_comm_set_timeout: host waits on a collective
+  // capacity-speculative sparse exchange (lgs_allreduce_grads_sparse_async / _wait)
+  int64_t sparse_cap = 0;          // rows per rank of the record blocks (0: not learnt yet)
+  uint32_t* sparse_ovf_dev = nullptr;   // [0] overflow flag, [1] largest row count
+  uint32_t* sparse_ovf_host = nullptr;  // pinned copy
+  cudaEvent_t sparse_done = nullptr;
+  bool sparse_pending = false;
   // phase profiling
   bool profiling = false;
   std::vector<PhaseMark> marks;
@@ -124,6 +134,18 @@ struct lgs_ctx {
 };
 
 namespace {
+
+// No C++ exception crosses the ABI: allocation failures of host containers become LGS_ENOMEM.
+template <class F>
+lgs_status guarded(F&& f) {
+  try {
+    return f();
+  } catch (const std::bad_alloc&) {
+    return fail(LGS_ENOMEM, "host allocation failed");
+  } catch (const std::exception& e) {
+    return fail(LGS_EIO, "%s", e.what());
+  }
+}
 
 // Conditional graph nodes inside a plan capture (CUDA 12.4+): cond_create makes the handle a
 // kernel sets with cudaGraphSetConditional, cond_begin adds an IF node after everything captured so
@@ -280,6 +302,9 @@ void ctx_release(lgs_ctx* ctx) {
     if (ctx->host_u32) cudaFreeHost(ctx->host_u32);
     if (ctx->dev_u32) cudaFree(ctx->dev_u32);
     if (ctx->pairs_ready) cudaEventDestroy(ctx->pairs_ready);
+    if (ctx->sparse_ovf_dev) cudaFree(ctx->sparse_ovf_dev);
+    if (ctx->sparse_ovf_host) cudaFreeHost(ctx->sparse_ovf_host);
+    if (ctx->sparse_done) cudaEventDestroy(ctx->sparse_done);
     for (auto& m : ctx->marks) {
       cudaEventDestroy(m.a);
       cudaEventDestroy(m.b);
@@ -1638,6 +1663,8 @@ LGS_API lgs_status lgs_comm_destroy(lgs_ctx* ctx) {
   if (nc) LGS_NCCL(nc->CommDestroy(ctx->comm));
   ctx->comm = nullptr;
   ctx->comm_world = ctx->comm_rank = 0;
+  ctx->sparse_cap = 0;
+  ctx->sparse_pending = false;
   return LGS_OK;
 }
 
@@ -1683,53 +1710,258 @@ LGS_API lgs_status lgs_allreduce_grads(lgs_ctx* ctx, const lgs_map* map, lgs_map
   LGS_NCCL(nc->GroupEnd());
   return LGS_OK;
 }
+}  // extern "C"
+
+namespace {
+
+// Device scratch of one call, released (stream-ordered) on every exit path.
+struct Scratch {
+  lgs_ctx* ctx;
+  std::vector<uint8_t*> bufs;
+  explicit Scratch(lgs_ctx* c) : ctx(c) {}
+  template <typename T>
+  lgs_status get(T** out, size_t count) {
+    LGS_TRY(dalloc(ctx, out, count));
+    bufs.push_back(reinterpret_cast<uint8_t*>(*out));
+    return LGS_OK;
+  }
+  ~Scratch() {
+    for (uint8_t*& b : bufs) dfree(ctx, b);
+  }
+};
+
+// The all-gather steps of the row-sparse exchange.  NcclGather: one rank per process over the
+// context's communicator; SimGather: `world` ranks simulated in one process (device copies), the
+// single-GPU test of the same kernels and host logic (lgs_debug_sparse_reduce_simulated).
+struct Gather {
+  virtual ~Gather() = default;
+  // send[r] (bytes each) of every local rank r -> recv[r] = all ranks' sends back to back
+  virtual lgs_status all_gather(const void* const* send, void* const* recv, size_t bytes) = 0;
+  // host wait for the stream (the counts), bounded and watching for collective failures
+  virtual lgs_status wait() = 0;
+};
+
+struct NcclGather final : Gather {
+  lgs_ctx* ctx;
+  const NcclApi* nc;
+  cudaEvent_t until = nullptr;  // wait(): for this event (else the whole stream)
+  NcclGather(lgs_ctx* c, const NcclApi* n) : ctx(c), nc(n) {}
+  lgs_status abort(const char* why) {
+    nc->CommAbort(ctx->comm);  // peers blocked in the collective are released with an error
+    ctx->comm = nullptr;
+    ctx->comm_world = ctx->comm_rank = 0;
+    return fail(LGS_ECUDA, "gradient exchange aborted (communicator destroyed): %s", why);
+  }
+  lgs_status all_gather(const void* const* send, void* const* recv, size_t bytes) override {
+    const ncclResult_t r = nc->AllGather(send[0], recv[0], bytes, ncclUint8, ctx->comm, ctx->stream);
+    if (r != ncclSuccess) return abort(nc->GetErrorString(r));
+    return LGS_OK;
+  }
+  lgs_status wait() override {
+    const auto t0 = std::chrono::steady_clock::now();
+    for (;;) {
+      const cudaError_t q = until ? cudaEventQuery(until) : cudaStreamQuery(ctx->stream);
+      if (q == cudaSuccess) return LGS_OK;
+      if (q != cudaErrorNotReady) return fail(LGS_ECUDA, "%s", cudaGetErrorString(q));
+      ncclResult_t ae = ncclSuccess;
+      nc->CommGetAsyncError(ctx->comm, &ae);
+      if (ae != ncclSuccess && ae != ncclInProgress) return abort(nc->GetErrorString(ae));
+      const auto ms = std::chrono::duration_cast<std::chrono::milliseconds>(std::chrono::steady_clock::now() - t0);
+      if (ms.count() > ctx->comm_timeout_ms) return abort("timed out waiting for the other ranks");
+      std::this_thread::yield();
+    }
+  }
+};
+
+struct SimGather final : Gather {
+  lgs_ctx* ctx;
+  int world;
+  SimGather(lgs_ctx* c, int w) : ctx(c), world(w) {}
+  lgs_status all_gather(const void* const* send, void* const* recv, size_t bytes) override {
+    for (int r = 0; r < world; ++r)
+      for (int q = 0; q < world; ++q)
+        LGS_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(recv[r]) + (size_t)q * bytes, send[q], bytes,
+                                 cudaMemcpyDeviceToDevice, ctx->stream));
+    return LGS_OK;
+  }
+  lgs_status wait() override {
+    LGS_CUDA(cudaStreamSynchronize(ctx->stream));
+    return LGS_OK;
+  }
+};
+
+// The exchange for the local ranks' gradient buffers (one in production, `world` when simulated).
+// cap == 0: exact -- the counts are read on the host (one wait) and size the record blocks;
+// *dense = true when the rows are not sparse enough and nothing was exchanged (the caller then
+// runs the dense all-reduce).  cap > 0: capacity-speculative, no host wait -- record blocks of
+// `cap` rows; if some rank has more rows nothing is applied (every rank keeps its own gradient)
+// and ovf[0] (device) is set; ovf[1] = the largest row count.
+lgs_status sparse_exchange(lgs_ctx* ctx, const lgs_map* map, lgs_map_grads* const* grads, int nlocal, int world,
+                           Gather& g, int64_t* rows_max, bool* dense, int64_t cap = 0, uint32_t* ovf = nullptr) {
+  cudaStream_t s = ctx->stream;
+  const int64_t n = map->dm.n;
+  const int width[6] = {3, 4, 3, 1, 3 * map->dm.K, map->dm.d};
+  *dense = false;
+  if (rows_max) *rows_max = 0;
+  std::vector<std::array<float*, 6>> ptr((size_t)nlocal);
+  for (int r = 0; r < nlocal; ++r)
+    ptr[r] = {grads[r]->position, grads[r]->rotation, grads[r]->log_scale, grads[r]->opacity_logit, grads[r]->sh,
+              grads[r]->feature};
+  const int R = rows_values(width, ptr[0].data());
+  if (n == 0 || R == 0) return LGS_OK;
+  Scratch sc(ctx);
+  std::vector<uint32_t*> list((size_t)nlocal), cnt((size_t)nlocal);
+  for (int r = 0; r < nlocal; ++r) {
+    LGS_TRY(sc.get(&list[r], (size_t)n));
+    LGS_TRY(sc.get(&cnt[r], (size_t)world + 1));  // [0] own count, [1 ..] all ranks'
+    launch_rows_scan(ptr[r].data(), width, n, list[r], cnt[r], s);
+  }
+  {
+    std::vector<const void*> snd((size_t)nlocal);
+    std::vector<void*> rcv((size_t)nlocal);
+    for (int r = 0; r < nlocal; ++r) {
+      snd[r] = cnt[r];
+      rcv[r] = cnt[r] + 1;
+    }
+    LGS_TRY(g.all_gather(snd.data(), rcv.data(), sizeof(uint32_t)));
+  }
+  int64_t maxc = cap;
+  if (cap <= 0) {
+    std::vector<uint32_t> counts((size_t)world);
+    LGS_CUDA(cudaMemcpyAsync(counts.data(), cnt[0] + 1, sizeof(uint32_t) * world, cudaMemcpyDeviceToHost, s));
+    LGS_TRY(g.wait());
+    maxc = 0;
+    for (uint32_t c : counts) maxc = std::max<int64_t>(maxc, c);
+    if (rows_max) *rows_max = maxc;
+    if (maxc == 0) return LGS_OK;
+    if (maxc * (int64_t)world * (R + 1) * 2 >= n * (int64_t)R) {  // not sparse enough: dense sum
+      *dense = true;
+      if (rows_max) *rows_max = -1;
+      return LGS_OK;
+    }
+  } else if (ovf) {
+    launch_rows_overflow(cnt[0] + 1, world, cap, ovf, s);
+  }
+  std::vector<float*> send((size_t)nlocal), recv((size_t)nlocal);
+  for (int r = 0; r < nlocal; ++r) {
+    LGS_TRY(sc.get(&send[r], (size_t)maxc * (R + 1)));
+    LGS_TRY(sc.get(&recv[r], (size_t)world * maxc * (R + 1)));
+    launch_rows_pack(ptr[r].data(), width, n, list[r], cnt[r], maxc, send[r], s);
+  }
+  {
+    std::vector<const void*> snd(send.begin(), send.end());
+    std::vector<void*> rcv(recv.begin(), recv.end());
+    LGS_TRY(g.all_gather(snd.data(), rcv.data(), sizeof(float) * (size_t)maxc * (R + 1)));
+  }
+  for (int r = 0; r < nlocal; ++r) launch_rows_apply(ptr[r].data(), width, n, recv[r], cnt[r] + 1, world, maxc, s);
+  LGS_CUDA(cudaGetLastError());
+  return LGS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
 LGS_API lgs_status lgs_allreduce_grads_sparse(lgs_ctx* ctx, const lgs_map* map, lgs_map_grads* grads,
                                               int64_t* rows_max) {
   if (!ctx || !map || !grads) return fail(LGS_EINVAL, "ctx/map/grads is NULL");
   if (grads->memory != LGS_MEM_DEVICE) return fail(LGS_EINVAL, "all-reduce needs device gradient buffers");
   if (!ctx->comm) return fail(LGS_EINVAL, "lgs_comm_init was not called on this context");
   LGS_CUDA(cudaSetDevice(ctx->device));
-  const NcclApi* nc = nccl_api(nullptr);
-  cudaStream_t s = ctx->stream;
-  const int64_t n = map->dm.n;
-  const int world = ctx->comm_world;
-  float* ptr[6] = {grads->position, grads->rotation, grads->log_scale, grads->opacity_logit, grads->sh,
-                   grads->feature};
-  const int width[6] = {3, 4, 3, 1, 3 * map->dm.K, map->dm.d};
-  const int R = rows_values(width, ptr);
-  if (rows_max) *rows_max = 0;
-  if (n == 0 || R == 0) return LGS_OK;
-  uint32_t *list = nullptr, *cnt = nullptr;
-  LGS_TRY(dalloc(ctx, &list, (size_t)n));
-  LGS_TRY(dalloc(ctx, &cnt, (size_t)world + 1));  // [0] own count, [1 ..] all ranks'
-  launch_rows_scan(ptr, width, n, list, cnt, s);
-  LGS_NCCL(nc->AllGather(cnt, cnt + 1, 1, ncclUint32, ctx->comm, s));
-  std::vector<uint32_t> counts((size_t)world);
-  LGS_CUDA(cudaMemcpyAsync(counts.data(), cnt + 1, sizeof(uint32_t) * world, cudaMemcpyDeviceToHost, s));
-  LGS_CUDA(cudaStreamSynchronize(s));
-  int64_t maxc = 0;
-  for (uint32_t c : counts) maxc = std::max<int64_t>(maxc, c);
-  if (rows_max) *rows_max = maxc;
-  lgs_status st = LGS_OK;
-  if (maxc > 0) {
-    if (maxc * (int64_t)world * (R + 1) * 2 >= n * (int64_t)R) {  // not sparse enough: dense sum
-      st = lgs_allreduce_grads(ctx, map, grads);
-      if (rows_max) *rows_max = -1;
-    } else {
-      float *send = nullptr, *recv = nullptr;
-      LGS_TRY(dalloc(ctx, &send, (size_t)maxc * (R + 1)));
-      LGS_TRY(dalloc(ctx, &recv, (size_t)world * maxc * (R + 1)));
-      launch_rows_pack(ptr, width, n, list, cnt, maxc, send, s);
-      LGS_NCCL(nc->AllGather(send, recv, (size_t)maxc * (R + 1), ncclFloat32, ctx->comm, s));
-      launch_rows_apply(ptr, width, n, recv, cnt + 1, world, maxc, s);
-      dfree(ctx, send);
-      dfree(ctx, recv);
+  return guarded([&]() -> lgs_status {
+    NcclGather g(ctx, nccl_api(nullptr));
+    bool dense = false;
+    LGS_TRY(sparse_exchange(ctx, map, &grads, 1, ctx->comm_world, g, rows_max, &dense));
+    return dense ? lgs_allreduce_grads(ctx, map, grads) : LGS_OK;
+  });
+}
+
+LGS_API lgs_status lgs_allreduce_grads_sparse_async(lgs_ctx* ctx, const lgs_map* map, lgs_map_grads* grads) {
+  if (!ctx || !map || !grads) return fail(LGS_EINVAL, "ctx/map/grads is NULL");
+  if (grads->memory != LGS_MEM_DEVICE) return fail(LGS_EINVAL, "all-reduce needs device gradient buffers");
+  if (!ctx->comm) return fail(LGS_EINVAL, "lgs_comm_init was not called on this context");
+  if (ctx->sparse_pending) return fail(LGS_EINVAL, "a sparse exchange is pending: call lgs_allreduce_grads_sparse_wait");
+  LGS_CUDA(cudaSetDevice(ctx->device));
+  return guarded([&]() -> lgs_status {
+    NcclGather g(ctx, nccl_api(nullptr));
+    bool dense = false;
+    int64_t rows = 0;
+    if (ctx->sparse_cap <= 0) {  // first exchange: exact sizes (one host wait), then the capacity
+      LGS_TRY(sparse_exchange(ctx, map, &grads, 1, ctx->comm_world, g, &rows, &dense));
+      if (dense) return lgs_allreduce_grads(ctx, map, grads);
+      ctx->sparse_cap = std::max<int64_t>(256, rows + rows / 4);
+      return LGS_OK;
     }
-  }
-  dfree(ctx, list);
-  dfree(ctx, cnt);
-  LGS_CUDA(cudaGetLastError());
-  return st;
+    if (!ctx->sparse_ovf_dev) {
+      LGS_CUDA(cudaMalloc(&ctx->sparse_ovf_dev, 2 * sizeof(uint32_t)));
+      LGS_CUDA(cudaMallocHost(&ctx->sparse_ovf_host, 2 * sizeof(uint32_t)));
+      LGS_CUDA(cudaEventCreateWithFlags(&ctx->sparse_done, cudaEventDisableTiming));
+    }
+    LGS_TRY(sparse_exchange(ctx, map, &grads, 1, ctx->comm_world, g, nullptr, &dense, ctx->sparse_cap,
+                            ctx->sparse_ovf_dev));
+    LGS_CUDA(cudaMemcpyAsync(ctx->sparse_ovf_host, ctx->sparse_ovf_dev, 2 * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                             ctx->stream));
+    LGS_CUDA(cudaEventRecord(ctx->sparse_done, ctx->stream));
+    ctx->sparse_pending = true;
+    return LGS_OK;
+  });
+}
+
+LGS_API lgs_status lgs_allreduce_grads_sparse_wait(lgs_ctx* ctx, const lgs_map* map, lgs_map_grads* grads,
+                                                   int64_t* rows_max) {
+  if (!ctx || !map || !grads) return fail(LGS_EINVAL, "ctx/map/grads is NULL");
+  if (rows_max) *rows_max = 0;
+  if (!ctx->sparse_pending) return LGS_OK;
+  LGS_CUDA(cudaSetDevice(ctx->device));
+  return guarded([&]() -> lgs_status {
+    NcclGather g(ctx, nccl_api(nullptr));
+    ctx->sparse_pending = false;
+    g.until = ctx->sparse_done;
+    LGS_TRY(g.wait());  // bounded, aborts the communicator on a peer failure
+    g.until = nullptr;
+    const int64_t mx = ctx->sparse_ovf_host[1];
+    if (rows_max) *rows_max = mx;
+    if (ctx->sparse_ovf_host[0] == 0) return LGS_OK;
+    // some rank outgrew the capacity: nothing was applied; exact exchange now, larger capacity
+    ctx->sparse_cap = std::max<int64_t>(ctx->sparse_cap * 2, mx + mx / 4);
+    bool dense = false;
+    LGS_TRY(sparse_exchange(ctx, map, &grads, 1, ctx->comm_world, g, rows_max, &dense));
+    return dense ? lgs_allreduce_grads(ctx, map, grads) : LGS_OK;
+  });
+}
+
+LGS_API lgs_status lgs_debug_sparse_reduce_simulated(lgs_ctx* ctx, const lgs_map* map, lgs_map_grads* const* grads,
+                                                     int32_t world, int64_t cap, int64_t* rows_max,
+                                                     int32_t* overflowed) {
+  if (!ctx || !map || !grads || world < 1 || cap < 0) return fail(LGS_EINVAL, "bad simulated exchange arguments");
+  for (int r = 0; r < world; ++r)
+    if (!grads[r] || grads[r]->memory != LGS_MEM_DEVICE) return fail(LGS_EINVAL, "device gradient buffers needed");
+  LGS_CUDA(cudaSetDevice(ctx->device));
+  if (overflowed) *overflowed = 0;
+  return guarded([&]() -> lgs_status {
+    SimGather g(ctx, world);
+    bool dense = false;
+    uint32_t* ovf = nullptr;
+    if (cap > 0) LGS_TRY(dalloc(ctx, &ovf, 2));
+    const lgs_status st = sparse_exchange(ctx, map, grads, world, world, g, rows_max, &dense, cap, ovf);
+    if (ovf) {
+      uint32_t h[2] = {0, 0};
+      cudaMemcpyAsync(h, ovf, sizeof h, cudaMemcpyDeviceToHost, ctx->stream);
+      cudaStreamSynchronize(ctx->stream);
+      dfree(ctx, ovf);
+      if (overflowed) *overflowed = (int32_t)h[0];
+      if (rows_max) *rows_max = h[1];
+    }
+    LGS_TRY(st);
+    if (dense) return fail(LGS_EINVAL, "rows not sparse: the exchange would take the dense all-reduce");
+    return LGS_OK;
+  });
+}
+
+LGS_API lgs_status lgs_comm_set_timeout(lgs_ctx* ctx, int64_t ms) {
+  if (!ctx || ms <= 0) return fail(LGS_EINVAL, "bad timeout");
+  ctx->comm_timeout_ms = ms;
+  return LGS_OK;
 }
 #undef LGS_NCCL
 
@@ -1926,18 +2158,6 @@ lgs_status check_map_file_size(std::ifstream& is, const char* path, const MapFil
   return fail(LGS_EIO, "map file truncated reading %s", what[f]);
 }
 
-// No C++ exception crosses the ABI: allocation failures of host containers become LGS_ENOMEM.
-template <class F>
-lgs_status guarded(F&& f) {
-  try {
-    return f();
-  } catch (const std::bad_alloc&) {
-    return fail(LGS_ENOMEM, "host allocation failed");
-  } catch (const std::exception& e) {
-    return fail(LGS_EIO, "%s", e.what());
-  }
-}
-
 }  // namespace
 
 extern "C" {
@@ -2121,6 +2341,9 @@ struct lgs_plan {
   bool profile = false;
   int64_t cap = 0;
   int64_t launches_per_run = 0;
+  int64_t recaptures = 0;
+  uint32_t* host_pairs = nullptr;  // pinned: this plan's pair count, written by every replay (each
+                                   // plan its own slot: several plans may share a context)
 };
 
 namespace {
@@ -2157,6 +2380,8 @@ lgs_status plan_capture(lgs_plan* p) {
   ctx->prezero_forked = false;
   plan_free_marks(p);
   ctx->capture_marks = p->profile ? &p->marks : nullptr;  // event nodes cost ~5 us each per replay
+  uint32_t* const saved_host = ctx->host_u32;
+  ctx->host_u32 = p->host_pairs;  // the replay's pair-count readback lands in the plan's own slot
   lgs_status st = LGS_OK;
   lgs_saved* tape = nullptr;
   if (cudaEventRecordWithFlags(p->ev0, s, cudaEventRecordExternal) != cudaSuccess)
@@ -2180,6 +2405,7 @@ lgs_status plan_capture(lgs_plan* p) {
   ctx->capturing = false;
   ctx->capture_marks = nullptr;
   ctx->stream = saved;
+  ctx->host_u32 = saved_host;
   cudaGraph_t graph = nullptr;
   const cudaError_t ec = cudaStreamEndCapture(s, &graph);
   if (st != LGS_OK) {
@@ -2208,7 +2434,8 @@ LGS_API lgs_status lgs_plan_create(lgs_ctx* ctx, lgs_map* map, const lgs_camera*
   if (targets->memory != LGS_MEM_DEVICE || grads->memory != LGS_MEM_DEVICE ||
       (images && images->memory != LGS_MEM_DEVICE))
     return fail(LGS_EINVAL, "a plan reads device targets and writes device images / gradients");
-  if (grads->accumulate) return fail(LGS_EINVAL, "a plan overwrites its gradients (accumulate = 0)");
+  // grads->accumulate: every replay adds its gradients (the later views of a multi-view batch); a
+  // replay whose tile lists overflowed adds nothing (empty lists) before lgs_plan_sync re-runs it
   LGS_CUDA(cudaSetDevice(ctx->device));
   lgs_plan* p = new lgs_plan();
   p->ctx = ctx;
@@ -2228,11 +2455,13 @@ LGS_API lgs_status lgs_plan_create(lgs_ctx* ctx, lgs_map* map, const lgs_camera*
     if (p->ev0) cudaEventDestroy(p->ev0);
     if (p->ev1) cudaEventDestroy(p->ev1);
     if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
+    if (p->host_pairs) cudaFreeHost(p->host_pairs);
     ctx_release(ctx);
     delete p;
     return st;
   };
   if (cudaEventCreate(&p->ev0) != cudaSuccess || cudaEventCreate(&p->ev1) != cudaSuccess ||
+      cudaMallocHost(&p->host_pairs, 64) != cudaSuccess ||
       cudaStreamCreateWithFlags(&p->cap_stream, cudaStreamNonBlocking) != cudaSuccess)
     return bail(fail(LGS_ECUDA, "event / stream creation failed"));
   // one eager step sizes the tile-list capacity (and runs every one-time kernel setup)
@@ -2258,9 +2487,10 @@ LGS_API lgs_status lgs_plan_run(lgs_ctx* ctx, lgs_plan* p) {
 LGS_API lgs_status lgs_plan_sync(lgs_ctx* ctx, lgs_plan* p, int64_t* pairs) {
   if (!ctx || !p || ctx != p->ctx) return fail(LGS_EINVAL, "plan / context mismatch");
   LGS_CUDA(cudaStreamSynchronize(ctx->stream));
-  const int64_t P = ctx->host_u32[0];
+  const int64_t P = p->host_pairs[0];
   if (P > p->cap) {  // the replay ran on empty tile lists: grow, re-capture, redo the step
-    ctx->pairs_cap = P + P / 4;
+    ctx->pairs_cap = std::max<int64_t>(ctx->pairs_cap, P + P / 4);
+    ++p->recaptures;
     LGS_TRY(plan_capture(p));
     LGS_TRY(lgs_plan_run(ctx, p));
     LGS_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -2312,9 +2542,12 @@ LGS_API lgs_status lgs_plan_destroy(lgs_plan* p) {
   plan_free_marks(p);
   if (p->ev1) cudaEventDestroy(p->ev1);
   if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
+  if (p->host_pairs) cudaFreeHost(p->host_pairs);
   delete p;
   ctx_release(ctx);
   return LGS_OK;
 }
+
+LGS_API int64_t lgs_plan_recaptures(const lgs_plan* p) { return p ? p->recaptures : -1; }
 
 }  // extern "C"

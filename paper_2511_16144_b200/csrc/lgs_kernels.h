@@ -185,6 +185,7 @@ void launch_rows_pack(float* const ptr[6], const int width[6], int64_t n, const 
                       int64_t max_rows, float* rec, cudaStream_t s);
 void launch_rows_apply(float* const ptr[6], const int width[6], int64_t n, const float* recs, const uint32_t* counts,
                        int world, int64_t stride, cudaStream_t s);
+void launch_rows_overflow(const uint32_t* counts, int world, int64_t cap, uint32_t* out, cudaStream_t s);
 
 struct GradOut {
   float* position;      // [N][3]

@@ -34,7 +34,8 @@ void load() {
          resolve(h, "ncclCommDestroy", g_api.CommDestroy) && resolve(h, "ncclAllReduce", g_api.AllReduce) &&
          resolve(h, "ncclReduceScatter", g_api.ReduceScatter) && resolve(h, "ncclAllGather", g_api.AllGather) &&
          resolve(h, "ncclGroupStart", g_api.GroupStart) && resolve(h, "ncclGroupEnd", g_api.GroupEnd) &&
-         resolve(h, "ncclGetErrorString", g_api.GetErrorString) && resolve(h, "ncclGetVersion", g_api.GetVersion);
+         resolve(h, "ncclGetErrorString", g_api.GetErrorString) && resolve(h, "ncclGetVersion", g_api.GetVersion) &&
+         resolve(h, "ncclCommAbort", g_api.CommAbort) && resolve(h, "ncclCommGetAsyncError", g_api.CommGetAsyncError);
 }
 
 }  // namespace

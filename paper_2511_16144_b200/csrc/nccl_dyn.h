@@ -23,6 +23,8 @@ struct NcclApi {
   ncclResult_t (*GroupEnd)();
   const char* (*GetErrorString)(ncclResult_t);
   ncclResult_t (*GetVersion)(int*);
+  ncclResult_t (*CommAbort)(ncclComm_t);
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*);
 };
 
 // nullptr (and *err set) when NCCL cannot be loaded.

@@ -51,12 +51,13 @@ __global__ void rows_scan_kernel(RowLayout L, uint32_t* __restrict__ list, uint3
   if (nz) list[base + __popc(bal & ((1u << lane) - 1u))] = (uint32_t)i;
 }
 
-// record k: [index bits, R values]; one warp per record, lanes over the values
+// record k: [index bits, R values]; one warp per record, lanes over the values; at most `cap`
+// records (a rank with more rows overflows the exchange: see rows_apply_kernel)
 __global__ void rows_pack_kernel(RowLayout L, const uint32_t* __restrict__ list, const uint32_t* __restrict__ count,
-                                 float* __restrict__ rec) {
+                                 int64_t cap, float* __restrict__ rec) {
   const int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (k >= *count) return;
+  if (k >= *count || k >= cap) return;
   const int64_t i = list[k];
   float* r = rec + k * (L.R + 1);
   if (lane == 0) r[0] = __uint_as_float((uint32_t)i);
@@ -69,9 +70,13 @@ __global__ void rows_pack_kernel(RowLayout L, const uint32_t* __restrict__ list,
 }
 
 // zero (add = false) or add rank r's records into the dense rows; recs of all ranks back to back,
-// each rank's block `stride` records long
+// each rank's block `stride` records long.  If any rank listed more rows than `stride` (a
+// capacity-speculative exchange that overflowed) nothing is touched: every rank keeps its own
+// gradient and the host re-runs the exchange with exact sizes.
 __global__ void rows_apply_kernel(RowLayout L, const float* __restrict__ recs, const uint32_t* __restrict__ counts,
-                                  int rank_lo, int rank_hi, int64_t stride, int add) {
+                                  int world, int rank_lo, int rank_hi, int64_t stride, int add) {
+  for (int q = 0; q < world; ++q)
+    if ((int64_t)counts[q] > stride) return;
   const int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const int64_t per = stride;
@@ -120,7 +125,20 @@ void launch_rows_pack(float* const ptr[6], const int width[6], int64_t n, const 
                       int64_t max_rows, float* rec, cudaStream_t s) {
   if (max_rows == 0) return;
   rows_pack_kernel<<<(unsigned)((max_rows * 32 + 255) / 256), 256, 0, s>>>(make_layout(ptr, width, n), list, count,
-                                                                           rec);
+                                                                           max_rows, rec);
+}
+
+// out[0] = 1 if some rank's count exceeds cap, out[1] = the largest count
+__global__ void rows_overflow_kernel(const uint32_t* __restrict__ counts, int world, int64_t cap, uint32_t* out) {
+  if (threadIdx.x != 0) return;
+  uint32_t mx = 0;
+  for (int q = 0; q < world; ++q) mx = max(mx, counts[q]);
+  out[0] = (int64_t)mx > cap ? 1u : 0u;
+  out[1] = mx;
+}
+
+void launch_rows_overflow(const uint32_t* counts, int world, int64_t cap, uint32_t* out, cudaStream_t s) {
+  rows_overflow_kernel<<<1, 32, 0, s>>>(counts, world, cap, out);
 }
 
 void launch_rows_apply(float* const ptr[6], const int width[6], int64_t n, const float* recs, const uint32_t* counts,
@@ -128,9 +146,10 @@ void launch_rows_apply(float* const ptr[6], const int width[6], int64_t n, const
   if (stride == 0) return;
   const RowLayout L = make_layout(ptr, width, n);
   const int64_t all = (int64_t)world * stride * 32;
-  rows_apply_kernel<<<(unsigned)((all + 255) / 256), 256, 0, s>>>(L, recs, counts, 0, world, stride, 0);
+  rows_apply_kernel<<<(unsigned)((all + 255) / 256), 256, 0, s>>>(L, recs, counts, world, 0, world, stride, 0);
   for (int r = 0; r < world; ++r)  // rank order: identical sums on every rank
-    rows_apply_kernel<<<(unsigned)((stride * 32 + 255) / 256), 256, 0, s>>>(L, recs, counts, r, r + 1, stride, 1);
+    rows_apply_kernel<<<(unsigned)((stride * 32 + 255) / 256), 256, 0, s>>>(L, recs, counts, world, r, r + 1, stride,
+                                                                          1);
 }
 
 }  // namespace lgs

@@ -96,6 +96,35 @@ class NativeComm:
         _lib.check(_lib.load().lgs_allreduce_grads_sparse(self.ctx.h, dmap.h, C.byref(gs), C.byref(rows)))
         return rows.value
 
+    def all_reduce_grads_sparse_async(self, dmap, grads):
+        """lgs_allreduce_grads_sparse_async: the same sum enqueued without a host wait (capacity-sized
+        row blocks); call ``wait_grads_sparse`` after the step."""
+        from . import _lib
+        from .renderer import _grads_struct
+
+        self._pending = _grads_struct(grads, False)
+        _lib.check(_lib.load().lgs_allreduce_grads_sparse_async(self.ctx.h, dmap.h, self._pending))
+
+    def wait_grads_sparse(self, dmap, grads) -> int:
+        """Completes an async sparse exchange (re-running it exactly if a rank outgrew the capacity);
+        returns the largest per-rank row count."""
+        import ctypes as C
+
+        from . import _lib
+        from .renderer import _grads_struct
+
+        gs = getattr(self, "_pending", None) or _grads_struct(grads, False)
+        rows = C.c_int64()
+        _lib.check(_lib.load().lgs_allreduce_grads_sparse_wait(self.ctx.h, dmap.h, gs, C.byref(rows)))
+        self._pending = None
+        return rows.value
+
+    def set_timeout(self, ms: int):
+        """Bound the host waits inside collectives (lgs_comm_set_timeout)."""
+        from . import _lib
+
+        _lib.check(_lib.load().lgs_comm_set_timeout(self.ctx.h, int(ms)))
+
     def close(self):
         from . import _lib
 
@@ -162,11 +191,13 @@ def sparse_sum_reference(rows_per_rank):
     return out
 
 
-def sparse_all_reduce_host(dense, group=None):
+def sparse_all_reduce_host(dense, group=None, cap=0):
     """lgs_allreduce_grads_sparse's exchange over torch.distributed on host arrays (any backend;
     the gloo tests run it): nonzero rows of a [N][R] float32 array are all-gathered as (index,
     row) records and merged like sparse_sum_reference (listed rows zeroed, ranks added in rank
-    order), in place.  Returns the largest per-rank row count."""
+    order), in place.  Returns the largest per-rank row count.  cap > 0: the capacity-speculative
+    form (lgs_allreduce_grads_sparse_async): record blocks of ``cap`` rows; if any rank has more
+    rows, nothing is merged and -(largest count) is returned."""
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -177,11 +208,15 @@ def sparse_all_reduce_host(dense, group=None):
     counts = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
     dist.all_gather(counts, cnt, group=group)
     maxc = int(max(c.item() for c in counts))
-    rec = torch.zeros(maxc, dense.shape[1] + 1, dtype=torch.float32)
-    rec[:idx.size, 0] = torch.from_numpy(idx.astype(np.int32).view(np.float32))
-    rec[:idx.size, 1:] = torch.from_numpy(dense[idx])
+    block = cap if cap > 0 else maxc
+    rec = torch.zeros(block, dense.shape[1] + 1, dtype=torch.float32)
+    k = min(idx.size, block)  # the pack kernel writes at most `block` records
+    rec[:k, 0] = torch.from_numpy(idx[:k].astype(np.int32).view(np.float32))
+    rec[:k, 1:] = torch.from_numpy(dense[idx[:k]])
     recs = [torch.zeros_like(rec) for _ in range(world)]
     dist.all_gather(recs, rec, group=group)
+    if maxc > block:  # some rank overflowed the capacity: every rank keeps its own gradient
+        return -maxc
     lists = [r[:int(c.item()), 0].numpy().view(np.int32) for r, c in zip(recs, counts)]
     for li in lists:
         dense[li] = 0.0

@@ -555,10 +555,11 @@ class Plan:
     enqueues the whole step with one graph launch; ``sync()`` waits for it (re-capturing if the
     tile lists outgrew their capacity).  ``targets``, ``grads`` and the optional ``images`` are CUDA
     buffers whose contents may change between runs; ``pose_out`` (pinned host or CUDA, 6 float32)
-    receives the pose gradient in stream order."""
+    receives the pose gradient in stream order.  ``accumulate``: the step adds its gradients into
+    ``grads`` (the later views of a multi-view batch) instead of overwriting them."""
 
     def __init__(self, dmap: DeviceMap, camera, targets: dict, grads: dict, images: dict | None = None,
-                 pose_out=None, cfg: RenderConfig | None = None):
+                 pose_out=None, cfg: RenderConfig | None = None, accumulate: bool = False):
         self.ctx = dmap.ctx
         self._keep = (targets, grads, images, pose_out)
         cam = make_camera(camera)
@@ -569,7 +570,7 @@ class Plan:
         if images is not None:
             imgs = _lib.LgsImages(_ptr(images["rgb"]), _ptr(images["depth"]), _ptr(images["feat"]) if d else None,
                                   _ptr(images["acc"]), LGS_MEM_DEVICE)
-        gs = _grads_struct(grads, False)
+        gs = _grads_struct(grads, accumulate)  # accumulate: add into grads (later views of a batch)
         c = (cfg or RenderConfig()).c()
         h = C.c_void_p()
         check(_lib.load().lgs_plan_create(self.ctx.h, dmap.h, C.byref(cam), C.byref(c), C.byref(tg),
@@ -608,6 +609,11 @@ class Plan:
     @property
     def launches(self) -> int:
         return int(_lib.load().lgs_plan_launches(self.h))
+
+    @property
+    def recaptures(self) -> int:
+        """How often sync() re-captured and re-ran the step (the tile lists outgrew the capacity)."""
+        return int(_lib.load().lgs_plan_recaptures(self.h))
 
     def __del__(self):
         try:

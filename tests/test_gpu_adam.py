@@ -23,8 +23,9 @@ def _dev(scene):
     return {k: torch.from_numpy(np.ascontiguousarray(v, np.float32)).cuda() for k, v in scene.items()}
 
 
-def test_map_download_round_trip():
-    scene, _, _ = scenes.make_config("c1", n=5000)
+@pytest.mark.parametrize("n", [5000, 4001])  # n % 4 != 0: rotation rows at float offset 3n
+def test_map_download_round_trip(n):
+    scene, _, _ = scenes.make_config("c1", n=n)
     dm = R.DeviceMap(_dev(scene))
     back = R.map_download(dm)
     for k, v in scene.items():
@@ -34,7 +35,7 @@ def test_map_download_round_trip():
         assert np.array_equal(dback[k].cpu().numpy(), np.asarray(v, np.float32)), k
 
 
-@pytest.mark.parametrize("name,n", [("c0", 4000), ("c1", 20_000)])
+@pytest.mark.parametrize("name,n", [("c0", 4000), ("c0", 4001), ("c1", 20_000), ("c1", 20_003)])
 def test_adam_steps_match_oracle(name, n):
     scene, cams, info = scenes.make_config(name, n=n)
     cam = cams[0]

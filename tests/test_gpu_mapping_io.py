@@ -22,8 +22,9 @@ def _sh0_scene(n=3000):
     return scene, cams[0], info
 
 
-def test_map_load_renders_like_the_scene(tmp_path):
-    scene, cam, _ = _sh0_scene()
+@pytest.mark.parametrize("n", [3000, 3001])  # n % 4 != 0: the download staging
+def test_map_load_renders_like_the_scene(tmp_path, n):
+    scene, cam, _ = _sh0_scene(n)
     p = str(tmp_path / "m.legomap")
     py_write(p, scene, np.zeros(scene["pos"].shape[0], np.uint64))
     dm = R.map_load(p)

@@ -94,3 +94,85 @@ def test_sparse_gradient_exchange_world1():
     assert 0 < rows < dmap.n
     assert torch.equal(grads["flat"], before)
     comm.close()
+
+
+def _simulated_exchange(dmap, grads_list, cap=0):
+    import ctypes as C
+    from paper_2511_16144_b200 import _lib
+    structs = [R._grads_struct(g, False) for g in grads_list]
+    arr = (C.POINTER(_lib.LgsMapGrads) * len(structs))(*[C.pointer(s) for s in structs])
+    rows, ovf = C.c_int64(), C.c_int32()
+    st = _lib.load().lgs_debug_sparse_reduce_simulated(dmap.ctx.h, dmap.h, arr, len(structs), cap, C.byref(rows),
+                                                       C.byref(ovf))
+    return (st, rows.value, ovf.value) if cap else (st, rows.value)
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_sparse_exchange_simulated_ranks_equals_dense_sum(world):
+    """The world > 1 path of lgs_allreduce_grads_sparse (scan, count all-gather, pack, record
+    all-gather, zero + rank-ordered add) over `world` ranks simulated on one GPU: every rank ends with
+    the dense sum over ranks -- bit for bit the fp32 sum taken in rank order -- and all ranks are
+    identical.  Each rank holds real per-view gradients (different c3 views), so rows overlap
+    partially across ranks."""
+    # the full c3 map: its views saturate on a few thousand Gaussians (sparse rows)
+    ctx, dmap, cams, tgs = _setup(nviews=world if world <= 8 else 8, n=500_000)
+    per_rank = []
+    for r in range(world):
+        g = R.alloc_grads(dmap.n, dmap.d, dmap.K, device=0)
+        out = R.render(dmap, cams[r % len(cams)], targets=tgs[r % len(cams)], ctx=ctx)
+        R.render_backward_l1(out, into=g)
+        per_rank.append(g)
+    torch.cuda.synchronize()
+    dense = torch.zeros_like(per_rank[0]["flat"])
+    for g in per_rank:  # ((0 + g0) + g1) + ...: the exchange's order
+        dense = dense + g["flat"]
+    st, rows = _simulated_exchange(dmap, per_rank)
+    torch.cuda.synchronize()
+    assert st == 0, st
+    assert rows > 1
+    for g in per_rank:
+        assert torch.equal(g["flat"], dense)
+
+
+def _per_rank_grads(world, n=500_000):
+    ctx, dmap, cams, tgs = _setup(nviews=min(world, 8), n=n)
+    per_rank = []
+    for r in range(world):
+        g = R.alloc_grads(dmap.n, dmap.d, dmap.K, device=0)
+        out = R.render(dmap, cams[r % len(cams)], targets=tgs[r % len(cams)], ctx=ctx)
+        R.render_backward_l1(out, into=g)
+        per_rank.append(g)
+    torch.cuda.synchronize()
+    return dmap, per_rank
+
+
+def test_sparse_exchange_capacity_speculative():
+    """The host-wait-free form (lgs_allreduce_grads_sparse_async): record blocks of a fixed capacity.
+    With room for every rank's rows it equals the exact exchange bit for bit; when a rank has more
+    rows than the capacity the kernels see it in the gathered counts and change nothing (each rank
+    keeps its own gradient), reporting the overflow and the largest count for the exact re-run."""
+    world = 4
+    dmap, per_rank = _per_rank_grads(world)
+    before = [g["flat"].clone() for g in per_rank]
+    dense = torch.zeros_like(before[0])
+    for b in before:
+        dense = dense + b
+    st, rows, ovf = _simulated_exchange(dmap, per_rank, cap=8)  # far too small
+    torch.cuda.synchronize()
+    assert st == 0 and ovf == 1 and rows > 8
+    for g, b in zip(per_rank, before):
+        assert torch.equal(g["flat"], b)
+    st, rows2, ovf = _simulated_exchange(dmap, per_rank, cap=rows + rows // 4)
+    torch.cuda.synchronize()
+    assert st == 0 and ovf == 0 and rows2 == rows
+    for g in per_rank:
+        assert torch.equal(g["flat"], dense)
+
+
+def test_sparse_exchange_simulated_refuses_dense_rows():
+    ctx, dmap, cams, tgs = _setup(nviews=1, n=4_000)
+    per_rank = [R.alloc_grads(dmap.n, dmap.d, dmap.K, device=0) for _ in range(2)]
+    for g in per_rank:
+        g["flat"].fill_(1.0)  # every row nonzero: the real exchange takes the dense all-reduce
+    st, rows = _simulated_exchange(dmap, per_rank)
+    assert st == 1 and rows == -1

@@ -104,3 +104,25 @@ def test_errors_match_reference(tmp_path):
     sh3 = dict(random_scene(2, 4, 1), sh=np.zeros((2, 16, 3), np.float32))
     with pytest.raises(ValueError):
         R.map_file_write(str(tmp_path / "sh3.bin"), sh3)
+
+
+def test_huge_declared_count_is_a_truncation_error(tmp_path):
+    """A corrupt header declaring 2^60 Gaussians: the file is sized against the count before any
+    buffer is sized from it (the reference reads record by record and raises "map file truncated";
+    sizing vectors first would throw std::bad_alloc through the C ABI)."""
+    import struct
+    p = str(tmp_path / "huge.bin")
+    R.map_file_write(p, random_scene(3, 4, 5))
+    with open(p, "r+b") as f:
+        f.seek(12)
+        f.write(struct.pack("<Q", 1 << 60))
+    with pytest.raises(_lib.LgsIoError, match="truncated reading"):
+        R.map_file_info(p)
+    with pytest.raises(_lib.LgsIoError, match="truncated reading"):
+        R.map_file_read(p)
+    # a count one past the records: the error names the field the reader runs out in
+    with open(p, "r+b") as f:
+        f.seek(12)
+        f.write(struct.pack("<Q", 4))
+    with pytest.raises(_lib.LgsIoError, match="truncated reading position"):
+        R.map_file_read(p)

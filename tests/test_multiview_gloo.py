@@ -104,13 +104,16 @@ def test_two_rank_allreduce_equals_single_process_sum():
     assert np.array_equal(res[0], res[1])
 
 
-def _sparse_worker(rank, world, port, q):
+def _sparse_worker(rank, world, port, q, caps=(0,)):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    dense = _sparse_rank_grads(rank)
-    maxc = multiview.sparse_all_reduce_host(dense)
-    q.put((rank, dense.copy(), maxc))
+    out = []
+    for cap in caps:
+        dense = _sparse_rank_grads(rank)
+        maxc = multiview.sparse_all_reduce_host(dense, cap=cap)
+        out.append((dense.copy(), maxc))
+    q.put((rank, out[0][0], out[0][1]) if len(caps) == 1 else (rank, out))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -152,3 +155,31 @@ def test_sparse_gradient_exchange_equals_dense_sum():
         assert np.array_equal(dense, res[0][0])
         assert np.array_equal(dense, merged)
         assert np.allclose(dense, want, rtol=1e-5, atol=1e-6)
+
+
+def test_sparse_exchange_capacity_overflow_changes_nothing():
+    """The capacity-speculative form (lgs_allreduce_grads_sparse_async) at world size 3: a capacity
+    below some rank's row count leaves every rank's gradient as it was and reports the count; a
+    sufficient capacity gives the exact exchange's result."""
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    caps = (50, 1000)
+    procs = [ctx.Process(target=_sparse_worker, args=(r, world, port, q, caps)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r, out = q.get(timeout=300)
+        res[r] = out
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    per_rank = [_sparse_rank_grads(r) for r in range(world)]
+    rows = max(int(np.any(g != 0, axis=1).sum()) for g in per_rank)
+    merged = multiview.sparse_sum_reference(per_rank)
+    for r in range(world):
+        (d_small, m_small), (d_big, m_big) = res[r]
+        assert m_small == -rows and np.array_equal(d_small, per_rank[r])
+        assert m_big == rows and np.array_equal(d_big, merged)
