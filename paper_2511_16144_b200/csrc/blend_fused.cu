@@ -19,7 +19,13 @@ namespace lgs {
 
 template <int DP>
 struct FusedSmem {
-  static constexpr int NB = 192;  // list entries per staged batch (static shared memory < 48 KB)
+#ifndef LGS_FUSED_NB
+#define LGS_FUSED_NB 192
+#endif
+#ifndef LGS_FUSED_DYN_PAD
+#define LGS_FUSED_DYN_PAD 0  // experiment builds only: unused dynamic shared memory (occupancy studies)
+#endif
+  static constexpr int NB = LGS_FUSED_NB;  // list entries per staged batch (static shared memory < 48 KB)
   float4 r0[NB];                  // u, v, depth, opacity
   float4 fa[NB];                  // conic frame S0, T0, ux, uy (blend_common.cuh stage_frame)
   float4 fb[NB];                  // conic frame wx, wy, dxc, dyc
@@ -27,7 +33,8 @@ struct FusedSmem {
   float4 col[NB];
   uint32_t gid[NB];
   float4 feat[NB][DP > 0 ? DP / 4 : 1];
-  float4 gfeat[DP > 0 ? DP / 4 : 1][kBlock];  // per-pixel feature cotangents
+  float4 gfeat[DP > 0 ? DP / 2 : 1][kBlock / 2];  // feature cotangents: [channel pair][thread] =
+                                                  // (pixel 0 c, pixel 1 c, pixel 0 c+1, pixel 1 c+1)
 };
 
 template <int SLOTS>
@@ -50,7 +57,7 @@ template <int DP>
 __global__ void __launch_bounds__(kBlock / 2) blend_fused_l1_kernel(DevMap m, DevCam c, ViewBufs v, TileLists tl,
                                                                       FwdOut o, float* __restrict__ gacc) {
   griddep_wait();
-  constexpr int PPT = 2;
+  constexpr int PPT = 2;  // the thread's two pixels are the two lanes of every paired (FFMA2) op
   constexpr int NT = kBlock / PPT;
   constexpr int DQ = DP > 0 ? DP / 4 : 1;
   constexpr int FD = DP > 0 ? DP : 1;
@@ -70,6 +77,9 @@ __global__ void __launch_bounds__(kBlock / 2) blend_fused_l1_kernel(DevMap m, De
   const float npx = (float)c.W * (float)c.H;
   const float inv_rgb = 1.0f / (3.0f * npx), inv_d = 1.0f / npx;
   const float inv_f = m.d > 0 ? 1.0f / ((float)m.d * npx) : 0.f;
+  // pixel offsets from the tile centre (the conic frames' origin), as lane pairs
+  const float2 ex2 = bc2((float)lx - 7.5f);
+  const float2 ey2 = make_float2((float)ly0 - 7.5f, (float)(ly0 + 1) - 7.5f);
 
   // stage list entries [b0, b0 + cnt) of the tile's list (range.x-relative positions); (xc, yc) =
   // the tile centre the conic frames are centred on
@@ -97,30 +107,19 @@ __global__ void __launch_bounds__(kBlock / 2) blend_fused_l1_kernel(DevMap m, De
     const int tx = tile % c.tiles_x, ty = tile / c.tiles_x;
     const int px = tx * kTile + lx;
     const int py0 = ty * kTile + ly0;
-    // pixel offsets from the tile centre (the conic frames' origin)
     const float xc = (float)(tx * kTile) + 7.5f, yc = (float)(ty * kTile) + 7.5f;
-    const float ex = (float)lx - 7.5f;
-    float ey[PPT];
-#pragma unroll
-    for (int k = 0; k < PPT; ++k) ey[k] = (float)(ly0 + k) - 7.5f;
     const uint2 range = tl.ranges[tile];
     const uint32_t len = range.y - range.x;
 
-    // ---------------- forward (blend_fwd.cu) ----------------
-    float T[PPT], cr[PPT], cg[PPT], cb[PPT], draw[PPT], acc[PPT];
-    float f[PPT][FD];
-    uint32_t last[PPT];
-    bool done[PPT];
-    bool all_done = true;
+    // ---------------- forward (blend_fwd.cu arithmetic, lane-paired) ----------------
+    float2 T = bc2(1.f), cr = bc2(0.f), cg = bc2(0.f), cb = bc2(0.f), draw = bc2(0.f), acc = bc2(0.f);
+    float2 f[FD];
 #pragma unroll
-    for (int k = 0; k < PPT; ++k) {
-      T[k] = 1.f; cr[k] = cg[k] = cb[k] = draw[k] = acc[k] = 0.f;
-#pragma unroll
-      for (int q = 0; q < FD; ++q) f[k][q] = 0.f;
-      last[k] = 0;
-      done[k] = !(px < c.W && py0 + k < c.H) || !(1.0f >= c.t_min);
-      all_done = all_done && done[k];
-    }
+    for (int q = 0; q < FD; ++q) f[q] = bc2(0.f);
+    uint32_t last0 = 0, last1 = 0;
+    bool done0 = !(px < c.W && py0 < c.H) || !(1.0f >= c.t_min);
+    bool done1 = !(px < c.W && py0 + 1 < c.H) || !(1.0f >= c.t_min);
+    bool all_done = done0 && done1;
     int res_batch = -1;  // batch index resident in shared memory
     for (uint32_t pos = 0; pos < len; pos += NB) {
       if (__syncthreads_count(all_done) == NT) break;
@@ -128,48 +127,35 @@ __global__ void __launch_bounds__(kBlock / 2) blend_fused_l1_kernel(DevMap m, De
       stage(range.x + pos, cnt, xc, yc);
       res_batch = (int)(pos / NB);
       __syncthreads();
-      auto composite = [&](int e, const float (&al)[PPT], const bool (&in)[PPT], float depth_z) {
-        float a[PPT];
-        bool ok[PPT];
-        bool any = false;
-#pragma unroll
-        for (int k = 0; k < PPT; ++k) {
-          const bool live = in[k] && !done[k];
-          ok[k] = live && al[k] >= c.alpha_skip;
-          a[k] = ok[k] ? fminf(al[k], c.alpha_clamp) : 0.f;
-          any = any || ok[k];
-        }
-        if (!any) return;
+      // composite one staged entry given its pixels' alphas; a pixel that does not contribute gets
+      // alpha = 0, which leaves T and the accumulators exactly unchanged (w = +0)
+      auto composite = [&](int e, float2 al, bool in0, bool in1, float depth_z) {
+        const bool ok0 = in0 && !done0 && al.x >= c.alpha_skip;
+        const bool ok1 = in1 && !done1 && al.y >= c.alpha_skip;
+        if (!ok0 && !ok1) return;
+        const float2 a = make_float2(ok0 ? fminf(al.x, c.alpha_clamp) : 0.f, ok1 ? fminf(al.y, c.alpha_clamp) : 0.f);
         const float4 col = sm.col[e];
-        float w[PPT];
-#pragma unroll
-        for (int k = 0; k < PPT; ++k) {
-          w[k] = __fmul_rn(a[k], T[k]);
-          cr[k] = fmaf(w[k], col.x, cr[k]);
-          cg[k] = fmaf(w[k], col.y, cg[k]);
-          cb[k] = fmaf(w[k], col.z, cb[k]);
-          draw[k] = fmaf(w[k], depth_z, draw[k]);
-          acc[k] += w[k];
-        }
+        const float2 w = mul2(a, T);
+        cr = fma2(w, bc2(col.x), cr);
+        cg = fma2(w, bc2(col.y), cg);
+        cb = fma2(w, bc2(col.z), cb);
+        draw = fma2(w, bc2(depth_z), draw);
+        acc = add2(acc, w);
         if (DP > 0) {
 #pragma unroll
           for (int q = 0; q < DQ; ++q) {
             const float4 fv = sm.feat[e][q];
-#pragma unroll
-            for (int k = 0; k < PPT; ++k) {
-              f[k][q * 4 + 0] = fmaf(w[k], fv.x, f[k][q * 4 + 0]);
-              f[k][q * 4 + 1] = fmaf(w[k], fv.y, f[k][q * 4 + 1]);
-              f[k][q * 4 + 2] = fmaf(w[k], fv.z, f[k][q * 4 + 2]);
-              f[k][q * 4 + 3] = fmaf(w[k], fv.w, f[k][q * 4 + 3]);
-            }
+            f[q * 4 + 0] = fma2(w, bc2(fv.x), f[q * 4 + 0]);
+            f[q * 4 + 1] = fma2(w, bc2(fv.y), f[q * 4 + 1]);
+            f[q * 4 + 2] = fma2(w, bc2(fv.z), f[q * 4 + 2]);
+            f[q * 4 + 3] = fma2(w, bc2(fv.w), f[q * 4 + 3]);
           }
         }
-#pragma unroll
-        for (int k = 0; k < PPT; ++k) {
-          T[k] = __fmul_rn(T[k], __fsub_rn(1.0f, a[k]));
-          if (ok[k]) last[k] = pos + e + 1;
-          done[k] = done[k] || T[k] < c.t_min;
-        }
+        T = mul2(T, make_float2(__fsub_rn(1.0f, a.x), __fsub_rn(1.0f, a.y)));
+        if (ok0) last0 = pos + e + 1;
+        if (ok1) last1 = pos + e + 1;
+        done0 = done0 || T.x < c.t_min;
+        done1 = done1 || T.y < c.t_min;
       };
       for (int e = 0; e < cnt && !all_done; e += 2) {
         const bool has1 = e + 1 < cnt;
@@ -182,72 +168,61 @@ __global__ void __launch_bounds__(kBlock / 2) blend_fused_l1_kernel(DevMap m, De
         if (!hit0 && !hit1) continue;
         const float4 r00 = sm.r0[e], fa0 = sm.fa[e], fb0 = sm.fb[e];
         const float4 r01 = has1 ? sm.r0[e + 1] : r00, fa1 = has1 ? sm.fa[e + 1] : fa0, fb1 = has1 ? sm.fb[e + 1] : fb0;
-        float al0[PPT], al1[PPT];
-        bool in0[PPT], in1[PPT];
-#pragma unroll
-        for (int k = 0; k < PPT; ++k) {
-          float S, T, G;
-          al0[k] = frame_alpha(fa0, fb0, r00.w, ex, ey[k], S, T, G);
-          al1[k] = frame_alpha(fa1, fb1, r01.w, ex, ey[k], S, T, G);
-        }
-#pragma unroll
-        for (int k = 0; k < PPT; ++k) {
-          const int py = py0 + k;
-          in0[k] = hit0 && py >= (int)(rc0.y & 0xffffu) && py <= (int)(rc0.y >> 16);
-          in1[k] = hit1 && py >= (int)(rc1.y & 0xffffu) && py <= (int)(rc1.y >> 16);
-        }
-        if (hit0) composite(e, al0, in0, r00.z);
-        if (hit1) composite(e + 1, al1, in1, r01.z);
-        all_done = true;
-#pragma unroll
-        for (int k = 0; k < PPT; ++k) all_done = all_done && done[k];
+        float2 S, Tt, G;
+        const float2 al0 = frame_alpha2(fa0, fb0, r00.w, ex2, ey2, S, Tt, G);
+        const float2 al1 = frame_alpha2(fa1, fb1, r01.w, ex2, ey2, S, Tt, G);
+        const int ya0 = (int)(rc0.y & 0xffffu), yb0 = (int)(rc0.y >> 16);
+        const int ya1 = (int)(rc1.y & 0xffffu), yb1 = (int)(rc1.y >> 16);
+        if (hit0) composite(e, al0, py0 >= ya0 && py0 <= yb0, py0 + 1 >= ya0 && py0 + 1 <= yb0, r00.z);
+        if (hit1) composite(e + 1, al1, py0 >= ya1 && py0 <= yb1, py0 + 1 >= ya1 && py0 + 1 <= yb1, r01.z);
+        all_done = done0 && done1;
       }
     }
 
     // ---------------- epilogue: images, loss, cotangents kept on chip ----------------
     const bool tile_done = o.unfinished ? __syncthreads_and(all_done) != 0 : true;
     if (!tile_done && tid == 0) o.unfinished[tile] = 1u;
-    float g_rgb[PPT][3], g_draw[PPT], g_acc[PPT];
-    uint32_t my_max = 0;
+    float2 g_r = bc2(0.f), g_g = bc2(0.f), g_b = bc2(0.f), g_draw = bc2(0.f), g_acc = bc2(0.f);
+    float gf[PPT][FD];
+    const float crv[PPT] = {cr.x, cr.y}, cgv[PPT] = {cg.x, cg.y}, cbv[PPT] = {cb.x, cb.y};
+    const float drv[PPT] = {draw.x, draw.y}, acv[PPT] = {acc.x, acc.y};
 #pragma unroll
     for (int k = 0; k < PPT; ++k) {
       const int py = py0 + k;
-      const int lp = (ly0 + k) * kTile + lx;
-      g_rgb[k][0] = g_rgb[k][1] = g_rgb[k][2] = 0.f;
-      g_draw[k] = g_acc[k] = 0.f;
-      float gf[FD];
 #pragma unroll
-      for (int q = 0; q < FD; ++q) gf[q] = 0.f;
+      for (int q = 0; q < FD; ++q) gf[k][q] = 0.f;
+      float grgb[3] = {0.f, 0.f, 0.f}, gdr = 0.f, gac = 0.f;
       if (px < c.W && py < c.H) {
         const size_t pix = (size_t)py * c.W + px;
-        const float dnorm = draw[k] / fmaxf(acc[k], 1e-6f);
+        const float dnorm = drv[k] / fmaxf(acv[k], 1e-6f);
         if (o.rgb) {
-          o.rgb[pix * 3 + 0] = cr[k];
-          o.rgb[pix * 3 + 1] = cg[k];
-          o.rgb[pix * 3 + 2] = cb[k];
+          o.rgb[pix * 3 + 0] = crv[k];
+          o.rgb[pix * 3 + 1] = cgv[k];
+          o.rgb[pix * 3 + 2] = cbv[k];
         }
         if (o.depth) o.depth[pix] = dnorm;
-        if (o.acc) o.acc[pix] = acc[k];
+        if (o.acc) o.acc[pix] = acv[k];
         if (DP > 0 && o.feat) {
           float* fo = o.feat + pix * m.d;
           if (m.d == DP) {
 #pragma unroll
             for (int q = 0; q < DQ; ++q)
-              reinterpret_cast<float4*>(fo)[q] = make_float4(f[k][q * 4], f[k][q * 4 + 1], f[k][q * 4 + 2],
-                                                             f[k][q * 4 + 3]);
+              reinterpret_cast<float4*>(fo)[q] =
+                  k == 0 ? make_float4(f[q * 4].x, f[q * 4 + 1].x, f[q * 4 + 2].x, f[q * 4 + 3].x)
+                         : make_float4(f[q * 4].y, f[q * 4 + 1].y, f[q * 4 + 2].y, f[q * 4 + 3].y);
           } else {
 #pragma unroll
             for (int q = 0; q < FD; ++q)
-              if (q < m.d) fo[q] = f[k][q];
+              if (q < m.d) fo[q] = k == 0 ? f[q].x : f[q].y;
           }
         }
         if (tile_done) {  // L1 (blend_fwd.cu): cotangent sign(diff) / count, loss partial
-          const float vals[3] = {cr[k], cg[k], cb[k]};
+          const float vals[3] = {crv[k], cgv[k], cbv[k]};
           float lr = 0.f, lf = 0.f;
 #pragma unroll
           for (int ch = 0; ch < 3; ++ch) {
             const float df = vals[ch] - o.t_rgb[pix * 3 + ch];
-            g_rgb[k][ch] = df > 0.f ? inv_rgb : (df < 0.f ? -inv_rgb : 0.f);
+            grgb[ch] = df > 0.f ? inv_rgb : (df < 0.f ? -inv_rgb : 0.f);
             lr += fabsf(df);
           }
           const float dd = dnorm - o.t_depth[pix];
@@ -255,34 +230,41 @@ __global__ void __launch_bounds__(kBlock / 2) blend_fused_l1_kernel(DevMap m, De
 #pragma unroll
           for (int q = 0; q < DP; ++q) {
             if (q < m.d) {
-              const float df = f[k][q] - o.t_feat[pix * m.d + q];
-              gf[q] = df > 0.f ? inv_f : (df < 0.f ? -inv_f : 0.f);
+              const float fq = k == 0 ? f[q].x : f[q].y;
+              const float df = fq - o.t_feat[pix * m.d + q];
+              gf[k][q] = df > 0.f ? inv_f : (df < 0.f ? -inv_f : 0.f);
               lf += fabsf(df);
             }
           }
           loss += lr * inv_rgb + fabsf(dd) * inv_d + lf * inv_f;
           // backward per-pixel constants (renderer.cpp:204-212)
-          const float mm = fmaxf(acc[k], 1e-6f);
-          g_draw[k] = g_d / mm;
-          g_acc[k] = acc[k] > 1e-6f ? -g_d * dnorm / mm : 0.f;
+          const float mm = fmaxf(acv[k], 1e-6f);
+          gdr = g_d / mm;
+          gac = acv[k] > 1e-6f ? -g_d * dnorm / mm : 0.f;
         }
       }
-      if (DP > 0) {
-#pragma unroll
-        for (int q = 0; q < DP / 4; ++q)
-          sm.gfeat[q][lp] = make_float4(gf[q * 4], gf[q * 4 + 1], gf[q * 4 + 2], gf[q * 4 + 3]);
+      if (k == 0) {
+        g_r.x = grgb[0]; g_g.x = grgb[1]; g_b.x = grgb[2]; g_draw.x = gdr; g_acc.x = gac;
+      } else {
+        g_r.y = grgb[0]; g_g.y = grgb[1]; g_b.y = grgb[2]; g_draw.y = gdr; g_acc.y = gac;
       }
-      if (!tile_done) last[k] = 0;  // rendered again by the second pass
-      my_max = max(my_max, last[k]);
     }
+    // feature cotangents, channel pairs of both pixels interleaved: (p0 c, p1 c, p0 c+1, p1 c+1)
+    if (DP > 0) {
+#pragma unroll
+      for (int j = 0; j < DP / 2; ++j)
+        sm.gfeat[j][tid] = make_float4(gf[0][2 * j], gf[1][2 * j], gf[0][2 * j + 1], gf[1][2 * j + 1]);
+    }
+    if (!tile_done) last0 = last1 = 0;  // rendered again by the second pass
+    const uint32_t my_max = max(last0, last1);
 
-    // ---------------- backward (blend_bwd.cu) ----------------
+    // ---------------- backward (blend_bwd.cu arithmetic, lane-paired) ----------------
     if (tid == 0) s_max = 0;
     __syncthreads();
     const uint32_t warp_last = __reduce_max_sync(0xffffffffu, my_max);
     if (lane == 0 && warp_last) atomicMax(&s_max, warp_last);
     __syncthreads();
-    float accum[PPT] = {};
+    float2 accum = bc2(0.f);
     for (int b = s_max ? (int)((s_max - 1) / NB) : -1; b >= 0; --b) {
       const uint32_t bpos = (uint32_t)b * NB;
       const int cnt = (int)min((uint32_t)NB, len - bpos);
@@ -302,79 +284,68 @@ __global__ void __launch_bounds__(kBlock / 2) blend_fused_l1_kernel(DevMap m, De
         if (!__any_sync(0xffffffffu, col_in)) continue;
         const float4 r0 = sm.r0[e];
         const float4 fa = sm.fa[e], fb = sm.fb[e];
-        float alphas[PPT], Gs[PPT], Ss[PPT], Ts[PPT];
-#pragma unroll
-        for (int k = 0; k < PPT; ++k) alphas[k] = frame_alpha(fa, fb, r0.w, ex, ey[k], Ss[k], Ts[k], Gs[k]);
-        bool any = false;
-#pragma unroll
-        for (int k = 0; k < PPT; ++k) {
-          const int py = py0 + k;
-          const float al = alphas[k];
-          const bool ok = col_in && jrel < last[k] && py >= ry0 && py <= ry1 && al >= c.alpha_skip;
-          alphas[k] = ok ? al : 0.f;
-          any = any || ok;
-        }
-        if (!__any_sync(0xffffffffu, any)) continue;
+        float2 S, Tt, G;
+        const float2 al = frame_alpha2(fa, fb, r0.w, ex2, ey2, S, Tt, G);
+        const bool ok0 = col_in && jrel < last0 && py0 >= ry0 && py0 <= ry1 && al.x >= c.alpha_skip;
+        const bool ok1 = col_in && jrel < last1 && py0 + 1 >= ry0 && py0 + 1 <= ry1 && al.y >= c.alpha_skip;
+        if (!__any_sync(0xffffffffu, ok0 || ok1)) continue;
+        const float2 alpha = make_float2(ok0 ? al.x : 0.f, ok1 ? al.y : 0.f);
         float vals[SLOTS];
 #pragma unroll
         for (int q = 0; q < SLOTS; ++q) vals[q] = 0.f;
         const float4 col = sm.col[e];
         const float op = r0.w;
         const float do_dlogit = op * (1.0f - op);
-        float w[PPT], dldw[PPT], inv1ma[PPT];
-#pragma unroll
-        for (int k = 0; k < PPT; ++k) {
-          const float a = fminf(alphas[k], c.alpha_clamp);
-          inv1ma[k] = fast_rcp(1.0f - a);
-          T[k] = T[k] * inv1ma[k];
-          w[k] = a * T[k];
-          float dl = fmaf(g_draw[k], r0.z, g_acc[k]);
-          dl = fmaf(g_rgb[k][0], col.x, dl);
-          dl = fmaf(g_rgb[k][1], col.y, dl);
-          dl = fmaf(g_rgb[k][2], col.z, dl);
-          dldw[k] = dl;
-        }
+        const float2 a = make_float2(fminf(alpha.x, c.alpha_clamp), fminf(alpha.y, c.alpha_clamp));
+        const float2 inv1ma = make_float2(fast_rcp(1.0f - a.x), fast_rcp(1.0f - a.y));
+        T = mul2(T, inv1ma);  // transmittance before this contributor (unchanged when a = 0)
+        const float2 w = mul2(a, T);
+        float2 dl = fma2(g_draw, bc2(r0.z), g_acc);
+        dl = fma2(g_r, bc2(col.x), dl);
+        dl = fma2(g_g, bc2(col.y), dl);
+        dl = fma2(g_b, bc2(col.z), dl);
         if (DP > 0) {
 #pragma unroll
           for (int q = 0; q < DQ; ++q) {
             const float4 fv = sm.feat[e][q];
-#pragma unroll
-            for (int k = 0; k < PPT; ++k) {
-              const int lp = (ly0 + k) * kTile + lx;
-              const float4 gv = sm.gfeat[q][lp];
-              dldw[k] = fmaf(gv.x, fv.x, dldw[k]);
-              dldw[k] = fmaf(gv.y, fv.y, dldw[k]);
-              dldw[k] = fmaf(gv.z, fv.z, dldw[k]);
-              dldw[k] = fmaf(gv.w, fv.w, dldw[k]);
-              vals[kSlotFeat + q * 4 + 0] = fmaf(gv.x, w[k], vals[kSlotFeat + q * 4 + 0]);
-              vals[kSlotFeat + q * 4 + 1] = fmaf(gv.y, w[k], vals[kSlotFeat + q * 4 + 1]);
-              vals[kSlotFeat + q * 4 + 2] = fmaf(gv.z, w[k], vals[kSlotFeat + q * 4 + 2]);
-              vals[kSlotFeat + q * 4 + 3] = fmaf(gv.w, w[k], vals[kSlotFeat + q * 4 + 3]);
-            }
+            const float4 g01 = sm.gfeat[2 * q][tid];      // channels 4q, 4q+1 of both pixels
+            const float4 g23 = sm.gfeat[2 * q + 1][tid];  // channels 4q+2, 4q+3
+            dl = fma2(make_float2(g01.x, g01.y), bc2(fv.x), dl);
+            dl = fma2(make_float2(g01.z, g01.w), bc2(fv.y), dl);
+            dl = fma2(make_float2(g23.x, g23.y), bc2(fv.z), dl);
+            dl = fma2(make_float2(g23.z, g23.w), bc2(fv.w), dl);
+            float* vf = vals + kSlotFeat + q * 4;
+            vf[0] = fmaf(g01.y, w.y, g01.x * w.x);
+            vf[1] = fmaf(g01.w, w.y, g01.z * w.x);
+            vf[2] = fmaf(g23.y, w.y, g23.x * w.x);
+            vf[3] = fmaf(g23.w, w.y, g23.z * w.x);
           }
         }
-#pragma unroll
-        for (int k = 0; k < PPT; ++k) {
-          const float alpha = alphas[k];
-          const float G = Gs[k];
-          const float dx = fb.z + ex, dy = fb.w + ey[k];  // pixel - mean (renderer.cpp:141-142)
-          float dq_ddx, dq_ddy;
-          frame_dq(fa, fb, Ss[k], Ts[k], dq_ddx, dq_ddy);
-          const float dl_da = (alpha != 0.f && !(alpha > c.alpha_clamp)) ? T[k] * dldw[k] - accum[k] * inv1ma[k] : 0.f;
-          accum[k] = fmaf(dldw[k], w[k], accum[k]);
-          vals[kSlotColor + 0] = fmaf(g_rgb[k][0], w[k], vals[kSlotColor + 0]);
-          vals[kSlotColor + 1] = fmaf(g_rgb[k][1], w[k], vals[kSlotColor + 1]);
-          vals[kSlotColor + 2] = fmaf(g_rgb[k][2], w[k], vals[kSlotColor + 2]);
-          vals[kSlotZ] = fmaf(g_draw[k], w[k], vals[kSlotZ]);
-          vals[kSlotOpac] = fmaf(dl_da * G, do_dlogit, vals[kSlotOpac]);
-          const float cf = dl_da * op * (-0.5f * G);
-          vals[kSlotMuX] = fmaf(-cf, dq_ddx, vals[kSlotMuX]);
-          vals[kSlotMuY] = fmaf(-cf, dq_ddy, vals[kSlotMuY]);
-          const float cdx = cf * dx;
-          vals[kSlotConA] = fmaf(cdx, dx, vals[kSlotConA]);
-          vals[kSlotConB] = fmaf(cdx, dy, vals[kSlotConB]);
-          vals[kSlotConC] = fmaf(cf * dy, dy, vals[kSlotConC]);
-        }
+        // dL/dalpha (renderer.cpp:256-257); the clamped contributor (and a non-contributing pixel)
+        // gets no opacity / mean / conic gradient (renderer.cpp:273-274)
+        const float2 dla = fma2(make_float2(-accum.x, -accum.y), inv1ma, mul2(T, dl));
+        const float2 dl_da = make_float2((alpha.x != 0.f && !(alpha.x > c.alpha_clamp)) ? dla.x : 0.f,
+                                         (alpha.y != 0.f && !(alpha.y > c.alpha_clamp)) ? dla.y : 0.f);
+        accum = fma2(dl, w, accum);
+        vals[kSlotColor + 0] = fmaf(g_r.y, w.y, g_r.x * w.x);
+        vals[kSlotColor + 1] = fmaf(g_g.y, w.y, g_g.x * w.x);
+        vals[kSlotColor + 2] = fmaf(g_b.y, w.y, g_b.x * w.x);
+        vals[kSlotZ] = fmaf(g_draw.y, w.y, g_draw.x * w.x);
+        const float2 dlg = mul2(dl_da, G);
+        vals[kSlotOpac] = (dlg.x + dlg.y) * do_dlogit;
+        const float2 cf = mul2(mul2(dl_da, bc2(op)), mul2(bc2(-0.5f), G));  // dl_dg * dg_dq
+        // grad q = (2/k) (S u + T w) (blend_common.cuh frame_dq), pixel - mean = frame offset + (ex, ey)
+        const float2 dqx = mul2(bc2(kTwoOverHalfLog2e), fma2(S, bc2(fa.z), mul2(Tt, bc2(fb.x))));
+        const float2 dqy = mul2(bc2(kTwoOverHalfLog2e), fma2(S, bc2(fa.w), mul2(Tt, bc2(fb.y))));
+        const float2 dx = add2(bc2(fb.z), ex2), dy = add2(bc2(fb.w), ey2);
+        const float2 mx = mul2(cf, dqx), my = mul2(cf, dqy);
+        vals[kSlotMuX] = -(mx.x + mx.y);
+        vals[kSlotMuY] = -(my.x + my.y);
+        const float2 cdx = mul2(cf, dx), cdy = mul2(cf, dy);
+        const float2 ca = mul2(cdx, dx), cb2_ = mul2(cdx, dy), cc = mul2(cdy, dy);
+        vals[kSlotConA] = ca.x + ca.y;
+        vals[kSlotConB] = cb2_.x + cb2_.y;
+        vals[kSlotConC] = cc.x + cc.y;
         fused_transpose_reduce<SLOTS>(vals, lane);
         gacc_add(gacc + (size_t)sm.gid[e] * SLOTS, lane, vals[0]);
       }
@@ -397,12 +368,14 @@ bool blend_fused_supported(int dp) { return dp == 16 || dp == 8 || dp == 4 || dp
 template <int DP>
 static void launch_fused_dp(const DevMap& m, const DevCam& c, const ViewBufs& v, const TileLists& tl, const FwdOut& o,
                             float* gacc, cudaStream_t s, bool counter_zeroed) {
-  const int ctas_per_sm = kernel_ctas_per_sm(reinterpret_cast<const void*>(blend_fused_l1_kernel<DP>), kBlock / 2, 0);
+  const void* kfn = reinterpret_cast<const void*>(blend_fused_l1_kernel<DP>);
+  if (LGS_FUSED_DYN_PAD > 0) ensure_dyn_smem(kfn, LGS_FUSED_DYN_PAD);
+  const int ctas_per_sm = kernel_ctas_per_sm(kfn, kBlock / 2, LGS_FUSED_DYN_PAD);
   const int sms = device_sm_count();
   const int ntiles = c.tiles_x * c.tiles_y;
   const int grid = min(ntiles, ctas_per_sm * sms);
   if (!counter_zeroed) cudaMemsetAsync(tl.counter, 0, sizeof(int), s);
-  launch_pdl(blend_fused_l1_kernel<DP>, dim3(grid), dim3(kBlock / 2), 0, s, m, c, v, tl, o, gacc);
+  launch_pdl(blend_fused_l1_kernel<DP>, dim3(grid), dim3(kBlock / 2), LGS_FUSED_DYN_PAD, s, m, c, v, tl, o, gacc);
 }
 
 void launch_blend_fused_l1(const DevMap& m, const DevCam& c, const ViewBufs& v, const TileLists& tl, const FwdOut& o,

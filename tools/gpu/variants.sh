@@ -1,0 +1,16 @@
+#!/bin/bash
+# A/B of experiment builds (tools/build_variant.py variants/var_NAME ...): the in-tree liblgs.so, then each
+# variants/var_*/liblgs.so swapped in, one short bench each.  Usage: bash tools/gpu/variants.sh
+mkdir -p gpurun_out/ab
+cp paper_2511_16144_b200/liblgs.so gpurun_out/ab/base.so
+run() {
+  python bench.py --steps 30 --warmup 5 --no-e2e --no-mapping --no-cpu-baseline --multiview none 2>/dev/null | \
+    tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$1', d['value'], d['roofline']['phases']['blend_fused']['ms'])"
+}
+run base
+for v in variants/var_*/; do
+  cp $v/liblgs.so paper_2511_16144_b200/liblgs.so
+  run $(basename $v)
+done
+cp gpurun_out/ab/base.so paper_2511_16144_b200/liblgs.so
+run base_again
