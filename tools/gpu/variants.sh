@@ -5,7 +5,7 @@ mkdir -p gpurun_out/ab
 cp paper_2511_16144_b200/liblgs.so gpurun_out/ab/base.so
 run() {
   python bench.py --steps 30 --warmup 5 --no-e2e --no-mapping --no-cpu-baseline --multiview none 2>/dev/null | \
-    tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$1', d['value'], d['roofline']['phases']['blend_fused']['ms'])"
+    tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$1', d['value'], d['roofline']['phases']['blend_fused']['ms'], d['clocks'].get('sm_mhz'))"
 }
 run base
 for v in variants/var_*/; do
