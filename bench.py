@@ -486,6 +486,10 @@ def run_ours(args):
         # the same with the whole map copied every step (LGS_MEM_HOST): 150 MB more H2D per step
         full = run_e2e(args, scene, cam, tg, R, local, mapped=False)
         result["e2e"]["whole_map_copied"] = {k: full[k] for k in ("value", "ms_per_step", "h2d_bytes_per_step")}
+        # and with every gradient row downloaded every step (no delta rows): 150 MB D2H per step
+        dense = run_e2e(args, scene, cam, tg, R, local, delta=False)
+        result["e2e"]["dense_grad_download"] = {k: dense[k] for k in ("value", "ms_per_step", "d2h_bytes_per_step")}
+        result["e2e"]["dense_grad_download"]["single_thread"] = dense["single_thread"]
 
     mv = args.multiview if args.multiview != "auto" else ("c3" if args.config == "c1_500k" else "none")
     if mv != "none":
@@ -669,7 +673,7 @@ def pinned_like(a):
     return t.numpy()
 
 
-def run_e2e(args, scene, cam, tg, R, device, mapped=True):
+def run_e2e(args, scene, cam, tg, R, device, mapped=True, delta=True):
     """Same step through the reference-facing API with HOST buffers: every step uploads the map
     and targets (H2D), renders, reads back the images, the gradients, the pose gradient and the
     loss (D2H).  PCIe, not the GPU, bounds this path (~350 MB moved per step), so the headline
@@ -680,7 +684,12 @@ def run_e2e(args, scene, cam, tg, R, device, mapped=True):
 
     ``mapped`` (the headline): the host map is page-locked and passed as LGS_MEM_HOST_MAPPED, so
     positions / rotations / scales / opacities are copied (22 MB) while the SH rows and features of
-    just the listed Gaussians are read in place over PCIe; otherwise the whole map is copied."""
+    just the listed Gaussians are read in place over PCIe; otherwise the whole map is copied.
+    ``delta`` (the headline): each worker passes the same host gradient buffers to every backward
+    and its context runs LGS_OPT_HOST_GRAD_DELTA -- the buffers hold the dense MapGradients after
+    every call, but only the rows nonzero now cross the link (the rows nonzero in the previous call
+    are zeroed on the host); otherwise all 150 MB come back every step.  Bytes per step are the
+    library's own copy counters (lgs_ctx_transfer_bytes) plus the mapped-memory reads."""
     import numpy as np
     import torch
 
@@ -700,7 +709,7 @@ def run_e2e(args, scene, cam, tg, R, device, mapped=True):
                         "acc": pinned_like(np.zeros((H, W), np.float32))}
             self.flat = pinned_like(np.zeros(total, np.float32))
             self.grads = R.alloc_grads(n, d, K, flat=self.flat)
-            self.ctx = R.Context(device, stream="own")
+            self.ctx = R.Context(device, stream="own", host_grad_delta=delta)
             self.loss = None
 
         def step(self):
@@ -714,6 +723,7 @@ def run_e2e(args, scene, cam, tg, R, device, mapped=True):
             w.step()
         torch.cuda.synchronize()
         errs = []
+        b0 = [w.ctx.transfer_bytes() for w in workers]
 
         def loop(w):
             try:
@@ -732,23 +742,24 @@ def run_e2e(args, scene, cam, tg, R, device, mapped=True):
         dt = time.perf_counter() - t0
         if errs:
             raise errs[0]
-        return 1e3 * dt / (steps * len(workers))
+        b1 = [w.ctx.transfer_bytes() for w in workers]
+        per = steps * len(workers)  # bytes the library copied per timed step (its own counters)
+        moved = (sum(b[0] - a[0] for a, b in zip(b0, b1)) / per, sum(b[1] - a[1] for a, b in zip(b0, b1)) / per)
+        return 1e3 * dt / per, moved
 
     nthreads = max(1, args.e2e_threads)
     workers = [Worker() for _ in range(nthreads)]
-    ms = timed(workers, args.e2e_steps)
-    ms1 = timed(workers[:1], args.e2e_steps) if nthreads > 1 else ms
-    if mapped:  # copied attributes + the listed Gaussians' SH rows and features read in place
+    ms, (h2d, d2h) = timed(workers, args.e2e_steps)
+    ms1 = timed(workers[:1], args.e2e_steps)[0] if nthreads > 1 else ms
+    d2h += 6 * 4 + 8  # + the pose gradient and the loss
+    if mapped:  # + the listed Gaussians' SH rows and features read in place over PCIe
         act = R.render(hscene, cam, ctx=workers[0].ctx, host_mapped=True).stats()["active"]
-        h2d = 4 * n * 11 + sum(v.nbytes for v in htg.values()) + act * 4 * (3 * K + d)
-    else:
-        h2d = sum(v.nbytes for v in hscene.values()) + sum(v.nbytes for v in htg.values())
-    d2h = sum(v.nbytes for v in workers[0].img.values()) + workers[0].flat.nbytes + 6 * 4 + 8
+        h2d += act * 4 * (3 * K + d)
     return {"value": round(1000.0 / ms, 3), "unit": UNIT, "ms_per_step": round(ms, 3), "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "host_threads": nthreads,
             "single_thread": {"value": round(1000.0 / ms1, 3), "ms_per_step": round(ms1, 3)},
             "api": f"renderer.render(host numpy map{', host_mapped' if mapped else ''}, host targets) + "
-                   "render_backward_l1(host grads) + l1_loss(); "
+                   f"render_backward_l1(host grads{', delta rows' if delta else ''}) + l1_loss(); "
                    f"{nthreads} host threads x own lgs_ctx/stream, wall clock over all steps"}
 
 

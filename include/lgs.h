@@ -171,10 +171,20 @@ LGS_API lgs_status lgs_ctx_set_full_tile_lists(lgs_ctx* ctx, int32_t full);
  *                              with complete lists (cross-check of the bucketed order; same result);
  *   LGS_OPT_FUSED_EAGER        1: an uncaptured render with L1 targets runs the fused forward+backward
  *                              kernel of lgs_plan (for profilers that cannot see inside a graph); its
- *                              tape accepts only lgs_render_backward_l1 / _loss (else LGS_EINVAL). */
-enum { LGS_OPT_FULL_TILE_LISTS = 0, LGS_OPT_RADIX_DEPTH_ORDER = 1, LGS_OPT_FUSED_EAGER = 2 };
+ *                              tape accepts only lgs_render_backward_l1 / _loss (else LGS_EINVAL);
+ *   LGS_OPT_HOST_GRAD_DELTA    1: host gradient buffers (lgs_map_grads.memory = LGS_MEM_HOST, not
+ *                              accumulating) that the caller passes again unchanged to the next
+ *                              backward on this context are rewritten row-sparse: only the rows
+ *                              nonzero now cross the link, the rows nonzero last time are zeroed
+ *                              on the host; the buffers hold the exact dense MapGradients after
+ *                              every call.  The first call (or new buffers) writes densely.  The
+ *                              caller must not modify the buffers between calls. */
+enum { LGS_OPT_FULL_TILE_LISTS = 0, LGS_OPT_RADIX_DEPTH_ORDER = 1, LGS_OPT_FUSED_EAGER = 2, LGS_OPT_HOST_GRAD_DELTA = 3 };
 LGS_API lgs_status lgs_ctx_set_option(lgs_ctx* ctx, int32_t option, int64_t value);
 LGS_API lgs_status lgs_ctx_set_stream(lgs_ctx* ctx, void* stream);
+/* Bytes the context has copied host->device and device->host since creation (map uploads,
+ * targets, cotangents, images, gradients; reads of LGS_MEM_HOST_MAPPED memory are not copies). */
+LGS_API lgs_status lgs_ctx_transfer_bytes(const lgs_ctx* ctx, int64_t* h2d, int64_t* d2h);
 LGS_API lgs_status lgs_ctx_synchronize(lgs_ctx* ctx);
 
 /* ---- device-resident map (K9 pack: reference layouts -> device SoA) ------------------- */

@@ -13,7 +13,7 @@ LIB_PATH = os.path.join(HERE, "liblgs.so")
 
 LGS_OK, LGS_EINVAL, LGS_ECUDA, LGS_ENOMEM, LGS_ENODEV, LGS_EIO = range(6)
 LGS_MEM_HOST, LGS_MEM_DEVICE, LGS_MEM_HOST_MAPPED = 0, 1, 2
-LGS_OPT_FULL_TILE_LISTS, LGS_OPT_RADIX_DEPTH_ORDER, LGS_OPT_FUSED_EAGER = 0, 1, 2
+LGS_OPT_FULL_TILE_LISTS, LGS_OPT_RADIX_DEPTH_ORDER, LGS_OPT_FUSED_EAGER, LGS_OPT_HOST_GRAD_DELTA = 0, 1, 2, 3
 
 _fp = C.POINTER(C.c_float)
 
@@ -95,6 +95,7 @@ SIGNATURES = [
     ("lgs_ctx_create", C.c_int, [C.c_int32, C.c_void_p, C.POINTER(C.c_void_p)]),
     ("lgs_ctx_set_full_tile_lists", C.c_int, [C.c_void_p, C.c_int32]),
     ("lgs_ctx_set_option", C.c_int, [C.c_void_p, C.c_int32, C.c_int64]),
+    ("lgs_ctx_transfer_bytes", C.c_int, [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     ("lgs_ctx_destroy", C.c_int, [C.c_void_p]),
     ("lgs_ctx_set_stream", C.c_int, [C.c_void_p, C.c_void_p]),
     ("lgs_ctx_synchronize", C.c_int, [C.c_void_p]),

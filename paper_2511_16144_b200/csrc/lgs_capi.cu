@@ -107,6 +107,13 @@ struct lgs_ctx {
   bool full_lists = false;  // lgs_ctx_set_full_tile_lists: single-pass binning of every pair
   bool radix_depth = false;  // LGS_OPT_RADIX_DEPTH_ORDER: CUB radix sort for the depth order (cross-check)
   bool fused_eager = false;  // LGS_OPT_FUSED_EAGER: uncaptured fused-L1 renders run the fused kernel
+  bool host_grad_delta = false;  // LGS_OPT_HOST_GRAD_DELTA: host gradients rewritten row-sparse
+  // host-gradient delta mode: the destination of the previous backward and the rows it left nonzero
+  std::array<float*, 6> delta_dst{};
+  int64_t delta_n = -1;
+  std::vector<uint32_t> delta_rows;
+  // bytes this context moved between host and device memory by copies (lgs_ctx_transfer_bytes)
+  std::atomic<int64_t> bytes_h2d{0}, bytes_d2h{0};
   cudaStream_t cond_stream = nullptr;  // captures the body of a plan's conditional node
   cudaStream_t cond_parent = nullptr;  // the capturing stream while a body is captured
   // lgs_plan capture: the zero rows of the plan's (non-accumulating) gradient buffers are written
@@ -384,6 +391,7 @@ lgs_status make_devcam(const lgs_camera* cam, const lgs_render_config* cfg, DevC
 
 lgs_status copy_in(lgs_ctx* ctx, void* dst, const void* src, size_t bytes, int memory) {
   if (bytes == 0) return LGS_OK;
+  if (memory == LGS_MEM_HOST) ctx->bytes_h2d += (int64_t)bytes;
   LGS_CUDA(cudaMemcpyAsync(dst, src, bytes, memory == LGS_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
                            ctx->stream));
   return LGS_OK;
@@ -578,8 +586,20 @@ LGS_API lgs_status lgs_ctx_set_option(lgs_ctx* ctx, int32_t option, int64_t valu
     case LGS_OPT_FULL_TILE_LISTS: ctx->full_lists = value != 0; return LGS_OK;
     case LGS_OPT_RADIX_DEPTH_ORDER: ctx->radix_depth = value != 0; return LGS_OK;
     case LGS_OPT_FUSED_EAGER: ctx->fused_eager = value != 0; return LGS_OK;
+    case LGS_OPT_HOST_GRAD_DELTA:
+      ctx->host_grad_delta = value != 0;
+      ctx->delta_n = -1;  // the next backward writes densely
+      ctx->delta_rows.clear();
+      return LGS_OK;
     default: return fail(LGS_EINVAL, "unknown context option");
   }
+}
+
+LGS_API lgs_status lgs_ctx_transfer_bytes(const lgs_ctx* ctx, int64_t* h2d, int64_t* d2h) {
+  if (!ctx) return fail(LGS_EINVAL, "ctx is NULL");
+  if (h2d) *h2d = ctx->bytes_h2d.load();
+  if (d2h) *d2h = ctx->bytes_d2h.load();
+  return LGS_OK;
 }
 
 LGS_API lgs_status lgs_ctx_destroy(lgs_ctx* ctx) {
@@ -840,6 +860,7 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
     fo.t_rgb = targets->rgb; fo.t_depth = targets->depth; fo.t_feat = targets->feat;
     if (targets->memory == LGS_MEM_HOST) {
       TRYB(dalloc(ctx, &tstage, npix * (4 + d)));
+      ctx->bytes_h2d += (int64_t)(sizeof(float) * npix * (4 + (size_t)(targets->feat ? d : 0)));
       CUDAB(cudaMemcpyAsync(tstage, targets->rgb, sizeof(float) * npix * 3, cudaMemcpyHostToDevice, s));
       CUDAB(cudaMemcpyAsync(tstage + npix * 3, targets->depth, sizeof(float) * npix, cudaMemcpyHostToDevice, s));
       if (d > 0)
@@ -1058,6 +1079,8 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
     if (di.depth) CUDAB(cudaMemcpyAsync(out->depth, di.depth, sizeof(float) * npix, cudaMemcpyDeviceToHost, s));
     if (di.feat) CUDAB(cudaMemcpyAsync(out->feat, di.feat, sizeof(float) * npix * d, cudaMemcpyDeviceToHost, s));
     if (di.acc) CUDAB(cudaMemcpyAsync(out->acc, di.acc, sizeof(float) * npix, cudaMemcpyDeviceToHost, s));
+    ctx->bytes_d2h += (int64_t)(sizeof(float) * npix * ((di.rgb ? 3 : 0) + (di.depth ? 1 : 0) + (di.feat ? d : 0) +
+                                                       (di.acc ? 1 : 0)));
     dfree(ctx, di.rgb); dfree(ctx, di.depth); dfree(ctx, di.feat); dfree(ctx, di.acc);
     CUDAB(cudaStreamSynchronize(s));
   }
@@ -1093,6 +1116,99 @@ LGS_API lgs_status lgs_render(lgs_ctx* ctx, const lgs_gaussians* src, const lgs_
 // backward
 // -------------------------------------------------------------------------------------------
 namespace {
+
+// ---- host-gradient delta mode (LGS_OPT_HOST_GRAD_DELTA) --------------------------------------
+// With the depth-layered binning a view's gradient is nonzero on a few thousand of N rows, yet
+// the dense MapGradients (renderer.hpp:59-68) of a host caller is N x (11 + 3K + d) floats (150 MB
+// at the headline size).  When the caller hands the same host buffers to every backward and leaves
+// them alone in between, the rows zero now AND in the previous backward already hold zeros: only
+// the rows nonzero now (packed on the device as (index, row) records, sparse_reduce.cu) cross the
+// link, and the rows nonzero last time but not now are zeroed on the host.  The buffers hold the
+// exact dense gradient after every call.
+
+// rows of the device gradient `src` with a nonzero component -> (index, row) records on the host
+lgs_status pack_nonzero_rows(lgs_ctx* ctx, float* const src[6], int64_t n, int K, int d, std::vector<float>* recs,
+                             uint32_t* rows_out) {
+  cudaStream_t s = ctx->stream;
+  const int width[6] = {3, 4, 3, 1, 3 * K, d};
+  const int R = rows_values(width, src);
+  uint32_t *list = nullptr, *cnt = nullptr;
+  LGS_TRY(dalloc(ctx, &list, (size_t)n));
+  LGS_TRY(dalloc(ctx, &cnt, 1));
+  launch_rows_scan(src, width, n, list, cnt, s);
+  uint32_t rows = 0;
+  LGS_CUDA(cudaMemcpyAsync(&rows, cnt, sizeof rows, cudaMemcpyDeviceToHost, s));
+  LGS_CUDA(cudaStreamSynchronize(s));
+  ctx->bytes_d2h += (int64_t)sizeof rows;
+  recs->resize((size_t)rows * (R + 1));
+  if (rows) {
+    float* drec = nullptr;
+    LGS_TRY(dalloc(ctx, &drec, (size_t)rows * (R + 1)));
+    launch_rows_pack(src, width, n, list, cnt, rows, drec, s);
+    LGS_CUDA(cudaMemcpyAsync(recs->data(), drec, sizeof(float) * recs->size(), cudaMemcpyDeviceToHost, s));
+    ctx->bytes_d2h += (int64_t)(sizeof(float) * recs->size());
+    dfree(ctx, drec);
+  }
+  dfree(ctx, list);
+  dfree(ctx, cnt);
+  LGS_CUDA(cudaStreamSynchronize(s));
+  *rows_out = rows;
+  return LGS_OK;
+}
+
+// write (or zero) row i of the six host arrays in the reference layouts; rec = R values or nullptr
+void host_row(float* const dst[6], const int width[6], int64_t n, uint32_t i, const float* rec) {
+  int off = 0;
+  for (int a = 0; a < 6; ++a) {
+    if (!dst[a] || !width[a]) continue;
+    for (int j = 0; j < width[a]; ++j) {
+      float* e = a == 5 ? dst[5] + (int64_t)j * n + i : dst[a] + (int64_t)i * width[a] + j;
+      *e = rec ? rec[off + j] : 0.f;
+    }
+    off += width[a];
+  }
+}
+
+lgs_status host_grads_delta(lgs_ctx* ctx, float* const dst[6], float* const src[6], int64_t n, int K, int d) {
+  std::vector<float> recs;
+  uint32_t rows = 0;
+  LGS_TRY(pack_nonzero_rows(ctx, src, n, K, d, &recs, &rows));
+  int width[6] = {3, 4, 3, 1, 3 * K, d};
+  for (int a = 0; a < 6; ++a)
+    if (!src[a]) width[a] = 0;
+  const int R = rows_values(width, src);
+  for (uint32_t i : ctx->delta_rows) host_row(dst, width, n, i, nullptr);  // last call's rows -> 0
+  ctx->delta_rows.resize(rows);
+  for (uint32_t k = 0; k < rows; ++k) {
+    const float* r = recs.data() + (size_t)k * (R + 1);
+    const uint32_t i = __builtin_bit_cast(uint32_t, r[0]);
+    host_row(dst, width, n, i, r + 1);
+    ctx->delta_rows[k] = i;
+  }
+  return LGS_OK;
+}
+
+// after a dense write: remember the destination and its nonzero rows for the next delta backward
+lgs_status host_grads_note_rows(lgs_ctx* ctx, float* const src[6], int64_t n, int K, int d,
+                                const std::array<float*, 6>& key) {
+  cudaStream_t s = ctx->stream;
+  const int width[6] = {3, 4, 3, 1, 3 * K, d};
+  uint32_t *list = nullptr, *cnt = nullptr;
+  LGS_TRY(dalloc(ctx, &list, (size_t)n));
+  LGS_TRY(dalloc(ctx, &cnt, 1));
+  launch_rows_scan(src, width, n, list, cnt, s);
+  uint32_t rows = 0;
+  LGS_CUDA(cudaMemcpyAsync(&rows, cnt, sizeof rows, cudaMemcpyDeviceToHost, s));
+  LGS_CUDA(cudaStreamSynchronize(s));
+  ctx->delta_rows.resize(rows);
+  if (rows) LGS_CUDA(cudaMemcpyAsync(ctx->delta_rows.data(), list, sizeof(uint32_t) * rows, cudaMemcpyDeviceToHost, s));
+  dfree(ctx, list);
+  dfree(ctx, cnt);
+  LGS_CUDA(cudaStreamSynchronize(s));
+  ctx->delta_dst = key;
+  ctx->delta_n = n;
+  return LGS_OK;
+}
 
 lgs_status run_backward(lgs_ctx* ctx, const lgs_saved* t, const BwdIn& in_dev, lgs_map_grads* grads, float* pose_grad,
                         bool async_pose = false) {
@@ -1168,9 +1284,18 @@ lgs_status run_backward(lgs_ctx* ctx, const lgs_saved* t, const BwdIn& in_dev, l
                      grads->feature};
     float* src[6] = {go.position, go.rotation, go.log_scale, go.opacity_logit, go.sh, go.feature};
     const size_t szs[6] = {sz_pos, sz_rot, sz_ls, sz_op, sz_sh, sz_ft};
-    for (int k = 0; k < 6; ++k)
-      if (dst[k] && src[k] && szs[k])
-        LGS_CUDA(cudaMemcpyAsync(dst[k], src[k], sizeof(float) * szs[k], cudaMemcpyDeviceToHost, s));
+    const std::array<float*, 6> key = {dst[0], dst[1], dst[2], dst[3], dst[4], dst[5]};
+    const bool delta = ctx->host_grad_delta && !go.accumulate && ctx->delta_n == n && ctx->delta_dst == key;
+    if (delta) {
+      LGS_TRY(host_grads_delta(ctx, dst, src, n, K, d));  // synchronizes
+    } else {
+      for (int k = 0; k < 6; ++k)
+        if (dst[k] && src[k] && szs[k]) {
+          LGS_CUDA(cudaMemcpyAsync(dst[k], src[k], sizeof(float) * szs[k], cudaMemcpyDeviceToHost, s));
+          ctx->bytes_d2h += (int64_t)(sizeof(float) * szs[k]);
+        }
+      if (ctx->host_grad_delta && !go.accumulate) LGS_TRY(host_grads_note_rows(ctx, src, n, K, d, key));
+    }
   }
   double hpose[6];
   if (pose_grad && async_pose) {

@@ -94,7 +94,7 @@ class Context:
     the reference's "concurrent renders between map mutations" contract)."""
 
     def __init__(self, device: int = 0, stream=None, full_lists: bool = False, radix_depth_order: bool = False,
-                 fused_eager: bool = False):
+                 fused_eager: bool = False, host_grad_delta: bool = False):
         L = _lib.load()
         if stream == "own":
             stream = None
@@ -114,9 +114,17 @@ class Context:
             check(L.lgs_ctx_set_option(h, _lib.LGS_OPT_RADIX_DEPTH_ORDER, 1))
         if fused_eager:
             check(L.lgs_ctx_set_option(h, _lib.LGS_OPT_FUSED_EAGER, 1))
+        if host_grad_delta:  # host gradient buffers reused unchanged: row-sparse rewrites (include/lgs.h)
+            check(L.lgs_ctx_set_option(h, _lib.LGS_OPT_HOST_GRAD_DELTA, 1))
 
     def synchronize(self):
         check(_lib.load().lgs_ctx_synchronize(self.h))
+
+    def transfer_bytes(self):
+        """(host->device, device->host) bytes this context has copied since creation."""
+        a, b = C.c_int64(), C.c_int64()
+        check(_lib.load().lgs_ctx_transfer_bytes(self.h, C.byref(a), C.byref(b)))
+        return a.value, b.value
 
     @property
     def launches(self) -> int:
