@@ -163,49 +163,18 @@ __device__ __forceinline__ void depth_emit(const DepthOut& o, const uint32_t* __
   }
 }
 
-// big buckets: *big_n of them, ids in big_ids
-__global__ void depth_rank_kernel(const uint2* __restrict__ tmp, int64_t n, uint32_t base,
-                                  const u64* __restrict__ off, const uint32_t* __restrict__ tiles,
-                                  const uint2* __restrict__ rect, const uint32_t* __restrict__ cut, int mode,
-                                  DepthOut o, uint32_t* __restrict__ big_n, uint32_t* __restrict__ big_ids) {
-  griddep_wait();
-  if (o.gate && *o.gate == 0u) return;
-  const int64_t p0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const uint32_t ra = cut ? cnt_of(off[cut_end_of(cut)]) : 0u;  // Gaussians in layer A
-  const int64_t p = mode == kDepthRest ? p0 + ra : p0;
-  if (p >= (mode == kDepthLayerA ? (int64_t)ra : n)) return;
-  const uint2 me = tmp[p];
-  const uint32_t b = depth_bucket(me.x, base);
-  if (b == kDepthBuckets) {  // culled: no pairs, any order
-    o.idx_sorted[p] = me.y;
-    if (o.cnt_sorted) o.cnt_sorted[p] = 0u;
-    return;
-  }
-  const uint32_t lo = cnt_of(off[b]), hi = cnt_of(off[b + 1]);
-  if (hi - lo > kMaxRankBucket) {
-    if (p == lo) big_ids[atomicAdd(big_n, 1u)] = b;
-    return;
-  }
-  uint32_t rank = 0;
-  for (uint32_t q = lo; q < hi; ++q) rank += precedes(tmp[q], me) ? 1u : 0u;
-  depth_emit(o, tiles, rect, lo + rank, me.y, ra);
-}
-
-// One CTA per big bucket: bitonic sort of the padded composite keys in `scratch` (2 n entries:
-// the padded sizes of all big buckets sum to less than twice their element count).
-__global__ void __launch_bounds__(1024) depth_big_kernel(const uint2* __restrict__ tmp, const u64* __restrict__ off,
-                                                         const uint32_t* __restrict__ tiles,
-                                                         const uint2* __restrict__ rect,
-                                                         const uint32_t* __restrict__ cut,
-                                                         const uint32_t* __restrict__ big_n,
-                                                         const uint32_t* __restrict__ big_ids,
-                                                         unsigned long long* __restrict__ scratch,
-                                                         uint32_t* __restrict__ cursor, DepthOut o) {
-  griddep_wait();
-  const uint32_t nbig = *big_n;
+// Big buckets (more than kMaxRankBucket members, e.g. splats at one identical depth): per bucket one
+// bitonic sort of the padded composite keys (key << 32 | index) in `scratch` (2 n entries: the padded
+// sizes of all big buckets sum to less than twice their element count), buckets k = first, first +
+// stride, ... of the *big_n listed in big_ids, by the calling CTA.
+__device__ void sort_big_buckets(const uint2* __restrict__ tmp, const u64* __restrict__ off,
+                                 const uint32_t* __restrict__ tiles, const uint2* __restrict__ rect,
+                                 const uint32_t* __restrict__ cut, uint32_t nbig, const uint32_t* __restrict__ big_ids,
+                                 unsigned long long* __restrict__ scratch, uint32_t* __restrict__ cursor,
+                                 const DepthOut& o, uint32_t first, uint32_t stride) {
   const uint32_t ra = cut ? cnt_of(off[cut_end_of(cut)]) : 0u;
   __shared__ uint32_t s_base;
-  for (uint32_t k = blockIdx.x; k < nbig; k += gridDim.x) {
+  for (uint32_t k = first; k < nbig; k += stride) {
     const uint32_t b = big_ids[k];
     const uint32_t lo = cnt_of(off[b]), m = cnt_of(off[b + 1]) - lo;
     uint32_t M = 1;
@@ -244,6 +213,63 @@ __global__ void __launch_bounds__(1024) depth_big_kernel(const uint2* __restrict
   }
 }
 
+// Exact in-bucket rank of every selected element.  Big buckets are listed (big_n, big_ids); with
+// `done` (layer A) the last CTA to finish sorts them itself -- one launch less in the chain, the
+// big-bucket case being rare -- otherwise depth_big_kernel follows.
+__global__ void depth_rank_kernel(const uint2* __restrict__ tmp, int64_t n, uint32_t base,
+                                  const u64* __restrict__ off, const uint32_t* __restrict__ tiles,
+                                  const uint2* __restrict__ rect, const uint32_t* __restrict__ cut, int mode,
+                                  DepthOut o, uint32_t* __restrict__ big_n, uint32_t* __restrict__ big_ids,
+                                  uint32_t* __restrict__ done, unsigned long long* __restrict__ scratch,
+                                  uint32_t* __restrict__ cursor) {
+  griddep_wait();
+  if (o.gate && *o.gate == 0u) return;
+  const int64_t p0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t ra = cut ? cnt_of(off[cut_end_of(cut)]) : 0u;  // Gaussians in layer A
+  const int64_t p = mode == kDepthRest ? p0 + ra : p0;
+  if (p < (mode == kDepthLayerA ? (int64_t)ra : n)) {
+    const uint2 me = tmp[p];
+    const uint32_t b = depth_bucket(me.x, base);
+    if (b == kDepthBuckets) {  // culled: no pairs, any order
+      o.idx_sorted[p] = me.y;
+      if (o.cnt_sorted) o.cnt_sorted[p] = 0u;
+    } else {
+      const uint32_t lo = cnt_of(off[b]), hi = cnt_of(off[b + 1]);
+      if (hi - lo > kMaxRankBucket) {
+        if (p == lo) big_ids[atomicAdd(big_n, 1u)] = b;
+      } else {
+        uint32_t rank = 0;
+        for (uint32_t q = lo; q < hi; ++q) rank += precedes(tmp[q], me) ? 1u : 0u;
+        depth_emit(o, tiles, rect, lo + rank, me.y, ra);
+      }
+    }
+  }
+  if (!done) return;
+  __shared__ bool s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const uint32_t nbig = atomicAdd(big_n, 0u);
+  if (nbig) sort_big_buckets(tmp, off, tiles, rect, cut, nbig, big_ids, scratch, cursor, o, 0u, 1u);
+}
+
+__global__ void __launch_bounds__(1024) depth_big_kernel(const uint2* __restrict__ tmp, const u64* __restrict__ off,
+                                                         const uint32_t* __restrict__ tiles,
+                                                         const uint2* __restrict__ rect,
+                                                         const uint32_t* __restrict__ cut,
+                                                         const uint32_t* __restrict__ big_n,
+                                                         const uint32_t* __restrict__ big_ids,
+                                                         unsigned long long* __restrict__ scratch,
+                                                         uint32_t* __restrict__ cursor, DepthOut o) {
+  griddep_wait();
+  sort_big_buckets(tmp, off, tiles, rect, cut, *big_n, big_ids, scratch, cursor, o, blockIdx.x, gridDim.x);
+}
+
 // ------------------------------------------------------------------------------------------
 // host side: one scratch block carved into the buffers below (DepthOrderState keeps the carving
 // so the second layered pass can finish the order later)
@@ -270,7 +296,7 @@ size_t depth_order_temp_bytes(int64_t n) {
 
 // scalars (zeroed together): cut, big-bucket counts of layer A / the rest, bitonic scratch
 // allocator, culled-slot allocator
-enum { kScCut = 0, kScBigA = 1, kScBigR = 2, kScScratch = 3, kScCulled = 4, kScalars = 8 };
+enum { kScCut = 0, kScBigA = 1, kScBigR = 2, kScScratch = 3, kScCulled = 4, kScRankDone = 5, kScalars = 8 };
 
 struct DepthCarve {
   unsigned long long *hist, *off;
@@ -332,7 +358,7 @@ void launch_depth_order(const ViewBufs& v, int64_t n, float near_plane, void* te
   depth_scatter_kernel<<<grid, 256, 0, s>>>(v.dkey, n, c.base, c.off, c.slot, nullptr, kDepthAll, c.tmp, nullptr, nullptr,
                                             nullptr);
   depth_rank_kernel<<<grid, 256, 0, s>>>(c.tmp, n, c.base, c.off, v.tiles, v.rect, nullptr, kDepthAll, o,
-                                         c.sc + kScBigA, c.big_a);
+                                         c.sc + kScBigA, c.big_a, nullptr, nullptr, nullptr);
   depth_big_kernel<<<8, 1024, 0, s>>>(c.tmp, c.off, v.tiles, v.rect, nullptr, c.sc + kScBigA, c.big_a, c.scratch,
                                       c.sc + kScScratch, o);
 }
@@ -379,12 +405,10 @@ void launch_depth_order_layer_a(const ViewBufs& v, int64_t n, float near_plane, 
   launch_pdl(depth_scatter_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, s, (const uint32_t*)v.dkey, n,
              c.base, (const u64*)c.off, (const uint32_t*)c.slot, cut, (int)kDepthLayerA, c.tmp, ra, (uint32_t*)nullptr,
              (const uint32_t*)nullptr);
+  // (big buckets, if any, are sorted by the rank kernel's last CTA)
   launch_pdl(depth_rank_kernel, dim3((unsigned)((ga + 255) / 256)), dim3(256), 0, s, (const uint2*)c.tmp, n, c.base,
              (const u64*)c.off, (const uint32_t*)v.tiles, (const uint2*)v.rect, cut, (int)kDepthLayerA, o,
-             c.sc + kScBigA, c.big_a);
-  launch_pdl(depth_big_kernel, dim3(8), dim3(1024), 0, s, (const uint2*)c.tmp, (const u64*)c.off,
-             (const uint32_t*)v.tiles, (const uint2*)v.rect, cut, (const uint32_t*)(c.sc + kScBigA),
-             (const uint32_t*)c.big_a, c.scratch, c.sc + kScScratch, o);
+             c.sc + kScBigA, c.big_a, c.sc + kScRankDone, c.scratch, c.sc + kScScratch);
 }
 
 // Layer-A tile lists: one CTA per run of kSegTiles tiles of a tile row.  Its warps split the R_A
@@ -498,7 +522,7 @@ void launch_depth_order_rest(const ViewBufs& v, int64_t n, float near_plane, voi
   depth_scatter_kernel<<<grid, 256, 0, s>>>(v.dkey, n, c.base, c.off, c.slot, cut, kDepthRest, c.tmp, nullptr,
                                             c.sc + kScCulled, gate);
   depth_rank_kernel<<<grid, 256, 0, s>>>(c.tmp, n, c.base, c.off, v.tiles, v.rect, cut, kDepthRest, o,
-                                         c.sc + kScBigR, c.big_r);
+                                         c.sc + kScBigR, c.big_r, nullptr, nullptr, nullptr);
   depth_big_kernel<<<8, 1024, 0, s>>>(c.tmp, c.off, v.tiles, v.rect, cut, c.sc + kScBigR, c.big_r, c.scratch,
                                       c.sc + kScScratch, o);
 }

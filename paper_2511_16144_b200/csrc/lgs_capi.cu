@@ -930,7 +930,7 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
       // Layered lists are short and even (every tile stops at its saturation): the blend kernels
       // take tiles in natural order (measured as fast as longest-list-first, one launch less).
       t->lpt_order = false;
-      ctx->launches += 6;
+      ctx->launches += 5;  // the rank kernel sorts big depth buckets itself (no depth_big launch)
       if (targets && !fuse) LGS_CUDA(cudaMemsetAsync(t->loss, 0, sizeof(double), s));
       FwdOut fo1 = fo;
       fo1.unfinished = unfinished;
