@@ -37,6 +37,34 @@ struct FusedSmem {
                                                   // (pixel 0 c, pixel 1 c, pixel 0 c+1, pixel 1 c+1)
 };
 
+
+#ifdef LGS_FUSED_BULK
+// Experiment: the colour and feature rows of a staged batch are copied by the bulk-copy
+// (TMA) engine, cp.async.bulk global -> shared completing on an mbarrier, instead of LDG -> STS.
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_addr(dst)),
+               "l"(src), "r"(bytes), "r"(smem_addr(bar))
+               : "memory");
+}
+__device__ __forceinline__ void bar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(uint64_t* bar) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok)
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(smem_addr(bar)), "r"(parity)
+        : "memory");
+}
+#endif
+
 template <int SLOTS>
 __device__ __forceinline__ void fused_transpose_reduce(float (&v)[SLOTS], int lane) {
 #pragma unroll
@@ -83,7 +111,18 @@ __global__ void __launch_bounds__(kBlock / 2) blend_fused_l1_kernel(DevMap m, De
 
   // stage list entries [b0, b0 + cnt) of the tile's list (range.x-relative positions); (xc, yc) =
   // the tile centre the conic frames are centred on
+#ifdef LGS_FUSED_BULK
+  __shared__ alignas(8) uint64_t s_bar;
+  uint32_t bar_parity = 0;
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&s_bar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+#endif
   auto stage = [&](uint32_t list0, int cnt, float xc, float yc) {
+#ifdef LGS_FUSED_BULK
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // earlier generic reads before async writes
+#endif
     for (int e = tid; e < cnt; e += NT) {
       const uint32_t g = __ldg(tl.vals + list0 + e);
       sm.gid[e] = g;
@@ -94,13 +133,27 @@ __global__ void __launch_bounds__(kBlock / 2) blend_fused_l1_kernel(DevMap m, De
       sm.fa[e] = f.a;
       sm.fb[e] = f.b;
       sm.rect[e] = __ldg(v.rect + g);
+#ifdef LGS_FUSED_BULK
+      bar_expect_tx(&s_bar, 16u * (1u + (DP > 0 ? DQ : 0)));
+      bulk_g2s(&sm.col[e], v.color + g, 16u, &s_bar);
+      if (DP > 0) bulk_g2s(&sm.feat[e][0], reinterpret_cast<const float4*>(m.feat) + (size_t)g * DQ, 16u * DQ, &s_bar);
+#else
       sm.col[e] = __ldg(v.color + g);
       if (DP > 0) {
         const float4* fg = reinterpret_cast<const float4*>(m.feat) + (size_t)g * DQ;
 #pragma unroll
         for (int q = 0; q < DQ; ++q) sm.feat[e][q] = __ldg(fg + q);
       }
+#endif
     }
+  };
+  // after stage() and the __syncthreads that follows it: the bulk copies have landed
+  auto staged = [&]() {
+#ifdef LGS_FUSED_BULK
+    if (tid == 0) bar_arrive(&s_bar);
+    bar_wait(&s_bar, bar_parity);
+    bar_parity ^= 1u;
+#endif
   };
 
   for (int tile = next_tile(tl, ntiles, &s_slot); tile >= 0; tile = next_tile(tl, ntiles, &s_slot)) {
@@ -127,6 +180,7 @@ __global__ void __launch_bounds__(kBlock / 2) blend_fused_l1_kernel(DevMap m, De
       stage(range.x + pos, cnt, xc, yc);
       res_batch = (int)(pos / NB);
       __syncthreads();
+      staged();
       // composite one staged entry given its pixels' alphas; a pixel that does not contribute gets
       // alpha = 0, which leaves T and the accumulators exactly unchanged (w = +0)
       auto composite = [&](int e, float2 al, bool in0, bool in1, float depth_z) {
@@ -273,6 +327,7 @@ __global__ void __launch_bounds__(kBlock / 2) blend_fused_l1_kernel(DevMap m, De
         stage(range.x + bpos, cnt, xc, yc);
         res_batch = b;
         __syncthreads();
+        staged();
       }
       const int e_top = (int)min((int64_t)cnt - 1, (int64_t)warp_last - 1 - (int64_t)bpos);
       for (int e = e_top; e >= 0; --e) {
