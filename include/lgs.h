@@ -369,6 +369,47 @@ LGS_API lgs_status lgs_map_file_write(const char* path, const lgs_gaussians* src
 LGS_API lgs_status lgs_map_load(lgs_ctx* ctx, const char* path, int32_t expected_dim, lgs_map** out);
 LGS_API lgs_status lgs_map_save(lgs_ctx* ctx, const lgs_map* map, const char* path, const uint64_t* anchors);
 
+/* ---- map pruning (SPEC.md:471-535 [MODULE] pruning) ---------------------
+ * The reference's pruning.cpp is a placeholder (proj/src/pruning.cpp:1); these restate the SPEC's
+ * operations on the resident map, with the reference's KD-tree KNN order (kdtree.hpp:36-55:
+ * ascending (squared distance, index), the live filter applied inside the search).
+ *
+ * find_language_redundant (Eq. 4): Gaussians visited in ascending index; a live
+ *   G_i takes its k_neighbors nearest LIVE others and marks each G_j among them with
+ *   |p_i - p_j|^2 < tau_dist^2 and cos(f_i, f_j) > tau_sim; a marked Gaussian is dead at once (it
+ *   marks nothing and leaves every later neighbour set).  Distances and cosines in fp64 from the
+ *   map's fp32 values: d2 = (dx*dx + dy*dy) + dz*dz, cos = dot / (|f_i| |f_j|) with sequential
+ *   channel sums and no fused multiply-adds; a zero-norm feature is similar to nothing, and a map
+ *   without features (d = 0) or with fewer than 2 Gaussians marks nothing.
+ * find_geometric: sigmoid(opacity logit) < alpha_min OR max_a exp(log_scale_a)
+ *   > scale_max, in fp64.
+ * Flags are one byte per Gaussian (1 = marked) in host or device memory (`memory`), counts
+ * optional.  k_neighbors 1..32, tau_dist > 0, -1 < tau_sim <= 1, else LGS_EINVAL. */
+typedef struct {
+  int32_t k_neighbors; /* K (default 8) */
+  double tau_dist;     /* metres (0.02) */
+  double tau_sim;      /* cosine (0.9) */
+  double alpha_min;    /* opacity (0.05) */
+  double scale_max;    /* metres (0.5) */
+} lgs_prune_config;
+LGS_API lgs_prune_config lgs_prune_config_default(void);
+LGS_API lgs_status lgs_find_language_redundant(lgs_ctx* ctx, const lgs_map* map, const lgs_prune_config* cfg,
+                                               uint8_t* flags, int32_t memory, int64_t* count);
+LGS_API lgs_status lgs_find_geometric(lgs_ctx* ctx, const lgs_map* map, const lgs_prune_config* cfg, uint8_t* flags,
+                                      int32_t memory, int64_t* count);
+/* prune: deletes the union of both sets from the map and, when `adam` is given,
+ * the same rows of its moments; survivors keep their relative order (so the caller's stable IDs
+ * follow by deleting the flagged rows).  The two flag arrays (optional, host or device, OLD
+ * indexing) report each rule's set; *kept = the new size.  Tapes and plans made on the map before
+ * the call are invalid afterwards (the map changed size): destroy them.  A host-mapped map is
+ * rejected (its owner compacts it). */
+LGS_API lgs_status lgs_prune(lgs_ctx* ctx, lgs_map* map, lgs_adam* adam, const lgs_prune_config* cfg,
+                             uint8_t* removed_language, uint8_t* removed_geometric, int32_t memory, int64_t* kept);
+/* Work counters of the last find_language_redundant on this context: Gaussians with a similar
+ * neighbour inside tau_dist (the only ones the greedy sweep can touch), dependency rounds of the
+ * parallel sweep (csrc/prune.cu). */
+LGS_API lgs_status lgs_prune_stats(const lgs_ctx* ctx, int64_t* candidates, int64_t* rounds);
+
 /* ---- captured steps (CUDA graphs) ---------------------------------------------------------------
  * A plan is one forward (fused L1 against device targets) + backward (device gradients, pose
  * gradient to pinned-host / device memory or NULL) on a resident map and a fixed camera,

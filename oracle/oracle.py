@@ -70,8 +70,8 @@ _lib = None
 def lib():
     global _lib
     if _lib is None:
-        if not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(
-                os.path.join(_HERE, "lgs_oracle.c")):
+        if not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < max(
+                os.path.getmtime(os.path.join(_HERE, f)) for f in ("lgs_oracle.c", "prune_oracle.c")):
             build()
         L = C.CDLL(_LIB_PATH)
         L.orc_render_forward.restype = C.c_void_p
@@ -80,6 +80,11 @@ def lib():
         L.orc_render_backward.restype = C.c_int
         L.orc_render_backward.argtypes = [C.c_void_p, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp]
         L.orc_render_free.argtypes = [C.c_void_p]
+        L.orc_find_language_redundant.restype = C.c_int64
+        L.orc_find_language_redundant.argtypes = [C.c_int64, C.c_int32, _dp, _dp, C.c_int32, C.c_double, C.c_double,
+                                                  _u8p]
+        L.orc_find_geometric.restype = C.c_int64
+        L.orc_find_geometric.argtypes = [C.c_int64, _dp, _dp, C.c_double, C.c_double, _u8p]
         for f in ("orc_render_num_projected", "orc_render_num_evaluated", "orc_render_num_contributions"):
             getattr(L, f).restype = C.c_int64
             getattr(L, f).argtypes = [C.c_void_p]
@@ -415,3 +420,35 @@ class Rng:
         if getattr(self, "_h", None):
             lib().orc_rng_free(self._h)
             self._h = None
+
+
+# --------------------------------------------------------------------------------------------
+# (D) map pruning (prune_oracle.c)
+# --------------------------------------------------------------------------------------------
+
+def prune_inputs(scene):
+    """fp64 copies of the map's fp32 values, as the GPU sees them: pos [N][3], feat [d][N]."""
+    pos = np.ascontiguousarray(np.asarray(scene["pos"], np.float32), dtype=np.float64)
+    feat = np.ascontiguousarray(np.asarray(scene["feat"], np.float32), dtype=np.float64)
+    return pos, feat
+
+
+def find_language_redundant(scene, k=8, tau_dist=0.02, tau_sim=0.9) -> np.ndarray:
+    """uint8 flags of the SPEC's greedy Eq. 4 sweep (prune_oracle.c)."""
+    pos, feat = prune_inputs(scene)
+    n, d = pos.shape[0], feat.shape[0]
+    flags = np.zeros(max(n, 1), np.uint8)
+    r = lib().orc_find_language_redundant(n, d, _ptr(pos, _dp), _ptr(feat, _dp), int(k), float(tau_dist),
+                                          float(tau_sim), _ptr(flags, _u8p))
+    if r < 0:
+        raise MemoryError("orc_find_language_redundant")
+    return flags[:n]
+
+
+def find_geometric(scene, alpha_min=0.05, scale_max=0.5) -> np.ndarray:
+    op = np.ascontiguousarray(np.asarray(scene["opac"], np.float32), dtype=np.float64)
+    ls = np.ascontiguousarray(np.asarray(scene["log_s"], np.float32), dtype=np.float64)
+    flags = np.zeros(max(op.shape[0], 1), np.uint8)
+    lib().orc_find_geometric(op.shape[0], _ptr(op, _dp), _ptr(ls, _dp), float(alpha_min), float(scale_max),
+                             _ptr(flags, _u8p))
+    return flags[:op.shape[0]]

@@ -32,6 +32,9 @@ def lib():
     global _lib
     if _lib is None:
         L = C.CDLL(LIB_PATH)
+        L.ref_find_language_redundant.restype = C.c_int64
+        L.ref_find_language_redundant.argtypes = [C.c_int64, C.c_int32, _dp, _dp, C.c_int32, C.c_double,
+                                                  C.c_double, C.POINTER(C.c_uint8)]
         L.ref_render.restype = C.c_void_p
         L.ref_render.argtypes = [C.POINTER(OrcMap), C.POINTER(OrcCamera), C.POINTER(OrcConfig), _dp, _dp, _dp, _dp]
         L.ref_num_projected.restype = C.c_int64
@@ -188,3 +191,14 @@ def bench_bands(scene, cam, targets, threads, iters, cfg=None):
     sec = lib().ref_bench_bands(C.byref(m), C.byref(c), C.byref(cfg), *(_ptr(x) for x in t), threads, iters,
                                 _ptr(loss))
     return sec, float(loss[0])
+
+
+def find_language_redundant(scene, k=8, tau_dist=0.02, tau_sim=0.9):
+    """The SPEC's Eq. 4 sweep on the reference's own KdTree3 (ref_bridge.cpp); uint8 flags."""
+    from oracle.oracle import prune_inputs
+    pos, feat = prune_inputs(scene)
+    n, d = pos.shape[0], feat.shape[0]
+    flags = np.zeros(max(n, 1), np.uint8)
+    lib().ref_find_language_redundant(n, d, _ptr(pos), _ptr(feat), int(k), float(tau_dist), float(tau_sim),
+                                      flags.ctypes.data_as(C.POINTER(C.c_uint8)))
+    return flags[:n]

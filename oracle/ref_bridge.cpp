@@ -20,6 +20,7 @@
 
 #include "gradcheck.hpp"
 #include "legoslam/gaussian_map.hpp"
+#include "legoslam/kdtree.hpp"
 #include "legoslam/renderer.hpp"
 
 namespace lego {
@@ -365,4 +366,44 @@ REF_API double ref_bench_bands(const RefMap* m, const RefCamera* cam, const RefC
     *loss = s;
   }
   return sec / std::max(1, iters);
+}
+
+// ---- map pruning (Eq. 4; the reference's pruning.cpp is a placeholder) ----------
+// The greedy ascending-index sweep of the SPEC run on the reference's own KD-tree
+// (kdtree.hpp: KdTree3::knn_if, exact k nearest among the accepted points, ties by index), with
+// the live filter and self-exclusion as the predicate.  d2 is KdTree3's (p - q).squaredNorm();
+// the cosine is restated as in oracle/prune_oracle.c.  pos [n][3], feat [d][n].
+REF_API int64_t ref_find_language_redundant(int64_t n, int32_t d, const double* pos, const double* feat, int32_t k,
+                                            double tau_dist, double tau_sim, uint8_t* flags) {
+  std::fill(flags, flags + n, uint8_t(0));
+  if (n < 2 || d <= 0 || k <= 0) return 0;
+  std::vector<lego::Vec3> pts((size_t)n);
+  for (int64_t i = 0; i < n; ++i) pts[(size_t)i] = lego::Vec3(pos[i * 3 + 0], pos[i * 3 + 1], pos[i * 3 + 2]);
+  const lego::KdTree3 tree(pts);
+  std::vector<double> norm((size_t)n);
+  for (int64_t i = 0; i < n; ++i) {
+    double s = 0.0;
+    for (int32_t c = 0; c < d; ++c) s += feat[(int64_t)c * n + i] * feat[(int64_t)c * n + i];
+    norm[(size_t)i] = std::sqrt(s);
+  }
+  const double tau2 = tau_dist * tau_dist;
+  std::vector<lego::KdTree3::Neighbor> nn;
+  int64_t marked = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    if (flags[i]) continue;
+    const auto live_other = [&](int j) { return j != (int)i && !flags[j]; };
+    tree.knn_if(pts[(size_t)i], k, live_other, nn);
+    for (const auto& nb : nn) {
+      const int64_t j = nb.index;
+      if (!(nb.dist_sq < tau2)) continue;
+      if (!(norm[(size_t)i] > 0.0) || !(norm[(size_t)j] > 0.0)) continue;
+      double dot = 0.0;
+      for (int32_t c = 0; c < d; ++c) dot += feat[(int64_t)c * n + i] * feat[(int64_t)c * n + j];
+      if (dot / (norm[(size_t)i] * norm[(size_t)j]) > tau_sim) {
+        flags[j] = 1;
+        ++marked;
+      }
+    }
+  }
+  return marked;
 }

@@ -55,6 +55,11 @@ class LgsCotangents(C.Structure):
                 ("rgb_shape", C.c_int32 * 3), ("depth_shape", C.c_int32 * 3), ("feat_shape", C.c_int32 * 3)]
 
 
+class LgsPruneConfig(C.Structure):
+    _fields_ = [("k_neighbors", C.c_int32), ("tau_dist", C.c_double), ("tau_sim", C.c_double),
+                ("alpha_min", C.c_double), ("scale_max", C.c_double)]
+
+
 class LgsRenderStats(C.Structure):
     _fields_ = [("visible", C.c_int64), ("pairs", C.c_int64), ("tiles", C.c_int64), ("max_tile_list", C.c_int64),
                 ("listed", C.c_int64), ("active", C.c_int64)]
@@ -140,6 +145,14 @@ SIGNATURES = [
     ("lgs_map_file_write", C.c_int, [C.c_char_p, C.POINTER(LgsGaussians), C.c_void_p]),
     ("lgs_map_load", C.c_int, [C.c_void_p, C.c_char_p, C.c_int32, C.POINTER(C.c_void_p)]),
     ("lgs_map_save", C.c_int, [C.c_void_p, C.c_void_p, C.c_char_p, C.c_void_p]),
+    ("lgs_prune_config_default", LgsPruneConfig, []),
+    ("lgs_find_language_redundant", C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(LgsPruneConfig), C.c_void_p,
+                                              C.c_int32, C.POINTER(C.c_int64)]),
+    ("lgs_find_geometric", C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(LgsPruneConfig), C.c_void_p, C.c_int32,
+                                     C.POINTER(C.c_int64)]),
+    ("lgs_prune", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(LgsPruneConfig), C.c_void_p, C.c_void_p,
+                            C.c_int32, C.POINTER(C.c_int64)]),
+    ("lgs_prune_stats", C.c_int, [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     ("lgs_plan_create", C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(LgsCamera), C.POINTER(LgsRenderConfig),
                                   C.POINTER(LgsL1Targets), C.POINTER(LgsImages), C.POINTER(LgsMapGrads), C.c_void_p,
                                   C.POINTER(C.c_void_p)]),

@@ -16,10 +16,12 @@
 #include <cstdio>
 #include <cstring>
 #include <fstream>
+#include <mutex>
 #include <new>
 #include <stdexcept>
 #include <string>
 #include <thread>
+#include <unordered_set>
 #include <vector>
 
 #include "../../include/lgs.h"
@@ -138,6 +140,8 @@ struct lgs_ctx {
   std::vector<cudaEvent_t> event_pool;
   double phase_ms[LGS_PHASE_COUNT] = {};
   int64_t phase_n[LGS_PHASE_COUNT] = {};
+  // last lgs_find_language_redundant: candidates (a similar neighbour inside tau_dist), rounds
+  int64_t prune_candidates = 0, prune_rounds = 0;
 };
 
 namespace {
@@ -255,6 +259,7 @@ struct lgs_map {
   float* feat = nullptr;
   bool mapped = false;             // LGS_MEM_HOST_MAPPED: dm.sh and feat_src point into page-locked host memory
   const float* feat_src = nullptr;  // [d][N], device-addressable (features gathered lazily)
+  uint64_t version = 0;  // live-map registry key: a new one after lgs_prune (tapes / plans check it)
 };
 
 struct lgs_adam {
@@ -271,6 +276,7 @@ struct lgs_adam {
 struct lgs_saved {
   lgs_ctx* ctx = nullptr;
   lgs_map* owned_map = nullptr;  // lgs_render convenience path
+  uint64_t map_version = 0;      // the map's version at render time (its buffers are the tape's dm)
   DevMap dm{};
   DevCam cam{};
   ViewBufs vb{};
@@ -459,8 +465,33 @@ lgs_status check_gaussians(const lgs_gaussians* src) {
   return LGS_OK;
 }
 
+// Registry of live map versions: a tape or plan holds raw pointers into its map's buffers, which
+// lgs_prune replaces and lgs_map_destroy frees; both drop the version, and the backward / plan
+// entry points refuse a stale one instead of reading freed memory.
+std::mutex g_version_mu;
+std::unordered_set<uint64_t>& live_versions() {
+  static auto* s = new std::unordered_set<uint64_t>();
+  return *s;
+}
+uint64_t g_next_version = 0;
+uint64_t version_new() {
+  std::lock_guard<std::mutex> lock(g_version_mu);
+  const uint64_t v = ++g_next_version;
+  live_versions().insert(v);
+  return v;
+}
+void version_drop(uint64_t v) {
+  std::lock_guard<std::mutex> lock(g_version_mu);
+  live_versions().erase(v);
+}
+bool version_live(uint64_t v) {
+  std::lock_guard<std::mutex> lock(g_version_mu);
+  return live_versions().count(v) != 0;
+}
+
 void free_map(lgs_map* m) {
   lgs_ctx* ctx = m->ctx;
+  version_drop(m->version);
   cudaSetDevice(ctx->device);
   dfree(ctx, m->pos_opa);
   dfree(ctx, m->rot);
@@ -658,6 +689,7 @@ LGS_API lgs_status lgs_map_create(lgs_ctx* ctx, const lgs_gaussians* src, lgs_ma
   m->dm.scale = m->scale;
   if (!m->mapped) m->dm.sh = m->sh;
   m->dm.feat = m->feat;
+  m->version = version_new();
   if (src->memory == LGS_MEM_HOST) LGS_CUDA(cudaStreamSynchronize(ctx->stream));
   *out = m;
   return LGS_OK;
@@ -712,6 +744,7 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
   t->ctx = ctx;
   ctx->refs++;
   t->dm = map->dm;
+  t->map_version = map->version;
   t->cam = dc;
   t->ntiles = ntiles;
   auto bail = [&](lgs_status st) {
@@ -1212,6 +1245,8 @@ lgs_status host_grads_note_rows(lgs_ctx* ctx, float* const src[6], int64_t n, in
 
 lgs_status run_backward(lgs_ctx* ctx, const lgs_saved* t, const BwdIn& in_dev, lgs_map_grads* grads, float* pose_grad,
                         bool async_pose = false) {
+  if (!version_live(t->map_version))
+    return fail(LGS_EINVAL, "the map of this tape was pruned or destroyed after the render");
   cudaStream_t s = ctx->stream;
   const int64_t n = t->dm.n;
   const int d = t->dm.d, K = t->dm.K;
@@ -2444,6 +2479,205 @@ LGS_API lgs_status lgs_map_save(lgs_ctx* ctx, const lgs_map* map, const char* pa
   });
 }
 
+// ---- map pruning (csrc/prune.cu) ---------------------------------------------
+LGS_API lgs_prune_config lgs_prune_config_default(void) {
+  lgs_prune_config c;
+  c.k_neighbors = 8;  // SPEC.md:476 defaults
+  c.tau_dist = 0.02;
+  c.tau_sim = 0.9;
+  c.alpha_min = 0.05;
+  c.scale_max = 0.5;
+  return c;
+}
+
+}  // extern "C"
+
+namespace {
+
+lgs_status prune_setup(lgs_ctx* ctx, const lgs_map* map, const lgs_prune_config* cfg_in, int32_t memory,
+                       PruneParams* pp, PruneIn* in) {
+  if (!ctx || !map) return fail(LGS_EINVAL, "ctx/map is NULL");
+  const lgs_prune_config c = cfg_in ? *cfg_in : lgs_prune_config_default();
+  if (c.k_neighbors < 1 || c.k_neighbors > 32) return fail(LGS_EINVAL, "k_neighbors %d out of range [1, 32]", c.k_neighbors);
+  if (!(c.tau_dist > 0.0) || !std::isfinite(c.tau_dist)) return fail(LGS_EINVAL, "tau_dist must be > 0");
+  if (!(c.tau_sim > -1.0 && c.tau_sim <= 1.0)) return fail(LGS_EINVAL, "tau_sim must be in (-1, 1]");
+  if (memory != LGS_MEM_HOST && memory != LGS_MEM_DEVICE) return fail(LGS_EINVAL, "bad memory kind for the flags");
+  *pp = PruneParams{c.k_neighbors, c.tau_dist, c.tau_sim, c.alpha_min, c.scale_max};
+  *in = PruneIn{map->pos_opa, map->scale, map->feat, map->dm.n, map->dm.d, map->dm.dp};
+  LGS_CUDA(cudaSetDevice(ctx->device));
+  if (map->mapped && map->feat_src && map->dm.n > 0)  // host-mapped: features are gathered lazily
+    launch_gather_features(map->feat_src, map->feat, map->dm.n, map->dm.d, map->dm.dp, ctx->stream);
+  return LGS_OK;
+}
+
+// flags produced on the device, handed out in `memory`
+lgs_status flags_out(lgs_ctx* ctx, const uint8_t* dflags, uint8_t* flags, int32_t memory, int64_t n) {
+  if (!flags || memory == LGS_MEM_DEVICE || n == 0) return LGS_OK;
+  LGS_CUDA(cudaMemcpyAsync(flags, dflags, (size_t)n, cudaMemcpyDeviceToHost, ctx->stream));
+  ctx->bytes_d2h += n;
+  LGS_CUDA(cudaStreamSynchronize(ctx->stream));
+  return LGS_OK;
+}
+
+lgs_status language_flags(lgs_ctx* ctx, const PruneIn& in, const PruneParams& pp, uint8_t* dflags, int64_t* count) {
+  uint8_t* scratch = nullptr;
+  LGS_TRY(dalloc(ctx, &scratch, prune_scratch_bytes(in.n)));
+  int64_t cand = 0, rounds = 0;
+  const cudaError_t e = run_language_redundant(in, pp, dflags, scratch, count, &cand, &rounds, ctx->stream);
+  dfree(ctx, scratch);
+  if (e != cudaSuccess) return fail(LGS_ECUDA, "language-redundancy sweep: %s", cudaGetErrorString(e));
+  ctx->prune_candidates = cand;
+  ctx->prune_rounds = rounds;
+  ctx->launches += 6 + 2 * rounds;
+  return LGS_OK;
+}
+
+lgs_status geometric_flags(lgs_ctx* ctx, const PruneIn& in, const PruneParams& pp, uint8_t* dflags, int64_t* count) {
+  uint64_t* scratch = nullptr;
+  LGS_TRY(dalloc(ctx, &scratch, 1));
+  const cudaError_t e = run_geometric(in, pp, dflags, scratch, count, ctx->stream);
+  dfree(ctx, scratch);
+  if (e != cudaSuccess) return fail(LGS_ECUDA, "geometric pruning rule: %s", cudaGetErrorString(e));
+  ctx->launches++;
+  return LGS_OK;
+}
+
+// allocate the compacted copy of buffer `p` (rows of `width_floats` floats); swapped in later
+struct Swap {
+  void** slot;
+  void* fresh;
+};
+template <typename T>
+lgs_status compact_alloc(lgs_ctx* ctx, T*& p, int width_floats, int64_t kept, RowCopies& rc, std::vector<Swap>& sw) {
+  if (!p) return LGS_OK;
+  T* q = nullptr;
+  LGS_TRY(dalloc(ctx, &q, (size_t)std::max<int64_t>(kept, 1) * (size_t)width_floats * sizeof(float) / sizeof(T)));
+  rc.src[rc.count] = reinterpret_cast<const float*>(p);
+  rc.dst[rc.count] = reinterpret_cast<float*>(q);
+  rc.width[rc.count] = width_floats;
+  rc.count++;
+  sw.push_back(Swap{reinterpret_cast<void**>(&p), q});
+  return LGS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+LGS_API lgs_status lgs_find_language_redundant(lgs_ctx* ctx, const lgs_map* map, const lgs_prune_config* cfg,
+                                               uint8_t* flags, int32_t memory, int64_t* count) {
+  return guarded([&]() -> lgs_status {
+    PruneParams pp;
+    PruneIn in;
+    LGS_TRY(prune_setup(ctx, map, cfg, memory, &pp, &in));
+    if (in.n > 0 && !flags) return fail(LGS_EINVAL, "flags is NULL");
+    uint8_t* dflags = memory == LGS_MEM_DEVICE ? flags : nullptr;
+    if (!dflags) LGS_TRY(dalloc(ctx, &dflags, (size_t)in.n));
+    lgs_status st = language_flags(ctx, in, pp, dflags, count);
+    if (st == LGS_OK) st = flags_out(ctx, dflags, flags, memory, in.n);
+    if (memory != LGS_MEM_DEVICE) dfree(ctx, dflags);
+    return st;
+  });
+}
+
+LGS_API lgs_status lgs_find_geometric(lgs_ctx* ctx, const lgs_map* map, const lgs_prune_config* cfg, uint8_t* flags,
+                                      int32_t memory, int64_t* count) {
+  return guarded([&]() -> lgs_status {
+    PruneParams pp;
+    PruneIn in;
+    LGS_TRY(prune_setup(ctx, map, cfg, memory, &pp, &in));
+    if (in.n > 0 && !flags) return fail(LGS_EINVAL, "flags is NULL");
+    uint8_t* dflags = memory == LGS_MEM_DEVICE ? flags : nullptr;
+    if (!dflags) LGS_TRY(dalloc(ctx, &dflags, (size_t)in.n));
+    lgs_status st = geometric_flags(ctx, in, pp, dflags, count);
+    if (st == LGS_OK) st = flags_out(ctx, dflags, flags, memory, in.n);
+    if (memory != LGS_MEM_DEVICE) dfree(ctx, dflags);
+    return st;
+  });
+}
+
+LGS_API lgs_status lgs_prune(lgs_ctx* ctx, lgs_map* map, lgs_adam* adam, const lgs_prune_config* cfg,
+                             uint8_t* removed_language, uint8_t* removed_geometric, int32_t memory, int64_t* kept) {
+  return guarded([&]() -> lgs_status {
+    PruneParams pp;
+    PruneIn in;
+    LGS_TRY(prune_setup(ctx, map, cfg, memory, &pp, &in));
+    if (map->mapped) return fail(LGS_EINVAL, "lgs_prune needs a device map (this one is LGS_MEM_HOST_MAPPED)");
+    if (adam && (adam->n != map->dm.n || adam->d != map->dm.d || adam->K != map->dm.K))
+      return fail(LGS_EINVAL, "Adam state was created for a different map shape");
+    const int64_t n = in.n;
+    if (kept) *kept = n;
+    if (n == 0) return LGS_OK;
+    cudaStream_t s = ctx->stream;
+    uint8_t *dl = nullptr, *dg = nullptr, *scratch = nullptr;
+    LGS_TRY(dalloc(ctx, &dl, (size_t)n));
+    LGS_TRY(dalloc(ctx, &dg, (size_t)n));
+    lgs_status st = language_flags(ctx, in, pp, dl, nullptr);
+    if (st == LGS_OK) st = geometric_flags(ctx, in, pp, dg, nullptr);
+    if (st == LGS_OK) st = flags_out(ctx, dl, removed_language, memory, n);
+    if (st == LGS_OK) st = flags_out(ctx, dg, removed_geometric, memory, n);
+    if (st == LGS_OK && memory == LGS_MEM_DEVICE) {
+      if (removed_language) LGS_CUDA(cudaMemcpyAsync(removed_language, dl, (size_t)n, cudaMemcpyDeviceToDevice, s));
+      if (removed_geometric) LGS_CUDA(cudaMemcpyAsync(removed_geometric, dg, (size_t)n, cudaMemcpyDeviceToDevice, s));
+    }
+    int64_t nk = n;
+    uint32_t *keep = nullptr, *dst_of = nullptr;
+    if (st == LGS_OK) st = dalloc(ctx, &scratch, compact_scratch_bytes(n));
+    if (st == LGS_OK) {
+      const cudaError_t e = run_compact(dl, dg, n, scratch, &nk, &keep, &dst_of, s);
+      if (e != cudaSuccess) st = fail(LGS_ECUDA, "prune compaction: %s", cudaGetErrorString(e));
+    }
+    if (st == LGS_OK && nk != n) {
+      RowCopies rc{};
+      std::vector<Swap> sw;
+      const int K3 = map->dm.K * 3, fw = map->dm.dp > 0 ? map->dm.dp : 1;
+      auto add = [&](auto*& p, int w) {
+        if (st == LGS_OK) st = compact_alloc(ctx, p, w, nk, rc, sw);
+      };
+      add(map->pos_opa, 4); add(map->rot, 4); add(map->scale, 4); add(map->sh, K3); add(map->feat, fw);
+      if (adam) {
+        add(adam->m_po, 4); add(adam->v_po, 4); add(adam->m_rot, 4); add(adam->v_rot, 4);
+        add(adam->m_sc, 4); add(adam->v_sc, 4); add(adam->m_sh, K3); add(adam->v_sh, K3);
+        add(adam->m_ft, fw); add(adam->v_ft, fw);
+      }
+      if (st != LGS_OK) {  // out of memory part way: drop the copies, the map stays as it was
+        for (Swap& w : sw) cudaFreeAsync(w.fresh, s);
+      } else {
+        launch_compact_rows(rc, keep, dst_of, n, s);
+        ctx->launches++;
+        for (Swap& w : sw) {
+          cudaFreeAsync(*w.slot, s);
+          *w.slot = w.fresh;
+        }
+        map->dm.n = nk;
+        map->dm.pos_opa = map->pos_opa;
+        map->dm.rot = map->rot;
+        map->dm.scale = map->scale;
+        map->dm.sh = map->sh;
+        map->dm.feat = map->feat;
+        version_drop(map->version);
+        map->version = version_new();
+        if (adam) adam->n = nk;
+      }
+    }
+    dfree(ctx, scratch);
+    dfree(ctx, dl);
+    dfree(ctx, dg);
+    if (st != LGS_OK) return st;
+    LGS_CUDA(cudaStreamSynchronize(s));
+    LGS_CUDA(cudaGetLastError());
+    if (kept) *kept = nk;
+    return LGS_OK;
+  });
+}
+
+LGS_API lgs_status lgs_prune_stats(const lgs_ctx* ctx, int64_t* candidates, int64_t* rounds) {
+  if (!ctx) return fail(LGS_EINVAL, "ctx is NULL");
+  if (candidates) *candidates = ctx->prune_candidates;
+  if (rounds) *rounds = ctx->prune_rounds;
+  return LGS_OK;
+}
+
 }  // extern "C"
 
 // -------------------------------------------------------------------------------------------
@@ -2452,6 +2686,7 @@ LGS_API lgs_status lgs_map_save(lgs_ctx* ctx, const lgs_map* map, const char* pa
 struct lgs_plan {
   lgs_ctx* ctx = nullptr;
   lgs_map* map = nullptr;
+  uint64_t map_version = 0;
   lgs_camera cam{};
   lgs_render_config cfg{};
   lgs_l1_targets targets{};
@@ -2565,6 +2800,7 @@ LGS_API lgs_status lgs_plan_create(lgs_ctx* ctx, lgs_map* map, const lgs_camera*
   lgs_plan* p = new lgs_plan();
   p->ctx = ctx;
   p->map = map;
+  p->map_version = map->version;
   p->cam = *cam;
   p->cfg = cfg ? *cfg : lgs_render_config_default();
   p->targets = *targets;
@@ -2604,6 +2840,7 @@ LGS_API lgs_status lgs_plan_create(lgs_ctx* ctx, lgs_map* map, const lgs_camera*
 
 LGS_API lgs_status lgs_plan_run(lgs_ctx* ctx, lgs_plan* p) {
   if (!ctx || !p || ctx != p->ctx) return fail(LGS_EINVAL, "plan / context mismatch");
+  if (!version_live(p->map_version)) return fail(LGS_EINVAL, "the plan's map was pruned or destroyed: recreate the plan");
   LGS_CUDA(cudaGraphLaunch(p->exec, ctx->stream));
   ctx->launches += p->launches_per_run;
   return LGS_OK;

@@ -256,4 +256,35 @@ void launch_adam(const MapParams& p, const MapParams& m, const MapParams& v, con
 void launch_unpack_map(const MapParams& p, float* pos, float* rot, float* log_s, float* opac, float* sh, float* feat_dn,
                        cudaStream_t s);
 
+// ---- map pruning (prune.cu) ------------------------------------------------
+struct PruneIn {
+  const float4* pos_opa;  // x, y, z, opacity logit
+  const float4* scale;    // log-scales
+  const float* feat;      // [n][dp]
+  int64_t n;
+  int d, dp;
+};
+struct PruneParams {
+  int k;
+  double tau_dist, tau_sim, alpha_min, scale_max;
+};
+size_t prune_scratch_bytes(int64_t n);
+// Greedy language rule (flags[i] = 1: killed); synchronizes the stream (host round loop).
+cudaError_t run_language_redundant(const PruneIn& in, const PruneParams& pp, uint8_t* flags, void* scratch,
+                                   int64_t* count, int64_t* candidates, int64_t* rounds, cudaStream_t s);
+// scratch: 8 bytes of device memory
+cudaError_t run_geometric(const PruneIn& in, const PruneParams& pp, uint8_t* flags, void* scratch, int64_t* count,
+                          cudaStream_t s);
+// Row compaction: keep[i] = !(drop_a[i] || drop_b[i]) (either may be null), dst_of = exclusive scan.
+size_t compact_scratch_bytes(int64_t n);
+cudaError_t run_compact(const uint8_t* drop_a, const uint8_t* drop_b, int64_t n, void* scratch, int64_t* kept,
+                        uint32_t** keep, uint32_t** dst_of, cudaStream_t s);
+struct RowCopies {
+  const float* src[24];
+  float* dst[24];
+  int width[24];  // floats per row
+  int count;
+};
+void launch_compact_rows(const RowCopies& rc, const uint32_t* keep, const uint32_t* dst_of, int64_t n, cudaStream_t s);
+
 }  // namespace lgs

@@ -206,3 +206,37 @@ def make_decoder(D: int, hidden: int, d: int, seed: int):
     b1 = r.normal(0.0, 0.05, size=hidden)
     b2 = r.normal(0.0, 0.05, size=D)
     return tuple(x.astype(np.float32) for x in (w1, b1, w2, b2))
+
+
+def make_prune_scene(n: int = 20000, d: int = 16, seed: int = 5, objects: int = 24, duplicate: float = 0.5,
+                     jitter: float = 0.004, feat_noise: float = 0.05, coherent: bool = True, extent: float = 1.0):
+    """A cluttered synthetic map for the pruning study ("duplicated insertion pass",
+    InsertConfig duplicate / duplicate_jitter = 0.004 m, gaussian_map.hpp:102-110): `objects`
+    spheres in an `extent`-metre box, each with its own unit feature; a Gaussian lies on its
+    sphere with that feature plus N(0, feat_noise) noise; a `duplicate` fraction of them is
+    inserted a second time `jitter` metres (N(0, jitter) per axis) away with fresh feature noise.
+    Opacity logits U(-4, 3) and scales U(0.002, 0.05) m (5 %: U(0.4, 0.9) m) make some Gaussians
+    fail the geometric criteria.  `coherent`: IDs in insertion order (object by object, the duplicates
+    after them) as a SLAM map grows; else a random permutation."""
+    rng = np.random.default_rng(seed)
+    base_n = max(1, int(round(n / (1.0 + duplicate))))
+    centers = rng.uniform(-extent / 2, extent / 2, (objects, 3))
+    radii = rng.uniform(0.05, 0.25, objects)
+    fobj = rng.standard_normal((objects, max(d, 1)))
+    fobj /= np.linalg.norm(fobj, axis=1, keepdims=True)
+    obj = np.sort(rng.integers(0, objects, base_n))
+    dirs = rng.standard_normal((base_n, 3))
+    dirs /= np.linalg.norm(dirs, axis=1, keepdims=True)
+    pos = centers[obj] + radii[obj, None] * dirs
+    feat = fobj[obj] + feat_noise * rng.standard_normal((base_n, max(d, 1)))
+    nd = n - base_n
+    src = np.sort(rng.choice(base_n, size=nd, replace=nd > base_n)) if nd > 0 else np.zeros(0, np.int64)
+    pos = np.concatenate([pos, pos[src] + jitter * rng.standard_normal((nd, 3))])
+    feat = np.concatenate([feat, feat[src] + feat_noise * rng.standard_normal((nd, max(d, 1)))])
+    if not coherent:
+        perm = rng.permutation(n)
+        pos, feat = pos[perm], feat[perm]
+    log_s = np.log(np.where(rng.uniform(size=(n, 1)) < 0.05, rng.uniform(0.4, 0.9, (n, 3)),
+                            rng.uniform(0.002, 0.05, (n, 3))))
+    opac = rng.uniform(-4.0, 3.0, n)
+    return _pack(pos, _unit_quats(rng, n), log_s, opac, _sh(rng, n, 0), feat[:, :d])

@@ -12,6 +12,10 @@ not exist on the GPU box, so the GPU tests read these committed vectors instead 
                    fp32 inputs): lego::render images, and lego::render_backward gradients for the L1
                    cotangents of the reference's own images against the seed-7 targets, stored as
                    fp32 (the GPU bounds are 1e-4 / 1e-3); the depth order and contributor counts.
+  ref_prune.npz    the SPEC's language-pruning sweep (Eq. 4) run on the reference's own KdTree3
+                   (kdtree.hpp; oracle/ref_bridge.cpp ref_find_language_redundant) over
+                   scenes.make_prune_scene(PRUNE_N, seed=11, coherent=c) for the PRUNE_CASES
+                   (coherent, k, tau_dist, tau_sim): flags per case, bit-packed.
 """
 import os
 import sys
@@ -25,6 +29,9 @@ from oracle import ref  # noqa: E402
 from paper_2511_16144_b200 import scenes  # noqa: E402
 
 C0_N = 4000
+PRUNE_N = 6000
+PRUNE_CASES = [(True, 8, 0.02, 0.9), (False, 8, 0.02, 0.9), (True, 1, 0.02, 0.9), (True, 32, 0.05, 0.5),
+               (False, 4, 0.03, 0.0), (True, 8, 0.02, -0.5)]
 
 
 def ref_grad101():
@@ -51,11 +58,20 @@ def ref_c0():
                 order=out.sorted_indices().astype(np.int32), contribs=out.contrib_counts().astype(np.int16))
 
 
+def ref_prune():
+    out = {"cases": np.array(PRUNE_CASES, np.float64)}
+    for ci, (coh, k, td, ts) in enumerate(PRUNE_CASES):
+        scene = scenes.make_prune_scene(PRUNE_N, seed=11, coherent=bool(coh))
+        out[f"flags{ci}"] = np.packbits(ref.find_language_redundant(scene, int(k), td, ts))
+    return out
+
+
 def main():
     if not ref.available():
         raise SystemExit("oracle/_ref/liblgs_ref.so is not built (make -C oracle, needs /root/reference)")
     np.savez_compressed(os.path.join(HERE, "ref_grad101.npz"), **ref_grad101())
     np.savez_compressed(os.path.join(HERE, "ref_c0.npz"), **ref_c0())
+    np.savez_compressed(os.path.join(HERE, "ref_prune.npz"), **ref_prune())
 
 
 if __name__ == "__main__":
