@@ -50,6 +50,7 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-mapping", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-pruning", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=10)
     p.add_argument("--e2e-threads", type=int, default=3)
     p.add_argument("--sampler", choices=["nvml", "smi", "none"], default="nvml", help=argparse.SUPPRESS)
@@ -495,6 +496,8 @@ def run_ours(args):
     if mv != "none":
         result["multiview_batch"] = run_multiview(args, mv, local, world, rank, flush)
 
+    if rank == 0 and world == 1 and not args.no_pruning:
+        result["pruning"] = run_pruning(local)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         result["cpu_baseline"] = cpu_baseline(scene, cam, tg, args)
     if world > 1:
@@ -761,6 +764,52 @@ def run_e2e(args, scene, cam, tg, R, device, mapped=True, delta=True):
             "api": f"renderer.render(host numpy map{', host_mapped' if mapped else ''}, host targets) + "
                    f"render_backward_l1(host grads{', delta rows' if delta else ''}) + l1_loss(); "
                    f"{nthreads} host threads x own lgs_ctx/stream, wall clock over all steps"}
+
+
+def run_pruning(device, n=500_000, reps=5):
+    """the language-pruning sweep (SPEC.md Eq. 4) + geometric rule on a 500k
+    cluttered map (scenes.make_prune_scene: 600 objects in a 6 m box, half the Gaussians inserted
+    twice 4 mm apart), through the public API (host flags out), against the CPU: oracle/prune_oracle.c
+    (the SPEC sweep, 1 thread) and the same sweep on the reference's own KdTree3 (oracle/_ref)."""
+    import numpy as np
+    import torch
+    from paper_2511_16144_b200 import pruning as P
+    from paper_2511_16144_b200 import renderer as R
+    from paper_2511_16144_b200 import scenes
+    s = scenes.make_prune_scene(n, seed=9, objects=600, extent=6.0)
+    dm = R.DeviceMap(s, R.Context(device))
+    cfg = P.PruneConfig()
+    P.find_language_redundant(dm, cfg)  # warm-up (allocator, module load)
+    torch.cuda.synchronize(device)
+    t = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        idx = P.find_language_redundant(dm, cfg)
+        t.append(time.perf_counter() - t0)
+    st = P.prune_stats(dm)
+    tg = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        gidx = P.find_geometric(dm, cfg)
+        tg.append(time.perf_counter() - t0)
+    out = {"workload": f"make_prune_scene({n}, objects=600, extent=6 m, 50% duplicated at 4 mm), K 8, tau 0.02 m, "
+                       "tau_sim 0.9; wall time of the API call (host flags out, includes the host round checks)",
+           "gpu_language_ms": round(1e3 * min(t), 3), "gpu_geometric_ms": round(1e3 * min(tg), 3),
+           "removed_language": int(idx.size), "removed_geometric": int(gidx.size), **st}
+    from oracle import oracle as orc
+    t0 = time.perf_counter()
+    want = orc.find_language_redundant(s)
+    out["cpu_port_ms"] = round(1e3 * (time.perf_counter() - t0), 1)
+    flags = np.zeros(n, np.uint8)
+    flags[idx] = 1
+    out["matches_oracle"] = bool(np.array_equal(flags, want))
+    ref = _ref_build()
+    if ref is not None:
+        t0 = time.perf_counter()
+        ref.find_language_redundant(s)
+        out["cpu_ref_kdtree_ms"] = round(1e3 * (time.perf_counter() - t0), 1)
+    out["cpu_cores"] = 1
+    return out
 
 
 def cpu_threads():
