@@ -1633,6 +1633,7 @@ LGS_API lgs_status lgs_saved_work(const lgs_saved* tape, int64_t* evaluated, int
   lgs_ctx* ctx = tape->ctx;
   LGS_CUDA(cudaSetDevice(ctx->device));
   if (!tape->ps.work) return fail(LGS_EINVAL, "work counters are collected only while profiling (lgs_ctx_profile)");
+  if (tape->bwd_fused) return fail(LGS_EINVAL, "the fused forward+backward kernel does not collect work counters");
   std::vector<uint2> w((size_t)tape->cam.W * tape->cam.H);
   LGS_CUDA(cudaMemcpyAsync(w.data(), tape->ps.work, sizeof(uint2) * w.size(), cudaMemcpyDeviceToHost, ctx->stream));
   LGS_CUDA(cudaStreamSynchronize(ctx->stream));
