@@ -28,10 +28,14 @@
  *      (proj/include/legoslam/random.hpp:12-50), to rebuild the reference
  *      tests' seeded scenes bit-for-bit.
  *
- * Parity pinning: the reference cannot be compiled here (Eigen3, libpng and
- * doctest are absent), and it ships no golden vectors.  (A) is
- * pinned against every known-answer test of proj/tests/test_renderer.cpp:38-204
- * including the seed-101 finite-difference gradcheck (gradcheck.hpp:31-148).
+ * Parity pinning: (A) is checked against the reference ITSELF -- its unmodified
+ * renderer.cpp / geometry.cpp compiled by oracle/Makefile into oracle/_ref
+ * (against the self-written Eigen subset in eigen_shim/) -- to fp64 rounding on
+ * images, gradients, depth order and contributor counts
+ * (tests/test_reference_build.py), and against the reference's own renderer
+ * tests (proj/tests/test_renderer.cpp:38-204, also run unmodified against that
+ * build), including the seed-101 finite-difference gradcheck
+ * (gradcheck.hpp:31-148).  Part (D), map pruning, is in prune_oracle.c.
  */
 #include <math.h>
 #include <pthread.h>

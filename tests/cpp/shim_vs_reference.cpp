@@ -2,7 +2,8 @@
 //
 // Built by oracle/Makefile (needs /root/reference: the reference headers, renderer.cpp and
 // geometry.cpp, unmodified, against oracle/eigen_shim) and linked with liblgs.so; run on a GPU by
-// tests/test_gpu_cpp_shim.py.  lego::gpu::render / render_backward are called with exactly the
+// tests/test_gpu_c_abi.py::test_cpp_drop_in_against_the_reference.  lego::gpu::render /
+// render_backward are called with exactly the
 // arguments lego::render / lego::render_backward take (renderer.hpp:55-56, 72-74) on:
 //   * the reference's own gradcheck scene (gradcheck.hpp:31-78, seed 101; no thresholds active):
 //     every image value within 1e-4 rel / 1e-5 abs, every gradient within 1e-3 (rel. to the
