@@ -755,9 +755,9 @@ def run_e2e(args, scene, cam, tg, R, device, mapped=True, delta=True):
     ms, (h2d, d2h) = timed(workers, args.e2e_steps)
     ms1 = timed(workers[:1], args.e2e_steps)[0] if nthreads > 1 else ms
     d2h += 6 * 4 + 8  # + the pose gradient and the loss
-    if mapped:  # + the listed Gaussians' SH rows and features read in place over PCIe
-        act = R.render(hscene, cam, ctx=workers[0].ctx, host_mapped=True).stats()["active"]
-        h2d += act * 4 * (3 * K + d)
+    if mapped:  # + the listed Gaussians' SH rows and features read in place over PCIe (zero-copy mode)
+        rows = R.render(hscene, cam, ctx=workers[0].ctx, host_mapped=True).stats()["host_rows"]
+        h2d += rows * 4 * (3 * K + d)
     return {"value": round(1000.0 / ms, 3), "unit": UNIT, "ms_per_step": round(ms, 3), "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "host_threads": nthreads,
             "single_thread": {"value": round(1000.0 / ms1, 3), "ms_per_step": round(ms1, 3)},

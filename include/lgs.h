@@ -149,6 +149,10 @@ typedef struct {
                              binning, saturated tiles keep only the prefix their pixels can reach */
   int64_t active;         /* Gaussians whose gradient rows the backward computes (listed in a traversed
                              tile list; = visible with complete lists); every other row is zero */
+  int64_t host_rows;      /* LGS_MEM_HOST_MAPPED maps: Gaussians whose SH row and features this render
+                             read in place over PCIe (0 when it copied the SH and feature blocks in bulk:
+                             an uncaptured render does when the previous render of the same host map
+                             listed more than 1/64 of it, or lists every Gaussian) */
 } lgs_render_stats;
 
 /* ---- library / context ---------------------------------------------------------------- */

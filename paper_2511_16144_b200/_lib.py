@@ -62,7 +62,7 @@ class LgsPruneConfig(C.Structure):
 
 class LgsRenderStats(C.Structure):
     _fields_ = [("visible", C.c_int64), ("pairs", C.c_int64), ("tiles", C.c_int64), ("max_tile_list", C.c_int64),
-                ("listed", C.c_int64), ("active", C.c_int64)]
+                ("listed", C.c_int64), ("active", C.c_int64), ("host_rows", C.c_int64)]
 
 
 class LgsDecoder(C.Structure):

@@ -140,6 +140,19 @@ struct lgs_ctx {
   std::vector<cudaEvent_t> event_pool;
   double phase_ms[LGS_PHASE_COUNT] = {};
   int64_t phase_n[LGS_PHASE_COUNT] = {};
+  // LGS_MEM_HOST_MAPPED renders: the last host-mapped map rendered (its SH pointer and size) and
+  // how many of its Gaussians that render listed.  Zero-copy reads of the listed rows win when
+  // few are listed (the headline: 2.5k of 500k); when many are (tiles that do not saturate on
+  // layer A take the complete lists), scattered PCIe reads of [d][N] feature columns lose to one
+  // DMA of the SH and feature blocks, so the next render of that map copies them in bulk.
+  uint32_t* mh_listed_dev = nullptr;
+  uint32_t* mh_listed_host = nullptr;  // pinned: the count of the render whose copy is pending
+  cudaEvent_t mh_event = nullptr;      // recorded after that copy
+  bool mh_pending = false;
+  const void* mh_pending_key = nullptr;  // its map (SH pointer) and size
+  int64_t mh_pending_n = 0;
+  const void* mh_key = nullptr;  // the last map whose count has landed, and that count
+  int64_t mh_n = 0, mh_listed = 0;
   // last lgs_find_language_redundant: candidates (a similar neighbour inside tau_dist), rounds
   int64_t prune_candidates = 0, prune_rounds = 0;
 };
@@ -277,6 +290,8 @@ struct lgs_saved {
   lgs_ctx* ctx = nullptr;
   lgs_map* owned_map = nullptr;  // lgs_render convenience path
   uint64_t map_version = 0;      // the map's version at render time (its buffers are the tape's dm)
+  float* sh_dev = nullptr;       // host-mapped map rendered in bulk-copy mode: its SH block (dm.sh)
+  bool host_rows_in_place = false;  // host-mapped map, zero-copy mode: listed rows were read over PCIe
   DevMap dm{};
   DevCam cam{};
   ViewBufs vb{};
@@ -313,6 +328,9 @@ void ctx_release(lgs_ctx* ctx) {
     if (ctx->side_join) cudaEventDestroy(ctx->side_join);
     if (ctx->pool) cudaMemPoolDestroy(ctx->pool);
     if (ctx->host_u32) cudaFreeHost(ctx->host_u32);
+    if (ctx->mh_listed_host) cudaFreeHost(ctx->mh_listed_host);
+    if (ctx->mh_listed_dev) cudaFree(ctx->mh_listed_dev);
+    if (ctx->mh_event) cudaEventDestroy(ctx->mh_event);
     if (ctx->dev_u32) cudaFree(ctx->dev_u32);
     if (ctx->pairs_ready) cudaEventDestroy(ctx->pairs_ready);
     if (ctx->sparse_ovf_dev) cudaFree(ctx->sparse_ovf_dev);
@@ -505,6 +523,7 @@ void free_map(lgs_map* m) {
 void free_saved(lgs_saved* t) {
   lgs_ctx* ctx = t->ctx;
   cudaSetDevice(ctx->device);
+  dfree(ctx, t->sh_dev);
   dfree(ctx, t->vb.rec0);
   dfree(ctx, t->vb.active);
   dfree(ctx, t->gacc);
@@ -790,23 +809,63 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
   void* otemp = nullptr;
   const size_t otemp_bytes = cub_depth ? 0 : depth_order_temp_bytes(n);
   if (!cub_depth) TRYB(dalloc(ctx, reinterpret_cast<uint8_t**>(&otemp), otemp_bytes));
+  // host-mapped map (LGS_MEM_HOST_MAPPED): the listed Gaussians' SH rows and features are read in
+  // place (zero-copy), unless the previous render of this map listed more than 1/64 of it (or
+  // every Gaussian may be listed: complete lists) -- then the SH and feature blocks are DMA-copied
+  // in bulk for this render (ctx->mh_*).  Uncaptured renders only; plans keep zero-copy.
+  const bool mapped = map->mapped && !ctx->capturing;
+  bool bulk = false;
+  if (mapped) {
+    if (!ctx->mh_listed_dev) {
+      CUDAB(cudaMalloc(reinterpret_cast<void**>(&ctx->mh_listed_dev), sizeof(uint32_t)));
+      CUDAB(cudaHostAlloc(reinterpret_cast<void**>(&ctx->mh_listed_host), sizeof(uint32_t), cudaHostAllocDefault));
+      CUDAB(cudaEventCreateWithFlags(&ctx->mh_event, cudaEventDisableTiming));
+    }
+    if (ctx->mh_pending && cudaEventQuery(ctx->mh_event) == cudaSuccess) {  // the last count has landed
+      ctx->mh_key = ctx->mh_pending_key;
+      ctx->mh_n = ctx->mh_pending_n;
+      ctx->mh_listed = *ctx->mh_listed_host;
+      ctx->mh_pending = false;
+    }
+    bulk = !layered || (ctx->mh_key == map->dm.sh && ctx->mh_n == n && ctx->mh_listed > n / 64);
+    if (!ctx->mh_pending) CUDAB(cudaMemsetAsync(ctx->mh_listed_dev, 0, sizeof(uint32_t), s));
+  }
+  t->host_rows_in_place = mapped && !bulk;
+  if (bulk) {
+    const size_t shn = (size_t)n * map->dm.K * 3;
+    TRYB(dalloc(ctx, &t->sh_dev, shn));
+    CUDAB(cudaMemcpyAsync(t->sh_dev, map->dm.sh, sizeof(float) * shn, cudaMemcpyDefault, s));
+    ctx->bytes_h2d += (int64_t)(sizeof(float) * shn);
+    t->dm.sh = t->sh_dev;
+    if (d > 0 && map->feat_src) {  // [d][N] block by DMA, packed to [N][dp] on the device
+      float* stage = nullptr;
+      TRYB(dalloc(ctx, &stage, (size_t)n * d));
+      CUDAB(cudaMemcpyAsync(stage, map->feat_src, sizeof(float) * (size_t)n * d, cudaMemcpyDefault, s));
+      ctx->bytes_h2d += (int64_t)(sizeof(float) * (size_t)n * d);
+      launch_gather_features(stage, map->feat, n, d, dp, s);
+      ctx->launches++;
+      dfree(ctx, stage);
+    }
+  }
+  const DevMap& dm = t->dm;  // the map's buffers (SH from the bulk copy in bulk mode)
   ColorJob cj;  // layered: colours of just the listed Gaussians, computed where first listed
   if (layered) {
-    cj.sh = map->dm.sh;
-    cj.pos_opa = map->dm.pos_opa;
+    cj.sh = dm.sh;
+    cj.pos_opa = dm.pos_opa;
     for (int a = 0; a < 3; ++a) cj.cc[a] = dc.cc[a];
-    cj.deg = map->dm.deg;
+    cj.deg = dm.deg;
     cj.color = t->vb.color;
-    if (map->mapped && map->feat_src) {
+    if (mapped && !ctx->mh_pending) cj.listed = ctx->mh_listed_dev;  // count this render (one in flight)
+    if (map->mapped && map->feat_src && !bulk) {
       cj.feat_src = map->feat_src;
       cj.feat_dst = map->feat;
       cj.n = n;
-      cj.d = map->dm.d;
-      cj.dp = map->dm.dp;
+      cj.d = dm.d;
+      cj.dp = dm.dp;
     }
   }
-  if (map->mapped && map->feat_src && !layered) {  // every Gaussian may be listed: gather all features
-    launch_gather_features(map->feat_src, map->feat, n, map->dm.d, map->dm.dp, s);
+  if (map->mapped && map->feat_src && !layered && !bulk) {  // every Gaussian may be listed: gather all features
+    launch_gather_features(map->feat_src, map->feat, n, dm.d, dm.dp, s);
     ctx->launches++;
   }
   if (layered) {
@@ -819,7 +878,7 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
   const uint32_t* dev_pairs = ctx->dev_u32;
   {
     PhaseScope ph(ctx, PH_PREPROCESS);
-    launch_preprocess(map->dm, dc, t->vb, !layered, s);
+    launch_preprocess(dm, dc, t->vb, !layered, s);
     // the pair count P = sum of tiles touched sizes the tile lists; it is read back while the GPU
     // is still busy with the depth order queued below, so the host wait never idles the GPU
     if (layered) launch_depth_scan(n, dc.near_plane, otemp, &dev_pairs, s);  // P = visible buckets' pairs
@@ -971,10 +1030,10 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
       {
         PhaseScope ph(ctx, PH_BLEND_FWD);
         if (fuse)
-          launch_blend_fused_l1(map->dm, dc, t->vb, TileLists{t->vals, t->ranges, nullptr, t->counter}, fo1, t->gacc, s,
+          launch_blend_fused_l1(dm, dc, t->vb, TileLists{t->vals, t->ranges, nullptr, t->counter}, fo1, t->gacc, s,
                                 true);
         else
-          launch_blend_fwd(map->dm, dc, t->vb, TileLists{t->vals, t->ranges, nullptr, t->counter}, t->ps, fo1, s);
+          launch_blend_fwd(dm, dc, t->vb, TileLists{t->vals, t->ranges, nullptr, t->counter}, t->ps, fo1, s);
       }
       ctx->launches++;
       // pass 2, inside a captured plan as the body of a conditional node (skipped when every tile
@@ -1006,10 +1065,10 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
         {
           PhaseScope ph(ctx, PH_BLEND_FWD);
           if (fuse)
-            launch_blend_fused_l1(map->dm, dc, t->vb, TileLists{t->vals, t->ranges, order2, t->counter, count2}, fo2,
+            launch_blend_fused_l1(dm, dc, t->vb, TileLists{t->vals, t->ranges, order2, t->counter, count2}, fo2,
                                   t->gacc, s2);
           else
-            launch_blend_fwd(map->dm, dc, t->vb, TileLists{t->vals, t->ranges, order2, t->counter, count2}, t->ps,
+            launch_blend_fwd(dm, dc, t->vb, TileLists{t->vals, t->ranges, order2, t->counter, count2}, t->ps,
                              fo2, s2);
         }
         if (cudaGetLastError() != cudaSuccess) st2 = fail(LGS_ECUDA, "layered binning pass 2 launch failed");
@@ -1071,7 +1130,7 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
     if (targets) LGS_CUDA(cudaMemsetAsync(t->loss, 0, sizeof(double), s));
     {
       PhaseScope ph(ctx, PH_BLEND_FWD);
-      launch_blend_fwd(map->dm, dc, t->vb, TileLists{t->vals, t->ranges, t->order, t->counter}, t->ps, fo, s);
+      launch_blend_fwd(dm, dc, t->vb, TileLists{t->vals, t->ranges, t->order, t->counter}, t->ps, fo, s);
     }
     ctx->launches++;
     LGS_CUDA(cudaGetLastError());
@@ -1107,6 +1166,13 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
   dfree(ctx, idx_sorted);
   dfree(ctx, incl);
   if (tstage) dfree(ctx, tstage);
+  if (mapped && !ctx->mh_pending && layered) {
+    CUDAB(cudaMemcpyAsync(ctx->mh_listed_host, ctx->mh_listed_dev, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    CUDAB(cudaEventRecord(ctx->mh_event, s));
+    ctx->mh_pending = true;
+    ctx->mh_pending_key = map->dm.sh;
+    ctx->mh_pending_n = n;
+  }
   if (di.staged) {
     if (di.rgb) CUDAB(cudaMemcpyAsync(out->rgb, di.rgb, sizeof(float) * npix * 3, cudaMemcpyDeviceToHost, s));
     if (di.depth) CUDAB(cudaMemcpyAsync(out->depth, di.depth, sizeof(float) * npix, cudaMemcpyDeviceToHost, s));
@@ -1625,6 +1691,7 @@ LGS_API lgs_status lgs_saved_stats(const lgs_saved* tape, lgs_render_stats* st) 
   st->max_tile_list = mx;
   st->listed = listed;
   st->active = tape->vb.active ? active : vis;
+  st->host_rows = tape->host_rows_in_place ? st->active : 0;
   return LGS_OK;
 }
 

@@ -236,6 +236,7 @@ struct ColorJob {
   float* feat_dst = nullptr;
   int64_t n = 0;
   int d = 0, dp = 0;
+  uint32_t* listed = nullptr;  // host-mapped maps: Gaussians listed by this render (lgs_capi.cu policy)
 };
 
 __device__ __forceinline__ void gather_features(const float* __restrict__ src, float* __restrict__ dst, int64_t n,
@@ -253,6 +254,7 @@ __device__ __forceinline__ void gather_features(const float* __restrict__ src, f
 }
 
 __device__ __forceinline__ void color_job_run(const ColorJob& j, uint32_t g) {
+  if (j.listed) atomicAdd(j.listed, 1u);
   if (j.feat_src) gather_features(j.feat_src, j.feat_dst, j.n, j.d, j.dp, g);
   const float4 po = j.pos_opa[g];
   float4 col;

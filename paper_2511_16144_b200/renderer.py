@@ -220,7 +220,7 @@ class RenderOutput:
         s = _lib.LgsRenderStats()
         check(_lib.load().lgs_saved_stats(self.tape, C.byref(s)))
         return dict(visible=s.visible, pairs=s.pairs, tiles=s.tiles, max_tile_list=s.max_tile_list, listed=s.listed,
-                    active=s.active)
+                    active=s.active, host_rows=s.host_rows)
 
     def work(self):
         """(evaluated (pixel, Gaussian) pairs, contributing pairs) of this forward."""
