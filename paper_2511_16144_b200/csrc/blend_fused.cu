@@ -65,6 +65,24 @@ __device__ __forceinline__ void bar_wait(uint64_t* bar, uint32_t parity) {
 }
 #endif
 
+// two independent reductions, step by step (their shuffles and adds interleave)
+template <int SLOTS>
+__device__ __forceinline__ void fused_transpose_reduce2(float (&v)[SLOTS], float (&u)[SLOTS], int lane) {
+#pragma unroll
+  for (int step = 0; step < 5; ++step) {
+    const int k = 16 >> step;
+    const int half = SLOTS >> (step + 1);
+    const bool upper = (lane & k) != 0;
+#pragma unroll
+    for (int i = 0; i < half; ++i) {
+      const float sv = upper ? v[i] : v[i + half], kv = upper ? v[i + half] : v[i];
+      const float su = upper ? u[i] : u[i + half], ku = upper ? u[i + half] : u[i];
+      v[i] = kv + __shfl_xor_sync(0xffffffffu, sv, k);
+      u[i] = ku + __shfl_xor_sync(0xffffffffu, su, k);
+    }
+  }
+}
+
 template <int SLOTS>
 __device__ __forceinline__ void fused_transpose_reduce(float (&v)[SLOTS], int lane) {
 #pragma unroll
@@ -81,10 +99,13 @@ __device__ __forceinline__ void fused_transpose_reduce(float (&v)[SLOTS], int la
   }
 }
 
-template <int DP>
-__global__ void __launch_bounds__(kBlock / 2) blend_fused_l1_kernel(DevMap m, DevCam c, ViewBufs v, TileLists tl,
-                                                                      FwdOut o, float* __restrict__ gacc) {
-  griddep_wait();
+// ILPF: list entries whose alphas the forward evaluates per step before compositing them in order.
+// 2 for the first layered pass (many tiles, 4 CTAs/SM at 128 registers); 4 for the second pass,
+// whose few unsaturated tiles walk long complete lists with ~1 CTA per SM (latency bound: more
+// independent work per warp, up to 255 registers).
+template <int DP, int ILPF>
+__device__ __forceinline__ void blend_fused_l1_body(const DevMap& m, const DevCam& c, const ViewBufs& v,
+                                                    const TileLists& tl, const FwdOut& o, float* __restrict__ gacc) {
   constexpr int PPT = 2;  // the thread's two pixels are the two lanes of every paired (FFMA2) op
   constexpr int NT = kBlock / PPT;
   constexpr int DQ = DP > 0 ? DP / 4 : 1;
@@ -211,6 +232,7 @@ __global__ void __launch_bounds__(kBlock / 2) blend_fused_l1_kernel(DevMap m, De
         done0 = done0 || T.x < c.t_min;
         done1 = done1 || T.y < c.t_min;
       };
+      if constexpr (ILPF == 2) {  // (hand-paired: the generic form below costs 18 registers more)
       for (int e = 0; e < cnt && !all_done; e += 2) {
         const bool has1 = e + 1 < cnt;
         const uint2 rc0 = sm.rect[e];
@@ -230,6 +252,37 @@ __global__ void __launch_bounds__(kBlock / 2) blend_fused_l1_kernel(DevMap m, De
         if (hit0) composite(e, al0, py0 >= ya0 && py0 <= yb0, py0 + 1 >= ya0 && py0 + 1 <= yb0, r00.z);
         if (hit1) composite(e + 1, al1, py0 >= ya1 && py0 <= yb1, py0 + 1 >= ya1 && py0 + 1 <= yb1, r01.z);
         all_done = done0 && done1;
+      }
+      } else {
+      for (int e = 0; e < cnt && !all_done; e += ILPF) {
+        uint2 rc[ILPF];
+        bool hit[ILPF];
+        bool any_hit = false;
+#pragma unroll
+        for (int j = 0; j < ILPF; ++j) {
+          rc[j] = e + j < cnt ? sm.rect[e + j] : make_uint2(0xffffu, 0xffffu);
+          hit[j] = px >= (int)(rc[j].x & 0xffffu) && px <= (int)(rc[j].x >> 16) && py0 <= (int)(rc[j].y >> 16) &&
+                   py0 + PPT - 1 >= (int)(rc[j].y & 0xffffu);
+          any_hit = any_hit || hit[j];
+        }
+        if (!any_hit) continue;
+        float2 al[ILPF];
+        float zj[ILPF];
+#pragma unroll
+        for (int j = 0; j < ILPF; ++j) {
+          const int ej = e + j < cnt ? e + j : e;
+          const float4 r0 = sm.r0[ej], fa = sm.fa[ej], fb = sm.fb[ej];
+          float2 S, Tt, G;
+          al[j] = frame_alpha2(fa, fb, r0.w, ex2, ey2, S, Tt, G);
+          zj[j] = r0.z;
+        }
+#pragma unroll
+        for (int j = 0; j < ILPF; ++j) {
+          const int ya = (int)(rc[j].y & 0xffffu), yb = (int)(rc[j].y >> 16);
+          if (hit[j]) composite(e + j, al[j], py0 >= ya && py0 <= yb, py0 + 1 >= ya && py0 + 1 <= yb, zj[j]);
+        }
+        all_done = done0 && done1;
+      }
       }
     }
 
@@ -330,6 +383,104 @@ __global__ void __launch_bounds__(kBlock / 2) blend_fused_l1_kernel(DevMap m, De
         staged();
       }
       const int e_top = (int)min((int64_t)cnt - 1, (int64_t)warp_last - 1 - (int64_t)bpos);
+      if constexpr (ILPF == 4) {
+        // two entries per step (e, then e - 1): their alphas, dl and gradient values are
+        // independent; only T and accum carry from one to the next, so the two transposed
+        // reductions interleave.  Same per-entry arithmetic and order as the loop below.
+        for (int e = e_top; e >= 0; e -= 2) {
+          bool col_in[2], okp[2][2];
+          float2 al[2], S2[2], T2[2], G2[2];
+          bool any[2];
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const int ej = e - j >= 0 ? e - j : e;
+            const uint2 rc = sm.rect[ej];
+            const int ry0 = (int)(rc.y & 0xffffu), ry1 = (int)(rc.y >> 16);
+            col_in[j] = e - j >= 0 && px >= (int)(rc.x & 0xffffu) && px <= (int)(rc.x >> 16) && py0 <= ry1 &&
+                        py0 + PPT - 1 >= ry0;
+            const float4 r0 = sm.r0[ej];
+            al[j] = frame_alpha2(sm.fa[ej], sm.fb[ej], r0.w, ex2, ey2, S2[j], T2[j], G2[j]);
+            const uint32_t jrel = bpos + (uint32_t)(e - j);
+            okp[j][0] = col_in[j] && jrel < last0 && py0 >= ry0 && py0 <= ry1 && al[j].x >= c.alpha_skip;
+            okp[j][1] = col_in[j] && jrel < last1 && py0 + 1 >= ry0 && py0 + 1 <= ry1 && al[j].y >= c.alpha_skip;
+            any[j] = __any_sync(0xffffffffu, okp[j][0] || okp[j][1]);
+          }
+          if (!any[0] && !any[1]) continue;
+          float vals[2][SLOTS];
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            if (!any[j]) continue;
+            const int ej = e - j;
+#pragma unroll
+            for (int q = 0; q < SLOTS; ++q) vals[j][q] = 0.f;
+            const float2 alpha = make_float2(okp[j][0] ? al[j].x : 0.f, okp[j][1] ? al[j].y : 0.f);
+            const float4 r0 = sm.r0[ej];
+            const float4 col = sm.col[ej];
+            const float4 fa = sm.fa[ej], fb = sm.fb[ej];
+            const float op = r0.w;
+            const float do_dlogit = op * (1.0f - op);
+            const float2 a = make_float2(fminf(alpha.x, c.alpha_clamp), fminf(alpha.y, c.alpha_clamp));
+            const float2 inv1ma = make_float2(fast_rcp(1.0f - a.x), fast_rcp(1.0f - a.y));
+            T = mul2(T, inv1ma);
+            const float2 w = mul2(a, T);
+            float2 dl = fma2(g_draw, bc2(r0.z), g_acc);
+            dl = fma2(g_r, bc2(col.x), dl);
+            dl = fma2(g_g, bc2(col.y), dl);
+            dl = fma2(g_b, bc2(col.z), dl);
+            if (DP > 0) {
+#pragma unroll
+              for (int q = 0; q < DQ; ++q) {
+                const float4 fv = sm.feat[ej][q];
+                const float4 g01 = sm.gfeat[2 * q][tid];
+                const float4 g23 = sm.gfeat[2 * q + 1][tid];
+                dl = fma2(make_float2(g01.x, g01.y), bc2(fv.x), dl);
+                dl = fma2(make_float2(g01.z, g01.w), bc2(fv.y), dl);
+                dl = fma2(make_float2(g23.x, g23.y), bc2(fv.z), dl);
+                dl = fma2(make_float2(g23.z, g23.w), bc2(fv.w), dl);
+                float* vf = vals[j] + kSlotFeat + q * 4;
+                vf[0] = fmaf(g01.y, w.y, g01.x * w.x);
+                vf[1] = fmaf(g01.w, w.y, g01.z * w.x);
+                vf[2] = fmaf(g23.y, w.y, g23.x * w.x);
+                vf[3] = fmaf(g23.w, w.y, g23.z * w.x);
+              }
+            }
+            const float2 dla = fma2(make_float2(-accum.x, -accum.y), inv1ma, mul2(T, dl));
+            const float2 dl_da = make_float2((alpha.x != 0.f && !(alpha.x > c.alpha_clamp)) ? dla.x : 0.f,
+                                             (alpha.y != 0.f && !(alpha.y > c.alpha_clamp)) ? dla.y : 0.f);
+            accum = fma2(dl, w, accum);
+            vals[j][kSlotColor + 0] = fmaf(g_r.y, w.y, g_r.x * w.x);
+            vals[j][kSlotColor + 1] = fmaf(g_g.y, w.y, g_g.x * w.x);
+            vals[j][kSlotColor + 2] = fmaf(g_b.y, w.y, g_b.x * w.x);
+            vals[j][kSlotZ] = fmaf(g_draw.y, w.y, g_draw.x * w.x);
+            const float2 G = G2[j], S = S2[j], Tt = T2[j];
+            const float2 dlg = mul2(dl_da, G);
+            vals[j][kSlotOpac] = (dlg.x + dlg.y) * do_dlogit;
+            const float2 cf = mul2(mul2(dl_da, bc2(op)), mul2(bc2(-0.5f), G));
+            const float2 dqx = mul2(bc2(kTwoOverHalfLog2e), fma2(S, bc2(fa.z), mul2(Tt, bc2(fb.x))));
+            const float2 dqy = mul2(bc2(kTwoOverHalfLog2e), fma2(S, bc2(fa.w), mul2(Tt, bc2(fb.y))));
+            const float2 dx = add2(bc2(fb.z), ex2), dy = add2(bc2(fb.w), ey2);
+            const float2 mx = mul2(cf, dqx), my = mul2(cf, dqy);
+            vals[j][kSlotMuX] = -(mx.x + mx.y);
+            vals[j][kSlotMuY] = -(my.x + my.y);
+            const float2 cdx = mul2(cf, dx), cdy = mul2(cf, dy);
+            const float2 ca = mul2(cdx, dx), cb2_ = mul2(cdx, dy), cc = mul2(cdy, dy);
+            vals[j][kSlotConA] = ca.x + ca.y;
+            vals[j][kSlotConB] = cb2_.x + cb2_.y;
+            vals[j][kSlotConC] = cc.x + cc.y;
+          }
+          if (any[0] && any[1]) {
+            fused_transpose_reduce2<SLOTS>(vals[0], vals[1], lane);
+            gacc_add(gacc + (size_t)sm.gid[e] * SLOTS, lane, vals[0][0]);
+            gacc_add(gacc + (size_t)sm.gid[e - 1] * SLOTS, lane, vals[1][0]);
+          } else if (any[0]) {
+            fused_transpose_reduce<SLOTS>(vals[0], lane);
+            gacc_add(gacc + (size_t)sm.gid[e] * SLOTS, lane, vals[0][0]);
+          } else {
+            fused_transpose_reduce<SLOTS>(vals[1], lane);
+            gacc_add(gacc + (size_t)sm.gid[e - 1] * SLOTS, lane, vals[1][0]);
+          }
+        }
+      } else {
       for (int e = e_top; e >= 0; --e) {
         const uint32_t jrel = bpos + (uint32_t)e;
         const uint2 rc = sm.rect[e];
@@ -404,6 +555,7 @@ __global__ void __launch_bounds__(kBlock / 2) blend_fused_l1_kernel(DevMap m, De
         fused_transpose_reduce<SLOTS>(vals, lane);
         gacc_add(gacc + (size_t)sm.gid[e] * SLOTS, lane, vals[0]);
       }
+      }
     }
   }
 
@@ -418,29 +570,59 @@ __global__ void __launch_bounds__(kBlock / 2) blend_fused_l1_kernel(DevMap m, De
   }
 }
 
+// Two entry points: the first pass (4 CTAs/SM at 128 registers; an explicit minimum-blocks bound
+// changes its code generation, so none is given) and the second pass's latency-bound variant
+// (register file free: ~1 CTA per SM).
+template <int DP>
+__global__ void __launch_bounds__(kBlock / 2) blend_fused_l1_kernel(DevMap m, DevCam c, ViewBufs v, TileLists tl,
+                                                                      FwdOut o, float* __restrict__ gacc) {
+  griddep_wait();
+  blend_fused_l1_body<DP, 2>(m, c, v, tl, o, gacc);
+}
+template <int DP>
+__global__ void __launch_bounds__(kBlock / 2, 1) blend_fused_l1_long_kernel(DevMap m, DevCam c, ViewBufs v,
+                                                                              TileLists tl, FwdOut o,
+                                                                              float* __restrict__ gacc) {
+  griddep_wait();
+  blend_fused_l1_body<DP, 4>(m, c, v, tl, o, gacc);
+}
+
 bool blend_fused_supported(int dp) { return dp == 16 || dp == 8 || dp == 4 || dp == 0; }
 
-template <int DP>
+template <int DP, int ILPF>
 static void launch_fused_dp(const DevMap& m, const DevCam& c, const ViewBufs& v, const TileLists& tl, const FwdOut& o,
                             float* gacc, cudaStream_t s, bool counter_zeroed) {
-  const void* kfn = reinterpret_cast<const void*>(blend_fused_l1_kernel<DP>);
+  auto kernel = ILPF == 2 ? blend_fused_l1_kernel<DP> : blend_fused_l1_long_kernel<DP>;
+  const void* kfn = reinterpret_cast<const void*>(kernel);
   if (LGS_FUSED_DYN_PAD > 0) ensure_dyn_smem(kfn, LGS_FUSED_DYN_PAD);
   const int ctas_per_sm = kernel_ctas_per_sm(kfn, kBlock / 2, LGS_FUSED_DYN_PAD);
   const int sms = device_sm_count();
   const int ntiles = c.tiles_x * c.tiles_y;
   const int grid = min(ntiles, ctas_per_sm * sms);
   if (!counter_zeroed) cudaMemsetAsync(tl.counter, 0, sizeof(int), s);
-  launch_pdl(blend_fused_l1_kernel<DP>, dim3(grid), dim3(kBlock / 2), LGS_FUSED_DYN_PAD, s, m, c, v, tl, o, gacc);
+  launch_pdl(kernel, dim3(grid), dim3(kBlock / 2), LGS_FUSED_DYN_PAD, s, m, c, v, tl, o, gacc);
+}
+
+template <int ILPF>
+static void launch_fused_ilp(const DevMap& m, const DevCam& c, const ViewBufs& v, const TileLists& tl, const FwdOut& o,
+                             float* gacc, cudaStream_t s, bool counter_zeroed) {
+  switch (m.dp) {
+    case 0: launch_fused_dp<0, ILPF>(m, c, v, tl, o, gacc, s, counter_zeroed); break;
+    case 4: launch_fused_dp<4, ILPF>(m, c, v, tl, o, gacc, s, counter_zeroed); break;
+    case 8: launch_fused_dp<8, ILPF>(m, c, v, tl, o, gacc, s, counter_zeroed); break;
+    default: launch_fused_dp<16, ILPF>(m, c, v, tl, o, gacc, s, counter_zeroed); break;
+  }
 }
 
 void launch_blend_fused_l1(const DevMap& m, const DevCam& c, const ViewBufs& v, const TileLists& tl, const FwdOut& o,
-                           float* gacc, cudaStream_t s, bool counter_zeroed) {
-  switch (m.dp) {
-    case 0: launch_fused_dp<0>(m, c, v, tl, o, gacc, s, counter_zeroed); break;
-    case 4: launch_fused_dp<4>(m, c, v, tl, o, gacc, s, counter_zeroed); break;
-    case 8: launch_fused_dp<8>(m, c, v, tl, o, gacc, s, counter_zeroed); break;
-    default: launch_fused_dp<16>(m, c, v, tl, o, gacc, s, counter_zeroed); break;
-  }
+                           float* gacc, cudaStream_t s, bool counter_zeroed, bool long_lists) {
+#ifndef LGS_PASS2_ILP
+#define LGS_PASS2_ILP 4
+#endif
+  if (long_lists && LGS_PASS2_ILP == 4)
+    launch_fused_ilp<4>(m, c, v, tl, o, gacc, s, counter_zeroed);
+  else
+    launch_fused_ilp<2>(m, c, v, tl, o, gacc, s, counter_zeroed);
 }
 
 }  // namespace lgs

@@ -25,6 +25,7 @@
 #include <vector>
 
 #include "../../include/lgs.h"
+#include "dev_cache.h"
 #include "lgs_internal.cuh"
 #include "lgs_kernels.h"
 #include "nccl_dyn.h"
@@ -1031,7 +1032,7 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
         PhaseScope ph(ctx, PH_BLEND_FWD);
         if (fuse)
           launch_blend_fused_l1(dm, dc, t->vb, TileLists{t->vals, t->ranges, nullptr, t->counter}, fo1, t->gacc, s,
-                                true);
+                                true, ntiles < 2 * device_sm_count());  // few tiles: latency-bound variant
         else
           launch_blend_fwd(dm, dc, t->vb, TileLists{t->vals, t->ranges, nullptr, t->counter}, t->ps, fo1, s);
       }
@@ -1066,7 +1067,7 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
           PhaseScope ph(ctx, PH_BLEND_FWD);
           if (fuse)
             launch_blend_fused_l1(dm, dc, t->vb, TileLists{t->vals, t->ranges, order2, t->counter, count2}, fo2,
-                                  t->gacc, s2);
+                                  t->gacc, s2, false, true);
           else
             launch_blend_fwd(dm, dc, t->vb, TileLists{t->vals, t->ranges, order2, t->counter, count2}, t->ps,
                              fo2, s2);

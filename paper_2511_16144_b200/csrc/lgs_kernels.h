@@ -172,8 +172,9 @@ void launch_blend_fwd(const DevMap& m, const DevCam& c, const ViewBufs& v, const
 // K5 + K6 fused for the fused-L1 loss (blend_fused.cu): images, loss and the screen-space
 // gradient accumulator gacc (rows of the listed Gaussians zeroed beforehand) in one pass per tile.
 bool blend_fused_supported(int dp);
+// long_lists: the second layered pass (few tiles, complete lists): the latency-bound variant
 void launch_blend_fused_l1(const DevMap& m, const DevCam& c, const ViewBufs& v, const TileLists& tl, const FwdOut& o,
-                           float* gacc, cudaStream_t s, bool counter_zeroed = false);
+                           float* gacc, cudaStream_t s, bool counter_zeroed = false, bool long_lists = false);
 void launch_blend_bwd(const DevMap& m, const DevCam& c, const ViewBufs& v, const TileLists& tl,
                       const PixelState& ps, const BwdIn& in, float* gacc, int slots, cudaStream_t s);
 // Row-sparse gradient exchange (sparse_reduce.cu): ptr/width = the six MapGradients attributes
