@@ -370,6 +370,7 @@ __device__ __forceinline__ void blend_fused_l1_body(const DevMap& m, const DevCa
     __syncthreads();
     const uint32_t warp_last = __reduce_max_sync(0xffffffffu, my_max);
     if (lane == 0 && warp_last) atomicMax(&s_max, warp_last);
+    if (lane == 0 && warp_last && o.consumed) atomicAdd(o.consumed, warp_last);
     __syncthreads();
     float2 accum = bc2(0.f);
     for (int b = s_max ? (int)((s_max - 1) / NB) : -1; b >= 0; --b) {

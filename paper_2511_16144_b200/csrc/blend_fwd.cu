@@ -189,6 +189,13 @@ __global__ void __launch_bounds__(kBlock / PPT, MINB) blend_fwd_kernel(DevMap m,
     // layered first pass: a tile with an unsaturated pixel is rendered again on its complete list
     const bool tile_done = o.unfinished ? __syncthreads_and(all_done) != 0 : true;
     if (!tile_done && tid == 0) o.unfinished[tile] = 1u;
+    if (o.consumed && tile_done) {  // list length this warp consumed (layer-A size policy)
+      uint32_t mx = 0;
+#pragma unroll
+      for (int k = 0; k < PPT; ++k) mx = max(mx, last[k]);
+      mx = __reduce_max_sync(0xffffffffu, mx);
+      if ((tid & 31) == 0 && mx) atomicAdd(o.consumed, mx);
+    }
 #pragma unroll
     for (int k = 0; k < PPT; ++k) {
       const int py = py0 + k;

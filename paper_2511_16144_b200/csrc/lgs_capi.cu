@@ -79,6 +79,7 @@ GradOut device_grad_out(const lgs_map_grads* g, int d) {
 }
 
 // layer A of the depth-layered binning owns ~1/kLayerDiv of the pairs (binning_fast.cu)
+// (the starting value: lgs_ctx::layer_div adapts it per context)
 constexpr uint32_t kLayerDiv = 16;
 
 int bits_for(int ntiles) {
@@ -154,6 +155,20 @@ struct lgs_ctx {
   int64_t mh_pending_n = 0;
   const void* mh_key = nullptr;  // the last map whose count has landed, and that count
   int64_t mh_n = 0, mh_listed = 0;
+  // Layer-A size of the depth-layered binning (~P / layer_div pairs, <= n / (2 layer_div)
+  // Gaussians).  Adapted between uncaptured renders from the previous one's counters (lp_*):
+  // when more than a quarter of the tiles needed the second pass, layer A doubles (and that size
+  // is remembered as too small); when almost every tile saturated having consumed less than 1/16
+  // of its list, it shrinks 4x (a dense view whose near splats cover most tiles).  Plans capture
+  // with the size their warm-up renders settle on.
+  uint32_t layer_div = kLayerDiv;
+  uint32_t layer_bad = UINT32_MAX;  // a div at which too many tiles were left unsaturated
+  uint32_t* lp_dev = nullptr;       // [0] consumed, [1] layer-A listed pairs, [2] unfinished tiles
+  uint32_t* lp_host = nullptr;      // pinned copy
+  cudaEvent_t lp_ev = nullptr;
+  bool lp_pending = false;
+  int lp_ntiles = 0;
+  uint32_t lp_div = 0;  // the div the pending counts were taken at
   // last lgs_find_language_redundant: candidates (a similar neighbour inside tau_dist), rounds
   int64_t prune_candidates = 0, prune_rounds = 0;
 };
@@ -332,6 +347,9 @@ void ctx_release(lgs_ctx* ctx) {
     if (ctx->mh_listed_host) cudaFreeHost(ctx->mh_listed_host);
     if (ctx->mh_listed_dev) cudaFree(ctx->mh_listed_dev);
     if (ctx->mh_event) cudaEventDestroy(ctx->mh_event);
+    if (ctx->lp_host) cudaFreeHost(ctx->lp_host);
+    if (ctx->lp_dev) cudaFree(ctx->lp_dev);
+    if (ctx->lp_ev) cudaEventDestroy(ctx->lp_ev);
     if (ctx->dev_u32) cudaFree(ctx->dev_u32);
     if (ctx->pairs_ready) cudaEventDestroy(ctx->pairs_ready);
     if (ctx->sparse_ovf_dev) cudaFree(ctx->sparse_ovf_dev);
@@ -743,6 +761,29 @@ LGS_API int64_t lgs_grads_flat_size(int64_t n, int32_t feature_dim, int32_t sh_d
 // -------------------------------------------------------------------------------------------
 // forward
 // -------------------------------------------------------------------------------------------
+}  // extern "C"
+
+namespace {
+// The layer-A size policy (lgs_ctx::layer_div): reads the counters of the previous uncaptured
+// layered render once they have landed (never waits).
+void layer_policy_update(lgs_ctx* ctx, int ntiles) {
+  if (!ctx->lp_pending || cudaEventQuery(ctx->lp_ev) != cudaSuccess) return;
+  ctx->lp_pending = false;
+  if (ctx->lp_ntiles != ntiles || ctx->lp_div != ctx->layer_div) return;  // counts of another image / size
+  const uint64_t consumed = ctx->lp_host[0], listed = ctx->lp_host[1], unfinished = ctx->lp_host[2];
+  uint32_t& div = ctx->layer_div;
+  if (unfinished * 4 > (uint64_t)ntiles) {
+    ctx->layer_bad = std::min(ctx->layer_bad, div);
+    div = std::max<uint32_t>(4, div / 2);
+  } else if (unfinished * 50 < (uint64_t)ntiles && listed > 0 && consumed * 4 < listed && div < 1024 &&
+             div * 4 < ctx->layer_bad) {
+    div *= 4;  // warps consumed < 1/16 of their lists on average (4 warps per tile)
+  }
+}
+}  // namespace
+
+extern "C" {
+
 LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lgs_camera* cam,
                                       const lgs_render_config* cfg_in, const lgs_l1_targets* targets,
                                       lgs_images* out, lgs_saved** tape) {
@@ -807,6 +848,7 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
   // the depth order of layer A is built with the binning below, the complete order only when some
   // tile needs the second pass
   const bool layered = fast && !ctx->full_lists && n > 0 && !cub_depth;
+  if (layered && !ctx->capturing) layer_policy_update(ctx, ntiles);
   void* otemp = nullptr;
   const size_t otemp_bytes = cub_depth ? 0 : depth_order_temp_bytes(n);
   if (!cub_depth) TRYB(dalloc(ctx, reinterpret_cast<uint8_t**>(&otemp), otemp_bytes));
@@ -981,8 +1023,9 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
       // the depth-ordered candidates) and the forward, which flags every tile it could not
       // saturate.  Those tiles get their complete lists (counting sort restricted to them, at
       // vals + capA) and are blended again: pass 2, a conditional node of a captured plan.
-      const uint32_t capA = (uint32_t)layer_a_cap(cap, ntiles, kLayerDiv);
-      const int64_t gcapA = std::min<int64_t>(n, std::max<int64_t>(4096, n / 32));
+      const uint32_t ldiv = ctx->layer_div;
+      const uint32_t capA = (uint32_t)layer_a_cap(cap, ntiles, ldiv);
+      const int64_t gcapA = std::min<int64_t>(n, std::max<int64_t>(4096, n / (2 * (int64_t)ldiv)));
       const size_t sat_n = (size_t)(dc.tiles_x + 1) * (dc.tiles_y + 1);
       uint32_t *ra = nullptr, *unfinished = nullptr, *sat = nullptr, *order2 = nullptr, *count2 = nullptr;
       uint32_t* scratch_b = nullptr;
@@ -1011,7 +1054,7 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
       }
       {
         PhaseScope ph(ctx, PH_DEPTH_SORT);
-        launch_depth_order_layer_a(t->vb, n, dc.near_plane, otemp, kLayerDiv, kLayerMinPairs, gcapA, capA,
+        launch_depth_order_layer_a(t->vb, n, dc.near_plane, otemp, ldiv, kLayerMinPairs, gcapA, capA,
                                    idx_sorted, cand_rect, ra, t->vb.active, fuse ? t->gacc : nullptr, !exact, cj, s);
       }
       {
@@ -1027,6 +1070,16 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
       if (targets && !fuse) LGS_CUDA(cudaMemsetAsync(t->loss, 0, sizeof(double), s));
       FwdOut fo1 = fo;
       fo1.unfinished = unfinished;
+      const bool policy = !ctx->capturing && !ctx->lp_pending;  // count this render for the layer-A policy
+      if (policy) {
+        if (!ctx->lp_dev) {
+          LGS_CUDA(cudaMalloc(reinterpret_cast<void**>(&ctx->lp_dev), 4 * sizeof(uint32_t)));
+          LGS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ctx->lp_host), 4 * sizeof(uint32_t), cudaHostAllocDefault));
+          LGS_CUDA(cudaEventCreateWithFlags(&ctx->lp_ev, cudaEventDisableTiming));
+        }
+        LGS_CUDA(cudaMemsetAsync(ctx->lp_dev, 0, sizeof(uint32_t), s));
+        fo1.consumed = ctx->lp_dev;
+      }
       TRYB(fork_prezero());
       {
         PhaseScope ph(ctx, PH_BLEND_FWD);
@@ -1047,6 +1100,15 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
         launch_layer_flag(unfinished, ntiles, count2, count2 + 1, use_cond ? &cond : nullptr, s);
       }
       ctx->launches++;
+      if (policy) {
+        LGS_CUDA(cudaMemcpyAsync(ctx->lp_dev + 1, ra + 1, sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+        LGS_CUDA(cudaMemcpyAsync(ctx->lp_dev + 2, count2, sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+        LGS_CUDA(cudaMemcpyAsync(ctx->lp_host, ctx->lp_dev, 4 * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+        LGS_CUDA(cudaEventRecord(ctx->lp_ev, s));
+        ctx->lp_pending = true;
+        ctx->lp_ntiles = ntiles;
+        ctx->lp_div = ldiv;
+      }
       if (use_cond) LGS_TRY(cond_begin(ctx, cond));
       lgs_status st2 = LGS_OK;
       {
@@ -2894,7 +2956,16 @@ LGS_API lgs_status lgs_plan_create(lgs_ctx* ctx, lgs_map* map, const lgs_camera*
       cudaMallocHost(&p->host_pairs, 64) != cudaSuccess ||
       cudaStreamCreateWithFlags(&p->cap_stream, cudaStreamNonBlocking) != cudaSuccess)
     return bail(fail(LGS_ECUDA, "event / stream creation failed"));
-  // one eager step sizes the tile-list capacity (and runs every one-time kernel setup)
+  // forward-only eager renders until the layer-A size policy settles (at most 4), then one eager
+  // step sizes the tile-list capacity (and runs every one-time kernel setup)
+  for (int it = 0; it < 4; ++it) {
+    const uint32_t div0 = ctx->layer_div;
+    lgs_status sw = lgs_render_forward(ctx, map, &p->cam, &p->cfg, &p->targets, nullptr, nullptr);
+    if (sw != LGS_OK) return bail(sw);
+    if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return bail(fail(LGS_ECUDA, "warm-up render failed"));
+    layer_policy_update(ctx, ((p->cam.width + LGS_TILE - 1) / LGS_TILE) * ((p->cam.height + LGS_TILE - 1) / LGS_TILE));
+    if (ctx->layer_div == div0 && it > 0) break;
+  }
   lgs_saved* tape = nullptr;
   lgs_status st =
       lgs_render_forward(ctx, map, &p->cam, &p->cfg, &p->targets, p->has_images ? &p->images : nullptr, &tape);

@@ -69,6 +69,9 @@ struct FwdOut {
   // depth-layered first pass: tiles not saturated by their (prefix) list are flagged here and get
   // no loss / cotangents (the second pass renders them again on their complete lists)
   uint32_t* unfinished = nullptr;
+  // ... and every warp of a saturated tile adds the list length its pixels consumed (the layer-A
+  // size policy of lgs_capi.cu)
+  uint32_t* consumed = nullptr;
 };
 
 struct BwdIn {
