@@ -190,6 +190,12 @@ LGS_API lgs_status lgs_ctx_set_stream(lgs_ctx* ctx, void* stream);
  * targets, cotangents, images, gradients; reads of LGS_MEM_HOST_MAPPED memory are not copies). */
 LGS_API lgs_status lgs_ctx_transfer_bytes(const lgs_ctx* ctx, int64_t* h2d, int64_t* d2h);
 LGS_API lgs_status lgs_ctx_synchronize(lgs_ctx* ctx);
+/* Depth-layered binning: layer A of the context's next render takes ~1/div of the (tile, Gaussian)
+ * pairs (at most n / (2 div) Gaussians).  div starts at 16 and adapts between uncaptured renders
+ * from the previous render's counters: x1/2 when more than a quarter of the tiles needed the
+ * second pass, x4 when fewer than 2% did and the tiles consumed less than 1/16 of their lists
+ * (views whose near splats cover most tiles).  Results do not depend on it; diagnostics only. */
+LGS_API int32_t lgs_ctx_layer_div(const lgs_ctx* ctx);
 
 /* ---- device-resident map (K9 pack: reference layouts -> device SoA) ------------------- */
 LGS_API lgs_status lgs_map_create(lgs_ctx* ctx, const lgs_gaussians* src, lgs_map** out);

@@ -105,6 +105,7 @@ SIGNATURES = [
     ("lgs_ctx_set_stream", C.c_int, [C.c_void_p, C.c_void_p]),
     ("lgs_ctx_synchronize", C.c_int, [C.c_void_p]),
     ("lgs_ctx_launch_count", C.c_int64, [C.c_void_p]),
+    ("lgs_ctx_layer_div", C.c_int32, [C.c_void_p]),
     ("lgs_map_create", C.c_int, [C.c_void_p, C.POINTER(LgsGaussians), C.POINTER(C.c_void_p)]),
     ("lgs_map_update", C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(LgsGaussians)]),
     ("lgs_map_destroy", C.c_int, [C.c_void_p]),

@@ -698,6 +698,8 @@ LGS_API lgs_status lgs_ctx_synchronize(lgs_ctx* ctx) {
 
 LGS_API int64_t lgs_ctx_launch_count(const lgs_ctx* ctx) { return ctx ? ctx->launches.load() : 0; }
 
+LGS_API int32_t lgs_ctx_layer_div(const lgs_ctx* ctx) { return ctx ? (int32_t)ctx->layer_div : -1; }
+
 LGS_API lgs_status lgs_map_create(lgs_ctx* ctx, const lgs_gaussians* src, lgs_map** out) {
   if (!ctx || !out) return fail(LGS_EINVAL, "ctx/out is NULL");
   *out = nullptr;

@@ -127,6 +127,11 @@ class Context:
         return a.value, b.value
 
     @property
+    def layer_div(self) -> int:
+        """Layer-A size policy of the depth-layered binning (lgs_ctx_layer_div; diagnostics)."""
+        return int(_lib.load().lgs_ctx_layer_div(self.h))
+
+    @property
     def launches(self) -> int:
         return int(_lib.load().lgs_ctx_launch_count(self.h))
 

@@ -480,6 +480,28 @@ def test_layered_binning_matches_full_lists(name, n):
     _layered_vs_full(scene, cam, tg)
 
 
+def test_layer_policy_keeps_results():
+    """The layer-A size adapts between renders of a context (lgs_ctx_layer_div): a view whose near
+    splats cover most tiles (configs[4] mid-arc, at 600k) shrinks layer A over successive renders;
+    every render stays bitwise identical (images) to complete lists and to the first render."""
+    scene, cams, info = scenes.make_config("c4", n=600_000)
+    cam = cams[8]
+    tg = scenes.make_targets(cam, scene["feat"].shape[0], info["depth_range"], 3)
+    ds = dev_scene(scene)
+    dtg = {k: torch.from_numpy(v).cuda() for k, v in tg.items()}
+    ref = R.render(ds, cam, targets=dtg, ctx=R.Context(0, full_lists=True))
+    ctx = R.Context(0)
+    divs = []
+    for _ in range(4):
+        divs.append(ctx.layer_div)
+        out = R.render(ds, cam, targets=dtg, ctx=ctx)
+        torch.cuda.synchronize()
+        for k in ("rgb", "depth", "feat", "acc"):
+            assert torch.equal(getattr(out, k), getattr(ref, k)), (k, divs)
+    print("\nlayer div per render", divs, "listed", out.stats()["listed"], "of", ref.stats()["listed"])
+    assert divs[0] == 16 and divs[-1] > 16
+
+
 def test_layered_binning_mixed_saturation():
     """Half the image covered by a dense near wall of splats (saturates on layer A), the other half
     by sparse far splats (second pass): both passes in one frame."""
