@@ -51,7 +51,7 @@ def parse():
     p.add_argument("--no-mapping", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-pruning", action="store_true")
-    p.add_argument("--e2e-steps", type=int, default=10)
+    p.add_argument("--e2e-steps", type=int, default=30)
     p.add_argument("--e2e-threads", type=int, default=3)
     p.add_argument("--sampler", choices=["nvml", "smi", "none"], default="nvml", help=argparse.SUPPRESS)
     return p.parse_args()

@@ -370,6 +370,20 @@ size_t layer_a_cap(int64_t pairs_cap, int ntiles, uint32_t div) {
 }
 
 
+// Copies up to 4 device counters into page-locked host memory mapped into the device: posted PCIe
+// writes from the SMs, so a tiny readback never queues behind another context's bulk copy in the
+// copy engines (the host reads them once an event after this kernel has completed).
+__global__ void publish_counters_kernel(CounterSrc c, uint32_t* dst) {
+  if ((int)threadIdx.x < c.n) {
+    reinterpret_cast<volatile uint32_t*>(dst)[threadIdx.x] = *c.src[threadIdx.x];
+    __threadfence_system();
+  }
+}
+
+void launch_publish_counters(const CounterSrc& c, uint32_t* dst_mapped, cudaStream_t s) {
+  publish_counters_kernel<<<1, 32, 0, s>>>(c, dst_mapped);
+}
+
 // One CTA: the number of unfinished tiles, and inside a captured plan the conditional that runs the
 // second pass only when there is one.
 __global__ void __launch_bounds__(1024) layer_flag_kernel(const uint32_t* __restrict__ unfinished, int ntiles,

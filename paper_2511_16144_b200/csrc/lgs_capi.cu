@@ -148,7 +148,8 @@ struct lgs_ctx {
   // layer A take the complete lists), scattered PCIe reads of [d][N] feature columns lose to one
   // DMA of the SH and feature blocks, so the next render of that map copies them in bulk.
   uint32_t* mh_listed_dev = nullptr;
-  uint32_t* mh_listed_host = nullptr;  // pinned: the count of the render whose copy is pending
+  uint32_t* mh_listed_host = nullptr;  // mapped pinned: the count of the render whose copy is pending
+  uint32_t* mh_listed_hdev = nullptr;  // its device address
   cudaEvent_t mh_event = nullptr;      // recorded after that copy
   bool mh_pending = false;
   const void* mh_pending_key = nullptr;  // its map (SH pointer) and size
@@ -163,8 +164,9 @@ struct lgs_ctx {
   // with the size their warm-up renders settle on.
   uint32_t layer_div = kLayerDiv;
   uint32_t layer_bad = UINT32_MAX;  // a div at which too many tiles were left unsaturated
-  uint32_t* lp_dev = nullptr;       // [0] consumed, [1] layer-A listed pairs, [2] unfinished tiles
-  uint32_t* lp_host = nullptr;      // pinned copy
+  uint32_t* lp_dev = nullptr;       // [0] consumed (the host copy: + [1] layer-A listed pairs, [2] unfinished tiles)
+  uint32_t* lp_host = nullptr;      // mapped pinned copy (written by launch_publish_counters)
+  uint32_t* lp_hdev = nullptr;      // its device address
   cudaEvent_t lp_ev = nullptr;
   bool lp_pending = false;
   int lp_ntiles = 0;
@@ -863,7 +865,8 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
   if (mapped) {
     if (!ctx->mh_listed_dev) {
       CUDAB(cudaMalloc(reinterpret_cast<void**>(&ctx->mh_listed_dev), sizeof(uint32_t)));
-      CUDAB(cudaHostAlloc(reinterpret_cast<void**>(&ctx->mh_listed_host), sizeof(uint32_t), cudaHostAllocDefault));
+      CUDAB(cudaHostAlloc(reinterpret_cast<void**>(&ctx->mh_listed_host), sizeof(uint32_t), cudaHostAllocMapped));
+      CUDAB(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->mh_listed_hdev), ctx->mh_listed_host, 0));
       CUDAB(cudaEventCreateWithFlags(&ctx->mh_event, cudaEventDisableTiming));
     }
     if (ctx->mh_pending && cudaEventQuery(ctx->mh_event) == cudaSuccess) {  // the last count has landed
@@ -1076,7 +1079,8 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
       if (policy) {
         if (!ctx->lp_dev) {
           LGS_CUDA(cudaMalloc(reinterpret_cast<void**>(&ctx->lp_dev), 4 * sizeof(uint32_t)));
-          LGS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ctx->lp_host), 4 * sizeof(uint32_t), cudaHostAllocDefault));
+          LGS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ctx->lp_host), 4 * sizeof(uint32_t), cudaHostAllocMapped));
+          LGS_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->lp_hdev), ctx->lp_host, 0));
           LGS_CUDA(cudaEventCreateWithFlags(&ctx->lp_ev, cudaEventDisableTiming));
         }
         LGS_CUDA(cudaMemsetAsync(ctx->lp_dev, 0, sizeof(uint32_t), s));
@@ -1103,9 +1107,13 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
       }
       ctx->launches++;
       if (policy) {
-        LGS_CUDA(cudaMemcpyAsync(ctx->lp_dev + 1, ra + 1, sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
-        LGS_CUDA(cudaMemcpyAsync(ctx->lp_dev + 2, count2, sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
-        LGS_CUDA(cudaMemcpyAsync(ctx->lp_host, ctx->lp_dev, 4 * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+        CounterSrc cs{};
+        cs.src[0] = ctx->lp_dev;  // consumed
+        cs.src[1] = ra + 1;       // layer-A listed pairs
+        cs.src[2] = count2;       // unfinished tiles
+        cs.n = 3;
+        launch_publish_counters(cs, ctx->lp_hdev, s);
+        ctx->launches++;
         LGS_CUDA(cudaEventRecord(ctx->lp_ev, s));
         ctx->lp_pending = true;
         ctx->lp_ntiles = ntiles;
@@ -1232,7 +1240,11 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
   dfree(ctx, incl);
   if (tstage) dfree(ctx, tstage);
   if (mapped && !ctx->mh_pending && layered) {
-    CUDAB(cudaMemcpyAsync(ctx->mh_listed_host, ctx->mh_listed_dev, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    CounterSrc cs{};
+    cs.src[0] = ctx->mh_listed_dev;
+    cs.n = 1;
+    launch_publish_counters(cs, ctx->mh_listed_hdev, s);
+    ctx->launches++;
     CUDAB(cudaEventRecord(ctx->mh_event, s));
     ctx->mh_pending = true;
     ctx->mh_pending_key = map->dm.sh;

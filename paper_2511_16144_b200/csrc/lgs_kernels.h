@@ -159,6 +159,12 @@ void launch_fast_binning(const ViewBufs& v, const uint32_t* idx_sorted, int64_t 
 // (at most gauss_cap Gaussians), then the complete lists of the tiles layer A left unsaturated.
 constexpr uint32_t kLayerMinPairs = 1u << 16;  // layer A takes at least this many pairs (or all)
 size_t layer_a_cap(int64_t pairs_cap, int ntiles, uint32_t div);
+// up to 4 device u32 counters -> mapped page-locked host memory (device address dst_mapped)
+struct CounterSrc {
+  const uint32_t* src[4];
+  int n;
+};
+void launch_publish_counters(const CounterSrc& c, uint32_t* dst_mapped, cudaStream_t s);
 // layer_flag: counts the unfinished tiles (count2), resets total2 and, inside a plan, sets the
 // conditional of the second pass; layer_prep (first kernel of that pass): summed-area table of the
 // unfinished mask and their longest-list-first order.
