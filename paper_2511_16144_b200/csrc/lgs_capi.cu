@@ -116,6 +116,10 @@ struct lgs_ctx {
   std::array<float*, 6> delta_dst{};
   int64_t delta_n = -1;
   std::vector<uint32_t> delta_rows;
+  // page-locked staging of the row records / row list read back by the delta mode (a pageable
+  // destination would route every readback through the driver's bounce buffers and the CPU)
+  void* delta_stage = nullptr;
+  size_t delta_stage_bytes = 0;
   // bytes this context moved between host and device memory by copies (lgs_ctx_transfer_bytes)
   std::atomic<int64_t> bytes_h2d{0}, bytes_d2h{0};
   cudaStream_t cond_stream = nullptr;  // captures the body of a plan's conditional node
@@ -348,6 +352,7 @@ void ctx_release(lgs_ctx* ctx) {
     if (ctx->host_u32) cudaFreeHost(ctx->host_u32);
     if (ctx->mh_listed_host) cudaFreeHost(ctx->mh_listed_host);
     if (ctx->mh_listed_dev) cudaFree(ctx->mh_listed_dev);
+    if (ctx->delta_stage) cudaFreeHost(ctx->delta_stage);
     if (ctx->mh_event) cudaEventDestroy(ctx->mh_event);
     if (ctx->lp_host) cudaFreeHost(ctx->lp_host);
     if (ctx->lp_dev) cudaFree(ctx->lp_dev);
@@ -1303,7 +1308,22 @@ namespace {
 // exact dense gradient after every call.
 
 // rows of the device gradient `src` with a nonzero component -> (index, row) records on the host
-lgs_status pack_nonzero_rows(lgs_ctx* ctx, float* const src[6], int64_t n, int K, int d, std::vector<float>* recs,
+// grows the context's page-locked staging block (1.5x headroom: a rare, synchronizing allocation)
+lgs_status delta_stage(lgs_ctx* ctx, size_t bytes, void** out) {
+  if (bytes > ctx->delta_stage_bytes) {
+    if (ctx->delta_stage) cudaFreeHost(ctx->delta_stage);
+    ctx->delta_stage = nullptr;
+    ctx->delta_stage_bytes = 0;
+    const size_t want = bytes + bytes / 2 + 4096;
+    LGS_CUDA(cudaHostAlloc(&ctx->delta_stage, want, cudaHostAllocDefault));
+    ctx->delta_stage_bytes = want;
+  }
+  *out = ctx->delta_stage;
+  return LGS_OK;
+}
+
+// (index, R values) records of the rows with any nonzero value, in the page-locked staging block
+lgs_status pack_nonzero_rows(lgs_ctx* ctx, float* const src[6], int64_t n, int K, int d, const float** recs,
                              uint32_t* rows_out) {
   cudaStream_t s = ctx->stream;
   const int width[6] = {3, 4, 3, 1, 3 * K, d};
@@ -1312,18 +1332,23 @@ lgs_status pack_nonzero_rows(lgs_ctx* ctx, float* const src[6], int64_t n, int K
   LGS_TRY(dalloc(ctx, &list, (size_t)n));
   LGS_TRY(dalloc(ctx, &cnt, 1));
   launch_rows_scan(src, width, n, list, cnt, s);
-  uint32_t rows = 0;
-  LGS_CUDA(cudaMemcpyAsync(&rows, cnt, sizeof rows, cudaMemcpyDeviceToHost, s));
+  uint32_t* hrows = ctx->host_u32 + 8;  // pinned scalar slot
+  LGS_CUDA(cudaMemcpyAsync(hrows, cnt, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
   LGS_CUDA(cudaStreamSynchronize(s));
-  ctx->bytes_d2h += (int64_t)sizeof rows;
-  recs->resize((size_t)rows * (R + 1));
+  const uint32_t rows = *hrows;
+  ctx->bytes_d2h += (int64_t)sizeof(uint32_t);
+  *recs = nullptr;
   if (rows) {
+    const size_t bytes = sizeof(float) * (size_t)rows * (R + 1);
+    void* stage = nullptr;
+    LGS_TRY(delta_stage(ctx, bytes, &stage));
     float* drec = nullptr;
     LGS_TRY(dalloc(ctx, &drec, (size_t)rows * (R + 1)));
     launch_rows_pack(src, width, n, list, cnt, rows, drec, s);
-    LGS_CUDA(cudaMemcpyAsync(recs->data(), drec, sizeof(float) * recs->size(), cudaMemcpyDeviceToHost, s));
-    ctx->bytes_d2h += (int64_t)(sizeof(float) * recs->size());
+    LGS_CUDA(cudaMemcpyAsync(stage, drec, bytes, cudaMemcpyDeviceToHost, s));
+    ctx->bytes_d2h += (int64_t)bytes;
     dfree(ctx, drec);
+    *recs = static_cast<const float*>(stage);
   }
   dfree(ctx, list);
   dfree(ctx, cnt);
@@ -1346,7 +1371,7 @@ void host_row(float* const dst[6], const int width[6], int64_t n, uint32_t i, co
 }
 
 lgs_status host_grads_delta(lgs_ctx* ctx, float* const dst[6], float* const src[6], int64_t n, int K, int d) {
-  std::vector<float> recs;
+  const float* recs = nullptr;
   uint32_t rows = 0;
   LGS_TRY(pack_nonzero_rows(ctx, src, n, K, d, &recs, &rows));
   int width[6] = {3, 4, 3, 1, 3 * K, d};
@@ -1356,7 +1381,7 @@ lgs_status host_grads_delta(lgs_ctx* ctx, float* const dst[6], float* const src[
   for (uint32_t i : ctx->delta_rows) host_row(dst, width, n, i, nullptr);  // last call's rows -> 0
   ctx->delta_rows.resize(rows);
   for (uint32_t k = 0; k < rows; ++k) {
-    const float* r = recs.data() + (size_t)k * (R + 1);
+    const float* r = recs + (size_t)k * (R + 1);
     const uint32_t i = __builtin_bit_cast(uint32_t, r[0]);
     host_row(dst, width, n, i, r + 1);
     ctx->delta_rows[k] = i;
@@ -1373,14 +1398,19 @@ lgs_status host_grads_note_rows(lgs_ctx* ctx, float* const src[6], int64_t n, in
   LGS_TRY(dalloc(ctx, &list, (size_t)n));
   LGS_TRY(dalloc(ctx, &cnt, 1));
   launch_rows_scan(src, width, n, list, cnt, s);
-  uint32_t rows = 0;
-  LGS_CUDA(cudaMemcpyAsync(&rows, cnt, sizeof rows, cudaMemcpyDeviceToHost, s));
+  uint32_t* hrows = ctx->host_u32 + 8;  // pinned scalar slot
+  LGS_CUDA(cudaMemcpyAsync(hrows, cnt, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
   LGS_CUDA(cudaStreamSynchronize(s));
-  ctx->delta_rows.resize(rows);
-  if (rows) LGS_CUDA(cudaMemcpyAsync(ctx->delta_rows.data(), list, sizeof(uint32_t) * rows, cudaMemcpyDeviceToHost, s));
+  const uint32_t rows = *hrows;
+  void* stage = nullptr;
+  if (rows) {
+    LGS_TRY(delta_stage(ctx, sizeof(uint32_t) * rows, &stage));
+    LGS_CUDA(cudaMemcpyAsync(stage, list, sizeof(uint32_t) * rows, cudaMemcpyDeviceToHost, s));
+  }
   dfree(ctx, list);
   dfree(ctx, cnt);
   LGS_CUDA(cudaStreamSynchronize(s));
+  ctx->delta_rows.assign(static_cast<const uint32_t*>(stage), static_cast<const uint32_t*>(stage) + rows);
   ctx->delta_dst = key;
   ctx->delta_n = n;
   return LGS_OK;
