@@ -65,6 +65,13 @@ __global__ void __launch_bounds__(kBlock / PPT) blend_bwd_kernel(DevMap m, DevCa
   constexpr int NT = kBlock / PPT;
   constexpr int DQ = DP > 0 ? DP / 4 : 1;
   constexpr int NB = bwd_batch<DP>();
+  // two pixels per thread, one gradient value per lane: paired FP32 (FFMA2) arithmetic, the
+  // fused kernel's backward step (blend_fused.cu) on the tape's per-pixel state
+#ifdef LGS_BWD_SCALAR
+  constexpr bool kPaired = false;
+#else
+  constexpr bool kPaired = PPT == 2 && SLOTS == 32 && DP <= 16;
+#endif
   __shared__ BwdSmem<DP> sm;
   __shared__ uint32_t s_max;
   __shared__ int s_slot;
@@ -129,7 +136,16 @@ __global__ void __launch_bounds__(kBlock / PPT) blend_bwd_kernel(DevMap m, DevCa
         g_draw[k] = g_d / mm;
         g_acc[k] = acc > 1e-6f ? -g_d * ps.depth[pix] / mm : 0.f;
       }
-      if (DP > 0) {
+      if constexpr (kPaired) {
+        // paired path: channel pairs of the thread's two pixels, (p0 c, p1 c, p0 c+1, p1 c+1) at
+        // [pair][thread] -- the pixels are the two lanes of every FFMA2 (blend_fused.cu layout)
+        float* g = reinterpret_cast<float*>(&sm.gfeat[0][0]);
+#pragma unroll
+        for (int j = 0; j < DP / 2; ++j) {
+          g[((size_t)j * NT + tid) * 4 + k] = gf[2 * j];
+          g[((size_t)j * NT + tid) * 4 + 2 + k] = gf[2 * j + 1];
+        }
+      } else if (DP > 0) {
 #pragma unroll
         for (int q = 0; q < DP / 4; ++q)
           sm.gfeat[q][lp] = make_float4(gf[q * 4], gf[q * 4 + 1], gf[q * 4 + 2], gf[q * 4 + 3]);
@@ -175,6 +191,84 @@ __global__ void __launch_bounds__(kBlock / PPT) blend_bwd_kernel(DevMap m, DevCa
         const bool col_in =
             px >= (int)(rc.x & 0xffffu) && px <= (int)(rc.x >> 16) && py0 <= ry1 && py0 + PPT - 1 >= ry0;
         if (!__any_sync(0xffffffffu, col_in)) continue;  // no pixel of this warp inside the Gaussian's rect
+        if constexpr (kPaired) {
+          const float4 r0 = sm.r0[e];
+          const float4 fa = sm.fa[e], fb = sm.fb[e];
+          const float2 ex2 = bc2(ex), ey2 = make_float2(ey[0], ey[PPT - 1]);
+          float2 S, Tt, G;
+          const float2 al = frame_alpha2(fa, fb, r0.w, ex2, ey2, S, Tt, G);
+          const bool ok0 = col_in && jrel < last[0] && py0 >= ry0 && py0 <= ry1 && al.x >= c.alpha_skip;
+          const bool ok1 = col_in && jrel < last[PPT - 1] && py0 + 1 >= ry0 && py0 + 1 <= ry1 && al.y >= c.alpha_skip;
+          if (!__any_sync(0xffffffffu, ok0 || ok1)) continue;
+          const float2 alpha = make_float2(ok0 ? al.x : 0.f, ok1 ? al.y : 0.f);
+          float vals[SLOTS];
+#pragma unroll
+          for (int q = 0; q < SLOTS; ++q) vals[q] = 0.f;
+          const float4 col = sm.col[e];
+          const float op = r0.w;
+          const float do_dlogit = op * (1.0f - op);
+          const float2 a = make_float2(fminf(alpha.x, c.alpha_clamp), fminf(alpha.y, c.alpha_clamp));
+          const float2 inv1ma = make_float2(fast_rcp(1.0f - a.x), fast_rcp(1.0f - a.y));
+          float2 Tp = make_float2(T[0], T[PPT - 1]);
+          Tp = mul2(Tp, inv1ma);  // transmittance before this contributor (unchanged when a = 0)
+          T[0] = Tp.x;
+          T[PPT - 1] = Tp.y;
+          const float2 w = mul2(a, Tp);
+          const float2 g_draw2 = make_float2(g_draw[0], g_draw[PPT - 1]);
+          const float2 g_r = make_float2(g_rgb[0][0], g_rgb[PPT - 1][0]);
+          const float2 g_g = make_float2(g_rgb[0][1], g_rgb[PPT - 1][1]);
+          const float2 g_b = make_float2(g_rgb[0][2], g_rgb[PPT - 1][2]);
+          float2 dl = fma2(g_draw2, bc2(r0.z), make_float2(g_acc[0], g_acc[PPT - 1]));
+          dl = fma2(g_r, bc2(col.x), dl);
+          dl = fma2(g_g, bc2(col.y), dl);
+          dl = fma2(g_b, bc2(col.z), dl);
+          if (DP > 0) {
+            const float4* gp = reinterpret_cast<const float4*>(&sm.gfeat[0][0]);
+#pragma unroll
+            for (int q = 0; q < DQ; ++q) {
+              const float4 fv = sm.feat[e][q];
+              const float4 g01 = gp[(size_t)(2 * q) * NT + tid];      // channels 4q, 4q+1 of both pixels
+              const float4 g23 = gp[(size_t)(2 * q + 1) * NT + tid];  // channels 4q+2, 4q+3
+              dl = fma2(make_float2(g01.x, g01.y), bc2(fv.x), dl);
+              dl = fma2(make_float2(g01.z, g01.w), bc2(fv.y), dl);
+              dl = fma2(make_float2(g23.x, g23.y), bc2(fv.z), dl);
+              dl = fma2(make_float2(g23.z, g23.w), bc2(fv.w), dl);
+              float* vf = vals + kSlotFeat + q * 4;
+              vf[0] = fmaf(g01.y, w.y, g01.x * w.x);
+              vf[1] = fmaf(g01.w, w.y, g01.z * w.x);
+              vf[2] = fmaf(g23.y, w.y, g23.x * w.x);
+              vf[3] = fmaf(g23.w, w.y, g23.z * w.x);
+            }
+          }
+          float2 acc2 = make_float2(accum[0], accum[PPT - 1]);
+          const float2 dla = fma2(make_float2(-acc2.x, -acc2.y), inv1ma, mul2(Tp, dl));
+          const float2 dl_da = make_float2((alpha.x != 0.f && !(alpha.x > c.alpha_clamp)) ? dla.x : 0.f,
+                                           (alpha.y != 0.f && !(alpha.y > c.alpha_clamp)) ? dla.y : 0.f);
+          acc2 = fma2(dl, w, acc2);
+          accum[0] = acc2.x;
+          accum[PPT - 1] = acc2.y;
+          vals[kSlotColor + 0] = fmaf(g_r.y, w.y, g_r.x * w.x);
+          vals[kSlotColor + 1] = fmaf(g_g.y, w.y, g_g.x * w.x);
+          vals[kSlotColor + 2] = fmaf(g_b.y, w.y, g_b.x * w.x);
+          vals[kSlotZ] = fmaf(g_draw2.y, w.y, g_draw2.x * w.x);
+          const float2 dlg = mul2(dl_da, G);
+          vals[kSlotOpac] = (dlg.x + dlg.y) * do_dlogit;
+          const float2 cf = mul2(mul2(dl_da, bc2(op)), mul2(bc2(-0.5f), G));  // dl_dg * dg_dq
+          const float2 dqx = mul2(bc2(kTwoOverHalfLog2e), fma2(S, bc2(fa.z), mul2(Tt, bc2(fb.x))));
+          const float2 dqy = mul2(bc2(kTwoOverHalfLog2e), fma2(S, bc2(fa.w), mul2(Tt, bc2(fb.y))));
+          const float2 dx = add2(bc2(fb.z), ex2), dy = add2(bc2(fb.w), ey2);
+          const float2 mx = mul2(cf, dqx), my = mul2(cf, dqy);
+          vals[kSlotMuX] = -(mx.x + mx.y);
+          vals[kSlotMuY] = -(my.x + my.y);
+          const float2 cdx = mul2(cf, dx), cdy = mul2(cf, dy);
+          const float2 ca = mul2(cdx, dx), cb2_ = mul2(cdx, dy), cc = mul2(cdy, dy);
+          vals[kSlotConA] = ca.x + ca.y;
+          vals[kSlotConB] = cb2_.x + cb2_.y;
+          vals[kSlotConC] = cc.x + cc.y;
+          warp_transpose_reduce<SLOTS>(vals, lane);
+          gacc_add(gacc + (size_t)sm.gid[e] * SLOTS, lane, vals[0]);
+          continue;
+        }
         // phase 1: alphas of this thread's pixels (cheap); most rect hits fail the alpha test
         const float4 r0 = sm.r0[e];
         const float4 fa = sm.fa[e], fb = sm.fb[e];
