@@ -500,6 +500,61 @@ __global__ void __launch_bounds__(kListWarps * 32) layer_tile_lists_kernel(
   }
 }
 
+// Tiles longest layer-A list first (exact lengths, >= 1023 in one bin; arbitrary order inside a bin:
+// which CTA takes which tile is racy anyway and no result depends on it).  One CTA counting sort.
+__global__ void __launch_bounds__(1024) tile_order_lpt_kernel(const uint2* __restrict__ ranges, int ntiles,
+                                                              uint32_t* __restrict__ order) {
+  __shared__ uint32_t s_bin[1024];
+  __shared__ uint32_t s_w[32];
+  const int t0 = threadIdx.x, lane = t0 & 31, warp = t0 >> 5;
+  s_bin[t0] = 0;
+  __syncthreads();
+  for (int t = t0; t < ntiles; t += blockDim.x) {
+    const uint2 r = ranges[t];
+    atomicAdd(&s_bin[1023 - min(r.y - r.x, 1023u)], 1u);  // bin 0 = longest
+  }
+  __syncthreads();
+  const uint32_t v = s_bin[t0];
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_w[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t w = s_w[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    s_w[lane] = w;
+  }
+  __syncthreads();
+  s_bin[t0] = x - v + (warp ? s_w[warp - 1] : 0u);
+  __syncthreads();
+  for (int t = t0; t < ntiles; t += blockDim.x) {
+    const uint2 r = ranges[t];
+    order[atomicAdd(&s_bin[1023 - min(r.y - r.x, 1023u)], 1u)] = (uint32_t)t;
+  }
+}
+
+void launch_tile_order_lpt(const uint2* ranges, int ntiles, uint32_t* order, cudaStream_t s) {
+  tile_order_lpt_kernel<<<1, 1024, 0, s>>>(ranges, ntiles, order);
+}
+
+__global__ void __launch_bounds__(1024) copy_u32_kernel(const uint32_t* __restrict__ src, int n,
+                                                        uint32_t* __restrict__ dst) {
+  griddep_wait();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+}
+
+void launch_copy_u32(const uint32_t* src, int n, uint32_t* dst, cudaStream_t s) {
+  launch_pdl(copy_u32_kernel, dim3(1), dim3(1024), 0, s, src, n, dst);
+}
+
 void launch_layer_tile_lists(const uint2* cand_rect, const uint32_t* cand_idx, const uint32_t* n_cand, int tiles_x,
                              int ntiles, uint32_t* cursor, uint32_t* vals, uint2* ranges, int* blend_counter,
                              double* loss, cudaStream_t s) {

@@ -128,6 +128,13 @@ struct lgs_ctx {
   // on a side branch forked after the preprocess and joined before the backward's chain kernel
   const lgs_map_grads* prezero = nullptr;
   bool prezero_forked = false;
+  // lgs_plan capture: the plan's longest-list-first tile orders.  A replay's first-pass blend takes
+  // tiles in the order computed from the previous replay's lists (cap_lpt_cur; identity before the
+  // first), while the side branch computes this replay's into cap_lpt_next, copied to cur after the
+  // join -- the ordering costs nothing on the critical path (the view is fixed between replays).
+  uint32_t* cap_lpt_cur = nullptr;
+  uint32_t* cap_lpt_next = nullptr;
+  bool lpt_forked = false;
   cudaStream_t side_stream = nullptr;
   cudaEvent_t side_fork = nullptr, side_join = nullptr;
   // multi-view gradient all-reduce (lgs_comm_*): one NCCL communicator per context / GPU
@@ -942,10 +949,21 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
   // backward's chain then writes only the active rows).  Forked right before the first blend,
   // which is issue-bound and leaves HBM to the stores (forking after K1 instead, beside the
   // latency-bound depth order, measured 10-15 us slower per replay).
+  // longest-list-first first pass (plans only): few tiles per CTA slot of the blend (~2 at the
+  // headline) leave the longest tiles' CTAs running alone at the end in natural order; with many
+  // per slot the natural order balances as well and keeps neighbours together
+  // (profiles/r2_ab_lpt.log)
+  const bool lpt = ctx->capturing && ctx->cap_lpt_cur && ctx->prezero && ntiles < 12 * device_sm_count();
   auto fork_prezero = [&]() -> lgs_status {
     if (!(layered && ctx->capturing && ctx->prezero && !ctx->prezero_forked && n > 0)) return LGS_OK;
     LGS_CUDA(cudaEventRecord(ctx->side_fork, s));
     LGS_CUDA(cudaStreamWaitEvent(ctx->side_stream, ctx->side_fork, 0));
+    if (lpt) {  // this replay's order, for the next replay (copied after the join); first on the
+                // branch, so its one CTA is resident before the blend fills the SMs
+      launch_tile_order_lpt(t->ranges, ntiles, ctx->cap_lpt_next, ctx->side_stream);
+      ctx->lpt_forked = true;
+      ctx->launches++;
+    }
     {
       PhaseScope ph(ctx, PH_GRAD_ZERO, ctx->side_stream);
       launch_grad_zero(device_grad_out(ctx->prezero, map->dm.d), n, map->dm.K, map->dm.dp > 0 ? map->dm.d : 0,
@@ -1095,8 +1113,8 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
       {
         PhaseScope ph(ctx, PH_BLEND_FWD);
         if (fuse)
-          launch_blend_fused_l1(dm, dc, t->vb, TileLists{t->vals, t->ranges, nullptr, t->counter}, fo1, t->gacc, s,
-                                true, ntiles < 2 * device_sm_count());  // few tiles: latency-bound variant
+          launch_blend_fused_l1(dm, dc, t->vb, TileLists{t->vals, t->ranges, lpt ? ctx->cap_lpt_cur : nullptr, t->counter},
+                                fo1, t->gacc, s, true, ntiles < 2 * device_sm_count());  // few tiles: latency-bound variant
         else
           launch_blend_fwd(dm, dc, t->vb, TileLists{t->vals, t->ranges, nullptr, t->counter}, t->ps, fo1, s);
       }
@@ -1474,6 +1492,11 @@ lgs_status run_backward(lgs_ctx* ctx, const lgs_saved* t, const BwdIn& in_dev, l
   if (ctx->prezero_forked) {
     LGS_CUDA(cudaStreamWaitEvent(s, ctx->side_join, 0));
     ctx->prezero_forked = false;
+    if (ctx->lpt_forked) {  // the next replay's tile order
+      launch_copy_u32(ctx->cap_lpt_next, t->ntiles, ctx->cap_lpt_cur, s);
+      ctx->launches++;
+      ctx->lpt_forked = false;
+    }
   }
   if (t->vb.active && !zeroed) {  // sparse chain below: the zero rows first (none when accumulating)
     PhaseScope ph(ctx, PH_GRAD_ZERO);
@@ -2879,6 +2902,8 @@ struct lgs_plan {
   int64_t recaptures = 0;
   uint32_t* host_pairs = nullptr;  // pinned: this plan's pair count, written by every replay (each
                                    // plan its own slot: several plans may share a context)
+  uint32_t* lpt[2] = {nullptr, nullptr};  // tile orders: [0] used by a replay, [1] computed by it
+  int lpt_n = 0;
 };
 
 namespace {
@@ -2908,11 +2933,28 @@ lgs_status plan_capture(lgs_plan* p) {
     LGS_CUDA(cudaEventCreateWithFlags(&ctx->side_fork, cudaEventDisableTiming));
     LGS_CUDA(cudaEventCreateWithFlags(&ctx->side_join, cudaEventDisableTiming));
   }
+  {  // the plan's tile-order buffers (identity before the first replay)
+    const int nt = ((p->cam.width + LGS_TILE - 1) / LGS_TILE) * ((p->cam.height + LGS_TILE - 1) / LGS_TILE);
+    if (nt != p->lpt_n) {
+      for (auto& b : p->lpt)
+        if (b) cudaFree(b), b = nullptr;
+      std::vector<uint32_t> id((size_t)nt);
+      for (int i = 0; i < nt; ++i) id[(size_t)i] = (uint32_t)i;
+      for (auto& b : p->lpt) {
+        LGS_CUDA(cudaMalloc(reinterpret_cast<void**>(&b), sizeof(uint32_t) * (size_t)std::max(nt, 1)));
+        LGS_CUDA(cudaMemcpy(b, id.data(), sizeof(uint32_t) * (size_t)nt, cudaMemcpyHostToDevice));
+      }
+      p->lpt_n = nt;
+    }
+  }
   LGS_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
   ctx->stream = s;
   ctx->capturing = true;
   ctx->prezero = (p->grads.memory != LGS_MEM_HOST && !p->grads.accumulate) ? &p->grads : nullptr;
   ctx->prezero_forked = false;
+  ctx->cap_lpt_cur = p->lpt[0];
+  ctx->cap_lpt_next = p->lpt[1];
+  ctx->lpt_forked = false;
   plan_free_marks(p);
   ctx->capture_marks = p->profile ? &p->marks : nullptr;  // event nodes cost ~5 us each per replay
   uint32_t* const saved_host = ctx->host_u32;
@@ -2936,6 +2978,8 @@ lgs_status plan_capture(lgs_plan* p) {
     cudaStreamWaitEvent(s, ctx->side_join, 0);
     ctx->prezero_forked = false;
   }
+  ctx->lpt_forked = false;
+  ctx->cap_lpt_cur = ctx->cap_lpt_next = nullptr;
   ctx->prezero = nullptr;
   ctx->capturing = false;
   ctx->capture_marks = nullptr;
@@ -2992,6 +3036,8 @@ LGS_API lgs_status lgs_plan_create(lgs_ctx* ctx, lgs_map* map, const lgs_camera*
     if (p->ev1) cudaEventDestroy(p->ev1);
     if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
     if (p->host_pairs) cudaFreeHost(p->host_pairs);
+    for (auto& b : p->lpt)
+      if (b) cudaFree(b);
     ctx_release(ctx);
     delete p;
     return st;
@@ -3089,6 +3135,8 @@ LGS_API lgs_status lgs_plan_destroy(lgs_plan* p) {
   if (p->ev1) cudaEventDestroy(p->ev1);
   if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
   if (p->host_pairs) cudaFreeHost(p->host_pairs);
+  for (auto& b : p->lpt)
+    if (b) cudaFree(b);
   delete p;
   ctx_release(ctx);
   return LGS_OK;
