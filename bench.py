@@ -51,6 +51,8 @@ def parse():
     p.add_argument("--no-mapping", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-pruning", action="store_true")
+    p.add_argument("--rng", choices=["pcg64", "reference"], default="pcg64",
+                   help="scene generator: numpy PCG64, or the reference's lego::Rng stream (scenes.RefRng)")
     p.add_argument("--e2e-steps", type=int, default=30)
     p.add_argument("--e2e-threads", type=int, default=3)
     p.add_argument("--sampler", choices=["nvml", "smi", "none"], default="nvml", help=argparse.SUPPRESS)
@@ -261,7 +263,7 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     _lib.load()  # fails loudly without the CUDA library: there is no fallback
 
-    scene, cams, info = scenes.make_config(args.config)
+    scene, cams, info = scenes.make_config(args.config, rng=args.rng)
     view = default_view(args.config) if args.view is None else args.view
     cam = rank_camera(cams[view], rank, world)
     d = scene["feat"].shape[0]
@@ -461,7 +463,7 @@ def run_ours(args):
         "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": round(ms_max, 4), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": f"synthetic (seeded; BASELINE {data}; no dataset ships with the reference)",
+        "data": f"synthetic (seeded, {args.rng} generator; BASELINE {data}; no dataset ships with the reference)",
         "config": {"workload": args.config, "view": view, "image": f"{cam['width']}x{cam['height']}", "gaussians": n,
                    "sh_degree": int(math.isqrt(K) - 1), "feature_dim": d, "views_per_gpu_per_step": 1,
                    "loss": "L1 rgb+depth+feat (fused)", "pose_grad": True,
@@ -599,7 +601,7 @@ def run_multiview(args, name, local, world, rank, flush):
     from paper_2511_16144_b200 import renderer as R
     from paper_2511_16144_b200 import scenes
 
-    scene, cams, info = scenes.make_config(name)
+    scene, cams, info = scenes.make_config(name, rng=args.rng)
     n, d, K = scene["pos"].shape[0], scene["feat"].shape[0], scene["sh"].shape[1]
     stream = torch.cuda.Stream(device=local)
     ctx = R.Context(local, stream=stream.cuda_stream)
@@ -883,7 +885,7 @@ def run_reference(args):
     if rank != 0:
         return
     from paper_2511_16144_b200 import scenes
-    scene, cams, info = scenes.make_config(args.config)
+    scene, cams, info = scenes.make_config(args.config, rng=args.rng)
     view = default_view(args.config) if args.view is None else args.view
     cam = cams[view]
     d = scene["feat"].shape[0]

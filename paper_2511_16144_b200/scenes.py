@@ -26,6 +26,111 @@ import numpy as np
 CONFIG_NAMES = ("c0", "c1", "c1_500k", "c2", "c3", "c4")
 
 
+class RefRng:
+    """The reference's lego::Rng (proj/include/legoslam/random.hpp:12-50) as a numpy generator with
+    the subset of the numpy Generator API the configs use, so a scene can be drawn from the
+    reference's own stream (``make_config(..., rng="reference")``): std::mt19937_64 (vectorized
+    twist, standard seeding and tempering), uniform() = (u64 >> 11) * 2^-53, uniform(lo, hi) =
+    lo + (hi - lo) uniform(), uniform_int(n) = int(uniform() n), normal() = Box-Muller with the
+    cached second value.  Draw order: every call consumes the stream in C order of its output;
+    normal(mu, sigma) = mu + sigma * normal() (the reference has only the standard normal).
+    Bit-identical to the C restatement in oracle/lgs_oracle.c (tests/test_scenes_rng.py), which is
+    pinned to the C++ standard's known mt19937_64 value."""
+
+    _N, _M = 312, 156
+    _MAG = np.uint64(0xB5026F5AA96619E9)
+    _UP, _LO = np.uint64(0xFFFFFFFF80000000), np.uint64(0x7FFFFFFF)
+
+    def __init__(self, seed: int):
+        mt = [int(seed) & 0xFFFFFFFFFFFFFFFF]
+        for i in range(1, self._N):
+            prev = mt[-1]
+            mt.append((6364136223846793005 * (prev ^ (prev >> 62)) + i) & 0xFFFFFFFFFFFFFFFF)
+        self._mt = np.array(mt, dtype=np.uint64)
+        self._buf = np.zeros(0, np.uint64)
+        self._spare = None
+
+    def _twist(self):
+        mt, N, M = self._mt, self._N, self._M
+        one = np.uint64(1)
+        x = (mt[:N - M] & self._UP) | (mt[1:N - M + 1] & self._LO)
+        mt[:N - M] = mt[M:] ^ (x >> one) ^ np.where((x & one) != 0, self._MAG, np.uint64(0))
+        x = (mt[N - M:N - 1] & self._UP) | (mt[N - M + 1:N] & self._LO)
+        mt[N - M:N - 1] = mt[:M - 1] ^ (x >> one) ^ np.where((x & one) != 0, self._MAG, np.uint64(0))
+        x = (mt[N - 1] & self._UP) | (mt[0] & self._LO)
+        mt[N - 1] = mt[M - 1] ^ (x >> one) ^ (self._MAG if int(x) & 1 else np.uint64(0))
+        y = mt.copy()
+        y ^= (y >> np.uint64(29)) & np.uint64(0x5555555555555555)
+        y ^= (y << np.uint64(17)) & np.uint64(0x71D67FFFEDA60000)
+        y ^= (y << np.uint64(37)) & np.uint64(0xFFF7EEE000000000)
+        y ^= y >> np.uint64(43)
+        return y
+
+    def next_u64(self, k: int) -> np.ndarray:
+        out = [self._buf]
+        have = self._buf.size
+        while have < k:
+            blk = self._twist()
+            out.append(blk)
+            have += blk.size
+        allv = np.concatenate(out) if len(out) > 1 else out[0]
+        self._buf = allv[k:]
+        return allv[:k]
+
+    def _unit(self, k: int) -> np.ndarray:  # random.hpp:20-22
+        return (self.next_u64(k) >> np.uint64(11)).astype(np.float64) * (2.0 ** -53)
+
+    def uniform(self, lo=0.0, hi=1.0, size=None):
+        shape = () if size is None else size
+        k = int(np.prod(shape))
+        v = lo + (hi - lo) * self._unit(k)
+        return v.reshape(shape) if size is not None else float(v[0])
+
+    def integers(self, lo, hi, size=None):  # uniform_int(hi - lo) + lo, random.hpp:27-29
+        shape = () if size is None else size
+        k = int(np.prod(shape))
+        v = (self._unit(k) * float(hi - lo)).astype(np.int64) + lo
+        return v.reshape(shape)
+
+    def _normal(self, k: int) -> np.ndarray:  # random.hpp:31-44, the spare kept across calls
+        out = np.empty(k, np.float64)
+        i = 0
+        if k and self._spare is not None:
+            out[0] = self._spare
+            self._spare = None
+            i = 1
+        need = k - i
+        pairs = (need + 1) // 2
+        if pairs:
+            u = self._unit(2 * pairs).reshape(pairs, 2)
+            if np.any(u[:, 0] <= 0.0):  # the reference redraws u1 until positive (p = 2^-53): exact slow path
+                vals = []
+                for a, b in u:
+                    while a <= 0.0:
+                        a = self._unit(1)[0]
+                    r = np.sqrt(-2.0 * np.log(a))
+                    vals += [r * np.cos(2.0 * np.pi * b), r * np.sin(2.0 * np.pi * b)]
+                z = np.array(vals)
+            else:
+                r = np.sqrt(-2.0 * np.log(u[:, 0]))
+                th = 2.0 * np.pi * u[:, 1]
+                z = np.stack([r * np.cos(th), r * np.sin(th)], 1).reshape(-1)
+            out[i:] = z[:need]
+            if z.size > need:
+                self._spare = float(z[need])
+        return out
+
+    def standard_normal(self, size=None):
+        shape = () if size is None else size
+        v = self._normal(int(np.prod(shape)))
+        return v.reshape(shape) if size is not None else float(v[0])
+
+    def normal(self, mu=0.0, sigma=1.0, size=None):
+        shape = () if size is None else size
+        v = mu + sigma * self._normal(int(np.prod(shape)))
+        return v.reshape(shape) if size is not None else float(v[0])
+
+
 def _f32(a):
     return np.ascontiguousarray(np.asarray(a, dtype=np.float64).astype(np.float32))
 
@@ -92,7 +197,7 @@ def _sh(rng, n, deg, dc=None):
     return sh
 
 
-def make_config(name: str, n: int | None = None, d: int = 16):
+def make_config(name: str, n: int | None = None, d: int = 16, rng: str = "pcg64"):
     """Returns (scene, [cameras], info) for a BASELINE.json config.
 
     c0      : configs[0]  160x120, 10k, SH0, identity pose.
@@ -101,10 +206,16 @@ def make_config(name: str, n: int | None = None, d: int = 16):
     c2      : configs[2]  1200x680, 1M, 200 blobs, SH3.
     c3      : configs[3]  500k (config-1 distributions), 8 views on a 1 m circle.
     c4      : configs[4]  3M, 70% in a 0.5 m sphere, 16 views on a 2 m arc.
+    rng     : "pcg64" (numpy, the default of every test and bench line) or "reference" (the same
+              draws from the reference's lego::Rng stream, RefRng: reproducible by a C++ program
+              calling the reference's generator in the same order).
     """
     cid = {"c0": 0, "c1": 1, "c1_500k": 1, "c2": 2, "c3": 3, "c4": 4}[name]
-    rng = np.random.Generator(np.random.PCG64(1000 + cid))
-    info = dict(config=name, seed=1000 + cid)
+    if rng not in ("pcg64", "reference"):
+        raise ValueError(rng)
+    info = dict(config=name, seed=1000 + cid, rng=rng)
+    # rng="reference": the same draws from the reference's own lego::Rng stream (RefRng)
+    rng = RefRng(1000 + cid) if rng == "reference" else np.random.Generator(np.random.PCG64(1000 + cid))
     if name == "c0":
         n = n or 10_000
         pos = np.stack([rng.uniform(-1, 1, n), rng.uniform(-1, 1, n), rng.uniform(2, 5, n)], 1)
