@@ -863,7 +863,14 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
   // depth-layered binning (binning_fast.cu, depth_order.cu): K1 fills the depth-bucket histogram,
   // the depth order of layer A is built with the binning below, the complete order only when some
   // tile needs the second pass
-  const bool layered = fast && !ctx->full_lists && n > 0 && !cub_depth;
+  // (a view whose pairs all fit a few layer-A minimums -- configs[0]: 43k -- gains nothing from the
+  // layering: its layer A would take nearly every pair and its second pass most tiles; it is binned
+  // in one pass, decided from the context's pair capacity, i.e. the earlier renders)
+#ifndef LGS_SMALL_PAIRS
+#define LGS_SMALL_PAIRS (4 * (int64_t)kLayerMinPairs)
+#endif
+  const bool small_view = ctx->pairs_cap > 0 && ctx->pairs_cap < LGS_SMALL_PAIRS;
+  const bool layered = fast && !ctx->full_lists && n > 0 && !cub_depth && !small_view;
   if (layered && !ctx->capturing) layer_policy_update(ctx, ntiles);
   void* otemp = nullptr;
   const size_t otemp_bytes = cub_depth ? 0 : depth_order_temp_bytes(n);
@@ -1224,9 +1231,23 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
     }
     ctx->launches++;
     if (targets) LGS_CUDA(cudaMemsetAsync(t->loss, 0, sizeof(double), s));
+    // complete lists with the fused L1 step (a small view binned in one pass): the fused kernel,
+    // with every visible Gaussian's accumulator row zeroed (any may be listed)
+    const bool fuse_all = (ctx->capturing || ctx->fused_eager) && targets && blend_fused_supported(dp) &&
+                          slots_for(dp) == 32 && n > 0;
+    if (fuse_all) {
+      dfree(ctx, t->gacc);
+      LGS_TRY(dalloc(ctx, &t->gacc, (size_t)n * 32));
+      LGS_CUDA(cudaMemsetAsync(t->gacc, 0, sizeof(float) * (size_t)n * 32, s));
+      t->bwd_fused = true;
+    }
     {
       PhaseScope ph(ctx, PH_BLEND_FWD);
-      launch_blend_fwd(dm, dc, t->vb, TileLists{t->vals, t->ranges, t->order, t->counter}, t->ps, fo, s);
+      if (fuse_all)
+        launch_blend_fused_l1(dm, dc, t->vb, TileLists{t->vals, t->ranges, t->order, t->counter}, fo, t->gacc, s,
+                              false, ntiles < 2 * device_sm_count());
+      else
+        launch_blend_fwd(dm, dc, t->vb, TileLists{t->vals, t->ranges, t->order, t->counter}, t->ps, fo, s);
     }
     ctx->launches++;
     LGS_CUDA(cudaGetLastError());

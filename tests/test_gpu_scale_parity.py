@@ -3,7 +3,9 @@
 The step bench.py times is a captured plan (lgs_plan: preprocess -> depth-layered binning -> the
 fused forward+backward blend kernel with the L1 loss -> preprocess backward -> pose gradient).  Here
 that exact step runs at the headline config (c1_500k: 640x480, 500k Gaussians, SH3, d=16), at
-configs[1] (c1: 200k) and at configs[2] (c2: 1200x680, 1M), and is compared with oracle A -- the
+configs[1] (c1: 200k), at configs[2] (c2: 1200x680, 1M) and at configs[0] (c0: 160x120, 10k -- a
+small view binned in one pass with complete lists, the fused kernel on every tile), and is
+compared with oracle A -- the
 fp64 restatement of renderer.cpp:94-356 -- run on the same fp32 projected records (oracle B,
 bit-exact with the GPU's; test_gpu_parity.py) and fed the cotangents the kernel computed from its
 own images (so an L1 sign at |render - target| ~ 0 cannot masquerade as a gradient error):
@@ -61,7 +63,7 @@ def run_bench_step(name, target_seed=7):
     return scene, cam, tg, out, g
 
 
-@pytest.mark.parametrize("name", ["c1_500k", "c1", "c2"])
+@pytest.mark.parametrize("name", ["c1_500k", "c1", "c2", "c0"])
 def test_benched_plan_matches_oracle_at_scale(oracle, name):
     scene, cam, tg, out, g = run_bench_step(name)
     for k in GROUPS:
