@@ -81,6 +81,7 @@ GradOut device_grad_out(const lgs_map_grads* g, int d) {
 // layer A of the depth-layered binning owns ~1/kLayerDiv of the pairs (binning_fast.cu)
 // (the starting value: lgs_ctx::layer_div adapts it per context)
 constexpr uint32_t kLayerDiv = 16;
+constexpr int64_t kSinglePassPairs = 16 << 20;  // complete lists in one pass at most this many pairs
 
 int bits_for(int ntiles) {
   int b = 0;
@@ -174,6 +175,15 @@ struct lgs_ctx {
   // of its list, it shrinks 4x (a dense view whose near splats cover most tiles).  Plans capture
   // with the size their warm-up renders settle on.
   uint32_t layer_div = kLayerDiv;
+  // when more than 1/20 of the tiles needed the second pass and the view has at most 16M pairs,
+  // one pass over complete lists is cheaper than two (configs[1]: +21%).  Kept for maps of the same
+  // size and the same image size while the pair capacity stays within 2x of the one it was taken
+  // at (then the counters of a layered render decide again).
+  bool single_pass = false;
+  int64_t sp_cap = 0;
+  uint64_t sp_map = 0;
+  int sp_ntiles = 0;
+  uint64_t lp_map = 0;  // the map size the pending layer counters were taken on
   uint32_t layer_bad = UINT32_MAX;  // a div at which too many tiles were left unsaturated
   uint32_t* lp_dev = nullptr;       // [0] consumed (the host copy: + [1] layer-A listed pairs, [2] unfinished tiles)
   uint32_t* lp_host = nullptr;      // mapped pinned copy (written by launch_publish_counters)
@@ -788,6 +798,12 @@ void layer_policy_update(lgs_ctx* ctx, int ntiles) {
   if (ctx->lp_ntiles != ntiles || ctx->lp_div != ctx->layer_div) return;  // counts of another image / size
   const uint64_t consumed = ctx->lp_host[0], listed = ctx->lp_host[1], unfinished = ctx->lp_host[2];
   uint32_t& div = ctx->layer_div;
+  if (unfinished * 20 > (uint64_t)ntiles && ctx->pairs_cap < kSinglePassPairs) {
+    ctx->single_pass = true;
+    ctx->sp_cap = ctx->pairs_cap;
+    ctx->sp_map = ctx->lp_map;
+    ctx->sp_ntiles = ntiles;
+  }
   if (unfinished * 4 > (uint64_t)ntiles) {
     ctx->layer_bad = std::min(ctx->layer_bad, div);
     div = std::max<uint32_t>(4, div / 2);
@@ -863,13 +879,15 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
   // depth-layered binning (binning_fast.cu, depth_order.cu): K1 fills the depth-bucket histogram,
   // the depth order of layer A is built with the binning below, the complete order only when some
   // tile needs the second pass
-  // (a view whose pairs all fit a few layer-A minimums -- configs[0]: 43k -- gains nothing from the
-  // layering: its layer A would take nearly every pair and its second pass most tiles; it is binned
-  // in one pass, decided from the context's pair capacity, i.e. the earlier renders)
-#ifndef LGS_SMALL_PAIRS
-#define LGS_SMALL_PAIRS (4 * (int64_t)kLayerMinPairs)
-#endif
-  const bool small_view = ctx->pairs_cap > 0 && ctx->pairs_cap < LGS_SMALL_PAIRS;
+  // One pass over complete lists instead of the layering, decided from the earlier renders: a view
+  // whose pairs all fit a few layer-A minimums (configs[0]: 43k; layer A would take nearly every
+  // pair and the second pass most tiles), or a context whose layered renders left more than 1/20 of
+  // the tiles to the second pass at up to 16M pairs (lgs_ctx::single_pass; configs[1]).
+  if (ctx->single_pass && (ctx->sp_map != (uint64_t)map->dm.n || ctx->sp_ntiles != ntiles ||
+                           ctx->pairs_cap > 2 * ctx->sp_cap || ctx->pairs_cap >= kSinglePassPairs))
+    ctx->single_pass = false;  // another view: layered renders decide again
+  const bool small_view =
+      ctx->pairs_cap > 0 && (ctx->pairs_cap < 4 * (int64_t)kLayerMinPairs || ctx->single_pass);
   const bool layered = fast && !ctx->full_lists && n > 0 && !cub_depth && !small_view;
   if (layered && !ctx->capturing) layer_policy_update(ctx, ntiles);
   void* otemp = nullptr;
@@ -1148,6 +1166,7 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
         ctx->lp_pending = true;
         ctx->lp_ntiles = ntiles;
         ctx->lp_div = ldiv;
+        ctx->lp_map = (uint64_t)map->dm.n;
       }
       if (use_cond) LGS_TRY(cond_begin(ctx, cond));
       lgs_status st2 = LGS_OK;
