@@ -397,7 +397,12 @@ cudaError_t run_language_redundant(const PruneIn& in, const PruneParams& pp, uin
     int par = 0;
     uint32_t left = host_cand;
     constexpr int kBatch = 8;  // rounds between host checks (an idle round costs two empty launches)
+    int64_t issued = 0;
     while (left) {
+      // every round resolves at least the smallest unresolved candidate: more rounds than
+      // candidates would be a bug, not a slow map -- fail instead of spinning
+      if (issued > (int64_t)host_cand + kBatch) return cudaErrorUnknown;
+      issued += kBatch;
       for (int b = 0; b < kBatch; ++b) {
         cudaMemsetAsync(c.small + (par ^ 1) * 2, 0, 8, s);
         round_u_kernel<<<grid, 256, 0, s>>>(r, in.pos_opa, par);
