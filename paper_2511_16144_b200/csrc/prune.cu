@@ -10,6 +10,8 @@
 //   * a spatial hash (cells of edge tau_dist, 27-cell ball queries) replaces the KD-tree;
 //   * "candidates": Gaussians with a similar neighbour inside tau_dist.  The others are never
 //     killed and kill nothing (similarity is symmetric); they only occupy neighbour slots.
+//   * the candidates' tau-balls are listed once (CSR: neighbour | similar bit, squared distance),
+//     so the rounds read lists instead of repeating the hash queries and cosines;
 //   * each round, phase 1 computes U(x) for every candidate x = the smallest UNRESOLVED
 //     Gaussian that could kill x (a similar neighbour within tau_dist); phase 2 resolves candidate
 //     i when (a) it was already killed by an earlier Gaussian (death[i] < i), or (b) U(i) >= i and
@@ -169,10 +171,52 @@ __global__ void candidates_kernel(Grid g, Feats F, int64_t n, double tau2, doubl
   }
 }
 
+// Neighbour lists of the candidates (CSR over their list positions): every other Gaussian inside
+// tau_dist, as (index | similar << 31) and its squared distance.  Built once: the rounds then read
+// them instead of repeating the ball queries and the cosines every round.
+__global__ void nb_count_kernel(Grid g, const uint32_t* __restrict__ list, const uint32_t* __restrict__ ncand,
+                                const float4* __restrict__ po, double tau2, uint32_t* __restrict__ cnt) {
+  const uint32_t nc = *ncand;
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < nc; k += gridDim.x * blockDim.x) {
+    const uint32_t i = list[k];
+    const float4 p = po[i];
+    const int cx = cell_coord(p.x, g.inv_h), cy = cell_coord(p.y, g.inv_h), cz = cell_coord(p.z, g.inv_h);
+    uint32_t c = 0;
+    for_ball<1>(g, cx, cy, cz, [&](uint32_t s) {
+      const float4 q = g.pos[s];
+      if (__float_as_uint(q.w) != i && dist2(p, q) < tau2) ++c;
+      return true;
+    });
+    cnt[k] = c;
+  }
+}
+
+__global__ void nb_fill_kernel(Grid g, Feats F, const uint32_t* __restrict__ list, const uint32_t* __restrict__ ncand,
+                               const float4* __restrict__ po, double tau2, double tau_sim,
+                               const uint32_t* __restrict__ off, uint32_t* __restrict__ nb, double* __restrict__ nbd2,
+                               uint32_t* __restrict__ pos_of) {
+  const uint32_t nc = *ncand;
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < nc; k += gridDim.x * blockDim.x) {
+    const uint32_t i = list[k];
+    pos_of[i] = k;
+    const float4 p = po[i];
+    const int cx = cell_coord(p.x, g.inv_h), cy = cell_coord(p.y, g.inv_h), cz = cell_coord(p.z, g.inv_h);
+    uint32_t w = off[k];
+    for_ball<1>(g, cx, cy, cz, [&](uint32_t s) {
+      const float4 q = g.pos[s];
+      const uint32_t j = __float_as_uint(q.w);
+      if (j == i) return true;
+      const double d2 = dist2(p, q);
+      if (!(d2 < tau2)) return true;
+      nb[w] = j | (similar(F, i, j, tau_sim) ? 0x80000000u : 0u);
+      nbd2[w] = d2;
+      ++w;
+      return true;
+    });
+  }
+}
+
 struct Rounds {
-  Grid g;
-  Feats F;
-  double tau2, tau_sim;
   int K;
   const uint8_t* cand;
   uint8_t* res;      // resolved
@@ -182,33 +226,35 @@ struct Rounds {
   uint32_t* list1[2];
   uint32_t* list2[2];
   uint32_t* rounds;  // rounds that found work
+  const uint32_t* pos_of;  // map index -> candidate list position (CSR row)
+  const uint32_t* off;     // CSR offsets
+  const uint32_t* nb;      // neighbour | similar << 31
+  const double* nbd2;      // squared distance
 };
 
 // phase 1: U(x) for the listed candidates; a candidate whose potential killers are all resolved
 // stays settled (U = UINT_MAX) and leaves the list
-__global__ void round_u_kernel(Rounds r, const float4* __restrict__ po, int par) {
+__global__ void round_u_kernel(Rounds r, int par) {
   const uint32_t cnt = r.counts[par * 2 + 0];
   const uint32_t* in = r.list1[par];
   uint32_t* out = r.list1[par ^ 1];
   uint32_t* out_cnt = r.counts + (par ^ 1) * 2 + 0;
   for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < cnt; t += gridDim.x * blockDim.x) {
     const uint32_t x = in[t];
-    const float4 p = po[x];
-    const int cx = cell_coord(p.x, r.g.inv_h), cy = cell_coord(p.y, r.g.inv_h), cz = cell_coord(p.z, r.g.inv_h);
+    const uint32_t k = r.pos_of[x];
     uint32_t u = UINT_MAX;
-    for_ball<1>(r.g, cx, cy, cz, [&](uint32_t s) {
-      const float4 q = r.g.pos[s];
-      const uint32_t j = __float_as_uint(q.w);
-      if (j != x && j < u && !r.res[j] && dist2(p, q) < r.tau2 && similar(r.F, x, j, r.tau_sim)) u = j;
-      return true;
-    });
+    for (uint32_t e = r.off[k], e1 = r.off[k + 1]; e < e1; ++e) {
+      const uint32_t v = r.nb[e];
+      const uint32_t j = v & 0x7fffffffu;
+      if ((v >> 31) && j < u && !r.res[j]) u = j;
+    }
     r.U[x] = u;
     if (u != UINT_MAX) out[atomicAdd(out_cnt, 1u)] = x;
   }
 }
 
 // phase 2: resolve the candidates nothing undecided can still influence
-__global__ void round_resolve_kernel(Rounds r, const float4* __restrict__ po, int par) {
+__global__ void round_resolve_kernel(Rounds r, int par) {
   const uint32_t cnt = r.counts[par * 2 + 1];
   if (blockIdx.x == 0 && threadIdx.x == 0 && cnt) atomicAdd(r.rounds, 1u);
   const uint32_t* in = r.list2[par];
@@ -221,42 +267,37 @@ __global__ void round_resolve_kernel(Rounds r, const float4* __restrict__ po, in
       continue;
     }
     bool blocked = r.U[i] < i;
-    // the K nearest others alive at time i, ascending (d2, index)
-    double bd[kKMax] = {};
-    uint32_t bi[kKMax] = {};
-    int nb = 0;
-    if (!blocked) {
-      const float4 p = po[i];
-      const int cx = cell_coord(p.x, r.g.inv_h), cy = cell_coord(p.y, r.g.inv_h), cz = cell_coord(p.z, r.g.inv_h);
-      for_ball<1>(r.g, cx, cy, cz, [&](uint32_t s) {
-        const float4 q = r.g.pos[s];
-        const uint32_t m = __float_as_uint(q.w);
-        if (m == i) return true;
-        const double d2 = dist2(p, q);
-        if (!(d2 < r.tau2)) return true;
-        if (r.cand[m] && r.U[m] < i) {
-          blocked = true;
-          return false;
-        }
-        if (r.death[m] <= i) return true;  // dead before i's turn
-        if (nb == r.K && !(d2 < bd[nb - 1] || (d2 == bd[nb - 1] && m < bi[nb - 1]))) return true;
-        int k = nb < r.K ? nb++ : nb - 1;
-        while (k > 0 && (d2 < bd[k - 1] || (d2 == bd[k - 1] && m < bi[k - 1]))) {
-          bd[k] = bd[k - 1];
-          bi[k] = bi[k - 1];
-          --k;
-        }
-        bd[k] = d2;
-        bi[k] = m;
-        return true;
-      });
+    const uint32_t k0 = r.pos_of[i];
+    const uint32_t e0 = r.off[k0], e1 = r.off[k0 + 1];
+    for (uint32_t e = e0; e < e1 && !blocked; ++e) {
+      const uint32_t m = r.nb[e] & 0x7fffffffu;
+      blocked = r.cand[m] && r.U[m] < i;
     }
     if (blocked) {
       out[atomicAdd(out_cnt, 1u)] = i;
       continue;
     }
-    for (int k = 0; k < nb; ++k)
-      if (r.cand[bi[k]] && similar(r.F, i, bi[k], r.tau_sim)) atomicMin(r.death + bi[k], i);
+    // the K nearest others alive at time i, ascending (d2, index)
+    double bd[kKMax] = {};
+    uint32_t bi[kKMax] = {};  // neighbour | similar << 31
+    int nbk = 0;
+    for (uint32_t e = e0; e < e1; ++e) {
+      const uint32_t v = r.nb[e];
+      const uint32_t m = v & 0x7fffffffu;
+      if (r.death[m] <= i) continue;  // dead before i's turn
+      const double d2 = r.nbd2[e];
+      if (nbk == r.K && !(d2 < bd[nbk - 1] || (d2 == bd[nbk - 1] && m < (bi[nbk - 1] & 0x7fffffffu)))) continue;
+      int q = nbk < r.K ? nbk++ : nbk - 1;
+      while (q > 0 && (d2 < bd[q - 1] || (d2 == bd[q - 1] && m < (bi[q - 1] & 0x7fffffffu)))) {
+        bd[q] = bd[q - 1];
+        bi[q] = bi[q - 1];
+        --q;
+      }
+      bd[q] = d2;
+      bi[q] = v;
+    }
+    for (int q = 0; q < nbk; ++q)
+      if (bi[q] >> 31) atomicMin(r.death + (bi[q] & 0x7fffffffu), i);
     r.res[i] = 1;
   }
 }
@@ -385,13 +426,57 @@ cudaError_t run_language_redundant(const PruneIn& in, const PruneParams& pp, uin
   candidates_kernel<<<nb, 256, 0, s>>>(g, F, n, tau2, pp.tau_sim, c.cand, c.l1[0], c.l2[0], c.small);
   // list 2 starts with the same count as list 1
   cudaMemcpyAsync(c.small + 1, c.small, 4, cudaMemcpyDeviceToDevice, s);
-  Rounds r{g, F, tau2, pp.tau_sim, pp.k, c.cand, c.res, c.death, c.U, c.small, {c.l1[0], c.l1[1]},
-           {c.l2[0], c.l2[1]}, c.small + 4};
   uint32_t host_cand = 0;
   cudaMemcpyAsync(&host_cand, c.small, 4, cudaMemcpyDeviceToHost, s);
   cudaError_t e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) return e;
   if (candidates) *candidates = host_cand;
+  // the candidates' neighbour lists (CSR), built once for all rounds
+  uint32_t *cnt = nullptr, *off = nullptr, *pos_of = nullptr, *nbl = nullptr;
+  double* nbd2 = nullptr;
+  auto release = [&]() {
+    if (cnt) cudaFreeAsync(cnt, s);
+    if (off) cudaFreeAsync(off, s);
+    if (pos_of) cudaFreeAsync(pos_of, s);
+    if (nbl) cudaFreeAsync(nbl, s);
+    if (nbd2) cudaFreeAsync(nbd2, s);
+  };
+  if (host_cand) {
+    const unsigned grid = (unsigned)std::min<int64_t>((host_cand + 255) / 256, (int64_t)device_sm_count() * 8);
+    if ((e = cudaMallocAsync(reinterpret_cast<void**>(&cnt), sizeof(uint32_t) * (host_cand + 1), s)) != cudaSuccess ||
+        (e = cudaMallocAsync(reinterpret_cast<void**>(&off), sizeof(uint32_t) * (host_cand + 1), s)) != cudaSuccess ||
+        (e = cudaMallocAsync(reinterpret_cast<void**>(&pos_of), sizeof(uint32_t) * (size_t)n, s)) != cudaSuccess) {
+      release();
+      return e;
+    }
+    cudaMemsetAsync(cnt + host_cand, 0, sizeof(uint32_t), s);
+    nb_count_kernel<<<grid, 256, 0, s>>>(g, c.l1[0], c.small, in.pos_opa, tau2, cnt);
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, off, (int)host_cand + 1);
+    void* tmp = nullptr;
+    if ((e = cudaMallocAsync(&tmp, tb, s)) != cudaSuccess) {
+      release();
+      return e;
+    }
+    cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, off, (int)host_cand + 1, s);
+    cudaFreeAsync(tmp, s);
+    uint32_t entries = 0;
+    cudaMemcpyAsync(&entries, off + host_cand, 4, cudaMemcpyDeviceToHost, s);
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) {
+      release();
+      return e;
+    }
+    if ((e = cudaMallocAsync(reinterpret_cast<void**>(&nbl), sizeof(uint32_t) * std::max<uint32_t>(entries, 1), s)) !=
+            cudaSuccess ||
+        (e = cudaMallocAsync(reinterpret_cast<void**>(&nbd2), sizeof(double) * std::max<uint32_t>(entries, 1), s)) !=
+            cudaSuccess) {
+      release();
+      return e;
+    }
+    nb_fill_kernel<<<grid, 256, 0, s>>>(g, F, c.l1[0], c.small, in.pos_opa, tau2, pp.tau_sim, off, nbl, nbd2, pos_of);
+  }
+  Rounds r{pp.k, c.cand, c.res, c.death, c.U, c.small, {c.l1[0], c.l1[1]}, {c.l2[0], c.l2[1]}, c.small + 4,
+           pos_of, off, nbl, nbd2};
   if (host_cand) {
     const unsigned grid = (unsigned)std::min<int64_t>((host_cand + 255) / 256, (int64_t)device_sm_count() * 8);
     int par = 0;
@@ -401,18 +486,25 @@ cudaError_t run_language_redundant(const PruneIn& in, const PruneParams& pp, uin
     while (left) {
       // every round resolves at least the smallest unresolved candidate: more rounds than
       // candidates would be a bug, not a slow map -- fail instead of spinning
-      if (issued > (int64_t)host_cand + kBatch) return cudaErrorUnknown;
+      if (issued > (int64_t)host_cand + kBatch) {
+        release();
+        return cudaErrorUnknown;
+      }
       issued += kBatch;
       for (int b = 0; b < kBatch; ++b) {
         cudaMemsetAsync(c.small + (par ^ 1) * 2, 0, 8, s);
-        round_u_kernel<<<grid, 256, 0, s>>>(r, in.pos_opa, par);
-        round_resolve_kernel<<<grid, 256, 0, s>>>(r, in.pos_opa, par);
+        round_u_kernel<<<grid, 256, 0, s>>>(r, par);
+        round_resolve_kernel<<<grid, 256, 0, s>>>(r, par);
         par ^= 1;
       }
       cudaMemcpyAsync(&left, c.small + par * 2 + 1, 4, cudaMemcpyDeviceToHost, s);
-      if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+      if ((e = cudaStreamSynchronize(s)) != cudaSuccess) {
+        release();
+        return e;
+      }
     }
   }
+  release();
   unsigned long long* total = reinterpret_cast<unsigned long long*>(c.small + 8);
   death_flags_kernel<<<nb, 256, 0, s>>>(c.death, n, flags, total);
   unsigned long long host_total = 0;
