@@ -51,6 +51,8 @@ def parse():
     p.add_argument("--no-mapping", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-pruning", action="store_true")
+    p.add_argument("--no-speculative-plans", action="store_true",
+                   help="always capture the layered binning's second pass (LGS_OPT_SPECULATIVE_PLANS = 0)")
     p.add_argument("--rng", choices=["pcg64", "reference"], default="pcg64",
                    help="scene generator: numpy PCG64, or the reference's lego::Rng stream (scenes.RefRng)")
     p.add_argument("--e2e-steps", type=int, default=30)
@@ -272,7 +274,7 @@ def run_ours(args):
     tg = scenes.make_targets(cam, d, info["depth_range"], 7 + rank)
 
     stream = torch.cuda.Stream(device=local)
-    ctx = R.Context(local, stream=stream.cuda_stream)
+    ctx = R.Context(local, stream=stream.cuda_stream, speculative_plans=not args.no_speculative_plans)
     with torch.cuda.stream(stream):
         dscene = {k: torch.from_numpy(v).cuda(local) for k, v in scene.items()}
         dtg = {k: torch.from_numpy(v).cuda(local) for k, v in tg.items()}
@@ -473,6 +475,9 @@ def run_ours(args):
                    "l2": "512 MiB L2 flush before every timed step"},
         "clocks": clk.summary(),
         "gpu_launches": int(launches),
+        # speculative: the plan was captured without the layered binning's second pass (every tile
+        # saturated on its first-pass list at warm-up); recaptures: steps sync() re-ran
+        "plan": {"speculative": plan.speculative, "recaptures": plan.recaptures},
         "roofline": roofline,
         "work": {"visible": V, "pairs": P, "listed": LST, "active": A, "evaluated": evaluated, "contributed": contributed,
                  "max_tile_list": st["max_tile_list"]},

@@ -182,8 +182,18 @@ LGS_API lgs_status lgs_ctx_set_full_tile_lists(lgs_ctx* ctx, int32_t full);
  *                              nonzero now cross the link, the rows nonzero last time are zeroed
  *                              on the host; the buffers hold the exact dense MapGradients after
  *                              every call.  The first call (or new buffers) writes densely.  The
- *                              caller must not modify the buffers between calls. */
-enum { LGS_OPT_FULL_TILE_LISTS = 0, LGS_OPT_RADIX_DEPTH_ORDER = 1, LGS_OPT_FUSED_EAGER = 2, LGS_OPT_HOST_GRAD_DELTA = 3 };
+ *                              caller must not modify the buffers between calls;
+ *   LGS_OPT_SPECULATIVE_PLANS  1 (default): a non-accumulating lgs_plan whose warm-up render
+ *                              saturated every tile on its layer-A list is captured without the
+ *                              layered binning's second pass (lgs_plan_speculative); 0: always
+ *                              with it. */
+enum {
+  LGS_OPT_FULL_TILE_LISTS = 0,
+  LGS_OPT_RADIX_DEPTH_ORDER = 1,
+  LGS_OPT_FUSED_EAGER = 2,
+  LGS_OPT_HOST_GRAD_DELTA = 3,
+  LGS_OPT_SPECULATIVE_PLANS = 4
+};
 LGS_API lgs_status lgs_ctx_set_option(lgs_ctx* ctx, int32_t option, int64_t value);
 LGS_API lgs_status lgs_ctx_set_stream(lgs_ctx* ctx, void* stream);
 /* Bytes the context has copied host->device and device->host since creation (map uploads,
@@ -425,7 +435,8 @@ LGS_API lgs_status lgs_prune_stats(const lgs_ctx* ctx, int64_t* candidates, int6
  * gradient to pinned-host / device memory or NULL) on a resident map and a fixed camera,
  * captured once into a CUDA graph and replayed with one launch (no host work inside the step).
  * The tile-list capacity comes from an eager warm-up step; lgs_plan_sync waits for the replay and
- * re-captures + re-runs it if the pair count outgrew the capacity.  Map contents, targets and
+ * re-captures + re-runs it if the pair count outgrew the capacity, or if a speculative plan
+ * (below) left a tile unsaturated.  Map contents, targets and
  * gradient buffers may change between replays (same pointers); a new camera re-captures.
  * grads->accumulate = 1: each replay adds its gradients into the buffers (the later views of a
  * multi-view batch; an overflowed replay adds nothing before lgs_plan_sync re-runs it).  The eager
@@ -445,8 +456,15 @@ LGS_API lgs_status lgs_plan_elapsed_ms(const lgs_plan* plan, float* ms);
 LGS_API lgs_status lgs_plan_set_profiling(lgs_ctx* ctx, lgs_plan* plan, int32_t on);
 LGS_API lgs_status lgs_plan_phase_times(const lgs_plan* plan, double* ms);
 LGS_API int64_t lgs_plan_launches(const lgs_plan* plan);
-/* Times lgs_plan_sync re-captured and re-ran the step (tile lists outgrew the capacity). */
+/* Times lgs_plan_sync re-captured and re-ran the step (tile lists outgrew the capacity, or a
+ * speculative replay left a tile unsaturated). */
 LGS_API int64_t lgs_plan_recaptures(const lgs_plan* plan);
+/* 1: the plan is speculative -- captured without the layered binning's second pass, because the
+ * warm-up render saturated every tile on its first-pass (layer-A) list; each replay reports an
+ * unsaturated tile through a mapped host word and lgs_plan_sync then re-captures the plan with the
+ * second pass (for good) and re-runs the step, so results never depend on the guess.  0: not
+ * speculative (accumulating plans never are). */
+LGS_API int32_t lgs_plan_speculative(const lgs_plan* plan);
 LGS_API lgs_status lgs_plan_destroy(lgs_plan* plan);
 
 /* ---- multi-view mapping batches --------------------------------------------

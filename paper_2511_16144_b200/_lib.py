@@ -14,6 +14,7 @@ LIB_PATH = os.path.join(HERE, "liblgs.so")
 LGS_OK, LGS_EINVAL, LGS_ECUDA, LGS_ENOMEM, LGS_ENODEV, LGS_EIO = range(6)
 LGS_MEM_HOST, LGS_MEM_DEVICE, LGS_MEM_HOST_MAPPED = 0, 1, 2
 LGS_OPT_FULL_TILE_LISTS, LGS_OPT_RADIX_DEPTH_ORDER, LGS_OPT_FUSED_EAGER, LGS_OPT_HOST_GRAD_DELTA = 0, 1, 2, 3
+LGS_OPT_SPECULATIVE_PLANS = 4
 
 _fp = C.POINTER(C.c_float)
 
@@ -165,6 +166,7 @@ SIGNATURES = [
     ("lgs_plan_phase_times", C.c_int, [C.c_void_p, C.POINTER(C.c_double)]),
     ("lgs_plan_launches", C.c_int64, [C.c_void_p]),
     ("lgs_plan_recaptures", C.c_int64, [C.c_void_p]),
+    ("lgs_plan_speculative", C.c_int32, [C.c_void_p]),
     ("lgs_plan_destroy", C.c_int, [C.c_void_p]),
     ("lgs_comm_unique_id", C.c_int, [C.POINTER(LgsCommId)]),
     ("lgs_comm_init", C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.POINTER(LgsCommId)]),

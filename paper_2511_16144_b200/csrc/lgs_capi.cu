@@ -113,6 +113,7 @@ struct lgs_ctx {
   bool radix_depth = false;  // LGS_OPT_RADIX_DEPTH_ORDER: CUB radix sort for the depth order (cross-check)
   bool fused_eager = false;  // LGS_OPT_FUSED_EAGER: uncaptured fused-L1 renders run the fused kernel
   bool host_grad_delta = false;  // LGS_OPT_HOST_GRAD_DELTA: host gradients rewritten row-sparse
+  bool no_speculative = false;   // LGS_OPT_SPECULATIVE_PLANS = 0: plans always capture pass 2
   // host-gradient delta mode: the destination of the previous backward and the rows it left nonzero
   std::array<float*, 6> delta_dst{};
   int64_t delta_n = -1;
@@ -192,6 +193,12 @@ struct lgs_ctx {
   bool lp_pending = false;
   int lp_ntiles = 0;
   uint32_t lp_div = 0;  // the div the pending counts were taken at
+  // the last counts the policy read: unfinished tiles at (ntiles, div) -- a plan captured right
+  // after a render that saturated every tile leaves pass 2 out (speculative plan, lgs_plan_sync)
+  uint64_t lp_last_unfinished = UINT64_MAX;
+  int lp_last_ntiles = 0;
+  uint32_t lp_last_div = 0;
+  uint32_t* cap_unfinished_any = nullptr;  // speculative plan capture: pass 1 only, reports here
   // last lgs_find_language_redundant: candidates (a similar neighbour inside tau_dist), rounds
   int64_t prune_candidates = 0, prune_rounds = 0;
 };
@@ -679,6 +686,7 @@ LGS_API lgs_status lgs_ctx_set_option(lgs_ctx* ctx, int32_t option, int64_t valu
     case LGS_OPT_FULL_TILE_LISTS: ctx->full_lists = value != 0; return LGS_OK;
     case LGS_OPT_RADIX_DEPTH_ORDER: ctx->radix_depth = value != 0; return LGS_OK;
     case LGS_OPT_FUSED_EAGER: ctx->fused_eager = value != 0; return LGS_OK;
+    case LGS_OPT_SPECULATIVE_PLANS: ctx->no_speculative = value == 0; return LGS_OK;
     case LGS_OPT_HOST_GRAD_DELTA:
       ctx->host_grad_delta = value != 0;
       ctx->delta_n = -1;  // the next backward writes densely
@@ -798,6 +806,9 @@ void layer_policy_update(lgs_ctx* ctx, int ntiles) {
   if (ctx->lp_ntiles != ntiles || ctx->lp_div != ctx->layer_div) return;  // counts of another image / size
   const uint64_t consumed = ctx->lp_host[0], listed = ctx->lp_host[1], unfinished = ctx->lp_host[2];
   uint32_t& div = ctx->layer_div;
+  ctx->lp_last_unfinished = unfinished;
+  ctx->lp_last_ntiles = ntiles;
+  ctx->lp_last_div = div;
   if (unfinished * 20 > (uint64_t)ntiles && ctx->pairs_cap < kSinglePassPairs) {
     ctx->single_pass = true;
     ctx->sp_cap = ctx->pairs_cap;
@@ -1083,15 +1094,21 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
       uint32_t *ra = nullptr, *unfinished = nullptr, *sat = nullptr, *order2 = nullptr, *count2 = nullptr;
       uint32_t* scratch_b = nullptr;
       uint2* cand_rect = nullptr;
-      LGS_TRY(dalloc(ctx, &t->vals, (size_t)capA + (size_t)cap));
-      t->vals_count = (int64_t)capA + cap;
+      // a speculative plan (captured after a render that saturated every tile) has no pass 2: a
+      // replay that leaves a tile unfinished says so through a mapped host word, and lgs_plan_sync
+      // re-captures the plan with pass 2 and runs the step again
+      uint32_t* const spec = ctx->capturing ? ctx->cap_unfinished_any : nullptr;
+      LGS_TRY(dalloc(ctx, &t->vals, (size_t)capA + (spec ? 0 : (size_t)cap)));
+      t->vals_count = (int64_t)capA + (spec ? 0 : cap);
       LGS_TRY(dalloc(ctx, &ra, 4 + (size_t)ntiles));  // [0] R_A, [1] list allocator, [4 ..] unfinished flags
       unfinished = ra + 4;
       LGS_TRY(dalloc(ctx, &cand_rect, gcapA));
-      LGS_TRY(dalloc(ctx, &sat, sat_n));
-      LGS_TRY(dalloc(ctx, &order2, ntiles));
-      LGS_TRY(dalloc(ctx, &count2, 2));  // [0] unfinished tiles, [1] pairs of the second pass
-      LGS_TRY(dalloc(ctx, reinterpret_cast<uint8_t**>(&scratch_b), fast_binning_scratch_bytes(cap, n, ntiles)));
+      if (!spec) {
+        LGS_TRY(dalloc(ctx, &sat, sat_n));
+        LGS_TRY(dalloc(ctx, &order2, ntiles));
+        LGS_TRY(dalloc(ctx, &count2, 2));  // [0] unfinished tiles, [1] pairs of the second pass
+        LGS_TRY(dalloc(ctx, reinterpret_cast<uint8_t**>(&scratch_b), fast_binning_scratch_bytes(cap, n, ntiles)));
+      }
       LGS_CUDA(cudaMemsetAsync(ra, 0, sizeof(uint32_t) * (4 + (size_t)ntiles), s));
       // captured fused-L1 step: each tile's backward runs right after its forward (blend_fused.cu);
       // the depth order flags the layer-A Gaussians active and zeroes their accumulator rows
@@ -1123,6 +1140,7 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
       if (targets && !fuse) LGS_CUDA(cudaMemsetAsync(t->loss, 0, sizeof(double), s));
       FwdOut fo1 = fo;
       fo1.unfinished = unfinished;
+      fo1.unfinished_any = spec;
       const bool policy = !ctx->capturing && !ctx->lp_pending;  // count this render for the layer-A policy
       if (policy) {
         if (!ctx->lp_dev) {
@@ -1144,6 +1162,12 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
           launch_blend_fwd(dm, dc, t->vb, TileLists{t->vals, t->ranges, nullptr, t->counter}, t->ps, fo1, s);
       }
       ctx->launches++;
+      if (spec) {
+        dfree(ctx, cand_rect);
+        dfree(ctx, ra);
+        LGS_CUDA(cudaGetLastError());
+        return LGS_OK;
+      }
       // pass 2, inside a captured plan as the body of a conditional node (skipped when every tile
       // saturated); eagerly its kernels find no unfinished tile and return at once
       cudaGraphConditionalHandle cond{};
@@ -2944,6 +2968,10 @@ struct lgs_plan {
                                    // plan its own slot: several plans may share a context)
   uint32_t* lpt[2] = {nullptr, nullptr};  // tile orders: [0] used by a replay, [1] computed by it
   int lpt_n = 0;
+  bool speculative = false;       // captured without the layered binning's pass 2
+  int64_t spec_misses = 0;        // speculative replays redone with pass 2
+  uint32_t* unf_host = nullptr;   // mapped pinned: set by a speculative replay that left a tile unfinished
+  uint32_t* unf_dev = nullptr;    // its device address
 };
 
 namespace {
@@ -2995,6 +3023,7 @@ lgs_status plan_capture(lgs_plan* p) {
   ctx->cap_lpt_cur = p->lpt[0];
   ctx->cap_lpt_next = p->lpt[1];
   ctx->lpt_forked = false;
+  ctx->cap_unfinished_any = p->speculative ? p->unf_dev : nullptr;
   plan_free_marks(p);
   ctx->capture_marks = p->profile ? &p->marks : nullptr;  // event nodes cost ~5 us each per replay
   uint32_t* const saved_host = ctx->host_u32;
@@ -3019,6 +3048,7 @@ lgs_status plan_capture(lgs_plan* p) {
     ctx->prezero_forked = false;
   }
   ctx->lpt_forked = false;
+  ctx->cap_unfinished_any = nullptr;
   ctx->cap_lpt_cur = ctx->cap_lpt_next = nullptr;
   ctx->prezero = nullptr;
   ctx->capturing = false;
@@ -3076,6 +3106,7 @@ LGS_API lgs_status lgs_plan_create(lgs_ctx* ctx, lgs_map* map, const lgs_camera*
     if (p->ev1) cudaEventDestroy(p->ev1);
     if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
     if (p->host_pairs) cudaFreeHost(p->host_pairs);
+    if (p->unf_host) cudaFreeHost(p->unf_host);
     for (auto& b : p->lpt)
       if (b) cudaFree(b);
     ctx_release(ctx);
@@ -3084,6 +3115,8 @@ LGS_API lgs_status lgs_plan_create(lgs_ctx* ctx, lgs_map* map, const lgs_camera*
   };
   if (cudaEventCreate(&p->ev0) != cudaSuccess || cudaEventCreate(&p->ev1) != cudaSuccess ||
       cudaMallocHost(&p->host_pairs, 64) != cudaSuccess ||
+      cudaHostAlloc(reinterpret_cast<void**>(&p->unf_host), 64, cudaHostAllocMapped) != cudaSuccess ||
+      cudaHostGetDevicePointer(reinterpret_cast<void**>(&p->unf_dev), p->unf_host, 0) != cudaSuccess ||
       cudaStreamCreateWithFlags(&p->cap_stream, cudaStreamNonBlocking) != cudaSuccess)
     return bail(fail(LGS_ECUDA, "event / stream creation failed"));
   // forward-only eager renders until the layer-A size policy settles (at most 4), then one eager
@@ -3103,6 +3136,15 @@ LGS_API lgs_status lgs_plan_create(lgs_ctx* ctx, lgs_map* map, const lgs_camera*
   if (tape) lgs_saved_destroy(tape);
   if (st != LGS_OK) return bail(st);
   if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return bail(fail(LGS_ECUDA, "warm-up step failed"));
+  {
+    // every tile of the last counted render saturated on its layer-A list (the step's pass 2 did
+    // nothing): capture pass 1 only; the replays report any unfinished tile (lgs_plan_sync)
+    const int nt = ((p->cam.width + LGS_TILE - 1) / LGS_TILE) * ((p->cam.height + LGS_TILE - 1) / LGS_TILE);
+    layer_policy_update(ctx, nt);
+    p->speculative = !p->grads.accumulate && !ctx->no_speculative && ctx->lp_last_unfinished == 0 &&
+                     ctx->lp_last_ntiles == nt && ctx->lp_last_div == ctx->layer_div;
+    *p->unf_host = 0;
+  }
   if ((st = plan_capture(p)) != LGS_OK) return bail(st);
   *out = p;
   return LGS_OK;
@@ -3111,6 +3153,7 @@ LGS_API lgs_status lgs_plan_create(lgs_ctx* ctx, lgs_map* map, const lgs_camera*
 LGS_API lgs_status lgs_plan_run(lgs_ctx* ctx, lgs_plan* p) {
   if (!ctx || !p || ctx != p->ctx) return fail(LGS_EINVAL, "plan / context mismatch");
   if (!version_live(p->map_version)) return fail(LGS_EINVAL, "the plan's map was pruned or destroyed: recreate the plan");
+  if (p->speculative) *reinterpret_cast<volatile uint32_t*>(p->unf_host) = 0;
   LGS_CUDA(cudaGraphLaunch(p->exec, ctx->stream));
   ctx->launches += p->launches_per_run;
   return LGS_OK;
@@ -3119,13 +3162,23 @@ LGS_API lgs_status lgs_plan_run(lgs_ctx* ctx, lgs_plan* p) {
 LGS_API lgs_status lgs_plan_sync(lgs_ctx* ctx, lgs_plan* p, int64_t* pairs) {
   if (!ctx || !p || ctx != p->ctx) return fail(LGS_EINVAL, "plan / context mismatch");
   LGS_CUDA(cudaStreamSynchronize(ctx->stream));
-  const int64_t P = p->host_pairs[0];
-  if (P > p->cap) {  // the replay ran on empty tile lists: grow, re-capture, redo the step
-    ctx->pairs_cap = std::max<int64_t>(ctx->pairs_cap, P + P / 4);
+  int64_t P = p->host_pairs[0];
+  for (int redo = 0; redo < 3; ++redo) {
+    // P > capacity: the replay ran on empty tile lists (grow, re-capture, redo the step); a
+    // speculative replay that left a tile unfinished: re-capture with pass 2 and redo the step
+    const bool over = P > p->cap;
+    const bool unfinished = !over && p->speculative && *reinterpret_cast<volatile uint32_t*>(p->unf_host) != 0;
+    if (!over && !unfinished) break;
+    if (over) ctx->pairs_cap = std::max<int64_t>(ctx->pairs_cap, P + P / 4);
+    if (unfinished) {
+      p->speculative = false;
+      ++p->spec_misses;
+    }
     ++p->recaptures;
     LGS_TRY(plan_capture(p));
     LGS_TRY(lgs_plan_run(ctx, p));
     LGS_CUDA(cudaStreamSynchronize(ctx->stream));
+    P = p->host_pairs[0];
   }
   if (pairs) *pairs = P;
   return LGS_OK;
@@ -3175,6 +3228,7 @@ LGS_API lgs_status lgs_plan_destroy(lgs_plan* p) {
   if (p->ev1) cudaEventDestroy(p->ev1);
   if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
   if (p->host_pairs) cudaFreeHost(p->host_pairs);
+  if (p->unf_host) cudaFreeHost(p->unf_host);
   for (auto& b : p->lpt)
     if (b) cudaFree(b);
   delete p;
@@ -3183,5 +3237,7 @@ LGS_API lgs_status lgs_plan_destroy(lgs_plan* p) {
 }
 
 LGS_API int64_t lgs_plan_recaptures(const lgs_plan* p) { return p ? p->recaptures : -1; }
+
+LGS_API int32_t lgs_plan_speculative(const lgs_plan* p) { return p ? (p->speculative ? 1 : 0) : -1; }
 
 }  // extern "C"

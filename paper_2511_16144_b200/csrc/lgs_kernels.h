@@ -69,6 +69,8 @@ struct FwdOut {
   // depth-layered first pass: tiles not saturated by their (prefix) list are flagged here and get
   // no loss / cotangents (the second pass renders them again on their complete lists)
   uint32_t* unfinished = nullptr;
+  // ... and, if set (a speculative plan without pass 2: mapped host memory), any such tile stores 1
+  uint32_t* unfinished_any = nullptr;
   // ... and every warp of a saturated tile adds the list length its pixels consumed (the layer-A
   // size policy of lgs_capi.cu)
   uint32_t* consumed = nullptr;

@@ -94,7 +94,7 @@ class Context:
     the reference's "concurrent renders between map mutations" contract)."""
 
     def __init__(self, device: int = 0, stream=None, full_lists: bool = False, radix_depth_order: bool = False,
-                 fused_eager: bool = False, host_grad_delta: bool = False):
+                 fused_eager: bool = False, host_grad_delta: bool = False, speculative_plans: bool = True):
         L = _lib.load()
         if stream == "own":
             stream = None
@@ -116,6 +116,8 @@ class Context:
             check(L.lgs_ctx_set_option(h, _lib.LGS_OPT_FUSED_EAGER, 1))
         if host_grad_delta:  # host gradient buffers reused unchanged: row-sparse rewrites (include/lgs.h)
             check(L.lgs_ctx_set_option(h, _lib.LGS_OPT_HOST_GRAD_DELTA, 1))
+        if not speculative_plans:  # plans always capture the layered binning's second pass
+            check(L.lgs_ctx_set_option(h, _lib.LGS_OPT_SPECULATIVE_PLANS, 0))
 
     def synchronize(self):
         check(_lib.load().lgs_ctx_synchronize(self.h))
@@ -627,6 +629,12 @@ class Plan:
     def recaptures(self) -> int:
         """How often sync() re-captured and re-ran the step (the tile lists outgrew the capacity)."""
         return int(_lib.load().lgs_plan_recaptures(self.h))
+
+    @property
+    def speculative(self) -> bool:
+        """Captured without the layered binning's second pass (every warm-up tile saturated on
+        its first-pass list); a replay that leaves a tile unsaturated is re-run by sync()."""
+        return bool(_lib.load().lgs_plan_speculative(self.h))
 
     def __del__(self):
         try:

@@ -131,3 +131,45 @@ def test_eager_backward_overwrites_every_row():
     for k in GROUPS:
         frac, worst = grad_mismatch(dirty[k], g[k])
         assert frac < 1e-3, (k, frac, worst)
+
+
+def test_speculative_plan_and_fallback():
+    """A plan whose warm-up render saturated every tile on its layer-A list is captured without the
+    second pass (lgs_plan_speculative).  Its replays match a plan captured with the pass and the
+    eager step; a replay that leaves tiles unsaturated (faint splats) is detected, re-captured with
+    the second pass and re-run inside sync(), and the results are again the eager ones."""
+    scene, cams, info = scenes.make_config("c1", n=500_000)
+    cam = cams[0]
+    tg_np = scenes.make_targets(cam, scene["feat"].shape[0], info["depth_range"], 3)
+    res = {}
+    for spec in (True, False):
+        ctx = R.Context(0, speculative_plans=spec)
+        dm = R.DeviceMap({k: torch.from_numpy(v).cuda() for k, v in scene.items()}, ctx)
+        tg = {k: torch.from_numpy(v).cuda() for k, v in tg_np.items()}
+        grads = R.alloc_grads(dm.n, dm.d, dm.K, device=0)
+        imgs = _images(cam, dm.d)
+        pose = torch.zeros(6, dtype=torch.float32, pin_memory=True)
+        plan = R.Plan(dm, cam, tg, grads, images=imgs, pose_out=pose)
+        assert plan.speculative == spec
+        plan.run()
+        plan.sync()
+        assert plan.recaptures == 0
+        res[spec] = ({k: v.clone() for k, v in imgs.items()}, plan, dm, tg, grads, imgs, pose)
+    for k in ("rgb", "depth", "feat", "acc"):
+        assert torch.equal(res[True][0][k], res[False][0][k]), k
+    _, plan, dm, tg, grads, imgs, pose = res[True]
+    out, g = _eager(dm, cam, tg)
+    _check(grads, pose, imgs, out, g)
+    faint = dict(scene, opac=(scene["opac"] - 4.0).astype(np.float32))
+    dm.update({k: torch.from_numpy(v).cuda() for k, v in faint.items()})
+    plan.run()
+    plan.sync()
+    assert plan.recaptures == 1 and not plan.speculative
+    out, g = _eager(dm, cam, tg)
+    _check(grads, pose, imgs, out, g)
+    dm.update({k: torch.from_numpy(v).cuda() for k, v in scene.items()})
+    plan.run()
+    plan.sync()
+    assert plan.recaptures == 1
+    out, g = _eager(dm, cam, tg)
+    _check(grads, pose, imgs, out, g)
