@@ -21,8 +21,6 @@
 // Culled Gaussians follow the visible ones in arbitrary order: they own no tile pairs, so their
 // order affects no output.
 // Roofline: HBM/L2 latency; ~(4 + 4) B read + written per Gaussian per step, ~20 B in total.
-#include <cub/device/device_scan.cuh>
-
 #include <algorithm>
 #include <cstring>
 
@@ -93,6 +91,153 @@ __global__ void depth_cut_kernel(const u64* __restrict__ off, uint32_t div, uint
       next_feas = (int64_t)cnt_of(in2) <= gauss_cap && prs_of(in2) <= cap_a;
     }
     if (!next_feas) offer((uint32_t)b + 1u);
+  }
+}
+
+// ---- bucket offsets in one launch ---------------------------------------------------------------
+// Exclusive scan of the kDepthBuckets + 2 bucket words (count << 32 | pairs) in one launch: each
+// CTA takes the next 2048-word tile (dynamic tile id, so every predecessor is already running),
+// stages it through shared memory (coalesced loads and stores, a blocked 4-word run per thread),
+// publishes its tile aggregate with a release flag, and adds up its (at most 128) predecessors'
+// aggregates in one parallel round, thread j waiting for tile j (a decoupled look-back without the
+// serial chain: the aggregates all land at about the same time).  The pair total P comes from K1's
+// per-CTA partial sums (read while the predecessors publish), so every thread also applies
+// depth_cut_kernel's rule to its own buckets: CUB's init + scan kernels and the cut kernel become
+// one launch.  Flags, aggregates and the tile counter live in the scalar block zeroed with the
+// histogram.
+constexpr int kScanThreads = 512, kScanItems = 4, kScanTile = kScanThreads * kScanItems;
+constexpr int kScanTiles = (kDepthBuckets + 2 + kScanTile - 1) / kScanTile;
+static_assert(kScanTiles <= kScanThreads, "one predecessor per thread");
+
+struct ScanCut {
+  const uint32_t* part;  // K1's per-CTA pair sums (null: offsets only, no cut)
+  uint32_t nparts;
+  uint32_t div, min_pairs, cap_a;
+  int64_t gauss_cap;
+  uint32_t* cut;
+};
+
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ u64 warp_incl_scan(u64 v, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const u64 y = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += y;
+  }
+  return v;
+}
+
+__device__ __forceinline__ int scan_pad(int i) { return i + (i >> 4); }  // one spare word per 16
+
+__global__ void __launch_bounds__(kScanThreads) bucket_scan_kernel(const u64* __restrict__ hist, u64* __restrict__ off,
+                                                                   uint32_t* __restrict__ tile_ctr,
+                                                                   uint32_t* __restrict__ flags, u64* __restrict__ agg,
+                                                                   ScanCut sc) {
+  constexpr int nitems = kDepthBuckets + 2;
+  constexpr int kWarps = kScanThreads / 32;
+  __shared__ u64 s_buf[kScanTile + kScanTile / 16];
+  __shared__ uint32_t s_tile, s_p[kWarps];
+  __shared__ u64 s_warp[kWarps], s_look[kWarps];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  griddep_wait();
+  if (tid == 0) s_tile = atomicAdd(tile_ctr, 1u);
+  __syncthreads();
+  const int t = (int)s_tile;
+  const int base = t * kScanTile;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    const int i = base + k * kScanThreads + tid;
+    s_buf[scan_pad(k * kScanThreads + tid)] = i < nitems ? __ldcg(hist + i) : 0ull;
+  }
+  __syncthreads();
+  u64 v[kScanItems];
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) v[k] = s_buf[scan_pad(tid * kScanItems + k)];
+  u64 mine = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) mine += v[k];
+  const u64 wincl = warp_incl_scan(mine, lane);
+  if (lane == 31) s_warp[warp] = wincl;
+  __syncthreads();
+  if (warp == 0) {
+    const u64 x = lane < kWarps ? s_warp[lane] : 0ull;
+    const u64 xi = warp_incl_scan(x, lane);
+    if (lane < kWarps) s_warp[lane] = xi - x;  // exclusive warp offsets
+    if (lane == 31) {  // publish the tile aggregate
+      agg[t] = xi;
+      st_release_u32(flags + t, 1u);
+    }
+  }
+  // the pair total from K1's partial sums (independent loads, issued while predecessors publish)
+  uint32_t p = 0;
+  if (sc.part) {
+    uint32_t j = tid;
+    for (; j + 3 * kScanThreads < sc.nparts; j += 4 * kScanThreads) {
+      const uint32_t a0 = __ldcg(sc.part + j), a1 = __ldcg(sc.part + j + kScanThreads);
+      const uint32_t a2 = __ldcg(sc.part + j + 2 * kScanThreads), a3 = __ldcg(sc.part + j + 3 * kScanThreads);
+      p += (a0 + a1) + (a2 + a3);
+    }
+    for (; j < sc.nparts; j += kScanThreads) p += __ldcg(sc.part + j);
+    p = __reduce_add_sync(0xffffffffu, p);
+    if (lane == 0) s_p[warp] = p;
+  }
+  // prefix = the sum of every predecessor's aggregate, thread j waiting for tile j
+  u64 pre = 0;
+  if (tid < t) {
+    while (ld_acquire_u32(flags + tid) == 0u) {
+    }
+    pre = __ldcg(agg + tid);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) pre += __shfl_xor_sync(0xffffffffu, pre, o);
+  if (lane == 0) s_look[warp] = pre;
+  __syncthreads();
+  u64 ex = s_warp[warp] + (wincl - mine);
+  uint32_t P = 0;
+#pragma unroll
+  for (int w = 0; w < kWarps; ++w) {
+    ex += s_look[w];
+    if (sc.part) P += s_p[w];
+  }
+  const uint32_t target = sc.part ? max(min(P, sc.min_pairs), P / sc.div) : 0u;
+  auto feas = [&](u64 in) { return (int64_t)cnt_of(in) <= sc.gauss_cap && prs_of(in) <= sc.cap_a; };
+  auto offer = [&](uint32_t end) { atomicMax(sc.cut, (uint32_t)kDepthBuckets + 1u - end); };
+  u64 exk[kScanItems];
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    const int b = base + tid * kScanItems + k;
+    exk[k] = ex;
+    const u64 in = ex + v[k];
+    if (sc.part && b < kDepthBuckets) {  // depth_cut_kernel's rule for bucket b
+      if (prs_of(in) >= target && prs_of(ex) < target) offer((uint32_t)b + 1u);
+      const bool f = feas(in);
+      if (b == 0 && !f) offer(0u);
+      if (f) {
+        u64 nx;
+        if (k + 1 < kScanItems) nx = v[k + 1];
+        else if (tid + 1 < kScanThreads) nx = s_buf[scan_pad((tid + 1) * kScanItems)];
+        else nx = __ldcg(hist + b + 1);
+        if (!(b + 1 < kDepthBuckets && feas(in + nx))) offer((uint32_t)b + 1u);
+      }
+    }
+    ex = in;
+  }
+  __syncthreads();  // every thread has read its neighbour's bucket: reuse the buffer for the offsets
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) s_buf[scan_pad(tid * kScanItems + k)] = exk[k];
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    const int i = base + k * kScanThreads + tid;
+    if (i < nitems) off[i] = s_buf[scan_pad(k * kScanThreads + tid)];
   }
 }
 
@@ -276,12 +421,16 @@ __global__ void __launch_bounds__(1024) depth_big_kernel(const uint2* __restrict
 // ------------------------------------------------------------------------------------------
 static size_t align_words(size_t w) { return (w + 63) & ~size_t(63); }
 
-static size_t scan_bytes_for() {
-  size_t scan = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, scan, (unsigned long long*)nullptr, (unsigned long long*)nullptr,
-                                kDepthBuckets + 2);
-  return scan;
-}
+// scalars (zeroed with the histogram): cut, big-bucket counts of layer A / the rest, bitonic
+// scratch allocator, culled-slot allocator, rank-done counter (the first kScRerun are zeroed again
+// by a re-run of layer A), bucket-scan tile counter, the pair total P (preprocess); then the bucket
+// scan's flags (zeroed too), tile aggregates and inclusive prefixes
+enum {
+  kScCut = 0, kScBigA = 1, kScBigR = 2, kScScratch = 3, kScCulled = 4, kScRankDone = 5, kScRerun = 6,
+  kScScanTile = 6
+};
+constexpr size_t kScFlags = 64, kScAgg = kScFlags + 256, kScWords = kScAgg + 2 * 256;
+constexpr size_t kScZeroed = kScFlags + kScanTiles;  // words zeroed per render
 
 size_t depth_order_temp_bytes(int64_t n) {
   const size_t nn = align_words((size_t)n);
@@ -290,21 +439,17 @@ size_t depth_order_temp_bytes(int64_t n) {
                        + 2 * nn                                 // tmp (uint2)
                        + 4 * nn                                 // scratch (2n u64)
                        + align_words((size_t)n / kMaxRankBucket + 2) * 2  // big lists (layer A, rest)
-                       + 64;                                    // scalars
-  return sizeof(uint32_t) * words + scan_bytes_for() + 1024;
+                       + kScWords                               // scalars + bucket-scan state
+                       + align_words((size_t)n / kPreThreads + 1);  // K1's per-CTA pair sums
+  return sizeof(uint32_t) * words + 1024;
 }
 
-// scalars (zeroed together): cut, big-bucket counts of layer A / the rest, bitonic scratch
-// allocator, culled-slot allocator
-enum { kScCut = 0, kScBigA = 1, kScBigR = 2, kScScratch = 3, kScCulled = 4, kScRankDone = 5, kScalars = 8 };
 
 struct DepthCarve {
   unsigned long long *hist, *off;
   uint2* tmp;
-  uint32_t *slot, *big_a, *big_r, *sc;
+  uint32_t *slot, *big_a, *big_r, *sc, *part;
   unsigned long long* scratch;
-  void* scan_temp;
-  size_t scan_bytes;
   uint32_t base;
 };
 
@@ -315,7 +460,7 @@ static DepthCarve carve(void* temp, int64_t n, float near_plane) {
   c.hist = reinterpret_cast<unsigned long long*>(w);
   w += 2 * nb;
   c.sc = w;  // right after the histogram: one memset zeroes both
-  w += 64;
+  w += kScWords;
   c.off = reinterpret_cast<unsigned long long*>(w);
   w += 2 * nb;
   c.slot = w;
@@ -329,8 +474,7 @@ static DepthCarve carve(void* temp, int64_t n, float near_plane) {
   w += nbig;
   c.big_r = w;
   w += nbig;
-  c.scan_temp = w;
-  c.scan_bytes = scan_bytes_for();
+  c.part = w;
   // near plane in key space: depths are > near, so buckets start there (2^13 per octave)
   const float nearp = near_plane > 0.f ? near_plane : 0.f;
   uint32_t nbits;
@@ -339,12 +483,16 @@ static DepthCarve carve(void* temp, int64_t n, float near_plane) {
   return c;
 }
 
+static void launch_bucket_scan(const DepthCarve& c, const ScanCut& sc, cudaStream_t s) {
+  launch_pdl(bucket_scan_kernel, dim3(kScanTiles), dim3(kScanThreads), 0, s, (const u64*)c.hist, c.off,
+             c.sc + kScScanTile, c.sc + kScFlags, reinterpret_cast<u64*>(c.sc + kScAgg), sc);
+}
+
 static void depth_front(const ViewBufs& v, int64_t n, const DepthCarve& c, cudaStream_t s) {
-  cudaMemsetAsync(c.hist, 0, sizeof(unsigned long long) * (kDepthBuckets + 2), s);
-  cudaMemsetAsync(c.sc, 0, sizeof(uint32_t) * kScalars, s);
+  // histogram, scalars and scan flags (contiguous)
+  cudaMemsetAsync(c.hist, 0, (size_t)(reinterpret_cast<char*>(c.sc + kScZeroed) - reinterpret_cast<char*>(c.hist)), s);
   depth_hist_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(v.dkey, v.tiles, n, c.base, c.hist, c.slot);
-  size_t sb = c.scan_bytes;
-  cub::DeviceScan::ExclusiveSum(c.scan_temp, sb, c.hist, c.off, kDepthBuckets + 2, s);
+  launch_bucket_scan(c, ScanCut{}, s);
 }
 
 void launch_depth_order(const ViewBufs& v, int64_t n, float near_plane, void* temp, size_t temp_bytes,
@@ -365,30 +513,35 @@ void launch_depth_order(const ViewBufs& v, int64_t n, float near_plane, void* te
 
 void launch_depth_prepare(int64_t n, float near_plane, void* temp, ViewBufs* v, cudaStream_t s) {
   const DepthCarve c = carve(temp, n, near_plane);
-  // histogram and the scalars behind it (layer A's cut, counts, allocators)
-  cudaMemsetAsync(c.hist, 0, (size_t)(reinterpret_cast<char*>(c.sc + kScalars) - reinterpret_cast<char*>(c.hist)), s);
+  // histogram and the scalars / scan flags behind it (layer A's cut, counts, allocators, P)
+  cudaMemsetAsync(c.hist, 0, (size_t)(reinterpret_cast<char*>(c.sc + kScZeroed) - reinterpret_cast<char*>(c.hist)), s);
   v->dhist = c.hist;
   v->dslot = c.slot;
   v->dbase = c.base;
+  v->dpart = c.part;
 }
 
 // After K1 filled the visible buckets (the culled ones get their slots in the rest pass): bucket
 // offsets; *pairs_out = the low word of the offset past the last visible bucket = the pair total P.
-void launch_depth_scan(int64_t n, float near_plane, void* temp, const uint32_t** pairs_out, cudaStream_t s) {
+void launch_depth_scan(int64_t n, float near_plane, void* temp, const LayerCut* cut, const uint32_t** pairs_out,
+                       cudaStream_t s) {
   const DepthCarve c = carve(temp, n, near_plane);
   *pairs_out = reinterpret_cast<const uint32_t*>(c.off + kDepthBuckets);  // little endian: low word = pairs
   if (n == 0) {
     cudaMemsetAsync(c.off, 0, sizeof(unsigned long long) * (kDepthBuckets + 2), s);
     return;
   }
-  size_t sb = c.scan_bytes;
-  cub::DeviceScan::ExclusiveSum(c.scan_temp, sb, c.hist, c.off, kDepthBuckets + 2, s);
+  ScanCut sc{};
+  if (cut)
+    sc = ScanCut{c.part, (uint32_t)((n + kPreThreads - 1) / kPreThreads), cut->div, cut->min_pairs, cut->cap_a,
+                 cut->gauss_cap, c.sc + kScCut};
+  launch_bucket_scan(c, sc, s);
 }
 
 void launch_depth_order_layer_a(const ViewBufs& v, int64_t n, float near_plane, void* temp, uint32_t div,
                                 uint32_t min_pairs, int64_t gauss_cap, uint32_t cap_a, uint32_t* idx_sorted,
                                 uint2* cand_rect, uint32_t* ra, uint8_t* active, float* gacc_zero, bool rerun,
-                                const ColorJob& cj, cudaStream_t s) {
+                                bool cut_ready, const ColorJob& cj, cudaStream_t s) {
   if (n == 0) {
     cudaMemsetAsync(ra, 0, sizeof(uint32_t), s);
     return;
@@ -396,9 +549,11 @@ void launch_depth_order_layer_a(const ViewBufs& v, int64_t n, float near_plane, 
   const DepthCarve c = carve(temp, n, near_plane);
   // (the scalars were zeroed with the histogram by launch_depth_prepare; a re-run after a pair
   // capacity overflow zeroes them again)
-  if (rerun) cudaMemsetAsync(c.sc, 0, sizeof(uint32_t) * kScalars, s);
-  launch_pdl(depth_cut_kernel, dim3((kDepthBuckets + 255) / 256), dim3(256), 0, s, (const u64*)c.off, div, min_pairs,
-             gauss_cap, cap_a, c.sc + kScCut);
+  if (rerun) cudaMemsetAsync(c.sc, 0, sizeof(uint32_t) * kScRerun, s);
+  // (cut_ready: the bucket scan already applied the cut with these parameters)
+  if (!cut_ready)
+    launch_pdl(depth_cut_kernel, dim3((kDepthBuckets + 255) / 256), dim3(256), 0, s, (const u64*)c.off, div,
+               min_pairs, gauss_cap, cap_a, c.sc + kScCut);
   const DepthOut o{idx_sorted, nullptr, cand_rect, active, gacc_zero, cj};
   const int64_t ga = std::min<int64_t>(n, gauss_cap);
   const uint32_t* cut = c.sc + kScCut;

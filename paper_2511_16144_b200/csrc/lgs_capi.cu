@@ -800,6 +800,11 @@ LGS_API int64_t lgs_grads_flat_size(int64_t n, int32_t feature_dim, int32_t sh_d
 namespace {
 // The layer-A size policy (lgs_ctx::layer_div): reads the counters of the previous uncaptured
 // layered render once they have landed (never waits).
+// Gaussians layer A may hold (the cut's second bound, with the pair cap of layer_a_cap)
+int64_t layer_a_gauss_cap(int64_t n, uint32_t div) {
+  return std::min<int64_t>(n, std::max<int64_t>(4096, n / (2 * (int64_t)div)));
+}
+
 void layer_policy_update(lgs_ctx* ctx, int ntiles) {
   if (!ctx->lp_pending || cudaEventQuery(ctx->lp_ev) != cudaSuccess) return;
   ctx->lp_pending = false;
@@ -972,15 +977,26 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
 
   // K1
   const uint32_t* dev_pairs = ctx->dev_u32;
+  // with a capacity known before K1 (bin_and_blend's first attempt below), the bucket scan also
+  // applies the layer-A cut (no separate cut launch)
+  const int64_t cut_cap = (layered && fast && n > 0 && ctx->pairs_cap > 0) ? ctx->pairs_cap : -1;
+  const uint32_t cut_div = ctx->layer_div;
   {
     PhaseScope ph(ctx, PH_PREPROCESS);
     launch_preprocess(dm, dc, t->vb, !layered, s);
     // the pair count P = sum of tiles touched sizes the tile lists; it is read back while the GPU
     // is still busy with the depth order queued below, so the host wait never idles the GPU
-    if (layered) launch_depth_scan(n, dc.near_plane, otemp, &dev_pairs, s);  // P = visible buckets' pairs
+    // P = visible buckets' pairs; with a known capacity the scan also cuts layer A
+    if (layered && cut_cap >= 0) {
+      const LayerCut lc{ctx->layer_div, kLayerMinPairs, (uint32_t)layer_a_cap(cut_cap, ntiles, ctx->layer_div),
+                        layer_a_gauss_cap(n, ctx->layer_div)};
+      launch_depth_scan(n, dc.near_plane, otemp, &lc, &dev_pairs, s);
+    } else if (layered) {
+      launch_depth_scan(n, dc.near_plane, otemp, nullptr, &dev_pairs, s);
+    }
     else launch_sum_tiles(t->vb.tiles, n, ctx->dev_u32, s);
   }
-  ctx->launches += layered ? 3 : 2;
+  ctx->launches += 2;
   // side branch of a plan: the gradient buffers' zero rows stream out beside the forward (the
   // backward's chain then writes only the active rows).  Forked right before the first blend,
   // which is issue-bound and leaves HBM to the stores (forking after K1 instead, beside the
@@ -1089,7 +1105,7 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
       // vals + capA) and are blended again: pass 2, a conditional node of a captured plan.
       const uint32_t ldiv = ctx->layer_div;
       const uint32_t capA = (uint32_t)layer_a_cap(cap, ntiles, ldiv);
-      const int64_t gcapA = std::min<int64_t>(n, std::max<int64_t>(4096, n / (2 * (int64_t)ldiv)));
+      const int64_t gcapA = layer_a_gauss_cap(n, ldiv);
       const size_t sat_n = (size_t)(dc.tiles_x + 1) * (dc.tiles_y + 1);
       uint32_t *ra = nullptr, *unfinished = nullptr, *sat = nullptr, *order2 = nullptr, *count2 = nullptr;
       uint32_t* scratch_b = nullptr;
@@ -1125,7 +1141,8 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
       {
         PhaseScope ph(ctx, PH_DEPTH_SORT);
         launch_depth_order_layer_a(t->vb, n, dc.near_plane, otemp, ldiv, kLayerMinPairs, gcapA, capA,
-                                   idx_sorted, cand_rect, ra, t->vb.active, fuse ? t->gacc : nullptr, !exact, cj, s);
+                                   idx_sorted, cand_rect, ra, t->vb.active, fuse ? t->gacc : nullptr, !exact,
+                                   exact && cap == cut_cap && ldiv == cut_div, cj, s);
       }
       {
         PhaseScope ph(ctx, PH_TILE_SORT);
@@ -1136,7 +1153,7 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
       // Layered lists are short and even (every tile stops at its saturation): the blend kernels
       // take tiles in natural order (measured as fast as longest-list-first, one launch less).
       t->lpt_order = false;
-      ctx->launches += 5;  // the rank kernel sorts big depth buckets itself (no depth_big launch)
+      ctx->launches += (exact && cap == cut_cap && ldiv == cut_div) ? 4 : 5;  // (the rank kernel sorts big buckets)
       if (targets && !fuse) LGS_CUDA(cudaMemsetAsync(t->loss, 0, sizeof(double), s));
       FwdOut fo1 = fo;
       fo1.unfinished = unfinished;
@@ -1352,6 +1369,7 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
   dfree(ctx, t->vb.iota);
   t->vb.dhist = nullptr;  // lived in the depth-order scratch, freed above
   t->vb.dslot = nullptr;
+  t->vb.dpart = nullptr;
   if (tape) *tape = t;
   else free_saved(t);
   return LGS_OK;

@@ -21,6 +21,7 @@ namespace lgs {
 // near plane, 2^13 buckets per octave of depth; bucket kDepthBuckets holds the culled Gaussians
 constexpr int kDepthShift = 10;
 constexpr int kDepthBuckets = 1 << 18;
+constexpr int kPreThreads = 128;  // K1 (preprocess) CTA size: one pair partial sum per CTA
 
 constexpr int kTile = 16;
 constexpr int kBlock = kTile * kTile;

@@ -25,6 +25,7 @@ struct ViewBufs {
   unsigned long long* dhist = nullptr;
   uint32_t* dslot = nullptr;
   uint32_t dbase = 0;  // near-plane bucket offset (depth_bucket)
+  uint32_t* dpart = nullptr;  // ... and stores each CTA's pair sum here (ceil(n / kPreThreads) words)
   // Gaussians that can hold a nonzero screen-space gradient (listed in some traversed tile list);
   // null: every visible one.  The backward zeroes and reads only their accumulator rows.
   uint8_t* active = nullptr;
@@ -116,12 +117,19 @@ void launch_depth_order(const ViewBufs& v, int64_t n, float near_plane, void* te
 // Split for the layered path: depth_prepare (before K1: zeroes the histogram, sets v.dhist/dslot/
 // dbase so K1 fills it), depth_scan (after K1: bucket offsets; *pairs_out = device address of the
 // visible pair total P), then launch_depth_order_layer_a (cut, scatter, rank of layer A).
+// depth_scan is one launch; given `cut` it also applies the layer-A cut with those parameters
+// (from the pair total K1's partial sums give), and layer_a is then called with cut_ready.
+struct LayerCut {
+  uint32_t div, min_pairs, cap_a;
+  int64_t gauss_cap;
+};
 void launch_depth_prepare(int64_t n, float near_plane, void* temp, ViewBufs* v, cudaStream_t s);
-void launch_depth_scan(int64_t n, float near_plane, void* temp, const uint32_t** pairs_out, cudaStream_t s);
+void launch_depth_scan(int64_t n, float near_plane, void* temp, const LayerCut* cut, const uint32_t** pairs_out,
+                       cudaStream_t s);
 void launch_depth_order_layer_a(const ViewBufs& v, int64_t n, float near_plane, void* temp, uint32_t div,
                                 uint32_t min_pairs, int64_t gauss_cap, uint32_t cap_a, uint32_t* idx_sorted,
                                 uint2* cand_rect, uint32_t* ra, uint8_t* active, float* gacc_zero, bool rerun,
-                                const ColorJob& cj, cudaStream_t s);
+                                bool cut_ready, const ColorJob& cj, cudaStream_t s);
 // gate (device, may be null): the kernels return at once when *gate == 0 (no unfinished tile)
 void launch_depth_order_rest(const ViewBufs& v, int64_t n, float near_plane, void* temp, uint32_t* idx_sorted,
                              const uint32_t* gate, cudaStream_t s);

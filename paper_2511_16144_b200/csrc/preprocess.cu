@@ -53,14 +53,11 @@ void launch_pack_map(const float* pos, const float* rot, const float* log_s, con
 // ------------------------------------------------------------------------------------------
 // K1
 // ------------------------------------------------------------------------------------------
-constexpr int kPreThreads = 128;
-
 // COLOR = false (depth-layered binning): no SH read here; the colours of the Gaussians that get
 // listed are computed where they are first listed (ColorJob, lgs_internal.cuh)
+// one Gaussian; returns the tiles it touches (0: culled)
 template <int DEG, bool COLOR>
-__global__ void __launch_bounds__(kPreThreads) preprocess_kernel(DevMap m, DevCam c, ViewBufs v) {
-  const int64_t i = (int64_t)blockIdx.x * kPreThreads + threadIdx.x;
-  if (i >= m.n) return;
+__device__ __forceinline__ uint32_t preprocess_one(const DevMap& m, const DevCam& c, const ViewBufs& v, int64_t i) {
   v.iota[i] = (uint32_t)i;
   const float4 po = m.pos_opa[i];
   const float P0 = po.x, P1 = po.y, P2 = po.z;
@@ -137,7 +134,7 @@ __global__ void __launch_bounds__(kPreThreads) preprocess_kernel(DevMap m, DevCa
   if (!ok) {  // culled: no tiles, sorts last; its records are never read (left unwritten)
     v.tiles[i] = 0;
     v.dkey[i] = 0xffffffffu;
-    return;
+    return 0u;
   }
   v.rec0[i] = make_float4(u, vv, t2, opacity);
   v.rec1[i] = make_float4(cc / det, -cb / det, ca / det, radius);
@@ -153,6 +150,25 @@ __global__ void __launch_bounds__(kPreThreads) preprocess_kernel(DevMap m, DevCa
 
   // colour (renderer.cpp:128; SH extension)
   if (COLOR) v.color[i] = gaussian_color<DEG>(m.sh, po, c.cc, i);
+  return ntl;
+}
+
+template <int DEG, bool COLOR>
+__global__ void __launch_bounds__(kPreThreads) preprocess_kernel(DevMap m, DevCam c, ViewBufs v) {
+  const int64_t i = (int64_t)blockIdx.x * kPreThreads + threadIdx.x;
+  const uint32_t ntl = i < m.n ? preprocess_one<DEG, COLOR>(m, c, v, i) : 0u;
+  if (!v.dpart) return;
+  // this CTA's pair sum (plain store: the bucket scan adds them up for the layer-A cut)
+  __shared__ uint32_t s_sum[kPreThreads / 32];
+  const uint32_t w = __reduce_add_sync(0xffffffffu, ntl);
+  if ((threadIdx.x & 31) == 0) s_sum[threadIdx.x >> 5] = w;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t t = 0;
+#pragma unroll
+    for (int k = 0; k < kPreThreads / 32; ++k) t += s_sum[k];
+    v.dpart[blockIdx.x] = t;
+  }
 }
 
 // colours of every visible Gaussian (debug exports of a layered render)

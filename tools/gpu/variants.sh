@@ -14,7 +14,7 @@ else
 run() {
   python bench.py --config $CONFIG --steps 30 --warmup 5 --no-e2e --no-mapping --no-cpu-baseline --no-pruning \
     --multiview none 2>/dev/null | \
-    tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$1', d['value'], d['roofline']['phases']['blend_fused']['ms'], d['clocks'].get('sm_mhz'), {k: v['ms'] for k, v in d['roofline']['phases'].items() if k != 'blend_fused'})"
+    tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$1', d['value'], d['roofline']['phases']['blend_fused']['ms'], d['clocks'].get('sm_mhz'), d['work']['listed'], {k: v['ms'] for k, v in d['roofline']['phases'].items() if k != 'blend_fused'})"
 }
 fi
 run base
