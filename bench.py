@@ -627,13 +627,13 @@ def run_multiview(args, name, local, world, rank, flush):
         for p in plans:
             p.run()
         if comm is not None:
-            for p in plans:  # every view final before the exchange (an overflowed view re-runs here)
-                p.sync()
+            # every view final before the exchange (a view that outgrew its lists or missed its
+            # speculation re-runs here; renderer.sync_plans)
+            R.sync_plans(plans)
             comm.all_reduce_grads_sparse_async(dmap, grads)
 
     def finish():
-        for p in plans:
-            p.sync()
+        R.sync_plans(plans)
         return comm.wait_grads_sparse(dmap, grads) if comm is not None else 0
 
     with torch.cuda.stream(stream):

@@ -439,7 +439,9 @@ LGS_API lgs_status lgs_prune_stats(const lgs_ctx* ctx, int64_t* candidates, int6
  * (below) left a tile unsaturated.  Map contents, targets and
  * gradient buffers may change between replays (same pointers); a new camera re-captures.
  * grads->accumulate = 1: each replay adds its gradients into the buffers (the later views of a
- * multi-view batch; an overflowed replay adds nothing before lgs_plan_sync re-runs it).  The eager
+ * multi-view batch; an overflowed or missed replay adds nothing before lgs_plan_sync re-runs it;
+ * if the batch's first, writing plan is re-run, the accumulating plans replayed before that
+ * re-run must be run again -- renderer.sync_plans does this).  The eager
  * warm-up step inside lgs_plan_create also writes (adds into) the gradient buffers. */
 LGS_API lgs_status lgs_plan_create(lgs_ctx* ctx, lgs_map* map, const lgs_camera* cam, const lgs_render_config* cfg,
                                    const lgs_l1_targets* targets, const lgs_images* images /* device or NULL */,
@@ -462,8 +464,9 @@ LGS_API int64_t lgs_plan_recaptures(const lgs_plan* plan);
 /* 1: the plan is speculative -- captured without the layered binning's second pass, because the
  * warm-up render saturated every tile on its first-pass (layer-A) list; each replay reports an
  * unsaturated tile through a mapped host word and lgs_plan_sync then re-captures the plan with the
- * second pass (for good) and re-runs the step, so results never depend on the guess.  0: not
- * speculative (accumulating plans never are). */
+ * second pass (for good) and re-runs the step, so results never depend on the guess (the replay
+ * that left a tile unsaturated writes no gradient rows, so an accumulating plan adds nothing
+ * before the re-run).  0: not speculative. */
 LGS_API int32_t lgs_plan_speculative(const lgs_plan* plan);
 LGS_API lgs_status lgs_plan_destroy(lgs_plan* plan);
 

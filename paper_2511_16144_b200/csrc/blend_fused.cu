@@ -290,7 +290,10 @@ __device__ __forceinline__ void blend_fused_l1_body(const DevMap& m, const DevCa
     const bool tile_done = o.unfinished ? __syncthreads_and(all_done) != 0 : true;
     if (!tile_done && tid == 0) {
       o.unfinished[tile] = 1u;
-      if (o.unfinished_any) *reinterpret_cast<volatile uint32_t*>(o.unfinished_any) = 1u;
+      if (o.unfinished_any) {
+        *reinterpret_cast<volatile uint32_t*>(o.unfinished_any) = 1u;
+        *o.miss = 1u;
+      }
     }
     float2 g_r = bc2(0.f), g_g = bc2(0.f), g_b = bc2(0.f), g_draw = bc2(0.f), g_acc = bc2(0.f);
     float gf[PPT][FD];

@@ -190,7 +190,10 @@ __global__ void __launch_bounds__(kBlock / PPT, MINB) blend_fwd_kernel(DevMap m,
     const bool tile_done = o.unfinished ? __syncthreads_and(all_done) != 0 : true;
     if (!tile_done && tid == 0) {
       o.unfinished[tile] = 1u;
-      if (o.unfinished_any) *reinterpret_cast<volatile uint32_t*>(o.unfinished_any) = 1u;
+      if (o.unfinished_any) {
+        *reinterpret_cast<volatile uint32_t*>(o.unfinished_any) = 1u;
+        *o.miss = 1u;
+      }
     }
     if (o.consumed && tile_done) {  // list length this warp consumed (layer-A size policy)
       uint32_t mx = 0;

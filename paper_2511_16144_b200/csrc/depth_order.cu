@@ -579,11 +579,12 @@ constexpr int kSegTiles = 8;
 __global__ void __launch_bounds__(kListWarps * 32) layer_tile_lists_kernel(
     const uint2* __restrict__ cand_rect, const uint32_t* __restrict__ cand_idx, const uint32_t* __restrict__ ra,
     int tiles_x, uint32_t* __restrict__ cursor, uint32_t* __restrict__ vals, uint2* __restrict__ ranges,
-    int* __restrict__ blend_counter, double* __restrict__ loss) {
+    int* __restrict__ blend_counter, double* __restrict__ loss, uint32_t* __restrict__ miss) {
   griddep_wait();
   if (blockIdx.x == 0 && threadIdx.x == 0) {  // for the blend launched next (no memset nodes between)
     if (blend_counter) *blend_counter = 0;
     if (loss) *loss = 0.0;
+    if (miss) *miss = 0u;
   }
   __shared__ uint32_t s_cnt[kListWarps][kSegTiles];
   __shared__ uint32_t s_base;
@@ -712,11 +713,11 @@ void launch_copy_u32(const uint32_t* src, int n, uint32_t* dst, cudaStream_t s) 
 
 void launch_layer_tile_lists(const uint2* cand_rect, const uint32_t* cand_idx, const uint32_t* n_cand, int tiles_x,
                              int ntiles, uint32_t* cursor, uint32_t* vals, uint2* ranges, int* blend_counter,
-                             double* loss, cudaStream_t s) {
+                             double* loss, uint32_t* miss, cudaStream_t s) {
   const int tiles_y = ntiles / tiles_x;
   const int runs = tiles_y * ((tiles_x + kSegTiles - 1) / kSegTiles);
   launch_pdl(layer_tile_lists_kernel, dim3(runs), dim3(kListWarps * 32), 0, s, cand_rect, cand_idx, n_cand, tiles_x,
-             cursor, vals, ranges, blend_counter, loss);
+             cursor, vals, ranges, blend_counter, loss, miss);
 }
 
 void launch_depth_order_rest(const ViewBufs& v, int64_t n, float near_plane, void* temp, uint32_t* idx_sorted,

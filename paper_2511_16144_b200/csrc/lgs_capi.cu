@@ -199,6 +199,7 @@ struct lgs_ctx {
   int lp_last_ntiles = 0;
   uint32_t lp_last_div = 0;
   uint32_t* cap_unfinished_any = nullptr;  // speculative plan capture: pass 1 only, reports here
+  uint32_t* cap_miss = nullptr;            // ... and here (device word the chain reads)
   // last lgs_find_language_redundant: candidates (a similar neighbour inside tau_dist), rounds
   int64_t prune_candidates = 0, prune_rounds = 0;
 };
@@ -355,6 +356,7 @@ struct lgs_saved {
   bool lpt_order = true;    // `order` holds the longest-list-first tile order (else natural order)
   float* gacc = nullptr;    // fused-L1 step (blend_fused.cu): screen-space gradients of the forward
   bool bwd_fused = false;
+  const uint32_t* miss = nullptr;  // speculative plan: nonzero -> the chain writes nothing
   int ntiles = 0;
 };
 
@@ -798,13 +800,13 @@ LGS_API int64_t lgs_grads_flat_size(int64_t n, int32_t feature_dim, int32_t sh_d
 }  // extern "C"
 
 namespace {
-// The layer-A size policy (lgs_ctx::layer_div): reads the counters of the previous uncaptured
-// layered render once they have landed (never waits).
 // Gaussians layer A may hold (the cut's second bound, with the pair cap of layer_a_cap)
 int64_t layer_a_gauss_cap(int64_t n, uint32_t div) {
   return std::min<int64_t>(n, std::max<int64_t>(4096, n / (2 * (int64_t)div)));
 }
 
+// The layer-A size policy (lgs_ctx::layer_div): reads the counters of the previous uncaptured
+// layered render once they have landed (never waits).
 void layer_policy_update(lgs_ctx* ctx, int ntiles) {
   if (!ctx->lp_pending || cudaEventQuery(ctx->lp_ev) != cudaSuccess) return;
   ctx->lp_pending = false;
@@ -814,6 +816,13 @@ void layer_policy_update(lgs_ctx* ctx, int ntiles) {
   ctx->lp_last_unfinished = unfinished;
   ctx->lp_last_ntiles = ntiles;
   ctx->lp_last_div = div;
+  if (unfinished * 20 > (uint64_t)ntiles && div > kLayerDiv) {
+    // a layer A shrunk for an earlier view: back towards the default size before judging the
+    // layering (a context rendering several views would otherwise switch them all to one pass)
+    ctx->layer_bad = std::min(ctx->layer_bad, div);
+    div = std::max<uint32_t>(kLayerDiv, div / 4);
+    return;
+  }
   if (unfinished * 20 > (uint64_t)ntiles && ctx->pairs_cap < kSinglePassPairs) {
     ctx->single_pass = true;
     ctx->sp_cap = ctx->pairs_cap;
@@ -1148,7 +1157,8 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
         PhaseScope ph(ctx, PH_TILE_SORT);
         // (the fused kernel follows directly: the list kernel zeroes its tile counter and the loss)
         launch_layer_tile_lists(cand_rect, idx_sorted, ra, dc.tiles_x, ntiles, ra + 1, t->vals, t->ranges,
-                                fuse ? t->counter : nullptr, fuse && targets ? t->loss : nullptr, s);
+                                fuse ? t->counter : nullptr, fuse && targets ? t->loss : nullptr,
+                                spec ? ctx->cap_miss : nullptr, s);
       }
       // Layered lists are short and even (every tile stops at its saturation): the blend kernels
       // take tiles in natural order (measured as fast as longest-list-first, one launch less).
@@ -1158,6 +1168,8 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
       FwdOut fo1 = fo;
       fo1.unfinished = unfinished;
       fo1.unfinished_any = spec;
+      fo1.miss = spec ? ctx->cap_miss : nullptr;
+      t->miss = fo1.miss;
       const bool policy = !ctx->capturing && !ctx->lp_pending;  // count this render for the layer-A policy
       if (policy) {
         if (!ctx->lp_dev) {
@@ -1540,6 +1552,7 @@ lgs_status run_backward(lgs_ctx* ctx, const lgs_saved* t, const BwdIn& in_dev, l
 
   GradOut go{};
   go.accumulate = grads ? grads->accumulate : 0;
+  go.skip = t->miss;
   float* gstage = nullptr;
   const size_t sz_pos = (size_t)n * 3, sz_rot = (size_t)n * 4, sz_ls = (size_t)n * 3, sz_op = (size_t)n,
                sz_sh = (size_t)n * K * 3, sz_ft = (size_t)n * d;
@@ -2990,6 +3003,7 @@ struct lgs_plan {
   int64_t spec_misses = 0;        // speculative replays redone with pass 2
   uint32_t* unf_host = nullptr;   // mapped pinned: set by a speculative replay that left a tile unfinished
   uint32_t* unf_dev = nullptr;    // its device address
+  uint32_t* miss_dev = nullptr;   // device copy of the flag (the chain of a missed replay adds nothing)
 };
 
 namespace {
@@ -3042,6 +3056,7 @@ lgs_status plan_capture(lgs_plan* p) {
   ctx->cap_lpt_next = p->lpt[1];
   ctx->lpt_forked = false;
   ctx->cap_unfinished_any = p->speculative ? p->unf_dev : nullptr;
+  ctx->cap_miss = p->speculative ? p->miss_dev : nullptr;
   plan_free_marks(p);
   ctx->capture_marks = p->profile ? &p->marks : nullptr;  // event nodes cost ~5 us each per replay
   uint32_t* const saved_host = ctx->host_u32;
@@ -3067,6 +3082,7 @@ lgs_status plan_capture(lgs_plan* p) {
   }
   ctx->lpt_forked = false;
   ctx->cap_unfinished_any = nullptr;
+  ctx->cap_miss = nullptr;
   ctx->cap_lpt_cur = ctx->cap_lpt_next = nullptr;
   ctx->prezero = nullptr;
   ctx->capturing = false;
@@ -3125,6 +3141,7 @@ LGS_API lgs_status lgs_plan_create(lgs_ctx* ctx, lgs_map* map, const lgs_camera*
     if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
     if (p->host_pairs) cudaFreeHost(p->host_pairs);
     if (p->unf_host) cudaFreeHost(p->unf_host);
+    if (p->miss_dev) cudaFree(p->miss_dev);
     for (auto& b : p->lpt)
       if (b) cudaFree(b);
     ctx_release(ctx);
@@ -3135,10 +3152,17 @@ LGS_API lgs_status lgs_plan_create(lgs_ctx* ctx, lgs_map* map, const lgs_camera*
       cudaMallocHost(&p->host_pairs, 64) != cudaSuccess ||
       cudaHostAlloc(reinterpret_cast<void**>(&p->unf_host), 64, cudaHostAllocMapped) != cudaSuccess ||
       cudaHostGetDevicePointer(reinterpret_cast<void**>(&p->unf_dev), p->unf_host, 0) != cudaSuccess ||
+      cudaMalloc(reinterpret_cast<void**>(&p->miss_dev), sizeof(uint32_t)) != cudaSuccess ||
       cudaStreamCreateWithFlags(&p->cap_stream, cudaStreamNonBlocking) != cudaSuccess)
     return bail(fail(LGS_ECUDA, "event / stream creation failed"));
-  // forward-only eager renders until the layer-A size policy settles (at most 4), then one eager
-  // step sizes the tile-list capacity (and runs every one-time kernel setup)
+  // the layer-A policy starts afresh for the plan's own view (several plans on one context -- the
+  // views of a batch -- would otherwise inherit each other's layer-A size or single-pass switch),
+  // then forward-only eager renders until it settles (at most 4), then one eager step sizes the
+  // tile-list capacity (and runs every one-time kernel setup)
+  ctx->layer_div = kLayerDiv;
+  ctx->layer_bad = UINT32_MAX;
+  ctx->single_pass = false;
+  ctx->lp_pending = false;
   for (int it = 0; it < 4; ++it) {
     const uint32_t div0 = ctx->layer_div;
     lgs_status sw = lgs_render_forward(ctx, map, &p->cam, &p->cfg, &p->targets, nullptr, nullptr);
@@ -3159,7 +3183,7 @@ LGS_API lgs_status lgs_plan_create(lgs_ctx* ctx, lgs_map* map, const lgs_camera*
     // nothing): capture pass 1 only; the replays report any unfinished tile (lgs_plan_sync)
     const int nt = ((p->cam.width + LGS_TILE - 1) / LGS_TILE) * ((p->cam.height + LGS_TILE - 1) / LGS_TILE);
     layer_policy_update(ctx, nt);
-    p->speculative = !p->grads.accumulate && !ctx->no_speculative && ctx->lp_last_unfinished == 0 &&
+    p->speculative = !ctx->no_speculative && ctx->lp_last_unfinished == 0 &&
                      ctx->lp_last_ntiles == nt && ctx->lp_last_div == ctx->layer_div;
     *p->unf_host = 0;
   }
@@ -3247,6 +3271,7 @@ LGS_API lgs_status lgs_plan_destroy(lgs_plan* p) {
   if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
   if (p->host_pairs) cudaFreeHost(p->host_pairs);
   if (p->unf_host) cudaFreeHost(p->unf_host);
+  if (p->miss_dev) cudaFree(p->miss_dev);
   for (auto& b : p->lpt)
     if (b) cudaFree(b);
   delete p;

@@ -70,8 +70,10 @@ struct FwdOut {
   // depth-layered first pass: tiles not saturated by their (prefix) list are flagged here and get
   // no loss / cotangents (the second pass renders them again on their complete lists)
   uint32_t* unfinished = nullptr;
-  // ... and, if set (a speculative plan without pass 2: mapped host memory), any such tile stores 1
+  // ... and, if set (a speculative plan without pass 2), any such tile stores 1 into mapped host
+  // memory (read by lgs_plan_sync) and into a device word (read by the chain: miss, GradOut::skip)
   uint32_t* unfinished_any = nullptr;
+  uint32_t* miss = nullptr;
   // ... and every warp of a saturated tile adds the list length its pixels consumed (the layer-A
   // size policy of lgs_capi.cu)
   uint32_t* consumed = nullptr;
@@ -140,7 +142,7 @@ void launch_tile_order_lpt(const uint2* ranges, int ntiles, uint32_t* order, cud
 void launch_copy_u32(const uint32_t* src, int n, uint32_t* dst, cudaStream_t s);
 void launch_layer_tile_lists(const uint2* cand_rect, const uint32_t* cand_idx, const uint32_t* n_cand, int tiles_x,
                              int ntiles, uint32_t* cursor, uint32_t* vals, uint2* ranges, int* blend_counter,
-                             double* loss, cudaStream_t s);
+                             double* loss, uint32_t* miss, cudaStream_t s);
 // blend_counter / loss (optional) are zeroed for the blend kernel launched next
 void launch_duplicate(const ViewBufs& v, const uint32_t* idx_sorted, const uint32_t* incl, int64_t n,
                       int tiles_x, uint16_t* key_out, uint32_t* val_out, cudaStream_t s);
@@ -219,6 +221,9 @@ struct GradOut {
   float* feature;       // [d][N]
   int accumulate;
   double* pose;         // 6 doubles (device, atomically accumulated) or null
+  // device word or null: nonzero -> the chain writes nothing (a speculative plan's replay left a
+  // tile unfinished; lgs_plan_sync re-runs it, so an accumulating replay must not add)
+  const uint32_t* skip = nullptr;
 };
 // With v.active (depth-layered binning) only the active rows run the chain; every other row is
 // written zero by launch_grad_zero first (skipped when `zeroed`: the caller already enqueued it).

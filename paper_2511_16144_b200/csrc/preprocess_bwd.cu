@@ -278,6 +278,7 @@ __device__ __forceinline__ void gaussian_bwd(const DevMap& m, const DevCam& c, c
 template <int DEG, int DP, int SLOTS>
 __global__ void __launch_bounds__(kPbThreads) preprocess_bwd_kernel(DevMap m, DevCam c, ViewBufs v,
                                                                       const float* __restrict__ gacc, GradOut g) {
+  if (g.skip && *g.skip) return;
   constexpr int K = (DEG + 1) * (DEG + 1);
   constexpr int KS = 3 * K;
   constexpr int SS = sh_stride<DEG>();
@@ -436,6 +437,7 @@ constexpr int kActRange = kPbThreads * kActFlags;       // rows per block
 template <int DEG, int DP, int SLOTS>
 __global__ void __launch_bounds__(kPbThreads) preprocess_bwd_active_kernel(DevMap m, DevCam c, ViewBufs v,
                                                                              const float* __restrict__ gacc, GradOut g) {
+  if (g.skip && *g.skip) return;
   constexpr int K = (DEG + 1) * (DEG + 1);
   constexpr int KS = 3 * K;
   constexpr int SS = sh_stride<DEG>();

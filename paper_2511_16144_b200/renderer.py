@@ -643,3 +643,20 @@ class Plan:
                 self.h = None
         except (AttributeError, TypeError):  # interpreter shutdown
             pass
+
+
+def sync_plans(plans):
+    """Wait for a batch of plans sharing one gradient buffer (the first writes, the others
+    accumulate) and finish it exactly: lgs_plan_sync re-runs a replay that outgrew its tile lists
+    or missed its speculation, having added nothing; when that is the FIRST plan, its re-run
+    rewrites the buffer, so the accumulating plans that already added are run again.  Returns the
+    pair counts."""
+    before = [p.recaptures for p in plans]
+    pairs = [p.sync() for p in plans]
+    if plans and plans[0].recaptures != before[0]:
+        redo = [p for p, b in zip(plans[1:], before[1:]) if p.recaptures == b]
+        for p in redo:
+            p.run()
+        for p in redo:
+            p.sync()
+    return pairs

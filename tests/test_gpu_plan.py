@@ -173,3 +173,61 @@ def test_speculative_plan_and_fallback():
     assert plan.recaptures == 1
     out, g = _eager(dm, cam, tg)
     _check(grads, pose, imgs, out, g)
+
+
+def test_speculative_accumulating_plans_miss_adds_nothing():
+    """Two speculative plans on one gradient buffer, the second accumulating (a two-view batch of
+    the same view): when faint splats leave tiles unsaturated both replays miss, their gradient
+    chains add nothing, and sync_plans() re-runs each with the second pass -- the buffer holds
+    exactly twice the eager gradients, not a partial sum on top."""
+    scene, cams, info = scenes.make_config("c1", n=500_000)
+    cam = cams[0]
+    ctx = R.Context(0)
+    dm = R.DeviceMap({k: torch.from_numpy(v).cuda() for k, v in scene.items()}, ctx)
+    tg = {k: torch.from_numpy(v).cuda() for k, v in scenes.make_targets(cam, dm.d, info["depth_range"], 3).items()}
+    grads = R.alloc_grads(dm.n, dm.d, dm.K, device=0)
+    poses = [torch.zeros(6, dtype=torch.float32, pin_memory=True) for _ in range(2)]
+    plans = [R.Plan(dm, cam, tg, grads, pose_out=poses[i], accumulate=i > 0) for i in range(2)]
+    assert all(p.speculative for p in plans)
+    for sc, misses in ((scene, 0), (dict(scene, opac=(scene["opac"] - 4.0).astype(np.float32)), 1)):
+        dm.update({k: torch.from_numpy(v).cuda() for k, v in sc.items()})
+        for p in plans:
+            p.run()
+        R.sync_plans(plans)
+        assert [p.recaptures for p in plans] == [misses, misses]
+        out, g = _eager(dm, cam, tg)
+        for k in GROUPS:
+            frac, worst = grad_mismatch(grads[k], 2.0 * g[k])
+            assert frac < 1e-3, (k, frac, worst)
+        for pose in poses:
+            assert np.allclose(pose.numpy(), g["pose"], rtol=1e-4, atol=1e-5 * np.abs(g["pose"]).max())
+
+
+def test_sync_plans_reruns_the_batch_after_the_first_plan():
+    """A batch whose first (writing) plan outgrows its tile lists while the accumulating plan does
+    not: the first plan's re-run rewrites the buffer, so sync_plans runs the second again."""
+    scene, cam, ctx, dm, tg = _setup()
+    cam2 = dict(cam, t=np.array([0.05, 0.0, 0.0]))
+    grads = R.alloc_grads(dm.n, dm.d, dm.K, device=0)
+    poses = [torch.zeros(6, dtype=torch.float32, pin_memory=True) for _ in range(2)]
+    bigger = dict(scene, log_s=(scene["log_s"] + 0.7).astype(np.float32))
+    dev = lambda sc: {k: torch.from_numpy(v).cuda() for k, v in sc.items()}  # noqa: E731
+    plans = [R.Plan(dm, cam, tg, grads, pose_out=poses[0])]
+    dm.update(dev(bigger))  # the context's list capacity grows before the second plan captures
+    R.render(dm, cam, targets=tg, ctx=ctx)
+    torch.cuda.synchronize()
+    dm.update(dev(scene))
+    plans.append(R.Plan(dm, cam2, tg, grads, pose_out=poses[1], accumulate=True))
+    for p in plans:
+        p.run()
+    R.sync_plans(plans)
+    dm.update(dev(bigger))
+    for p in plans:
+        p.run()
+    R.sync_plans(plans)
+    assert [p.recaptures for p in plans] == [1, 0]
+    _, g0 = _eager(dm, cam, tg)
+    _, g1 = _eager(dm, cam2, tg)
+    for k in GROUPS:
+        frac, worst = grad_mismatch(grads[k], g0[k] + g1[k])
+        assert frac < 1e-3, (k, frac, worst)
