@@ -369,7 +369,10 @@ __global__ void depth_rank_kernel(const uint2* __restrict__ tmp, int64_t n, uint
                                   uint32_t* __restrict__ cursor) {
   griddep_wait();
   if (o.gate && *o.gate == 0u) return;
-  const int64_t p0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  // layer A (a few thousand positions on a grid sized for gauss_cap): positions interleaved
+  // over the CTAs, so every SM takes a share of the latency-bound work
+  const int64_t p0 = mode == kDepthLayerA ? (int64_t)threadIdx.x * gridDim.x + blockIdx.x
+                                          : (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const uint32_t ra = cut ? cnt_of(off[cut_end_of(cut)]) : 0u;  // Gaussians in layer A
   const int64_t p = mode == kDepthRest ? p0 + ra : p0;
   if (p < (mode == kDepthLayerA ? (int64_t)ra : n)) {
@@ -384,6 +387,7 @@ __global__ void depth_rank_kernel(const uint2* __restrict__ tmp, int64_t n, uint
         if (p == lo) big_ids[atomicAdd(big_n, 1u)] = b;
       } else {
         uint32_t rank = 0;
+#pragma unroll 4
         for (uint32_t q = lo; q < hi; ++q) rank += precedes(tmp[q], me) ? 1u : 0u;
         depth_emit(o, tiles, rect, lo + rank, me.y, ra);
       }
