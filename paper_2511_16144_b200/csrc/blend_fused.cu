@@ -117,6 +117,7 @@ __device__ __forceinline__ void blend_fused_l1_body(const DevMap& m, const DevCa
   __shared__ float s_loss[NT / 32];
   __shared__ uint32_t s_max;
   __shared__ int s_slot;
+  __shared__ long long s_t0;  // tile_cost: clock at the current tile's start (thread 0)
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   int lx, ly0;
@@ -177,7 +178,16 @@ __device__ __forceinline__ void blend_fused_l1_body(const DevMap& m, const DevCa
 #endif
   };
 
-  for (int tile = next_tile(tl, ntiles, &s_slot); tile >= 0; tile = next_tile(tl, ntiles, &s_slot)) {
+  int prev_tile = -1;  // tile_cost: thread 0 closes the previous tile's interval (every warp is past
+                      // next_tile's barrier, so the whole tile is done)
+  for (int tile = next_tile(tl, ntiles, &s_slot);; tile = next_tile(tl, ntiles, &s_slot)) {
+    if (o.tile_cost && tid == 0) {
+      const long long now = clock64();
+      if (prev_tile >= 0) o.tile_cost[prev_tile] = (uint32_t)min((now - s_t0) >> 4, 0xffffffffll);
+      s_t0 = now;
+    }
+    if (tile < 0) break;
+    prev_tile = tile;
     const int tx = tile % c.tiles_x, ty = tile / c.tiles_x;
     const int px = tx * kTile + lx;
     const int py0 = ty * kTile + ly0;

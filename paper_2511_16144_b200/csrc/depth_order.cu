@@ -662,17 +662,39 @@ __global__ void __launch_bounds__(kListWarps * 32) layer_tile_lists_kernel(
 
 // Tiles longest layer-A list first (exact lengths, >= 1023 in one bin; arbitrary order inside a bin:
 // which CTA takes which tile is racy anyway and no result depends on it).  One CTA counting sort.
-__global__ void __launch_bounds__(1024) tile_order_lpt_kernel(const uint2* __restrict__ ranges, int ntiles,
+// Longest-first tile order for the next replay: by list length, or (cost non-null) by the measured
+// duration of each tile in the previous replay (the fused blend's per-tile clock deltas; a view is
+// fixed between replays).  Keys are read once into shared memory (the blend of this replay may
+// rewrite the costs meanwhile: the counting sort must see one key per tile to stay a permutation).
+__global__ void __launch_bounds__(1024) tile_order_lpt_kernel(const uint2* __restrict__ ranges,
+                                                              const uint32_t* __restrict__ cost, int ntiles,
                                                               uint32_t* __restrict__ order) {
+  extern __shared__ uint32_t s_key[];  // [ntiles] when cost
   __shared__ uint32_t s_bin[1024];
   __shared__ uint32_t s_w[32];
+  __shared__ uint32_t s_max;
   const int t0 = threadIdx.x, lane = t0 & 31, warp = t0 >> 5;
   s_bin[t0] = 0;
+  if (t0 == 0) s_max = 0;
   __syncthreads();
-  for (int t = t0; t < ntiles; t += blockDim.x) {
-    const uint2 r = ranges[t];
-    atomicAdd(&s_bin[1023 - min(r.y - r.x, 1023u)], 1u);  // bin 0 = longest
+  if (cost) {
+    uint32_t mx = 0;
+    for (int t = t0; t < ntiles; t += blockDim.x) {
+      const uint32_t c = __ldcg(cost + t);
+      s_key[t] = c;
+      mx = max(mx, c);
+    }
+    mx = __reduce_max_sync(0xffffffffu, mx);
+    if (lane == 0) atomicMax(&s_max, mx);
+    __syncthreads();
   }
+  const uint32_t cmax = max(s_max, 1u);
+  auto bin_of = [&](int t) -> uint32_t {  // bin 0 = longest
+    if (cost) return 1023u - (uint32_t)(((uint64_t)s_key[t] * 1023u) / cmax);
+    const uint2 r = ranges[t];
+    return 1023u - min(r.y - r.x, 1023u);
+  };
+  for (int t = t0; t < ntiles; t += blockDim.x) atomicAdd(&s_bin[bin_of(t)], 1u);
   __syncthreads();
   const uint32_t v = s_bin[t0];
   uint32_t x = v;
@@ -695,14 +717,12 @@ __global__ void __launch_bounds__(1024) tile_order_lpt_kernel(const uint2* __res
   __syncthreads();
   s_bin[t0] = x - v + (warp ? s_w[warp - 1] : 0u);
   __syncthreads();
-  for (int t = t0; t < ntiles; t += blockDim.x) {
-    const uint2 r = ranges[t];
-    order[atomicAdd(&s_bin[1023 - min(r.y - r.x, 1023u)], 1u)] = (uint32_t)t;
-  }
+  for (int t = t0; t < ntiles; t += blockDim.x) order[atomicAdd(&s_bin[bin_of(t)], 1u)] = (uint32_t)t;
 }
 
-void launch_tile_order_lpt(const uint2* ranges, int ntiles, uint32_t* order, cudaStream_t s) {
-  tile_order_lpt_kernel<<<1, 1024, 0, s>>>(ranges, ntiles, order);
+void launch_tile_order_lpt(const uint2* ranges, const uint32_t* cost, int ntiles, uint32_t* order, cudaStream_t s) {
+  if (ntiles > kLptCostMaxTiles) cost = nullptr;  // (48 KB of keys)
+  tile_order_lpt_kernel<<<1, 1024, cost ? sizeof(uint32_t) * (size_t)ntiles : 0, s>>>(ranges, cost, ntiles, order);
 }
 
 __global__ void __launch_bounds__(1024) copy_u32_kernel(const uint32_t* __restrict__ src, int n,

@@ -136,6 +136,7 @@ struct lgs_ctx {
   // join -- the ordering costs nothing on the critical path (the view is fixed between replays).
   uint32_t* cap_lpt_cur = nullptr;
   uint32_t* cap_lpt_next = nullptr;
+  uint32_t* cap_tile_cost = nullptr;  // per-tile durations of the previous replay (first pass)
   bool lpt_forked = false;
   cudaStream_t side_stream = nullptr;
   cudaEvent_t side_fork = nullptr, side_join = nullptr;
@@ -1010,10 +1011,13 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
   // backward's chain then writes only the active rows).  Forked right before the first blend,
   // which is issue-bound and leaves HBM to the stores (forking after K1 instead, beside the
   // latency-bound depth order, measured 10-15 us slower per replay).
-  // longest-list-first first pass (plans only): few tiles per CTA slot of the blend (~2 at the
-  // headline) leave the longest tiles' CTAs running alone at the end in natural order; with many
-  // per slot the natural order balances as well and keeps neighbours together
-  // (profiles/r2_ab_lpt.log)
+  // longest-first tile order of the first pass (plans only): with few tiles per CTA slot of the
+  // blend (~2 at the headline) the longest tiles' CTAs run alone at the end in natural order.  The
+  // tiles are ranked by their measured durations in the previous replay (the view is fixed between
+  // replays; list lengths correlate only ~0.3 with them): +2% over ranking by list length.  With
+  // many tiles per slot (c2, c4: 3225 tiles) the natural order is faster than either ranking -- it
+  // keeps neighbouring tiles, which share most of their Gaussians, on the SMs together
+  // (profiles/r2_ab_lpt.log, r2_ab_lpt_cost.log, r2_tile_schedule.md)
   const bool lpt = ctx->capturing && ctx->cap_lpt_cur && ctx->prezero && ntiles < 12 * device_sm_count();
   auto fork_prezero = [&]() -> lgs_status {
     if (!(layered && ctx->capturing && ctx->prezero && !ctx->prezero_forked && n > 0)) return LGS_OK;
@@ -1021,7 +1025,7 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
     LGS_CUDA(cudaStreamWaitEvent(ctx->side_stream, ctx->side_fork, 0));
     if (lpt) {  // this replay's order, for the next replay (copied after the join); first on the
                 // branch, so its one CTA is resident before the blend fills the SMs
-      launch_tile_order_lpt(t->ranges, ntiles, ctx->cap_lpt_next, ctx->side_stream);
+      launch_tile_order_lpt(t->ranges, ctx->cap_tile_cost, ntiles, ctx->cap_lpt_next, ctx->side_stream);
       ctx->lpt_forked = true;
       ctx->launches++;
     }
@@ -1167,6 +1171,7 @@ LGS_API lgs_status lgs_render_forward(lgs_ctx* ctx, const lgs_map* map, const lg
       if (targets && !fuse) LGS_CUDA(cudaMemsetAsync(t->loss, 0, sizeof(double), s));
       FwdOut fo1 = fo;
       fo1.unfinished = unfinished;
+      fo1.tile_cost = lpt && fuse ? ctx->cap_tile_cost : nullptr;
       fo1.unfinished_any = spec;
       fo1.miss = spec ? ctx->cap_miss : nullptr;
       t->miss = fo1.miss;
@@ -2997,7 +3002,8 @@ struct lgs_plan {
   int64_t recaptures = 0;
   uint32_t* host_pairs = nullptr;  // pinned: this plan's pair count, written by every replay (each
                                    // plan its own slot: several plans may share a context)
-  uint32_t* lpt[2] = {nullptr, nullptr};  // tile orders: [0] used by a replay, [1] computed by it
+  uint32_t* lpt[3] = {nullptr, nullptr, nullptr};  // tile orders: [0] used by a replay, [1] computed
+                                                   // by it; [2] its per-tile durations
   int lpt_n = 0;
   bool speculative = false;       // captured without the layered binning's pass 2
   int64_t spec_misses = 0;        // speculative replays redone with pass 2
@@ -3044,6 +3050,7 @@ lgs_status plan_capture(lgs_plan* p) {
         LGS_CUDA(cudaMalloc(reinterpret_cast<void**>(&b), sizeof(uint32_t) * (size_t)std::max(nt, 1)));
         LGS_CUDA(cudaMemcpy(b, id.data(), sizeof(uint32_t) * (size_t)nt, cudaMemcpyHostToDevice));
       }
+      LGS_CUDA(cudaMemset(p->lpt[2], 0, sizeof(uint32_t) * (size_t)std::max(nt, 1)));
       p->lpt_n = nt;
     }
   }
@@ -3054,6 +3061,7 @@ lgs_status plan_capture(lgs_plan* p) {
   ctx->prezero_forked = false;
   ctx->cap_lpt_cur = p->lpt[0];
   ctx->cap_lpt_next = p->lpt[1];
+  ctx->cap_tile_cost = p->lpt[2];
   ctx->lpt_forked = false;
   ctx->cap_unfinished_any = p->speculative ? p->unf_dev : nullptr;
   ctx->cap_miss = p->speculative ? p->miss_dev : nullptr;
@@ -3083,7 +3091,7 @@ lgs_status plan_capture(lgs_plan* p) {
   ctx->lpt_forked = false;
   ctx->cap_unfinished_any = nullptr;
   ctx->cap_miss = nullptr;
-  ctx->cap_lpt_cur = ctx->cap_lpt_next = nullptr;
+  ctx->cap_lpt_cur = ctx->cap_lpt_next = ctx->cap_tile_cost = nullptr;
   ctx->prezero = nullptr;
   ctx->capturing = false;
   ctx->capture_marks = nullptr;

@@ -77,6 +77,9 @@ struct FwdOut {
   // ... and every warp of a saturated tile adds the list length its pixels consumed (the layer-A
   // size policy of lgs_capi.cu)
   uint32_t* consumed = nullptr;
+  // ... and (plans, first pass) each tile's duration in units of 16 SM cycles (the next replays'
+  // longest-first tile order, launch_tile_order_lpt)
+  uint32_t* tile_cost = nullptr;
 };
 
 struct BwdIn {
@@ -138,7 +141,9 @@ void launch_depth_order_rest(const ViewBufs& v, int64_t n, float near_plane, voi
 // Layer-A tile lists (one warp per tile scanning the depth-ordered candidates, order-preserving
 // compaction): vals[ranges[t]] for every tile; *cursor (zeroed by the caller) allocates list space.
 // Tiles longest layer-A list first (one CTA counting sort on the list lengths).
-void launch_tile_order_lpt(const uint2* ranges, int ntiles, uint32_t* order, cudaStream_t s);
+// cost (device, may be null): per-tile durations of the previous replay (FwdOut::tile_cost)
+constexpr int kLptCostMaxTiles = 12288;
+void launch_tile_order_lpt(const uint2* ranges, const uint32_t* cost, int ntiles, uint32_t* order, cudaStream_t s);
 void launch_copy_u32(const uint32_t* src, int n, uint32_t* dst, cudaStream_t s);
 void launch_layer_tile_lists(const uint2* cand_rect, const uint32_t* cand_idx, const uint32_t* n_cand, int tiles_x,
                              int ntiles, uint32_t* cursor, uint32_t* vals, uint2* ranges, int* blend_counter,
