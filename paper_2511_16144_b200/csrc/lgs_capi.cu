@@ -106,6 +106,10 @@ struct lgs_ctx {
   uint32_t* dev_u32 = nullptr;   // device scalars: [0] pair count, [1] binning overflow flag
   cudaEvent_t pairs_ready = nullptr;
   cudaMemPool_t pool = nullptr;  // this context's stream-ordered arena (no cross-context reuse waits)
+  // blocks of 256 MB and more (tile lists of huge views: 8.8 GB at configs[4]) come from their own
+  // pool: freed into the main pool they were carved up by the next render's small buffers, and the
+  // next big request mapped fresh memory (36-48 ms of host time in the enqueue)
+  cudaMemPool_t big_pool = nullptr;
   bool capturing = false;        // inside lgs_plan capture: no host waits, graph memory nodes
   std::vector<PhaseMark>* capture_marks = nullptr;  // lgs_plan capture: phase events recorded as graph nodes
   int64_t pairs_cap = 0;  // tile-list capacity for the next render (0: size from the exact count)
@@ -376,6 +380,7 @@ void ctx_release(lgs_ctx* ctx) {
     if (ctx->side_fork) cudaEventDestroy(ctx->side_fork);
     if (ctx->side_join) cudaEventDestroy(ctx->side_join);
     if (ctx->pool) cudaMemPoolDestroy(ctx->pool);
+    if (ctx->big_pool) cudaMemPoolDestroy(ctx->big_pool);
     if (ctx->host_u32) cudaFreeHost(ctx->host_u32);
     if (ctx->mh_listed_host) cudaFreeHost(ctx->mh_listed_host);
     if (ctx->mh_listed_dev) cudaFree(ctx->mh_listed_dev);
@@ -398,6 +403,8 @@ void ctx_release(lgs_ctx* ctx) {
   }
 }
 
+constexpr size_t kBigBlock = size_t(256) << 20;
+
 template <typename T>
 lgs_status dalloc(lgs_ctx* ctx, T** p, size_t count) {
   *p = nullptr;
@@ -405,7 +412,8 @@ lgs_status dalloc(lgs_ctx* ctx, T** p, size_t count) {
   if (ctx->capturing)  // captured into a graph memory node (graph-owned memory)
     LGS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(p), sizeof(T) * count, ctx->stream));
   else
-    LGS_CUDA(cudaMallocFromPoolAsync(reinterpret_cast<void**>(p), sizeof(T) * count, ctx->pool, ctx->stream));
+    LGS_CUDA(cudaMallocFromPoolAsync(reinterpret_cast<void**>(p), sizeof(T) * count,
+                                     sizeof(T) * count >= kBigBlock ? ctx->big_pool : ctx->pool, ctx->stream));
   return LGS_OK;
 }
 
@@ -665,8 +673,15 @@ LGS_API lgs_status lgs_ctx_create(int32_t device, void* stream, lgs_ctx** out) {
       delete ctx;
       return fail(LGS_ENOMEM, "cudaMemPoolCreate failed");
     }
+    if (cudaMemPoolCreate(&ctx->big_pool, &props) != cudaSuccess) {
+      cudaMemPoolDestroy(ctx->pool);
+      if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+      delete ctx;
+      return fail(LGS_ENOMEM, "cudaMemPoolCreate failed");
+    }
     uint64_t thr = UINT64_MAX;
     cudaMemPoolSetAttribute(ctx->pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    cudaMemPoolSetAttribute(ctx->big_pool, cudaMemPoolAttrReleaseThreshold, &thr);
   }
   if (cudaMallocHost(&ctx->host_u32, 64) != cudaSuccess || cudaMalloc(&ctx->dev_u32, 64) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->pairs_ready, cudaEventDisableTiming) != cudaSuccess) {
