@@ -56,7 +56,8 @@ def parse():
     p.add_argument("--rng", choices=["pcg64", "reference"], default="pcg64",
                    help="scene generator: numpy PCG64, or the reference's lego::Rng stream (scenes.RefRng)")
     p.add_argument("--e2e-steps", type=int, default=30)
-    p.add_argument("--e2e-threads", type=int, default=3)
+    p.add_argument("--e2e-threads", type=int, default=0,
+                   help="host threads of the e2e leg (0: 6 up to 1M Gaussians, else 3)")
     p.add_argument("--sampler", choices=["nvml", "smi", "none"], default="nvml", help=argparse.SUPPRESS)
     return p.parse_args()
 
@@ -757,7 +758,10 @@ def run_e2e(args, scene, cam, tg, R, device, mapped=True, delta=True):
         moved = (sum(b[0] - a[0] for a, b in zip(b0, b1)) / per, sum(b[1] - a[1] for a, b in zip(b0, b1)) / per)
         return 1e3 * dt / per, moved
 
-    nthreads = max(1, args.e2e_threads)
+    # host threads, each with its own context: PCIe transfers of one overlap the others' compute;
+    # 6 measured +10% over 3 at the headline (profiles/r2_e2e_threads.log), big maps keep 3
+    # (each context holds its own tile-list blocks: 2 x 8.8 GB at configs[4])
+    nthreads = args.e2e_threads if args.e2e_threads > 0 else (6 if n <= 1_000_000 else 3)
     workers = [Worker() for _ in range(nthreads)]
     # three measurement windows, the median reported: concurrent host-mapped contexts occasionally
     # stall for hundreds of ms together (PCIe zero-copy reads beside other contexts' DMA), which

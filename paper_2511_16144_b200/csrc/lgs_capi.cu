@@ -1572,7 +1572,6 @@ lgs_status run_backward(lgs_ctx* ctx, const lgs_saved* t, const BwdIn& in_dev, l
 
   GradOut go{};
   go.accumulate = grads ? grads->accumulate : 0;
-  go.skip = t->miss;
   float* gstage = nullptr;
   const size_t sz_pos = (size_t)n * 3, sz_rot = (size_t)n * 4, sz_ls = (size_t)n * 3, sz_op = (size_t)n,
                sz_sh = (size_t)n * K * 3, sz_ft = (size_t)n * d;
@@ -1596,6 +1595,7 @@ lgs_status run_backward(lgs_ctx* ctx, const lgs_saved* t, const BwdIn& in_dev, l
       go = device_grad_out(grads, d);
     }
   }
+  go.skip = t->miss;  // (after device_grad_out above rebuilt go)
   double* dpose = nullptr;
   if (pose_grad) {
     LGS_TRY(dalloc(ctx, &dpose, 6));
