@@ -1596,20 +1596,43 @@ lgs_status run_backward(lgs_ctx* ctx, const lgs_saved* t, const BwdIn& in_dev, l
     }
   }
   go.skip = t->miss;  // (after device_grad_out above rebuilt go)
+  // captured step with the active-row chain: its last CTA writes the pose gradient in place and
+  // copies the next tile order (GradOut::done) when the destination is device-accessible
+  bool epi = ctx->capturing && t->vb.active && async_pose;
+  if (epi && pose_grad) {
+    cudaPointerAttributes pa{};
+    epi = cudaPointerGetAttributes(&pa, pose_grad) == cudaSuccess && pa.type != cudaMemoryTypeUnregistered &&
+          pa.devicePointer != nullptr;
+    cudaGetLastError();
+  }
   double* dpose = nullptr;
-  if (pose_grad) {
-    LGS_TRY(dalloc(ctx, &dpose, 6));
-    LGS_CUDA(cudaMemsetAsync(dpose, 0, sizeof(double) * 6, s));
-    go.pose = dpose;
+  if (pose_grad || epi) {
+    LGS_TRY(dalloc(ctx, &dpose, 8));  // 6 accumulators, [6]: the chain's CTA counter
+    LGS_CUDA(cudaMemsetAsync(dpose, 0, sizeof(double) * 8, s));
+    if (pose_grad) go.pose = dpose;
+  }
+  if (epi) {
+    go.done = reinterpret_cast<uint32_t*>(dpose + 6);
+    if (pose_grad) {
+      cudaPointerAttributes pa{};
+      cudaPointerGetAttributes(&pa, pose_grad);
+      go.pose_out = static_cast<float*>(pa.devicePointer);
+    }
   }
   // zero rows already enqueued on the plan's side branch (the forward forked it)?
   bool zeroed = ctx->prezero_forked && grads == ctx->prezero && !host && t->vb.active;
   if (ctx->prezero_forked) {
     LGS_CUDA(cudaStreamWaitEvent(s, ctx->side_join, 0));
     ctx->prezero_forked = false;
-    if (ctx->lpt_forked) {  // the next replay's tile order
-      launch_copy_u32(ctx->cap_lpt_next, t->ntiles, ctx->cap_lpt_cur, s);
-      ctx->launches++;
+    if (ctx->lpt_forked) {  // the next replay's tile order (by the chain's last CTA if it can)
+      if (epi) {
+        go.copy_src = ctx->cap_lpt_next;
+        go.copy_dst = ctx->cap_lpt_cur;
+        go.copy_n = t->ntiles;
+      } else {
+        launch_copy_u32(ctx->cap_lpt_next, t->ntiles, ctx->cap_lpt_cur, s);
+        ctx->launches++;
+      }
       ctx->lpt_forked = false;
     }
   }
@@ -1644,7 +1667,9 @@ lgs_status run_backward(lgs_ctx* ctx, const lgs_saved* t, const BwdIn& in_dev, l
     }
   }
   double hpose[6];
-  if (pose_grad && async_pose) {
+  if (pose_grad && async_pose && go.pose_out) {
+    // written by the chain's last CTA
+  } else if (pose_grad && async_pose) {
     // stream-ordered: fp64 accumulator -> float, copied to pinned-host or device memory
     launch_pose_to_float(dpose, reinterpret_cast<float*>(dpose), s);
     LGS_CUDA(cudaMemcpyAsync(pose_grad, dpose, sizeof(float) * 6, cudaMemcpyDefault, s));

@@ -229,6 +229,15 @@ struct GradOut {
   // device word or null: nonzero -> the chain writes nothing (a speculative plan's replay left a
   // tile unfinished; lgs_plan_sync re-runs it, so an accumulating replay must not add)
   const uint32_t* skip = nullptr;
+  // captured steps, active-row chain only: its last CTA also writes the pose gradient as float to
+  // pose_out (device or page-locked host memory, written in place) and copies copy_n words
+  // copy_src -> copy_dst (the next replay's tile order) -- two launches and a copy node fewer.
+  // done: CTA counter, zeroed with the pose accumulators.
+  float* pose_out = nullptr;
+  const uint32_t* copy_src = nullptr;
+  uint32_t* copy_dst = nullptr;
+  int copy_n = 0;
+  uint32_t* done = nullptr;
 };
 // With v.active (depth-layered binning) only the active rows run the chain; every other row is
 // written zero by launch_grad_zero first (skipped when `zeroed`: the caller already enqueued it).

@@ -524,6 +524,17 @@ __global__ void __launch_bounds__(kPbThreads) preprocess_bwd_active_kernel(DevMa
       if (s != 0.0) atomicAdd(g.pose + threadIdx.x, s);
     }
   }
+  if (g.done) {  // the last CTA: pose as float, the next tile order (GradOut)
+    __shared__ bool s_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(g.done, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if (g.pose_out && threadIdx.x < 6) g.pose_out[threadIdx.x] = (float)__ldcg(g.pose + threadIdx.x);
+    for (int i = threadIdx.x; i < g.copy_n; i += blockDim.x) g.copy_dst[i] = __ldcg(g.copy_src + i);
+  }
 }
 
 template <int DEG, int DP>
