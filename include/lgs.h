@@ -300,9 +300,9 @@ LGS_API lgs_status lgs_saved_work(const lgs_saved* tape, int64_t* evaluated, int
  * 0.01^2, C2 = 0.03^2, statistics at the valid window positions, channel-averaged);
  * l_depth = mean |depth - kf.depth| over pixels with a valid measurement (finite, > 0) and
  * rendered acc > 0.5; l_feat = mean |decode(feat) - feat_gt| with the frozen decoder
- * decode(z) = W2 relu(W1 z + b1) + b2 (proj/src/codec.cpp:135-149); l_total = l_rgb +
+ * decode(z) = W2 relu(W1 z + b1) + b2 (proj/src/codec.cpp:88-103 apply_net); l_total = l_rgb +
  * w_depth l_depth + w_feat l_feat.  lgs_mapping_loss writes d l_total / d (rgb, depth, feat) into
- * the tape (the decoder chain is codec.cpp:167-188 decode_backward_input), which
+ * the tape (the decoder chain is codec.cpp:121-143 decode_backward_input), which
  * lgs_render_backward_loss then back-propagates to the map.  New in this layer: the reference
  * specifies these losses but leaves mapping.cpp / metrics.cpp unimplemented. */
 typedef struct {

@@ -12,9 +12,9 @@ Restates:
   (w_l1 = 0.8); l_depth = L1 over pixels whose measured depth is valid (finite, > 0)
   and whose rendered acc > 0.5, averaged over those pixels; l_feat = L1(decode(feat), F_gt);
   l_total = l_rgb + w_depth l_depth + w_feat l_feat (defaults 0.5 / 1.0).
-  sign(0) = 0 in every L1 cotangent (as Eigen's .sign() in codec.cpp:196).
-* ``decode`` / ``decode_backward_input`` -- proj/src/codec.cpp:126-166 (apply_net, :135-149;
-  decode_backward_input, :167-188): y = W2 relu(W1 z + b1) + b2 per pixel,
+  sign(0) = 0 in every L1 cotangent (as Eigen's .sign() in codec.cpp:193).
+* ``decode`` / ``decode_backward_input`` -- proj/src/codec.cpp:88-143 (apply_net, :88-103;
+  decode, :114-119; decode_backward_input, :121-143): y = W2 relu(W1 z + b1) + b2 per pixel,
   g_z = W1^T ((W1 z + b1 > 0) * (W2^T g_y)).
 Returns the loss breakdown and the cotangents (grad_rgb, grad_depth, grad_feat) that
 lgs_render_backward consumes.
@@ -96,14 +96,14 @@ def ssim(a, b, with_grad=False):
 
 
 def decode(z, w1, b1, w2, b2):
-    """codec.cpp:135-149 apply_net (decoder weights): z [..., d] -> y [..., D]."""
+    """codec.cpp:88-103 apply_net (via Codec::decode, :114-119) (decoder weights): z [..., d] -> y [..., D]."""
     z = np.asarray(z, np.float64)
     pre = z @ np.asarray(w1, np.float64).T + b1
     return np.maximum(pre, 0.0) @ np.asarray(w2, np.float64).T + b2
 
 
 def decode_backward_input(z, g_out, w1, b1, w2):
-    """codec.cpp:167-188."""
+    """codec.cpp:121-143 (ReLU mask of the pre-activation at :136)."""
     z = np.asarray(z, np.float64)
     pre = z @ np.asarray(w1, np.float64).T + b1
     gh = np.asarray(g_out, np.float64) @ np.asarray(w2, np.float64)

@@ -1,5 +1,5 @@
 // loss.cu -- K8: the mapping losses and the decoder chain that produce the rasterizer's cotangents
-// (SPEC.md:418-426 compute_losses; proj/src/codec.cpp:135-188 decoder).
+// (SPEC.md:418-426 compute_losses; proj/src/codec.cpp:88-143 decoder).
 //
 //   l_rgb   = w_l1 L1(rgb, kf.rgb) + (1 - w_l1) (1 - SSIM) / 2     (11x11 Gaussian, sigma 1.5,
 //             'valid' window positions, channel-averaged; oracle/loss.py documents the choice)
@@ -298,7 +298,7 @@ __global__ void __launch_bounds__(128) decoder_l1_kernel(const float* __restrict
     for (int k = 0; k < DP; ++k) gz[k] = 0.f;
 #pragma unroll
     for (int j = 0; j < HID; ++j) {
-      const float gm = h[j] > 0.f ? gh[j] : 0.f;  // ReLU mask: pre-activation > 0 (codec.cpp:184)
+      const float gm = h[j] > 0.f ? gh[j] : 0.f;  // ReLU mask: pre-activation > 0 (codec.cpp:136)
       const float4* wr = reinterpret_cast<const float4*>(sw1 + j * DP);
 #pragma unroll
       for (int q = 0; q < DP / 4; ++q) {
